@@ -1,0 +1,374 @@
+/*
+ * rk_oracle.c — plain fp64 CPU oracle.  TEST INFRASTRUCTURE ONLY (see rk_oracle.h):
+ * only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs may use it.
+ *
+ * Each function cites the passage it follows.  The method computes (up to rounding
+ * order) a textbook explicit Runge–Kutta step of the semi-discrete ODE system, so the
+ * oracle is that definition written out: every stage value Y_i and every k_i is
+ * materialised over the whole global array, sums run left to right and skip zero
+ * coefficients (R-17), no blocking, fusion or reordering.
+ *
+ * Pins: tests/test_oracle_*.py (closed forms, order conditions, invariants).
+ * Controller constants: "parity unpinned" against Odeint itself (R-12);
+ * pinned internally by the SURVEY App. B accept/reject magnitudes and tie-break tests.
+ */
+#include "rk_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------
+ * Butcher tableaux (exact rationals).  Table 1 names the schemes; the
+ * paper delegates the coefficients to Odeint, so these are the standard
+ * published tables (Euler; classic RK4; Cash & Karp 1990; Dormand & Prince 1980),
+ * typed here independently of the CUDA library's copy.
+ * --------------------------------------------------------------------------- */
+typedef struct { int64_t n, d; } rat;
+#define MAXS 7
+typedef struct {
+    int s, order, err_order, has_err;
+    rat c[MAXS];
+    rat a[MAXS][MAXS];
+    rat b[MAXS];
+    rat bh[MAXS]; /* embedded (lower-order) weights, zero if !has_err */
+} tableau;
+
+static const tableau TAB_EULER = {
+    1, 1, 0, 0,
+    {{0, 1}},
+    {{{0, 1}}},
+    {{1, 1}},
+    {{0, 1}},
+};
+
+static const tableau TAB_RK4 = {
+    4, 4, 0, 0,
+    {{0, 1}, {1, 2}, {1, 2}, {1, 1}},
+    {{{0, 1}},
+     {{1, 2}},
+     {{0, 1}, {1, 2}},
+     {{0, 1}, {0, 1}, {1, 1}}},
+    {{1, 6}, {1, 3}, {1, 3}, {1, 6}},
+    {{0, 1}},
+};
+
+static const tableau TAB_CK54 = {
+    6, 5, 4, 1,
+    {{0, 1}, {1, 5}, {3, 10}, {3, 5}, {1, 1}, {7, 8}},
+    {{{0, 1}},
+     {{1, 5}},
+     {{3, 40}, {9, 40}},
+     {{3, 10}, {-9, 10}, {6, 5}},
+     {{-11, 54}, {5, 2}, {-70, 27}, {35, 27}},
+     {{1631, 55296}, {175, 512}, {575, 13824}, {44275, 110592}, {253, 4096}}},
+    {{37, 378}, {0, 1}, {250, 621}, {125, 594}, {0, 1}, {512, 1771}},
+    {{2825, 27648}, {0, 1}, {18575, 48384}, {13525, 55296}, {277, 14336}, {1, 4}},
+};
+
+static const tableau TAB_DOPRI5 = {
+    7, 5, 4, 1,
+    {{0, 1}, {1, 5}, {3, 10}, {4, 5}, {8, 9}, {1, 1}, {1, 1}},
+    {{{0, 1}},
+     {{1, 5}},
+     {{3, 40}, {9, 40}},
+     {{44, 45}, {-56, 15}, {32, 9}},
+     {{19372, 6561}, {-25360, 2187}, {64448, 6561}, {-212, 729}},
+     {{9017, 3168}, {-355, 33}, {46732, 5247}, {49, 176}, {-5103, 18656}},
+     {{35, 384}, {0, 1}, {500, 1113}, {125, 192}, {-2187, 6784}, {11, 84}}},
+    {{35, 384}, {0, 1}, {500, 1113}, {125, 192}, {-2187, 6784}, {11, 84}, {0, 1}},
+    {{5179, 57600}, {0, 1}, {7571, 16695}, {393, 640}, {-92097, 339200}, {187, 2100}, {1, 40}},
+};
+
+static const tableau* get_tableau(int scheme) {
+    switch (scheme) {
+    case ORC_EULER: return &TAB_EULER;
+    case ORC_RK4: return &TAB_RK4;
+    case ORC_CASH_KARP54: return &TAB_CK54;
+    case ORC_DOPRI5: return &TAB_DOPRI5;
+    default: return NULL;
+    }
+}
+
+static double rat_to_double(rat r) { return r.d == 0 ? 0.0 : (double)r.n / (double)r.d; }
+
+/* gcd for the exact error weight e_j = b_j - bhat_j (rounded once, R-11). */
+static int64_t gcd64(int64_t a, int64_t b) {
+    if (a < 0) a = -a;
+    if (b < 0) b = -b;
+    while (b) { int64_t t = a % b; a = b; b = t; }
+    return a ? a : 1;
+}
+static rat rat_sub(rat x, rat y) {
+    /* denominators here are < 2^20, so the cross products fit in int64 */
+    int64_t n = x.n * y.d - y.n * x.d, d = x.d * y.d;
+    int64_t g = gcd64(n, d);
+    rat r = {n / g, d / g};
+    if (r.d < 0) { r.n = -r.n; r.d = -r.d; }
+    return r;
+}
+
+int orc_tableau(int scheme, int64_t* a_num, int64_t* a_den, int64_t* b_num, int64_t* b_den,
+                int64_t* bh_num, int64_t* bh_den, int64_t* c_num, int64_t* c_den, int* order,
+                int* err_order) {
+    const tableau* T = get_tableau(scheme);
+    if (!T) return -1;
+    int s = T->s;
+    for (int i = 0; i < s; ++i) {
+        for (int j = 0; j < s; ++j) {
+            rat r = (j < i) ? T->a[i][j] : (rat){0, 1};
+            if (r.d == 0) r = (rat){0, 1};
+            a_num[i * s + j] = r.n;
+            a_den[i * s + j] = r.d;
+        }
+        b_num[i] = T->b[i].n; b_den[i] = T->b[i].d;
+        rat bh = T->has_err ? T->bh[i] : (rat){0, 1};
+        bh_num[i] = bh.n; bh_den[i] = bh.d ? bh.d : 1;
+        c_num[i] = T->c[i].n; c_den[i] = T->c[i].d;
+    }
+    *order = T->order;
+    *err_order = T->err_order;
+    return s;
+}
+
+/* ------------------------------------------------------------------------------
+ * Right-hand sides.
+ * --------------------------------------------------------------------------- */
+
+/* Eq. 1a: df/dt = f; generalised to du/dt = lambda*u (R-9). */
+static void rhs_exp(int64_t count, const double* u, double* f, double lambda) {
+    for (int64_t i = 0; i < count; ++i) f[i] = lambda * u[i];
+}
+
+/* Eq. 1b: df/dt = f(1 - f). */
+static void rhs_logistic(int64_t count, const double* u, double* f) {
+    for (int64_t i = 0; i < count; ++i) f[i] = u[i] * (1.0 - u[i]);
+}
+
+/* Gray–Scott, Listing 2 lines 25-26, parameters P:L150 (R-1, R-2):
+ *   f0 = d1*Lap(C0) - C0*C1*C1 + F - F*C0
+ *   f1 = d2*Lap(C1) + C0*C1*C1 - (F+K)*C1
+ * evaluated in C++ left-to-right order.  Lap = 7-point second-order central
+ * difference in difference form (R-3), periodic in x, y, z. */
+static void rhs_gray_scott(const orc_problem* p, const double* u, double* f) {
+    const int64_t nx = p->nx, ny = p->ny, nz = p->nz;
+    const int64_t plane = nx * ny;       /* one component of one z-plane */
+    const int64_t zstride = 2 * plane;   /* layout [z][c][y][x] */
+    const double inv_h2 = 1.0 / (p->h * p->h);
+    const double FK = p->F + p->K;
+    for (int64_t z = 0; z < nz; ++z) {
+        const int64_t zm = (z + nz - 1) % nz, zp = (z + 1) % nz;
+        for (int64_t y = 0; y < ny; ++y) {
+            const int64_t ym = (y + ny - 1) % ny, yp = (y + 1) % ny;
+            for (int64_t x = 0; x < nx; ++x) {
+                const int64_t xm = (x + nx - 1) % nx, xp = (x + 1) % nx;
+                double L[2], cc[2];
+                for (int c = 0; c < 2; ++c) {
+                    const double* v = u + c * plane;
+                    const double ctr = v[z * zstride + y * nx + x];
+                    double s = (v[z * zstride + y * nx + xm] - ctr) + (v[z * zstride + y * nx + xp] - ctr);
+                    s = s + ((v[z * zstride + ym * nx + x] - ctr) + (v[z * zstride + yp * nx + x] - ctr));
+                    s = s + ((v[zm * zstride + y * nx + x] - ctr) + (v[zp * zstride + y * nx + x] - ctr));
+                    L[c] = s * inv_h2;
+                    cc[c] = ctr;
+                }
+                const double C0 = cc[0], C1 = cc[1];
+                const double r = C0 * C1 * C1;                     /* (C0*C1)*C1 */
+                const int64_t o = z * zstride + y * nx + x;
+                f[o] = p->d1 * L[0] - r + p->F - p->F * C0;         /* ((d1*L0 - r) + F) - F*C0 */
+                f[o + plane] = p->d2 * L[1] + r - FK * C1;          /* ((d2*L1) + r) - (F+K)*C1 */
+            }
+        }
+    }
+}
+
+void orc_rhs(const orc_problem* p, const double* u, double* f) {
+    const int64_t count = p->n * p->ncomp;
+    switch (p->kind) {
+    case ORC_RHS_EXP: rhs_exp(count, u, f, p->lambda); break;
+    case ORC_RHS_LOGISTIC: rhs_logistic(count, u, f); break;
+    case ORC_RHS_GRAY_SCOTT: rhs_gray_scott(p, u, f); break;
+    default: break;
+    }
+}
+
+/* ------------------------------------------------------------------------------
+ * One explicit RK step, textbook form ("extrapolate the state ... update it
+ * in-place", P:L42 error steppers).  Coefficients prepared once per
+ * (scheme, dt): g_ij = dt*a_ij, beta_j = dt*b_j, delta_j = dt*(b_j - bhat_j).
+ * --------------------------------------------------------------------------- */
+int orc_step(const orc_problem* p, int scheme, double t, double dt, const double* u,
+             double* u_new, double* err) {
+    (void)t; /* all three systems are autonomous */
+    const tableau* T = get_tableau(scheme);
+    if (!T) return ORC_ERR_ARG;
+    if (err && !T->has_err) return ORC_ERR_UNSUPPORTED;
+    const int64_t count = p->n * p->ncomp;
+    const int s = T->s;
+
+    double g[MAXS][MAXS], beta[MAXS], delta[MAXS];
+    for (int i = 0; i < s; ++i) {
+        for (int j = 0; j < i; ++j) g[i][j] = dt * rat_to_double(T->a[i][j]);
+        beta[i] = dt * rat_to_double(T->b[i]);
+        delta[i] = T->has_err ? dt * rat_to_double(rat_sub(T->b[i], T->bh[i])) : 0.0;
+    }
+    /* stages needed: up to the last j with b_j != 0 (or delta_j != 0 if err wanted) */
+    int s_eff = 0;
+    for (int i = 0; i < s; ++i)
+        if (T->b[i].n != 0 || (err && delta[i] != 0.0)) s_eff = i + 1;
+
+    double* k[MAXS] = {0};
+    double* Y = (double*)malloc(sizeof(double) * (size_t)count);
+    for (int i = 0; i < s_eff; ++i) {
+        k[i] = (double*)malloc(sizeof(double) * (size_t)count);
+        /* Y_i = u + sum_{j<i, a_ij != 0} g_ij k_j, left to right */
+        for (int64_t e = 0; e < count; ++e) {
+            double y = u[e];
+            for (int j = 0; j < i; ++j)
+                if (T->a[i][j].n != 0) y = y + g[i][j] * k[j][e];
+            Y[e] = y;
+        }
+        orc_rhs(p, Y, k[i]); /* k_i = F(t + c_i dt, Y_i) */
+    }
+    /* u_new = u + sum_{b_j != 0} beta_j k_j */
+    for (int64_t e = 0; e < count; ++e) {
+        double w = u[e];
+        for (int j = 0; j < s_eff; ++j)
+            if (T->b[j].n != 0) w = w + beta[j] * k[j][e];
+        u_new[e] = w;
+    }
+    /* err = sum_{delta_j != 0} delta_j k_j, first term not added to zero */
+    if (err) {
+        for (int64_t e = 0; e < count; ++e) {
+            double acc = 0.0;
+            int first = 1;
+            for (int j = 0; j < s_eff; ++j) {
+                if (delta[j] == 0.0) continue;
+                if (first) { acc = delta[j] * k[j][e]; first = 0; }
+                else acc = acc + delta[j] * k[j][e];
+            }
+            err[e] = acc;
+        }
+    }
+    for (int i = 0; i < s_eff; ++i) free(k[i]);
+    free(Y);
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------
+ * Error control (P:L46 norm requirement; P:L135 for_each_norm).
+ * --------------------------------------------------------------------------- */
+double orc_error_ratio_max(int64_t count, const double* err, const double* u, const double* k1,
+                           double dt, double atol, double rtol) {
+    double E = 0.0;
+    for (int64_t i = 0; i < count; ++i) {
+        const double r = fabs(err[i]) / (atol + rtol * (fabs(u[i]) + dt * fabs(k1[i])));
+        if (isnan(r)) return NAN;
+        if (r > E) E = r;
+    }
+    return E;
+}
+
+int orc_controller(double E, int p, int q, double* dt) {
+    if (E > 1.0) {
+        /* reject: decrease_step */
+        double fac = (9.0 / 10.0) * pow(E, -1.0 / (double)(q - 1));
+        if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
+        *dt = *dt * fac;
+        return 0;
+    }
+    /* accept: increase_step */
+    if (E < 0.5) {
+        double Ec = pow(5.0, -(double)p);
+        if (E > Ec) Ec = E;
+        *dt = *dt * ((9.0 / 10.0) * pow(Ec, -1.0 / (double)p));
+    }
+    return 1;
+}
+
+/* ------------------------------------------------------------------------------
+ * Drivers (P:L198 integrate_const, P:L201 do_step / integrate_adaptive).
+ * --------------------------------------------------------------------------- */
+int orc_integrate_const(const orc_problem* p, int scheme, double* u, double t0, double t1,
+                        double dt, int64_t* steps) {
+    if (!(dt > 0.0) || !(t1 > t0)) return ORC_ERR_ARG;
+    const int64_t count = p->n * p->ncomp;
+    double* un = (double*)malloc(sizeof(double) * (size_t)count);
+    int64_t n = 0;
+    double t = t0;
+    while ((t + dt) - t1 <= DBL_EPSILON) {
+        int rc = orc_step(p, scheme, t, dt, u, un, NULL);
+        if (rc != ORC_OK) { free(un); return rc; }
+        memcpy(u, un, sizeof(double) * (size_t)count);
+        ++n;
+        t = t0 + (double)n * dt;
+    }
+    free(un);
+    *steps = n;
+    return ORC_OK;
+}
+
+int orc_integrate_adaptive(const orc_problem* p, int scheme, double* u, double t0, double t1,
+                           double dt0, double atol, double rtol, int64_t* accepted,
+                           int64_t* rejected) {
+    const tableau* T = get_tableau(scheme);
+    if (!T) return ORC_ERR_ARG;
+    if (!T->has_err) return ORC_ERR_UNSUPPORTED;
+    if (!(dt0 > 0.0) || !(t1 > t0) || !(atol > 0.0) || !(rtol >= 0.0)) return ORC_ERR_ARG;
+    const int64_t count = p->n * p->ncomp;
+    double* un = (double*)malloc(sizeof(double) * (size_t)count);
+    double* er = (double*)malloc(sizeof(double) * (size_t)count);
+    double* k1 = (double*)malloc(sizeof(double) * (size_t)count);
+    int64_t acc = 0, rej = 0;
+    int rc = ORC_OK;
+    double t = t0, dt = dt0;
+    while (t1 - t > DBL_EPSILON) {
+        if ((t + dt) - t1 > DBL_EPSILON) dt = t1 - t;
+        orc_rhs(p, u, k1); /* dxdt at the start of the step (ratio denominator) */
+        int tries = 0;
+        for (;;) {
+            rc = orc_step(p, scheme, t, dt, u, un, er);
+            if (rc != ORC_OK) goto done;
+            const double E = orc_error_ratio_max(count, er, u, k1, dt, atol, rtol);
+            if (isnan(E)) { rc = ORC_ERR_DIVERGED; goto done; }
+            const double dt_used = dt;
+            if (orc_controller(E, T->order, T->err_order, &dt)) {
+                memcpy(u, un, sizeof(double) * (size_t)count);
+                t = t + dt_used;
+                ++acc;
+                break;
+            }
+            ++rej;
+            if (++tries >= 500) { rc = ORC_ERR_STALL; goto done; }
+        }
+    }
+done:
+    free(un); free(er); free(k1);
+    *accepted = acc;
+    *rejected = rej;
+    return rc;
+}
+
+/* ------------------------------------------------------------------------------
+ * Algebra ops.
+ * --------------------------------------------------------------------------- */
+int orc_lincomb(int64_t count, double* out, int k, const double* coef, const double* const* in) {
+    if (k < 1 || k > 14) return ORC_ERR_ARG;
+    for (int64_t i = 0; i < count; ++i) {
+        double acc = coef[0] * in[0][i];
+        for (int j = 1; j < k; ++j) acc = acc + coef[j] * in[j][i];
+        out[i] = acc;
+    }
+    return ORC_OK;
+}
+
+double orc_norm_inf(int64_t count, const double* u) {
+    double m = 0.0;
+    for (int64_t i = 0; i < count; ++i) {
+        const double a = fabs(u[i]);
+        if (isnan(a)) return NAN;
+        if (a > m) m = a;
+    }
+    return m;
+}

@@ -1,0 +1,110 @@
+"""Pins of the oracle's error control ("If the tolerance is violated, the step is
+rejected and the step size is reduced. This is repeated until the step is accepted. For
+error estimations below the tolerance, the step size is increased.").
+
+The controller constants are Odeint's defaults as read in DESIGN.md R-12 -- the paper
+delegates them to Odeint, so this part is "parity unpinned" against Odeint itself.  It
+is pinned internally by (i) the accept/reject counts of an independent replay
+(tests/golden/adaptive_counts.json), (ii) the closed-form tie-breaks
+below, (iii) the tolerance actually achieved against the Eq. 1a/1b closed forms.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import rk_inputs
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "adaptive_counts.json")))
+
+
+@pytest.mark.parametrize("run", GOLD["runs"], ids=[r["name"] for r in GOLD["runs"]])
+def test_adaptive_counts_golden(run):
+    n, t0, t1 = run["n"], run["t0"], run["t1"]
+    if run["problem"] == "logistic":
+        u0 = rk_inputs.logistic_u0(n, t0, run["shifted"])
+        s = rk_inputs.logistic_shift(n) if run["shifted"] else np.zeros(n)
+        p, exact = oracle.logistic_problem(n), 1.0 / (1.0 + np.exp(-(t1 - s)))
+    else:
+        u0 = np.ones(n)
+        p, exact = oracle.exp_problem(n, -1.0), np.full(n, math.exp(-(t1 - t0)))
+    u, acc, rej, rc = oracle.integrate_adaptive(p, oracle.SCHEMES[run["scheme"]], u0, t0, t1,
+                                                run["dt0"], run["tol"], run["tol"])
+    assert rc == oracle.OK
+    assert (acc, rej) == (run["accepted"], run["rejected"])
+    err = float(np.max(np.abs(u - exact)))
+    assert 0.9 * run["final_err"] <= err <= 1.1 * run["final_err"]
+    assert err <= 100 * run["tol"]  # final error <= 100*rtol
+
+
+def test_controller_tie_breaks():
+    """DESIGN.md R-14: E == 1 accepts; E == 0.5 leaves dt; E == 0 clamps to 5^-5 (x4.5)."""
+    assert oracle.controller(1.0, 0.5) == (True, 0.5)   # accepted, no growth at E >= 0.5
+    assert oracle.controller(0.5, 0.5) == (True, 0.5)
+    acc, dt = oracle.controller(0.0, 1.0)
+    assert acc and abs(dt - 4.5) < 1e-14            # 0.9 * (5^-5)^(-1/5) = 0.9 * 5
+    acc, dt = oracle.controller(1.0 + 2 ** -52, 1.0)
+    assert not acc and dt < 1.0                      # rejected, decreased
+    acc, dt = oracle.controller(1e6, 1.0)
+    assert not acc and dt == 0.2                     # shrink floor 1/5
+
+
+@pytest.mark.parametrize("E", [1e-9, 0.01, 0.3, 0.49])
+def test_accept_grows(E):
+    acc, dt = oracle.controller(E, 1.0)
+    assert acc and 1.0 < dt <= 4.5 + 1e-14
+    assert abs(dt - 0.9 * max(E, 5.0 ** -5) ** (-0.2)) < 1e-12
+
+
+@pytest.mark.parametrize("E", [1.5, 10.0, 300.0])
+def test_reject_shrinks(E):
+    acc, dt = oracle.controller(E, 1.0)
+    assert not acc and 0.2 <= dt < 0.9
+    assert abs(dt - max(0.9 * E ** (-1.0 / 3.0), 0.2)) < 1e-15
+
+
+def test_error_ratio_formula_pins():
+    """r = |e| / (atol + rtol*(|u| + dt*|k1|)): zero error -> 0; boundary values."""
+    assert oracle.error_ratio_max([0.0], [5.0], [1.0], 0.1, 1e-6, 1e-6) == 0.0
+    # e = 1e-6, u = k1 = 0, rtol = 0 -> exactly 1 (S:L82 analogue)
+    assert oracle.error_ratio_max([1e-6], [0.0], [0.0], 0.5, 1e-6, 0.0) == 1.0
+    # the k1 term: u = 0, k1 = 1, dt = 1, atol tiny: r = |e| / (rtol*dt*|k1|)
+    r = oracle.error_ratio_max([2e-4], [0.0], [1.0], 1.0, 1e-300, 1e-4)
+    assert abs(r - 2.0) < 1e-12
+    assert math.isnan(oracle.error_ratio_max([1.0, float("nan")], [0.0, 0.0], [0.0, 0.0],
+                                             1.0, 1.0, 1.0))
+
+
+def test_adaptive_rejects_diverged_state():
+    """A NaN error ratio is a divergence (R-14), not an accepted step."""
+    p = oracle.logistic_problem(2)
+    u, acc, rej, rc = oracle.integrate_adaptive(p, oracle.DOPRI5, [0.5, float("nan")], 0.0, 1.0,
+                                                0.1, 1e-8, 1e-8)
+    assert rc == oracle.ERR_DIVERGED and acc == 0
+
+
+def test_adaptive_unsupported_for_fixed_schemes():
+    p = oracle.logistic_problem(1)
+    for s in (oracle.EULER, oracle.RK4):
+        assert oracle.integrate_adaptive(p, s, [0.5], 0.0, 1.0, 0.1, 1e-8, 1e-8)[3] == \
+            oracle.ERR_UNSUPPORTED
+
+
+def test_zero_rhs_one_step():
+    """du/dt = 0: one accepted step of size t1 - t0 when dt0 already covers it."""
+    p = oracle.exp_problem(3, 0.0)
+    u, acc, rej, rc = oracle.integrate_adaptive(p, oracle.DOPRI5, [1.0, 2.0, 3.0], 0.0, 1.0, 2.0,
+                                                1e-8, 1e-8)
+    assert rc == 0 and (acc, rej) == (1, 0) and list(u) == [1.0, 2.0, 3.0]
+
+
+def test_adaptive_hits_t1_exactly():
+    """Last step truncated to t1 (R-16): decay solved to t1 = 1 within tolerance."""
+    p = oracle.exp_problem(1, -1.0)
+    for dt0 in (0.013, 0.37, 5.0):
+        u, acc, rej, rc = oracle.integrate_adaptive(p, oracle.DOPRI5, [1.0], 0.0, 1.0, dt0,
+                                                    1e-10, 1e-10)
+        assert rc == 0 and abs(u[0] - math.exp(-1.0)) < 1e-8
