@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark: Gray–Scott cell-updates/s per RK step (fp64) on 1..8 B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Headline workload (BASELINE configs[4], weak scaling): a 3D
+Gray–Scott z-slab of 512^3 cells per GPU (global 512 x 512 x 512N, h = 2.5/64, one seeded
+cube per 512^3 block), integrated with Dormand–Prince 5(4) under error control
+(atol = rtol = 1e-6, dt0 = 1): one "step" = one accepted adaptive step, i.e. the whole hot
+path: stage values, halo exchange, stencil RHS, final combination, embedded error, max
+norm + allreduce, host controller.  value = cells x accepted steps
+/ device time (max over ranks).  RK4 fixed-step is measured in the same run ("extra").
+
+Timing: W warm-up steps, then K steps between barrier + synchronize, CUDA events on the
+library's stream (torch's current stream).  Arrays are 2 GiB >> 126 MB L2, so no flush is
+needed.  Roofline: the fused stage kernel (K3), algorithmic bytes counted by the library
+per launch (rk_stats.stage_bytes) over its CUDA-event-timed launch durations.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_PER_GPU = 512
+TOL = 1e-6
+H = 2.5 / 64  # DESIGN.md R-4: h fixed at the paper's 64^3 spacing
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the stage kernel from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.result = None
+        if not self.proc:
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if sm:
+            self.result = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+                           "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle (test infrastructure) on the host cores
+# ---------------------------------------------------------------------------------------
+def oracle_try_seconds(nz_sample: int, scheme_name: str = "dopri5"):
+    import oracle
+    import rk_inputs
+    n = N_PER_GPU
+    u0 = rk_inputs.gray_scott_ic(n, n, nz_sample, seed=42)
+    p = oracle.gray_scott_problem(n, n, nz_sample, h=H)
+    t = time.perf_counter()
+    if scheme_name == "dopri5":
+        un, err = oracle.step(p, oracle.DOPRI5, 0.0, 1.0, u0, with_error=True)
+        k1 = oracle.rhs(p, u0)
+        E = oracle.error_ratio_max(err, u0, k1, 1.0, TOL, TOL)
+        oracle.controller(E, 1.0)
+    else:
+        oracle.step(p, oracle.RK4, 0.0, 1.0, u0)
+    return time.perf_counter() - t, n * n * nz_sample
+
+
+def cpu_baseline(nz_sample=128):
+    secs, cells = oracle_try_seconds(nz_sample)
+    return {"value": cells / secs, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+            "sample": f"one DOPRI5 error-controlled try (7 RHS evals, error ratio, max norm, "
+                      f"controller) on a 512x512x{nz_sample} periodic slab (same per-cell work "
+                      f"as the 512^3 workload), single-threaded C oracle -O2 -ffp-contract=off, "
+                      f"{secs:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    nz_sample = 32
+    for _ in range(args.warmup):
+        oracle_try_seconds(nz_sample)
+    tot, cells = 0.0, 0
+    for _ in range(args.steps):
+        s, c = oracle_try_seconds(nz_sample)
+        tot += s
+        cells += c
+    v = cells / tot
+    line = {"impl": "reference", "metric": "gray_scott_cell_updates_per_s", "value": v,
+            "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Gray-Scott IC, DESIGN.md R-6)",
+            "config": {"workload": "gray_scott_dopri5_adaptive_512^3_per_gpu",
+                       "sample": f"512x512x{nz_sample} periodic slab per step"},
+            "cpu_baseline": {"value": v, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+                             "sample": f"each step = one DOPRI5 try on a 512x512x{nz_sample} slab"},
+            "e2e": {"value": v, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the RK4 / e2e / CPU legs")
+    ap.add_argument("--overlap", type=int, default=1)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("BENCH_ALLOW_SHORT")
+
+    rank, world, local = dist_setup()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_05331_b200 as rk
+    import rk_inputs
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    if world > 1:
+        ctx = rk.Context.from_torch_distributed(local, stream)
+    else:
+        ctx = rk.Context(0, 1, local, stream)
+
+    n = args.n
+    nzg = n * world
+    st = ctx.grid(n, n, nzg, 2)
+    st.set_rhs_gray_scott(h=H)
+    st.set_option(rk.OPT_HALO_OVERLAP, args.overlap)
+    u0 = rk_inputs.gray_scott_ic(n, n, nzg, seed=42, z0=st.begin, nzl=st.local, zblocks=world)
+    u0_dev = torch.from_numpy(u0).cuda(local)
+    st.set(u0_dev)
+    cells_local = n * n * st.local
+    cells_total = n * n * nzg
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- headline: DOPRI5 adaptive, one accepted step per "step" ---------------------
+    state = {"t": 0.0, "dt": 1.0}
+
+    def adaptive_step():
+        tries = 0
+        while True:
+            acc, E, dtn = st.try_step("dopri5", state["t"], state["dt"], TOL, TOL)
+            tries += 1
+            if acc:
+                state["t"] += state["dt"]
+                state["dt"] = dtn
+                return tries
+            state["dt"] = dtn
+
+    for _ in range(args.warmup):
+        adaptive_step()
+    st.set_option(rk.OPT_TIMING, 1)
+    st.reset_stats()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tries = 0
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            tries += adaptive_step()
+        ev1.record(stream)
+        barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    s = st.stats()
+    st.set_option(rk.OPT_TIMING, 0)
+    value = cells_total * args.steps / (ms / 1e3)
+    peak, peak_src = peaks()
+    k_ms = s["stage_kernel_ms"]
+    achieved = s["stage_bytes"] / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
+    traffic = ncu_traffic()
+    step_bytes = s["stage_bytes"] / max(1, s["tries"])
+    halo = None
+    if world > 1 and s["halo_exchanges"]:
+        halo = {"exchanges": s["halo_exchanges"], "ms_total": s["halo_ms"],
+                "ms_per_exchange": s["halo_ms"] / s["halo_exchanges"],
+                "bytes_per_exchange": s["halo_bytes"] / s["halo_exchanges"],
+                "nvlink_gbs": (s["halo_bytes"] / (s["halo_ms"] / 1e3) / 1e9) if s["halo_ms"] else None}
+
+    line = {
+        "metric": "gray_scott_cell_updates_per_s",
+        "value": value,
+        "unit": "cell-updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded Gray-Scott IC, DESIGN.md R-6)",
+        "config": {"workload": "gray_scott_dopri5_adaptive_512^3_per_gpu", "nx": n, "ny": n,
+                   "nz_global": nzg, "nz_per_gpu": int(st.local), "h": H, "atol": TOL, "rtol": TOL,
+                   "scheme": "dopri5 (FSAL, error-controlled)", "tries": tries,
+                   "halo_overlap": bool(args.overlap),
+                   "l2": "no flush: every array is 2 GiB per GPU, >> 126 MB L2",
+                   "parallelism": f"z-slab x{world} (NCCL send/recv halos + allreduce max)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": traffic.get("dopri5_bytes_per_launch") if traffic else None,
+                     "kernel": "gs_stage_kernel (K3, fused stage value + 7-pt stencil + "
+                               "reaction + epilogue)",
+                     "algorithmic_bytes_per_try": step_bytes,
+                     "algorithmic_bytes_per_cell_try": step_bytes / cells_local,
+                     "avg_launch_ms": k_ms / max(1, s["stage_launches"]),
+                     "launches": s["stage_launches"], "peak_source": peak_src},
+        "gpu_launches": s["kernel_launches"],
+    }
+    if halo:
+        line["halo"] = halo
+    line["clocks"] = getattr(clk, "result", None)
+
+    if not args.no_extra:
+        # ---- RK4 fixed step (north_star: RK4 and DOPRI5 at 512^3) -------------------------
+        st.set(u0_dev)
+        for _ in range(args.warmup):
+            st.do_step("rk4", 0.0, 1.0)
+        st.set_option(rk.OPT_TIMING, 1)
+        st.reset_stats()
+        barrier()
+        ev0.record(stream)
+        for k in range(args.steps):
+            st.do_step("rk4", float(k), 1.0)
+        ev1.record(stream)
+        barrier()
+        ms4 = max_over_ranks(ev0.elapsed_time(ev1))
+        s4 = st.stats()
+        st.set_option(rk.OPT_TIMING, 0)
+        a4 = s4["stage_bytes"] / (s4["stage_kernel_ms"] / 1e3) / 1e9 if s4["stage_kernel_ms"] else None
+        line["extra"] = {"rk4": {
+            "value": cells_total * args.steps / (ms4 / 1e3), "ms_per_step": ms4 / args.steps,
+            "roofline": {"bound": "hbm", "achieved": a4, "peak": peak, "unit": "GB/s",
+                         "frac": a4 / peak if a4 else None,
+                         "traffic": traffic.get("rk4_bytes_per_launch") if traffic else None,
+                         "algorithmic_bytes_per_cell_step": s4["stage_bytes"] / args.steps / cells_local,
+                         "avg_launch_ms": s4["stage_kernel_ms"] / max(1, s4["stage_launches"])},
+            "gpu_launches": s4["kernel_launches"]}}
+
+        # ---- e2e: through the C-ABI with HOST buffers, copies inside the timed region ----
+        host_in = torch.from_numpy(u0).pin_memory()
+        host_out = torch.empty_like(host_in).pin_memory()
+        state["t"], state["dt"] = 0.0, 1.0
+        st.set(host_in)
+        for _ in range(1):
+            adaptive_step()
+        ke = max(1, min(args.steps, 5))
+        barrier()
+        ev0.record(stream)
+        for _ in range(ke):
+            st.set(host_in)            # H2D of the step's input state (pinned)
+            adaptive_step()            # includes the 8-byte error-ratio D2H per try
+            st.get(host_out)           # D2H of the step's result state (pinned)
+        ev1.record(stream)
+        barrier()
+        mse = max_over_ranks(ev0.elapsed_time(ev1))
+        nbytes = u0.nbytes
+        line["e2e"] = {"value": cells_total * ke / (mse / 1e3), "unit": "cell-updates/s",
+                       "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 8,
+                       "steps": ke, "ms_per_step": mse / ke}
+        if rank == 0 and world == 1:
+            line["cpu_baseline"] = cpu_baseline()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    st.close()
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,186 @@
+/*
+ * rk_b200.h — C-ABI of librkb200.so: B200-native explicit Runge–Kutta time stepping of a
+ * block-distributed fp64 state (the data-parallel hot path of arxiv 2309.05331,
+ * "OpenFPM + Boost.Odeint distributed algebra").
+ *
+ * Citations: P:Lnn = PAPER.md line nn; S:Lnn = SPEC.md line nn; DESIGN.md R-n = a
+ * recorded reading of the paper where it is silent, garbled or self-contradictory.
+ *
+ * Conventions (all entry points):
+ *   - Return an rk_status; never abort or throw across the ABI.  On failure the message
+ *     is available from rk_last_error() (thread-local).  CUDA/NCCL errors poison the ctx:
+ *     every later call on it returns RK_ERR_CUDA / RK_ERR_NCCL.
+ *   - Handles are opaque, created and destroyed by the caller.  The library owns all
+ *     device buffers it allocates; pointers passed in are borrowed for the call only.
+ *   - All device work is ordered on the ctx compute stream (the stream given to
+ *     rk_ctx_create, normally torch's current stream).  Calls that return host values
+ *     (step counts, norms, error ratios) synchronise that stream.
+ *   - "Collective" calls must be made by every rank of the ctx, in the same order and
+ *     with identical scalar arguments (MPI style), because they exchange halos (NCCL
+ *     send/recv over NVLink) or reduce (NCCL allreduce max).
+ *   - Floating point: fp64 throughout, IEEE division, no FMA contraction, no flush to
+ *     zero.  Sums run left to right in increasing stage index and skip zero Butcher
+ *     coefficients (R-17), so results are bitwise identical for any number of
+ *     GPUs ("the same, regardless of the degree of parallelism").
+ *
+ * Data layout of a state's local block (host or device arrays in rk_state_set/get):
+ *   grid state   (Gray–Scott):   [z][c][y][x], x fastest; the rank owns global planes
+ *                                z in [begin, begin+count) of a z-slab partition.
+ *   vector state (exp/logistic): [c][i]; the rank owns elements [begin, begin+count) of
+ *                                every component.
+ *   Partition rule: Nz (or N) split into world contiguous blocks; the remainder goes one
+ *   each to the lowest ranks.  Every rank must own >= 1 plane / element.
+ */
+#ifndef RK_B200_H
+#define RK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RK_ABI_VERSION 1
+#define RK_UNIQUE_ID_BYTES 128
+
+typedef struct rk_ctx_s* rk_ctx;     /* one per rank: device, streams, NCCL communicator */
+typedef struct rk_state_s* rk_state; /* a distributed state plus its stage workspace      */
+
+typedef enum {
+    RK_OK = 0,
+    RK_ERR_ARG = 1,          /* invalid argument (dt <= 0, t1 <= t0, atol <= 0, rtol < 0,
+                                ncomp not in [1,6], dims <= 0, a rank owning no plane ...) */
+    RK_ERR_CONTRACT = 2,     /* shape mismatch (lincomb), arity k not in [1,14]   */
+    RK_ERR_UNSUPPORTED = 3,  /* adaptive stepping with a scheme without error estimate   */
+    RK_ERR_STATE = 4,        /* RHS unset; Gray–Scott on a vector state or ncomp != 2     */
+    RK_ERR_DIVERGED = 5,     /* non-finite error ratio (NaN) during adaptive stepping     */
+    RK_ERR_DT_UNDERFLOW = 6, /* adaptive dt fell below 16*eps*max(|t|,1)                  */
+    RK_ERR_STALL = 7,        /* more than 500 tries for one step (Odeint default)         */
+    RK_ERR_CUDA = 8,         /* CUDA error; the ctx is poisoned                           */
+    RK_ERR_NCCL = 9,         /* NCCL error; the ctx is poisoned                           */
+    RK_ERR_OOM = 10          /* device allocation failed                                  */
+} rk_status;
+
+/* Table 1, the explicit one-step rows on the hot path.  CK54 and DOPRI5 are
+ * used fixed-step (do_step / integrate_const) or error-controlled (integrate_adaptive),
+ * reproducing both the "fixed" and "dynamic step size" rows of Table 1. */
+typedef enum { RK_EULER = 0, RK_RK4 = 1, RK_CASH_KARP54 = 2, RK_DOPRI5 = 3 } rk_scheme;
+
+/* Options for rk_set_option. */
+typedef enum {
+    RK_OPT_HALO_OVERLAP = 1, /* 1 (default): interior stencil overlaps the halo exchange;
+                                0: exchange first, then one full-slab launch              */
+    RK_OPT_HALO_LOOPBACK = 2,/* world==1 only: 1 runs the multi-GPU halo path (pack, ghost
+                                planes, interior+boundary launches) with a device-to-device
+                                self-exchange instead of in-kernel periodic wrap (testing) */
+    RK_OPT_MAX_TRIES = 3,    /* adaptive: tries per step before RK_ERR_STALL (default 500) */
+    RK_OPT_TIMING = 4,       /* 1: time every stage-kernel launch with CUDA events (stats) */
+    RK_OPT_USE_GRAPH = 5     /* 1: replay fixed-step grid steps from captured CUDA graphs    */
+} rk_option;
+
+/* Counters since creation or the last rk_reset_stats. */
+typedef struct {
+    int64_t rhs_evals;        /* stage RHS evaluations (per rank)                         */
+    int64_t steps;            /* completed fixed steps                                    */
+    int64_t tries;            /* adaptive tries                                           */
+    int64_t accepted;         /* adaptive accepted tries                                  */
+    int64_t rejected;         /* adaptive rejected tries                                  */
+    int64_t kernel_launches;  /* kernels launched by this library                         */
+    int64_t halo_exchanges;   /* halo exchanges (one per stage that needs ghost planes)   */
+    int64_t halo_bytes;       /* bytes sent by this rank in halo exchanges                */
+    int64_t stage_launches;   /* Gray–Scott stage-kernel launches                         */
+    double stage_kernel_ms;   /* sum of their durations (RK_OPT_TIMING=1, else 0)         */
+    double halo_ms;           /* time of the halo exchanges on the comm stream (TIMING=1) */
+    double last_err_ratio;    /* E of the last adaptive try                               */
+    double last_dt;           /* dt proposed after the last adaptive try                  */
+    int64_t stage_bytes;      /* algorithmic HBM bytes of the stage-kernel launches: per
+                                 launch (1 + #k_j read) arrays read + arrays written, over
+                                 the launch's cells; halo re-reads,
+                                 ghost planes and reductions are not counted              */
+} rk_stats;
+
+/* ---- library ------------------------------------------------------------------------ */
+int rk_abi_version(void);
+const char* rk_last_error(void);
+/* Host-only helpers (no GPU needed). */
+/* Partition rule above: rank's [begin, begin+count) of n_global items. */
+rk_status rk_partition(int64_t n_global, int world, int rank, int64_t* begin, int64_t* count);
+/* Library's Butcher tableau as doubles a[s*s], b[s], e[s] = b - bhat (exact rational rounded
+ * once, R-11), c[s]; *s <= 7; *order, *err_order (0 if none). */
+rk_status rk_tableau(rk_scheme scheme, double* a, double* b, double* e, double* c, int* s,
+                     int* order, int* err_order);
+/* Odeint default step adjuster (R-12/R-14) applied to E and *dt: returns 1 in
+ * *accepted if E <= 1 (then dt grows when E < 0.5), 0 if rejected (dt shrinks). */
+rk_status rk_controller(rk_scheme scheme, double E, double* dt, int* accepted);
+
+/* ---- context ------------------------------------------------------------------------ */
+/* Rank 0 creates the NCCL unique id (RK_UNIQUE_ID_BYTES bytes); the caller broadcasts it
+ * (torch.distributed) to all ranks before rk_ctx_create.  Not needed when world == 1. */
+rk_status rk_nccl_unique_id(void* out);
+/* Collective when world > 1.  device: CUDA ordinal; cuda_stream: cudaStream_t to order
+ * work on (NULL = a new non-blocking stream owned by the ctx); uid: NULL if world == 1. */
+rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* cuda_stream,
+                        rk_ctx* out);
+rk_status rk_ctx_destroy(rk_ctx ctx);
+
+/* ---- state --------------------------------------------------------------------------- */
+/* Distributed Nx x Ny x Nz periodic grid of ncomp fp64 components, z-slab partitioned
+ * (R-20).  Collective. */
+rk_status rk_state_create_grid(rk_ctx ctx, int64_t nx, int64_t ny, int64_t nz, int ncomp,
+                               rk_state* out);
+/* Distributed vector of n elements x ncomp components (block partition).  Collective. */
+rk_status rk_state_create_vector(rk_ctx ctx, int64_t n, int ncomp, rk_state* out);
+rk_status rk_state_destroy(rk_state st);
+/* This rank's owned planes (grid) or elements (vector). */
+rk_status rk_state_local_range(rk_state st, int64_t* begin, int64_t* count);
+/* Number of fp64 values in this rank's block (count * ncomp * Nx * Ny for a grid). */
+rk_status rk_state_local_size(rk_state st, int64_t* n_values);
+/* Copy this rank's block in (set) or out (get), layout above.  on_device != 0: the pointer
+ * is device memory on the ctx device (copied on the ctx stream); else host memory (pinned
+ * or pageable).  Returns after the copy completes. */
+rk_status rk_state_set(rk_state st, const double* src, int src_on_device);
+rk_status rk_state_get(rk_state st, double* dst, int dst_on_device);
+
+/* ---- right-hand sides --------------------------------------------------------------- */
+/* du/dt = lambda*u, elementwise (Eq. 1a; R-9). */
+rk_status rk_set_rhs_exponential(rk_state st, double lambda);
+/* du/dt = u*(1-u), elementwise (Eq. 1b). */
+rk_status rk_set_rhs_logistic(rk_state st);
+/* 3D Gray–Scott, Listing 2 (R-1..R-3): grid state, ncomp==2.
+ *   f0 = d1*Lap(C0) - C0*C1*C1 + F - F*C0,  f1 = d2*Lap(C1) + C0*C1*C1 - (F+K)*C1,
+ * Lap = 7-point periodic central difference with spacing h (difference form). */
+rk_status rk_set_rhs_gray_scott(rk_state st, double d1, double d2, double F, double K, double h);
+rk_status rk_set_option(rk_state st, int key, int64_t value);
+
+/* ---- stepping (all collective) ------------------------------------------------------ */
+/* One explicit step u <- u + dt*sum_j b_j k_j in place ("do_step()"). */
+rk_status rk_do_step(rk_state st, rk_scheme scheme, double t, double dt);
+/* One error-controlled try: computes the embedded error ratio
+ * E = max_i |e_i| / (atol + rtol*(|u_i| + dt*|k1_i|)) (R-12/R-13), accepts
+ * (u <- u_new) iff E <= 1, and proposes the next dt.  CK54 / DOPRI5 only. */
+rk_status rk_try_step(rk_state st, rk_scheme scheme, double t, double dt, double atol,
+                      double rtol, int* accepted, double* err_ratio, double* dt_next);
+/* Fixed-step loop of Odeint's integrate_const (R-15): steps while
+ * (t_n + dt) - t1 <= eps, t_n = t0 + n*dt; *steps = n. */
+rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1, double dt,
+                             int64_t* steps);
+/* Error-controlled loop of Odeint's integrate_adaptive (R-16): advances
+ * u from t0 to exactly t1; *accepted / *rejected count tries.  DOPRI5 reuses k7 as the next
+ * k1 (FSAL); CK54 reuses k1 across retries. */
+rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double t1, double dt0,
+                                double atol, double rtol, int64_t* accepted, int64_t* rejected);
+
+/* ---- algebra ops (P:L133-135 for_each# / for_each_norm) ------------------- */
+/* out = sum_{j<k} coef[j]*in[j] elementwise, left to right, 1 <= k <= 14 (the paper's 15
+ * participating states).  out may alias an input.  coef: host array. */
+rk_status rk_lincomb(rk_state out, int k, const double* coef, const rk_state* in);
+/* Global max |u| over all ranks (collective); NaN if any element is NaN. */
+rk_status rk_norm_inf(rk_state st, double* out);
+
+rk_status rk_get_stats(rk_state st, rk_stats* out);
+rk_status rk_reset_stats(rk_state st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RK_B200_H */

@@ -1,0 +1,229 @@
+"""Thin Python API over librkb200.so (include/rk_b200.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; PyTorch supplies the
+CUDA stream, device tensors for set/get, and the process group that broadcasts the NCCL
+unique id.  Names follow the C-ABI (and the paper's Odeint vocabulary: do_step,
+integrate_const, integrate_adaptive).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from ._native import Stats, call
+
+EULER, RK4, CASH_KARP54, DOPRI5 = 0, 1, 2, 3
+SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5}
+
+
+def _scheme(s) -> int:
+    return SCHEMES[s] if isinstance(s, str) else int(s)
+
+
+def _stream_handle(stream) -> int | None:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)  # torch.cuda.Stream
+
+
+class Context:
+    """One per rank (one process per device).  world > 1 needs the NCCL unique id,
+    which ``Context.from_torch_distributed`` broadcasts over the torch process group."""
+
+    def __init__(self, rank: int = 0, world: int = 1, device: int = 0, stream=None,
+                 unique_id: bytes | None = None):
+        L = _native.lib()
+        h = ctypes.c_void_p()
+        uid = None
+        if world > 1:
+            if unique_id is None or len(unique_id) != _native.UNIQUE_ID_BYTES:
+                raise ValueError("world > 1 needs a 128-byte NCCL unique id")
+            uid = ctypes.create_string_buffer(bytes(unique_id), _native.UNIQUE_ID_BYTES)
+        sh = _stream_handle(stream)
+        call("rk_ctx_create", rank, world, device, uid, ctypes.c_void_p(sh) if sh else None,
+             ctypes.byref(h))
+        self._h = h
+        self._L = L
+        self.rank, self.world, self.device = rank, world, device
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(_native.UNIQUE_ID_BYTES)
+        call("rk_nccl_unique_id", buf)
+        return buf.raw
+
+    @classmethod
+    def from_torch_distributed(cls, device: int, stream=None, group=None) -> "Context":
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = None
+        if world > 1:
+            t = torch.zeros(_native.UNIQUE_ID_BYTES, dtype=torch.uint8)
+            if rank == 0:
+                t[:] = torch.frombuffer(bytearray(cls.nccl_unique_id()), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda(device)
+            dist.broadcast(t, src=0, group=group)
+            uid = bytes(t.cpu().numpy().tobytes())
+        return cls(rank, world, device, stream, uid)
+
+    def grid(self, nx: int, ny: int, nz: int, ncomp: int = 2) -> "State":
+        h = ctypes.c_void_p()
+        call("rk_state_create_grid", self._h, nx, ny, nz, ncomp, ctypes.byref(h))
+        return State(self, h, grid=True, dims=(nx, ny, nz), ncomp=ncomp)
+
+    def vector(self, n: int, ncomp: int = 1) -> "State":
+        h = ctypes.c_void_p()
+        call("rk_state_create_vector", self._h, n, ncomp, ctypes.byref(h))
+        return State(self, h, grid=False, dims=(n,), ncomp=ncomp)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.rk_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class State:
+    """A distributed state: z-slab grid [z][c][y][x] or block vector [c][i] (rk_b200.h)."""
+
+    def __init__(self, ctx: Context, h, grid: bool, dims, ncomp: int):
+        self.ctx, self._h, self.grid, self.dims, self.ncomp = ctx, h, grid, dims, ncomp
+        b, c, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        call("rk_state_local_range", h, ctypes.byref(b), ctypes.byref(c))
+        call("rk_state_local_size", h, ctypes.byref(n))
+        self.begin, self.local, self.size = b.value, c.value, n.value
+
+    @property
+    def local_shape(self) -> tuple:
+        if self.grid:
+            nx, ny, _ = self.dims
+            return (self.local, self.ncomp, ny, nx)
+        return (self.ncomp, self.local)
+
+    # ---- data movement -------------------------------------------------------------
+    def set(self, src) -> None:
+        """src: numpy array (host) or torch tensor (host or on this device), fp64."""
+        if hasattr(src, "data_ptr"):  # torch
+            assert src.dtype.__repr__() == "torch.float64" and src.is_contiguous()
+            assert src.numel() == self.size
+            call("rk_state_set", self._h, ctypes.c_void_p(src.data_ptr()), 1 if src.is_cuda else 0)
+        else:
+            a = np.ascontiguousarray(src, dtype=np.float64)
+            assert a.size == self.size, (a.size, self.size)
+            call("rk_state_set", self._h, a.ctypes.data_as(ctypes.c_void_p), 0)
+
+    def get(self, out=None):
+        """Returns a numpy array of local_shape, or fills `out` (numpy / torch)."""
+        if out is None:
+            out = np.empty(self.local_shape, dtype=np.float64)
+        if hasattr(out, "data_ptr"):
+            assert out.numel() == self.size and out.is_contiguous()
+            call("rk_state_get", self._h, ctypes.c_void_p(out.data_ptr()), 1 if out.is_cuda else 0)
+        else:
+            assert out.size == self.size and out.flags.c_contiguous and out.dtype == np.float64
+            call("rk_state_get", self._h, out.ctypes.data_as(ctypes.c_void_p), 0)
+        return out
+
+    # ---- RHS / options -------------------------------------------------------------
+    def set_rhs_exponential(self, lam: float) -> None:
+        call("rk_set_rhs_exponential", self._h, lam)
+
+    def set_rhs_logistic(self) -> None:
+        call("rk_set_rhs_logistic", self._h)
+
+    def set_rhs_gray_scott(self, d1=2e-4, d2=1e-4, F=0.014, K=0.053, h=2.5 / 64) -> None:
+        call("rk_set_rhs_gray_scott", self._h, d1, d2, F, K, h)
+
+    def set_option(self, key: int, value: int) -> None:
+        call("rk_set_option", self._h, key, value)
+
+    # ---- stepping ------------------------------------------------------------------
+    def do_step(self, scheme, t: float, dt: float) -> None:
+        call("rk_do_step", self._h, _scheme(scheme), t, dt)
+
+    def try_step(self, scheme, t: float, dt: float, atol: float, rtol: float):
+        """Returns (accepted, err_ratio, dt_next)."""
+        a, e, d = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+        call("rk_try_step", self._h, _scheme(scheme), t, dt, atol, rtol, ctypes.byref(a),
+             ctypes.byref(e), ctypes.byref(d))
+        return bool(a.value), e.value, d.value
+
+    def integrate_const(self, scheme, t0: float, t1: float, dt: float) -> int:
+        n = ctypes.c_int64()
+        call("rk_integrate_const", self._h, _scheme(scheme), t0, t1, dt, ctypes.byref(n))
+        return n.value
+
+    def integrate_adaptive(self, scheme, t0, t1, dt0, atol, rtol):
+        """Returns (accepted, rejected)."""
+        a, r = ctypes.c_int64(), ctypes.c_int64()
+        call("rk_integrate_adaptive", self._h, _scheme(scheme), t0, t1, dt0, atol, rtol,
+             ctypes.byref(a), ctypes.byref(r))
+        return a.value, r.value
+
+    # ---- algebra -------------------------------------------------------------------
+    def lincomb(self, coef, states) -> None:
+        """self = sum_j coef[j] * states[j] (1 <= k <= 14)."""
+        k = len(states)
+        c = (ctypes.c_double * max(k, 1))(*coef)
+        hs = (ctypes.c_void_p * max(k, 1))(*[s._h for s in states])
+        call("rk_lincomb", self._h, k, c, hs)
+
+    def norm_inf(self) -> float:
+        d = ctypes.c_double()
+        call("rk_norm_inf", self._h, ctypes.byref(d))
+        return d.value
+
+    def stats(self) -> dict:
+        s = Stats()
+        call("rk_get_stats", self._h, ctypes.byref(s))
+        return s.as_dict()
+
+    def reset_stats(self) -> None:
+        call("rk_reset_stats", self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _native.lib().rk_state_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- host-only helpers (no GPU) ------------------------------------------------------
+def partition(n_global: int, world: int, rank: int) -> tuple[int, int]:
+    b, c = ctypes.c_int64(), ctypes.c_int64()
+    call("rk_partition", n_global, world, rank, ctypes.byref(b), ctypes.byref(c))
+    return b.value, c.value
+
+
+def tableau(scheme) -> dict:
+    S = 7
+    a, b, e, c = (ctypes.c_double * (S * S))(), (ctypes.c_double * S)(), (ctypes.c_double * S)(), \
+        (ctypes.c_double * S)()
+    s, o, eo = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    call("rk_tableau", _scheme(scheme), a, b, e, c, ctypes.byref(s), ctypes.byref(o), ctypes.byref(eo))
+    n = s.value
+    return {"s": n, "a": [[a[i * n + j] for j in range(n)] for i in range(n)], "b": list(b[:n]),
+            "e": list(e[:n]), "c": list(c[:n]), "order": o.value, "err_order": eo.value}
+
+
+def controller(scheme, E: float, dt: float):
+    """Library's host step adjuster: returns (accepted, dt_next)."""
+    d, a = ctypes.c_double(dt), ctypes.c_int()
+    call("rk_controller", _scheme(scheme), E, ctypes.byref(d), ctypes.byref(a))
+    return bool(a.value), d.value

@@ -1,0 +1,120 @@
+// rk_pointwise.cu — K1: the whole explicit RK step of a pointwise RHS in registers.
+//
+// For du/dt = lambda*u (Eq. 1a) and du/dt = u(1-u) (Eq. 1b) every element
+// is an independent ODE, so all stages Y_i, k_i, the final combination u_new and the
+// embedded error live in registers: one 16 B/element HBM round trip per launch however
+// many stages or fixed steps it covers (the "on-the-fly computation of stages" the paper
+// credits for Odeint's speed).  Expression trees follow DESIGN.md R-17 exactly:
+//   Y_i = u (+) (g_ij (x) k_j) over a_ij != 0, left to right;  u_new likewise with beta_j;
+//   e = (delta_j (x) k_j) (+) ... over e_j != 0;  r = |e| / (atol (+) rtol (x) (|u| (+) dt (x) |k1|)).
+#include "rk_device.cuh"
+#include "rk_kernels.cuh"
+#include "rk_tableau.h"
+
+namespace rkb {
+
+__host__ __device__ constexpr bool a_nz(int S, int i, int j) { return rat_nz(tableau_of(S).a[i][j]); }
+__host__ __device__ constexpr bool b_nz(int S, int j) { return rat_nz(tableau_of(S).b[j]); }
+__host__ __device__ constexpr bool e_nz(int S, int j) { return rat_nz(err_weight(tableau_of(S), j)); }
+// stages actually evaluated: up to the last j with b_j != 0 (or e_j != 0 with error)
+__host__ __device__ constexpr int s_eff(int S, bool err) {
+    int n = 0;
+    for (int j = 0; j < tableau_of(S).s; ++j)
+        if (b_nz(S, j) || (err && e_nz(S, j))) n = j + 1;
+    return n;
+}
+
+template <int RHS>
+__device__ __forceinline__ double f_pointwise(double y, double lambda) {
+    if constexpr (RHS == RHS_EXP) return mul(lambda, y);
+    else return mul(y, sub(1.0, y));
+}
+
+template <int S, int RHS, bool ERR>
+__device__ __forceinline__ double pw_steps(double x, const PwArgs& a, unsigned long long& rmax) {
+    constexpr int SE = s_eff(S, ERR);
+    const int nsteps = ERR ? 1 : a.nsteps;
+    for (int n = 0; n < nsteps; ++n) {
+        double k[7];
+#pragma unroll
+        for (int i = 0; i < SE; ++i) {
+            double y = x;
+#pragma unroll
+            for (int j = 0; j < i; ++j)
+                if (a_nz(S, i, j)) y = add(y, mul(a.cf.g[i][j], k[j]));
+            k[i] = f_pointwise<RHS>(y, a.lambda);
+        }
+        double w = x;
+#pragma unroll
+        for (int j = 0; j < SE; ++j)
+            if (b_nz(S, j)) w = add(w, mul(a.cf.beta[j], k[j]));
+        if constexpr (ERR) {
+            double e = 0.0;
+            bool first = true;
+#pragma unroll
+            for (int j = 0; j < SE; ++j) {
+                if (!e_nz(S, j)) continue;
+                const double t = mul(a.cf.delta[j], k[j]);
+                e = first ? t : add(e, t);
+                first = false;
+            }
+            const double den = add(a.atol, mul(a.rtol, add(fabs(x), mul(a.dt, fabs(k[0])))));
+            const unsigned long long rb = ratio_bits(fabs(e) / den);
+            rmax = rb > rmax ? rb : rmax;
+        }
+        x = w;
+    }
+    return x;
+}
+
+template <int S, int RHS, bool ERR>
+__global__ void __launch_bounds__(256) pointwise_kernel(const PwArgs a) {
+    unsigned long long rmax = 0ull;
+    const int64_t n2 = a.count >> 1;
+    const double2* __restrict__ u2 = reinterpret_cast<const double2*>(a.u);
+    double2* __restrict__ o2 = reinterpret_cast<double2*>(a.u_out);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+        double2 v = __ldg(u2 + i);
+        v.x = pw_steps<S, RHS, ERR>(v.x, a, rmax);
+        v.y = pw_steps<S, RHS, ERR>(v.y, a, rmax);
+        o2[i] = v;
+    }
+    if ((a.count & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = a.count - 1;
+        a.u_out[i] = pw_steps<S, RHS, ERR>(a.u[i], a, rmax);
+    }
+    if constexpr (ERR) block_max_to_global(rmax, a.errmax);
+}
+
+template <int S, int RHS>
+static cudaError_t launch_s_rhs(const PwArgs& a, cudaStream_t st, int num_sms) {
+    const int64_t n2 = (a.count + 1) / 2;
+    int64_t blocks = (n2 + 255) / 256;
+    const int64_t cap = (int64_t)num_sms * 8;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    if (a.errmax)
+        pointwise_kernel<S, RHS, true><<<(unsigned)blocks, 256, 0, st>>>(a);
+    else
+        pointwise_kernel<S, RHS, false><<<(unsigned)blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int S>
+static cudaError_t launch_s(const PwArgs& a, cudaStream_t st, int num_sms) {
+    if (a.rhs == RHS_EXP) return launch_s_rhs<S, RHS_EXP>(a, st, num_sms);
+    return launch_s_rhs<S, RHS_LOGISTIC>(a, st, num_sms);
+}
+
+cudaError_t launch_pointwise(int scheme, const PwArgs& a, cudaStream_t st, int num_sms) {
+    switch (scheme) {
+    case 0: return launch_s<0>(a, st, num_sms);
+    case 1: return launch_s<1>(a, st, num_sms);
+    case 2: return launch_s<2>(a, st, num_sms);
+    case 3: return launch_s<3>(a, st, num_sms);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace rkb

@@ -1,0 +1,1051 @@
+// rk_runtime.cu — host runtime behind the C-ABI (include/rk_b200.h).
+//
+// Context (device, compute + comm streams, NCCL communicator), distributed states
+// (z-slab grid / block vector, ping-pong u/u_new, lazily sized k_j workspace, ghost
+// planes), the stage scheduler (per stage: pack -> NCCL send/recv on the comm stream,
+// overlapped with the interior stencil launch; boundary launch after the halo event),
+// the drivers do_step / try_step / integrate_const / integrate_adaptive (Odeint loops,
+// P:L198) and the host step-size controller (R-12).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "rk_b200.h"
+#include "rk_kernels.cuh"
+#include "rk_tableau.h"
+
+using namespace rkb;
+
+// ------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static rk_status fail(rk_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+struct rk_ctx_s {
+    int rank = 0, world = 1, device = 0;
+    cudaStream_t stream = nullptr, comm = nullptr;
+    bool own_stream = false;
+    ncclComm_t nccl = nullptr;
+    int num_sms = 148;
+    rk_status poisoned = RK_OK;
+    unsigned long long* d_scratch = nullptr;  // 8 B reduction word (norm_inf)
+    unsigned long long* h_scratch = nullptr;  // pinned
+};
+
+#define CK_CTX(ctx, call)                                                                     \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) {                                                              \
+            (ctx)->poisoned = RK_ERR_CUDA;                                                    \
+            return fail(RK_ERR_CUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_),   \
+                        __FILE__, __LINE__, #call);                                           \
+        }                                                                                     \
+    } while (0)
+
+#define NK_CTX(ctx, call)                                                                     \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess) {                                                              \
+            (ctx)->poisoned = RK_ERR_NCCL;                                                    \
+            return fail(RK_ERR_NCCL, "NCCL error %s at %s:%d", ncclGetErrorString(r_),        \
+                        __FILE__, __LINE__);                                                  \
+        }                                                                                     \
+    } while (0)
+
+#define TRY(call)                          \
+    do {                                   \
+        rk_status s_ = (call);             \
+        if (s_ != RK_OK) return s_;        \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ------------------------------------------------------------------------------------
+// state
+// ------------------------------------------------------------------------------------
+struct TimedPair {
+    cudaEvent_t a, b;
+    int kind;  // 0 stage kernel, 1 halo
+};
+
+struct rk_state_s {
+    rk_ctx ctx = nullptr;
+    bool grid = false;
+    int ncomp = 1;
+    int64_t nx = 1, ny = 1, nz = 1;  // grid (global dims)
+    int64_t n = 0;                   // vector: global elements
+    int64_t begin = 0, local = 0;    // owned planes (grid) or elements (vector)
+    int64_t count = 0;               // fp64 values in the local block
+    double* u = nullptr;
+    double* u_new = nullptr;
+    double* k[7] = {nullptr};
+    int nk = 0;
+    bool k1_valid = false;           // k[0] == F(u) for the current u
+    // halo (grid, world > 1 or loopback)
+    double* sendbuf = nullptr;       // [lo plane | hi plane]
+    double* ghostbuf = nullptr;      // [ghost_hi | ghost_lo] (so one message serves world==2)
+    cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    unsigned long long* d_err = nullptr;
+    unsigned long long* h_err = nullptr;
+    // rhs
+    int rhs = RHS_NONE;
+    double lambda = 0.0, d1 = 0.0, d2 = 0.0, F = 0.0, K = 0.0, h = 1.0;
+    // options
+    bool overlap = true, loopback = false, timing = false, use_graph = false;
+    int max_tries = 500;
+    // stats
+    rk_stats stats{};
+    std::vector<TimedPair> pending;
+    std::vector<cudaEvent_t> event_pool;
+};
+
+static rk_status check_state(rk_state st) {
+    if (!st || !st->ctx) return fail(RK_ERR_ARG, "null state");
+    if (st->ctx->poisoned != RK_OK) return fail(st->ctx->poisoned, "context poisoned by an earlier CUDA/NCCL error");
+    return RK_OK;
+}
+
+static rk_status dev_alloc(rk_ctx ctx, double** p, int64_t count) {
+    cudaError_t e = cudaMalloc((void**)p, sizeof(double) * (size_t)std::max<int64_t>(count, 1));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RK_ERR_OOM, "cudaMalloc of %lld doubles failed: %s", (long long)count,
+                    cudaGetErrorString(e));
+    }
+    (void)ctx;
+    return RK_OK;
+}
+
+static rk_status ensure_k(rk_state st, int nk) {
+    for (int j = st->nk; j < nk; ++j) {
+        TRY(dev_alloc(st->ctx, &st->k[j], st->count));
+        st->nk = j + 1;
+    }
+    return RK_OK;
+}
+
+static int64_t plane_values(rk_state st) { return st->nx * st->ny * st->ncomp; }
+
+static cudaEvent_t pool_event(rk_state st) {
+    if (!st->event_pool.empty()) {
+        cudaEvent_t e = st->event_pool.back();
+        st->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+static rk_status resolve_timing(rk_state st) {
+    if (st->pending.empty()) return RK_OK;
+    rk_ctx ctx = st->ctx;
+    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->comm) CK_CTX(ctx, cudaStreamSynchronize(ctx->comm));
+    for (auto& p : st->pending) {
+        float ms = 0.f;
+        CK_CTX(ctx, cudaEventElapsedTime(&ms, p.a, p.b));
+        if (p.kind == 0) st->stats.stage_kernel_ms += ms;
+        else st->stats.halo_ms += ms;
+        st->event_pool.push_back(p.a);
+        st->event_pool.push_back(p.b);
+    }
+    st->pending.clear();
+    return RK_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// stage plans (built from the library's tableau; DESIGN.md §Stage schedule)
+// ------------------------------------------------------------------------------------
+struct StagePlan {
+    int stage = 0;
+    int nslots = 0;
+    int slot_j[kMaxSlots] = {0};
+    double g[kMaxSlots] = {0}, beta[kMaxSlots] = {0}, delta[kMaxSlots] = {0};
+    double beta_new = 0.0, delta_new = 0.0;
+    int epi = EPI_K;
+    int out_k = -1;      // k buffer written (EPI_K, EPI_FSAL_ERR)
+    bool writes_u = false;
+};
+
+struct Coeffs {
+    int s = 0, order = 0, err_order = 0;
+    double a[7][7] = {{0}}, b[7] = {0}, e[7] = {0}, c[7] = {0};
+    bool anz[7][7] = {{false}}, bnz[7] = {false}, enz[7] = {false};
+};
+
+static Coeffs coeffs_of(int scheme) {
+    Coeffs C;
+    const Tableau T = tableau_of(scheme);
+    C.s = T.s;
+    C.order = T.order;
+    C.err_order = T.err_order;
+    for (int i = 0; i < T.s; ++i) {
+        for (int j = 0; j < i; ++j) {
+            C.a[i][j] = rat_double(T.a[i][j]);
+            C.anz[i][j] = rat_nz(T.a[i][j]);
+        }
+        C.b[i] = rat_double(T.b[i]);
+        C.bnz[i] = rat_nz(T.b[i]);
+        const Rat e = err_weight(T, i);
+        C.e[i] = rat_double(e);
+        C.enz[i] = rat_nz(e);
+        C.c[i] = rat_double(T.c[i]);
+    }
+    return C;
+}
+
+static bool valid_scheme(int s) { return s >= RK_EULER && s <= RK_DOPRI5; }
+
+// Fixed step: stages up to the last b_j != 0, the last one fused with u_new.
+// Adaptive: stages up to the last b_j or e_j != 0, the last one fused with the error
+// ratio; a FSAL last stage (row s == b, b_s == 0) writes Y_s as u_new and k_s.
+static std::vector<StagePlan> build_plan(int scheme, bool adaptive, double dt) {
+    const Coeffs C = coeffs_of(scheme);
+    int last = 0;
+    for (int j = 0; j < C.s; ++j)
+        if (C.bnz[j] || (adaptive && C.enz[j])) last = j;
+    bool fsal = false;
+    if (adaptive && !C.bnz[last]) {
+        fsal = true;
+        for (int j = 0; j < last; ++j)
+            if (C.anz[last][j] != C.bnz[j] || C.a[last][j] != C.b[j]) fsal = false;
+    }
+    std::vector<StagePlan> plan;
+    for (int i = 0; i <= last; ++i) {
+        StagePlan p;
+        p.stage = i;
+        const bool fin = (i == last);
+        for (int j = 0; j < i; ++j) {
+            const bool need = C.anz[i][j] || (fin && C.bnz[j]) || (fin && adaptive && (C.enz[j] || j == 0));
+            if (!need) continue;
+            const int s = p.nslots++;
+            p.slot_j[s] = j;
+            p.g[s] = C.anz[i][j] ? dt * C.a[i][j] : 0.0;
+            p.beta[s] = (fin && C.bnz[j]) ? dt * C.b[j] : 0.0;
+            p.delta[s] = (fin && adaptive && C.enz[j]) ? dt * C.e[j] : 0.0;
+        }
+        if (!fin) {
+            p.epi = EPI_K;
+            p.out_k = i;
+        } else if (!adaptive) {
+            p.epi = EPI_FINAL;
+            p.writes_u = true;
+            p.beta_new = C.bnz[i] ? dt * C.b[i] : 0.0;
+        } else if (fsal) {
+            p.epi = EPI_FSAL_ERR;
+            p.writes_u = true;
+            p.delta_new = C.enz[i] ? dt * C.e[i] : 0.0;
+            // k_s goes into a buffer no slot of this stage reads: the first unused j
+            int free_j = -1;
+            for (int j = 1; j < i && free_j < 0; ++j) {
+                bool used = false;
+                for (int s = 0; s < p.nslots; ++s) used |= (p.slot_j[s] == j);
+                if (!used) free_j = j;
+            }
+            p.out_k = free_j;
+        } else {
+            p.epi = EPI_FINAL_ERR;
+            p.writes_u = true;
+            p.beta_new = C.bnz[i] ? dt * C.b[i] : 0.0;
+            p.delta_new = C.enz[i] ? dt * C.e[i] : 0.0;
+        }
+        plan.push_back(p);
+    }
+    return plan;
+}
+
+static int plan_num_k(const std::vector<StagePlan>& plan) {
+    int nk = 0;
+    for (auto& p : plan) {
+        if (p.out_k >= 0) nk = std::max(nk, p.out_k + 1);
+        for (int s = 0; s < p.nslots; ++s) nk = std::max(nk, p.slot_j[s] + 1);
+    }
+    return nk;
+}
+
+// ------------------------------------------------------------------------------------
+// Gray–Scott stage execution
+// ------------------------------------------------------------------------------------
+static bool halo_path(rk_state st) { return st->ctx->world > 1 || st->loopback; }
+
+static rk_status ensure_halo(rk_state st) {
+    if (!halo_path(st) || st->sendbuf) return RK_OK;
+    TRY(dev_alloc(st->ctx, &st->sendbuf, 2 * plane_values(st)));
+    TRY(dev_alloc(st->ctx, &st->ghostbuf, 2 * plane_values(st)));
+    CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_pack, cudaEventDisableTiming));
+    CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_halo, cudaEventDisableTiming));
+    return RK_OK;
+}
+
+static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
+    GsStageArgs a{};
+    a.u = st->u;
+    a.nslots = p.nslots;
+    for (int s = 0; s < p.nslots; ++s) {
+        a.k[s] = st->k[p.slot_j[s]];
+        a.g[s] = p.g[s];
+        a.beta[s] = p.beta[s];
+        a.delta[s] = p.delta[s];
+    }
+    a.beta_new = p.beta_new;
+    a.delta_new = p.delta_new;
+    a.out_k = p.out_k >= 0 ? st->k[p.out_k] : nullptr;
+    a.out_u = p.writes_u ? st->u_new : nullptr;
+    a.errmax = st->d_err;
+    a.dt = dt;
+    a.atol = atol;
+    a.rtol = rtol;
+    a.d1 = st->d1;
+    a.d2 = st->d2;
+    a.F = st->F;
+    a.FK = st->F + st->K;
+    a.inv_h2 = 1.0 / (st->h * st->h);
+    a.nx = (int)st->nx;
+    a.ny = (int)st->ny;
+    a.nzl = (int)st->local;
+    a.z_lo = 0;
+    a.z_hi = (int)st->local;
+    a.zmode = 0;
+    return a;
+}
+
+// planes per CTA: enough CTAs for ~16 per SM (2 resident x ~8 waves), >= 8 planes each
+static int pick_zchunk(rk_state st, int range) {
+    const int tiles = (int)(((st->nx + 31) / 32) * ((st->ny + 7) / 8));
+    const int target = st->ctx->num_sms * 16;
+    int nchunks = std::max(1, (target + tiles - 1) / tiles);
+    int zc = (range + nchunks - 1) / nchunks;
+    return std::max(zc, std::min(8, range));
+}
+
+static rk_status launch_stage_timed(rk_state st, int epi, GsStageArgs& a) {
+    rk_ctx ctx = st->ctx;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (st->timing) {
+        e0 = pool_event(st);
+        e1 = pool_event(st);
+        CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+    }
+    int nl = 0;
+    CK_CTX(ctx, launch_gs_stage(epi, a, ctx->stream, &nl));
+    st->stats.kernel_launches += nl;
+    st->stats.stage_launches += nl;
+    if (nl) {
+        const int64_t planes = a.zmode == 1 ? (a.nzl > 1 ? 2 : 1) : (int64_t)(a.z_hi - a.z_lo);
+        const int64_t arrays = 1 + a.nslots + (a.out_k ? 1 : 0) + (a.out_u ? 1 : 0);
+        st->stats.stage_bytes += planes * st->nx * st->ny * 2 * (int64_t)sizeof(double) * arrays;
+    }
+    if (st->timing) {
+        CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+        st->pending.push_back({e0, e1, 0});
+        if (st->pending.size() > 4096) TRY(resolve_timing(st));
+    }
+    return RK_OK;
+}
+
+static rk_status halo_exchange(rk_state st) {
+    rk_ctx ctx = st->ctx;
+    const int64_t pv = plane_values(st);
+    CK_CTX(ctx, cudaEventRecord(st->ev_pack, ctx->stream));
+    CK_CTX(ctx, cudaStreamWaitEvent(ctx->comm, st->ev_pack, 0));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (st->timing) {
+        e0 = pool_event(st);
+        e1 = pool_event(st);
+        CK_CTX(ctx, cudaEventRecord(e0, ctx->comm));
+    }
+    double* send_lo = st->sendbuf;
+    double* send_hi = st->sendbuf + pv;
+    double* ghost_hi = st->ghostbuf;
+    double* ghost_lo = st->ghostbuf + pv;
+    if (ctx->world == 1) {
+        // loopback: my lower neighbour is myself: ghost_lo <- my hi plane, ghost_hi <- my lo
+        CK_CTX(ctx, cudaMemcpyAsync(st->ghostbuf, st->sendbuf, sizeof(double) * 2 * pv,
+                                    cudaMemcpyDeviceToDevice, ctx->comm));
+    } else {
+        const int up = (ctx->rank + 1) % ctx->world;
+        const int down = (ctx->rank - 1 + ctx->world) % ctx->world;
+        NK_CTX(ctx, ncclGroupStart());
+        if (up == down) {
+            // world == 2: both neighbours are one peer; one message each way,
+            // [lo|hi] lands in the peer's [ghost_hi|ghost_lo]
+            NK_CTX(ctx, ncclSend(st->sendbuf, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->comm));
+            NK_CTX(ctx, ncclRecv(st->ghostbuf, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->comm));
+        } else {
+            NK_CTX(ctx, ncclSend(send_hi, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->comm));
+            NK_CTX(ctx, ncclSend(send_lo, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->comm));
+            NK_CTX(ctx, ncclRecv(ghost_lo, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->comm));
+            NK_CTX(ctx, ncclRecv(ghost_hi, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->comm));
+        }
+        NK_CTX(ctx, ncclGroupEnd());
+    }
+    if (st->timing) {
+        CK_CTX(ctx, cudaEventRecord(e1, ctx->comm));
+        st->pending.push_back({e0, e1, 1});
+    }
+    CK_CTX(ctx, cudaEventRecord(st->ev_halo, ctx->comm));
+    st->stats.halo_exchanges += 1;
+    st->stats.halo_bytes += (int64_t)sizeof(double) * 2 * pv;
+    return RK_OK;
+}
+
+static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
+    rk_ctx ctx = st->ctx;
+    GsStageArgs a = stage_args(st, p, dt, atol, rtol);
+    const int nzl = (int)st->local;
+    st->stats.rhs_evals += 1;
+    if (!halo_path(st)) {
+        a.zchunk = pick_zchunk(st, nzl);
+        return launch_stage_timed(st, p.epi, a);
+    }
+    // multi-GPU path: Y_i on the two boundary planes -> neighbours' ghost planes
+    CK_CTX(ctx, launch_gs_pack(a, st->sendbuf, ctx->stream));
+    st->stats.kernel_launches += 1;
+    TRY(halo_exchange(st));
+    a.ghost_hi = st->ghostbuf;
+    a.ghost_lo = st->ghostbuf + plane_values(st);
+    if (st->overlap && nzl > 2) {
+        GsStageArgs in = a;  // interior planes [1, nzl-1) never touch ghost planes
+        in.z_lo = 1;
+        in.z_hi = nzl - 1;
+        in.zchunk = pick_zchunk(st, nzl - 2);
+        TRY(launch_stage_timed(st, p.epi, in));
+        CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_halo, 0));
+        GsStageArgs bd = a;
+        bd.zmode = 1;
+        return launch_stage_timed(st, p.epi, bd);
+    }
+    CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_halo, 0));
+    a.zchunk = pick_zchunk(st, nzl);
+    return launch_stage_timed(st, p.epi, a);
+}
+
+// Run the stages of one step / try.  Stage 0 (k1 = F(u)) is skipped when k1 is valid.
+static rk_status run_grid_plan(rk_state st, const std::vector<StagePlan>& plan, double dt,
+                               double atol, double rtol) {
+    TRY(ensure_k(st, plan_num_k(plan)));
+    TRY(ensure_halo(st));
+    for (const StagePlan& p : plan) {
+        if (p.stage == 0 && p.epi == EPI_K && st->k1_valid) continue;
+        if (p.epi == EPI_FINAL_ERR || p.epi == EPI_FSAL_ERR)
+            CK_CTX(st->ctx, cudaMemsetAsync(st->d_err, 0, sizeof(unsigned long long), st->ctx->stream));
+        TRY(run_gs_stage(st, p, dt, atol, rtol));
+        if (p.stage == 0 && p.epi == EPI_K) st->k1_valid = true;
+    }
+    return RK_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// pointwise (vector) execution
+// ------------------------------------------------------------------------------------
+static PwCoef pw_coef(int scheme, double dt) {
+    const Coeffs C = coeffs_of(scheme);
+    PwCoef cf{};
+    for (int i = 0; i < C.s; ++i) {
+        for (int j = 0; j < i; ++j) cf.g[i][j] = dt * C.a[i][j];
+        cf.beta[i] = dt * C.b[i];
+        cf.delta[i] = dt * C.e[i];
+    }
+    return cf;
+}
+
+static rk_status run_pointwise(rk_state st, int scheme, double dt, int nsteps, bool err,
+                               double atol, double rtol) {
+    rk_ctx ctx = st->ctx;
+    PwArgs a{};
+    a.u = st->u;
+    a.u_out = st->u_new;
+    a.count = st->count;
+    a.rhs = st->rhs;
+    a.lambda = st->lambda;
+    a.nsteps = nsteps;
+    a.dt = dt;
+    a.atol = atol;
+    a.rtol = rtol;
+    a.errmax = err ? st->d_err : nullptr;
+    a.cf = pw_coef(scheme, dt);
+    if (err) CK_CTX(ctx, cudaMemsetAsync(st->d_err, 0, sizeof(unsigned long long), ctx->stream));
+    CK_CTX(ctx, launch_pointwise(scheme, a, ctx->stream, ctx->num_sms));
+    st->stats.kernel_launches += 1;
+    const Coeffs C = coeffs_of(scheme);
+    int se = 0;
+    for (int j = 0; j < C.s; ++j)
+        if (C.bnz[j] || (err && C.enz[j])) se = j + 1;
+    st->stats.rhs_evals += (int64_t)se * (err ? 1 : nsteps);
+    return RK_OK;
+}
+
+// ------------------------------------------------------------------------------------
+// controller (host, Odeint default_step_adjuster; R-12, R-14)
+// ------------------------------------------------------------------------------------
+static bool step_adjust(double E, int p, int q, double* dt) {
+    if (E > 1.0) {
+        double fac = (9.0 / 10.0) * std::pow(E, -1.0 / (double)(q - 1));
+        if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
+        *dt = *dt * fac;
+        return false;
+    }
+    if (E < 0.5) {
+        double Ec = std::pow(5.0, -(double)p);
+        if (E > Ec) Ec = E;
+        *dt = *dt * ((9.0 / 10.0) * std::pow(Ec, -1.0 / (double)p));
+    }
+    return true;
+}
+
+static rk_status check_rhs(rk_state st) {
+    if (st->rhs == RHS_NONE) return fail(RK_ERR_STATE, "RHS not set");
+    if (st->rhs == RHS_GRAY_SCOTT && (!st->grid || st->ncomp != 2))
+        return fail(RK_ERR_STATE, "Gray-Scott RHS needs a grid state with ncomp == 2");
+    if (st->rhs != RHS_GRAY_SCOTT && st->grid)
+        return fail(RK_ERR_STATE, "pointwise RHS on grid state: use a vector state");
+    return RK_OK;
+}
+
+// one fixed step, u <- u_new
+static rk_status fixed_step(rk_state st, int scheme, double dt) {
+    if (st->grid) {
+        auto plan = build_plan(scheme, false, dt);
+        TRY(run_grid_plan(st, plan, dt, 0.0, 0.0));
+    } else {
+        TRY(run_pointwise(st, scheme, dt, 1, false, 0.0, 0.0));
+    }
+    std::swap(st->u, st->u_new);
+    st->k1_valid = false;
+    st->stats.steps += 1;
+    return RK_OK;
+}
+
+// one try: E (global), accept -> swap
+static rk_status one_try(rk_state st, int scheme, double t, double dt, double atol, double rtol,
+                         int* accepted, double* E_out, double* dt_next) {
+    rk_ctx ctx = st->ctx;
+    const Coeffs C = coeffs_of(scheme);
+    bool fsal = false;
+    if (st->grid) {
+        auto plan = build_plan(scheme, true, dt);
+        fsal = plan.back().epi == EPI_FSAL_ERR;
+        TRY(run_grid_plan(st, plan, dt, atol, rtol));
+    } else {
+        TRY(run_pointwise(st, scheme, dt, 1, true, atol, rtol));
+    }
+    if (ctx->world > 1)
+        NK_CTX(ctx, ncclAllReduce(st->d_err, st->d_err, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
+    CK_CTX(ctx, cudaMemcpyAsync(st->h_err, st->d_err, sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    double E;
+    std::memcpy(&E, st->h_err, sizeof E);
+    st->stats.tries += 1;
+    st->stats.last_err_ratio = E;
+    if (std::isnan(E)) return fail(RK_ERR_DIVERGED, "non-finite error ratio at t=%.17g dt=%.17g", t, dt);
+    double dtn = dt;
+    const bool acc = step_adjust(E, C.order, C.err_order, &dtn);
+    st->stats.last_dt = dtn;
+    if (acc) {
+        std::swap(st->u, st->u_new);
+        if (st->grid && fsal) {
+            // k_s (FSAL) was written into a free k buffer: it is F(u_new), the next k1
+            const auto plan = build_plan(scheme, true, dt);
+            std::swap(st->k[0], st->k[plan.back().out_k]);
+            st->k1_valid = true;
+        } else {
+            st->k1_valid = false;
+        }
+        st->stats.accepted += 1;
+    } else {
+        st->stats.rejected += 1;
+    }
+    *accepted = acc ? 1 : 0;
+    *E_out = E;
+    *dt_next = dtn;
+    return RK_OK;
+}
+
+// ====================================================================================
+// C-ABI
+// ====================================================================================
+extern "C" {
+
+int rk_abi_version(void) { return RK_ABI_VERSION; }
+
+const char* rk_last_error(void) { return g_err.c_str(); }
+
+rk_status rk_partition(int64_t n_global, int world, int rank, int64_t* begin, int64_t* count) {
+    if (!begin || !count || world < 1 || rank < 0 || rank >= world || n_global < 1)
+        return fail(RK_ERR_ARG, "rk_partition: bad arguments");
+    const int64_t base = n_global / world, rem = n_global % world;
+    *count = base + (rank < rem ? 1 : 0);
+    *begin = rank * base + std::min<int64_t>(rank, rem);
+    if (*count < 1) return fail(RK_ERR_ARG, "rank %d would own no plane/element", rank);
+    return RK_OK;
+}
+
+rk_status rk_tableau(rk_scheme scheme, double* a, double* b, double* e, double* c, int* s,
+                     int* order, int* err_order) {
+    if (!valid_scheme(scheme)) return fail(RK_ERR_ARG, "bad scheme %d", (int)scheme);
+    const Coeffs C = coeffs_of(scheme);
+    for (int i = 0; i < C.s; ++i) {
+        for (int j = 0; j < C.s; ++j)
+            if (a) a[i * C.s + j] = j < i ? C.a[i][j] : 0.0;
+        if (b) b[i] = C.b[i];
+        if (e) e[i] = C.e[i];
+        if (c) c[i] = C.c[i];
+    }
+    if (s) *s = C.s;
+    if (order) *order = C.order;
+    if (err_order) *err_order = C.err_order;
+    return RK_OK;
+}
+
+rk_status rk_controller(rk_scheme scheme, double E, double* dt, int* accepted) {
+    if (!valid_scheme(scheme) || !dt || !accepted) return fail(RK_ERR_ARG, "bad arguments");
+    const Coeffs C = coeffs_of(scheme);
+    if (C.err_order == 0) return fail(RK_ERR_UNSUPPORTED, "scheme has no error estimate");
+    if (std::isnan(E)) return fail(RK_ERR_DIVERGED, "NaN error ratio");
+    *accepted = step_adjust(E, C.order, C.err_order, dt) ? 1 : 0;
+    return RK_OK;
+}
+
+rk_status rk_nccl_unique_id(void* out) {
+    if (!out) return fail(RK_ERR_ARG, "null output");
+    static_assert(sizeof(ncclUniqueId) == RK_UNIQUE_ID_BYTES, "unique id size");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(RK_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+    std::memcpy(out, &id, sizeof id);
+    return RK_OK;
+}
+
+rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* cuda_stream,
+                        rk_ctx* out) {
+    if (!out || world < 1 || rank < 0 || rank >= world || device < 0)
+        return fail(RK_ERR_ARG, "rk_ctx_create: bad arguments");
+    if (world > 1 && !uid) return fail(RK_ERR_ARG, "world > 1 needs the NCCL unique id");
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(RK_ERR_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+    }
+    if (device >= ndev) return fail(RK_ERR_ARG, "device %d >= device count %d", device, ndev);
+    rk_ctx ctx = new rk_ctx_s();
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->device = device;
+    DeviceGuard g(device);
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    auto bail = [&](rk_status s) {
+        if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+        if (ctx->comm) cudaStreamDestroy(ctx->comm);
+        delete ctx;
+        return s;
+    };
+    if (cuda_stream) {
+        ctx->stream = (cudaStream_t)cuda_stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(RK_ERR_CUDA, "cudaStreamCreate failed"));
+        ctx->own_stream = true;
+    }
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi) != cudaSuccess)
+        return bail(fail(RK_ERR_CUDA, "comm stream create failed"));
+    if (cudaMalloc((void**)&ctx->d_scratch, 8) != cudaSuccess ||
+        cudaMallocHost((void**)&ctx->h_scratch, 8) != cudaSuccess)
+        return bail(fail(RK_ERR_OOM, "scratch allocation failed"));
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, uid, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&ctx->nccl, world, id, rank);
+        if (r != ncclSuccess) return bail(fail(RK_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+    }
+    *out = ctx;
+    return RK_OK;
+}
+
+rk_status rk_ctx_destroy(rk_ctx ctx) {
+    if (!ctx) return RK_OK;
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+    if (ctx->comm) cudaStreamDestroy(ctx->comm);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    cudaFree(ctx->d_scratch);
+    cudaFreeHost(ctx->h_scratch);
+    delete ctx;
+    return RK_OK;
+}
+
+static rk_status state_common(rk_ctx ctx, rk_state st) {
+    DeviceGuard g(ctx->device);
+    TRY(dev_alloc(ctx, &st->u, st->count));
+    TRY(dev_alloc(ctx, &st->u_new, st->count));
+    CK_CTX(ctx, cudaMalloc((void**)&st->d_err, sizeof(unsigned long long)));
+    CK_CTX(ctx, cudaMallocHost((void**)&st->h_err, sizeof(unsigned long long)));
+    CK_CTX(ctx, cudaMemsetAsync(st->u, 0, sizeof(double) * (size_t)st->count, ctx->stream));
+    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    return RK_OK;
+}
+
+rk_status rk_state_create_grid(rk_ctx ctx, int64_t nx, int64_t ny, int64_t nz, int ncomp,
+                               rk_state* out) {
+    if (!ctx || !out) return fail(RK_ERR_ARG, "null argument");
+    if (ctx->poisoned) return fail(ctx->poisoned, "context poisoned");
+    if (nx < 1 || ny < 1 || nz < 1 || ncomp < 1 || ncomp > 6)
+        return fail(RK_ERR_ARG, "bad grid dims / ncomp");
+    if (nx * ny > (int64_t)1 << 30) return fail(RK_ERR_ARG, "plane too large");
+    rk_state st = new rk_state_s();
+    st->ctx = ctx;
+    st->grid = true;
+    st->ncomp = ncomp;
+    st->nx = nx;
+    st->ny = ny;
+    st->nz = nz;
+    rk_status s = rk_partition(nz, ctx->world, ctx->rank, &st->begin, &st->local);
+    if (s != RK_OK) {
+        delete st;
+        return s;
+    }
+    st->count = st->local * nx * ny * ncomp;
+    s = state_common(ctx, st);
+    if (s != RK_OK) {
+        rk_state_destroy(st);
+        return s;
+    }
+    *out = st;
+    return RK_OK;
+}
+
+rk_status rk_state_create_vector(rk_ctx ctx, int64_t n, int ncomp, rk_state* out) {
+    if (!ctx || !out) return fail(RK_ERR_ARG, "null argument");
+    if (ctx->poisoned) return fail(ctx->poisoned, "context poisoned");
+    if (n < 1 || ncomp < 1 || ncomp > 6) return fail(RK_ERR_ARG, "bad vector size / ncomp");
+    rk_state st = new rk_state_s();
+    st->ctx = ctx;
+    st->grid = false;
+    st->ncomp = ncomp;
+    st->n = n;
+    rk_status s = rk_partition(n, ctx->world, ctx->rank, &st->begin, &st->local);
+    if (s != RK_OK) {
+        delete st;
+        return s;
+    }
+    st->count = st->local * ncomp;
+    s = state_common(ctx, st);
+    if (s != RK_OK) {
+        rk_state_destroy(st);
+        return s;
+    }
+    *out = st;
+    return RK_OK;
+}
+
+rk_status rk_state_destroy(rk_state st) {
+    if (!st) return RK_OK;
+    DeviceGuard g(st->ctx->device);
+    cudaStreamSynchronize(st->ctx->stream);
+    if (st->ctx->comm) cudaStreamSynchronize(st->ctx->comm);
+    cudaFree(st->u);
+    cudaFree(st->u_new);
+    for (int j = 0; j < st->nk; ++j) cudaFree(st->k[j]);
+    cudaFree(st->sendbuf);
+    cudaFree(st->ghostbuf);
+    cudaFree(st->d_err);
+    cudaFreeHost(st->h_err);
+    if (st->ev_pack) cudaEventDestroy(st->ev_pack);
+    if (st->ev_halo) cudaEventDestroy(st->ev_halo);
+    for (auto& p : st->pending) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (auto e : st->event_pool) cudaEventDestroy(e);
+    delete st;
+    return RK_OK;
+}
+
+rk_status rk_state_local_range(rk_state st, int64_t* begin, int64_t* count) {
+    TRY(check_state(st));
+    if (begin) *begin = st->begin;
+    if (count) *count = st->local;
+    return RK_OK;
+}
+
+rk_status rk_state_local_size(rk_state st, int64_t* n_values) {
+    TRY(check_state(st));
+    if (n_values) *n_values = st->count;
+    return RK_OK;
+}
+
+rk_status rk_state_set(rk_state st, const double* src, int src_on_device) {
+    TRY(check_state(st));
+    if (!src) return fail(RK_ERR_ARG, "null src");
+    rk_ctx ctx = st->ctx;
+    DeviceGuard g(ctx->device);
+    CK_CTX(ctx, cudaMemcpyAsync(st->u, src, sizeof(double) * (size_t)st->count,
+                                src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                ctx->stream));
+    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    st->k1_valid = false;
+    return RK_OK;
+}
+
+rk_status rk_state_get(rk_state st, double* dst, int dst_on_device) {
+    TRY(check_state(st));
+    if (!dst) return fail(RK_ERR_ARG, "null dst");
+    rk_ctx ctx = st->ctx;
+    DeviceGuard g(ctx->device);
+    CK_CTX(ctx, cudaMemcpyAsync(dst, st->u, sizeof(double) * (size_t)st->count,
+                                dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    return RK_OK;
+}
+
+rk_status rk_set_rhs_exponential(rk_state st, double lambda) {
+    TRY(check_state(st));
+    st->rhs = RHS_EXP;
+    st->lambda = lambda;
+    st->k1_valid = false;
+    return RK_OK;
+}
+
+rk_status rk_set_rhs_logistic(rk_state st) {
+    TRY(check_state(st));
+    st->rhs = RHS_LOGISTIC;
+    st->k1_valid = false;
+    return RK_OK;
+}
+
+rk_status rk_set_rhs_gray_scott(rk_state st, double d1, double d2, double F, double K, double h) {
+    TRY(check_state(st));
+    if (!st->grid || st->ncomp != 2)
+        return fail(RK_ERR_STATE, "Gray-Scott RHS needs a grid state with ncomp == 2");
+    if (!(h > 0.0) || !std::isfinite(d1) || !std::isfinite(d2) || !std::isfinite(F) || !std::isfinite(K))
+        return fail(RK_ERR_ARG, "bad Gray-Scott parameters");
+    st->rhs = RHS_GRAY_SCOTT;
+    st->d1 = d1;
+    st->d2 = d2;
+    st->F = F;
+    st->K = K;
+    st->h = h;
+    st->k1_valid = false;
+    return RK_OK;
+}
+
+rk_status rk_set_option(rk_state st, int key, int64_t value) {
+    TRY(check_state(st));
+    switch (key) {
+    case RK_OPT_HALO_OVERLAP: st->overlap = value != 0; break;
+    case RK_OPT_HALO_LOOPBACK:
+        if (value && st->ctx->world != 1) return fail(RK_ERR_ARG, "loopback needs world == 1");
+        st->loopback = value != 0;
+        break;
+    case RK_OPT_MAX_TRIES:
+        if (value < 1) return fail(RK_ERR_ARG, "max tries must be >= 1");
+        st->max_tries = (int)value;
+        break;
+    case RK_OPT_TIMING: st->timing = value != 0; break;
+    case RK_OPT_USE_GRAPH: st->use_graph = value != 0; break;
+    default: return fail(RK_ERR_ARG, "unknown option %d", key);
+    }
+    return RK_OK;
+}
+
+rk_status rk_do_step(rk_state st, rk_scheme scheme, double t, double dt) {
+    (void)t;
+    TRY(check_state(st));
+    if (!valid_scheme(scheme)) return fail(RK_ERR_ARG, "bad scheme %d", (int)scheme);
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(RK_ERR_ARG, "dt must be finite and > 0");
+    TRY(check_rhs(st));
+    DeviceGuard g(st->ctx->device);
+    return fixed_step(st, scheme, dt);
+}
+
+rk_status rk_try_step(rk_state st, rk_scheme scheme, double t, double dt, double atol, double rtol,
+                      int* accepted, double* err_ratio, double* dt_next) {
+    TRY(check_state(st));
+    if (!valid_scheme(scheme)) return fail(RK_ERR_ARG, "bad scheme %d", (int)scheme);
+    if (!accepted || !err_ratio || !dt_next) return fail(RK_ERR_ARG, "null output");
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(RK_ERR_ARG, "dt must be finite and > 0");
+    if (!(atol > 0.0) || !(rtol >= 0.0)) return fail(RK_ERR_ARG, "need atol > 0, rtol >= 0");
+    if (coeffs_of(scheme).err_order == 0)
+        return fail(RK_ERR_UNSUPPORTED, "scheme %d has no embedded error estimate", (int)scheme);
+    TRY(check_rhs(st));
+    DeviceGuard g(st->ctx->device);
+    return one_try(st, scheme, t, dt, atol, rtol, accepted, err_ratio, dt_next);
+}
+
+rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1, double dt,
+                             int64_t* steps) {
+    TRY(check_state(st));
+    if (!valid_scheme(scheme)) return fail(RK_ERR_ARG, "bad scheme %d", (int)scheme);
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(RK_ERR_ARG, "dt must be finite and > 0");
+    if (!(t1 > t0)) return fail(RK_ERR_ARG, "need t1 > t0");
+    TRY(check_rhs(st));
+    DeviceGuard g(st->ctx->device);
+    // Odeint integrate_const: while (t_n + dt) - t1 <= eps, t_n = t0 + n*dt
+    int64_t n = 0;
+    double t = t0;
+    while ((t + dt) - t1 <= DBL_EPSILON) {
+        ++n;
+        t = t0 + (double)n * dt;
+    }
+    if (!st->grid) {
+        // pointwise RHS: all n steps of every element in registers, chunked launches
+        int64_t left = n;
+        while (left > 0) {
+            const int chunk = (int)std::min<int64_t>(left, 1 << 20);
+            TRY(run_pointwise(st, scheme, dt, chunk, false, 0.0, 0.0));
+            std::swap(st->u, st->u_new);
+            left -= chunk;
+        }
+        st->k1_valid = false;
+        st->stats.steps += n;
+    } else {
+        for (int64_t i = 0; i < n; ++i) TRY(fixed_step(st, scheme, dt));
+    }
+    CK_CTX(st->ctx, cudaStreamSynchronize(st->ctx->stream));
+    if (steps) *steps = n;
+    return RK_OK;
+}
+
+rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double t1, double dt0,
+                                double atol, double rtol, int64_t* accepted, int64_t* rejected) {
+    TRY(check_state(st));
+    if (!valid_scheme(scheme)) return fail(RK_ERR_ARG, "bad scheme %d", (int)scheme);
+    if (!(dt0 > 0.0) || !std::isfinite(dt0)) return fail(RK_ERR_ARG, "dt0 must be finite and > 0");
+    if (!(t1 > t0)) return fail(RK_ERR_ARG, "need t1 > t0");
+    if (!(atol > 0.0) || !(rtol >= 0.0)) return fail(RK_ERR_ARG, "need atol > 0, rtol >= 0");
+    if (coeffs_of(scheme).err_order == 0)
+        return fail(RK_ERR_UNSUPPORTED, "scheme %d has no embedded error estimate", (int)scheme);
+    TRY(check_rhs(st));
+    DeviceGuard g(st->ctx->device);
+    int64_t acc = 0, rej = 0;
+    double t = t0, dt = dt0;
+    rk_status rc = RK_OK;
+    while (t1 - t > DBL_EPSILON) {
+        if ((t + dt) - t1 > DBL_EPSILON) dt = t1 - t;
+        int tries = 0;
+        for (;;) {
+            if (dt < 16.0 * DBL_EPSILON * std::max(std::fabs(t), 1.0)) {
+                rc = fail(RK_ERR_DT_UNDERFLOW, "dt underflow at t=%.17g", t);
+                goto done;
+            }
+            int ok = 0;
+            double E = 0.0, dtn = dt;
+            rc = one_try(st, scheme, t, dt, atol, rtol, &ok, &E, &dtn);
+            if (rc != RK_OK) goto done;
+            if (ok) {
+                t = t + dt;
+                dt = dtn;
+                ++acc;
+                break;
+            }
+            dt = dtn;
+            ++rej;
+            if (++tries >= st->max_tries) {
+                rc = fail(RK_ERR_STALL, "more than %d tries at t=%.17g", st->max_tries, t);
+                goto done;
+            }
+        }
+    }
+done:
+    if (accepted) *accepted = acc;
+    if (rejected) *rejected = rej;
+    return rc;
+}
+
+rk_status rk_lincomb(rk_state out, int k, const double* coef, const rk_state* in) {
+    TRY(check_state(out));
+    if (k < 1 || k > 14) return fail(RK_ERR_CONTRACT, "lincomb arity %d not in [1,14]", k);
+    if (!coef || !in) return fail(RK_ERR_ARG, "null argument");
+    LincombArgs a{};
+    a.out = out->u;
+    a.k = k;
+    a.count = out->count;
+    for (int j = 0; j < k; ++j) {
+        rk_state s = in[j];
+        TRY(check_state(s));
+        if (s->ctx != out->ctx || s->count != out->count || s->grid != out->grid ||
+            s->ncomp != out->ncomp || s->nx != out->nx || s->ny != out->ny || s->nz != out->nz ||
+            s->n != out->n)
+            return fail(RK_ERR_CONTRACT, "lincomb input %d does not conform to the output", j);
+        a.in[j] = s->u;
+        a.coef[j] = coef[j];
+    }
+    DeviceGuard g(out->ctx->device);
+    CK_CTX(out->ctx, launch_lincomb(a, out->ctx->stream, out->ctx->num_sms));
+    out->stats.kernel_launches += 1;
+    out->k1_valid = false;
+    CK_CTX(out->ctx, cudaStreamSynchronize(out->ctx->stream));
+    return RK_OK;
+}
+
+rk_status rk_norm_inf(rk_state st, double* out) {
+    TRY(check_state(st));
+    if (!out) return fail(RK_ERR_ARG, "null output");
+    rk_ctx ctx = st->ctx;
+    DeviceGuard g(ctx->device);
+    CK_CTX(ctx, cudaMemsetAsync(ctx->d_scratch, 0, 8, ctx->stream));
+    CK_CTX(ctx, launch_norm_inf(st->u, st->count, ctx->d_scratch, ctx->stream, ctx->num_sms));
+    st->stats.kernel_launches += 1;
+    if (ctx->world > 1)
+        NK_CTX(ctx, ncclAllReduce(ctx->d_scratch, ctx->d_scratch, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
+    CK_CTX(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(out, ctx->h_scratch, 8);
+    return RK_OK;
+}
+
+rk_status rk_get_stats(rk_state st, rk_stats* out) {
+    TRY(check_state(st));
+    if (!out) return fail(RK_ERR_ARG, "null output");
+    DeviceGuard g(st->ctx->device);
+    TRY(resolve_timing(st));
+    *out = st->stats;
+    return RK_OK;
+}
+
+rk_status rk_reset_stats(rk_state st) {
+    TRY(check_state(st));
+    DeviceGuard g(st->ctx->device);
+    TRY(resolve_timing(st));
+    st->stats = rk_stats{};
+    return RK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// rk_tableau.h — Butcher tableaux of the library (Table 1).
+//
+// The paper delegates the coefficients to Odeint; these are the standard
+// published tables: explicit Euler, classic Runge–Kutta 4, Cash & Karp (1990) 5(4),
+// Dormand & Prince (1980) 5(4) with FSAL.  Typed here independently of oracle/ (the two
+// share no code); tests/test_abi.py cross-checks the two tables bit for bit.
+#pragma once
+#include <cstdint>
+
+namespace rkb {
+
+struct Rat {
+    long long n, d;
+};
+
+struct Tableau {
+    int s;          // stages
+    int order;      // order of the propagated (b) solution
+    int err_order;  // order of the embedded (bhat) solution, 0 if none
+    Rat c[7];
+    Rat a[7][7];    // strictly lower triangular
+    Rat b[7];
+    Rat bh[7];
+};
+
+__host__ __device__ constexpr Tableau tableau_of(int scheme) {
+    switch (scheme) {
+    case 0:  // explicit Euler
+        return Tableau{1, 1, 0, {{0, 1}}, {{{0, 1}}}, {{1, 1}}, {{0, 1}}};
+    case 1:  // classic RK4
+        return Tableau{4, 4, 0,
+                       {{0, 1}, {1, 2}, {1, 2}, {1, 1}},
+                       {{{0, 1}}, {{1, 2}}, {{0, 1}, {1, 2}}, {{0, 1}, {0, 1}, {1, 1}}},
+                       {{1, 6}, {1, 3}, {1, 3}, {1, 6}},
+                       {{0, 1}}};
+    case 2:  // Cash–Karp 5(4)
+        return Tableau{6, 5, 4,
+                       {{0, 1}, {1, 5}, {3, 10}, {3, 5}, {1, 1}, {7, 8}},
+                       {{{0, 1}},
+                        {{1, 5}},
+                        {{3, 40}, {9, 40}},
+                        {{3, 10}, {-9, 10}, {6, 5}},
+                        {{-11, 54}, {5, 2}, {-70, 27}, {35, 27}},
+                        {{1631, 55296}, {175, 512}, {575, 13824}, {44275, 110592}, {253, 4096}}},
+                       {{37, 378}, {0, 1}, {250, 621}, {125, 594}, {0, 1}, {512, 1771}},
+                       {{2825, 27648}, {0, 1}, {18575, 48384}, {13525, 55296}, {277, 14336}, {1, 4}}};
+    case 3:  // Dormand–Prince 5(4), FSAL
+        return Tableau{7, 5, 4,
+                       {{0, 1}, {1, 5}, {3, 10}, {4, 5}, {8, 9}, {1, 1}, {1, 1}},
+                       {{{0, 1}},
+                        {{1, 5}},
+                        {{3, 40}, {9, 40}},
+                        {{44, 45}, {-56, 15}, {32, 9}},
+                        {{19372, 6561}, {-25360, 2187}, {64448, 6561}, {-212, 729}},
+                        {{9017, 3168}, {-355, 33}, {46732, 5247}, {49, 176}, {-5103, 18656}},
+                        {{35, 384}, {0, 1}, {500, 1113}, {125, 192}, {-2187, 6784}, {11, 84}}},
+                       {{35, 384}, {0, 1}, {500, 1113}, {125, 192}, {-2187, 6784}, {11, 84}, {0, 1}},
+                       {{5179, 57600}, {0, 1}, {7571, 16695}, {393, 640}, {-92097, 339200}, {187, 2100}, {1, 40}}};
+    default:
+        return Tableau{0, 0, 0, {}, {}, {}, {}};
+    }
+}
+
+__host__ __device__ constexpr bool rat_nz(Rat r) { return r.n != 0 && r.d != 0; }
+
+// Exact e_j = b_j - bhat_j as a rational (rounded to double once by the caller, R-11).
+__host__ __device__ constexpr long long gcd_ll(long long a, long long b) {
+    a = a < 0 ? -a : a;
+    b = b < 0 ? -b : b;
+    while (b) {
+        long long t = a % b;
+        a = b;
+        b = t;
+    }
+    return a ? a : 1;
+}
+__host__ __device__ constexpr Rat err_weight(const Tableau& T, int j) {
+    if (T.err_order == 0) return Rat{0, 1};
+    Rat x = T.b[j], y = T.bh[j];
+    if (x.d == 0) x = Rat{0, 1};
+    if (y.d == 0) y = Rat{0, 1};
+    long long n = x.n * y.d - y.n * x.d, d = x.d * y.d;
+    long long g = gcd_ll(n, d);
+    return Rat{n / g, d / g};
+}
+
+inline double rat_double(Rat r) { return r.d == 0 ? 0.0 : (double)r.n / (double)r.d; }
+
+}  // namespace rkb

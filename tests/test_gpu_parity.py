@@ -1,0 +1,314 @@
+"""GPU parity: the CUDA path through the C-ABI against the fp64 oracle on the same seeded
+inputs (rk_inputs).  Design target and gate: bitwise identity (R-17/R-18), which
+implies the BASELINE north_star tolerances (1e-12 per step, 1e-9 final, identical
+accepted/rejected counts).  Sizes span several tiles (32x8 xy tiles, z chunks) with ragged
+tails, plus degenerate grids (1..4 cells per axis)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import rk_inputs
+
+pytestmark = pytest.mark.gpu
+
+SCHEMES = ["euler", "rk4", "cash_karp54", "dopri5"]
+OS = oracle.SCHEMES
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2309_05331_b200 as rk
+    c = rk.Context(0, 1, 0)
+    yield c
+    c.close()
+
+
+def bitwise(a, b):
+    a, b = np.asarray(a).ravel(), np.asarray(b).ravel()
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def gs_state(ctx, nx, ny, nz, u0, **prm):
+    st = ctx.grid(nx, ny, nz, 2)
+    st.set_rhs_gray_scott(**prm)
+    st.set(u0)
+    return st
+
+
+# ---------------------------------------------------------------------------------------
+# pointwise (exp / logistic) vector path
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("n", [1, 2, 3, 1000, 100001])
+@pytest.mark.parametrize("rhs", ["exp", "logistic"])
+def test_pointwise_do_step_bitwise(ctx, scheme, n, rhs):
+    u0 = rk_inputs.logistic_u0(n) if rhs == "logistic" else rk_inputs.exp_decay_u0(n)
+    st = ctx.vector(n)
+    if rhs == "exp":
+        st.set_rhs_exponential(-1.0)
+        p = oracle.exp_problem(n, -1.0)
+    else:
+        st.set_rhs_logistic()
+        p = oracle.logistic_problem(n)
+    st.set(u0)
+    u = u0
+    for k in range(3):
+        st.do_step(scheme, 0.0, 0.1 * (k + 1))
+        u = oracle.step(p, OS[scheme], 0.0, 0.1 * (k + 1), u)
+        assert bitwise(st.get(), u), (scheme, n, k)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+def test_config1_exp_decay_integrate_const(ctx, scheme):
+    """BASELINE configs[0]: du/dt=-u, N=1e5, t in [0,1]; multi-step in-register kernel."""
+    n = 100000
+    u0 = rk_inputs.exp_decay_u0(n)
+    st = ctx.vector(n)
+    st.set_rhs_exponential(-1.0)
+    for dt in (0.1, 2.0 ** -5):
+        st.set(u0)
+        steps = st.integrate_const(scheme, 0.0, 1.0, dt)
+        uo, so = oracle.integrate_const(oracle.exp_problem(n, -1.0), OS[scheme], u0, 0.0, 1.0, dt)
+        assert steps == so == round(1.0 / dt)
+        g = st.get()
+        assert bitwise(g, uo)
+        order = {"euler": 1, "rk4": 4, "cash_karp54": 5, "dopri5": 5}[scheme]
+        err = np.max(np.abs(g - u0 * math.exp(-1.0)))
+        assert err < 2 * dt ** order
+
+
+@pytest.mark.parametrize("scheme,tol,acc_rej", [("dopri5", 1e-8, (51, 2)), ("cash_karp54", 1e-8, None)])
+def test_config2_logistic_adaptive(ctx, scheme, tol, acc_rej):
+    """BASELINE configs[1]: logistic N=1e6 adaptive (atol = rtol = 1e-8): accepted and
+    rejected counts identical to the oracle, final state bitwise."""
+    n = 1000000
+    u0 = rk_inputs.logistic_u0(n)
+    st = ctx.vector(n)
+    st.set_rhs_logistic()
+    st.set(u0)
+    a, r = st.integrate_adaptive(scheme, -5.0, 5.0, 0.1, tol, tol)
+    uo, ao, ro, rc = oracle.integrate_adaptive(oracle.logistic_problem(n), OS[scheme], u0, -5.0,
+                                               5.0, 0.1, tol, tol)
+    assert rc == 0 and (a, r) == (ao, ro)
+    if acc_rej:
+        assert (a, r) == acc_rej
+    assert bitwise(st.get(), uo)
+
+
+def test_try_step_rejection_leaves_state(ctx):
+    n = 4096
+    u0 = rk_inputs.logistic_u0(n)
+    st = ctx.vector(n)
+    st.set_rhs_logistic()
+    st.set(u0)
+    acc, E, dtn = st.try_step("dopri5", -5.0, 8.0, 1e-12, 1e-12)
+    assert not acc and E > 1 and dtn < 8.0
+    assert bitwise(st.get(), u0)
+    accepted, Eo = oracle.controller(E, 8.0)
+    assert (acc, dtn) == (accepted, Eo)
+
+
+# ---------------------------------------------------------------------------------------
+# Gray–Scott grid path
+# ---------------------------------------------------------------------------------------
+GRIDS = [(4, 4, 4), (8, 8, 8), (16, 16, 16), (33, 17, 9), (64, 40, 12), (1, 1, 3), (2, 3, 1),
+         (5, 1, 2), (70, 9, 20)]
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("dims", GRIDS, ids=lambda d: "x".join(map(str, d)))
+def test_gs_steps_bitwise(ctx, scheme, dims):
+    nx, ny, nz = dims
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=42)
+    # perturb so every cell is non-trivial (the IC is mostly the (1,0) steady state)
+    u0 = u0 + 0.01 * rk_inputs.random_state(u0.size, 5).reshape(u0.shape)
+    st = gs_state(ctx, nx, ny, nz, u0)
+    p = oracle.gray_scott_problem(nx, ny, nz)
+    u = u0
+    for k in range(3):
+        st.do_step(scheme, float(k), 1.0)
+        u = oracle.step(p, OS[scheme], float(k), 1.0, u)
+        assert bitwise(st.get(), u), (scheme, dims, k)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("dims", [(16, 16, 16), (33, 17, 9), (8, 8, 1), (8, 8, 2), (8, 8, 3)],
+                         ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("overlap", [1, 0])
+def test_gs_halo_loopback_bitwise(ctx, scheme, dims, overlap):
+    """The multi-GPU code path (pack -> exchange -> interior + boundary launches, ghost
+    planes) on one GPU with a self-exchange: bitwise equal to the oracle."""
+    import paper_2309_05331_b200 as rk
+    nx, ny, nz = dims
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=1) + 0.01 * rk_inputs.random_state(
+        2 * nx * ny * nz, 9).reshape(nz, 2, ny, nx)
+    st = gs_state(ctx, nx, ny, nz, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+    st.set_option(rk.OPT_HALO_OVERLAP, overlap)
+    p = oracle.gray_scott_problem(nx, ny, nz)
+    u = u0
+    for k in range(2):
+        st.do_step(scheme, 0.0, 1.0)
+        u = oracle.step(p, OS[scheme], 0.0, 1.0, u)
+        assert bitwise(st.get(), u)
+    assert st.stats()["halo_exchanges"] > 0
+
+
+def test_config3_gray_scott_64_rk4(ctx):
+    """BASELINE configs[2]: 64^3 periodic, RK4, dt=1, t in [0,20]: bitwise after every step."""
+    n = 64
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    st = gs_state(ctx, n, n, n, u0)
+    p = oracle.gray_scott_problem(n, n, n)
+    u = u0
+    for k in range(20):
+        st.do_step("rk4", float(k), 1.0)
+        u = oracle.step(p, oracle.RK4, float(k), 1.0, u)
+        assert bitwise(st.get(), u), k
+    st.set(u0)
+    assert st.integrate_const("rk4", 0.0, 20.0, 1.0) == 20
+    assert bitwise(st.get(), u)
+
+
+@pytest.mark.parametrize("scheme", ["dopri5", "cash_karp54"])
+@pytest.mark.parametrize("tol", [1e-6, 1e-8])
+def test_gs_adaptive_counts_and_state(ctx, scheme, tol):
+    n = 32
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    st = gs_state(ctx, n, n, n, u0)
+    a, r = st.integrate_adaptive(scheme, 0.0, 20.0, 1.0, tol, tol)
+    uo, ao, ro, rc = oracle.integrate_adaptive(oracle.gray_scott_problem(n, n, n), OS[scheme],
+                                               u0, 0.0, 20.0, 1.0, tol, tol)
+    assert rc == 0 and (a, r) == (ao, ro) and a > 0
+    assert bitwise(st.get(), uo)
+
+
+def test_gs_try_step_matches_oracle_ratio(ctx):
+    n = 24
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=3) + 0.05 * rk_inputs.random_state(
+        2 * n ** 3, 4).reshape(n, 2, n, n)
+    p = oracle.gray_scott_problem(n, n, n)
+    for scheme in ("dopri5", "cash_karp54"):
+        st = gs_state(ctx, n, n, n, u0)
+        for dt in (4.0, 1.0, 0.25):
+            st.set(u0)
+            acc, E, dtn = st.try_step(scheme, 0.0, dt, 1e-7, 1e-7)
+            un, err = oracle.step(p, OS[scheme], 0.0, dt, u0, with_error=True)
+            Eo = oracle.error_ratio_max(err, u0, oracle.rhs(p, u0), dt, 1e-7, 1e-7)
+            assert E == Eo
+            assert bitwise(st.get(), un if acc else u0)
+
+
+# ---------------------------------------------------------------------------------------
+# full BASELINE size (512^3), launch configuration of bench.py, sampled outputs
+# ---------------------------------------------------------------------------------------
+def _sample_block(u, z, y, x, r=8):
+    """(2r+1)^3 periodic neighbourhood of cell (z,y,x) from a [z][c][y][x] array."""
+    nz, _, ny, nx = u.shape
+    zi = np.arange(z - r, z + r + 1) % nz
+    yi = np.arange(y - r, y + r + 1) % ny
+    xi = np.arange(x - r, x + r + 1) % nx
+    return np.ascontiguousarray(u[zi][:, :, yi][:, :, :, xi])
+
+
+@pytest.mark.parametrize("scheme,adaptive", [("rk4", False), ("dopri5", True), ("dopri5", False),
+                                             ("cash_karp54", True), ("euler", False)])
+def test_512_sampled_parity(ctx, scheme, adaptive):
+    """One step (or one adaptive try) at 512^3 exactly as bench.py runs it; every sampled
+    cell's new value is recomputed by the oracle on its 17^3 periodic neighbourhood (the
+    step's dependency radius is <= 7 stages), and must match bitwise."""
+    n = 512
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    st = gs_state(ctx, n, n, n, u0)
+    if adaptive:
+        acc, E, _ = st.try_step(scheme, 0.0, 1.0, 1e-6, 1e-6)
+        assert acc and 0.0 <= E <= 1.0
+    else:
+        st.do_step(scheme, 0.0, 1.0)
+    g = st.get()
+    lo, hi = rk_inputs.cube_range(n)
+    rng = np.random.default_rng(0)
+    pts = [(lo, lo, lo), (hi - 1, hi, lo - 1), (0, 0, 0), (511, 511, 511), (lo + 3, 255, 256),
+           (lo, lo + 5, 31), (hi, lo, 32)] + [tuple(rng.integers(lo - 4, hi + 4, 3)) for _ in range(12)]
+    r = 8
+    p = oracle.gray_scott_problem(2 * r + 1, 2 * r + 1, 2 * r + 1)
+    for (z, y, x) in pts:
+        blk = _sample_block(u0, z, y, x, r)
+        out = oracle.step(p, OS[scheme], 0.0, 1.0, blk).reshape(blk.shape)
+        assert bitwise(g[z, :, y, x], out[r, :, r, r]), (z, y, x)
+
+
+# ---------------------------------------------------------------------------------------
+# algebra ops and error conventions
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("k", [1, 2, 5, 14])
+def test_lincomb_bitwise(ctx, k):
+    n = 10007
+    ins = [rk_inputs.random_state(n, 100 + j) for j in range(k)]
+    coef = list(rk_inputs.random_state(k, 7))
+    sts = []
+    for x in ins:
+        s = ctx.vector(n)
+        s.set(x)
+        sts.append(s)
+    out = ctx.vector(n)
+    out.lincomb(coef, sts)
+    assert bitwise(out.get(), oracle.lincomb(coef, ins))
+    sts[0].lincomb(coef, sts)  # aliasing: out is an input
+    assert bitwise(sts[0].get(), oracle.lincomb(coef, ins))
+
+
+def test_norm_inf(ctx):
+    x = rk_inputs.random_state(123457, 3)
+    st = ctx.vector(x.size)
+    st.set(x)
+    assert st.norm_inf() == oracle.norm_inf(x)
+    x[777] = -5.0
+    st.set(x)
+    assert st.norm_inf() == 5.0
+    x[5] = np.nan
+    st.set(x)
+    assert math.isnan(st.norm_inf())
+
+
+def test_error_conventions(ctx):
+    import paper_2309_05331_b200 as rk
+    v = ctx.vector(10)
+    with pytest.raises(rk.RKError) as e:
+        v.do_step("rk4", 0.0, 0.1)
+    assert e.value.status == "RK_ERR_STATE"          # RHS unset
+    v.set_rhs_logistic()
+    with pytest.raises(rk.RKError) as e:
+        v.integrate_adaptive("rk4", 0.0, 1.0, 0.1, 1e-6, 1e-6)
+    assert e.value.status == "RK_ERR_UNSUPPORTED"
+    for bad in (0.0, -1.0, math.inf, math.nan):
+        with pytest.raises(rk.RKError) as e:
+            v.do_step("rk4", 0.0, bad)
+        assert e.value.status == "RK_ERR_ARG"
+    with pytest.raises(rk.RKError) as e:
+        v.set_rhs_gray_scott()
+    assert e.value.status == "RK_ERR_STATE"
+    with pytest.raises(rk.RKError) as e:
+        v.lincomb([1.0] * 15, [v] * 15)
+    assert e.value.status == "RK_ERR_CONTRACT"
+    w = ctx.vector(11)
+    with pytest.raises(rk.RKError) as e:
+        v.lincomb([1.0], [w])
+    assert e.value.status == "RK_ERR_CONTRACT"
+    x = np.full(10, 0.5)
+    x[3] = np.nan
+    v.set(x)
+    with pytest.raises(rk.RKError) as e:
+        v.integrate_adaptive("dopri5", 0.0, 1.0, 0.1, 1e-6, 1e-6)
+    assert e.value.status == "RK_ERR_DIVERGED"
+
+
+def test_stats_count_launches(ctx):
+    n = 16
+    st = gs_state(ctx, n, n, n, rk_inputs.gray_scott_ic(n, n, n))
+    st.reset_stats()
+    st.do_step("rk4", 0.0, 1.0)
+    s = st.stats()
+    assert s["rhs_evals"] == 4 and s["stage_launches"] == 4 and s["kernel_launches"] >= 4
