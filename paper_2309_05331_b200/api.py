@@ -8,6 +8,7 @@ integrate_const, integrate_adaptive, P:L198-201).
 from __future__ import annotations
 
 import ctypes
+import weakref
 
 import numpy as np
 
@@ -23,11 +24,13 @@ def _scheme(s) -> int:
 
 
 def _stream_handle(stream) -> int | None:
+    """None -> the library creates its own stream; a torch stream (or raw handle) is used
+    as is; torch's default stream (handle 0) maps to cudaStreamLegacy (0x1), since a NULL
+    handle means "create one" in rk_ctx_create."""
     if stream is None:
         return None
-    if isinstance(stream, int):
-        return stream
-    return int(stream.cuda_stream)  # torch.cuda.Stream
+    h = stream if isinstance(stream, int) else int(stream.cuda_stream)
+    return h if h != 0 else 1
 
 
 class Context:
@@ -48,6 +51,7 @@ class Context:
              ctypes.byref(h))
         self._h = h
         self._L = L
+        self._states = weakref.WeakSet()
         self.rank, self.world, self.device = rank, world, device
 
     @staticmethod
@@ -75,15 +79,21 @@ class Context:
     def grid(self, nx: int, ny: int, nz: int, ncomp: int = 2) -> "State":
         h = ctypes.c_void_p()
         call("rk_state_create_grid", self._h, nx, ny, nz, ncomp, ctypes.byref(h))
-        return State(self, h, grid=True, dims=(nx, ny, nz), ncomp=ncomp)
+        st = State(self, h, grid=True, dims=(nx, ny, nz), ncomp=ncomp)
+        self._states.add(st)
+        return st
 
     def vector(self, n: int, ncomp: int = 1) -> "State":
         h = ctypes.c_void_p()
         call("rk_state_create_vector", self._h, n, ncomp, ctypes.byref(h))
-        return State(self, h, grid=False, dims=(n,), ncomp=ncomp)
+        st = State(self, h, grid=False, dims=(n,), ncomp=ncomp)
+        self._states.add(st)
+        return st
 
     def close(self):
         if getattr(self, "_h", None):
+            for st in list(self._states):  # states first: they live on this ctx
+                st.close()
             self._L.rk_ctx_destroy(self._h)
             self._h = None
 

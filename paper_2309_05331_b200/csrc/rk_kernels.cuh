@@ -1,8 +1,10 @@
 // rk_kernels.cuh — device kernels of librkb200 and their host launchers.
 //
-// K1 pointwise fused step (exp / logistic), K2 lincomb + plane pack, K3 fused Gray–Scott
-// stage kernel, K4 max-norm reductions.  See DESIGN.md §Kernels for the roofline of each.
+// K1 pointwise fused step (exp / logistic), K2 lincomb + halo-plane pack, K3 fused
+// Gray–Scott stage kernel (TMA-fed), K4 max-norm reductions.  DESIGN.md §Kernels gives the
+// roofline and the algorithmic bytes of each.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -42,32 +44,51 @@ struct PwArgs {
 cudaError_t launch_pointwise(int scheme, const PwArgs& a, cudaStream_t st, int num_sms);
 
 // ---------------------------------------------------------------------------------------
-// K3: fused Gray–Scott stage kernel.  Grid state layout [z][c][y][x], 2 components.
+// Grid arrays in HBM use a PADDED periodic layout: [z][c][ny+2][P] fp64 with P >= nx+2 even
+// (16-byte rows for TMA); logical cell (x, y) sits at padded (x+1, y+1), and the producer
+// of every array also writes the periodic copies x=-1 -> nx-1, x=nx -> 0 (and y alike) into
+// the 1-cell ring, so a TMA box of (TX+2) x (TY+2) cells around any tile is exactly the
+// periodic neighbourhood, with no wrap logic in the consumer.
+struct GridGeom {
+    int nx, ny, nzl;
+    int P;          // padded row pitch (elements)
+    int64_t cs;     // component stride = (ny+2)*P
+    int64_t ps;     // plane stride = 2*cs
+};
+void gs_tile_dims(int* tx, int* ty);
+// 4D tensor map (x, y, c, z) over a padded array of `nplanes` planes; box = one tile + ring.
+cudaError_t encode_grid_map(CUtensorMap* m, const double* base, const GridGeom& g, int nplanes);
+
+// K3: fused Gray–Scott stage kernel.
 struct GsStageArgs {
-    const double* u;
-    const double* k[kMaxSlots];  // slot arrays, increasing stage index j
-    double g[kMaxSlots];         // Y coefficient per slot (0: slot not in Y, no halo load)
+    CUtensorMap tm_u;
+    CUtensorMap tm_k[kMaxSlots];
+    CUtensorMap tm_glo, tm_ghi;  // ghost planes z=-1, z=nzl (multi-GPU); else periodic wrap
+    GridGeom geo;
+    const double* u;             // raw pointers (pack kernel)
+    const double* k[kMaxSlots];
+    double g[kMaxSlots];         // Y coefficient per slot (0: slot not in Y)
     double beta[kMaxSlots];      // final-combination weight per slot (0: skip)
     double delta[kMaxSlots];     // error weight per slot (0: skip)
     double beta_new, delta_new;  // weights of the k_i computed by this stage
     double* out_k;
     double* out_u;
-    const double* ghost_lo;      // Y_i plane z=-1   [2][ny][nx]; null => periodic wrap in slab
-    const double* ghost_hi;      // Y_i plane z=nzl  [2][ny][nx]
     unsigned long long* errmax;
     double dt, atol, rtol;
     double d1, d2, F, FK, inv_h2;
-    int nx, ny, nzl;
-    int z_lo, z_hi;              // output planes [z_lo, z_hi) (boundary mode: see zmode)
+    int has_glo, has_ghi;
+    int z_lo, z_hi;              // output planes [z_lo, z_hi) (zmode 0)
     int zchunk;                  // output planes per CTA
     int zmode;                   // 0: contiguous chunks; 1: chunk 0 = plane 0, chunk 1 = nzl-1
     int nslots;
 };
-// Launch over the planes described by a.z_lo/z_hi/zmode; epi = Epilogue.
 cudaError_t launch_gs_stage(int epi, const GsStageArgs& a, cudaStream_t st, int* nlaunch);
 
-// Pack Y_i on own planes 0 and nzl-1 into send[0 .. 2*plane) = [lo | hi].
+// Y_i on own planes 0 and nzl-1 (whole padded planes) -> send = [lo plane | hi plane].
 cudaError_t launch_gs_pack(const GsStageArgs& a, double* send, cudaStream_t st);
+// Refresh the periodic ring of every (plane, component) slice of a padded array (after a
+// user copy into the interior); nslices = planes * components.
+cudaError_t launch_fill_ring(double* a, const GridGeom& g, int nslices, cudaStream_t st);
 
 // ---------------------------------------------------------------------------------------
 // K2 / K4: algebra.

@@ -49,6 +49,7 @@ struct rk_ctx_s {
     rk_status poisoned = RK_OK;
     unsigned long long* d_scratch = nullptr;  // 8 B reduction word (norm_inf)
     unsigned long long* h_scratch = nullptr;  // pinned
+    std::vector<rk_state_s*> states;          // live states (destroyed with the ctx)
 };
 
 #define CK_CTX(ctx, call)                                                                     \
@@ -105,10 +106,13 @@ struct rk_state_s {
     int64_t nx = 1, ny = 1, nz = 1;  // grid (global dims)
     int64_t n = 0;                   // vector: global elements
     int64_t begin = 0, local = 0;    // owned planes (grid) or elements (vector)
-    int64_t count = 0;               // fp64 values in the local block
+    int64_t count = 0;               // fp64 values in the local block (user layout)
+    int64_t alloc = 0;               // fp64 values per device array (padded layout for grids)
+    GridGeom geo{};                  // padded periodic layout (grid states, rk_kernels.cuh)
     double* u = nullptr;
     double* u_new = nullptr;
     double* k[7] = {nullptr};
+    CUtensorMap tm_u{}, tm_unew{}, tm_k[7]{}, tm_glo{}, tm_ghi{};
     int nk = 0;
     bool k1_valid = false;           // k[0] == F(u) for the current u
     // halo (grid, world > 1 or loopback)
@@ -146,15 +150,34 @@ static rk_status dev_alloc(rk_ctx ctx, double** p, int64_t count) {
     return RK_OK;
 }
 
+// zero-filled array (pads and ring corners stay 0) with its TMA tensor map (grids)
+static rk_status alloc_array(rk_state st, double** p, CUtensorMap* tm) {
+    TRY(dev_alloc(st->ctx, p, st->alloc));
+    CK_CTX(st->ctx, cudaMemsetAsync(*p, 0, sizeof(double) * (size_t)st->alloc, st->ctx->stream));
+    if (st->grid && st->ncomp == 2 && tm)
+        CK_CTX(st->ctx, encode_grid_map(tm, *p, st->geo, (int)st->local));
+    return RK_OK;
+}
+
 static rk_status ensure_k(rk_state st, int nk) {
     for (int j = st->nk; j < nk; ++j) {
-        TRY(dev_alloc(st->ctx, &st->k[j], st->count));
+        TRY(alloc_array(st, &st->k[j], &st->tm_k[j]));
         st->nk = j + 1;
     }
     return RK_OK;
 }
 
-static int64_t plane_values(rk_state st) { return st->nx * st->ny * st->ncomp; }
+static void swap_u(rk_state st) {
+    std::swap(st->u, st->u_new);
+    std::swap(st->tm_u, st->tm_unew);
+}
+
+static void swap_k(rk_state st, int i, int j) {
+    std::swap(st->k[i], st->k[j]);
+    std::swap(st->tm_k[i], st->tm_k[j]);
+}
+
+static int64_t plane_values(rk_state st) { return st->geo.ps; }  // one padded plane, 2 comps
 
 static cudaEvent_t pool_event(rk_state st) {
     if (!st->event_pool.empty()) {
@@ -303,6 +326,9 @@ static rk_status ensure_halo(rk_state st) {
     if (!halo_path(st) || st->sendbuf) return RK_OK;
     TRY(dev_alloc(st->ctx, &st->sendbuf, 2 * plane_values(st)));
     TRY(dev_alloc(st->ctx, &st->ghostbuf, 2 * plane_values(st)));
+    CK_CTX(st->ctx, cudaMemsetAsync(st->ghostbuf, 0, sizeof(double) * 2 * plane_values(st), st->ctx->stream));
+    CK_CTX(st->ctx, encode_grid_map(&st->tm_ghi, st->ghostbuf, st->geo, 1));
+    CK_CTX(st->ctx, encode_grid_map(&st->tm_glo, st->ghostbuf + plane_values(st), st->geo, 1));
     CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_pack, cudaEventDisableTiming));
     CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_halo, cudaEventDisableTiming));
     return RK_OK;
@@ -310,10 +336,13 @@ static rk_status ensure_halo(rk_state st) {
 
 static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
     GsStageArgs a{};
+    a.geo = st->geo;
     a.u = st->u;
+    a.tm_u = st->tm_u;
     a.nslots = p.nslots;
     for (int s = 0; s < p.nslots; ++s) {
         a.k[s] = st->k[p.slot_j[s]];
+        a.tm_k[s] = st->tm_k[p.slot_j[s]];
         a.g[s] = p.g[s];
         a.beta[s] = p.beta[s];
         a.delta[s] = p.delta[s];
@@ -331,9 +360,6 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     a.F = st->F;
     a.FK = st->F + st->K;
     a.inv_h2 = 1.0 / (st->h * st->h);
-    a.nx = (int)st->nx;
-    a.ny = (int)st->ny;
-    a.nzl = (int)st->local;
     a.z_lo = 0;
     a.z_hi = (int)st->local;
     a.zmode = 0;
@@ -362,7 +388,7 @@ static rk_status launch_stage_timed(rk_state st, int epi, GsStageArgs& a) {
     st->stats.kernel_launches += nl;
     st->stats.stage_launches += nl;
     if (nl) {
-        const int64_t planes = a.zmode == 1 ? (a.nzl > 1 ? 2 : 1) : (int64_t)(a.z_hi - a.z_lo);
+        const int64_t planes = a.zmode == 1 ? (a.geo.nzl > 1 ? 2 : 1) : (int64_t)(a.z_hi - a.z_lo);
         const int64_t arrays = 1 + a.nslots + (a.out_k ? 1 : 0) + (a.out_u ? 1 : 0);
         st->stats.stage_bytes += planes * st->nx * st->ny * 2 * (int64_t)sizeof(double) * arrays;
     }
@@ -433,8 +459,10 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
     CK_CTX(ctx, launch_gs_pack(a, st->sendbuf, ctx->stream));
     st->stats.kernel_launches += 1;
     TRY(halo_exchange(st));
-    a.ghost_hi = st->ghostbuf;
-    a.ghost_lo = st->ghostbuf + plane_values(st);
+    a.has_ghi = 1;
+    a.has_glo = 1;
+    a.tm_ghi = st->tm_ghi;
+    a.tm_glo = st->tm_glo;
     if (st->overlap && nzl > 2) {
         GsStageArgs in = a;  // interior planes [1, nzl-1) never touch ghost planes
         in.z_lo = 1;
@@ -541,7 +569,7 @@ static rk_status fixed_step(rk_state st, int scheme, double dt) {
     } else {
         TRY(run_pointwise(st, scheme, dt, 1, false, 0.0, 0.0));
     }
-    std::swap(st->u, st->u_new);
+    swap_u(st);
     st->k1_valid = false;
     st->stats.steps += 1;
     return RK_OK;
@@ -574,11 +602,11 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
     const bool acc = step_adjust(E, C.order, C.err_order, &dtn);
     st->stats.last_dt = dtn;
     if (acc) {
-        std::swap(st->u, st->u_new);
+        swap_u(st);
         if (st->grid && fsal) {
             // k_s (FSAL) was written into a free k buffer: it is F(u_new), the next k1
             const auto plan = build_plan(scheme, true, dt);
-            std::swap(st->k[0], st->k[plan.back().out_k]);
+            swap_k(st, 0, plan.back().out_k);
             st->k1_valid = true;
         } else {
             st->k1_valid = false;
@@ -700,6 +728,7 @@ rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* 
 rk_status rk_ctx_destroy(rk_ctx ctx) {
     if (!ctx) return RK_OK;
     DeviceGuard g(ctx->device);
+    while (!ctx->states.empty()) rk_state_destroy(ctx->states.back());
     cudaStreamSynchronize(ctx->stream);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
     if (ctx->comm) cudaStreamDestroy(ctx->comm);
@@ -712,11 +741,10 @@ rk_status rk_ctx_destroy(rk_ctx ctx) {
 
 static rk_status state_common(rk_ctx ctx, rk_state st) {
     DeviceGuard g(ctx->device);
-    TRY(dev_alloc(ctx, &st->u, st->count));
-    TRY(dev_alloc(ctx, &st->u_new, st->count));
+    TRY(alloc_array(st, &st->u, &st->tm_u));
+    TRY(alloc_array(st, &st->u_new, &st->tm_unew));
     CK_CTX(ctx, cudaMalloc((void**)&st->d_err, sizeof(unsigned long long)));
     CK_CTX(ctx, cudaMallocHost((void**)&st->h_err, sizeof(unsigned long long)));
-    CK_CTX(ctx, cudaMemsetAsync(st->u, 0, sizeof(double) * (size_t)st->count, ctx->stream));
     CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
     return RK_OK;
 }
@@ -741,11 +769,19 @@ rk_status rk_state_create_grid(rk_ctx ctx, int64_t nx, int64_t ny, int64_t nz, i
         return s;
     }
     st->count = st->local * nx * ny * ncomp;
+    st->geo.nx = (int)nx;
+    st->geo.ny = (int)ny;
+    st->geo.nzl = (int)st->local;
+    st->geo.P = (int)((nx + 2 + 1) / 2 * 2);  // even pitch: 16-byte rows for TMA
+    st->geo.cs = (ny + 2) * (int64_t)st->geo.P;
+    st->geo.ps = ncomp * st->geo.cs;
+    st->alloc = st->local * st->geo.ps;
     s = state_common(ctx, st);
     if (s != RK_OK) {
         rk_state_destroy(st);
         return s;
     }
+    ctx->states.push_back(st);
     *out = st;
     return RK_OK;
 }
@@ -765,11 +801,13 @@ rk_status rk_state_create_vector(rk_ctx ctx, int64_t n, int ncomp, rk_state* out
         return s;
     }
     st->count = st->local * ncomp;
+    st->alloc = st->count;
     s = state_common(ctx, st);
     if (s != RK_OK) {
         rk_state_destroy(st);
         return s;
     }
+    ctx->states.push_back(st);
     *out = st;
     return RK_OK;
 }
@@ -793,6 +831,8 @@ rk_status rk_state_destroy(rk_state st) {
         cudaEventDestroy(p.b);
     }
     for (auto e : st->event_pool) cudaEventDestroy(e);
+    auto& v = st->ctx->states;
+    v.erase(std::remove(v.begin(), v.end(), st), v.end());
     delete st;
     return RK_OK;
 }
@@ -810,14 +850,42 @@ rk_status rk_state_local_size(rk_state st, int64_t* n_values) {
     return RK_OK;
 }
 
+// dense user layout [z][c][y][x] <-> padded device layout [z][c][ny+2][P] (one 3D copy)
+static cudaMemcpy3DParms pad_copy(rk_state st, const double* dense, double* padded, bool to_padded,
+                                  cudaMemcpyKind kind) {
+    cudaMemcpy3DParms p{};
+    const size_t nx = (size_t)st->nx, ny = (size_t)st->ny;
+    cudaPitchedPtr d = make_cudaPitchedPtr((void*)dense, nx * sizeof(double), nx, ny);
+    cudaPitchedPtr q = make_cudaPitchedPtr((void*)padded, (size_t)st->geo.P * sizeof(double),
+                                           (size_t)st->geo.P, ny + 2);
+    if (to_padded) {
+        p.srcPtr = d;
+        p.dstPtr = q;
+        p.dstPos = make_cudaPos(sizeof(double), 1, 0);
+    } else {
+        p.srcPtr = q;
+        p.srcPos = make_cudaPos(sizeof(double), 1, 0);
+        p.dstPtr = d;
+    }
+    p.extent = make_cudaExtent(nx * sizeof(double), ny, (size_t)(st->local * st->ncomp));
+    p.kind = kind;
+    return p;
+}
+
 rk_status rk_state_set(rk_state st, const double* src, int src_on_device) {
     TRY(check_state(st));
     if (!src) return fail(RK_ERR_ARG, "null src");
     rk_ctx ctx = st->ctx;
     DeviceGuard g(ctx->device);
-    CK_CTX(ctx, cudaMemcpyAsync(st->u, src, sizeof(double) * (size_t)st->count,
-                                src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                ctx->stream));
+    const cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (st->grid) {
+        cudaMemcpy3DParms p = pad_copy(st, src, st->u, true, kind);
+        CK_CTX(ctx, cudaMemcpy3DAsync(&p, ctx->stream));
+        CK_CTX(ctx, launch_fill_ring(st->u, st->geo, (int)(st->local * st->ncomp), ctx->stream));
+        st->stats.kernel_launches += 1;
+    } else {
+        CK_CTX(ctx, cudaMemcpyAsync(st->u, src, sizeof(double) * (size_t)st->count, kind, ctx->stream));
+    }
     CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
     st->k1_valid = false;
     return RK_OK;
@@ -828,9 +896,13 @@ rk_status rk_state_get(rk_state st, double* dst, int dst_on_device) {
     if (!dst) return fail(RK_ERR_ARG, "null dst");
     rk_ctx ctx = st->ctx;
     DeviceGuard g(ctx->device);
-    CK_CTX(ctx, cudaMemcpyAsync(dst, st->u, sizeof(double) * (size_t)st->count,
-                                dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                                ctx->stream));
+    const cudaMemcpyKind kind = dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (st->grid) {
+        cudaMemcpy3DParms p = pad_copy(st, dst, st->u, false, kind);
+        CK_CTX(ctx, cudaMemcpy3DAsync(&p, ctx->stream));
+    } else {
+        CK_CTX(ctx, cudaMemcpyAsync(dst, st->u, sizeof(double) * (size_t)st->count, kind, ctx->stream));
+    }
     CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
     return RK_OK;
 }
@@ -930,7 +1002,7 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
         while (left > 0) {
             const int chunk = (int)std::min<int64_t>(left, 1 << 20);
             TRY(run_pointwise(st, scheme, dt, chunk, false, 0.0, 0.0));
-            std::swap(st->u, st->u_new);
+            swap_u(st);
             left -= chunk;
         }
         st->k1_valid = false;
@@ -996,7 +1068,7 @@ rk_status rk_lincomb(rk_state out, int k, const double* coef, const rk_state* in
     LincombArgs a{};
     a.out = out->u;
     a.k = k;
-    a.count = out->count;
+    a.count = out->alloc;  // padded grids: ring copies combine linearly, pads stay 0
     for (int j = 0; j < k; ++j) {
         rk_state s = in[j];
         TRY(check_state(s));
@@ -1021,7 +1093,7 @@ rk_status rk_norm_inf(rk_state st, double* out) {
     rk_ctx ctx = st->ctx;
     DeviceGuard g(ctx->device);
     CK_CTX(ctx, cudaMemsetAsync(ctx->d_scratch, 0, 8, ctx->stream));
-    CK_CTX(ctx, launch_norm_inf(st->u, st->count, ctx->d_scratch, ctx->stream, ctx->num_sms));
+    CK_CTX(ctx, launch_norm_inf(st->u, st->alloc, ctx->d_scratch, ctx->stream, ctx->num_sms));
     st->stats.kernel_launches += 1;
     if (ctx->world > 1)
         NK_CTX(ctx, ncclAllReduce(ctx->d_scratch, ctx->d_scratch, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));

@@ -1,25 +1,28 @@
-// rk_stencil.cu — K3: fused Gray–Scott stage kernel, and the halo-plane pack.
+// rk_stencil.cu — K3: fused Gray–Scott stage kernel (TMA-fed), halo-plane pack, ring fill.
 //
 // One launch evaluates one Runge–Kutta stage i of the 3D Gray–Scott system (Listing 2,
 // P:L169-170; R-1..R-3) over a z-slab:
 //   Y_i = u + sum_{j<i} (dt a_ij) k_j      computed on the fly for every loaded cell
 //                                          (Odeint's scale_sum algebra, fused
-//                                          into the stencil's loads: Y_i never hits HBM)
+//                                          into the stencil: Y_i never goes to HBM)
 //   k_i = d*Lap(Y_i) + reaction(Y_i)       7-point periodic stencil + reaction terms
 //   epilogue: store k_i, or u_new = u + sum_j (dt b_j) k_j, and/or the embedded error
 //             ratio with a warp-shuffle / block max (P:L42, P:L135 for_each_norm).
 //
-// Decomposition: a CTA owns a TX x TY tile of the xy plane and sweeps a chunk of z planes.
-// Per plane it stages Y on the tile plus its 1-cell xy halo in shared memory (double
-// buffered, one __syncthreads per plane) and keeps the own column's Y(z-1), Y(z), Y(z+1)
-// in registers (register queue along the sweep axis).  Raw inputs (u, k_j) of plane z+2
-// are loaded into registers while plane z is being computed (one-plane software
-// pipeline), so each HBM byte is read once; halo cells are re-read from L2.
-// Periodic x/y wrap is by index arithmetic; the z neighbours of the slab come from ghost
-// planes (multi-GPU, filled by NCCL) or by wrapping inside the slab (one GPU).
+// Data movement (sm_100a): a CTA owns a 32x8 tile of the xy plane and sweeps a chunk of z
+// planes.  For every plane, one elected thread issues one 4D TMA box load per input array
+// (u and each k_j: 34x10 cells x 2 components, the tile plus its periodic ring thanks to
+// the padded layout) into an R-deep shared-memory ring guarded by mbarriers, R-1 planes
+// ahead of the plane being computed, so HBM sees a deep, register-free stream of loads.
+// Each plane's Y is formed once from the staged raw tiles into a double-buffered Y tile;
+// the own column keeps Y(z-1), Y(z), Y(z+1) in registers (register queue along z).  One
+// __syncthreads per plane.  Periodic x/y wrap is in the padded layout; z neighbours come
+// from ghost planes (multi-GPU, filled by NCCL) or by wrapping inside the slab (one GPU).
 //
-// Every arithmetic expression follows DESIGN.md R-17 bit for bit (no FMA: __dadd_rn /
-// __dmul_rn), so results equal the oracle's for any tile/chunk/GPU decomposition.
+// Arithmetic follows DESIGN.md R-17 bit for bit (no FMA: __dadd_rn / __dmul_rn), so the
+// results equal the oracle's for any tile/chunk/GPU decomposition.
+#include <cudaTypedefs.h>
+
 #include "rk_device.cuh"
 #include "rk_kernels.cuh"
 
@@ -27,64 +30,74 @@ namespace rkb {
 
 namespace {
 
-constexpr int TX = 32;  // tile width  (one warp per row, 8 B per lane: 256 B coalesced)
-constexpr int TY = 8;   // tile height (8 warps)
+constexpr int TX = 32;            // tile width  (one warp per row)
+constexpr int TY = 8;             // tile height (8 warps)
 constexpr int NT = TX * TY;
-static_assert(NT >= 2 * TX + 2 * TY, "halo items need one thread each");
+constexpr int BW = TX + 2, BH = TY + 2;
+constexpr int BOX = BW * BH;                  // cells per component in one TMA box
+constexpr int BOX_BYTES = 2 * BOX * 8;        // one array, both components (5440 B)
+constexpr int ARR_BYTES = (BOX_BYTES + 127) / 128 * 128;  // 128-B aligned slot stride
+constexpr int ARR_DBL = ARR_BYTES / 8;
+constexpr int NHALO = BOX - NT;               // ring positions of the box (84)
+static_assert(NHALO <= NT, "one ring position per thread");
 
+__host__ __device__ constexpr int ring_depth(int ns) { return ns <= 3 ? 4 : 3; }
+__host__ __device__ constexpr int smem_bytes(int ns) {
+    return ring_depth(ns) * (ns + 1) * ARR_BYTES + 2 * ARR_BYTES + ring_depth(ns) * 8;
+}
+
+// ---- PTX wrappers -------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
+__device__ __forceinline__ bool plane_is_ghost(const GsStageArgs& a, int p) {
+    return (p < 0 && a.has_glo) || (p >= a.geo.nzl && a.has_ghi);
+}
+
+// Y = u (+) g_s (x) k_s over slots with g_s != 0, left to right (R-17); a ghost plane holds
+// Y itself.  r points at component c, box position pos, of array 0 of a ring slot.
 template <int NS>
-struct Raw {
-    double u[2];
-    double k[NS > 0 ? NS : 1][2];
-};
-
-// Load the raw inputs of one cell (offset o inside a plane) of plane p in [-1, nzl].
-// ghost: the plane is a received Y plane, stored in r.u directly.
-template <int NS, bool HALO>
-__device__ __forceinline__ void load_cell(const GsStageArgs& a, int p, int64_t o, int64_t cs,
-                                          int64_t ps, Raw<NS>& r) {
-    const double* gh = nullptr;
-    if (p < 0 && a.ghost_lo) gh = a.ghost_lo;
-    if (p >= a.nzl && a.ghost_hi) gh = a.ghost_hi;
-    if (gh) {
-        r.u[0] = __ldg(gh + o);
-        r.u[1] = __ldg(gh + cs + o);
-        return;
-    }
-    const int q = p < 0 ? p + a.nzl : (p >= a.nzl ? p - a.nzl : p);
-    const int64_t base = (int64_t)q * ps + o;
-    r.u[0] = __ldg(a.u + base);
-    r.u[1] = __ldg(a.u + base + cs);
+__device__ __forceinline__ double y_at(const GsStageArgs& a, const double* r, bool ghost) {
+    double v = r[0];
+    if (!ghost) {
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-        if (HALO && a.g[s] == 0.0) continue;  // uniform: slot not part of Y
-        r.k[s][0] = __ldg(a.k[s] + base);
-        r.k[s][1] = __ldg(a.k[s] + base + cs);
+        for (int s = 0; s < NS; ++s)
+            if (a.g[s] != 0.0) v = add(v, mul(a.g[s], r[(s + 1) * ARR_DBL]));
     }
+    return v;
 }
 
-__device__ __forceinline__ bool is_ghost(const GsStageArgs& a, int p) {
-    return (p < 0 && a.ghost_lo) || (p >= a.nzl && a.ghost_hi);
-}
-
-// Y = u (+) g_s (x) k_s over slots with g_s != 0, left to right (R-17).
-template <int NS>
-__device__ __forceinline__ void combine_y(const GsStageArgs& a, bool ghost, const Raw<NS>& r,
-                                          double (&y)[2]) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        double v = r.u[c];
-        if (!ghost) {
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-                if (a.g[s] != 0.0) v = add(v, mul(a.g[s], r.k[s][c]));
-        }
-        y[c] = v;
-    }
-}
-
-// Per-cell partial sums that the epilogue completes with the new k_i (bitwise identical to
-// the full left-to-right sums because j = i is always the last term).
+// Per-cell partial sums the epilogue completes with the new k_i (bitwise identical to the
+// full left-to-right sums because j = i is always the last term).
 struct EState {
     double w[2];  // u (+) sum beta_j k_j
     double e[2];  // sum delta_j k_j (first term not added to 0)
@@ -92,16 +105,19 @@ struct EState {
 };
 
 template <int NS, int EPI>
-__device__ __forceinline__ void make_estate(const GsStageArgs& a, const Raw<NS>& r, EState& es) {
+__device__ __forceinline__ void make_estate(const GsStageArgs& a, const double* slot, int pos,
+                                            EState& es) {
     constexpr bool FIN = (EPI == EPI_FINAL || EPI == EPI_FINAL_ERR);
     constexpr bool ERR = (EPI == EPI_FINAL_ERR || EPI == EPI_FSAL_ERR);
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
+        const double* r = slot + c * BOX + pos;
+        const double u = r[0];
         if constexpr (FIN) {
-            double w = r.u[c];
+            double w = u;
 #pragma unroll
             for (int s = 0; s < NS; ++s)
-                if (a.beta[s] != 0.0) w = add(w, mul(a.beta[s], r.k[s][c]));
+                if (a.beta[s] != 0.0) w = add(w, mul(a.beta[s], r[(s + 1) * ARR_DBL]));
             es.w[c] = w;
         }
         if constexpr (ERR) {
@@ -110,132 +126,160 @@ __device__ __forceinline__ void make_estate(const GsStageArgs& a, const Raw<NS>&
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
                 if (a.delta[s] == 0.0) continue;
-                const double t = mul(a.delta[s], r.k[s][c]);
+                const double t = mul(a.delta[s], r[(s + 1) * ARR_DBL]);
                 e = first ? t : add(e, t);
                 first = false;
             }
             es.e[c] = e;
-            const double k1 = NS > 0 ? r.k[0][c] : 0.0;  // slot 0 holds k1 in error stages
-            es.d[c] = add(a.atol, mul(a.rtol, add(fabs(r.u[c]), mul(a.dt, fabs(k1)))));
+            const double k1 = NS > 0 ? r[ARR_DBL] : 0.0;  // slot 0 holds k1 in error stages
+            es.d[c] = add(a.atol, mul(a.rtol, add(fabs(u), mul(a.dt, fabs(k1)))));
         }
     }
 }
 
+// Store one cell of a padded array and its periodic ring copies (corners are never read).
+__device__ __forceinline__ void store_cell(double* out, const GridGeom& g, int64_t off, int x, int y,
+                                           double v) {
+    out[off + (int64_t)(y + 1) * g.P + (x + 1)] = v;
+    if (x == 0) out[off + (int64_t)(y + 1) * g.P + (g.nx + 1)] = v;
+    if (x == g.nx - 1) out[off + (int64_t)(y + 1) * g.P] = v;
+    if (y == 0) out[off + (int64_t)(g.ny + 1) * g.P + (x + 1)] = v;
+    if (y == g.ny - 1) out[off + (x + 1)] = v;
+}
+
 template <int NS, int EPI>
-__global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const GsStageArgs a) {
-    constexpr int SW = TX + 2, SH = TY + 2;
+__global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const __grid_constant__ GsStageArgs a) {
+    constexpr int R = ring_depth(NS);
+    constexpr int NA = NS + 1;
     constexpr bool FIN = (EPI == EPI_FINAL || EPI == EPI_FINAL_ERR);
     constexpr bool ERR = (EPI == EPI_FINAL_ERR || EPI == EPI_FSAL_ERR);
-    __shared__ double sY[2][2][SH][SW];
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* raw = reinterpret_cast<double*>(smem);                          // [R][NA][2][BH][BW]
+    double* sY = reinterpret_cast<double*>(smem + R * NA * ARR_BYTES);      // [2][2][BH][BW]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R * NA * ARR_BYTES + 2 * ARR_BYTES);
 
+    const GridGeom& G = a.geo;
     const int tid = threadIdx.x;
-    const int ntx = (a.nx + TX - 1) / TX;
+    const int ntx = (G.nx + TX - 1) / TX;
     const int x0 = (int)(blockIdx.x % ntx) * TX, y0 = (int)(blockIdx.x / ntx) * TY;
-    const int w = min(TX, a.nx - x0), hg = min(TY, a.ny - y0);
+    const int w = min(TX, G.nx - x0), hg = min(TY, G.ny - y0);
 
     int zb, ze;
     if (a.zmode == 0) {
         zb = a.z_lo + (int)blockIdx.y * a.zchunk;
         ze = min(zb + a.zchunk, a.z_hi);
     } else {
-        zb = blockIdx.y == 0 ? 0 : a.nzl - 1;
+        zb = blockIdx.y == 0 ? 0 : G.nzl - 1;
         ze = zb + 1;
     }
     if (zb >= ze) return;  // CTA-uniform, before any barrier
+    const int nplanes = ze - zb + 2;  // planes zb-1 .. ze, plane i is global zb-1+i
 
-    const int64_t cs = (int64_t)a.nx * a.ny;  // component stride
-    const int64_t ps = 2 * cs;                // plane stride
-
-    // own cell
     const int lx = tid % TX, ly = tid / TX;
     const bool own = (lx < w) && (ly < hg);
-    const int64_t o_own = (int64_t)(y0 + ly) * a.nx + (x0 + lx);
+    const int pos_own = (ly + 1) * BW + (lx + 1);
+    // ring position handled by this thread (all 84 box positions outside the tile)
+    const bool hal = tid < NHALO;
+    int pos_h = 0;
+    if (tid < BW) pos_h = tid;                                  // row 0
+    else if (tid < 2 * BW) pos_h = (BH - 1) * BW + (tid - BW);  // row BH-1
+    else if (tid < 2 * BW + TY) pos_h = (tid - 2 * BW + 1) * BW;             // col 0
+    else if (tid < NHALO) pos_h = (tid - 2 * BW - TY + 1) * BW + (BW - 1);  // col BW-1
 
-    // halo item: rows y0-1 / y0+hg, columns x0-1 / x0+w (corners are not needed)
-    bool hal = false;
-    int hr = 0, hc = 0;
-    int64_t o_hal = 0;
-    if (tid < TX) {
-        hal = tid < w;
-        o_hal = (int64_t)((y0 - 1 + a.ny) % a.ny) * a.nx + (x0 + tid);
-        hr = 0; hc = tid + 1;
-    } else if (tid < 2 * TX) {
-        const int t = tid - TX;
-        hal = t < w;
-        o_hal = (int64_t)((y0 + hg) % a.ny) * a.nx + (x0 + t);
-        hr = hg + 1; hc = t + 1;
-    } else if (tid < 2 * TX + TY) {
-        const int t = tid - 2 * TX;
-        hal = t < hg;
-        o_hal = (int64_t)(y0 + t) * a.nx + ((x0 - 1 + a.nx) % a.nx);
-        hr = t + 1; hc = 0;
-    } else if (tid < 2 * TX + 2 * TY) {
-        const int t = tid - 2 * TX - TY;
-        hal = t < hg;
-        o_hal = (int64_t)(y0 + t) * a.nx + ((x0 + w) % a.nx);
-        hr = t + 1; hc = w + 1;
+    auto issue = [&](int i) {  // thread 0 only
+        const int p = zb - 1 + i, s = i % R;
+        double* dst = raw + (size_t)s * NA * ARR_DBL;
+        if (plane_is_ghost(a, p)) {
+            mbar_expect_tx(&bar[s], BOX_BYTES);
+            tma_load_4d(dst, p < 0 ? &a.tm_glo : &a.tm_ghi, &bar[s], x0, y0, 0, 0);
+        } else {
+            const int q = p < 0 ? p + G.nzl : (p >= G.nzl ? p - G.nzl : p);
+            mbar_expect_tx(&bar[s], NA * BOX_BYTES);
+            tma_load_4d(dst, &a.tm_u, &bar[s], x0, y0, 0, q);
+#pragma unroll
+            for (int k = 0; k < NS; ++k)
+                tma_load_4d(dst + (k + 1) * ARR_DBL, &a.tm_k[k], &bar[s], x0, y0, 0, q);
+        }
+    };
+    auto slot_of = [&](int i) -> const double* { return raw + (size_t)(i % R) * NA * ARR_DBL; };
+    auto wait_plane = [&](int i) { mbar_wait(&bar[i % R], (uint32_t)((i / R) & 1)); };
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < R; ++s) mbar_init(&bar[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int n0 = nplanes < R ? nplanes : R;
+        for (int i = 0; i < n0; ++i) issue(i);
     }
 
-    Raw<NS> P, H;  // raw inputs in flight: own cell, halo cell
     double Ym[2] = {0.0, 0.0}, Yc[2] = {0.0, 0.0}, Yp[2] = {0.0, 0.0};
     EState Ec{}, En{};
     unsigned long long rmax = 0ull;
 
-    // ---- prologue: Y(zb-1) own column; Y(zb) tile + halo; issue plane zb+1 -------------
-    if (own) {
-        load_cell<NS, false>(a, zb - 1, o_own, cs, ps, P);
-        combine_y<NS>(a, is_ghost(a, zb - 1), P, Ym);
-        load_cell<NS, false>(a, zb, o_own, cs, ps, P);
+    // ---- prologue: plane zb-1 (own column only), plane zb (tile + ring) -----------------
+    {
+        wait_plane(0);
+        const double* s0 = slot_of(0);
+        const bool gh = plane_is_ghost(a, zb - 1);
+        if (own) {
+            Ym[0] = y_at<NS>(a, s0 + pos_own, gh);
+            Ym[1] = y_at<NS>(a, s0 + BOX + pos_own, gh);
+        }
+        wait_plane(1);
+        const double* s1 = slot_of(1);
+        if (own) {
+            Yc[0] = y_at<NS>(a, s1 + pos_own, false);
+            Yc[1] = y_at<NS>(a, s1 + BOX + pos_own, false);
+            sY[pos_own] = Yc[0];
+            sY[BOX + pos_own] = Yc[1];
+            make_estate<NS, EPI>(a, s1, pos_own, Ec);
+        }
+        if (hal) {
+            sY[pos_h] = y_at<NS>(a, s1 + pos_h, false);
+            sY[BOX + pos_h] = y_at<NS>(a, s1 + BOX + pos_h, false);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (R < nplanes) issue(R);
+            if (R + 1 < nplanes) issue(R + 1);
+        }
     }
-    if (hal) load_cell<NS, true>(a, zb, o_hal, cs, ps, H);
-    if (own) {
-        combine_y<NS>(a, false, P, Yc);
-        sY[0][0][ly + 1][lx + 1] = Yc[0];
-        sY[0][1][ly + 1][lx + 1] = Yc[1];
-        make_estate<NS, EPI>(a, P, Ec);
-    }
-    if (hal) {
-        double y[2];
-        combine_y<NS>(a, false, H, y);
-        sY[0][0][hr][hc] = y[0];
-        sY[0][1][hr][hc] = y[1];
-    }
-    if (own) load_cell<NS, false>(a, zb + 1, o_own, cs, ps, P);
-    if (hal && zb + 1 < ze) load_cell<NS, true>(a, zb + 1, o_hal, cs, ps, H);
-    __syncthreads();
 
     for (int z = zb; z < ze; ++z) {
+        const int i = z - zb + 2;  // plane z+1
         const int b = (z - zb) & 1;
         const bool more = z + 1 < ze;  // plane z+1 is an output plane of this CTA
-        const bool gz1 = is_ghost(a, z + 1);
-        // [A] consume plane z+1
+        double* yc = sY + b * 2 * BOX;
+        double* yn = sY + (b ^ 1) * 2 * BOX;
+        // [A] plane z+1 from the ring
+        wait_plane(i);
+        const double* si = slot_of(i);
+        const bool gh = plane_is_ghost(a, z + 1);
         if (own) {
-            combine_y<NS>(a, gz1, P, Yp);
+            Yp[0] = y_at<NS>(a, si + pos_own, gh);
+            Yp[1] = y_at<NS>(a, si + BOX + pos_own, gh);
             if (more) {
-                sY[b ^ 1][0][ly + 1][lx + 1] = Yp[0];
-                sY[b ^ 1][1][ly + 1][lx + 1] = Yp[1];
-                make_estate<NS, EPI>(a, P, En);
+                yn[pos_own] = Yp[0];
+                yn[BOX + pos_own] = Yp[1];
+                make_estate<NS, EPI>(a, si, pos_own, En);
             }
         }
         if (hal && more) {
-            double y[2];
-            combine_y<NS>(a, gz1, H, y);
-            sY[b ^ 1][0][hr][hc] = y[0];
-            sY[b ^ 1][1][hr][hc] = y[1];
-        }
-        // [A'] issue loads of plane z+2 (own: needed as the z+1 neighbour; halo: if output)
-        if (more) {
-            if (own) load_cell<NS, false>(a, z + 2, o_own, cs, ps, P);
-            if (hal && z + 2 < ze) load_cell<NS, true>(a, z + 2, o_hal, cs, ps, H);
+            yn[pos_h] = y_at<NS>(a, si + pos_h, false);
+            yn[BOX + pos_h] = y_at<NS>(a, si + BOX + pos_h, false);
         }
         // [C] stencil + reaction + epilogue at plane z
         if (own) {
             double L[2];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
+                const double* v = yc + c * BOX + pos_own;
                 const double ctr = Yc[c];
-                double s = add(sub(sY[b][c][ly + 1][lx], ctr), sub(sY[b][c][ly + 1][lx + 2], ctr));
-                s = add(s, add(sub(sY[b][c][ly][lx + 1], ctr), sub(sY[b][c][ly + 2][lx + 1], ctr)));
+                double s = add(sub(v[-1], ctr), sub(v[1], ctr));
+                s = add(s, add(sub(v[-BW], ctr), sub(v[BW], ctr)));
                 s = add(s, add(sub(Ym[c], ctr), sub(Yp[c], ctr)));
                 L[c] = mul(s, a.inv_h2);
             }
@@ -244,15 +288,17 @@ __global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const GsStageArgs a) {
             double f[2];
             f[0] = sub(add(sub(mul(a.d1, L[0]), r), a.F), mul(a.F, C0));
             f[1] = sub(add(mul(a.d2, L[1]), r), mul(a.FK, C1));
-            const int64_t oz = (int64_t)z * ps + o_own;
+            const int x = x0 + lx, y = y0 + ly;
+            const int64_t qo = (int64_t)z * G.ps;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                if constexpr (EPI == EPI_K || EPI == EPI_FSAL_ERR) a.out_k[oz + c * cs] = f[c];
+                const int64_t off = qo + c * G.cs;
+                if constexpr (EPI == EPI_K || EPI == EPI_FSAL_ERR) store_cell(a.out_k, G, off, x, y, f[c]);
                 if constexpr (FIN) {
                     const double wv = a.beta_new != 0.0 ? add(Ec.w[c], mul(a.beta_new, f[c])) : Ec.w[c];
-                    a.out_u[oz + c * cs] = wv;
+                    store_cell(a.out_u, G, off, x, y, wv);
                 }
-                if constexpr (EPI == EPI_FSAL_ERR) a.out_u[oz + c * cs] = Yc[c];
+                if constexpr (EPI == EPI_FSAL_ERR) store_cell(a.out_u, G, off, x, y, Yc[c]);
                 if constexpr (ERR) {
                     bool has_prev = false;
 #pragma unroll
@@ -270,19 +316,20 @@ __global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const GsStageArgs a) {
         Ym[0] = Yc[0]; Ym[1] = Yc[1];
         Yc[0] = Yp[0]; Yc[1] = Yp[1];
         Ec = En;
-        __syncthreads();
+        __syncthreads();  // Y(z+1) tile complete; ring slot of plane z+1 free
+        if (tid == 0 && i + R < nplanes) issue(i + R);
     }
     if constexpr (ERR) block_max_to_global(rmax, a.errmax);
 }
 
+// ---- halo-plane pack and ring fill -------------------------------------------------------
 template <int NS>
 __global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, double* __restrict__ send) {
-    const int64_t cs = (int64_t)a.nx * a.ny, ps = 2 * cs;
-    const int64_t total = 2 * ps;
+    const int64_t ps = a.geo.ps, total = 2 * ps;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t sel = e / ps, rest = e - sel * ps;
-        const int64_t base = (sel ? (int64_t)(a.nzl - 1) : 0) * ps + rest;
+        const int64_t base = (sel ? (int64_t)(a.geo.nzl - 1) : 0) * ps + rest;
         double v = __ldg(a.u + base);
 #pragma unroll
         for (int s = 0; s < NS; ++s)
@@ -291,26 +338,80 @@ __global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, doubl
     }
 }
 
+__global__ void fill_ring_kernel(double* __restrict__ p, GridGeom g, int nslices) {
+    const int64_t zc = blockIdx.y;  // (plane, component) slice of (ny+2) x P values
+    if (zc >= nslices) return;
+    double* b = p + zc * g.cs;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < max(g.nx, g.ny); t += gridDim.x * blockDim.x) {
+        if (t < g.ny) {
+            double* row = b + (int64_t)(t + 1) * g.P;
+            row[0] = row[g.nx];
+            row[g.nx + 1] = row[1];
+        }
+        if (t < g.nx) {
+            b[t + 1] = b[(int64_t)g.ny * g.P + t + 1];
+            b[(int64_t)(g.ny + 1) * g.P + t + 1] = b[(int64_t)g.P + t + 1];
+        }
+    }
+}
+
+template <int NS, int EPI>
+cudaError_t launch_one(const GsStageArgs& a, dim3 grid, cudaStream_t st) {
+    static bool configured = false;
+    constexpr int bytes = smem_bytes(NS);
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gs_stage_kernel<NS, EPI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    gs_stage_kernel<NS, EPI><<<grid, NT, bytes, st>>>(a);
+    return cudaGetLastError();
+}
+
 template <int NS>
 cudaError_t launch_ns(int epi, const GsStageArgs& a, dim3 grid, cudaStream_t st) {
     switch (epi) {
-    case EPI_K: gs_stage_kernel<NS, EPI_K><<<grid, NT, 0, st>>>(a); break;
-    case EPI_FINAL: gs_stage_kernel<NS, EPI_FINAL><<<grid, NT, 0, st>>>(a); break;
-    case EPI_FINAL_ERR: gs_stage_kernel<NS, EPI_FINAL_ERR><<<grid, NT, 0, st>>>(a); break;
-    case EPI_FSAL_ERR: gs_stage_kernel<NS, EPI_FSAL_ERR><<<grid, NT, 0, st>>>(a); break;
+    case EPI_K: return launch_one<NS, EPI_K>(a, grid, st);
+    case EPI_FINAL: return launch_one<NS, EPI_FINAL>(a, grid, st);
+    case EPI_FINAL_ERR: return launch_one<NS, EPI_FINAL_ERR>(a, grid, st);
+    case EPI_FSAL_ERR: return launch_one<NS, EPI_FSAL_ERR>(a, grid, st);
     default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
 }
 
 }  // namespace
 
+void gs_tile_dims(int* tx, int* ty) {
+    *tx = TX;
+    *ty = TY;
+}
+
+cudaError_t encode_grid_map(CUtensorMap* m, const double* base, const GridGeom& g, int nplanes) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[4] = {(cuuint64_t)g.P, (cuuint64_t)(g.ny + 2), 2, (cuuint64_t)nplanes};
+    const cuuint64_t strides[3] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.cs * 8, (cuuint64_t)g.ps * 8};
+    const cuuint32_t box[4] = {BW, BH, 2, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t launch_gs_stage(int epi, const GsStageArgs& a, cudaStream_t st, int* nlaunch) {
-    const int ntx = (a.nx + TX - 1) / TX, nty = (a.ny + TY - 1) / TY;
+    const int ntx = (a.geo.nx + TX - 1) / TX, nty = (a.geo.ny + TY - 1) / TY;
     const int tiles = ntx * nty;
     int nchunks;
     if (a.zmode == 1) {
-        nchunks = a.nzl > 1 ? 2 : 1;
+        nchunks = a.geo.nzl > 1 ? 2 : 1;
     } else {
         const int range = a.z_hi - a.z_lo;
         if (range <= 0) return cudaSuccess;
@@ -330,7 +431,7 @@ cudaError_t launch_gs_stage(int epi, const GsStageArgs& a, cudaStream_t st, int*
 }
 
 cudaError_t launch_gs_pack(const GsStageArgs& a, double* send, cudaStream_t st) {
-    const int64_t total = 4 * (int64_t)a.nx * a.ny;
+    const int64_t total = 2 * a.geo.ps;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     switch (a.nslots) {
@@ -342,6 +443,13 @@ cudaError_t launch_gs_pack(const GsStageArgs& a, double* send, cudaStream_t st) 
     case 5: gs_pack_kernel<5><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
     default: return cudaErrorInvalidValue;
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_ring(double* p, const GridGeom& g, int nslices, cudaStream_t st) {
+    const int n = g.nx > g.ny ? g.nx : g.ny;
+    dim3 grid((unsigned)((n + 255) / 256), (unsigned)nslices);
+    fill_ring_kernel<<<grid, 256, 0, st>>>(p, g, nslices);
     return cudaGetLastError();
 }
 

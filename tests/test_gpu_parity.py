@@ -222,11 +222,17 @@ def test_512_sampled_parity(ctx, scheme, adaptive):
     n = 512
     u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
     st = gs_state(ctx, n, n, n, u0)
-    if adaptive:
-        acc, E, _ = st.try_step(scheme, 0.0, 1.0, 1e-6, 1e-6)
+    dt = 1.0
+    if adaptive:  # as bench.py: tries until accepted; a rejected try leaves u untouched
+        for _ in range(10):
+            acc, E, dtn = st.try_step(scheme, 0.0, dt, 1e-6, 1e-6)
+            if acc:
+                break
+            assert E > 1.0 and dtn < dt
+            dt = dtn
         assert acc and 0.0 <= E <= 1.0
     else:
-        st.do_step(scheme, 0.0, 1.0)
+        st.do_step(scheme, 0.0, dt)
     g = st.get()
     lo, hi = rk_inputs.cube_range(n)
     rng = np.random.default_rng(0)
@@ -236,7 +242,7 @@ def test_512_sampled_parity(ctx, scheme, adaptive):
     p = oracle.gray_scott_problem(2 * r + 1, 2 * r + 1, 2 * r + 1)
     for (z, y, x) in pts:
         blk = _sample_block(u0, z, y, x, r)
-        out = oracle.step(p, OS[scheme], 0.0, 1.0, blk).reshape(blk.shape)
+        out = oracle.step(p, OS[scheme], 0.0, dt, blk).reshape(blk.shape)
         assert bitwise(g[z, :, y, x], out[r, :, r, r]), (z, y, x)
 
 
