@@ -224,19 +224,17 @@ __global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const __grid_constant__
         wait_plane(0);
         const double* s0 = slot_of(0);
         const bool gh = plane_is_ghost(a, zb - 1);
-        if (own) {
-            Ym[0] = y_at<NS>(a, s0 + pos_own, gh);
-            Ym[1] = y_at<NS>(a, s0 + BOX + pos_own, gh);
-        }
+        // every thread forms Y at its tile position, valid or not: for a partial tile
+        // (w < TX or hg < TY) the periodic ring sits inside the box at column w+1 / row hg+1
+        Ym[0] = y_at<NS>(a, s0 + pos_own, gh);
+        Ym[1] = y_at<NS>(a, s0 + BOX + pos_own, gh);
         wait_plane(1);
         const double* s1 = slot_of(1);
-        if (own) {
-            Yc[0] = y_at<NS>(a, s1 + pos_own, false);
-            Yc[1] = y_at<NS>(a, s1 + BOX + pos_own, false);
-            sY[pos_own] = Yc[0];
-            sY[BOX + pos_own] = Yc[1];
-            make_estate<NS, EPI>(a, s1, pos_own, Ec);
-        }
+        Yc[0] = y_at<NS>(a, s1 + pos_own, false);
+        Yc[1] = y_at<NS>(a, s1 + BOX + pos_own, false);
+        sY[pos_own] = Yc[0];
+        sY[BOX + pos_own] = Yc[1];
+        if (own) make_estate<NS, EPI>(a, s1, pos_own, Ec);
         if (hal) {
             sY[pos_h] = y_at<NS>(a, s1 + pos_h, false);
             sY[BOX + pos_h] = y_at<NS>(a, s1 + BOX + pos_h, false);
@@ -258,14 +256,12 @@ __global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const __grid_constant__
         wait_plane(i);
         const double* si = slot_of(i);
         const bool gh = plane_is_ghost(a, z + 1);
-        if (own) {
-            Yp[0] = y_at<NS>(a, si + pos_own, gh);
-            Yp[1] = y_at<NS>(a, si + BOX + pos_own, gh);
-            if (more) {
-                yn[pos_own] = Yp[0];
-                yn[BOX + pos_own] = Yp[1];
-                make_estate<NS, EPI>(a, si, pos_own, En);
-            }
+        Yp[0] = y_at<NS>(a, si + pos_own, gh);
+        Yp[1] = y_at<NS>(a, si + BOX + pos_own, gh);
+        if (more) {
+            yn[pos_own] = Yp[0];
+            yn[BOX + pos_own] = Yp[1];
+            if (own) make_estate<NS, EPI>(a, si, pos_own, En);
         }
         if (hal && more) {
             yn[pos_h] = y_at<NS>(a, si + pos_h, false);
