@@ -9,19 +9,11 @@
 
 #include <cstdint>
 
+#include "rk_stage_spec.h"
+
 namespace rkb {
 
 enum RhsKind { RHS_NONE = -1, RHS_EXP = 0, RHS_LOGISTIC = 1, RHS_GRAY_SCOTT = 2 };
-
-// Epilogues of the fused Gray–Scott stage kernel.
-enum Epilogue {
-    EPI_K = 0,          // write k_i = F(Y_i)
-    EPI_FINAL = 1,      // write u_new = u + sum beta_j k_j (+ beta_i k_i), k_i not stored
-    EPI_FINAL_ERR = 2,  // EPI_FINAL + embedded error ratio and its max (CK54 adaptive)
-    EPI_FSAL_ERR = 3    // Y_s is u_new (FSAL): write Y_s and k_s, error ratio + max (DOPRI5)
-};
-
-constexpr int kMaxSlots = 5;  // k_j arrays read by one stage (DOPRI5 stages 6/7, CK54 stage 6)
 
 // ---------------------------------------------------------------------------------------
 // K1: pointwise step of a whole RK scheme in registers (vector states).
@@ -56,33 +48,38 @@ struct GridGeom {
     int64_t ps;     // plane stride = 2*cs
 };
 void gs_tile_dims(int* tx, int* ty);
-// 4D tensor map (x, y, c, z) over a padded array of `nplanes` planes; box = one tile + ring.
-cudaError_t encode_grid_map(CUtensorMap* m, const double* base, const GridGeom& g, int nplanes);
 
-// K3: fused Gray–Scott stage kernel.
+// K3: fused Gray–Scott stage kernel.  Which terms exist is compile-time (StageSpec of
+// (scheme, adaptive, stage)); the runtime arguments are pointers, TMA maps and values.
 struct GsStageArgs {
-    CUtensorMap tm_u;
-    CUtensorMap tm_k[kMaxSlots];
-    CUtensorMap tm_glo, tm_ghi;  // ghost planes z=-1, z=nzl (multi-GPU); else periodic wrap
+    CUtensorMap tm_base;             // Y source: u (or u_new for EPI_TAIL_ERR), tile+ring box
+    CUtensorMap tm_slot[kMaxSlots];  // slot s: tile+ring box if it enters Y, else interior box
+    CUtensorMap tm_glo, tm_ghi;      // ghost planes z=-1, z=nzl (multi-GPU); else periodic wrap
     GridGeom geo;
-    const double* u;             // raw pointers (pack kernel)
-    const double* k[kMaxSlots];
-    double g[kMaxSlots];         // Y coefficient per slot (0: slot not in Y)
-    double beta[kMaxSlots];      // final-combination weight per slot (0: skip)
-    double delta[kMaxSlots];     // error weight per slot (0: skip)
-    double beta_new, delta_new;  // weights of the k_i computed by this stage
+    const double* base;              // raw pointers (pack kernel)
+    const double* slot[kMaxSlots];
+    double g[kMaxSlots];             // dt*a_ij per slot
+    double beta[kMaxSlots];          // dt*b_j per slot
+    double delta[kMaxSlots];         // dt*e_j per slot
+    double beta_new, delta_new;      // weights of the k_i computed by this stage
     double* out_k;
     double* out_u;
     unsigned long long* errmax;
     double dt, atol, rtol;
     double d1, d2, F, FK, inv_h2;
     int has_glo, has_ghi;
-    int z_lo, z_hi;              // output planes [z_lo, z_hi) (zmode 0)
-    int zchunk;                  // output planes per CTA
-    int zmode;                   // 0: contiguous chunks; 1: chunk 0 = plane 0, chunk 1 = nzl-1
-    int nslots;
+    int z_lo, z_hi;                  // output planes [z_lo, z_hi) (zmode 0)
+    int zchunk;                      // output planes per CTA
+    int zmode;                       // 0: contiguous chunks; 1: chunk 0 = plane 0, chunk 1 = nzl-1
+    int nyslots;                     // pack kernel: slots [0, nyslots) with g != 0 (Y terms)
 };
-cudaError_t launch_gs_stage(int epi, const GsStageArgs& a, cudaStream_t st, int* nlaunch);
+// (scheme, adaptive, stage) selects the compile-time StageSpec instance.
+cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageArgs& a,
+                            cudaStream_t st, int* nlaunch);
+// 4D tensor maps over a padded array of `nplanes` planes: tile + ring box ("halo") and
+// interior tile box ("own").
+cudaError_t encode_grid_maps(CUtensorMap* halo, CUtensorMap* own, const double* base,
+                             const GridGeom& g, int nplanes);
 
 // Y_i on own planes 0 and nzl-1 (whole padded planes) -> send = [lo plane | hi plane].
 cudaError_t launch_gs_pack(const GsStageArgs& a, double* send, cudaStream_t st);

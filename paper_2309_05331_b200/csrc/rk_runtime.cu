@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -112,7 +113,8 @@ struct rk_state_s {
     double* u = nullptr;
     double* u_new = nullptr;
     double* k[7] = {nullptr};
-    CUtensorMap tm_u{}, tm_unew{}, tm_k[7]{}, tm_glo{}, tm_ghi{};
+    CUtensorMap tm_u[2]{}, tm_unew[2]{}, tm_k[7][2]{};  // [0] tile+ring box, [1] interior box
+    CUtensorMap tm_glo{}, tm_ghi{};
     int nk = 0;
     bool k1_valid = false;           // k[0] == F(u) for the current u
     // halo (grid, world > 1 or loopback)
@@ -150,18 +152,18 @@ static rk_status dev_alloc(rk_ctx ctx, double** p, int64_t count) {
     return RK_OK;
 }
 
-// zero-filled array (pads and ring corners stay 0) with its TMA tensor map (grids)
+// zero-filled array (pads and ring corners stay 0) with its two TMA tensor maps (grids)
 static rk_status alloc_array(rk_state st, double** p, CUtensorMap* tm) {
     TRY(dev_alloc(st->ctx, p, st->alloc));
     CK_CTX(st->ctx, cudaMemsetAsync(*p, 0, sizeof(double) * (size_t)st->alloc, st->ctx->stream));
     if (st->grid && st->ncomp == 2 && tm)
-        CK_CTX(st->ctx, encode_grid_map(tm, *p, st->geo, (int)st->local));
+        CK_CTX(st->ctx, encode_grid_maps(&tm[0], &tm[1], *p, st->geo, (int)st->local));
     return RK_OK;
 }
 
 static rk_status ensure_k(rk_state st, int nk) {
     for (int j = st->nk; j < nk; ++j) {
-        TRY(alloc_array(st, &st->k[j], &st->tm_k[j]));
+        TRY(alloc_array(st, &st->k[j], st->tm_k[j]));
         st->nk = j + 1;
     }
     return RK_OK;
@@ -169,12 +171,12 @@ static rk_status ensure_k(rk_state st, int nk) {
 
 static void swap_u(rk_state st) {
     std::swap(st->u, st->u_new);
-    std::swap(st->tm_u, st->tm_unew);
+    for (int b = 0; b < 2; ++b) std::swap(st->tm_u[b], st->tm_unew[b]);
 }
 
 static void swap_k(rk_state st, int i, int j) {
     std::swap(st->k[i], st->k[j]);
-    std::swap(st->tm_k[i], st->tm_k[j]);
+    for (int b = 0; b < 2; ++b) std::swap(st->tm_k[i][b], st->tm_k[j][b]);
 }
 
 static int64_t plane_values(rk_state st) { return st->geo.ps; }  // one padded plane, 2 comps
@@ -208,23 +210,11 @@ static rk_status resolve_timing(rk_state st) {
 }
 
 // ------------------------------------------------------------------------------------
-// stage plans (built from the library's tableau; DESIGN.md §Stage schedule)
+// stage plans: the compile-time StageSpec table (rk_stage_spec.h) + this step's values
 // ------------------------------------------------------------------------------------
-struct StagePlan {
-    int stage = 0;
-    int nslots = 0;
-    int slot_j[kMaxSlots] = {0};
-    double g[kMaxSlots] = {0}, beta[kMaxSlots] = {0}, delta[kMaxSlots] = {0};
-    double beta_new = 0.0, delta_new = 0.0;
-    int epi = EPI_K;
-    int out_k = -1;      // k buffer written (EPI_K, EPI_FSAL_ERR)
-    bool writes_u = false;
-};
-
 struct Coeffs {
     int s = 0, order = 0, err_order = 0;
     double a[7][7] = {{0}}, b[7] = {0}, e[7] = {0}, c[7] = {0};
-    bool anz[7][7] = {{false}}, bnz[7] = {false}, enz[7] = {false};
 };
 
 static Coeffs coeffs_of(int scheme) {
@@ -234,15 +224,9 @@ static Coeffs coeffs_of(int scheme) {
     C.order = T.order;
     C.err_order = T.err_order;
     for (int i = 0; i < T.s; ++i) {
-        for (int j = 0; j < i; ++j) {
-            C.a[i][j] = rat_double(T.a[i][j]);
-            C.anz[i][j] = rat_nz(T.a[i][j]);
-        }
+        for (int j = 0; j < i; ++j) C.a[i][j] = rat_double(T.a[i][j]);
         C.b[i] = rat_double(T.b[i]);
-        C.bnz[i] = rat_nz(T.b[i]);
-        const Rat e = err_weight(T, i);
-        C.e[i] = rat_double(e);
-        C.enz[i] = rat_nz(e);
+        C.e[i] = rat_double(err_weight(T, i));
         C.c[i] = rat_double(T.c[i]);
     }
     return C;
@@ -250,59 +234,31 @@ static Coeffs coeffs_of(int scheme) {
 
 static bool valid_scheme(int s) { return s >= RK_EULER && s <= RK_DOPRI5; }
 
-// Fixed step: stages up to the last b_j != 0, the last one fused with u_new.
-// Adaptive: stages up to the last b_j or e_j != 0, the last one fused with the error
-// ratio; a FSAL last stage (row s == b, b_s == 0) writes Y_s as u_new and k_s.
+struct StagePlan {
+    int scheme = 0, adaptive = 0, stage = 0;
+    StageSpec sp{};
+    double g[kMaxSlots] = {0}, beta[kMaxSlots] = {0}, delta[kMaxSlots] = {0};
+    double beta_new = 0.0, delta_new = 0.0;
+};
+
 static std::vector<StagePlan> build_plan(int scheme, bool adaptive, double dt) {
     const Coeffs C = coeffs_of(scheme);
-    int last = 0;
-    for (int j = 0; j < C.s; ++j)
-        if (C.bnz[j] || (adaptive && C.enz[j])) last = j;
-    bool fsal = false;
-    if (adaptive && !C.bnz[last]) {
-        fsal = true;
-        for (int j = 0; j < last; ++j)
-            if (C.anz[last][j] != C.bnz[j] || C.a[last][j] != C.b[j]) fsal = false;
-    }
     std::vector<StagePlan> plan;
-    for (int i = 0; i <= last; ++i) {
+    const int n = num_stages(scheme, adaptive);
+    for (int i = 0; i < n; ++i) {
         StagePlan p;
+        p.scheme = scheme;
+        p.adaptive = adaptive ? 1 : 0;
         p.stage = i;
-        const bool fin = (i == last);
-        for (int j = 0; j < i; ++j) {
-            const bool need = C.anz[i][j] || (fin && C.bnz[j]) || (fin && adaptive && (C.enz[j] || j == 0));
-            if (!need) continue;
-            const int s = p.nslots++;
-            p.slot_j[s] = j;
-            p.g[s] = C.anz[i][j] ? dt * C.a[i][j] : 0.0;
-            p.beta[s] = (fin && C.bnz[j]) ? dt * C.b[j] : 0.0;
-            p.delta[s] = (fin && adaptive && C.enz[j]) ? dt * C.e[j] : 0.0;
+        p.sp = stage_spec(scheme, adaptive, i);
+        for (int s = 0; s < p.sp.nslots; ++s) {
+            const int j = p.sp.j[s];
+            p.g[s] = p.sp.gnz[s] ? dt * C.a[i][j] : 0.0;
+            p.beta[s] = p.sp.bnz[s] ? dt * C.b[j] : 0.0;
+            p.delta[s] = p.sp.dnz[s] ? dt * C.e[j] : 0.0;
         }
-        if (!fin) {
-            p.epi = EPI_K;
-            p.out_k = i;
-        } else if (!adaptive) {
-            p.epi = EPI_FINAL;
-            p.writes_u = true;
-            p.beta_new = C.bnz[i] ? dt * C.b[i] : 0.0;
-        } else if (fsal) {
-            p.epi = EPI_FSAL_ERR;
-            p.writes_u = true;
-            p.delta_new = C.enz[i] ? dt * C.e[i] : 0.0;
-            // k_s goes into a buffer no slot of this stage reads: the first unused j
-            int free_j = -1;
-            for (int j = 1; j < i && free_j < 0; ++j) {
-                bool used = false;
-                for (int s = 0; s < p.nslots; ++s) used |= (p.slot_j[s] == j);
-                if (!used) free_j = j;
-            }
-            p.out_k = free_j;
-        } else {
-            p.epi = EPI_FINAL_ERR;
-            p.writes_u = true;
-            p.beta_new = C.bnz[i] ? dt * C.b[i] : 0.0;
-            p.delta_new = C.enz[i] ? dt * C.e[i] : 0.0;
-        }
+        p.beta_new = p.sp.bnew ? dt * C.b[i] : 0.0;
+        p.delta_new = p.sp.dnew ? dt * C.e[i] : 0.0;
         plan.push_back(p);
     }
     return plan;
@@ -311,10 +267,15 @@ static std::vector<StagePlan> build_plan(int scheme, bool adaptive, double dt) {
 static int plan_num_k(const std::vector<StagePlan>& plan) {
     int nk = 0;
     for (auto& p : plan) {
-        if (p.out_k >= 0) nk = std::max(nk, p.out_k + 1);
-        for (int s = 0; s < p.nslots; ++s) nk = std::max(nk, p.slot_j[s] + 1);
+        if (p.sp.out_k >= 0) nk = std::max(nk, p.sp.out_k + 1);
+        for (int s = 0; s < p.sp.nslots; ++s)
+            if (p.sp.src[s] >= 0) nk = std::max(nk, p.sp.src[s] + 1);
     }
     return nk;
+}
+
+static bool is_ratio_stage(const StagePlan& p) {
+    return p.sp.epi == EPI_FINAL_ERR || p.sp.epi == EPI_TAIL_ERR;
 }
 
 // ------------------------------------------------------------------------------------
@@ -327,8 +288,8 @@ static rk_status ensure_halo(rk_state st) {
     TRY(dev_alloc(st->ctx, &st->sendbuf, 2 * plane_values(st)));
     TRY(dev_alloc(st->ctx, &st->ghostbuf, 2 * plane_values(st)));
     CK_CTX(st->ctx, cudaMemsetAsync(st->ghostbuf, 0, sizeof(double) * 2 * plane_values(st), st->ctx->stream));
-    CK_CTX(st->ctx, encode_grid_map(&st->tm_ghi, st->ghostbuf, st->geo, 1));
-    CK_CTX(st->ctx, encode_grid_map(&st->tm_glo, st->ghostbuf + plane_values(st), st->geo, 1));
+    CK_CTX(st->ctx, encode_grid_maps(&st->tm_ghi, nullptr, st->ghostbuf, st->geo, 1));
+    CK_CTX(st->ctx, encode_grid_maps(&st->tm_glo, nullptr, st->ghostbuf + plane_values(st), st->geo, 1));
     CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_pack, cudaEventDisableTiming));
     CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_halo, cudaEventDisableTiming));
     return RK_OK;
@@ -337,20 +298,24 @@ static rk_status ensure_halo(rk_state st) {
 static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
     GsStageArgs a{};
     a.geo = st->geo;
-    a.u = st->u;
-    a.tm_u = st->tm_u;
-    a.nslots = p.nslots;
-    for (int s = 0; s < p.nslots; ++s) {
-        a.k[s] = st->k[p.slot_j[s]];
-        a.tm_k[s] = st->tm_k[p.slot_j[s]];
+    a.base = p.sp.base_unew ? st->u_new : st->u;
+    a.tm_base = p.sp.base_unew ? st->tm_unew[0] : st->tm_u[0];
+    int ny = 0;
+    for (int s = 0; s < p.sp.nslots; ++s) {
+        const int src = p.sp.src[s];
+        const int box = p.sp.halo[s] ? 0 : 1;
+        a.slot[s] = src >= 0 ? st->k[src] : st->u;
+        a.tm_slot[s] = src >= 0 ? st->tm_k[src][box] : st->tm_u[box];
         a.g[s] = p.g[s];
         a.beta[s] = p.beta[s];
         a.delta[s] = p.delta[s];
+        if (p.sp.gnz[s]) ++ny;
     }
+    a.nyslots = ny;
     a.beta_new = p.beta_new;
     a.delta_new = p.delta_new;
-    a.out_k = p.out_k >= 0 ? st->k[p.out_k] : nullptr;
-    a.out_u = p.writes_u ? st->u_new : nullptr;
+    a.out_k = p.sp.out_k >= 0 ? st->k[p.sp.out_k] : nullptr;
+    a.out_u = p.sp.writes_u ? st->u_new : nullptr;
     a.errmax = st->d_err;
     a.dt = dt;
     a.atol = atol;
@@ -366,16 +331,38 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     return a;
 }
 
-// planes per CTA: enough CTAs for ~16 per SM (2 resident x ~8 waves), >= 8 planes each
-static int pick_zchunk(rk_state st, int range) {
-    const int tiles = (int)(((st->nx + 31) / 32) * ((st->ny + 7) / 8));
-    const int target = st->ctx->num_sms * 16;
-    int nchunks = std::max(1, (target + tiles - 1) / tiles);
-    int zc = (range + nchunks - 1) / nchunks;
-    return std::max(zc, std::min(8, range));
+// pack arguments: the Y terms only, compacted in stage order (left-to-right sum preserved)
+static GsStageArgs pack_args(const GsStageArgs& a, const StagePlan& p) {
+    GsStageArgs q = a;
+    int n = 0;
+    for (int s = 0; s < p.sp.nslots; ++s) {
+        if (!p.sp.gnz[s] || p.sp.base_unew) continue;
+        q.slot[n] = a.slot[s];
+        q.g[n] = a.g[s];
+        ++n;
+    }
+    q.nyslots = n;
+    return q;
 }
 
-static rk_status launch_stage_timed(rk_state st, int epi, GsStageArgs& a) {
+// Planes per CTA.  Short z chunks keep y-neighbouring tiles (which re-read each other's
+// ring rows through L2) progressing together; measured at 512^2 planes (profiles/r1_*tune*):
+// 16 planes for stages with <= 1 k input (4 CTAs/SM), 32 for the two-output DOPRI5 stage 6,
+// 48 otherwise.  Small grids: shorten further so every SM gets work.
+static int pick_zchunk(rk_state st, const StagePlan& p, int range) {
+    if (range <= 0) return 1;
+    if (const char* e = getenv("RKB_ZCHUNK")) {  // developer tuning knob
+        const int v = atoi(e);
+        if (v > 0) return std::min(v, range);
+    }
+    int zc = p.sp.nslots <= 1 ? 16 : (p.sp.epi == EPI_FINAL_EPART ? 32 : 48);
+    const int tiles = (int)(((st->nx + 31) / 32) * ((st->ny + 7) / 8));
+    const int want = st->ctx->num_sms * 4;  // >= 2 waves of 2 CTAs per SM
+    while (zc > 4 && (int64_t)tiles * ((range + zc - 1) / zc) < want) zc /= 2;
+    return std::min(zc, range);
+}
+
+static rk_status launch_stage_timed(rk_state st, const StagePlan& p, GsStageArgs& a) {
     rk_ctx ctx = st->ctx;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (st->timing) {
@@ -384,12 +371,12 @@ static rk_status launch_stage_timed(rk_state st, int epi, GsStageArgs& a) {
         CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
     }
     int nl = 0;
-    CK_CTX(ctx, launch_gs_stage(epi, a, ctx->stream, &nl));
+    CK_CTX(ctx, launch_gs_stage(p.scheme, p.adaptive, p.stage, a, ctx->stream, &nl));
     st->stats.kernel_launches += nl;
     st->stats.stage_launches += nl;
     if (nl) {
         const int64_t planes = a.zmode == 1 ? (a.geo.nzl > 1 ? 2 : 1) : (int64_t)(a.z_hi - a.z_lo);
-        const int64_t arrays = 1 + a.nslots + (a.out_k ? 1 : 0) + (a.out_u ? 1 : 0);
+        const int64_t arrays = 1 + p.sp.nslots + (a.out_k ? 1 : 0) + (a.out_u ? 1 : 0);
         st->stats.stage_bytes += planes * st->nx * st->ny * 2 * (int64_t)sizeof(double) * arrays;
     }
     if (st->timing) {
@@ -452,11 +439,11 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
     const int nzl = (int)st->local;
     st->stats.rhs_evals += 1;
     if (!halo_path(st)) {
-        a.zchunk = pick_zchunk(st, nzl);
-        return launch_stage_timed(st, p.epi, a);
+        a.zchunk = pick_zchunk(st, p, nzl);
+        return launch_stage_timed(st, p, a);
     }
     // multi-GPU path: Y_i on the two boundary planes -> neighbours' ghost planes
-    CK_CTX(ctx, launch_gs_pack(a, st->sendbuf, ctx->stream));
+    CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->sendbuf, ctx->stream));
     st->stats.kernel_launches += 1;
     TRY(halo_exchange(st));
     a.has_ghi = 1;
@@ -467,16 +454,16 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
         GsStageArgs in = a;  // interior planes [1, nzl-1) never touch ghost planes
         in.z_lo = 1;
         in.z_hi = nzl - 1;
-        in.zchunk = pick_zchunk(st, nzl - 2);
-        TRY(launch_stage_timed(st, p.epi, in));
+        in.zchunk = pick_zchunk(st, p, nzl - 2);
+        TRY(launch_stage_timed(st, p, in));
         CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_halo, 0));
         GsStageArgs bd = a;
         bd.zmode = 1;
-        return launch_stage_timed(st, p.epi, bd);
+        return launch_stage_timed(st, p, bd);
     }
     CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_halo, 0));
-    a.zchunk = pick_zchunk(st, nzl);
-    return launch_stage_timed(st, p.epi, a);
+    a.zchunk = pick_zchunk(st, p, nzl);
+    return launch_stage_timed(st, p, a);
 }
 
 // Run the stages of one step / try.  Stage 0 (k1 = F(u)) is skipped when k1 is valid.
@@ -485,11 +472,11 @@ static rk_status run_grid_plan(rk_state st, const std::vector<StagePlan>& plan, 
     TRY(ensure_k(st, plan_num_k(plan)));
     TRY(ensure_halo(st));
     for (const StagePlan& p : plan) {
-        if (p.stage == 0 && p.epi == EPI_K && st->k1_valid) continue;
-        if (p.epi == EPI_FINAL_ERR || p.epi == EPI_FSAL_ERR)
+        if (p.stage == 0 && p.sp.epi == EPI_K && st->k1_valid) continue;
+        if (is_ratio_stage(p))
             CK_CTX(st->ctx, cudaMemsetAsync(st->d_err, 0, sizeof(unsigned long long), st->ctx->stream));
         TRY(run_gs_stage(st, p, dt, atol, rtol));
-        if (p.stage == 0 && p.epi == EPI_K) st->k1_valid = true;
+        if (p.stage == 0 && p.sp.epi == EPI_K) st->k1_valid = true;
     }
     return RK_OK;
 }
@@ -526,11 +513,7 @@ static rk_status run_pointwise(rk_state st, int scheme, double dt, int nsteps, b
     if (err) CK_CTX(ctx, cudaMemsetAsync(st->d_err, 0, sizeof(unsigned long long), ctx->stream));
     CK_CTX(ctx, launch_pointwise(scheme, a, ctx->stream, ctx->num_sms));
     st->stats.kernel_launches += 1;
-    const Coeffs C = coeffs_of(scheme);
-    int se = 0;
-    for (int j = 0; j < C.s; ++j)
-        if (C.bnz[j] || (err && C.enz[j])) se = j + 1;
-    st->stats.rhs_evals += (int64_t)se * (err ? 1 : nsteps);
+    st->stats.rhs_evals += (int64_t)num_stages(scheme, err) * (err ? 1 : nsteps);
     return RK_OK;
 }
 
@@ -580,10 +563,10 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
                          int* accepted, double* E_out, double* dt_next) {
     rk_ctx ctx = st->ctx;
     const Coeffs C = coeffs_of(scheme);
-    bool fsal = false;
+    int fsal_k = -1;  // FSAL: buffer holding k_s = F(u_new), the next step's k1
     if (st->grid) {
         auto plan = build_plan(scheme, true, dt);
-        fsal = plan.back().epi == EPI_FSAL_ERR;
+        if (plan.back().sp.epi == EPI_TAIL_ERR) fsal_k = plan.back().sp.out_k;
         TRY(run_grid_plan(st, plan, dt, atol, rtol));
     } else {
         TRY(run_pointwise(st, scheme, dt, 1, true, atol, rtol));
@@ -603,10 +586,8 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
     st->stats.last_dt = dtn;
     if (acc) {
         swap_u(st);
-        if (st->grid && fsal) {
-            // k_s (FSAL) was written into a free k buffer: it is F(u_new), the next k1
-            const auto plan = build_plan(scheme, true, dt);
-            swap_k(st, 0, plan.back().out_k);
+        if (fsal_k > 0) {
+            swap_k(st, 0, fsal_k);
             st->k1_valid = true;
         } else {
             st->k1_valid = false;
@@ -741,8 +722,8 @@ rk_status rk_ctx_destroy(rk_ctx ctx) {
 
 static rk_status state_common(rk_ctx ctx, rk_state st) {
     DeviceGuard g(ctx->device);
-    TRY(alloc_array(st, &st->u, &st->tm_u));
-    TRY(alloc_array(st, &st->u_new, &st->tm_unew));
+    TRY(alloc_array(st, &st->u, st->tm_u));
+    TRY(alloc_array(st, &st->u_new, st->tm_unew));
     CK_CTX(ctx, cudaMalloc((void**)&st->d_err, sizeof(unsigned long long)));
     CK_CTX(ctx, cudaMallocHost((void**)&st->h_err, sizeof(unsigned long long)));
     CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
@@ -772,7 +753,11 @@ rk_status rk_state_create_grid(rk_ctx ctx, int64_t nx, int64_t ny, int64_t nz, i
     st->geo.nx = (int)nx;
     st->geo.ny = (int)ny;
     st->geo.nzl = (int)st->local;
-    st->geo.P = (int)((nx + 2 + 1) / 2 * 2);  // even pitch: 16-byte rows for TMA
+    // row pitch: even (16-byte rows for TMA); RKB_PITCH_ALIGN (developer tuning knob) rounds
+    // it up to a larger multiple of elements
+    int palign = 2;
+    if (const char* e = getenv("RKB_PITCH_ALIGN")) palign = std::max(2, atoi(e) / 2 * 2);
+    st->geo.P = (int)((nx + 2 + palign - 1) / palign * palign);
     st->geo.cs = (ny + 2) * (int64_t)st->geo.P;
     st->geo.ps = ncomp * st->geo.cs;
     st->alloc = st->local * st->geo.ps;

@@ -1,0 +1,128 @@
+// rk_stage_spec.h — compile-time description of every fused stage launch.
+//
+// One table, used by the host scheduler (which k buffers to bind, which coefficients) and
+// by the device kernels (which terms exist), so zero Butcher coefficients are skipped at
+// compile time on the GPU exactly where the oracle skips them (R-17).
+//
+// Fixed step (do_step / integrate_const): stages 0..L, L = last j with b_j != 0; stage L is
+// fused with u_new = u + sum beta_j k_j (EPI_FINAL).
+// Adaptive, no FSAL (CK54): stage L fused with u_new and the error ratio (EPI_FINAL_ERR).
+// Adaptive, FSAL (DOPRI5, row s == b, b_s == 0): stage s-1 writes u_new and the partial
+// error sum e' = sum_{j<s} delta_j k_j (EPI_FINAL_EPART, into k_{s-1}'s buffer, which no
+// later stage needs); stage s reads Y_s = u_new directly (a_sj = b_j), computes
+// k_s = F(u_new) (the next step's k1), e = e' + delta_s k_s and the ratio (EPI_TAIL_ERR).
+// That is 31 arrays per try instead of 33.
+#pragma once
+#include "rk_tableau.h"
+
+namespace rkb {
+
+enum Epilogue {
+    EPI_K = 0,            // store k_i
+    EPI_FINAL = 1,        // store u_new = w + beta_i k_i
+    EPI_FINAL_ERR = 2,    // EPI_FINAL + error ratio max
+    EPI_FINAL_EPART = 3,  // EPI_FINAL + store e' = e + delta_i k_i
+    EPI_TAIL_ERR = 4      // Y = u_new (base); store k_i; e = e' + delta_i k_i; ratio max
+};
+
+constexpr int kMaxSlots = 5;
+constexpr int SLOT_U = -1;  // slot source: the state u itself (TAIL stage: old u)
+
+struct StageSpec {
+    int valid = 0;
+    int epi = EPI_K;
+    int nslots = 0;
+    int src[kMaxSlots] = {0, 0, 0, 0, 0};  // k index (>= 0) or SLOT_U
+    bool halo[kMaxSlots] = {};             // slot enters Y (needs the periodic ring)
+    bool gnz[kMaxSlots] = {}, bnz[kMaxSlots] = {}, dnz[kMaxSlots] = {};
+    int j[kMaxSlots] = {0, 0, 0, 0, 0};    // stage index of the slot (coefficients)
+    bool bnew = false, dnew = false;       // beta_i / delta_i nonzero
+    int out_k = -1;                        // k buffer written (EPI_K, EPI_FINAL_EPART e', TAIL k_s)
+    bool writes_u = false;                 // stores u_new
+    bool base_unew = false;                // TAIL: array 0 (Y source) is u_new, used as is
+    int den_u = SLOT_U - 1;                // TAIL: slot holding old u for the ratio (else base)
+    int den_k1 = -1;                       // slot holding k1 for the ratio
+    int epart = -1;                        // TAIL: slot holding e'
+};
+
+__host__ __device__ constexpr bool t_anz(const Tableau& T, int i, int j) { return rat_nz(T.a[i][j]); }
+__host__ __device__ constexpr bool t_bnz(const Tableau& T, int j) { return rat_nz(T.b[j]); }
+__host__ __device__ constexpr bool t_enz(const Tableau& T, int j) { return rat_nz(err_weight(T, j)); }
+
+__host__ __device__ constexpr int last_stage(const Tableau& T, bool ad) {
+    int last = 0;
+    for (int j = 0; j < T.s; ++j)
+        if (t_bnz(T, j) || (ad && t_enz(T, j))) last = j;
+    return last;
+}
+
+__host__ __device__ constexpr bool is_fsal(const Tableau& T, bool ad) {
+    if (!ad || T.err_order == 0) return false;
+    const int L = last_stage(T, true);
+    if (t_bnz(T, L)) return false;
+    for (int j = 0; j < L; ++j)
+        if (T.a[L][j].n * T.b[j].d != T.b[j].n * T.a[L][j].d) return false;
+    return true;
+}
+
+__host__ __device__ constexpr int num_stages(int S, bool ad) {
+    return last_stage(tableau_of(S), ad) + 1;
+}
+
+__host__ __device__ constexpr StageSpec stage_spec(int S, bool ad, int i) {
+    const Tableau T = tableau_of(S);
+    StageSpec p{};
+    if (T.s == 0 || (ad && T.err_order == 0)) return p;
+    const int L = last_stage(T, ad);
+    if (i < 0 || i > L) return p;
+    const bool fsal = is_fsal(T, ad);
+    p.valid = 1;
+    if (fsal && i == L) {  // TAIL: Y_s = u_new, slots e' (k_{L-1} buffer), u, k1
+        p.epi = EPI_TAIL_ERR;
+        p.base_unew = true;
+        p.nslots = 3;
+        p.src[0] = L - 1; p.j[0] = L - 1;
+        p.src[1] = SLOT_U; p.j[1] = 0;
+        p.src[2] = 0; p.j[2] = 0;
+        p.epart = 0;
+        p.den_u = 1;
+        p.den_k1 = 2;
+        p.dnew = t_enz(T, i);
+        p.out_k = 1;  // k2's buffer: dead after the stage values (a_s2 = 0 for DOPRI5)
+        return p;
+    }
+    const bool fin = fsal ? (i == L - 1) : (i == L);
+    const bool err = ad && fin;
+    for (int j = 0; j < i; ++j) {
+        const bool need = t_anz(T, i, j) || (fin && t_bnz(T, j)) || (err && (t_enz(T, j) || j == 0));
+        if (!need) continue;
+        const int s = p.nslots++;
+        p.src[s] = j;
+        p.j[s] = j;
+        p.halo[s] = t_anz(T, i, j);
+        p.gnz[s] = t_anz(T, i, j);
+        p.bnz[s] = fin && t_bnz(T, j);
+        p.dnz[s] = err && t_enz(T, j);
+        if (err && j == 0) p.den_k1 = s;
+    }
+    if (!fin) {
+        p.epi = EPI_K;
+        p.out_k = i;
+    } else {
+        p.writes_u = true;
+        p.bnew = t_bnz(T, i);
+        if (!ad) {
+            p.epi = EPI_FINAL;
+        } else if (fsal) {
+            p.epi = EPI_FINAL_EPART;
+            p.dnew = t_enz(T, i);
+            p.out_k = i;  // e' into k_i's own buffer (k_i itself is not needed later)
+        } else {
+            p.epi = EPI_FINAL_ERR;
+            p.dnew = t_enz(T, i);
+        }
+    }
+    return p;
+}
+
+}  // namespace rkb

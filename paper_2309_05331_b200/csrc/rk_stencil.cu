@@ -8,20 +8,24 @@
 //   k_i = d*Lap(Y_i) + reaction(Y_i)       7-point periodic stencil + reaction terms
 //   epilogue: store k_i, or u_new = u + sum_j (dt b_j) k_j, and/or the embedded error
 //             ratio with a warp-shuffle / block max (P:L42, P:L135 for_each_norm).
+// Which terms exist is the compile-time StageSpec of (scheme, adaptive, stage): zero Butcher
+// coefficients are skipped by the compiler, exactly where the oracle skips them.
 //
 // Data movement (sm_100a): a CTA owns a 32x8 tile of the xy plane and sweeps a chunk of z
 // planes.  For every plane, one elected thread issues one 4D TMA box load per input array
-// (u and each k_j: 34x10 cells x 2 components, the tile plus its periodic ring thanks to
-// the padded layout) into an R-deep shared-memory ring guarded by mbarriers, R-1 planes
-// ahead of the plane being computed, so HBM sees a deep, register-free stream of loads.
-// Each plane's Y is formed once from the staged raw tiles into a double-buffered Y tile;
-// the own column keeps Y(z-1), Y(z), Y(z+1) in registers (register queue along z).  One
-// __syncthreads per plane.  Periodic x/y wrap is in the padded layout; z neighbours come
-// from ghost planes (multi-GPU, filled by NCCL) or by wrapping inside the slab (one GPU).
+// into an R-deep shared-memory ring guarded by mbarriers, R-1 planes ahead of the plane being
+// computed: a deep, register-free HBM stream.  Arrays that enter Y_i are loaded as the tile
+// plus its periodic ring (34x10 cells x 2 components, exact thanks to the padded layout);
+// arrays only needed at the tile's own cells (final-combination / error terms) as the bare
+// 32x8 tile.  Each plane's Y is formed once into a double-buffered smem tile; the own column
+// keeps Y(z-1), Y(z), Y(z+1) in registers.  One __syncthreads per plane.  z neighbours at the
+// slab ends come from ghost planes (multi-GPU, filled by NCCL) or by wrapping (one GPU).
 //
 // Arithmetic follows DESIGN.md R-17 bit for bit (no FMA: __dadd_rn / __dmul_rn), so the
 // results equal the oracle's for any tile/chunk/GPU decomposition.
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "rk_device.cuh"
 #include "rk_kernels.cuh"
@@ -30,20 +34,45 @@ namespace rkb {
 
 namespace {
 
-constexpr int TX = 32;            // tile width  (one warp per row)
-constexpr int TY = 8;             // tile height (8 warps)
+constexpr int TX = 32;  // tile width  (one warp per row)
+constexpr int TY = 8;   // tile height (8 warps)
 constexpr int NT = TX * TY;
 constexpr int BW = TX + 2, BH = TY + 2;
-constexpr int BOX = BW * BH;                  // cells per component in one TMA box
-constexpr int BOX_BYTES = 2 * BOX * 8;        // one array, both components (5440 B)
-constexpr int ARR_BYTES = (BOX_BYTES + 127) / 128 * 128;  // 128-B aligned slot stride
-constexpr int ARR_DBL = ARR_BYTES / 8;
-constexpr int NHALO = BOX - NT;               // ring positions of the box (84)
+constexpr int BOX = BW * BH;                              // cells per component, ring box
+constexpr int BOX_BYTES = 2 * BOX * 8;                    // 5440 B
+constexpr int HALO_SLOT = (BOX_BYTES + 127) / 128 * 128;  // 5504 B
+// interior box: the tile's own rows, but 34 wide from the 16-byte aligned column x0 (TMA
+// needs a 16-byte aligned inner start); 4352 B
+constexpr int OWN_ROW = BW;
+constexpr int OWN_BOX = TY * OWN_ROW;
+constexpr int OWN_BYTES = 2 * OWN_BOX * 8;
+constexpr int NHALO = BOX - NT;                           // ring positions (84)
+constexpr int SMEM_BUDGET = 110 * 1024;                   // 2 CTAs per SM
 static_assert(NHALO <= NT, "one ring position per thread");
 
-__host__ __device__ constexpr int ring_depth(int ns) { return ns <= 3 ? 4 : 3; }
-__host__ __device__ constexpr int smem_bytes(int ns) {
-    return ring_depth(ns) * (ns + 1) * ARR_BYTES + 2 * ARR_BYTES + ring_depth(ns) * 8;
+struct Layout {
+    int off[kMaxSlots] = {0, 0, 0, 0, 0};  // byte offset of slot s inside a ring stage
+    int stage_bytes = 0;                   // one ring stage (base + slots)
+    int tx_bytes = 0;                      // TMA bytes landing per non-ghost plane
+    int R = 2;                             // ring depth
+    int smem = 0;
+};
+
+__host__ __device__ constexpr Layout layout_of(const StageSpec& P) {
+    Layout L{};
+    int o = HALO_SLOT, tx = BOX_BYTES;
+    for (int s = 0; s < P.nslots; ++s) {
+        L.off[s] = o;
+        o += P.halo[s] ? HALO_SLOT : OWN_BYTES;
+        tx += P.halo[s] ? BOX_BYTES : OWN_BYTES;
+    }
+    L.stage_bytes = o;
+    L.tx_bytes = tx;
+    int R = (SMEM_BUDGET - 2 * HALO_SLOT - 64) / o;
+    R = R > 4 ? 4 : (R < 2 ? 2 : R);
+    L.R = R;
+    L.smem = R * o + 2 * HALO_SLOT + R * 8;
+    return L;
 }
 
 // ---- PTX wrappers -------------------------------------------------------------------
@@ -83,80 +112,46 @@ __device__ __forceinline__ bool plane_is_ghost(const GsStageArgs& a, int p) {
     return (p < 0 && a.has_glo) || (p >= a.geo.nzl && a.has_ghi);
 }
 
-// Y = u (+) g_s (x) k_s over slots with g_s != 0, left to right (R-17); a ghost plane holds
-// Y itself.  r points at component c, box position pos, of array 0 of a ring slot.
-template <int NS>
-__device__ __forceinline__ double y_at(const GsStageArgs& a, const double* r, bool ghost) {
-    double v = r[0];
-    if (!ghost) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-            if (a.g[s] != 0.0) v = add(v, mul(a.g[s], r[(s + 1) * ARR_DBL]));
-    }
-    return v;
+// Store one cell of a padded array and its periodic ring copies (corners are never read).
+struct Edge {
+    bool x0, x1, y0, y1;
+};
+__device__ __forceinline__ void store_cell(double* out, const GridGeom& g, int64_t off, int x, int y,
+                                           Edge e, double v) {
+    out[off + (int64_t)(y + 1) * g.P + (x + 1)] = v;
+    if (e.x0) out[off + (int64_t)(y + 1) * g.P + (g.nx + 1)] = v;
+    if (e.x1) out[off + (int64_t)(y + 1) * g.P] = v;
+    if (e.y0) out[off + (int64_t)(g.ny + 1) * g.P + (x + 1)] = v;
+    if (e.y1) out[off + (x + 1)] = v;
 }
 
-// Per-cell partial sums the epilogue completes with the new k_i (bitwise identical to the
-// full left-to-right sums because j = i is always the last term).
+// Per-cell partial sums completed by the epilogue with the new k_i (bitwise identical to the
+// full left-to-right sums: j = i is always the last term).
 struct EState {
     double w[2];  // u (+) sum beta_j k_j
-    double e[2];  // sum delta_j k_j (first term not added to 0)
+    double e[2];  // sum delta_j k_j (first term not added to 0), or e' (TAIL)
     double d[2];  // atol (+) rtol (x) (|u| (+) dt (x) |k1|)
 };
 
-template <int NS, int EPI>
-__device__ __forceinline__ void make_estate(const GsStageArgs& a, const double* slot, int pos,
-                                            EState& es) {
-    constexpr bool FIN = (EPI == EPI_FINAL || EPI == EPI_FINAL_ERR);
-    constexpr bool ERR = (EPI == EPI_FINAL_ERR || EPI == EPI_FSAL_ERR);
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        const double* r = slot + c * BOX + pos;
-        const double u = r[0];
-        if constexpr (FIN) {
-            double w = u;
-#pragma unroll
-            for (int s = 0; s < NS; ++s)
-                if (a.beta[s] != 0.0) w = add(w, mul(a.beta[s], r[(s + 1) * ARR_DBL]));
-            es.w[c] = w;
-        }
-        if constexpr (ERR) {
-            double e = 0.0;
-            bool first = true;
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                if (a.delta[s] == 0.0) continue;
-                const double t = mul(a.delta[s], r[(s + 1) * ARR_DBL]);
-                e = first ? t : add(e, t);
-                first = false;
-            }
-            es.e[c] = e;
-            const double k1 = NS > 0 ? r[ARR_DBL] : 0.0;  // slot 0 holds k1 in error stages
-            es.d[c] = add(a.atol, mul(a.rtol, add(fabs(u), mul(a.dt, fabs(k1)))));
-        }
-    }
+// the error sum already holds a term before delta_i k_i is added
+__host__ __device__ constexpr bool has_prev_e(const StageSpec& P) {
+    bool h = P.epi == EPI_TAIL_ERR;
+    for (int s = 0; s < P.nslots; ++s) h = h || P.dnz[s];
+    return h;
 }
 
-// Store one cell of a padded array and its periodic ring copies (corners are never read).
-__device__ __forceinline__ void store_cell(double* out, const GridGeom& g, int64_t off, int x, int y,
-                                           double v) {
-    out[off + (int64_t)(y + 1) * g.P + (x + 1)] = v;
-    if (x == 0) out[off + (int64_t)(y + 1) * g.P + (g.nx + 1)] = v;
-    if (x == g.nx - 1) out[off + (int64_t)(y + 1) * g.P] = v;
-    if (y == 0) out[off + (int64_t)(g.ny + 1) * g.P + (x + 1)] = v;
-    if (y == g.ny - 1) out[off + (x + 1)] = v;
-}
-
-template <int NS, int EPI>
+template <int S, int AD, int I>
 __global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const __grid_constant__ GsStageArgs a) {
-    constexpr int R = ring_depth(NS);
-    constexpr int NA = NS + 1;
-    constexpr bool FIN = (EPI == EPI_FINAL || EPI == EPI_FINAL_ERR);
-    constexpr bool ERR = (EPI == EPI_FINAL_ERR || EPI == EPI_FSAL_ERR);
+    constexpr StageSpec P = stage_spec(S, AD != 0, I);
+    constexpr Layout LY = layout_of(P);
+    constexpr int NS = P.nslots, EPI = P.epi, R = LY.R;
+    constexpr bool FIN = EPI == EPI_FINAL || EPI == EPI_FINAL_ERR || EPI == EPI_FINAL_EPART;
+    constexpr bool ESUM = EPI == EPI_FINAL_ERR || EPI == EPI_FINAL_EPART;  // e from slots
+    constexpr bool RATIO = EPI == EPI_FINAL_ERR || EPI == EPI_TAIL_ERR;
+    constexpr bool STORE_K = EPI == EPI_K || EPI == EPI_TAIL_ERR;
     extern __shared__ __align__(128) unsigned char smem[];
-    double* raw = reinterpret_cast<double*>(smem);                          // [R][NA][2][BH][BW]
-    double* sY = reinterpret_cast<double*>(smem + R * NA * ARR_BYTES);      // [2][2][BH][BW]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R * NA * ARR_BYTES + 2 * ARR_BYTES);
+    double* sY = reinterpret_cast<double*>(smem + R * LY.stage_bytes);  // [2][2][BH][BW]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R * LY.stage_bytes + 2 * HALO_SLOT);
 
     const GridGeom& G = a.geo;
     const int tid = threadIdx.x;
@@ -173,36 +168,90 @@ __global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const __grid_constant__
         ze = zb + 1;
     }
     if (zb >= ze) return;  // CTA-uniform, before any barrier
-    const int nplanes = ze - zb + 2;  // planes zb-1 .. ze, plane i is global zb-1+i
+    const int nplanes = ze - zb + 2;  // planes zb-1 .. ze; plane i is global zb-1+i
 
     const int lx = tid % TX, ly = tid / TX;
     const bool own = (lx < w) && (ly < hg);
-    const int pos_own = (ly + 1) * BW + (lx + 1);
-    // ring position handled by this thread (all 84 box positions outside the tile)
-    const bool hal = tid < NHALO;
+    const int pos = (ly + 1) * BW + (lx + 1);  // own cell in a ring box
+    const int poi = ly * OWN_ROW + lx + 1;     // own cell in an interior box
+    const bool hal = tid < NHALO;              // one ring position per thread
     int pos_h = 0;
-    if (tid < BW) pos_h = tid;                                  // row 0
-    else if (tid < 2 * BW) pos_h = (BH - 1) * BW + (tid - BW);  // row BH-1
-    else if (tid < 2 * BW + TY) pos_h = (tid - 2 * BW + 1) * BW;             // col 0
-    else if (tid < NHALO) pos_h = (tid - 2 * BW - TY + 1) * BW + (BW - 1);  // col BW-1
+    if (tid < BW) pos_h = tid;
+    else if (tid < 2 * BW) pos_h = (BH - 1) * BW + (tid - BW);
+    else if (tid < 2 * BW + TY) pos_h = (tid - 2 * BW + 1) * BW;
+    else if (tid < NHALO) pos_h = (tid - 2 * BW - TY + 1) * BW + (BW - 1);
+    const int x = x0 + lx, y = y0 + ly;
+    const Edge edge{x == 0, x == G.nx - 1, y == 0, y == G.ny - 1};
 
+    auto stage_of = [&](int i) -> unsigned char* { return smem + (size_t)(i % R) * LY.stage_bytes; };
     auto issue = [&](int i) {  // thread 0 only
-        const int p = zb - 1 + i, s = i % R;
-        double* dst = raw + (size_t)s * NA * ARR_DBL;
+        const int p = zb - 1 + i;
+        unsigned char* st = stage_of(i);
+        uint64_t* b = &bar[i % R];
         if (plane_is_ghost(a, p)) {
-            mbar_expect_tx(&bar[s], BOX_BYTES);
-            tma_load_4d(dst, p < 0 ? &a.tm_glo : &a.tm_ghi, &bar[s], x0, y0, 0, 0);
+            mbar_expect_tx(b, BOX_BYTES);
+            tma_load_4d(st, p < 0 ? &a.tm_glo : &a.tm_ghi, b, x0, y0, 0, 0);
         } else {
             const int q = p < 0 ? p + G.nzl : (p >= G.nzl ? p - G.nzl : p);
-            mbar_expect_tx(&bar[s], NA * BOX_BYTES);
-            tma_load_4d(dst, &a.tm_u, &bar[s], x0, y0, 0, q);
+            mbar_expect_tx(b, LY.tx_bytes);
+            tma_load_4d(st, &a.tm_base, b, x0, y0, 0, q);
 #pragma unroll
-            for (int k = 0; k < NS; ++k)
-                tma_load_4d(dst + (k + 1) * ARR_DBL, &a.tm_k[k], &bar[s], x0, y0, 0, q);
+            for (int s = 0; s < NS; ++s) {
+                if (P.halo[s]) tma_load_4d(st + LY.off[s], &a.tm_slot[s], b, x0, y0, 0, q);
+                else tma_load_4d(st + LY.off[s], &a.tm_slot[s], b, x0, y0 + 1, 0, q);
+            }
         }
     };
-    auto slot_of = [&](int i) -> const double* { return raw + (size_t)(i % R) * NA * ARR_DBL; };
     auto wait_plane = [&](int i) { mbar_wait(&bar[i % R], (uint32_t)((i / R) & 1)); };
+
+    // Y at ring-box position hp, component c (base + Y slots; a ghost plane is Y itself)
+    auto y_at = [&](const unsigned char* st, int c, int hp, bool ghost) -> double {
+        double v = reinterpret_cast<const double*>(st)[c * BOX + hp];
+        if (!ghost && !P.base_unew) {
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+                if (P.gnz[s])
+                    v = add(v, mul(a.g[s], reinterpret_cast<const double*>(st + LY.off[s])[c * BOX + hp]));
+        }
+        return v;
+    };
+    // own-cell value of slot s (ring box or interior box), component c
+    auto sval = [&](const unsigned char* st, int s, int c) -> double {
+        const double* p = reinterpret_cast<const double*>(st + LY.off[s]);
+        return P.halo[s] ? p[c * BOX + pos] : p[c * OWN_BOX + poi];
+    };
+    auto make_estate = [&](const unsigned char* st, EState& es) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const double ub = reinterpret_cast<const double*>(st)[c * BOX + pos];
+            if constexpr (FIN) {
+                double wv = ub;
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+                    if (P.bnz[s]) wv = add(wv, mul(a.beta[s], sval(st, s, c)));
+                es.w[c] = wv;
+            }
+            if constexpr (ESUM) {
+                double e = 0.0;
+                bool first = true;
+#pragma unroll
+                for (int s = 0; s < NS; ++s) {
+                    if (!P.dnz[s]) continue;
+                    const double t = mul(a.delta[s], sval(st, s, c));
+                    e = first ? t : add(e, t);
+                    first = false;
+                }
+                es.e[c] = e;
+            }
+            if constexpr (EPI == EPI_TAIL_ERR) es.e[c] = sval(st, P.epart, c);
+            if constexpr (RATIO) {
+                const double uu = P.den_u >= 0 ? sval(st, P.den_u, c) : ub;
+                const double k1 = sval(st, P.den_k1, c);
+                es.d[c] = add(a.atol, mul(a.rtol, add(fabs(uu), mul(a.dt, fabs(k1)))));
+            }
+        }
+    };
+    constexpr bool HAS_PREV_E = has_prev_e(P);
 
     if (tid == 0) {
 #pragma unroll
@@ -215,29 +264,30 @@ __global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const __grid_constant__
         for (int i = 0; i < n0; ++i) issue(i);
     }
 
-    double Ym[2] = {0.0, 0.0}, Yc[2] = {0.0, 0.0}, Yp[2] = {0.0, 0.0};
+    double Ym[2], Yc[2], Yp[2];
     EState Ec{}, En{};
-    unsigned long long rmax = 0ull;
+    double rmax = 0.0;               // running max of the ratio (exact)
+    unsigned long long rbits = 0ull;  // its bit pattern (NaN-propagating)
 
     // ---- prologue: plane zb-1 (own column only), plane zb (tile + ring) -----------------
+    // Every thread forms Y at its tile position, valid or not: for a partial tile (w < TX or
+    // hg < TY) the periodic ring sits inside the box at column w+1 / row hg+1.
     {
         wait_plane(0);
-        const double* s0 = slot_of(0);
+        const unsigned char* s0 = stage_of(0);
         const bool gh = plane_is_ghost(a, zb - 1);
-        // every thread forms Y at its tile position, valid or not: for a partial tile
-        // (w < TX or hg < TY) the periodic ring sits inside the box at column w+1 / row hg+1
-        Ym[0] = y_at<NS>(a, s0 + pos_own, gh);
-        Ym[1] = y_at<NS>(a, s0 + BOX + pos_own, gh);
+        Ym[0] = y_at(s0, 0, pos, gh);
+        Ym[1] = y_at(s0, 1, pos, gh);
         wait_plane(1);
-        const double* s1 = slot_of(1);
-        Yc[0] = y_at<NS>(a, s1 + pos_own, false);
-        Yc[1] = y_at<NS>(a, s1 + BOX + pos_own, false);
-        sY[pos_own] = Yc[0];
-        sY[BOX + pos_own] = Yc[1];
-        if (own) make_estate<NS, EPI>(a, s1, pos_own, Ec);
+        const unsigned char* s1 = stage_of(1);
+        Yc[0] = y_at(s1, 0, pos, false);
+        Yc[1] = y_at(s1, 1, pos, false);
+        sY[pos] = Yc[0];
+        sY[BOX + pos] = Yc[1];
+        if (own) make_estate(s1, Ec);
         if (hal) {
-            sY[pos_h] = y_at<NS>(a, s1 + pos_h, false);
-            sY[BOX + pos_h] = y_at<NS>(a, s1 + BOX + pos_h, false);
+            sY[pos_h] = y_at(s1, 0, pos_h, false);
+            sY[BOX + pos_h] = y_at(s1, 1, pos_h, false);
         }
         __syncthreads();
         if (tid == 0) {
@@ -254,25 +304,25 @@ __global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const __grid_constant__
         double* yn = sY + (b ^ 1) * 2 * BOX;
         // [A] plane z+1 from the ring
         wait_plane(i);
-        const double* si = slot_of(i);
+        const unsigned char* si = stage_of(i);
         const bool gh = plane_is_ghost(a, z + 1);
-        Yp[0] = y_at<NS>(a, si + pos_own, gh);
-        Yp[1] = y_at<NS>(a, si + BOX + pos_own, gh);
+        Yp[0] = y_at(si, 0, pos, gh);
+        Yp[1] = y_at(si, 1, pos, gh);
         if (more) {
-            yn[pos_own] = Yp[0];
-            yn[BOX + pos_own] = Yp[1];
-            if (own) make_estate<NS, EPI>(a, si, pos_own, En);
-        }
-        if (hal && more) {
-            yn[pos_h] = y_at<NS>(a, si + pos_h, false);
-            yn[BOX + pos_h] = y_at<NS>(a, si + BOX + pos_h, false);
+            yn[pos] = Yp[0];
+            yn[BOX + pos] = Yp[1];
+            if (own) make_estate(si, En);
+            if (hal) {
+                yn[pos_h] = y_at(si, 0, pos_h, false);
+                yn[BOX + pos_h] = y_at(si, 1, pos_h, false);
+            }
         }
         // [C] stencil + reaction + epilogue at plane z
         if (own) {
             double L[2];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const double* v = yc + c * BOX + pos_own;
+                const double* v = yc + c * BOX + pos;
                 const double ctr = Yc[c];
                 double s = add(sub(v[-1], ctr), sub(v[1], ctr));
                 s = add(s, add(sub(v[-BW], ctr), sub(v[BW], ctr)));
@@ -284,52 +334,60 @@ __global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const __grid_constant__
             double f[2];
             f[0] = sub(add(sub(mul(a.d1, L[0]), r), a.F), mul(a.F, C0));
             f[1] = sub(add(mul(a.d2, L[1]), r), mul(a.FK, C1));
-            const int x = x0 + lx, y = y0 + ly;
             const int64_t qo = (int64_t)z * G.ps;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int64_t off = qo + c * G.cs;
-                if constexpr (EPI == EPI_K || EPI == EPI_FSAL_ERR) store_cell(a.out_k, G, off, x, y, f[c]);
+                if constexpr (STORE_K) store_cell(a.out_k, G, off, x, y, edge, f[c]);
                 if constexpr (FIN) {
-                    const double wv = a.beta_new != 0.0 ? add(Ec.w[c], mul(a.beta_new, f[c])) : Ec.w[c];
-                    store_cell(a.out_u, G, off, x, y, wv);
+                    const double wv = P.bnew ? add(Ec.w[c], mul(a.beta_new, f[c])) : Ec.w[c];
+                    store_cell(a.out_u, G, off, x, y, edge, wv);
                 }
-                if constexpr (EPI == EPI_FSAL_ERR) store_cell(a.out_u, G, off, x, y, Yc[c]);
-                if constexpr (ERR) {
-                    bool has_prev = false;
-#pragma unroll
-                    for (int s2 = 0; s2 < NS; ++s2) has_prev |= (a.delta[s2] != 0.0);
-                    double e = Ec.e[c];
-                    if (a.delta_new != 0.0) {
+                double e = Ec.e[c];
+                if constexpr (ESUM || EPI == EPI_TAIL_ERR) {
+                    if constexpr (P.dnew) {
                         const double t = mul(a.delta_new, f[c]);
-                        e = has_prev ? add(e, t) : t;
+                        e = HAS_PREV_E ? add(e, t) : t;
                     }
-                    const unsigned long long rb = ratio_bits(fabs(e) / Ec.d[c]);
-                    rmax = rb > rmax ? rb : rmax;
+                }
+                if constexpr (EPI == EPI_FINAL_EPART) store_cell(a.out_k, G, off, x, y, edge, e);
+                if constexpr (RATIO) {
+                    // r = |e| / d exactly; skip the division when e == 0 (r = +0) or when
+                    // |e| <= rmax*d*(1-2^-52) (a normal number) proves r <= rmax by
+                    // monotone rounding; NaN never skips.
+                    const double ae = fabs(e), dd = Ec.d[c];
+                    const double th = mul(mul(rmax, dd), 0.99999999999999978);
+                    if (!(ae == 0.0 || (ae <= th && th >= 2.2250738585072014e-308))) {
+                        const double rr = ae / dd;
+                        const unsigned long long rb = ratio_bits(rr);
+                        if (rb > rbits) {
+                            rbits = rb;
+                            rmax = rr;
+                        }
+                    }
                 }
             }
         }
         Ym[0] = Yc[0]; Ym[1] = Yc[1];
         Yc[0] = Yp[0]; Yc[1] = Yp[1];
         Ec = En;
-        __syncthreads();  // Y(z+1) tile complete; ring slot of plane z+1 free
+        __syncthreads();  // Y(z+1) tile complete; ring stage of plane z+1 free
         if (tid == 0 && i + R < nplanes) issue(i + R);
     }
-    if constexpr (ERR) block_max_to_global(rmax, a.errmax);
+    if constexpr (RATIO) block_max_to_global(rbits, a.errmax);
 }
 
 // ---- halo-plane pack and ring fill -------------------------------------------------------
-template <int NS>
+template <int NY>
 __global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, double* __restrict__ send) {
     const int64_t ps = a.geo.ps, total = 2 * ps;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t sel = e / ps, rest = e - sel * ps;
         const int64_t base = (sel ? (int64_t)(a.geo.nzl - 1) : 0) * ps + rest;
-        double v = __ldg(a.u + base);
+        double v = __ldg(a.base + base);
 #pragma unroll
-        for (int s = 0; s < NS; ++s)
-            if (a.g[s] != 0.0) v = add(v, mul(a.g[s], __ldg(a.k[s] + base)));
+        for (int s = 0; s < NY; ++s) v = add(v, mul(a.g[s], __ldg(a.slot[s] + base)));
         send[e] = v;
     }
 }
@@ -351,27 +409,47 @@ __global__ void fill_ring_kernel(double* __restrict__ p, GridGeom g, int nslices
     }
 }
 
-template <int NS, int EPI>
+template <int S, int AD, int I>
 cudaError_t launch_one(const GsStageArgs& a, dim3 grid, cudaStream_t st) {
+    constexpr StageSpec P = stage_spec(S, AD != 0, I);
+    static_assert(P.valid, "invalid stage");
+    constexpr int bytes = layout_of(P).smem;
     static bool configured = false;
-    constexpr int bytes = smem_bytes(NS);
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gs_stage_kernel<NS, EPI>,
+        cudaError_t e = cudaFuncSetAttribute(gs_stage_kernel<S, AD, I>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    gs_stage_kernel<NS, EPI><<<grid, NT, bytes, st>>>(a);
+    gs_stage_kernel<S, AD, I><<<grid, NT, bytes, st>>>(a);
     return cudaGetLastError();
 }
 
-template <int NS>
-cudaError_t launch_ns(int epi, const GsStageArgs& a, dim3 grid, cudaStream_t st) {
-    switch (epi) {
-    case EPI_K: return launch_one<NS, EPI_K>(a, grid, st);
-    case EPI_FINAL: return launch_one<NS, EPI_FINAL>(a, grid, st);
-    case EPI_FINAL_ERR: return launch_one<NS, EPI_FINAL_ERR>(a, grid, st);
-    case EPI_FSAL_ERR: return launch_one<NS, EPI_FSAL_ERR>(a, grid, st);
+// Stages whose spec does not depend on the adaptive flag share one instantiation.
+template <int S, int AD, int I>
+cudaError_t launch_norm(const GsStageArgs& a, dim3 grid, cudaStream_t st) {
+    constexpr StageSpec P = stage_spec(S, AD != 0, I);
+    if constexpr (!P.valid) {
+        return cudaErrorInvalidValue;
+    } else if constexpr (P.epi == EPI_K && I == 0) {
+        return launch_one<1, 0, 0>(a, grid, st);  // k1 = F(u): identical for every scheme
+    } else if constexpr (P.epi == EPI_K && AD != 0) {
+        return launch_one<S, 0, I>(a, grid, st);
+    } else {
+        return launch_one<S, AD, I>(a, grid, st);
+    }
+}
+
+template <int S, int AD>
+cudaError_t launch_stage_i(int i, const GsStageArgs& a, dim3 grid, cudaStream_t st) {
+    switch (i) {
+    case 0: return launch_norm<S, AD, 0>(a, grid, st);
+    case 1: return launch_norm<S, AD, 1>(a, grid, st);
+    case 2: return launch_norm<S, AD, 2>(a, grid, st);
+    case 3: return launch_norm<S, AD, 3>(a, grid, st);
+    case 4: return launch_norm<S, AD, 4>(a, grid, st);
+    case 5: return launch_norm<S, AD, 5>(a, grid, st);
+    case 6: return launch_norm<S, AD, 6>(a, grid, st);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -383,7 +461,22 @@ void gs_tile_dims(int* tx, int* ty) {
     *ty = TY;
 }
 
-cudaError_t encode_grid_map(CUtensorMap* m, const double* base, const GridGeom& g, int nplanes) {
+// Developer tuning knob (not part of the ABI): RKB_L2PROMO = 0 none, 1 64B, 2 128B, 3 256B.
+static CUtensorMapL2promotion l2_promotion() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("RKB_L2PROMO");
+        v = e ? atoi(e) : 3;
+        if (v < 0 || v > 3) v = 3;
+    }
+    const CUtensorMapL2promotion tab[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
+    return tab[v];
+}
+
+cudaError_t encode_grid_maps(CUtensorMap* halo, CUtensorMap* own, const double* base,
+                             const GridGeom& g, int nplanes) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -394,15 +487,24 @@ cudaError_t encode_grid_map(CUtensorMap* m, const double* base, const GridGeom& 
     }
     const cuuint64_t dims[4] = {(cuuint64_t)g.P, (cuuint64_t)(g.ny + 2), 2, (cuuint64_t)nplanes};
     const cuuint64_t strides[3] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.cs * 8, (cuuint64_t)g.ps * 8};
-    const cuuint32_t box[4] = {BW, BH, 2, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides,
-                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+    const cuuint32_t box_h[4] = {BW, BH, 2, 1};
+    const cuuint32_t box_o[4] = {OWN_ROW, TY, 2, 1};
+    CUresult r = encode(halo, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
+                        strides, box_h, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    if (own) {
+        r = encode(own, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides,
+                   box_o, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+    return cudaSuccess;
 }
 
-cudaError_t launch_gs_stage(int epi, const GsStageArgs& a, cudaStream_t st, int* nlaunch) {
+cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageArgs& a,
+                            cudaStream_t st, int* nlaunch) {
     const int ntx = (a.geo.nx + TX - 1) / TX, nty = (a.geo.ny + TY - 1) / TY;
     const int tiles = ntx * nty;
     int nchunks;
@@ -415,13 +517,14 @@ cudaError_t launch_gs_stage(int epi, const GsStageArgs& a, cudaStream_t st, int*
     }
     dim3 grid((unsigned)tiles, (unsigned)nchunks);
     if (nlaunch) ++*nlaunch;
-    switch (a.nslots) {
-    case 0: return launch_ns<0>(epi, a, grid, st);
-    case 1: return launch_ns<1>(epi, a, grid, st);
-    case 2: return launch_ns<2>(epi, a, grid, st);
-    case 3: return launch_ns<3>(epi, a, grid, st);
-    case 4: return launch_ns<4>(epi, a, grid, st);
-    case 5: return launch_ns<5>(epi, a, grid, st);
+    const int ad = adaptive ? 1 : 0;
+    switch (scheme * 2 + ad) {
+    case 0: return launch_stage_i<0, 0>(stage, a, grid, st);
+    case 2: return launch_stage_i<1, 0>(stage, a, grid, st);
+    case 4: return launch_stage_i<2, 0>(stage, a, grid, st);
+    case 5: return launch_stage_i<2, 1>(stage, a, grid, st);
+    case 6: return launch_stage_i<3, 0>(stage, a, grid, st);
+    case 7: return launch_stage_i<3, 1>(stage, a, grid, st);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -430,7 +533,7 @@ cudaError_t launch_gs_pack(const GsStageArgs& a, double* send, cudaStream_t st) 
     const int64_t total = 2 * a.geo.ps;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    switch (a.nslots) {
+    switch (a.nyslots) {
     case 0: gs_pack_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
     case 1: gs_pack_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
     case 2: gs_pack_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
