@@ -113,6 +113,26 @@ rk_status rk_tableau(rk_scheme scheme, double* a, double* b, double* e, double* 
  * *accepted if E <= 1 (then dt grows when E < 0.5), 0 if rejected (dt shrinks). */
 rk_status rk_controller(rk_scheme scheme, double E, double* dt, int* accepted);
 
+/* Per-stage halo exchange of a z-slab grid (P:L168, P:L176 ghost_get), as
+ * executed by every stage on the comm stream.  Buffers hold padded planes of Y_i:
+ *   send  = [plane 0 | plane nzl-1] (this rank's lowest and highest owned planes),
+ *   ghost = [plane nzl (from up) | plane -1 (from down)].
+ * Each message moves `nplanes` planes between plane slots of those buffers.  world == 1
+ * (loopback) is one self-message; world == 2 one message each way (the only peer is both
+ * neighbours); world >= 3 two sends and two receives.  Host-only (no GPU needed). */
+typedef struct {
+    int recv;        /* 0: send from the send buffer, 1: receive into the ghost buffer */
+    int peer;        /* rank (== own rank for the world == 1 self-exchange)           */
+    int slot;        /* first plane slot (0 or 1) in the buffer                        */
+    int nplanes;     /* 1 or 2                                                          */
+} rk_halo_msg;
+typedef struct {
+    int up, down;    /* periodic z-neighbours: (rank+1) % world, (rank-1+world) % world */
+    int nmsg;
+    rk_halo_msg msg[4]; /* in posting order (sends, then receives) */
+} rk_halo_plan;
+rk_status rk_halo_plan_get(int world, int rank, rk_halo_plan* out);
+
 /* ---- context ------------------------------------------------------------------------ */
 /* Rank 0 creates the NCCL unique id (RK_UNIQUE_ID_BYTES bytes); the caller broadcasts it
  * (torch.distributed) to all ranks before rk_ctx_create.  Not needed when world == 1. */

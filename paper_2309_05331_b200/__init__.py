@@ -5,10 +5,10 @@ The compute path is librkb200.so (hand-written sm_100a CUDA behind the C-ABI in
 include/rk_b200.h); this package is its thin ctypes binding.  There is no CPU fallback.
 """
 from .api import (CASH_KARP54, DOPRI5, EULER, RK4, SCHEMES, Context, State, controller,
-                  partition, tableau)
+                  halo_plan, partition, tableau)
 from ._native import (OPT_HALO_LOOPBACK, OPT_HALO_OVERLAP, OPT_MAX_TRIES, OPT_TIMING,
                       OPT_USE_GRAPH, RKError, lib)
 
 __all__ = ["Context", "State", "EULER", "RK4", "CASH_KARP54", "DOPRI5", "SCHEMES", "RKError",
-           "partition", "tableau", "controller", "lib", "OPT_HALO_OVERLAP", "OPT_HALO_LOOPBACK",
+           "partition", "tableau", "controller", "halo_plan", "lib", "OPT_HALO_OVERLAP", "OPT_HALO_LOOPBACK",
            "OPT_MAX_TRIES", "OPT_TIMING", "OPT_USE_GRAPH"]

@@ -38,6 +38,16 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class HaloMsg(ctypes.Structure):
+    _fields_ = [("recv", ctypes.c_int), ("peer", ctypes.c_int), ("slot", ctypes.c_int),
+                ("nplanes", ctypes.c_int)]
+
+
+class HaloPlan(ctypes.Structure):
+    _fields_ = [("up", ctypes.c_int), ("down", ctypes.c_int), ("nmsg", ctypes.c_int),
+                ("msg", HaloMsg * 4)]
+
+
 _v, _p, _i, _i64, _d = ctypes.c_void_p, ctypes.POINTER, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 _dp = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -50,6 +60,7 @@ SIGNATURES = {
     "rk_partition": (_i, [_i64, _i, _i, _i64p, _i64p]),
     "rk_tableau": (_i, [_i, _dp, _dp, _dp, _dp, _ip, _ip, _ip]),
     "rk_controller": (_i, [_i, _d, _dp, _ip]),
+    "rk_halo_plan_get": (_i, [_i, _i, _p(HaloPlan)]),
     "rk_nccl_unique_id": (_i, [_v]),
     "rk_ctx_create": (_i, [_i, _i, _i, _v, _v, _p(_v)]),
     "rk_ctx_destroy": (_i, [_v]),

@@ -33,6 +33,20 @@ def _stream_handle(stream) -> int | None:
     return h if h != 0 else 1
 
 
+def broadcast_unique_id(group=None, device: int | None = None) -> bytes:
+    """Rank 0 creates the NCCL unique id (rk_nccl_unique_id); every rank of the torch process
+    group receives the same 128 bytes (plumbing for rk_ctx_create, world > 1)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.zeros(_native.UNIQUE_ID_BYTES, dtype=torch.uint8)
+    if dist.get_rank(group) == 0:
+        t[:] = torch.frombuffer(bytearray(Context.nccl_unique_id()), dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda(device)
+    dist.broadcast(t, src=0, group=group)
+    return bytes(t.cpu().numpy().tobytes())
+
+
 class Context:
     """One per rank (one process per device).  world > 1 needs the NCCL unique id,
     which ``Context.from_torch_distributed`` broadcasts over the torch process group."""
@@ -62,18 +76,9 @@ class Context:
 
     @classmethod
     def from_torch_distributed(cls, device: int, stream=None, group=None) -> "Context":
-        import torch
         import torch.distributed as dist
         rank, world = dist.get_rank(group), dist.get_world_size(group)
-        uid = None
-        if world > 1:
-            t = torch.zeros(_native.UNIQUE_ID_BYTES, dtype=torch.uint8)
-            if rank == 0:
-                t[:] = torch.frombuffer(bytearray(cls.nccl_unique_id()), dtype=torch.uint8)
-            if dist.get_backend(group) == "nccl":
-                t = t.cuda(device)
-            dist.broadcast(t, src=0, group=group)
-            uid = bytes(t.cpu().numpy().tobytes())
+        uid = broadcast_unique_id(group, device) if world > 1 else None
         return cls(rank, world, device, stream, uid)
 
     def grid(self, nx: int, ny: int, nz: int, ncomp: int = 2) -> "State":
@@ -230,6 +235,15 @@ def tableau(scheme) -> dict:
     n = s.value
     return {"s": n, "a": [[a[i * n + j] for j in range(n)] for i in range(n)], "b": list(b[:n]),
             "e": list(e[:n]), "c": list(c[:n]), "order": o.value, "err_order": eo.value}
+
+
+def halo_plan(world: int, rank: int) -> dict:
+    """The library's per-stage halo exchange plan for `rank` (rk_halo_plan_get)."""
+    p = _native.HaloPlan()
+    call("rk_halo_plan_get", world, rank, ctypes.byref(p))
+    return {"up": p.up, "down": p.down,
+            "msgs": [{"recv": bool(m.recv), "peer": m.peer, "slot": m.slot, "nplanes": m.nplanes}
+                     for m in p.msg[:p.nmsg]]}
 
 
 def controller(scheme, E: float, dt: float):

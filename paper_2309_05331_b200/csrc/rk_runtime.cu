@@ -398,28 +398,23 @@ static rk_status halo_exchange(rk_state st) {
         e1 = pool_event(st);
         CK_CTX(ctx, cudaEventRecord(e0, ctx->comm));
     }
-    double* send_lo = st->sendbuf;
-    double* send_hi = st->sendbuf + pv;
-    double* ghost_hi = st->ghostbuf;
-    double* ghost_lo = st->ghostbuf + pv;
+    rk_halo_plan plan;
+    TRY(rk_halo_plan_get(ctx->world, ctx->rank, &plan));
     if (ctx->world == 1) {
-        // loopback: my lower neighbour is myself: ghost_lo <- my hi plane, ghost_hi <- my lo
-        CK_CTX(ctx, cudaMemcpyAsync(st->ghostbuf, st->sendbuf, sizeof(double) * 2 * pv,
-                                    cudaMemcpyDeviceToDevice, ctx->comm));
+        // loopback self-exchange: my lower neighbour is myself (ghost_lo <- my hi plane)
+        const rk_halo_msg& m = plan.msg[0];
+        CK_CTX(ctx, cudaMemcpyAsync(st->ghostbuf + m.slot * pv, st->sendbuf + m.slot * pv,
+                                    sizeof(double) * m.nplanes * pv, cudaMemcpyDeviceToDevice,
+                                    ctx->comm));
     } else {
-        const int up = (ctx->rank + 1) % ctx->world;
-        const int down = (ctx->rank - 1 + ctx->world) % ctx->world;
         NK_CTX(ctx, ncclGroupStart());
-        if (up == down) {
-            // world == 2: both neighbours are one peer; one message each way,
-            // [lo|hi] lands in the peer's [ghost_hi|ghost_lo]
-            NK_CTX(ctx, ncclSend(st->sendbuf, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->comm));
-            NK_CTX(ctx, ncclRecv(st->ghostbuf, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->comm));
-        } else {
-            NK_CTX(ctx, ncclSend(send_hi, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->comm));
-            NK_CTX(ctx, ncclSend(send_lo, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->comm));
-            NK_CTX(ctx, ncclRecv(ghost_lo, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->comm));
-            NK_CTX(ctx, ncclRecv(ghost_hi, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->comm));
+        for (int i = 0; i < plan.nmsg; ++i) {
+            const rk_halo_msg& m = plan.msg[i];
+            const size_t cnt = (size_t)(m.nplanes * pv);
+            if (m.recv)
+                NK_CTX(ctx, ncclRecv(st->ghostbuf + m.slot * pv, cnt, ncclDouble, m.peer, ctx->nccl, ctx->comm));
+            else
+                NK_CTX(ctx, ncclSend(st->sendbuf + m.slot * pv, cnt, ncclDouble, m.peer, ctx->nccl, ctx->comm));
         }
         NK_CTX(ctx, ncclGroupEnd());
     }
@@ -644,6 +639,28 @@ rk_status rk_controller(rk_scheme scheme, double E, double* dt, int* accepted) {
     if (C.err_order == 0) return fail(RK_ERR_UNSUPPORTED, "scheme has no error estimate");
     if (std::isnan(E)) return fail(RK_ERR_DIVERGED, "NaN error ratio");
     *accepted = step_adjust(E, C.order, C.err_order, dt) ? 1 : 0;
+    return RK_OK;
+}
+
+rk_status rk_halo_plan_get(int world, int rank, rk_halo_plan* out) {
+    if (!out || world < 1 || rank < 0 || rank >= world) return fail(RK_ERR_ARG, "rk_halo_plan_get: bad arguments");
+    rk_halo_plan p{};
+    p.up = (rank + 1) % world;
+    p.down = (rank - 1 + world) % world;
+    if (world <= 2) {
+        // one peer is both neighbours: [lo|hi] lands in its [ghost_hi|ghost_lo]
+        // (its plane above my top is my lowest plane, its plane below its bottom my top one)
+        p.nmsg = 2;
+        p.msg[0] = {0, p.up, 0, 2};
+        p.msg[1] = {1, p.up, 0, 2};
+    } else {
+        p.nmsg = 4;
+        p.msg[0] = {0, p.up, 1, 1};    // my top plane      -> up's ghost_lo
+        p.msg[1] = {0, p.down, 0, 1};  // my bottom plane   -> down's ghost_hi
+        p.msg[2] = {1, p.down, 1, 1};  // ghost_lo (z = -1) <- down's top plane
+        p.msg[3] = {1, p.up, 0, 1};    // ghost_hi (z=nzl)  <- up's bottom plane
+    }
+    *out = p;
     return RK_OK;
 }
 
