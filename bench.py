@@ -175,16 +175,20 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
-    ap.add_argument("--no-extra", action="store_true", help="skip the RK4 / e2e / CPU legs")
-    ap.add_argument("--overlap", type=int, default=1)
+    ap.add_argument("--legs", default="adaptive,rk4,e2e,cpu",
+                    help="comma list of legs (profiling runs use e.g. --legs rk4)")
+    ap.add_argument("--no-extra", action="store_true", help="same as --legs adaptive")
+    ap.add_argument("--overlap", type=int, default=1, help="halo exchange overlapped (N > 1)")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference" or os.environ.get("BENCH_ALLOW_SHORT")
+    legs = set(args.legs.split(","))
+    if args.no_extra:
+        legs = {"adaptive"}
 
     rank, world, local = dist_setup()
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -210,6 +214,9 @@ def main():
     st.set(u0_dev)
     cells_local = n * n * st.local
     cells_total = n * n * nzg
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    peak, peak_src = peaks()
+    traffic = ncu_traffic() or {}
 
     def barrier():
         if world > 1:
@@ -222,6 +229,13 @@ def main():
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    def halo_of(s):
+        if world == 1 or not s["halo_exchanges"]:
+            return None
+        return {"exchanges": s["halo_exchanges"], "ms_per_exchange": s["halo_ms"] / s["halo_exchanges"],
+                "bytes_per_exchange": s["halo_bytes"] / s["halo_exchanges"],
+                "nvlink_gbs": (s["halo_bytes"] / (s["halo_ms"] / 1e3) / 1e9) if s["halo_ms"] else None}
 
     # ---- headline: DOPRI5 adaptive, one accepted step per "step" ---------------------
     state = {"t": 0.0, "dt": 1.0}
@@ -237,71 +251,65 @@ def main():
                 return tries
             state["dt"] = dtn
 
-    for _ in range(args.warmup):
-        adaptive_step()
-    st.set_option(rk.OPT_TIMING, 1)
-    st.reset_stats()
-    barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tries = 0
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            tries += adaptive_step()
-        ev1.record(stream)
+    def adaptive_leg():
+        st.set(u0_dev)
+        state["t"], state["dt"] = 0.0, 1.0
+        for _ in range(args.warmup):
+            adaptive_step()
+        st.set_option(rk.OPT_TIMING, 1)
+        st.reset_stats()
         barrier()
-    ms = max_over_ranks(ev0.elapsed_time(ev1))
-    s = st.stats()
-    st.set_option(rk.OPT_TIMING, 0)
-    value = cells_total * args.steps / (ms / 1e3)
-    peak, peak_src = peaks()
-    k_ms = s["stage_kernel_ms"]
-    achieved = s["stage_bytes"] / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
-    traffic = ncu_traffic()
-    step_bytes = s["stage_bytes"] / max(1, s["tries"])
-    halo = None
-    if world > 1 and s["halo_exchanges"]:
-        halo = {"exchanges": s["halo_exchanges"], "ms_total": s["halo_ms"],
-                "ms_per_exchange": s["halo_ms"] / s["halo_exchanges"],
-                "bytes_per_exchange": s["halo_bytes"] / s["halo_exchanges"],
-                "nvlink_gbs": (s["halo_bytes"] / (s["halo_ms"] / 1e3) / 1e9) if s["halo_ms"] else None}
+        tries = 0
+        with ClockSampler(local) as clk:
+            ev0.record(stream)
+            for _ in range(args.steps):
+                tries += adaptive_step()
+            ev1.record(stream)
+            barrier()
+        ms = max_over_ranks(ev0.elapsed_time(ev1))
+        s = st.stats()
+        st.set_option(rk.OPT_TIMING, 0)
+        k_ms = s["stage_kernel_ms"]
+        achieved = s["stage_bytes"] / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
+        step_bytes = s["stage_bytes"] / max(1, s["tries"])
+        line = {
+            "metric": "gray_scott_cell_updates_per_s",
+            "value": cells_total * args.steps / (ms / 1e3),
+            "unit": "cell-updates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded Gray-Scott IC, DESIGN.md R-6)",
+            "config": {"workload": "gray_scott_dopri5_adaptive_512^3_per_gpu", "nx": n, "ny": n,
+                       "nz_global": nzg, "nz_per_gpu": int(st.local), "h": H, "atol": TOL,
+                       "rtol": TOL, "scheme": "dopri5 (FSAL, error-controlled)", "tries": tries,
+                       "halo_overlap": bool(args.overlap),
+                       "l2": "no flush: every array is 2 GiB per GPU, >> 126 MB L2",
+                       "parallelism": f"z-slab x{world} (NCCL send/recv halos + allreduce max)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": traffic.get("dopri5_adaptive", {}).get("bytes_per_launch"),
+                         "kernel": "gs_stage_kernel (K3: fused stage value + 7-pt stencil + "
+                                   "reaction + epilogue), all stage launches of the timed tries",
+                         "algorithmic_bytes_per_launch": s["stage_bytes"] / max(1, s["stage_launches"]),
+                         "algorithmic_bytes_per_cell_try": step_bytes / cells_local,
+                         "avg_launch_ms": k_ms / max(1, s["stage_launches"]),
+                         "launches": s["stage_launches"], "peak_source": peak_src},
+            "gpu_launches": s["kernel_launches"],
+            "clocks": getattr(clk, "result", None),
+        }
+        h = halo_of(s)
+        if h:
+            line["halo"] = h
+        return line
 
-    line = {
-        "metric": "gray_scott_cell_updates_per_s",
-        "value": value,
-        "unit": "cell-updates/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": ms / args.steps,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic (seeded Gray-Scott IC, DESIGN.md R-6)",
-        "config": {"workload": "gray_scott_dopri5_adaptive_512^3_per_gpu", "nx": n, "ny": n,
-                   "nz_global": nzg, "nz_per_gpu": int(st.local), "h": H, "atol": TOL, "rtol": TOL,
-                   "scheme": "dopri5 (FSAL, error-controlled)", "tries": tries,
-                   "halo_overlap": bool(args.overlap),
-                   "l2": "no flush: every array is 2 GiB per GPU, >> 126 MB L2",
-                   "parallelism": f"z-slab x{world} (NCCL send/recv halos + allreduce max)"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic.get("dopri5_bytes_per_launch") if traffic else None,
-                     "kernel": "gs_stage_kernel (K3, fused stage value + 7-pt stencil + "
-                               "reaction + epilogue)",
-                     "algorithmic_bytes_per_try": step_bytes,
-                     "algorithmic_bytes_per_cell_try": step_bytes / cells_local,
-                     "avg_launch_ms": k_ms / max(1, s["stage_launches"]),
-                     "launches": s["stage_launches"], "peak_source": peak_src},
-        "gpu_launches": s["kernel_launches"],
-    }
-    if halo:
-        line["halo"] = halo
-    line["clocks"] = getattr(clk, "result", None)
-
-    if not args.no_extra:
-        # ---- RK4 fixed step (north_star: RK4 and DOPRI5 at 512^3) -------------------------
+    def rk4_leg(overlap: int):
+        st.set_option(rk.OPT_HALO_OVERLAP, overlap)
         st.set(u0_dev)
         for _ in range(args.warmup):
             st.do_step("rk4", 0.0, 1.0)
@@ -316,39 +324,55 @@ def main():
         ms4 = max_over_ranks(ev0.elapsed_time(ev1))
         s4 = st.stats()
         st.set_option(rk.OPT_TIMING, 0)
+        st.set_option(rk.OPT_HALO_OVERLAP, args.overlap)
         a4 = s4["stage_bytes"] / (s4["stage_kernel_ms"] / 1e3) / 1e9 if s4["stage_kernel_ms"] else None
-        line["extra"] = {"rk4": {
-            "value": cells_total * args.steps / (ms4 / 1e3), "ms_per_step": ms4 / args.steps,
-            "roofline": {"bound": "hbm", "achieved": a4, "peak": peak, "unit": "GB/s",
-                         "frac": a4 / peak if a4 else None,
-                         "traffic": traffic.get("rk4_bytes_per_launch") if traffic else None,
-                         "algorithmic_bytes_per_cell_step": s4["stage_bytes"] / args.steps / cells_local,
-                         "avg_launch_ms": s4["stage_kernel_ms"] / max(1, s4["stage_launches"])},
-            "gpu_launches": s4["kernel_launches"]}}
+        out = {"value": cells_total * args.steps / (ms4 / 1e3), "ms_per_step": ms4 / args.steps,
+               "halo_overlap": bool(overlap),
+               "roofline": {"bound": "hbm", "achieved": a4, "peak": peak, "unit": "GB/s",
+                            "frac": a4 / peak if a4 else None,
+                            "traffic": traffic.get("rk4", {}).get("bytes_per_launch"),
+                            "algorithmic_bytes_per_cell_step": s4["stage_bytes"] / args.steps / cells_local,
+                            "avg_launch_ms": s4["stage_kernel_ms"] / max(1, s4["stage_launches"])},
+               "gpu_launches": s4["kernel_launches"]}
+        h = halo_of(s4)
+        if h:
+            out["halo"] = h
+        return out
 
-        # ---- e2e: through the C-ABI with HOST buffers, copies inside the timed region ----
+    def e2e_leg():
+        # the same metric through the C-ABI with HOST buffers: every step copies the state in
+        # (pinned H2D) and the result out (pinned D2H) inside the timed region
         host_in = torch.from_numpy(u0).pin_memory()
         host_out = torch.empty_like(host_in).pin_memory()
-        state["t"], state["dt"] = 0.0, 1.0
         st.set(host_in)
-        for _ in range(1):
-            adaptive_step()
+        state["t"], state["dt"] = 0.0, 1.0
+        adaptive_step()
         ke = max(1, min(args.steps, 5))
         barrier()
         ev0.record(stream)
         for _ in range(ke):
-            st.set(host_in)            # H2D of the step's input state (pinned)
-            adaptive_step()            # includes the 8-byte error-ratio D2H per try
-            st.get(host_out)           # D2H of the step's result state (pinned)
+            st.set(host_in)   # H2D of the step's input state
+            adaptive_step()   # includes the 8-byte error-ratio D2H per try
+            st.get(host_out)  # D2H of the step's result
         ev1.record(stream)
         barrier()
         mse = max_over_ranks(ev0.elapsed_time(ev1))
-        nbytes = u0.nbytes
-        line["e2e"] = {"value": cells_total * ke / (mse / 1e3), "unit": "cell-updates/s",
-                       "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes + 8,
-                       "steps": ke, "ms_per_step": mse / ke}
-        if rank == 0 and world == 1:
-            line["cpu_baseline"] = cpu_baseline()
+        return {"value": cells_total * ke / (mse / 1e3), "unit": "cell-updates/s",
+                "h2d_bytes_per_step": u0.nbytes, "d2h_bytes_per_step": u0.nbytes + 8,
+                "steps": ke, "ms_per_step": mse / ke}
+
+    line = adaptive_leg() if "adaptive" in legs else {}
+    extra = {}
+    if "rk4" in legs:
+        extra["rk4"] = rk4_leg(args.overlap)
+        if world > 1:
+            extra["rk4_overlap_off"] = rk4_leg(0)
+    if extra:
+        line["extra"] = extra
+    if "e2e" in legs:
+        line["e2e"] = e2e_leg()
+    if "cpu" in legs and rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline()
     if rank == 0:
         print(json.dumps(line), flush=True)
     st.close()
