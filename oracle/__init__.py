@@ -21,8 +21,9 @@ _SRC = os.path.join(_HERE, "rk_oracle.c")
 _HDR = os.path.join(_HERE, "rk_oracle.h")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-EULER, RK4, CASH_KARP54, DOPRI5 = 0, 1, 2, 3
-SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5}
+EULER, RK4, CASH_KARP54, DOPRI5, RKF78 = 0, 1, 2, 3, 4
+SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5,
+           "rkf78": RKF78}
 RHS_EXP, RHS_LOGISTIC, RHS_GRAY_SCOTT = 0, 1, 2
 OK, ERR_ARG, ERR_UNSUPPORTED, ERR_DIVERGED, ERR_STALL = 0, 1, 2, 3, 4
 
@@ -116,7 +117,7 @@ def _arr(u) -> np.ndarray:
 
 def tableau(scheme: int) -> dict:
     """The oracle's Butcher tableau as exact Fractions (for the order-condition pins)."""
-    S = 7
+    S = 13
     bufs = [(ctypes.c_int64 * (S * S))() for _ in range(2)] + \
            [(ctypes.c_int64 * S)() for _ in range(6)]
     order, err_order = ctypes.c_int(), ctypes.c_int()

@@ -26,7 +26,7 @@
  * typed here independently of the CUDA library's copy.
  * --------------------------------------------------------------------------- */
 typedef struct { int64_t n, d; } rat;
-#define MAXS 7
+#define MAXS 13
 typedef struct {
     int s, order, err_order, has_err;
     rat c[MAXS];
@@ -81,12 +81,35 @@ static const tableau TAB_DOPRI5 = {
     {{5179, 57600}, {0, 1}, {7571, 16695}, {393, 640}, {-92097, 339200}, {187, 2100}, {1, 40}},
 };
 
+/* Runge–Kutta–Fehlberg 7(8) (Fehlberg 1968).  b = 8th-order weights
+ * (propagated, R-11), bh = 7th-order embedded weights. */
+static const tableau TAB_RKF78 = {
+    13, 8, 7, 1,
+    {{0, 1}, {2, 27}, {1, 9}, {1, 6}, {5, 12}, {1, 2}, {5, 6}, {1, 6}, {2, 3}, {1, 3}, {1, 1}, {0, 1}, {1, 1}},
+    {{{0, 1}},
+     {{2, 27}},
+     {{1, 36}, {1, 12}},
+     {{1, 24}, {0, 1}, {1, 8}},
+     {{5, 12}, {0, 1}, {-25, 16}, {25, 16}},
+     {{1, 20}, {0, 1}, {0, 1}, {1, 4}, {1, 5}},
+     {{-25, 108}, {0, 1}, {0, 1}, {125, 108}, {-65, 27}, {125, 54}},
+     {{31, 300}, {0, 1}, {0, 1}, {0, 1}, {61, 225}, {-2, 9}, {13, 900}},
+     {{2, 1}, {0, 1}, {0, 1}, {-53, 6}, {704, 45}, {-107, 9}, {67, 90}, {3, 1}},
+     {{-91, 108}, {0, 1}, {0, 1}, {23, 108}, {-976, 135}, {311, 54}, {-19, 60}, {17, 6}, {-1, 12}},
+     {{2383, 4100}, {0, 1}, {0, 1}, {-341, 164}, {4496, 1025}, {-301, 82}, {2133, 4100}, {45, 82}, {45, 164}, {18, 41}},
+     {{3, 205}, {0, 1}, {0, 1}, {0, 1}, {0, 1}, {-6, 41}, {-3, 205}, {-3, 41}, {3, 41}, {6, 41}, {0, 1}},
+     {{-1777, 4100}, {0, 1}, {0, 1}, {-341, 164}, {4496, 1025}, {-289, 82}, {2193, 4100}, {51, 82}, {33, 164}, {12, 41}, {0, 1}, {1, 1}}},
+    {{0, 1}, {0, 1}, {0, 1}, {0, 1}, {0, 1}, {34, 105}, {9, 35}, {9, 35}, {9, 280}, {9, 280}, {0, 1}, {41, 840}, {41, 840}},
+    {{41, 840}, {0, 1}, {0, 1}, {0, 1}, {0, 1}, {34, 105}, {9, 35}, {9, 35}, {9, 280}, {9, 280}, {41, 840}, {0, 1}, {0, 1}},
+};
+
 static const tableau* get_tableau(int scheme) {
     switch (scheme) {
     case ORC_EULER: return &TAB_EULER;
     case ORC_RK4: return &TAB_RK4;
     case ORC_CASH_KARP54: return &TAB_CK54;
     case ORC_DOPRI5: return &TAB_DOPRI5;
+    case ORC_RKF78: return &TAB_RKF78;
     default: return NULL;
     }
 }

@@ -27,7 +27,7 @@ extern "C" {
 #endif
 
 /* Schemes of Table 1 on the hot path. */
-enum { ORC_EULER = 0, ORC_RK4 = 1, ORC_CASH_KARP54 = 2, ORC_DOPRI5 = 3 };
+enum { ORC_EULER = 0, ORC_RK4 = 1, ORC_CASH_KARP54 = 2, ORC_DOPRI5 = 3, ORC_RKF78 = 4 };
 /* RHS kinds: Eq. 1a as du/dt = lambda*u, Eq. 1b, Eq. 3 / Listing 2. */
 enum { ORC_RHS_EXP = 0, ORC_RHS_LOGISTIC = 1, ORC_RHS_GRAY_SCOTT = 2 };
 /* Status codes. */
@@ -44,7 +44,7 @@ typedef struct {
 } orc_problem;
 
 /* Tableau access for tests: exact rationals as (num, den) int64 pairs.
- * a is s*s row-major (strictly lower triangular), b/bhat/c length s.  bhat is all
+ * a is s*s row-major (strictly lower triangular), b/bhat/c length s (s <= 13).  bhat is all
  * zero for schemes without an embedded solution.  Returns s, or -1 for bad scheme. */
 int orc_tableau(int scheme, int64_t* a_num, int64_t* a_den, int64_t* b_num, int64_t* b_den,
                 int64_t* bh_num, int64_t* bh_den, int64_t* c_num, int64_t* c_den,

@@ -108,3 +108,14 @@ def test_adaptive_hits_t1_exactly():
         u, acc, rej, rc = oracle.integrate_adaptive(p, oracle.DOPRI5, [1.0], 0.0, 1.0, dt0,
                                                     1e-10, 1e-10)
         assert rc == 0 and abs(u[0] - math.exp(-1.0)) < 1e-8
+
+
+def test_rkf78_adaptive_meets_tolerance():
+    """RKF78 error-controlled (stepper order 8, error order 7, R-12) on Eq. 1b:
+    reaches t1 exactly, final error <= 100*tol, rejections recover."""
+    u0 = rk_inputs.logistic_u0(1, -5.0, shifted=False)
+    for tol in (1e-6, 1e-8, 1e-10):
+        u, acc, rej, rc = oracle.integrate_adaptive(oracle.logistic_problem(1), oracle.RKF78, u0,
+                                                    -5.0, 5.0, 0.1, tol, tol)
+        assert rc == oracle.OK and acc > 0
+        assert abs(u[0] - 1.0 / (1.0 + math.exp(-5.0))) <= 100 * tol

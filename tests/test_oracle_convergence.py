@@ -87,3 +87,37 @@ def test_final_time_superconvergence_is_real():
     fin = [run_traj(p, oracle.DOPRI5, exact(-5.0), -5.0, 5.0, 0.5 * 2.0 ** -k, exact)[1]
            for k in range(1, 5)]
     assert local_orders(fin)[-1] > 5.6
+
+
+# ---- Runge–Kutta–Fehlberg 7(8) (Table 1) -------------------------
+def _assert_order_tol(errs, p, tol, floor):
+    ords = local_orders(errs)
+    good = [abs(o - p) <= tol and errs[i + 1] > floor for i, o in enumerate(ords)]
+    assert any(good[i] and good[i + 1] for i in range(len(good) - 1)), (p, ords, errs)
+
+
+def test_rkf78_orders():
+    """Order 8 (S:L512 allows 8 +- 0.8; gated here at +-0.5 on two consecutive pairs) on
+    Eq. 1b, the Eq. 1a family and the decay problem, dt halving from 2.5 (or 2)."""
+    p = oracle.logistic_problem(1)
+    exact = lambda t: np.array([1.0 / (1.0 + math.exp(-t))])
+    errs = [run_traj(p, oracle.RKF78, exact(-5.0), -5.0, 5.0, 2.5 * 2.0 ** -k, exact)[0] for k in range(5)]
+    _assert_order_tol(errs, 8, 0.5, 5e-14)
+    u0 = rk_inputs.exp_family_u0(16, -5.0)
+    A = u0 * math.exp(5.0)
+    pe = oracle.exp_problem(u0.size, 1.0)
+    errs = [run_traj(pe, oracle.RKF78, u0, -5.0, 5.0, 2.5 * 2.0 ** -k, lambda t: A * math.exp(t))[0]
+            for k in range(5)]
+    _assert_order_tol(errs, 8, 0.5, 1e-10)
+    u0 = rk_inputs.exp_decay_u0(100)
+    pd = oracle.exp_problem(u0.size, -1.0)
+    errs = [run_traj(pd, oracle.RKF78, u0, 0.0, 4.0, 2.0 * 2.0 ** -k, lambda t: u0 * math.exp(-t))[0]
+            for k in range(5)]
+    _assert_order_tol(errs, 8, 0.5, 5e-15)
+
+
+def test_rkf78_roundoff_floor():
+    """at the finest dt, RKF78's L-inf error on the sigmoid is <= 1e-12."""
+    p = oracle.logistic_problem(1)
+    exact = lambda t: np.array([1.0 / (1.0 + math.exp(-t))])
+    assert run_traj(p, oracle.RKF78, exact(-5.0), -5.0, 5.0, 2.0 ** -6, exact)[0] <= 1e-12

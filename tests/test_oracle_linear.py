@@ -88,3 +88,36 @@ def test_zero_rhs_fixed_point(scheme):
     else:
         un = oracle.step(p, scheme, 0.0, 0.7, u0)
     assert np.array_equal(un, u0)
+
+
+def _R_from_tableau(tab, w, z):
+    """R(z) = 1 + sum_k (w^T A^{k-1} 1) z^k, exact (the tableau itself is pinned by the
+    order conditions in test_oracle_tableau.py)."""
+    A, s = tab["a"], tab["s"]
+    v, out = [Fraction(1)] * s, Fraction(1)
+    for k in range(1, s + 1):
+        out += sum(w[i] * v[i] for i in range(s)) * z ** k
+        v = [sum(A[i][j] * v[j] for j in range(s)) for i in range(s)]
+    return out
+
+
+@pytest.mark.parametrize("lam,dt,n", [(-1.0, 0.1, 10), (1.0, 0.5, 20), (-3.0, 0.3, 7), (-1.0, 2.0, 3)])
+def test_rkf78_linear_closed_form(lam, dt, n):
+    """RKF78 step arithmetic (13 stages, 8th-order weights) vs u0*R(z)^n, and the embedded
+    error vs (R_b - R_bhat)(z)*u0."""
+    tab = oracle.tableau(oracle.RKF78)
+    u0 = np.array([1.0, 0.3, -2.5])
+    p = oracle.exp_problem(u0.size, lam)
+    z = Fraction(lam) * Fraction(dt)
+    R = _R_from_tableau(tab, tab["b"], z)
+    u = u0.copy()
+    for _ in range(n):
+        u = oracle.step(p, oracle.RKF78, 0.0, dt, u)
+    for i in range(u0.size):
+        exact = Fraction(u0[i]) * R ** n
+        assert abs(Fraction(u[i]) - exact) <= 8 * n * abs(float(exact)) * EPS + 1e-300
+    un, err = oracle.step(p, oracle.RKF78, 0.0, dt, u0, with_error=True)
+    E = R - _R_from_tableau(tab, tab["bhat"], z)
+    for i in range(u0.size):
+        scale = abs(u0[i]) * abs(lam) * dt * 8 * max(1.0, float(abs(R)))
+        assert abs(Fraction(err[i]) - E * Fraction(u0[i])) <= 16 * EPS * scale
