@@ -64,7 +64,7 @@ typedef enum {
 /* Table 1, the explicit one-step rows on the hot path.  CK54 and DOPRI5 are
  * used fixed-step (do_step / integrate_const) or error-controlled (integrate_adaptive),
  * reproducing both the "fixed" and "dynamic step size" rows of Table 1. */
-typedef enum { RK_EULER = 0, RK_RK4 = 1, RK_CASH_KARP54 = 2, RK_DOPRI5 = 3 } rk_scheme;
+typedef enum { RK_EULER = 0, RK_RK4 = 1, RK_CASH_KARP54 = 2, RK_DOPRI5 = 3, RK_FEHLBERG78 = 4 } rk_scheme;
 
 /* Options for rk_set_option. */
 typedef enum {
@@ -106,7 +106,7 @@ const char* rk_last_error(void);
 /* Partition rule above: rank's [begin, begin+count) of n_global items. */
 rk_status rk_partition(int64_t n_global, int world, int rank, int64_t* begin, int64_t* count);
 /* Library's Butcher tableau as doubles a[s*s], b[s], e[s] = b - bhat (exact rational rounded
- * once, R-11), c[s]; *s <= 7; *order, *err_order (0 if none). */
+ * once, R-11), c[s]; *s <= 13; *order, *err_order (0 if none). */
 rk_status rk_tableau(rk_scheme scheme, double* a, double* b, double* e, double* c, int* s,
                      int* order, int* err_order);
 /* Odeint default step adjuster (R-12/R-14) applied to E and *dt: returns 1 in

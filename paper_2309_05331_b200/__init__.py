@@ -4,7 +4,7 @@ block-distributed fp64 state (the hot path of arxiv 2309.05331, OpenFPM + Odeint
 The compute path is librkb200.so (hand-written sm_100a CUDA behind the C-ABI in
 include/rk_b200.h); this package is its thin ctypes binding.  There is no CPU fallback.
 """
-from .api import (CASH_KARP54, DOPRI5, EULER, RK4, SCHEMES, Context, State, controller,
+from .api import (CASH_KARP54, DOPRI5, EULER, FEHLBERG78, RK4, SCHEMES, Context, State, controller,
                   halo_plan, partition, tableau)
 from ._native import (OPT_HALO_LOOPBACK, OPT_HALO_OVERLAP, OPT_MAX_TRIES, OPT_TIMING,
                       OPT_USE_GRAPH, RKError, lib)

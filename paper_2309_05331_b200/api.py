@@ -15,8 +15,9 @@ import numpy as np
 from . import _native
 from ._native import Stats, call
 
-EULER, RK4, CASH_KARP54, DOPRI5 = 0, 1, 2, 3
-SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5}
+EULER, RK4, CASH_KARP54, DOPRI5, FEHLBERG78 = 0, 1, 2, 3, 4
+SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5,
+           "rkf78": FEHLBERG78}
 
 
 def _scheme(s) -> int:
@@ -227,7 +228,7 @@ def partition(n_global: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def tableau(scheme) -> dict:
-    S = 7
+    S = 13
     a, b, e, c = (ctypes.c_double * (S * S))(), (ctypes.c_double * S)(), (ctypes.c_double * S)(), \
         (ctypes.c_double * S)()
     s, o, eo = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()

@@ -18,9 +18,9 @@ enum RhsKind { RHS_NONE = -1, RHS_EXP = 0, RHS_LOGISTIC = 1, RHS_GRAY_SCOTT = 2 
 // ---------------------------------------------------------------------------------------
 // K1: pointwise step of a whole RK scheme in registers (vector states).
 struct PwCoef {
-    double g[7][7];    // dt * a_ij
-    double beta[7];    // dt * b_j
-    double delta[7];   // dt * (b_j - bhat_j)
+    double g[13][13];  // dt * a_ij
+    double beta[13];   // dt * b_j
+    double delta[13];  // dt * (b_j - bhat_j)
 };
 struct PwArgs {
     const double* u;

@@ -35,7 +35,7 @@ __device__ __forceinline__ double pw_steps(double x, const PwArgs& a, unsigned l
     constexpr int SE = s_eff(S, ERR);
     const int nsteps = ERR ? 1 : a.nsteps;
     for (int n = 0; n < nsteps; ++n) {
-        double k[7];
+        double k[13];
 #pragma unroll
         for (int i = 0; i < SE; ++i) {
             double y = x;
@@ -113,6 +113,7 @@ cudaError_t launch_pointwise(int scheme, const PwArgs& a, cudaStream_t st, int n
     case 1: return launch_s<1>(a, st, num_sms);
     case 2: return launch_s<2>(a, st, num_sms);
     case 3: return launch_s<3>(a, st, num_sms);
+    case 4: return launch_s<4>(a, st, num_sms);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -112,8 +112,8 @@ struct rk_state_s {
     GridGeom geo{};                  // padded periodic layout (grid states, rk_kernels.cuh)
     double* u = nullptr;
     double* u_new = nullptr;
-    double* k[7] = {nullptr};
-    CUtensorMap tm_u[2]{}, tm_unew[2]{}, tm_k[7][2]{};  // [0] tile+ring box, [1] interior box
+    double* k[13] = {nullptr};
+    CUtensorMap tm_u[2]{}, tm_unew[2]{}, tm_k[13][2]{};  // [0] tile+ring box, [1] interior box
     CUtensorMap tm_glo{}, tm_ghi{};
     int nk = 0;
     bool k1_valid = false;           // k[0] == F(u) for the current u
@@ -214,7 +214,7 @@ static rk_status resolve_timing(rk_state st) {
 // ------------------------------------------------------------------------------------
 struct Coeffs {
     int s = 0, order = 0, err_order = 0;
-    double a[7][7] = {{0}}, b[7] = {0}, e[7] = {0}, c[7] = {0};
+    double a[13][13] = {{0}}, b[13] = {0}, e[13] = {0}, c[13] = {0};
 };
 
 static Coeffs coeffs_of(int scheme) {
@@ -232,7 +232,7 @@ static Coeffs coeffs_of(int scheme) {
     return C;
 }
 
-static bool valid_scheme(int s) { return s >= RK_EULER && s <= RK_DOPRI5; }
+static bool valid_scheme(int s) { return s >= RK_EULER && s <= RK_FEHLBERG78; }
 
 struct StagePlan {
     int scheme = 0, adaptive = 0, stage = 0;

@@ -25,17 +25,17 @@ enum Epilogue {
     EPI_TAIL_ERR = 4      // Y = u_new (base); store k_i; e = e' + delta_i k_i; ratio max
 };
 
-constexpr int kMaxSlots = 5;
+constexpr int kMaxSlots = 10;  // RKF78 adaptive final stage: k1, k4..k12
 constexpr int SLOT_U = -1;  // slot source: the state u itself (TAIL stage: old u)
 
 struct StageSpec {
     int valid = 0;
     int epi = EPI_K;
     int nslots = 0;
-    int src[kMaxSlots] = {0, 0, 0, 0, 0};  // k index (>= 0) or SLOT_U
+    int src[kMaxSlots] = {};               // k index (>= 0) or SLOT_U
     bool halo[kMaxSlots] = {};             // slot enters Y (needs the periodic ring)
     bool gnz[kMaxSlots] = {}, bnz[kMaxSlots] = {}, dnz[kMaxSlots] = {};
-    int j[kMaxSlots] = {0, 0, 0, 0, 0};    // stage index of the slot (coefficients)
+    int j[kMaxSlots] = {};                 // stage index of the slot (coefficients)
     bool bnew = false, dnew = false;       // beta_i / delta_i nonzero
     int out_k = -1;                        // k buffer written (EPI_K, EPI_FINAL_EPART e', TAIL k_s)
     bool writes_u = false;                 // stores u_new

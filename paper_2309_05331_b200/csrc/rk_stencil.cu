@@ -48,13 +48,15 @@ constexpr int OWN_BOX = TY * OWN_ROW;
 constexpr int OWN_BYTES = 2 * OWN_BOX * 8;
 constexpr int NHALO = BOX - NT;                           // ring positions (84)
 constexpr int SMEM_BUDGET = 110 * 1024;                   // 2 CTAs per SM
+constexpr int SMEM_BUDGET_1 = 226 * 1024;                 // 1 CTA per SM (wide RKF78 stages)
 static_assert(NHALO <= NT, "one ring position per thread");
 
 struct Layout {
-    int off[kMaxSlots] = {0, 0, 0, 0, 0};  // byte offset of slot s inside a ring stage
-    int stage_bytes = 0;                   // one ring stage (base + slots)
-    int tx_bytes = 0;                      // TMA bytes landing per non-ghost plane
-    int R = 2;                             // ring depth
+    int off[kMaxSlots] = {};  // byte offset of slot s inside a ring stage
+    int stage_bytes = 0;      // one ring stage (base + slots)
+    int tx_bytes = 0;         // TMA bytes landing per non-ghost plane
+    int R = 2;                // ring depth
+    int minb = 2;             // CTAs per SM the layout is sized for (__launch_bounds__)
     int smem = 0;
 };
 
@@ -69,11 +71,18 @@ __host__ __device__ constexpr Layout layout_of(const StageSpec& P) {
     L.stage_bytes = o;
     L.tx_bytes = tx;
     int R = (SMEM_BUDGET - 2 * HALO_SLOT - 64) / o;
+    if (R < 2) {  // too wide for 2 CTAs per SM: one CTA with a deeper ring
+        L.minb = 1;
+        R = (SMEM_BUDGET_1 - 2 * HALO_SLOT - 64) / o;
+    }
     R = R > 4 ? 4 : (R < 2 ? 2 : R);
     L.R = R;
     L.smem = R * o + 2 * HALO_SLOT + R * 8;
     return L;
 }
+
+template <int S, int AD, int I>
+constexpr int kMinBlocks = layout_of(stage_spec(S, AD != 0, I)).minb;
 
 // ---- PTX wrappers -------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -141,7 +150,7 @@ __host__ __device__ constexpr bool has_prev_e(const StageSpec& P) {
 }
 
 template <int S, int AD, int I>
-__global__ void __launch_bounds__(NT, 2) gs_stage_kernel(const __grid_constant__ GsStageArgs a) {
+__global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(const __grid_constant__ GsStageArgs a) {
     constexpr StageSpec P = stage_spec(S, AD != 0, I);
     constexpr Layout LY = layout_of(P);
     constexpr int NS = P.nslots, EPI = P.epi, R = LY.R;
@@ -450,6 +459,12 @@ cudaError_t launch_stage_i(int i, const GsStageArgs& a, dim3 grid, cudaStream_t 
     case 4: return launch_norm<S, AD, 4>(a, grid, st);
     case 5: return launch_norm<S, AD, 5>(a, grid, st);
     case 6: return launch_norm<S, AD, 6>(a, grid, st);
+    case 7: return launch_norm<S, AD, 7>(a, grid, st);
+    case 8: return launch_norm<S, AD, 8>(a, grid, st);
+    case 9: return launch_norm<S, AD, 9>(a, grid, st);
+    case 10: return launch_norm<S, AD, 10>(a, grid, st);
+    case 11: return launch_norm<S, AD, 11>(a, grid, st);
+    case 12: return launch_norm<S, AD, 12>(a, grid, st);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -525,6 +540,8 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
     case 5: return launch_stage_i<2, 1>(stage, a, grid, st);
     case 6: return launch_stage_i<3, 0>(stage, a, grid, st);
     case 7: return launch_stage_i<3, 1>(stage, a, grid, st);
+    case 8: return launch_stage_i<4, 0>(stage, a, grid, st);
+    case 9: return launch_stage_i<4, 1>(stage, a, grid, st);
     default: return cudaErrorInvalidValue;
     }
 }
@@ -540,6 +557,11 @@ cudaError_t launch_gs_pack(const GsStageArgs& a, double* send, cudaStream_t st) 
     case 3: gs_pack_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
     case 4: gs_pack_kernel<4><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
     case 5: gs_pack_kernel<5><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
+    case 6: gs_pack_kernel<6><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
+    case 7: gs_pack_kernel<7><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
+    case 8: gs_pack_kernel<8><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
+    case 9: gs_pack_kernel<9><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
+    case 10: gs_pack_kernel<10><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

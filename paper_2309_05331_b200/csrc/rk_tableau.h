@@ -17,10 +17,10 @@ struct Tableau {
     int s;          // stages
     int order;      // order of the propagated (b) solution
     int err_order;  // order of the embedded (bhat) solution, 0 if none
-    Rat c[7];
-    Rat a[7][7];    // strictly lower triangular
-    Rat b[7];
-    Rat bh[7];
+    Rat c[13];
+    Rat a[13][13];  // strictly lower triangular
+    Rat b[13];
+    Rat bh[13];
 };
 
 __host__ __device__ constexpr Tableau tableau_of(int scheme) {
@@ -56,6 +56,29 @@ __host__ __device__ constexpr Tableau tableau_of(int scheme) {
                         {{35, 384}, {0, 1}, {500, 1113}, {125, 192}, {-2187, 6784}, {11, 84}}},
                        {{35, 384}, {0, 1}, {500, 1113}, {125, 192}, {-2187, 6784}, {11, 84}, {0, 1}},
                        {{5179, 57600}, {0, 1}, {7571, 16695}, {393, 640}, {-92097, 339200}, {187, 2100}, {1, 40}}};
+    case 4:  // Runge–Kutta–Fehlberg 7(8): b = 8th order (propagated), bh = 7th
+        return Tableau{
+            13, 8, 7,
+            {{0, 1}, {2, 27}, {1, 9}, {1, 6}, {5, 12}, {1, 2}, {5, 6}, {1, 6}, {2, 3}, {1, 3}, {1, 1}, {0, 1}, {1, 1}},
+            {{},
+             {{2, 27}},
+             {{1, 36}, {1, 12}},
+             {{1, 24}, {0, 1}, {1, 8}},
+             {{5, 12}, {0, 1}, {-25, 16}, {25, 16}},
+             {{1, 20}, {0, 1}, {0, 1}, {1, 4}, {1, 5}},
+             {{-25, 108}, {0, 1}, {0, 1}, {125, 108}, {-65, 27}, {125, 54}},
+             {{31, 300}, {0, 1}, {0, 1}, {0, 1}, {61, 225}, {-2, 9}, {13, 900}},
+             {{2, 1}, {0, 1}, {0, 1}, {-53, 6}, {704, 45}, {-107, 9}, {67, 90}, {3, 1}},
+             {{-91, 108}, {0, 1}, {0, 1}, {23, 108}, {-976, 135}, {311, 54}, {-19, 60}, {17, 6}, {-1, 12}},
+             {{2383, 4100}, {0, 1}, {0, 1}, {-341, 164}, {4496, 1025}, {-301, 82}, {2133, 4100}, {45, 82},
+              {45, 164}, {18, 41}},
+             {{3, 205}, {0, 1}, {0, 1}, {0, 1}, {0, 1}, {-6, 41}, {-3, 205}, {-3, 41}, {3, 41}, {6, 41}, {0, 1}},
+             {{-1777, 4100}, {0, 1}, {0, 1}, {-341, 164}, {4496, 1025}, {-289, 82}, {2193, 4100}, {51, 82},
+              {33, 164}, {12, 41}, {0, 1}, {1, 1}}},
+            {{0, 1}, {0, 1}, {0, 1}, {0, 1}, {0, 1}, {34, 105}, {9, 35}, {9, 35}, {9, 280}, {9, 280}, {0, 1},
+             {41, 840}, {41, 840}},
+            {{41, 840}, {0, 1}, {0, 1}, {0, 1}, {0, 1}, {34, 105}, {9, 35}, {9, 35}, {9, 280}, {9, 280},
+             {41, 840}, {0, 1}, {0, 1}}};
     default:
         return Tableau{0, 0, 0, {}, {}, {}, {}};
     }

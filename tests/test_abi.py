@@ -54,7 +54,7 @@ def test_partition_rejects_empty_ranks(rk):
     assert e.value.status == "RK_ERR_ARG"
 
 
-@pytest.mark.parametrize("name", ["euler", "rk4", "cash_karp54", "dopri5"])
+@pytest.mark.parametrize("name", ["euler", "rk4", "cash_karp54", "dopri5", "rkf78"])
 def test_tableau_bitwise_equal_to_oracle(rk, name):
     lt = rk.tableau(name)
     ot = oracle.tableau(oracle.SCHEMES[name])
@@ -74,10 +74,10 @@ def test_tableau_bitwise_equal_to_oracle(rk, name):
 def test_controller_bitwise_equal_to_oracle(rk):
     rng = np.random.default_rng(11)
     Es = list(10.0 ** rng.uniform(-12, 4, 2000)) + [0.0, 0.5, 1.0, 1.0 + 2 ** -52, 5.0 ** -5, 1e300]
-    for scheme in ("cash_karp54", "dopri5"):
+    for scheme, p, q in (("cash_karp54", 5, 4), ("dopri5", 5, 4), ("rkf78", 8, 7)):
         for E in Es:
             dt = float(rng.uniform(1e-3, 10.0))
-            assert rk.controller(scheme, E, dt) == oracle.controller(E, dt, 5, 4), (E, dt)
+            assert rk.controller(scheme, E, dt) == oracle.controller(E, dt, p, q), (E, dt)
 
 
 def test_controller_errors(rk):

@@ -13,7 +13,7 @@ import rk_inputs
 
 pytestmark = pytest.mark.gpu
 
-SCHEMES = ["euler", "rk4", "cash_karp54", "dopri5"]
+SCHEMES = ["euler", "rk4", "cash_karp54", "dopri5", "rkf78"]
 OS = oracle.SCHEMES
 
 
@@ -74,7 +74,7 @@ def test_config1_exp_decay_integrate_const(ctx, scheme):
         assert steps == so == round(1.0 / dt)
         g = st.get()
         assert bitwise(g, uo)
-        order = {"euler": 1, "rk4": 4, "cash_karp54": 5, "dopri5": 5}[scheme]
+        order = {"euler": 1, "rk4": 4, "cash_karp54": 5, "dopri5": 5, "rkf78": 8}[scheme]
         err = np.max(np.abs(g - u0 * math.exp(-1.0)))
         assert err < 2 * dt ** order
 
@@ -172,7 +172,7 @@ def test_config3_gray_scott_64_rk4(ctx):
     assert bitwise(st.get(), u)
 
 
-@pytest.mark.parametrize("scheme", ["dopri5", "cash_karp54"])
+@pytest.mark.parametrize("scheme", ["dopri5", "cash_karp54", "rkf78"])
 @pytest.mark.parametrize("tol", [1e-6, 1e-8])
 def test_gs_adaptive_counts_and_state(ctx, scheme, tol):
     n = 32
@@ -190,7 +190,7 @@ def test_gs_try_step_matches_oracle_ratio(ctx):
     u0 = rk_inputs.gray_scott_ic(n, n, n, seed=3) + 0.05 * rk_inputs.random_state(
         2 * n ** 3, 4).reshape(n, 2, n, n)
     p = oracle.gray_scott_problem(n, n, n)
-    for scheme in ("dopri5", "cash_karp54"):
+    for scheme in ("dopri5", "cash_karp54", "rkf78"):
         st = gs_state(ctx, n, n, n, u0)
         for dt in (4.0, 1.0, 0.25):
             st.set(u0)
@@ -214,11 +214,13 @@ def _sample_block(u, z, y, x, r=8):
 
 
 @pytest.mark.parametrize("scheme,adaptive", [("rk4", False), ("dopri5", True), ("dopri5", False),
-                                             ("cash_karp54", True), ("euler", False)])
+                                             ("cash_karp54", True), ("euler", False),
+                                             ("rkf78", False), ("rkf78", True)])
 def test_512_sampled_parity(ctx, scheme, adaptive):
     """One step (or one adaptive try) at 512^3 exactly as bench.py runs it; every sampled
-    cell's new value is recomputed by the oracle on its 17^3 periodic neighbourhood (the
-    step's dependency radius is <= 7 stages), and must match bitwise."""
+    cell's new value is recomputed by the oracle on its periodic neighbourhood of radius
+    (#stages + 1) (a cell's new value depends on cells at most #stages away), and must
+    match bitwise."""
     n = 512
     u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
     st = gs_state(ctx, n, n, n, u0)
@@ -238,7 +240,7 @@ def test_512_sampled_parity(ctx, scheme, adaptive):
     rng = np.random.default_rng(0)
     pts = [(lo, lo, lo), (hi - 1, hi, lo - 1), (0, 0, 0), (511, 511, 511), (lo + 3, 255, 256),
            (lo, lo + 5, 31), (hi, lo, 32)] + [tuple(rng.integers(lo - 4, hi + 4, 3)) for _ in range(12)]
-    r = 8
+    r = 14 if scheme == "rkf78" else 8
     p = oracle.gray_scott_problem(2 * r + 1, 2 * r + 1, 2 * r + 1)
     for (z, y, x) in pts:
         blk = _sample_block(u0, z, y, x, r)
