@@ -308,17 +308,17 @@ def main():
             line["halo"] = h
         return line
 
-    def rk4_leg(overlap: int):
+    def rk4_leg(overlap: int, scheme: str = "rk4"):
         st.set_option(rk.OPT_HALO_OVERLAP, overlap)
         st.set(u0_dev)
         for _ in range(args.warmup):
-            st.do_step("rk4", 0.0, 1.0)
+            st.do_step(scheme, 0.0, 1.0)
         st.set_option(rk.OPT_TIMING, 1)
         st.reset_stats()
         barrier()
         ev0.record(stream)
         for k in range(args.steps):
-            st.do_step("rk4", float(k), 1.0)
+            st.do_step(scheme, float(k), 1.0)
         ev1.record(stream)
         barrier()
         ms4 = max_over_ranks(ev0.elapsed_time(ev1))
@@ -327,10 +327,10 @@ def main():
         st.set_option(rk.OPT_HALO_OVERLAP, args.overlap)
         a4 = s4["stage_bytes"] / (s4["stage_kernel_ms"] / 1e3) / 1e9 if s4["stage_kernel_ms"] else None
         out = {"value": cells_total * args.steps / (ms4 / 1e3), "ms_per_step": ms4 / args.steps,
-               "halo_overlap": bool(overlap),
+               "halo_overlap": bool(overlap), "scheme": scheme,
                "roofline": {"bound": "hbm", "achieved": a4, "peak": peak, "unit": "GB/s",
                             "frac": a4 / peak if a4 else None,
-                            "traffic": traffic.get("rk4", {}).get("bytes_per_launch"),
+                            "traffic": traffic.get(scheme, {}).get("bytes_per_launch"),
                             "algorithmic_bytes_per_cell_step": s4["stage_bytes"] / args.steps / cells_local,
                             "avg_launch_ms": s4["stage_kernel_ms"] / max(1, s4["stage_launches"])},
                "gpu_launches": s4["kernel_launches"]}
@@ -367,6 +367,9 @@ def main():
         extra["rk4"] = rk4_leg(args.overlap)
         if world > 1:
             extra["rk4_overlap_off"] = rk4_leg(0)
+    for sch in ("euler", "cash_karp54", "dopri5", "rkf78"):  # scheme sweep (configs[4])
+        if sch in legs:
+            extra[sch] = rk4_leg(args.overlap, sch)
     if extra:
         line["extra"] = extra
     if "e2e" in legs:

@@ -64,7 +64,14 @@ typedef enum {
 /* Table 1, the explicit one-step rows on the hot path.  CK54 and DOPRI5 are
  * used fixed-step (do_step / integrate_const) or error-controlled (integrate_adaptive),
  * reproducing both the "fixed" and "dynamic step size" rows of Table 1. */
-typedef enum { RK_EULER = 0, RK_RK4 = 1, RK_CASH_KARP54 = 2, RK_DOPRI5 = 3, RK_FEHLBERG78 = 4 } rk_scheme;
+typedef enum {
+    RK_EULER = 0,        /* explicit Euler, order 1                               */
+    RK_RK4 = 1,          /* classic Runge–Kutta 4                                 */
+    RK_CASH_KARP54 = 2,  /* Cash–Karp 5(4), fixed or error-controlled      */
+    RK_DOPRI5 = 3,       /* Dormand–Prince 5(4), FSAL, fixed or error-controlled  */
+    RK_FEHLBERG78 = 4,   /* Runge–Kutta–Fehlberg 7(8), fixed or error-controlled  */
+    RK_MIDPOINT = 5      /* modified midpoint, order 2 (R-22)            */
+} rk_scheme;
 
 /* Options for rk_set_option. */
 typedef enum {

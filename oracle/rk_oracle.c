@@ -43,6 +43,17 @@ static const tableau TAB_EULER = {
     {{0, 1}},
 };
 
+/* Modified midpoint (Table 1, order 2) read as the explicit midpoint rule: an Euler
+ * half step, then the full step with the midpoint slope (R-22). */
+static const tableau TAB_MIDPOINT = {
+    2, 2, 0, 0,
+    {{0, 1}, {1, 2}},
+    {{{0, 1}},
+     {{1, 2}}},
+    {{0, 1}, {1, 1}},
+    {{0, 1}},
+};
+
 static const tableau TAB_RK4 = {
     4, 4, 0, 0,
     {{0, 1}, {1, 2}, {1, 2}, {1, 1}},
@@ -110,6 +121,7 @@ static const tableau* get_tableau(int scheme) {
     case ORC_CASH_KARP54: return &TAB_CK54;
     case ORC_DOPRI5: return &TAB_DOPRI5;
     case ORC_RKF78: return &TAB_RKF78;
+    case ORC_MIDPOINT: return &TAB_MIDPOINT;
     default: return NULL;
     }
 }

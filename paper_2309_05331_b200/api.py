@@ -15,9 +15,9 @@ import numpy as np
 from . import _native
 from ._native import Stats, call
 
-EULER, RK4, CASH_KARP54, DOPRI5, FEHLBERG78 = 0, 1, 2, 3, 4
+EULER, RK4, CASH_KARP54, DOPRI5, FEHLBERG78, MIDPOINT = 0, 1, 2, 3, 4, 5
 SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5,
-           "rkf78": FEHLBERG78}
+           "rkf78": FEHLBERG78, "midpoint": MIDPOINT}
 
 
 def _scheme(s) -> int:

@@ -232,7 +232,7 @@ static Coeffs coeffs_of(int scheme) {
     return C;
 }
 
-static bool valid_scheme(int s) { return s >= RK_EULER && s <= RK_FEHLBERG78; }
+static bool valid_scheme(int s) { return s >= RK_EULER && s <= RK_MIDPOINT; }
 
 struct StagePlan {
     int scheme = 0, adaptive = 0, stage = 0;

@@ -542,6 +542,7 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
     case 7: return launch_stage_i<3, 1>(stage, a, grid, st);
     case 8: return launch_stage_i<4, 0>(stage, a, grid, st);
     case 9: return launch_stage_i<4, 1>(stage, a, grid, st);
+    case 10: return launch_stage_i<5, 0>(stage, a, grid, st);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -79,6 +79,8 @@ __host__ __device__ constexpr Tableau tableau_of(int scheme) {
              {41, 840}, {41, 840}},
             {{41, 840}, {0, 1}, {0, 1}, {0, 1}, {0, 1}, {34, 105}, {9, 35}, {9, 35}, {9, 280}, {9, 280},
              {41, 840}, {0, 1}, {0, 1}}};
+    case 5:  // modified midpoint as the explicit midpoint rule (R-22)
+        return Tableau{2, 2, 0, {{0, 1}, {1, 2}}, {{}, {{1, 2}}}, {{0, 1}, {1, 1}}, {{0, 1}}};
     default:
         return Tableau{0, 0, 0, {}, {}, {}, {}};
     }

@@ -54,7 +54,7 @@ def test_partition_rejects_empty_ranks(rk):
     assert e.value.status == "RK_ERR_ARG"
 
 
-@pytest.mark.parametrize("name", ["euler", "rk4", "cash_karp54", "dopri5", "rkf78"])
+@pytest.mark.parametrize("name", ["euler", "rk4", "cash_karp54", "dopri5", "rkf78", "midpoint"])
 def test_tableau_bitwise_equal_to_oracle(rk, name):
     lt = rk.tableau(name)
     ot = oracle.tableau(oracle.SCHEMES[name])

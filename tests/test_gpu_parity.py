@@ -13,7 +13,7 @@ import rk_inputs
 
 pytestmark = pytest.mark.gpu
 
-SCHEMES = ["euler", "rk4", "cash_karp54", "dopri5", "rkf78"]
+SCHEMES = ["euler", "rk4", "cash_karp54", "dopri5", "rkf78", "midpoint"]
 OS = oracle.SCHEMES
 
 
@@ -74,7 +74,8 @@ def test_config1_exp_decay_integrate_const(ctx, scheme):
         assert steps == so == round(1.0 / dt)
         g = st.get()
         assert bitwise(g, uo)
-        order = {"euler": 1, "rk4": 4, "cash_karp54": 5, "dopri5": 5, "rkf78": 8}[scheme]
+        order = {"euler": 1, "rk4": 4, "cash_karp54": 5, "dopri5": 5, "rkf78": 8,
+                 "midpoint": 2}[scheme]
         err = np.max(np.abs(g - u0 * math.exp(-1.0)))
         assert err < 2 * dt ** order
 

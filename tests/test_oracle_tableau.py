@@ -82,7 +82,7 @@ def test_tree_counts():
 
 SCHEMES = [("euler", oracle.EULER, 1, None), ("rk4", oracle.RK4, 4, None),
            ("cash_karp54", oracle.CASH_KARP54, 5, 4), ("dopri5", oracle.DOPRI5, 5, 4),
-           ("rkf78", oracle.RKF78, 8, 7)]
+           ("rkf78", oracle.RKF78, 8, 7), ("midpoint", oracle.MIDPOINT, 2, None)]
 
 
 def test_tree_counts_to_order_9():
@@ -99,7 +99,7 @@ def test_order_conditions(name, scheme, p, q):
         for t in rooted_trees(m):
             assert elementary_weight(tab, tab["b"], t) == Fraction(1, gamma(t)), (name, t)
             n_checked += 1
-    assert n_checked == {1: 1, 4: 8, 5: 17, 8: 200}[p]
+    assert n_checked == {1: 1, 2: 2, 4: 8, 5: 17, 8: 200}[p]
     # the method is NOT of order p+1 (some tree of order p+1 fails): the order is exact
     assert any(elementary_weight(tab, tab["b"], t) != Fraction(1, gamma(t))
                for t in rooted_trees(p + 1))
