@@ -102,6 +102,11 @@ def lib():
         L.orc_lincomb.restype = ctypes.c_int
         L.orc_norm_inf.argtypes = [ctypes.c_int64, dp]
         L.orc_norm_inf.restype = ctypes.c_double
+        L.orc_ab_coefficients.argtypes = [ctypes.c_int, i64p, i64p]
+        L.orc_ab_coefficients.restype = ctypes.c_int
+        L.orc_ab_integrate.argtypes = [P, ctypes.c_int, dp, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_int64, dp]
+        L.orc_ab_integrate.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -203,3 +208,24 @@ def lincomb(coef, inputs) -> np.ndarray:
 def norm_inf(u) -> float:
     u = _arr(u)
     return lib().orc_norm_inf(u.size, _ptr(u))
+
+
+def ab_coefficients(k: int) -> list:
+    """Adams–Bashforth k-step coefficients beta_0..beta_{k-1} (newest first), Fractions."""
+    num, den = (ctypes.c_int64 * 8)(), (ctypes.c_int64 * 8)()
+    if lib().orc_ab_coefficients(k, num, den) != k:
+        raise ValueError("k must be 1..8")
+    return [Fraction(num[j], den[j]) for j in range(k)]
+
+
+def ab_integrate(p: Problem, k: int, u, t0: float, dt: float, nsteps: int,
+                 trajectory: bool = False):
+    """Adams–Bashforth k, nsteps fixed steps (RKF78 bootstrap).  Returns the final state, or
+    (final, trajectory[nsteps, count]) if trajectory."""
+    u = _arr(u).copy()
+    tr = np.empty((nsteps, u.size)) if trajectory else None
+    rc = lib().orc_ab_integrate(ctypes.byref(p), k, _ptr(u), t0, dt, nsteps,
+                                _ptr(tr) if trajectory else None)
+    if rc != OK:
+        raise RuntimeError(f"orc_ab_integrate rc={rc}")
+    return (u, tr) if trajectory else u

@@ -386,6 +386,63 @@ done:
 }
 
 /* ------------------------------------------------------------------------------
+ * Adams–Bashforth (Table 1 multi-step row; Fig. 2c/d).
+ * Published coefficients over a common denominator (newest first), e.g. Hairer, Norsett &
+ * Wanner I, III.1; pinned in tests against the Lagrange-integral definition.
+ * --------------------------------------------------------------------------- */
+static const int64_t AB_NUM[8][8] = {
+    {1},
+    {3, -1},
+    {23, -16, 5},
+    {55, -59, 37, -9},
+    {1901, -2774, 2616, -1274, 251},
+    {4277, -7923, 9982, -7298, 2877, -475},
+    {198721, -447288, 705549, -688256, 407139, -134472, 19087},
+    {434241, -1152169, 2183877, -2664477, 2102243, -1041723, 295767, -36799},
+};
+static const int64_t AB_DEN[8] = {1, 2, 12, 24, 720, 1440, 60480, 120960};
+
+int orc_ab_coefficients(int k, int64_t* num, int64_t* den) {
+    if (k < 1 || k > 8) return -1;
+    for (int j = 0; j < k; ++j) {
+        num[j] = AB_NUM[k - 1][j];
+        den[j] = AB_DEN[k - 1];
+    }
+    return k;
+}
+
+int orc_ab_integrate(const orc_problem* p, int k, double* u, double t0, double dt, int64_t nsteps,
+                     double* traj) {
+    if (k < 1 || k > 8 || !(dt > 0.0) || nsteps < 0) return ORC_ERR_ARG;
+    const int64_t count = p->n * p->ncomp;
+    double g[8];
+    for (int j = 0; j < k; ++j) g[j] = dt * ((double)AB_NUM[k - 1][j] / (double)AB_DEN[k - 1]);
+    double* f[8];
+    for (int j = 0; j < k; ++j) f[j] = (double*)malloc(sizeof(double) * (size_t)count);
+    double* un = (double*)malloc(sizeof(double) * (size_t)count);
+    int rc = ORC_OK;
+    for (int64_t n = 0; n < nsteps; ++n) {
+        const double t = t0 + (double)n * dt;
+        orc_rhs(p, u, f[n % k]); /* f_n = F(t_n, u_n) */
+        if (n < k - 1) {
+            rc = orc_step(p, ORC_RKF78, t, dt, u, un, NULL); /* bootstrap (R-23) */
+            if (rc != ORC_OK) break;
+        } else {
+            for (int64_t e = 0; e < count; ++e) {
+                double w = u[e];
+                for (int j = 0; j < k; ++j) w = w + g[j] * f[(n - j) % k][e];
+                un[e] = w;
+            }
+        }
+        memcpy(u, un, sizeof(double) * (size_t)count);
+        if (traj) memcpy(traj + n * count, u, sizeof(double) * (size_t)count);
+    }
+    for (int j = 0; j < k; ++j) free(f[j]);
+    free(un);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------------
  * Algebra ops.
  * --------------------------------------------------------------------------- */
 int orc_lincomb(int64_t count, double* out, int k, const double* coef, const double* const* in) {

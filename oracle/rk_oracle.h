@@ -87,6 +87,19 @@ int orc_integrate_adaptive(const orc_problem* p, int scheme, double* u, double t
                            double dt0, double atol, double rtol, int64_t* accepted,
                            int64_t* rejected);
 
+/* Adams–Bashforth k-step coefficients beta_0..beta_{k-1} (newest first) as exact rationals
+ * (Table 1 "multi-step, Adams-Bashforth 1..8").  Returns k, or -1 if k not in 1..8. */
+int orc_ab_coefficients(int k, int64_t* num, int64_t* den);
+
+/* Adams–Bashforth k-step integration of nsteps fixed steps of size dt from t0 (
+ * S:L144-152).  Step n evaluates f_n = F(u_n) and keeps the last k values.
+ * The first min(k-1, nsteps) steps are bootstrap steps with RKF78 (R-23); after
+ * that u_{n+1} = u_n + sum_{j=0}^{k-1} (dt*beta_j) f_{n-j}, summed newest first (Odeint's
+ * order, R-24).  Updates u in place; if traj != NULL, u after step n+1 is also
+ * stored at traj + n*count (trajectory-max error norms, R-8). */
+int orc_ab_integrate(const orc_problem* p, int k, double* u, double t0, double dt, int64_t nsteps,
+                     double* traj);
+
 /* Algebra ops ("for_each#" / "for_each_norm").
  * out = sum_{j=0}^{k-1} coef[j]*in[j], left to right, 1 <= k <= 14. */
 int orc_lincomb(int64_t count, double* out, int k, const double* coef, const double* const* in);
