@@ -70,7 +70,14 @@ typedef enum {
     RK_CASH_KARP54 = 2,  /* Cash–Karp 5(4), fixed or error-controlled      */
     RK_DOPRI5 = 3,       /* Dormand–Prince 5(4), FSAL, fixed or error-controlled  */
     RK_FEHLBERG78 = 4,   /* Runge–Kutta–Fehlberg 7(8), fixed or error-controlled  */
-    RK_MIDPOINT = 5      /* modified midpoint, order 2 (R-22)            */
+    RK_MIDPOINT = 5,     /* modified midpoint, order 2 (R-22)            */
+    /* Adams–Bashforth k-step, order k, fixed dt only (Table 1 multi-step row).
+     * The state keeps the last k-1 slopes F(u_{n-j}); the first k-1 steps after any other
+     * change of u (set, another scheme, a new dt) are RKF78 bootstrap steps (R-23).
+     * u_{n+1} = u_n + dt*sum_{j<k} beta_j F(u_{n-j}), summed newest first (R-24).          */
+    RK_ADAMS_BASHFORTH1 = 11, RK_ADAMS_BASHFORTH2 = 12, RK_ADAMS_BASHFORTH3 = 13,
+    RK_ADAMS_BASHFORTH4 = 14, RK_ADAMS_BASHFORTH5 = 15, RK_ADAMS_BASHFORTH6 = 16,
+    RK_ADAMS_BASHFORTH7 = 17, RK_ADAMS_BASHFORTH8 = 18
 } rk_scheme;
 
 /* Options for rk_set_option. */

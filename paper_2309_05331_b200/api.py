@@ -18,6 +18,7 @@ from ._native import Stats, call
 EULER, RK4, CASH_KARP54, DOPRI5, FEHLBERG78, MIDPOINT = 0, 1, 2, 3, 4, 5
 SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5,
            "rkf78": FEHLBERG78, "midpoint": MIDPOINT}
+SCHEMES.update({f"ab{k}": 10 + k for k in range(1, 9)})  # Adams–Bashforth k (rk_b200.h)
 
 
 def _scheme(s) -> int:

@@ -35,6 +35,21 @@ struct PwArgs {
 };
 cudaError_t launch_pointwise(int scheme, const PwArgs& a, cudaStream_t st, int num_sms);
 
+// K1 (Adams–Bashforth): nsteps k-step updates with the history in registers.
+struct AbPwArgs {
+    double* u;         // in/out
+    double* hist[7];   // f_{n-1} .. f_{n-k+1}, newest first (in/out)
+    int64_t count;
+    int rhs;
+    double lambda;
+    int nsteps;
+    double g[8];       // dt*beta_j, newest first
+};
+cudaError_t launch_ab_pointwise(int k, const AbPwArgs& a, cudaStream_t st, int num_sms);
+// f = F(u) for a pointwise RHS (history bootstrap).
+cudaError_t launch_rhs_pointwise(const double* u, double* f, int64_t count, int rhs, double lambda,
+                                 cudaStream_t st, int num_sms);
+
 // ---------------------------------------------------------------------------------------
 // Grid arrays in HBM use a PADDED periodic layout: [z][c][ny+2][P] fp64 with P >= nx+2 even
 // (16-byte rows for TMA); logical cell (x, y) sits at padded (x+1, y+1), and the producer

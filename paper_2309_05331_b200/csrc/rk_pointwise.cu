@@ -107,6 +107,77 @@ static cudaError_t launch_s(const PwArgs& a, cudaStream_t st, int num_sms) {
     return launch_s_rhs<S, RHS_LOGISTIC>(a, st, num_sms);
 }
 
+// ---- Adams–Bashforth (Table 1 multi-step row): f_n = F(u_n),
+// u_{n+1} = u_n (+) g_0 f_n (+) g_1 f_{n-1} (+) ... newest first (R-24).  The k-1
+// past slopes stay in registers across all nsteps; each element is read and written once.
+template <int K, int RHS>
+__global__ void __launch_bounds__(256) ab_pointwise_kernel(const AbPwArgs a) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.count; i += stride) {
+        double x = a.u[i];
+        double h[K > 1 ? K - 1 : 1];
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j) h[j] = a.hist[j][i];
+        for (int n = 0; n < a.nsteps; ++n) {
+            const double f = f_pointwise<RHS>(x, a.lambda);
+            double w = add(x, mul(a.g[0], f));
+#pragma unroll
+            for (int j = 0; j < K - 1; ++j) w = add(w, mul(a.g[j + 1], h[j]));
+#pragma unroll
+            for (int j = K - 2; j > 0; --j) h[j] = h[j - 1];
+            if (K > 1) h[0] = f;
+            x = w;
+        }
+        a.u[i] = x;
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j) a.hist[j][i] = h[j];
+    }
+}
+
+template <int K>
+static cudaError_t launch_ab_k(const AbPwArgs& a, unsigned blocks, cudaStream_t st) {
+    if (a.rhs == RHS_EXP) ab_pointwise_kernel<K, RHS_EXP><<<blocks, 256, 0, st>>>(a);
+    else ab_pointwise_kernel<K, RHS_LOGISTIC><<<blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ab_pointwise(int k, const AbPwArgs& a, cudaStream_t st, int num_sms) {
+    int64_t blocks = (a.count + 255) / 256;
+    if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+    if (blocks < 1) blocks = 1;
+    const unsigned b = (unsigned)blocks;
+    switch (k) {
+    case 1: return launch_ab_k<1>(a, b, st);
+    case 2: return launch_ab_k<2>(a, b, st);
+    case 3: return launch_ab_k<3>(a, b, st);
+    case 4: return launch_ab_k<4>(a, b, st);
+    case 5: return launch_ab_k<5>(a, b, st);
+    case 6: return launch_ab_k<6>(a, b, st);
+    case 7: return launch_ab_k<7>(a, b, st);
+    case 8: return launch_ab_k<8>(a, b, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int RHS>
+__global__ void __launch_bounds__(256) rhs_pointwise_kernel(const double* __restrict__ u,
+                                                            double* __restrict__ f, int64_t n,
+                                                            double lambda) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        f[i] = f_pointwise<RHS>(__ldg(u + i), lambda);
+}
+
+cudaError_t launch_rhs_pointwise(const double* u, double* f, int64_t count, int rhs, double lambda,
+                                 cudaStream_t st, int num_sms) {
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+    if (blocks < 1) blocks = 1;
+    if (rhs == RHS_EXP) rhs_pointwise_kernel<RHS_EXP><<<(unsigned)blocks, 256, 0, st>>>(u, f, count, lambda);
+    else rhs_pointwise_kernel<RHS_LOGISTIC><<<(unsigned)blocks, 256, 0, st>>>(u, f, count, lambda);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pointwise(int scheme, const PwArgs& a, cudaStream_t st, int num_sms) {
     switch (scheme) {
     case 0: return launch_s<0>(a, st, num_sms);

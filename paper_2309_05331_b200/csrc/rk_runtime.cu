@@ -117,6 +117,12 @@ struct rk_state_s {
     CUtensorMap tm_glo{}, tm_ghi{};
     int nk = 0;
     bool k1_valid = false;           // k[0] == F(u) for the current u
+    // Adams–Bashforth history: hist[0..ab_count) = f_{n-1}, f_{n-2}, ... (newest first),
+    // hist[ab_k-1] is the scratch slot that receives f_n; valid for (ab_k, ab_dt) only
+    int ab_k = 0, ab_count = 0, nhist = 0;
+    double ab_dt = 0.0;
+    double* hist[8] = {nullptr};
+    CUtensorMap tm_hist[8][2]{};
     // halo (grid, world > 1 or loopback)
     double* sendbuf = nullptr;       // [lo plane | hi plane]
     double* ghostbuf = nullptr;      // [ghost_hi | ghost_lo] (so one message serves world==2)
@@ -232,13 +238,14 @@ static Coeffs coeffs_of(int scheme) {
     return C;
 }
 
-static bool valid_scheme(int s) { return s >= RK_EULER && s <= RK_MIDPOINT; }
+static bool valid_scheme(int s) { return (s >= RK_EULER && s <= RK_MIDPOINT) || is_ab_scheme(s); }
 
 struct StagePlan {
     int scheme = 0, adaptive = 0, stage = 0;
     StageSpec sp{};
     double g[kMaxSlots] = {0}, beta[kMaxSlots] = {0}, delta[kMaxSlots] = {0};
     double beta_new = 0.0, delta_new = 0.0;
+    int out_hist = -1;  // >= 0: the stage writes its k into Adams–Bashforth history slot
 };
 
 static std::vector<StagePlan> build_plan(int scheme, bool adaptive, double dt) {
@@ -301,11 +308,12 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     a.base = p.sp.base_unew ? st->u_new : st->u;
     a.tm_base = p.sp.base_unew ? st->tm_unew[0] : st->tm_u[0];
     int ny = 0;
+    const bool ab = is_ab_scheme(p.scheme);  // slots are history entries, newest first
     for (int s = 0; s < p.sp.nslots; ++s) {
         const int src = p.sp.src[s];
         const int box = p.sp.halo[s] ? 0 : 1;
-        a.slot[s] = src >= 0 ? st->k[src] : st->u;
-        a.tm_slot[s] = src >= 0 ? st->tm_k[src][box] : st->tm_u[box];
+        a.slot[s] = ab ? st->hist[src] : (src >= 0 ? st->k[src] : st->u);
+        a.tm_slot[s] = ab ? st->tm_hist[src][box] : (src >= 0 ? st->tm_k[src][box] : st->tm_u[box]);
         a.g[s] = p.g[s];
         a.beta[s] = p.beta[s];
         a.delta[s] = p.delta[s];
@@ -314,7 +322,8 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     a.nyslots = ny;
     a.beta_new = p.beta_new;
     a.delta_new = p.delta_new;
-    a.out_k = p.sp.out_k >= 0 ? st->k[p.sp.out_k] : nullptr;
+    a.out_k = p.out_hist >= 0 ? st->hist[p.out_hist]
+                              : (p.sp.out_k >= 0 ? st->k[p.sp.out_k] : nullptr);
     a.out_u = p.sp.writes_u ? st->u_new : nullptr;
     a.errmax = st->d_err;
     a.dt = dt;
@@ -539,8 +548,8 @@ static rk_status check_rhs(rk_state st) {
     return RK_OK;
 }
 
-// one fixed step, u <- u_new
-static rk_status fixed_step(rk_state st, int scheme, double dt) {
+// one fixed Runge–Kutta step, u <- u_new (does not touch the Adams–Bashforth history)
+static rk_status rk_fixed_step(rk_state st, int scheme, double dt) {
     if (st->grid) {
         auto plan = build_plan(scheme, false, dt);
         TRY(run_grid_plan(st, plan, dt, 0.0, 0.0));
@@ -553,11 +562,120 @@ static rk_status fixed_step(rk_state st, int scheme, double dt) {
     return RK_OK;
 }
 
+// ---- Adams–Bashforth k-step (Table 1 multi-step row; R-23, R-24) ---------
+static void ab_invalidate(rk_state st) {
+    st->ab_k = 0;
+    st->ab_count = 0;
+}
+
+static rk_status ab_prepare(rk_state st, int k, double dt) {
+    if (st->ab_k != k || st->ab_dt != dt) {  // new method or step size: restart the history
+        st->ab_k = k;
+        st->ab_dt = dt;
+        st->ab_count = 0;
+    }
+    for (int j = st->nhist; j < k; ++j) {
+        TRY(alloc_array(st, &st->hist[j], st->tm_hist[j]));
+        st->nhist = j + 1;
+    }
+    return RK_OK;
+}
+
+// the scratch slot hist[k-1] (just written with f_n) becomes the newest entry
+static void ab_rotate(rk_state st) {
+    const int k = st->ab_k;
+    double* p = st->hist[k - 1];
+    CUtensorMap m0 = st->tm_hist[k - 1][0], m1 = st->tm_hist[k - 1][1];
+    for (int j = k - 1; j > 0; --j) {
+        st->hist[j] = st->hist[j - 1];
+        st->tm_hist[j][0] = st->tm_hist[j - 1][0];
+        st->tm_hist[j][1] = st->tm_hist[j - 1][1];
+    }
+    st->hist[0] = p;
+    st->tm_hist[0][0] = m0;
+    st->tm_hist[0][1] = m1;
+    st->ab_count = std::min(st->ab_count + 1, k - 1);
+}
+
+static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double atol, double rtol);
+
+// Bootstrap step (R-23): f_n = F(u_n) into the history, then one RKF78 step.
+static rk_status ab_bootstrap_step(rk_state st, double dt) {
+    const int k = st->ab_k;
+    if (st->grid) {
+        StagePlan p;  // k1-type stage (no inputs but u) writing into the scratch slot
+        p.scheme = RK_RK4;
+        p.stage = 0;
+        p.sp = stage_spec(RK_RK4, false, 0);
+        p.out_hist = k - 1;
+        TRY(run_gs_stage(st, p, dt, 0.0, 0.0));
+    } else {
+        CK_CTX(st->ctx, launch_rhs_pointwise(st->u, st->hist[k - 1], st->count, st->rhs, st->lambda,
+                                             st->ctx->stream, st->ctx->num_sms));
+        st->stats.kernel_launches += 1;
+        st->stats.rhs_evals += 1;
+    }
+    ab_rotate(st);
+    return rk_fixed_step(st, RK_FEHLBERG78, dt);
+}
+
+// nsteps Adams–Bashforth steps (bootstrapping first while the history is short)
+static rk_status ab_steps(rk_state st, int k, double dt, int64_t nsteps) {
+    TRY(ab_prepare(st, k, dt));
+    while (nsteps > 0 && st->ab_count < k - 1) {
+        TRY(ab_bootstrap_step(st, dt));
+        --nsteps;
+    }
+    if (nsteps <= 0) return RK_OK;
+    double g[8];
+    for (int j = 0; j < k; ++j) g[j] = dt * rat_double(ab_beta(k, j));
+    if (!st->grid) {  // all remaining steps in one launch, history in registers
+        AbPwArgs a{};
+        a.u = st->u;
+        for (int j = 0; j < k - 1; ++j) a.hist[j] = st->hist[j];
+        a.count = st->count;
+        a.rhs = st->rhs;
+        a.lambda = st->lambda;
+        for (int j = 0; j < k; ++j) a.g[j] = g[j];
+        while (nsteps > 0) {
+            a.nsteps = (int)std::min<int64_t>(nsteps, 1 << 20);
+            CK_CTX(st->ctx, launch_ab_pointwise(k, a, st->ctx->stream, st->ctx->num_sms));
+            st->stats.kernel_launches += 1;
+            st->stats.rhs_evals += a.nsteps;
+            st->stats.steps += a.nsteps;
+            nsteps -= a.nsteps;
+        }
+        return RK_OK;
+    }
+    for (; nsteps > 0; --nsteps) {
+        StagePlan p;
+        p.scheme = kSchemeAB0 + k;
+        p.stage = 0;
+        p.sp = stage_spec(p.scheme, false, 0);
+        for (int s = 0; s < k - 1; ++s) p.beta[s] = g[s + 1];
+        p.beta_new = g[0];
+        p.out_hist = k - 1;
+        TRY(run_gs_stage(st, p, dt, 0.0, 0.0));
+        swap_u(st);
+        ab_rotate(st);
+        st->stats.steps += 1;
+    }
+    return RK_OK;
+}
+
+// one fixed step of any scheme (public do_step / integrate_const path)
+static rk_status fixed_step(rk_state st, int scheme, double dt) {
+    if (is_ab_scheme(scheme)) return ab_steps(st, scheme - kSchemeAB0, dt, 1);
+    ab_invalidate(st);
+    return rk_fixed_step(st, scheme, dt);
+}
+
 // one try: E (global), accept -> swap
 static rk_status one_try(rk_state st, int scheme, double t, double dt, double atol, double rtol,
                          int* accepted, double* E_out, double* dt_next) {
     rk_ctx ctx = st->ctx;
     const Coeffs C = coeffs_of(scheme);
+    ab_invalidate(st);
     int fsal_k = -1;  // FSAL: buffer holding k_s = F(u_new), the next step's k1
     if (st->grid) {
         auto plan = build_plan(scheme, true, dt);
@@ -822,6 +940,7 @@ rk_status rk_state_destroy(rk_state st) {
     cudaFree(st->u);
     cudaFree(st->u_new);
     for (int j = 0; j < st->nk; ++j) cudaFree(st->k[j]);
+    for (int j = 0; j < st->nhist; ++j) cudaFree(st->hist[j]);
     cudaFree(st->sendbuf);
     cudaFree(st->ghostbuf);
     cudaFree(st->d_err);
@@ -890,6 +1009,7 @@ rk_status rk_state_set(rk_state st, const double* src, int src_on_device) {
     }
     CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
     st->k1_valid = false;
+    ab_invalidate(st);
     return RK_OK;
 }
 
@@ -914,6 +1034,7 @@ rk_status rk_set_rhs_exponential(rk_state st, double lambda) {
     st->rhs = RHS_EXP;
     st->lambda = lambda;
     st->k1_valid = false;
+    ab_invalidate(st);
     return RK_OK;
 }
 
@@ -921,6 +1042,7 @@ rk_status rk_set_rhs_logistic(rk_state st) {
     TRY(check_state(st));
     st->rhs = RHS_LOGISTIC;
     st->k1_valid = false;
+    ab_invalidate(st);
     return RK_OK;
 }
 
@@ -937,6 +1059,7 @@ rk_status rk_set_rhs_gray_scott(rk_state st, double d1, double d2, double F, dou
     st->K = K;
     st->h = h;
     st->k1_valid = false;
+    ab_invalidate(st);
     return RK_OK;
 }
 
@@ -998,8 +1121,11 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
         ++n;
         t = t0 + (double)n * dt;
     }
-    if (!st->grid) {
+    if (is_ab_scheme(scheme)) {
+        TRY(ab_steps(st, scheme - kSchemeAB0, dt, n));
+    } else if (!st->grid) {
         // pointwise RHS: all n steps of every element in registers, chunked launches
+        ab_invalidate(st);
         int64_t left = n;
         while (left > 0) {
             const int chunk = (int)std::min<int64_t>(left, 1 << 20);
@@ -1085,6 +1211,7 @@ rk_status rk_lincomb(rk_state out, int k, const double* coef, const rk_state* in
     CK_CTX(out->ctx, launch_lincomb(a, out->ctx->stream, out->ctx->num_sms));
     out->stats.kernel_launches += 1;
     out->k1_valid = false;
+    ab_invalidate(out);
     CK_CTX(out->ctx, cudaStreamSynchronize(out->ctx->stream));
     return RK_OK;
 }

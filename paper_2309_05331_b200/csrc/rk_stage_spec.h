@@ -22,8 +22,13 @@ enum Epilogue {
     EPI_FINAL = 1,        // store u_new = w + beta_i k_i
     EPI_FINAL_ERR = 2,    // EPI_FINAL + error ratio max
     EPI_FINAL_EPART = 3,  // EPI_FINAL + store e' = e + delta_i k_i
-    EPI_TAIL_ERR = 4      // Y = u_new (base); store k_i; e = e' + delta_i k_i; ratio max
+    EPI_TAIL_ERR = 4,     // Y = u_new (base); store k_i; e = e' + delta_i k_i; ratio max
+    EPI_AB = 5            // Adams–Bashforth: store f_n; u_new = u + g_0 f_n + sum_s g_s h_s
 };
+
+// Scheme ids of the Adams–Bashforth k-step methods (rk_b200.h RK_ADAMS_BASHFORTH1..8).
+constexpr int kSchemeAB0 = 10;
+__host__ __device__ constexpr bool is_ab_scheme(int S) { return S > kSchemeAB0 && S <= kSchemeAB0 + 8; }
 
 constexpr int kMaxSlots = 10;  // RKF78 adaptive final stage: k1, k4..k12
 constexpr int SLOT_U = -1;  // slot source: the state u itself (TAIL stage: old u)
@@ -66,12 +71,30 @@ __host__ __device__ constexpr bool is_fsal(const Tableau& T, bool ad) {
 }
 
 __host__ __device__ constexpr int num_stages(int S, bool ad) {
-    return last_stage(tableau_of(S), ad) + 1;
+    return is_ab_scheme(S) ? 1 : last_stage(tableau_of(S), ad) + 1;
 }
 
 __host__ __device__ constexpr StageSpec stage_spec(int S, bool ad, int i) {
-    const Tableau T = tableau_of(S);
     StageSpec p{};
+    if (is_ab_scheme(S)) {
+        // one RHS evaluation per step: base = u_n (tile + ring), slots = f_{n-1} .. f_{n-k+1}
+        // (own cells only, newest first); the host binds out_k to a free history buffer
+        if (ad || i != 0) return p;
+        const int k = S - kSchemeAB0;
+        p.valid = 1;
+        p.epi = EPI_AB;
+        p.nslots = k - 1;
+        for (int s = 0; s < k - 1; ++s) {
+            p.src[s] = s;  // history position (newest first), resolved by the host
+            p.j[s] = s + 1;
+            p.bnz[s] = true;
+        }
+        p.bnew = true;
+        p.writes_u = true;
+        p.out_k = 0;
+        return p;
+    }
+    const Tableau T = tableau_of(S);
     if (T.s == 0 || (ad && T.err_order == 0)) return p;
     const int L = last_stage(T, ad);
     if (i < 0 || i > L) return p;

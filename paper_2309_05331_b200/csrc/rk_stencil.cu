@@ -136,10 +136,12 @@ __device__ __forceinline__ void store_cell(double* out, const GridGeom& g, int64
 
 // Per-cell partial sums completed by the epilogue with the new k_i (bitwise identical to the
 // full left-to-right sums: j = i is always the last term).
+template <int NH>
 struct EState {
-    double w[2];  // u (+) sum beta_j k_j
+    double w[2];  // u (+) sum beta_j k_j  (Adams–Bashforth: u)
     double e[2];  // sum delta_j k_j (first term not added to 0), or e' (TAIL)
     double d[2];  // atol (+) rtol (x) (|u| (+) dt (x) |k1|)
+    double h[NH > 0 ? NH : 1][2];  // Adams–Bashforth: f_{n-1} .. f_{n-k+1} at the own cell
 };
 
 // the error sum already holds a term before delta_i k_i is added
@@ -157,7 +159,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     constexpr bool FIN = EPI == EPI_FINAL || EPI == EPI_FINAL_ERR || EPI == EPI_FINAL_EPART;
     constexpr bool ESUM = EPI == EPI_FINAL_ERR || EPI == EPI_FINAL_EPART;  // e from slots
     constexpr bool RATIO = EPI == EPI_FINAL_ERR || EPI == EPI_TAIL_ERR;
-    constexpr bool STORE_K = EPI == EPI_K || EPI == EPI_TAIL_ERR;
+    constexpr bool STORE_K = EPI == EPI_K || EPI == EPI_TAIL_ERR || EPI == EPI_AB;
+    constexpr bool AB = EPI == EPI_AB;
+    using ES = EState<AB ? NS : 0>;
     extern __shared__ __align__(128) unsigned char smem[];
     double* sY = reinterpret_cast<double*>(smem + R * LY.stage_bytes);  // [2][2][BH][BW]
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R * LY.stage_bytes + 2 * HALO_SLOT);
@@ -229,10 +233,15 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         const double* p = reinterpret_cast<const double*>(st + LY.off[s]);
         return P.halo[s] ? p[c * BOX + pos] : p[c * OWN_BOX + poi];
     };
-    auto make_estate = [&](const unsigned char* st, EState& es) {
+    auto make_estate = [&](const unsigned char* st, ES& es) {
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const double ub = reinterpret_cast<const double*>(st)[c * BOX + pos];
+            if constexpr (AB) {  // newest-first sum needs f_n first: keep the raw terms
+                es.w[c] = ub;
+#pragma unroll
+                for (int s = 0; s < NS; ++s) es.h[s][c] = sval(st, s, c);
+            }
             if constexpr (FIN) {
                 double wv = ub;
 #pragma unroll
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     }
 
     double Ym[2], Yc[2], Yp[2];
-    EState Ec{}, En{};
+    ES Ec{}, En{};
     double rmax = 0.0;               // running max of the ratio (exact)
     unsigned long long rbits = 0ull;  // its bit pattern (NaN-propagating)
 
@@ -348,6 +357,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
             for (int c = 0; c < 2; ++c) {
                 const int64_t off = qo + c * G.cs;
                 if constexpr (STORE_K) store_cell(a.out_k, G, off, x, y, edge, f[c]);
+                if constexpr (AB) {
+                    // u_{n+1} = u_n (+) g_0 f_n (+) g_1 f_{n-1} (+) ... newest first (R-24)
+                    double wv = add(Ec.w[c], mul(a.beta_new, f[c]));
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) wv = add(wv, mul(a.beta[s], Ec.h[s][c]));
+                    store_cell(a.out_u, G, off, x, y, edge, wv);
+                }
                 if constexpr (FIN) {
                     const double wv = P.bnew ? add(Ec.w[c], mul(a.beta_new, f[c])) : Ec.w[c];
                     store_cell(a.out_u, G, off, x, y, edge, wv);
@@ -543,6 +559,14 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
     case 8: return launch_stage_i<4, 0>(stage, a, grid, st);
     case 9: return launch_stage_i<4, 1>(stage, a, grid, st);
     case 10: return launch_stage_i<5, 0>(stage, a, grid, st);
+    case 22: return launch_one<11, 0, 0>(a, grid, st);  // Adams–Bashforth 1..8: one launch/step
+    case 24: return launch_one<12, 0, 0>(a, grid, st);
+    case 26: return launch_one<13, 0, 0>(a, grid, st);
+    case 28: return launch_one<14, 0, 0>(a, grid, st);
+    case 30: return launch_one<15, 0, 0>(a, grid, st);
+    case 32: return launch_one<16, 0, 0>(a, grid, st);
+    case 34: return launch_one<17, 0, 0>(a, grid, st);
+    case 36: return launch_one<18, 0, 0>(a, grid, st);
     default: return cudaErrorInvalidValue;
     }
 }

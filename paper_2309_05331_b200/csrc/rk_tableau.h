@@ -111,4 +111,22 @@ __host__ __device__ constexpr Rat err_weight(const Tableau& T, int j) {
 
 inline double rat_double(Rat r) { return r.d == 0 ? 0.0 : (double)r.n / (double)r.d; }
 
+// Adams–Bashforth k-step weights beta_j (j = 0 newest .. k-1 oldest), Table 1 multi-step row
+// (P:L68): u_{n+1} = u_n + dt * sum_j beta_j f_{n-j}.  Standard values, reduced fractions.
+__host__ __device__ constexpr Rat ab_beta(int k, int j) {
+    constexpr Rat T[8][8] = {
+        {{1, 1}},
+        {{3, 2}, {-1, 2}},
+        {{23, 12}, {-4, 3}, {5, 12}},
+        {{55, 24}, {-59, 24}, {37, 24}, {-3, 8}},
+        {{1901, 720}, {-1387, 360}, {109, 30}, {-637, 360}, {251, 720}},
+        {{4277, 1440}, {-2641, 480}, {4991, 720}, {-3649, 720}, {959, 480}, {-95, 288}},
+        {{198721, 60480}, {-18637, 2520}, {235183, 20160}, {-10754, 945}, {135713, 20160},
+         {-5603, 2520}, {19087, 60480}},
+        {{16083, 4480}, {-1152169, 120960}, {242653, 13440}, {-296053, 13440}, {2102243, 120960},
+         {-115747, 13440}, {32863, 13440}, {-5257, 17280}},
+    };
+    return (k >= 1 && k <= 8 && j >= 0 && j < k) ? T[k - 1][j] : Rat{0, 1};
+}
+
 }  // namespace rkb

@@ -321,3 +321,68 @@ def test_stats_count_launches(ctx):
     st.do_step("rk4", 0.0, 1.0)
     s = st.stats()
     assert s["rhs_evals"] == 4 and s["stage_launches"] == 4 and s["kernel_launches"] >= 4
+
+
+# ---------------------------------------------------------------------------------------
+# Adams–Bashforth k = 1..8: RKF78 bootstrap + one fused launch per step
+# ---------------------------------------------------------------------------------------
+def _odeint_steps(t0, t1, dt):
+    n, t = 0, t0
+    while (t + dt) - t1 <= np.finfo(float).eps:
+        n += 1
+        t = t0 + n * dt
+    return n
+
+
+@pytest.mark.parametrize("k", range(1, 9))
+@pytest.mark.parametrize("rhs", ["exp", "logistic"])
+def test_ab_vector_bitwise(ctx, k, rhs):
+    n = 10001
+    if rhs == "exp":
+        u0 = rk_inputs.exp_decay_u0(n)
+        p = oracle.exp_problem(n, -1.0)
+    else:
+        u0 = rk_inputs.logistic_u0(n)
+        p = oracle.logistic_problem(n)
+    st = ctx.vector(n)
+    st.set_rhs_exponential(-1.0) if rhs == "exp" else st.set_rhs_logistic()
+    st.set(u0)
+    dt = 2.0 ** -5
+    steps = st.integrate_const(f"ab{k}", 0.0, 1.0, dt)
+    assert steps == _odeint_steps(0.0, 1.0, dt)
+    assert bitwise(st.get(), oracle.ab_integrate(p, k, u0, 0.0, dt, steps))
+    # do_step continues the same history (no re-bootstrap)
+    for _ in range(3):
+        st.do_step(f"ab{k}", 0.0, dt)
+    assert bitwise(st.get(), oracle.ab_integrate(p, k, u0, 0.0, dt, steps + 3))
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+@pytest.mark.parametrize("dims", [(16, 12, 10), (33, 17, 9)], ids=lambda d: "x".join(map(str, d)))
+def test_ab_grid_bitwise(ctx, k, dims):
+    nx, ny, nz = dims
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=7) + 0.01 * rk_inputs.random_state(
+        2 * nx * ny * nz, 11).reshape(nz, 2, ny, nx)
+    st = gs_state(ctx, nx, ny, nz, u0)
+    p = oracle.gray_scott_problem(nx, ny, nz)
+    nsteps = k + 4
+    for m in range(nsteps):
+        st.do_step(f"ab{k}", float(m), 1.0)
+    assert bitwise(st.get(), oracle.ab_integrate(p, k, u0, 0.0, 1.0, nsteps))
+
+
+def test_ab_history_restarts(ctx):
+    """A new dt (or set / another scheme) restarts the bootstrap, as documented."""
+    n = 64
+    u0 = rk_inputs.logistic_u0(n)
+    p = oracle.logistic_problem(n)
+    st = ctx.vector(n)
+    st.set_rhs_logistic()
+    st.set(u0)
+    for _ in range(5):
+        st.do_step("ab3", 0.0, 0.1)
+    mid = oracle.ab_integrate(p, 3, u0, 0.0, 0.1, 5)
+    assert bitwise(st.get(), mid)
+    for _ in range(4):
+        st.do_step("ab3", 0.0, 0.05)
+    assert bitwise(st.get(), oracle.ab_integrate(p, 3, mid, 0.0, 0.05, 4))
