@@ -1,0 +1,37 @@
+"""Small workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
+every scheme on a ragged 16x12x10 grid, the loopback multi-GPU halo path, adaptive tries,
+Adams-Bashforth and the algebra ops.  Run:  compute-sanitizer --tool racecheck python tools/sanitize_run.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2309_05331_b200 as rk  # noqa: E402
+import rk_inputs  # noqa: E402
+
+ctx = rk.Context(0, 1, 0)
+nx, ny, nz = 40, 12, 10
+u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=3) + 0.01 * rk_inputs.random_state(2 * nx * ny * nz, 1).reshape(nz, 2, ny, nx)
+for loop in (0, 1):
+    st = ctx.grid(nx, ny, nz, 2)
+    st.set_rhs_gray_scott()
+    st.set_option(rk.OPT_HALO_LOOPBACK, loop)
+    st.set(u0)
+    for s in ("euler", "midpoint", "rk4", "cash_karp54", "dopri5", "rkf78", "ab3"):
+        st.do_step(s, 0.0, 1.0)
+    for s in ("cash_karp54", "dopri5", "rkf78"):
+        st.try_step(s, 0.0, 0.5, 1e-6, 1e-6)
+    st.get()
+    st.close()
+v = ctx.vector(1001)
+v.set_rhs_logistic()
+v.set(rk_inputs.logistic_u0(1001))
+v.integrate_adaptive("dopri5", -5.0, 5.0, 0.1, 1e-8, 1e-8)
+v.integrate_const("ab4", 0.0, 1.0, 0.05)
+w = ctx.vector(1001)
+w.lincomb([1.0, 2.0], [v, v])
+print("norm", w.norm_inf())
+ctx.close()
+print("sanitize workload done")
