@@ -62,7 +62,6 @@ struct GridGeom {
     int64_t cs;     // component stride = (ny+2)*P
     int64_t ps;     // plane stride = 2*cs
 };
-void gs_tile_dims(int* tx, int* ty);
 
 // K3: fused Gray–Scott stage kernel.  Which terms exist is compile-time (StageSpec of
 // (scheme, adaptive, stage)); the runtime arguments are pointers, TMA maps and values.
@@ -91,10 +90,10 @@ struct GsStageArgs {
 // (scheme, adaptive, stage) selects the compile-time StageSpec instance.
 cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageArgs& a,
                             cudaStream_t st, int* nlaunch);
-// 4D tensor maps over a padded array of `nplanes` planes: tile + ring box ("halo") and
-// interior tile box ("own").
-cudaError_t encode_grid_maps(CUtensorMap* halo, CUtensorMap* own, const double* base,
-                             const GridGeom& g, int nplanes);
+// 4D tensor maps over a padded array of `nplanes` planes, maps[4]: for 32x8 tiles the
+// tile + ring box [0] and the interior box [1]; for 32x16 tiles [2] and [3]
+// (stage_rows(spec) selects the pair).
+cudaError_t encode_grid_maps(CUtensorMap* maps, const double* base, const GridGeom& g, int nplanes);
 
 // Y_i on own planes 0 and nzl-1 (whole padded planes) -> send = [lo plane | hi plane].
 cudaError_t launch_gs_pack(const GsStageArgs& a, double* send, cudaStream_t st);

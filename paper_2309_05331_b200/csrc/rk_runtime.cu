@@ -100,6 +100,12 @@ struct TimedPair {
     int kind;  // 0 stage kernel, 1 halo
 };
 
+// the four TMA maps of one padded grid array: [0]/[1] ring / interior box of 32x8 tiles,
+// [2]/[3] of 32x16 tiles (rk_kernels.cuh encode_grid_maps)
+struct Maps {
+    CUtensorMap m[4];
+};
+
 struct rk_state_s {
     rk_ctx ctx = nullptr;
     bool grid = false;
@@ -113,8 +119,8 @@ struct rk_state_s {
     double* u = nullptr;
     double* u_new = nullptr;
     double* k[13] = {nullptr};
-    CUtensorMap tm_u[2]{}, tm_unew[2]{}, tm_k[13][2]{};  // [0] tile+ring box, [1] interior box
-    CUtensorMap tm_glo{}, tm_ghi{};
+    Maps tm_u{}, tm_unew{}, tm_k[13]{};  // TMA maps per array (encode_grid_maps)
+    Maps tm_glo{}, tm_ghi{};
     int nk = 0;
     bool k1_valid = false;           // k[0] == F(u) for the current u
     // Adams–Bashforth history: hist[0..ab_count) = f_{n-1}, f_{n-2}, ... (newest first),
@@ -122,7 +128,7 @@ struct rk_state_s {
     int ab_k = 0, ab_count = 0, nhist = 0;
     double ab_dt = 0.0;
     double* hist[8] = {nullptr};
-    CUtensorMap tm_hist[8][2]{};
+    Maps tm_hist[8]{};
     // halo (grid, world > 1 or loopback)
     double* sendbuf = nullptr;       // [lo plane | hi plane]
     double* ghostbuf = nullptr;      // [ghost_hi | ghost_lo] (so one message serves world==2)
@@ -158,18 +164,18 @@ static rk_status dev_alloc(rk_ctx ctx, double** p, int64_t count) {
     return RK_OK;
 }
 
-// zero-filled array (pads and ring corners stay 0) with its two TMA tensor maps (grids)
-static rk_status alloc_array(rk_state st, double** p, CUtensorMap* tm) {
+// zero-filled array (pads and ring corners stay 0) with its TMA tensor maps (grids)
+static rk_status alloc_array(rk_state st, double** p, Maps* tm) {
     TRY(dev_alloc(st->ctx, p, st->alloc));
     CK_CTX(st->ctx, cudaMemsetAsync(*p, 0, sizeof(double) * (size_t)st->alloc, st->ctx->stream));
     if (st->grid && st->ncomp == 2 && tm)
-        CK_CTX(st->ctx, encode_grid_maps(&tm[0], &tm[1], *p, st->geo, (int)st->local));
+        CK_CTX(st->ctx, encode_grid_maps(tm->m, *p, st->geo, (int)st->local));
     return RK_OK;
 }
 
 static rk_status ensure_k(rk_state st, int nk) {
     for (int j = st->nk; j < nk; ++j) {
-        TRY(alloc_array(st, &st->k[j], st->tm_k[j]));
+        TRY(alloc_array(st, &st->k[j], &st->tm_k[j]));
         st->nk = j + 1;
     }
     return RK_OK;
@@ -177,12 +183,12 @@ static rk_status ensure_k(rk_state st, int nk) {
 
 static void swap_u(rk_state st) {
     std::swap(st->u, st->u_new);
-    for (int b = 0; b < 2; ++b) std::swap(st->tm_u[b], st->tm_unew[b]);
+    std::swap(st->tm_u, st->tm_unew);
 }
 
 static void swap_k(rk_state st, int i, int j) {
     std::swap(st->k[i], st->k[j]);
-    for (int b = 0; b < 2; ++b) std::swap(st->tm_k[i][b], st->tm_k[j][b]);
+    std::swap(st->tm_k[i], st->tm_k[j]);
 }
 
 static int64_t plane_values(rk_state st) { return st->geo.ps; }  // one padded plane, 2 comps
@@ -295,8 +301,8 @@ static rk_status ensure_halo(rk_state st) {
     TRY(dev_alloc(st->ctx, &st->sendbuf, 2 * plane_values(st)));
     TRY(dev_alloc(st->ctx, &st->ghostbuf, 2 * plane_values(st)));
     CK_CTX(st->ctx, cudaMemsetAsync(st->ghostbuf, 0, sizeof(double) * 2 * plane_values(st), st->ctx->stream));
-    CK_CTX(st->ctx, encode_grid_maps(&st->tm_ghi, nullptr, st->ghostbuf, st->geo, 1));
-    CK_CTX(st->ctx, encode_grid_maps(&st->tm_glo, nullptr, st->ghostbuf + plane_values(st), st->geo, 1));
+    CK_CTX(st->ctx, encode_grid_maps(st->tm_ghi.m, st->ghostbuf, st->geo, 1));
+    CK_CTX(st->ctx, encode_grid_maps(st->tm_glo.m, st->ghostbuf + plane_values(st), st->geo, 1));
     CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_pack, cudaEventDisableTiming));
     CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_halo, cudaEventDisableTiming));
     return RK_OK;
@@ -305,15 +311,16 @@ static rk_status ensure_halo(rk_state st) {
 static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
     GsStageArgs a{};
     a.geo = st->geo;
+    const int hb = 2 * (stage_rows(p.sp) - 1);  // map pair of this stage's tile height
     a.base = p.sp.base_unew ? st->u_new : st->u;
-    a.tm_base = p.sp.base_unew ? st->tm_unew[0] : st->tm_u[0];
+    a.tm_base = (p.sp.base_unew ? st->tm_unew : st->tm_u).m[hb];
     int ny = 0;
     const bool ab = is_ab_scheme(p.scheme);  // slots are history entries, newest first
     for (int s = 0; s < p.sp.nslots; ++s) {
         const int src = p.sp.src[s];
-        const int box = p.sp.halo[s] ? 0 : 1;
+        const int box = hb + (p.sp.halo[s] ? 0 : 1);
         a.slot[s] = ab ? st->hist[src] : (src >= 0 ? st->k[src] : st->u);
-        a.tm_slot[s] = ab ? st->tm_hist[src][box] : (src >= 0 ? st->tm_k[src][box] : st->tm_u[box]);
+        a.tm_slot[s] = ab ? st->tm_hist[src].m[box] : (src >= 0 ? st->tm_k[src].m[box] : st->tm_u.m[box]);
         a.g[s] = p.g[s];
         a.beta[s] = p.beta[s];
         a.delta[s] = p.delta[s];
@@ -365,7 +372,8 @@ static int pick_zchunk(rk_state st, const StagePlan& p, int range) {
         if (v > 0) return std::min(v, range);
     }
     int zc = p.sp.nslots <= 1 ? 16 : (p.sp.epi == EPI_FINAL_EPART ? 32 : 48);
-    const int tiles = (int)(((st->nx + 31) / 32) * ((st->ny + 7) / 8));
+    const int th = 8 * stage_rows(p.sp);
+    const int tiles = (int)(((st->nx + 31) / 32) * ((st->ny + th - 1) / th));
     const int want = st->ctx->num_sms * 4;  // >= 2 waves of 2 CTAs per SM
     while (zc > 4 && (int64_t)tiles * ((range + zc - 1) / zc) < want) zc /= 2;
     return std::min(zc, range);
@@ -452,8 +460,8 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
     TRY(halo_exchange(st));
     a.has_ghi = 1;
     a.has_glo = 1;
-    a.tm_ghi = st->tm_ghi;
-    a.tm_glo = st->tm_glo;
+    a.tm_ghi = st->tm_ghi.m[2 * (stage_rows(p.sp) - 1)];
+    a.tm_glo = st->tm_glo.m[2 * (stage_rows(p.sp) - 1)];
     if (st->overlap && nzl > 2) {
         GsStageArgs in = a;  // interior planes [1, nzl-1) never touch ghost planes
         in.z_lo = 1;
@@ -575,7 +583,7 @@ static rk_status ab_prepare(rk_state st, int k, double dt) {
         st->ab_count = 0;
     }
     for (int j = st->nhist; j < k; ++j) {
-        TRY(alloc_array(st, &st->hist[j], st->tm_hist[j]));
+        TRY(alloc_array(st, &st->hist[j], &st->tm_hist[j]));
         st->nhist = j + 1;
     }
     return RK_OK;
@@ -585,15 +593,13 @@ static rk_status ab_prepare(rk_state st, int k, double dt) {
 static void ab_rotate(rk_state st) {
     const int k = st->ab_k;
     double* p = st->hist[k - 1];
-    CUtensorMap m0 = st->tm_hist[k - 1][0], m1 = st->tm_hist[k - 1][1];
+    const Maps m = st->tm_hist[k - 1];
     for (int j = k - 1; j > 0; --j) {
         st->hist[j] = st->hist[j - 1];
-        st->tm_hist[j][0] = st->tm_hist[j - 1][0];
-        st->tm_hist[j][1] = st->tm_hist[j - 1][1];
+        st->tm_hist[j] = st->tm_hist[j - 1];
     }
     st->hist[0] = p;
-    st->tm_hist[0][0] = m0;
-    st->tm_hist[0][1] = m1;
+    st->tm_hist[0] = m;
     st->ab_count = std::min(st->ab_count + 1, k - 1);
 }
 
@@ -857,8 +863,8 @@ rk_status rk_ctx_destroy(rk_ctx ctx) {
 
 static rk_status state_common(rk_ctx ctx, rk_state st) {
     DeviceGuard g(ctx->device);
-    TRY(alloc_array(st, &st->u, st->tm_u));
-    TRY(alloc_array(st, &st->u_new, st->tm_unew));
+    TRY(alloc_array(st, &st->u, &st->tm_u));
+    TRY(alloc_array(st, &st->u_new, &st->tm_unew));
     CK_CTX(ctx, cudaMalloc((void**)&st->d_err, sizeof(unsigned long long)));
     CK_CTX(ctx, cudaMallocHost((void**)&st->h_err, sizeof(unsigned long long)));
     CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));

@@ -70,6 +70,13 @@ __host__ __device__ constexpr bool is_fsal(const Tableau& T, bool ad) {
     return true;
 }
 
+// Tile rows per thread in the stencil kernel (1 or 2).  Two-row tiles (32x16) amortise the
+// per-plane overhead of the light stages (at most one k input, or Adams–Bashforth k <= 4,
+// whose extra inputs are own-cell only) and halve their ring re-reads.
+__host__ __device__ constexpr int stage_rows(const StageSpec& P) {
+    return (P.nslots <= 1 || (P.epi == EPI_AB && P.nslots <= 3)) ? 2 : 1;
+}
+
 __host__ __device__ constexpr int num_stages(int S, bool ad) {
     return is_ab_scheme(S) ? 1 : last_stage(tableau_of(S), ad) + 1;
 }

@@ -34,22 +34,28 @@ namespace rkb {
 
 namespace {
 
-constexpr int TX = 32;  // tile width  (one warp per row)
-constexpr int TY = 8;   // tile height (8 warps)
-constexpr int NT = TX * TY;
-constexpr int BW = TX + 2, BH = TY + 2;
-constexpr int BOX = BW * BH;                              // cells per component, ring box
-constexpr int BOX_BYTES = 2 * BOX * 8;                    // 5440 B
-constexpr int HALO_SLOT = (BOX_BYTES + 127) / 128 * 128;  // 5504 B
-// interior box: the tile's own rows, but 34 wide from the 16-byte aligned column x0 (TMA
-// needs a 16-byte aligned inner start); 4352 B
-constexpr int OWN_ROW = BW;
-constexpr int OWN_BOX = TY * OWN_ROW;
-constexpr int OWN_BYTES = 2 * OWN_BOX * 8;
-constexpr int NHALO = BOX - NT;                           // ring positions (84)
-constexpr int SMEM_BUDGET = 110 * 1024;                   // 2 CTAs per SM
-constexpr int SMEM_BUDGET_1 = 226 * 1024;                 // 1 CTA per SM (wide RKF78 stages)
-static_assert(NHALO <= NT, "one ring position per thread");
+constexpr int TX = 32;  // tile width (one warp per row)
+constexpr int NT = 256;  // threads per CTA (8 warps); a thread owns ROWS cells of a column
+constexpr int BW = TX + 2;
+constexpr int SMEM_BUDGET = 110 * 1024;    // 2 CTAs per SM
+constexpr int SMEM_BUDGET_1 = 226 * 1024;  // 1 CTA per SM (wide RKF78 stages)
+
+// Tile geometry for ROWS tile rows per thread: a 32 x (8*ROWS) tile.
+template <int ROWS>
+struct Tile {
+    static constexpr int TH = 8 * ROWS;                             // tile height
+    static constexpr int BH = TH + 2;
+    static constexpr int BOX = BW * BH;                             // ring box cells / component
+    static constexpr int BOX_BYTES = 2 * BOX * 8;                   // 5440 | 9792 B
+    static constexpr int HALO_SLOT = (BOX_BYTES + 127) / 128 * 128;
+    // interior box: the tile's own rows, 34 wide from the 16-byte aligned column x0 (TMA
+    // needs a 16-byte aligned inner start)
+    static constexpr int OWN_BOX = TH * BW;
+    static constexpr int OWN_BYTES = 2 * OWN_BOX * 8;               // 4352 | 8704 B
+    static constexpr int NHALO = BOX - TX * TH;                     // ring positions (84 | 100)
+    static_assert(NHALO <= NT, "one ring position per thread");
+    static_assert(OWN_BYTES % 128 == 0, "TMA destinations stay 128-byte aligned");
+};
 
 struct Layout {
     int off[kMaxSlots] = {};  // byte offset of slot s inside a ring stage
@@ -60,29 +66,33 @@ struct Layout {
     int smem = 0;
 };
 
+template <int ROWS>
 __host__ __device__ constexpr Layout layout_of(const StageSpec& P) {
+    using T = Tile<ROWS>;
     Layout L{};
-    int o = HALO_SLOT, tx = BOX_BYTES;
+    int o = T::HALO_SLOT, tx = T::BOX_BYTES;
     for (int s = 0; s < P.nslots; ++s) {
         L.off[s] = o;
-        o += P.halo[s] ? HALO_SLOT : OWN_BYTES;
-        tx += P.halo[s] ? BOX_BYTES : OWN_BYTES;
+        o += P.halo[s] ? T::HALO_SLOT : T::OWN_BYTES;
+        tx += P.halo[s] ? T::BOX_BYTES : T::OWN_BYTES;
     }
     L.stage_bytes = o;
     L.tx_bytes = tx;
-    int R = (SMEM_BUDGET - 2 * HALO_SLOT - 64) / o;
+    int R = (SMEM_BUDGET - 2 * T::HALO_SLOT - 64) / o;
     if (R < 2) {  // too wide for 2 CTAs per SM: one CTA with a deeper ring
         L.minb = 1;
-        R = (SMEM_BUDGET_1 - 2 * HALO_SLOT - 64) / o;
+        R = (SMEM_BUDGET_1 - 2 * T::HALO_SLOT - 64) / o;
     }
     R = R > 4 ? 4 : (R < 2 ? 2 : R);
     L.R = R;
-    L.smem = R * o + 2 * HALO_SLOT + R * 8;
+    L.smem = R * o + 2 * T::HALO_SLOT + R * 8;
     return L;
 }
 
 template <int S, int AD, int I>
-constexpr int kMinBlocks = layout_of(stage_spec(S, AD != 0, I)).minb;
+constexpr int kRows = stage_rows(stage_spec(S, AD != 0, I));
+template <int S, int AD, int I>
+constexpr int kMinBlocks = layout_of<kRows<S, AD, I>>(stage_spec(S, AD != 0, I)).minb;
 
 // ---- PTX wrappers -------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -121,17 +131,20 @@ __device__ __forceinline__ bool plane_is_ghost(const GsStageArgs& a, int p) {
     return (p < 0 && a.has_glo) || (p >= a.geo.nzl && a.has_ghi);
 }
 
-// Store one cell of a padded array and its periodic ring copies (corners are never read).
-struct Edge {
+// One own cell of a padded array: its offset inside a (plane, component) slice and the
+// periodic ring copies it must also write (corners are never read).
+struct Cell {
+    int64_t off;      // (y+1)*P + (x+1)
     bool x0, x1, y0, y1;
 };
-__device__ __forceinline__ void store_cell(double* out, const GridGeom& g, int64_t off, int x, int y,
-                                           Edge e, double v) {
-    out[off + (int64_t)(y + 1) * g.P + (x + 1)] = v;
-    if (e.x0) out[off + (int64_t)(y + 1) * g.P + (g.nx + 1)] = v;
-    if (e.x1) out[off + (int64_t)(y + 1) * g.P] = v;
-    if (e.y0) out[off + (int64_t)(g.ny + 1) * g.P + (x + 1)] = v;
-    if (e.y1) out[off + (x + 1)] = v;
+__device__ __forceinline__ void store_cell(double* out, const GridGeom& g, int64_t slice, const Cell& e,
+                                           double v) {
+    double* p = out + slice + e.off;
+    p[0] = v;
+    if (e.x0) p[g.nx] = v;                    // x = 0     -> ring column nx+1
+    if (e.x1) p[-g.nx] = v;                   // x = nx-1  -> ring column 0
+    if (e.y0) p[(int64_t)g.ny * g.P] = v;     // y = 0     -> ring row ny+1
+    if (e.y1) p[-(int64_t)g.ny * g.P] = v;    // y = ny-1  -> ring row 0
 }
 
 // Per-cell partial sums completed by the epilogue with the new k_i (bitwise identical to the
@@ -154,7 +167,10 @@ __host__ __device__ constexpr bool has_prev_e(const StageSpec& P) {
 template <int S, int AD, int I>
 __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(const __grid_constant__ GsStageArgs a) {
     constexpr StageSpec P = stage_spec(S, AD != 0, I);
-    constexpr Layout LY = layout_of(P);
+    constexpr int ROWS = stage_rows(P);
+    using T = Tile<ROWS>;
+    constexpr int TH = T::TH, BH = T::BH, BOX = T::BOX, OWN_BOX = T::OWN_BOX, NHALO = T::NHALO;
+    constexpr Layout LY = layout_of<ROWS>(P);
     constexpr int NS = P.nslots, EPI = P.epi, R = LY.R;
     constexpr bool FIN = EPI == EPI_FINAL || EPI == EPI_FINAL_ERR || EPI == EPI_FINAL_EPART;
     constexpr bool ESUM = EPI == EPI_FINAL_ERR || EPI == EPI_FINAL_EPART;  // e from slots
@@ -164,13 +180,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     using ES = EState<AB ? NS : 0>;
     extern __shared__ __align__(128) unsigned char smem[];
     double* sY = reinterpret_cast<double*>(smem + R * LY.stage_bytes);  // [2][2][BH][BW]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R * LY.stage_bytes + 2 * HALO_SLOT);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R * LY.stage_bytes + 2 * T::HALO_SLOT);
 
     const GridGeom& G = a.geo;
     const int tid = threadIdx.x;
     const int ntx = (G.nx + TX - 1) / TX;
-    const int x0 = (int)(blockIdx.x % ntx) * TX, y0 = (int)(blockIdx.x / ntx) * TY;
-    const int w = min(TX, G.nx - x0), hg = min(TY, G.ny - y0);
+    const int x0 = (int)(blockIdx.x % ntx) * TX, y0 = (int)(blockIdx.x / ntx) * TH;
+    const int w = min(TX, G.nx - x0), hg = min(TH, G.ny - y0);
 
     int zb, ze;
     if (a.zmode == 0) {
@@ -183,18 +199,26 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     if (zb >= ze) return;  // CTA-uniform, before any barrier
     const int nplanes = ze - zb + 2;  // planes zb-1 .. ze; plane i is global zb-1+i
 
-    const int lx = tid % TX, ly = tid / TX;
-    const bool own = (lx < w) && (ly < hg);
-    const int pos = (ly + 1) * BW + (lx + 1);  // own cell in a ring box
-    const int poi = ly * OWN_ROW + lx + 1;     // own cell in an interior box
-    const bool hal = tid < NHALO;              // one ring position per thread
+    // own cells: column lx, rows ly0 + 8r (r < ROWS)
+    const int lx = tid % TX, ly0 = tid / TX;
+    const int x = x0 + lx;
+    bool own[ROWS];
+    int pos[ROWS], poi[ROWS];  // position in a ring box / in an interior box
+    Cell cell[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+        const int ly = ly0 + 8 * r, y = y0 + ly;
+        own[r] = (lx < w) && (ly < hg);
+        pos[r] = (ly + 1) * BW + (lx + 1);
+        poi[r] = ly * BW + lx + 1;
+        cell[r] = Cell{(int64_t)(y + 1) * G.P + (x + 1), x == 0, x == G.nx - 1, y == 0, y == G.ny - 1};
+    }
+    const bool hal = tid < NHALO;  // one ring position per thread
     int pos_h = 0;
     if (tid < BW) pos_h = tid;
     else if (tid < 2 * BW) pos_h = (BH - 1) * BW + (tid - BW);
-    else if (tid < 2 * BW + TY) pos_h = (tid - 2 * BW + 1) * BW;
-    else if (tid < NHALO) pos_h = (tid - 2 * BW - TY + 1) * BW + (BW - 1);
-    const int x = x0 + lx, y = y0 + ly;
-    const Edge edge{x == 0, x == G.nx - 1, y == 0, y == G.ny - 1};
+    else if (tid < 2 * BW + TH) pos_h = (tid - 2 * BW + 1) * BW;
+    else if (tid < NHALO) pos_h = (tid - 2 * BW - TH + 1) * BW + (BW - 1);
 
     auto stage_of = [&](int i) -> unsigned char* { return smem + (size_t)(i % R) * LY.stage_bytes; };
     auto issue = [&](int i) {  // thread 0 only
@@ -202,7 +226,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         unsigned char* st = stage_of(i);
         uint64_t* b = &bar[i % R];
         if (plane_is_ghost(a, p)) {
-            mbar_expect_tx(b, BOX_BYTES);
+            mbar_expect_tx(b, T::BOX_BYTES);
             tma_load_4d(st, p < 0 ? &a.tm_glo : &a.tm_ghi, b, x0, y0, 0, 0);
         } else {
             const int q = p < 0 ? p + G.nzl : (p >= G.nzl ? p - G.nzl : p);
@@ -228,25 +252,25 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         }
         return v;
     };
-    // own-cell value of slot s (ring box or interior box), component c
-    auto sval = [&](const unsigned char* st, int s, int c) -> double {
+    // own-cell value of slot s (ring box or interior box), component c, tile row r
+    auto sval = [&](const unsigned char* st, int s, int c, int r) -> double {
         const double* p = reinterpret_cast<const double*>(st + LY.off[s]);
-        return P.halo[s] ? p[c * BOX + pos] : p[c * OWN_BOX + poi];
+        return P.halo[s] ? p[c * BOX + pos[r]] : p[c * OWN_BOX + poi[r]];
     };
-    auto make_estate = [&](const unsigned char* st, ES& es) {
+    auto make_estate = [&](const unsigned char* st, int r, ES& es) {
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            const double ub = reinterpret_cast<const double*>(st)[c * BOX + pos];
+            const double ub = reinterpret_cast<const double*>(st)[c * BOX + pos[r]];
             if constexpr (AB) {  // newest-first sum needs f_n first: keep the raw terms
                 es.w[c] = ub;
 #pragma unroll
-                for (int s = 0; s < NS; ++s) es.h[s][c] = sval(st, s, c);
+                for (int s = 0; s < NS; ++s) es.h[s][c] = sval(st, s, c, r);
             }
             if constexpr (FIN) {
                 double wv = ub;
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
-                    if (P.bnz[s]) wv = add(wv, mul(a.beta[s], sval(st, s, c)));
+                    if (P.bnz[s]) wv = add(wv, mul(a.beta[s], sval(st, s, c, r)));
                 es.w[c] = wv;
             }
             if constexpr (ESUM) {
@@ -255,16 +279,16 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
 #pragma unroll
                 for (int s = 0; s < NS; ++s) {
                     if (!P.dnz[s]) continue;
-                    const double t = mul(a.delta[s], sval(st, s, c));
+                    const double t = mul(a.delta[s], sval(st, s, c, r));
                     e = first ? t : add(e, t);
                     first = false;
                 }
                 es.e[c] = e;
             }
-            if constexpr (EPI == EPI_TAIL_ERR) es.e[c] = sval(st, P.epart, c);
+            if constexpr (EPI == EPI_TAIL_ERR) es.e[c] = sval(st, P.epart, c, r);
             if constexpr (RATIO) {
-                const double uu = P.den_u >= 0 ? sval(st, P.den_u, c) : ub;
-                const double k1 = sval(st, P.den_k1, c);
+                const double uu = P.den_u >= 0 ? sval(st, P.den_u, c, r) : ub;
+                const double k1 = sval(st, P.den_k1, c, r);
                 es.d[c] = add(a.atol, mul(a.rtol, add(fabs(uu), mul(a.dt, fabs(k1)))));
             }
         }
@@ -282,27 +306,33 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         for (int i = 0; i < n0; ++i) issue(i);
     }
 
-    double Ym[2], Yc[2], Yp[2];
-    ES Ec{}, En{};
+    double Ym[ROWS][2], Yc[ROWS][2], Yp[ROWS][2];
+    ES Ec[ROWS] = {}, En[ROWS] = {};
     double rmax = 0.0;               // running max of the ratio (exact)
     unsigned long long rbits = 0ull;  // its bit pattern (NaN-propagating)
 
     // ---- prologue: plane zb-1 (own column only), plane zb (tile + ring) -----------------
-    // Every thread forms Y at its tile position, valid or not: for a partial tile (w < TX or
-    // hg < TY) the periodic ring sits inside the box at column w+1 / row hg+1.
+    // Every thread forms Y at its tile positions, valid or not: for a partial tile (w < TX or
+    // hg < TH) the periodic ring sits inside the box at column w+1 / row hg+1.
     {
         wait_plane(0);
         const unsigned char* s0 = stage_of(0);
         const bool gh = plane_is_ghost(a, zb - 1);
-        Ym[0] = y_at(s0, 0, pos, gh);
-        Ym[1] = y_at(s0, 1, pos, gh);
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+            Ym[r][0] = y_at(s0, 0, pos[r], gh);
+            Ym[r][1] = y_at(s0, 1, pos[r], gh);
+        }
         wait_plane(1);
         const unsigned char* s1 = stage_of(1);
-        Yc[0] = y_at(s1, 0, pos, false);
-        Yc[1] = y_at(s1, 1, pos, false);
-        sY[pos] = Yc[0];
-        sY[BOX + pos] = Yc[1];
-        if (own) make_estate(s1, Ec);
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+            Yc[r][0] = y_at(s1, 0, pos[r], false);
+            Yc[r][1] = y_at(s1, 1, pos[r], false);
+            sY[pos[r]] = Yc[r][0];
+            sY[BOX + pos[r]] = Yc[r][1];
+            if (own[r]) make_estate(s1, r, Ec[r]);
+        }
         if (hal) {
             sY[pos_h] = y_at(s1, 0, pos_h, false);
             sY[BOX + pos_h] = y_at(s1, 1, pos_h, false);
@@ -324,63 +354,68 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         wait_plane(i);
         const unsigned char* si = stage_of(i);
         const bool gh = plane_is_ghost(a, z + 1);
-        Yp[0] = y_at(si, 0, pos, gh);
-        Yp[1] = y_at(si, 1, pos, gh);
-        if (more) {
-            yn[pos] = Yp[0];
-            yn[BOX + pos] = Yp[1];
-            if (own) make_estate(si, En);
-            if (hal) {
-                yn[pos_h] = y_at(si, 0, pos_h, false);
-                yn[BOX + pos_h] = y_at(si, 1, pos_h, false);
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+            Yp[r][0] = y_at(si, 0, pos[r], gh);
+            Yp[r][1] = y_at(si, 1, pos[r], gh);
+            if (more) {
+                yn[pos[r]] = Yp[r][0];
+                yn[BOX + pos[r]] = Yp[r][1];
+                if (own[r]) make_estate(si, r, En[r]);
             }
         }
+        if (more && hal) {
+            yn[pos_h] = y_at(si, 0, pos_h, false);
+            yn[BOX + pos_h] = y_at(si, 1, pos_h, false);
+        }
         // [C] stencil + reaction + epilogue at plane z
-        if (own) {
+        const int64_t qo = (int64_t)z * G.ps;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+            if (!own[r]) continue;
             double L[2];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const double* v = yc + c * BOX + pos;
-                const double ctr = Yc[c];
+                const double* v = yc + c * BOX + pos[r];
+                const double ctr = Yc[r][c];
                 double s = add(sub(v[-1], ctr), sub(v[1], ctr));
                 s = add(s, add(sub(v[-BW], ctr), sub(v[BW], ctr)));
-                s = add(s, add(sub(Ym[c], ctr), sub(Yp[c], ctr)));
+                s = add(s, add(sub(Ym[r][c], ctr), sub(Yp[r][c], ctr)));
                 L[c] = mul(s, a.inv_h2);
             }
-            const double C0 = Yc[0], C1 = Yc[1];
-            const double r = mul(mul(C0, C1), C1);
+            const double C0 = Yc[r][0], C1 = Yc[r][1];
+            const double rc = mul(mul(C0, C1), C1);
             double f[2];
-            f[0] = sub(add(sub(mul(a.d1, L[0]), r), a.F), mul(a.F, C0));
-            f[1] = sub(add(mul(a.d2, L[1]), r), mul(a.FK, C1));
-            const int64_t qo = (int64_t)z * G.ps;
+            f[0] = sub(add(sub(mul(a.d1, L[0]), rc), a.F), mul(a.F, C0));
+            f[1] = sub(add(mul(a.d2, L[1]), rc), mul(a.FK, C1));
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int64_t off = qo + c * G.cs;
-                if constexpr (STORE_K) store_cell(a.out_k, G, off, x, y, edge, f[c]);
+                const int64_t slice = qo + c * G.cs;
+                if constexpr (STORE_K) store_cell(a.out_k, G, slice, cell[r], f[c]);
                 if constexpr (AB) {
                     // u_{n+1} = u_n (+) g_0 f_n (+) g_1 f_{n-1} (+) ... newest first (R-24)
-                    double wv = add(Ec.w[c], mul(a.beta_new, f[c]));
+                    double wv = add(Ec[r].w[c], mul(a.beta_new, f[c]));
 #pragma unroll
-                    for (int s = 0; s < NS; ++s) wv = add(wv, mul(a.beta[s], Ec.h[s][c]));
-                    store_cell(a.out_u, G, off, x, y, edge, wv);
+                    for (int s = 0; s < NS; ++s) wv = add(wv, mul(a.beta[s], Ec[r].h[s][c]));
+                    store_cell(a.out_u, G, slice, cell[r], wv);
                 }
                 if constexpr (FIN) {
-                    const double wv = P.bnew ? add(Ec.w[c], mul(a.beta_new, f[c])) : Ec.w[c];
-                    store_cell(a.out_u, G, off, x, y, edge, wv);
+                    const double wv = P.bnew ? add(Ec[r].w[c], mul(a.beta_new, f[c])) : Ec[r].w[c];
+                    store_cell(a.out_u, G, slice, cell[r], wv);
                 }
-                double e = Ec.e[c];
+                double e = Ec[r].e[c];
                 if constexpr (ESUM || EPI == EPI_TAIL_ERR) {
                     if constexpr (P.dnew) {
                         const double t = mul(a.delta_new, f[c]);
                         e = HAS_PREV_E ? add(e, t) : t;
                     }
                 }
-                if constexpr (EPI == EPI_FINAL_EPART) store_cell(a.out_k, G, off, x, y, edge, e);
+                if constexpr (EPI == EPI_FINAL_EPART) store_cell(a.out_k, G, slice, cell[r], e);
                 if constexpr (RATIO) {
                     // r = |e| / d exactly; skip the division when e == 0 (r = +0) or when
                     // |e| <= rmax*d*(1-2^-52) (a normal number) proves r <= rmax by
                     // monotone rounding; NaN never skips.
-                    const double ae = fabs(e), dd = Ec.d[c];
+                    const double ae = fabs(e), dd = Ec[r].d[c];
                     const double th = mul(mul(rmax, dd), 0.99999999999999978);
                     if (!(ae == 0.0 || (ae <= th && th >= 2.2250738585072014e-308))) {
                         const double rr = ae / dd;
@@ -393,9 +428,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                 }
             }
         }
-        Ym[0] = Yc[0]; Ym[1] = Yc[1];
-        Yc[0] = Yp[0]; Yc[1] = Yp[1];
-        Ec = En;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+            Ym[r][0] = Yc[r][0]; Ym[r][1] = Yc[r][1];
+            Yc[r][0] = Yp[r][0]; Yc[r][1] = Yp[r][1];
+            Ec[r] = En[r];
+        }
         __syncthreads();  // Y(z+1) tile complete; ring stage of plane z+1 free
         if (tid == 0 && i + R < nplanes) issue(i + R);
     }
@@ -438,7 +476,7 @@ template <int S, int AD, int I>
 cudaError_t launch_one(const GsStageArgs& a, dim3 grid, cudaStream_t st) {
     constexpr StageSpec P = stage_spec(S, AD != 0, I);
     static_assert(P.valid, "invalid stage");
-    constexpr int bytes = layout_of(P).smem;
+    constexpr int bytes = layout_of<kRows<S, AD, I>>(P).smem;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(gs_stage_kernel<S, AD, I>,
@@ -487,11 +525,6 @@ cudaError_t launch_stage_i(int i, const GsStageArgs& a, dim3 grid, cudaStream_t 
 
 }  // namespace
 
-void gs_tile_dims(int* tx, int* ty) {
-    *tx = TX;
-    *ty = TY;
-}
-
 // Developer tuning knob (not part of the ABI): RKB_L2PROMO = 0 none, 1 64B, 2 128B, 3 256B.
 static CUtensorMapL2promotion l2_promotion() {
     static int v = -1;
@@ -506,8 +539,7 @@ static CUtensorMapL2promotion l2_promotion() {
     return tab[v];
 }
 
-cudaError_t encode_grid_maps(CUtensorMap* halo, CUtensorMap* own, const double* base,
-                             const GridGeom& g, int nplanes) {
+cudaError_t encode_grid_maps(CUtensorMap* maps, const double* base, const GridGeom& g, int nplanes) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q;
@@ -519,16 +551,13 @@ cudaError_t encode_grid_maps(CUtensorMap* halo, CUtensorMap* own, const double* 
     const cuuint64_t dims[4] = {(cuuint64_t)g.P, (cuuint64_t)(g.ny + 2), 2, (cuuint64_t)nplanes};
     const cuuint64_t strides[3] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.cs * 8, (cuuint64_t)g.ps * 8};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
-    const cuuint32_t box_h[4] = {BW, BH, 2, 1};
-    const cuuint32_t box_o[4] = {OWN_ROW, TY, 2, 1};
-    CUresult r = encode(halo, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
-                        strides, box_h, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    if (own) {
-        r = encode(own, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides,
-                   box_o, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    // maps[2*(ROWS-1) + 0]: tile + ring box, maps[2*(ROWS-1) + 1]: interior box (own rows)
+    const cuuint32_t boxes[4][4] = {{BW, Tile<1>::BH, 2, 1}, {BW, Tile<1>::TH, 2, 1},
+                                    {BW, Tile<2>::BH, 2, 1}, {BW, Tile<2>::TH, 2, 1}};
+    for (int m = 0; m < 4; ++m) {
+        CUresult r = encode(&maps[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims,
+                            strides, boxes[m], estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
     return cudaSuccess;
@@ -536,7 +565,8 @@ cudaError_t encode_grid_maps(CUtensorMap* halo, CUtensorMap* own, const double* 
 
 cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageArgs& a,
                             cudaStream_t st, int* nlaunch) {
-    const int ntx = (a.geo.nx + TX - 1) / TX, nty = (a.geo.ny + TY - 1) / TY;
+    const int th = 8 * stage_rows(stage_spec(scheme, adaptive != 0, stage));
+    const int ntx = (a.geo.nx + TX - 1) / TX, nty = (a.geo.ny + th - 1) / th;
     const int tiles = ntx * nty;
     int nchunks;
     if (a.zmode == 1) {
