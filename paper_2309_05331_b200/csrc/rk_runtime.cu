@@ -371,7 +371,23 @@ static int pick_zchunk(rk_state st, const StagePlan& p, int range) {
         const int v = atoi(e);
         if (v > 0) return std::min(v, range);
     }
-    int zc = p.sp.nslots <= 1 ? 16 : (p.sp.epi == EPI_FINAL_EPART ? 32 : 48);
+    // classes: 0 Y-direct (no slot enters Y), 1 other two-row stages, 2 EPART, 3 the rest
+    bool yd = true;
+    for (int s = 0; s < p.sp.nslots; ++s) yd = yd && !p.sp.gnz[s];
+    const int cls = yd ? 0 : (stage_rows(p.sp) == 2 ? 1 : (p.sp.epi == EPI_FINAL_EPART ? 2 : 3));
+    static int tab[4] = {0, 0, 0, 0};
+    static bool parsed = false;
+    if (!parsed) {  // developer tuning knob RKB_ZC="yd,light,epart,heavy"
+        const int def[4] = {8, 16, 32, 48};
+        for (int c = 0; c < 4; ++c) tab[c] = def[c];
+        if (const char* e = getenv("RKB_ZC")) {
+            int v[4], n = sscanf(e, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]);
+            for (int c = 0; c < n; ++c)
+                if (v[c] > 0) tab[c] = v[c];
+        }
+        parsed = true;
+    }
+    int zc = tab[cls];
     const int th = 8 * stage_rows(p.sp);
     const int tiles = (int)(((st->nx + 31) / 32) * ((st->ny + th - 1) / th));
     const int want = st->ctx->num_sms * 4;  // >= 2 waves of 2 CTAs per SM

@@ -60,32 +60,44 @@ struct Tile {
 struct Layout {
     int off[kMaxSlots] = {};  // byte offset of slot s inside a ring stage
     int stage_bytes = 0;      // one ring stage (base + slots)
-    int tx_bytes = 0;         // TMA bytes landing per non-ghost plane
+    int tx_bytes = 0;         // TMA bytes landing per non-ghost output plane
+    int tx_edge = 0;          // ... per z-halo plane (zb-1, ze): Y arrays only
     int R = 2;                // ring depth
     int minb = 2;             // CTAs per SM the layout is sized for (__launch_bounds__)
+    bool ydirect = false;     // Y_i == base array: stencil reads the ring stage directly
     int smem = 0;
 };
 
+// Y-direct stages (no slot enters Y: every first stage, Euler, Adams–Bashforth, the FSAL
+// tail) read their x/y neighbours straight from the TMA ring stage of the centre plane and
+// need no Y tile in shared memory; the others form Y once per plane into a double buffer.
 template <int ROWS>
 __host__ __device__ constexpr Layout layout_of(const StageSpec& P) {
     using T = Tile<ROWS>;
     Layout L{};
-    int o = T::HALO_SLOT, tx = T::BOX_BYTES;
+    bool yd = true;
+    for (int s = 0; s < P.nslots; ++s) yd = yd && !P.gnz[s];
+    L.ydirect = yd;
+    const int ybuf = yd ? 0 : 2 * T::HALO_SLOT;
+    int o = T::HALO_SLOT, tx = T::BOX_BYTES, te = T::BOX_BYTES;
     for (int s = 0; s < P.nslots; ++s) {
         L.off[s] = o;
         o += P.halo[s] ? T::HALO_SLOT : T::OWN_BYTES;
         tx += P.halo[s] ? T::BOX_BYTES : T::OWN_BYTES;
+        te += P.halo[s] ? T::BOX_BYTES : 0;
     }
     L.stage_bytes = o;
     L.tx_bytes = tx;
-    int R = (SMEM_BUDGET - 2 * T::HALO_SLOT - 64) / o;
-    if (R < 2) {  // too wide for 2 CTAs per SM: one CTA with a deeper ring
+    L.tx_edge = te;
+    const int rmax = yd ? 6 : 4;  // a Y-direct ring also holds the centre plane
+    int R = (SMEM_BUDGET - ybuf - 64) / o;
+    if (R < (yd ? 3 : 2)) {  // too wide for 2 CTAs per SM: one CTA with a deeper ring
         L.minb = 1;
-        R = (SMEM_BUDGET_1 - 2 * T::HALO_SLOT - 64) / o;
+        R = (SMEM_BUDGET_1 - ybuf - 64) / o;
     }
-    R = R > 4 ? 4 : (R < 2 ? 2 : R);
+    R = R > rmax ? rmax : (R < 2 ? 2 : R);
     L.R = R;
-    L.smem = R * o + 2 * T::HALO_SLOT + R * 8;
+    L.smem = R * o + ybuf + R * 8;
     return L;
 }
 
@@ -135,16 +147,19 @@ __device__ __forceinline__ bool plane_is_ghost(const GsStageArgs& a, int p) {
 // periodic ring copies it must also write (corners are never read).
 struct Cell {
     int64_t off;      // (y+1)*P + (x+1)
+    bool ring;        // on the domain edge: some ring copy below applies
     bool x0, x1, y0, y1;
 };
 __device__ __forceinline__ void store_cell(double* out, const GridGeom& g, int64_t slice, const Cell& e,
                                            double v) {
     double* p = out + slice + e.off;
     p[0] = v;
-    if (e.x0) p[g.nx] = v;                    // x = 0     -> ring column nx+1
-    if (e.x1) p[-g.nx] = v;                   // x = nx-1  -> ring column 0
-    if (e.y0) p[(int64_t)g.ny * g.P] = v;     // y = 0     -> ring row ny+1
-    if (e.y1) p[-(int64_t)g.ny * g.P] = v;    // y = ny-1  -> ring row 0
+    if (e.ring) {  // warp-uniformly false away from the domain edges
+        if (e.x0) p[g.nx] = v;                    // x = 0     -> ring column nx+1
+        if (e.x1) p[-g.nx] = v;                   // x = nx-1  -> ring column 0
+        if (e.y0) p[(int64_t)g.ny * g.P] = v;     // y = 0     -> ring row ny+1
+        if (e.y1) p[-(int64_t)g.ny * g.P] = v;    // y = ny-1  -> ring row 0
+    }
 }
 
 // Per-cell partial sums completed by the epilogue with the new k_i (bitwise identical to the
@@ -179,8 +194,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     constexpr bool AB = EPI == EPI_AB;
     using ES = EState<AB ? NS : 0>;
     extern __shared__ __align__(128) unsigned char smem[];
-    double* sY = reinterpret_cast<double*>(smem + R * LY.stage_bytes);  // [2][2][BH][BW]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R * LY.stage_bytes + 2 * T::HALO_SLOT);
+    constexpr bool YD = LY.ydirect;
+    double* sY = reinterpret_cast<double*>(smem + R * LY.stage_bytes);  // [2][2][BH][BW] (!YD)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R * LY.stage_bytes + (YD ? 0 : 2 * T::HALO_SLOT));
 
     const GridGeom& G = a.geo;
     const int tid = threadIdx.x;
@@ -211,7 +227,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         own[r] = (lx < w) && (ly < hg);
         pos[r] = (ly + 1) * BW + (lx + 1);
         poi[r] = ly * BW + lx + 1;
-        cell[r] = Cell{(int64_t)(y + 1) * G.P + (x + 1), x == 0, x == G.nx - 1, y == 0, y == G.ny - 1};
+        const bool ex0 = x == 0, ex1 = x == G.nx - 1, ey0 = y == 0, ey1 = y == G.ny - 1;
+        cell[r] = Cell{(int64_t)(y + 1) * G.P + (x + 1), ex0 || ex1 || ey0 || ey1, ex0, ex1, ey0, ey1};
     }
     const bool hal = tid < NHALO;  // one ring position per thread
     int pos_h = 0;
@@ -230,12 +247,14 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
             tma_load_4d(st, p < 0 ? &a.tm_glo : &a.tm_ghi, b, x0, y0, 0, 0);
         } else {
             const int q = p < 0 ? p + G.nzl : (p >= G.nzl ? p - G.nzl : p);
-            mbar_expect_tx(b, LY.tx_bytes);
+            // z-halo planes feed only Y: own-cell slots are not loaded there
+            const bool edge = i == 0 || i == nplanes - 1;
+            mbar_expect_tx(b, edge ? LY.tx_edge : LY.tx_bytes);
             tma_load_4d(st, &a.tm_base, b, x0, y0, 0, q);
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
                 if (P.halo[s]) tma_load_4d(st + LY.off[s], &a.tm_slot[s], b, x0, y0, 0, q);
-                else tma_load_4d(st + LY.off[s], &a.tm_slot[s], b, x0, y0 + 1, 0, q);
+                else if (!edge) tma_load_4d(st + LY.off[s], &a.tm_slot[s], b, x0, y0 + 1, 0, q);
             }
         }
     };
@@ -294,6 +313,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         }
     };
     constexpr bool HAS_PREV_E = has_prev_e(P);
+    constexpr bool DNEW = P.dnew;
 
     if (tid == 0) {
 #pragma unroll
@@ -306,8 +326,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         for (int i = 0; i < n0; ++i) issue(i);
     }
 
-    double Ym[ROWS][2], Yc[ROWS][2], Yp[ROWS][2];
-    ES Ec[ROWS] = {}, En[ROWS] = {};
+    double Y0[ROWS][2], Y1[ROWS][2], Y2[ROWS][2];  // Y at planes z-1, z, z+1 (rotating)
+    ES Ec[ROWS] = {}, En[ROWS] = {};               // !YD: epilogue state of planes z, z+1
     double rmax = 0.0;               // running max of the ratio (exact)
     unsigned long long rbits = 0ull;  // its bit pattern (NaN-propagating)
 
@@ -320,36 +340,39 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         const bool gh = plane_is_ghost(a, zb - 1);
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-            Ym[r][0] = y_at(s0, 0, pos[r], gh);
-            Ym[r][1] = y_at(s0, 1, pos[r], gh);
+            Y0[r][0] = y_at(s0, 0, pos[r], gh);
+            Y0[r][1] = y_at(s0, 1, pos[r], gh);
         }
         wait_plane(1);
         const unsigned char* s1 = stage_of(1);
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-            Yc[r][0] = y_at(s1, 0, pos[r], false);
-            Yc[r][1] = y_at(s1, 1, pos[r], false);
-            sY[pos[r]] = Yc[r][0];
-            sY[BOX + pos[r]] = Yc[r][1];
-            if (own[r]) make_estate(s1, r, Ec[r]);
+            Y1[r][0] = y_at(s1, 0, pos[r], false);
+            Y1[r][1] = y_at(s1, 1, pos[r], false);
+            if constexpr (!YD) {
+                sY[pos[r]] = Y1[r][0];
+                sY[BOX + pos[r]] = Y1[r][1];
+                if (own[r]) make_estate(s1, r, Ec[r]);
+            }
         }
-        if (hal) {
-            sY[pos_h] = y_at(s1, 0, pos_h, false);
-            sY[BOX + pos_h] = y_at(s1, 1, pos_h, false);
+        if constexpr (!YD) {
+            if (hal) {
+                sY[pos_h] = y_at(s1, 0, pos_h, false);
+                sY[BOX + pos_h] = y_at(s1, 1, pos_h, false);
+            }
         }
-        __syncthreads();
+        __syncthreads();  // ring stage 0 free (YD: stage 1 stays, it is the centre plane)
         if (tid == 0) {
             if (R < nplanes) issue(R);
-            if (R + 1 < nplanes) issue(R + 1);
+            if constexpr (!YD)
+                if (R + 1 < nplanes) issue(R + 1);
         }
     }
 
-    for (int z = zb; z < ze; ++z) {
+    // One output plane z: Ym, Yc hold Y(z-1), Y(z); Yp receives Y(z+1).
+    auto step = [&](int z, double (&Ym)[ROWS][2], double (&Yc)[ROWS][2], double (&Yp)[ROWS][2]) {
         const int i = z - zb + 2;  // plane z+1
-        const int b = (z - zb) & 1;
         const bool more = z + 1 < ze;  // plane z+1 is an output plane of this CTA
-        double* yc = sY + b * 2 * BOX;
-        double* yn = sY + (b ^ 1) * 2 * BOX;
         // [A] plane z+1 from the ring
         wait_plane(i);
         const unsigned char* si = stage_of(i);
@@ -358,21 +381,36 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         for (int r = 0; r < ROWS; ++r) {
             Yp[r][0] = y_at(si, 0, pos[r], gh);
             Yp[r][1] = y_at(si, 1, pos[r], gh);
-            if (more) {
-                yn[pos[r]] = Yp[r][0];
-                yn[BOX + pos[r]] = Yp[r][1];
-                if (own[r]) make_estate(si, r, En[r]);
-            }
         }
-        if (more && hal) {
-            yn[pos_h] = y_at(si, 0, pos_h, false);
-            yn[BOX + pos_h] = y_at(si, 1, pos_h, false);
+        const unsigned char* sc = stage_of(i - 1);  // YD: the centre plane's ring stage
+        const double* yc;                            // Y(z) tile + ring, [c][BH][BW]
+        if constexpr (YD) {
+            yc = reinterpret_cast<const double*>(sc);
+        } else {
+            const int b = (z - zb) & 1;
+            yc = sY + b * 2 * BOX;
+            double* yn = sY + (b ^ 1) * 2 * BOX;
+            if (more) {
+#pragma unroll
+                for (int r = 0; r < ROWS; ++r) {
+                    yn[pos[r]] = Yp[r][0];
+                    yn[BOX + pos[r]] = Yp[r][1];
+                    if (own[r]) make_estate(si, r, En[r]);
+                }
+                if (hal) {
+                    yn[pos_h] = y_at(si, 0, pos_h, false);
+                    yn[BOX + pos_h] = y_at(si, 1, pos_h, false);
+                }
+            }
         }
         // [C] stencil + reaction + epilogue at plane z
         const int64_t qo = (int64_t)z * G.ps;
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
             if (!own[r]) continue;
+            ES el;
+            if constexpr (YD) make_estate(sc, r, el);
+            const ES& ec = YD ? el : Ec[r];
             double L[2];
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -394,18 +432,18 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                 if constexpr (STORE_K) store_cell(a.out_k, G, slice, cell[r], f[c]);
                 if constexpr (AB) {
                     // u_{n+1} = u_n (+) g_0 f_n (+) g_1 f_{n-1} (+) ... newest first (R-24)
-                    double wv = add(Ec[r].w[c], mul(a.beta_new, f[c]));
+                    double wv = add(ec.w[c], mul(a.beta_new, f[c]));
 #pragma unroll
-                    for (int s = 0; s < NS; ++s) wv = add(wv, mul(a.beta[s], Ec[r].h[s][c]));
+                    for (int s = 0; s < NS; ++s) wv = add(wv, mul(a.beta[s], ec.h[s][c]));
                     store_cell(a.out_u, G, slice, cell[r], wv);
                 }
                 if constexpr (FIN) {
-                    const double wv = P.bnew ? add(Ec[r].w[c], mul(a.beta_new, f[c])) : Ec[r].w[c];
+                    const double wv = P.bnew ? add(ec.w[c], mul(a.beta_new, f[c])) : ec.w[c];
                     store_cell(a.out_u, G, slice, cell[r], wv);
                 }
-                double e = Ec[r].e[c];
+                double e = ec.e[c];
                 if constexpr (ESUM || EPI == EPI_TAIL_ERR) {
-                    if constexpr (P.dnew) {
+                    if constexpr (DNEW) {
                         const double t = mul(a.delta_new, f[c]);
                         e = HAS_PREV_E ? add(e, t) : t;
                     }
@@ -415,7 +453,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                     // r = |e| / d exactly; skip the division when e == 0 (r = +0) or when
                     // |e| <= rmax*d*(1-2^-52) (a normal number) proves r <= rmax by
                     // monotone rounding; NaN never skips.
-                    const double ae = fabs(e), dd = Ec[r].d[c];
+                    const double ae = fabs(e), dd = ec.d[c];
                     const double th = mul(mul(rmax, dd), 0.99999999999999978);
                     if (!(ae == 0.0 || (ae <= th && th >= 2.2250738585072014e-308))) {
                         const double rr = ae / dd;
@@ -428,14 +466,32 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                 }
             }
         }
+        if constexpr (!YD) {
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) Ec[r] = En[r];
+        }
+        __syncthreads();  // !YD: Y(z+1) tile complete, stage of plane z+1 free; YD: plane z free
+        if (tid == 0) {
+            const int nx_issue = YD ? i - 1 + R : i + R;
+            if (nx_issue < nplanes) issue(nx_issue);
+        }
+    };
+
+    int z = zb;
+    if constexpr (ROWS == 2 || YD) {  // rotate the z queue by renaming: no register moves
+        for (; z + 2 < ze; z += 3) {
+            step(z, Y0, Y1, Y2);
+            step(z + 1, Y1, Y2, Y0);
+            step(z + 2, Y2, Y0, Y1);
+        }
+    }
+    for (; z < ze; ++z) {
+        step(z, Y0, Y1, Y2);
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
-            Ym[r][0] = Yc[r][0]; Ym[r][1] = Yc[r][1];
-            Yc[r][0] = Yp[r][0]; Yc[r][1] = Yp[r][1];
-            Ec[r] = En[r];
+            Y0[r][0] = Y1[r][0]; Y0[r][1] = Y1[r][1];
+            Y1[r][0] = Y2[r][0]; Y1[r][1] = Y2[r][1];
         }
-        __syncthreads();  // Y(z+1) tile complete; ring stage of plane z+1 free
-        if (tid == 0 && i + R < nplanes) issue(i + R);
     }
     if constexpr (RATIO) block_max_to_global(rbits, a.errmax);
 }
