@@ -107,6 +107,11 @@ def lib():
         L.orc_ab_integrate.argtypes = [P, ctypes.c_int, dp, ctypes.c_double, ctypes.c_double,
                                        ctypes.c_int64, dp]
         L.orc_ab_integrate.restype = ctypes.c_int
+        L.orc_am_coefficients.argtypes = [ctypes.c_int, i64p, i64p]
+        L.orc_am_coefficients.restype = ctypes.c_int
+        L.orc_abm_integrate.argtypes = [P, ctypes.c_int, dp, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_int64, dp]
+        L.orc_abm_integrate.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -228,4 +233,25 @@ def ab_integrate(p: Problem, k: int, u, t0: float, dt: float, nsteps: int,
                                 _ptr(tr) if trajectory else None)
     if rc != OK:
         raise RuntimeError(f"orc_ab_integrate rc={rc}")
+    return (u, tr) if trajectory else u
+
+
+def am_coefficients(k: int) -> list:
+    """Adams–Moulton k-term corrector coefficients m_0..m_{k-1} (m_0 weighs f_{n+1}), Fractions."""
+    num, den = (ctypes.c_int64 * 8)(), (ctypes.c_int64 * 8)()
+    if lib().orc_am_coefficients(k, num, den) != k:
+        raise ValueError("k must be 1..8")
+    return [Fraction(num[j], den[j]) for j in range(k)]
+
+
+def abm_integrate(p: Problem, k: int, u, t0: float, dt: float, nsteps: int,
+                  trajectory: bool = False):
+    """Adams–Bashforth–Moulton k (PECE), nsteps fixed steps after the RKF78 bootstrap.
+    Returns the final state, or (final, trajectory[nsteps, count]) if trajectory."""
+    u = _arr(u).copy()
+    tr = np.empty((nsteps, u.size)) if trajectory else None
+    rc = lib().orc_abm_integrate(ctypes.byref(p), k, _ptr(u), t0, dt, nsteps,
+                                 _ptr(tr) if trajectory else None)
+    if rc != OK:
+        raise RuntimeError(f"orc_abm_integrate rc={rc}")
     return (u, tr) if trajectory else u

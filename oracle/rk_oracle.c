@@ -442,6 +442,74 @@ int orc_ab_integrate(const orc_problem* p, int k, double* u, double t0, double d
     return rc;
 }
 
+/* Adams–Moulton k-term coefficients m_0..m_{k-1} (m_0 weighs f_{n+1}, then f_n, f_{n-1} ...),
+ * the corrector of Table 1's "Adams-Bashforth-Moulton 1..8" row: the integrals over
+ * [t_n, t_{n+1}] of the Lagrange basis on t_{n+1}, t_n, ..., t_{n-k+2} (textbook values). */
+static const int64_t AM_NUM[8][8] = {
+    {1},
+    {1, 1},
+    {5, 8, -1},
+    {9, 19, -5, 1},
+    {251, 646, -264, 106, -19},
+    {475, 1427, -798, 482, -173, 27},
+    {19087, 65112, -46461, 37504, -20211, 6312, -863},
+    {36799, 139849, -121797, 123133, -88547, 41499, -11351, 1375},
+};
+static const int64_t AM_DEN[8] = {1, 2, 12, 24, 720, 1440, 60480, 120960};
+
+int orc_am_coefficients(int k, int64_t* num, int64_t* den) {
+    if (k < 1 || k > 8) return -1;
+    for (int j = 0; j < k; ++j) {
+        num[j] = AM_NUM[k - 1][j];
+        den[j] = AM_DEN[k - 1];
+    }
+    return k;
+}
+
+int orc_abm_integrate(const orc_problem* p, int k, double* u, double t0, double dt, int64_t nsteps,
+                      double* traj) {
+    if (k < 1 || k > 8 || !(dt > 0.0) || nsteps < 0) return ORC_ERR_ARG;
+    const int64_t count = p->n * p->ncomp;
+    double g[8], m[8];
+    for (int j = 0; j < k; ++j) {
+        g[j] = dt * ((double)AB_NUM[k - 1][j] / (double)AB_DEN[k - 1]);
+        m[j] = dt * ((double)AM_NUM[k - 1][j] / (double)AM_DEN[k - 1]);
+    }
+    double* f[8];
+    for (int j = 0; j < k; ++j) f[j] = (double*)malloc(sizeof(double) * (size_t)count);
+    double* un = (double*)malloc(sizeof(double) * (size_t)count);
+    double* fp = (double*)malloc(sizeof(double) * (size_t)count);
+    int rc = ORC_OK;
+    for (int64_t n = 0; n < nsteps; ++n) {
+        const double t = t0 + (double)n * dt;
+        orc_rhs(p, u, f[n % k]); /* E: f_n = F(t_n, u_n) */
+        if (n < k - 1) {
+            rc = orc_step(p, ORC_RKF78, t, dt, u, un, NULL); /* bootstrap (R-23) */
+            if (rc != ORC_OK) break;
+        } else {
+            /* P: predictor u_p = u_n + sum_{j<k} (dt*beta_j) f_{n-j}, newest first (R-24) */
+            for (int64_t e = 0; e < count; ++e) {
+                double w = u[e];
+                for (int j = 0; j < k; ++j) w = w + g[j] * f[(n - j) % k][e];
+                un[e] = w;
+            }
+            orc_rhs(p, un, fp); /* E: f_p = F(t_{n+1}, u_p) */
+            /* C: u_{n+1} = u_n + (dt*m_0) f_p + sum_{j=1}^{k-1} (dt*m_j) f_{n-j+1}, newest first */
+            for (int64_t e = 0; e < count; ++e) {
+                double w = u[e] + m[0] * fp[e];
+                for (int j = 1; j < k; ++j) w = w + m[j] * f[(n - j + 1) % k][e];
+                un[e] = w;
+            }
+        }
+        memcpy(u, un, sizeof(double) * (size_t)count);
+        if (traj) memcpy(traj + n * count, u, sizeof(double) * (size_t)count);
+    }
+    for (int j = 0; j < k; ++j) free(f[j]);
+    free(un);
+    free(fp);
+    return rc;
+}
+
 /* ------------------------------------------------------------------------------
  * Algebra ops.
  * --------------------------------------------------------------------------- */

@@ -100,6 +100,17 @@ int orc_ab_coefficients(int k, int64_t* num, int64_t* den);
 int orc_ab_integrate(const orc_problem* p, int k, double* u, double t0, double dt, int64_t nsteps,
                      double* traj);
 
+/* Adams–Moulton k-term corrector coefficients m_0..m_{k-1} (m_0 weighs f_{n+1}; then f_n,
+ * f_{n-1}, ...) as exact rationals (Table 1 "Adams-Bashforth-Moulton 1..8"). */
+int orc_am_coefficients(int k, int64_t* num, int64_t* den);
+
+/* Adams–Bashforth–Moulton k, PECE (R-26): the RKF78 bootstrap of R-23, then
+ * per step  E: f_n = F(u_n);  P: u_p = u_n + sum_{j<k} (dt*beta_j) f_{n-j};  E: f_p = F(u_p);
+ * C: u_{n+1} = u_n + (dt*m_0) f_p + sum_{j=1}^{k-1} (dt*m_j) f_{n-j+1}; both sums newest
+ * first (R-24).  Arguments and trajectory as orc_ab_integrate. */
+int orc_abm_integrate(const orc_problem* p, int k, double* u, double t0, double dt, int64_t nsteps,
+                      double* traj);
+
 /* Algebra ops ("for_each#" / "for_each_norm").
  * out = sum_{j=0}^{k-1} coef[j]*in[j], left to right, 1 <= k <= 14. */
 int orc_lincomb(int64_t count, double* out, int k, const double* coef, const double* const* in);
