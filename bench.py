@@ -175,7 +175,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
-    ap.add_argument("--legs", default="adaptive,rk4,e2e,cpu",
+    ap.add_argument("--legs", default="adaptive,rk4,rk4_native,exp512,small,e2e,cpu",
                     help="comma list of legs (profiling runs use e.g. --legs rk4)")
     ap.add_argument("--no-extra", action="store_true", help="same as --legs adaptive")
     ap.add_argument("--overlap", type=int, default=1, help="halo exchange overlapped (N > 1)")
@@ -312,7 +312,7 @@ def main():
         st.set_option(rk.OPT_HALO_OVERLAP, overlap)
         st.set(u0_dev)
         # Adams–Bashforth k: the first k-1 steps are RKF78 bootstrap steps; keep them untimed
-        nwarm = max(args.warmup, int(scheme[2:]) if scheme.startswith("ab") else 0)
+        nwarm = max(args.warmup, int(scheme.lstrip("abm")) if scheme.startswith("ab") else 0)
         for _ in range(nwarm):
             st.do_step(scheme, 0.0, 1.0)
         st.set_option(rk.OPT_TIMING, 1)
@@ -363,13 +363,128 @@ def main():
                 "h2d_bytes_per_step": u0.nbytes, "d2h_bytes_per_step": u0.nbytes + 8,
                 "steps": ke, "ms_per_step": mse / ke}
 
+    def native_rk4_leg():
+        # f4 ablation: RK4 from separate ops, every stage value and k_j
+        # through HBM (4 rk_eval_rhs + 4 rk_lincomb launches per step), vs the fused stages
+        from paper_2309_05331_b200.ablation import NativeRK4
+        st.set(u0_dev)
+        nat = NativeRK4(st)
+        for _ in range(args.warmup):
+            nat.step(1.0)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            nat.step(1.0)
+        ev1.record(stream)
+        barrier()
+        ms = max_over_ranks(ev0.elapsed_time(ev1))
+        nat.close()
+        # per cell and step: 4 x (Y or u -> k) + 3 x (u, k -> Y) + (u, k1..k4 -> u), 16 B arrays
+        bpc = 4 * 32 + 3 * 48 + 96
+        ach = bpc * cells_local * args.steps / (ms / 1e3) / 1e9
+        return {"value": cells_total * args.steps / (ms / 1e3), "ms_per_step": ms / args.steps,
+                "scheme": "rk4 unfused (4 eval_rhs + 4 lincomb launches per step)",
+                "algorithmic_bytes_per_cell_step": bpc, "achieved_gbs": ach, "frac_of_peak": ach / peak}
+
+    def exp512_leg():
+        # f4: the exponential-family workload: 512 x 512 = 262,144
+        # independent ODEs du/dt = u, block-split over the ranks (strong scaling), RK4
+        n_side = 512
+        nv = n_side * n_side
+        ve = ctx.vector(nv)
+        ve.set_rhs_exponential(1.0)
+        ue = rk_inputs.exp_family_u0(n_side)[ve.begin:ve.begin + ve.local].copy()
+        out = {"config": {"workload": "exp_family_512^2 (262,144 ODEs, du/dt=u), RK4 dt=1e-3",
+                          "partition": f"block x{world}", "scaling": "strong"}}
+        for mode, nstep in (("do_step", 200), ("integrate_const", 1000)):
+            ve.set(ue)
+            if mode == "do_step":
+                run = lambda: [ve.do_step("rk4", 0.0, 1e-3) for _ in range(nstep)]  # noqa: E731
+            else:
+                run = lambda: ve.integrate_const("rk4", 0.0, nstep * 1e-3, 1e-3)  # noqa: E731
+            for _ in range(args.warmup):
+                run()
+            ve.reset_stats()
+            barrier()
+            ev0.record(stream)
+            for _ in range(args.steps):
+                run()
+            ev1.record(stream)
+            barrier()
+            ms = max_over_ranks(ev0.elapsed_time(ev1))
+            out[mode] = {"value": nv * nstep * args.steps / (ms / 1e3), "unit": "element-updates/s",
+                         "ms_per_step": ms / (nstep * args.steps),
+                         "gpu_launches_per_step": ve.stats()["kernel_launches"] / (nstep * args.steps)}
+        ve.close()
+        return out
+
+    def small_configs_leg():
+        # f3: the launch-bound configs.  configs[2]: Gray–Scott 64^3 RK4 dt=1,
+        # integrate_const 0..20 launched step by step vs replayed from a CUDA graph
+        # (RK_OPT_USE_GRAPH); configs[1]: logistic N=1e6 DOPRI5 adaptive tol 1e-8 on [-5, 5]
+        # with the host-driven try loop vs the one-launch device loop (RK_OPT_DEVICE_LOOP)
+        out = {}
+        if world == 1:
+            n64 = 64
+            g = ctx.grid(n64, n64, n64, 2)
+            g.set_rhs_gray_scott(h=H)
+            u64 = rk_inputs.gray_scott_ic(n64, n64, n64, seed=42)
+            for graph in (0, 1):
+                g.set_option(rk.OPT_USE_GRAPH, graph)
+                g.set(u64)
+                g.integrate_const("rk4", 0.0, 20.0, 1.0)
+                ms = []
+                for _ in range(max(3, args.steps)):
+                    g.set(u64)
+                    torch.cuda.synchronize()
+                    ev0.record(stream)
+                    g.integrate_const("rk4", 0.0, 20.0, 1.0)
+                    ev1.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(ev0.elapsed_time(ev1))
+                m = statistics.median(ms)
+                out["gs64_rk4_graph" if graph else "gs64_rk4"] = {
+                    "value": n64 ** 3 * 20 / (m / 1e3), "unit": "cell-updates/s", "ms_per_step": m / 20,
+                    "config": "configs[2]: 64^3, RK4, dt=1, t in [0,20], median of integrate_const calls"}
+            g.close()
+            nv = 1000000
+            v = ctx.vector(nv)
+            v.set_rhs_logistic()
+            ul = rk_inputs.logistic_u0(nv)
+            for dl in (0, 1):
+                v.set_option(rk.OPT_DEVICE_LOOP, dl)
+                ms, tries = [], 0
+                for _ in range(max(3, args.steps)):
+                    v.set(ul)
+                    torch.cuda.synchronize()
+                    ev0.record(stream)
+                    a, r = v.integrate_adaptive("dopri5", -5.0, 5.0, 0.1, 1e-8, 1e-8)
+                    ev1.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(ev0.elapsed_time(ev1))
+                    tries = a + r
+                m = statistics.median(ms)
+                out["logistic_1e6_dopri5_device_loop" if dl else "logistic_1e6_dopri5"] = {
+                    "value": nv * tries / (m / 1e3), "unit": "element-tries/s", "ms_per_step": m / tries,
+                    "ms_per_integration": m, "tries": tries,
+                    "config": "configs[1]: N=1e6 logistic, DOPRI5 adaptive atol=rtol=1e-8, t in [-5,5], dt0=0.1"}
+            v.close()
+        return out
+
     line = adaptive_leg() if "adaptive" in legs else {}
     extra = {}
     if "rk4" in legs:
         extra["rk4"] = rk4_leg(args.overlap)
         if world > 1:
             extra["rk4_overlap_off"] = rk4_leg(0)
-    for sch in ("euler", "midpoint", "cash_karp54", "dopri5", "rkf78") + tuple(f"ab{k}" for k in range(1, 9)):
+    if "rk4_native" in legs:
+        extra["rk4_native"] = native_rk4_leg()
+    if "exp512" in legs:
+        extra["exp512"] = exp512_leg()
+    if "small" in legs:
+        extra["small_configs"] = small_configs_leg()
+    for sch in (("euler", "midpoint", "cash_karp54", "dopri5", "rkf78") + tuple(f"ab{k}" for k in range(1, 9))
+                + tuple(f"abm{k}" for k in range(1, 9))):
         # scheme sweep (configs[4])
         if sch in legs:
             extra[sch] = rk4_leg(args.overlap, sch)

@@ -77,7 +77,15 @@ typedef enum {
      * u_{n+1} = u_n + dt*sum_{j<k} beta_j F(u_{n-j}), summed newest first (R-24).          */
     RK_ADAMS_BASHFORTH1 = 11, RK_ADAMS_BASHFORTH2 = 12, RK_ADAMS_BASHFORTH3 = 13,
     RK_ADAMS_BASHFORTH4 = 14, RK_ADAMS_BASHFORTH5 = 15, RK_ADAMS_BASHFORTH6 = 16,
-    RK_ADAMS_BASHFORTH7 = 17, RK_ADAMS_BASHFORTH8 = 18
+    RK_ADAMS_BASHFORTH7 = 17, RK_ADAMS_BASHFORTH8 = 18,
+    /* Adams–Bashforth–Moulton k, PECE, order k, fixed dt only (Table 1; DESIGN.md
+     * R-26): the AB_k history and start-up above, then per step f_n = F(u_n),
+     * u_p = u_n + dt*sum_j beta_j f_{n-j}, u_{n+1} = u_n + dt*(m_0 F(u_p) + sum_{j>=1} m_j
+     * f_{n-j+1}) with the k-term Adams–Moulton weights m (newest first); 2 RHS per step.     */
+    RK_ADAMS_BASHFORTH_MOULTON1 = 21, RK_ADAMS_BASHFORTH_MOULTON2 = 22,
+    RK_ADAMS_BASHFORTH_MOULTON3 = 23, RK_ADAMS_BASHFORTH_MOULTON4 = 24,
+    RK_ADAMS_BASHFORTH_MOULTON5 = 25, RK_ADAMS_BASHFORTH_MOULTON6 = 26,
+    RK_ADAMS_BASHFORTH_MOULTON7 = 27, RK_ADAMS_BASHFORTH_MOULTON8 = 28
 } rk_scheme;
 
 /* Options for rk_set_option. */
@@ -89,7 +97,13 @@ typedef enum {
                                 self-exchange instead of in-kernel periodic wrap (testing) */
     RK_OPT_MAX_TRIES = 3,    /* adaptive: tries per step before RK_ERR_STALL (default 500) */
     RK_OPT_TIMING = 4,       /* 1: time every stage-kernel launch with CUDA events (stats) */
-    RK_OPT_USE_GRAPH = 5     /* 1: replay fixed-step grid steps from captured CUDA graphs    */
+    RK_OPT_USE_GRAPH = 5,    /* 1: rk_integrate_const of a grid (world == 1, no loopback, >= 5
+                                steps) replays pairs of steps from one captured CUDA graph
+                                (SURVEY f3): identical results, no per-launch host cost   */
+    RK_OPT_DEVICE_LOOP = 6   /* 1: rk_integrate_adaptive of a vector state (world == 1) runs
+                                as one cooperative kernel: tries, error max, controller and
+                                accept/reject on the device, no host sync per try (
+                                DESIGN.md R-27).  Same results; else the host loop is used.   */
 } rk_option;
 
 /* Counters since creation or the last rk_reset_stats. */
@@ -210,6 +224,13 @@ rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double
 rk_status rk_lincomb(rk_state out, int k, const double* coef, const rk_state* in);
 /* Global max |u| over all ranks (collective); NaN if any element is NaN. */
 rk_status rk_norm_inf(rk_state st, double* out);
+/* The right-hand side on its own: out.u = F(in.u) with in's RHS (Eq. 1a/1b, P:L208-209;
+ * Listing 2), the same arithmetic as a fused stage (R-17); a grid
+ * exchanges in's boundary planes first (collective when world > 1).  out: a state of the same
+ * kind and shape (its own RHS is ignored), distinct from in.  Together with rk_lincomb it is the
+ * unfused "native" stepping of the ablation.  Errors: RK_ERR_CONTRACT
+ * on a shape mismatch, RK_ERR_ARG if out == in, RK_ERR_STATE if in has no RHS. */
+rk_status rk_eval_rhs(rk_state in, rk_state out);
 
 rk_status rk_get_stats(rk_state st, rk_stats* out);
 rk_status rk_reset_stats(rk_state st);

@@ -19,6 +19,7 @@ EULER, RK4, CASH_KARP54, DOPRI5, FEHLBERG78, MIDPOINT = 0, 1, 2, 3, 4, 5
 SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5,
            "rkf78": FEHLBERG78, "midpoint": MIDPOINT}
 SCHEMES.update({f"ab{k}": 10 + k for k in range(1, 9)})  # Adams–Bashforth k (rk_b200.h)
+SCHEMES.update({f"abm{k}": 20 + k for k in range(1, 9)})  # Adams–Bashforth–Moulton k (PECE)
 
 
 def _scheme(s) -> int:
@@ -116,6 +117,7 @@ class State:
 
     def __init__(self, ctx: Context, h, grid: bool, dims, ncomp: int):
         self.ctx, self._h, self.grid, self.dims, self.ncomp = ctx, h, grid, dims, ncomp
+        self._rhs = None  # (setter name, args) of the last set_rhs_* call
         b, c, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         call("rk_state_local_range", h, ctypes.byref(b), ctypes.byref(c))
         call("rk_state_local_size", h, ctypes.byref(n))
@@ -155,12 +157,20 @@ class State:
     # ---- RHS / options -------------------------------------------------------------
     def set_rhs_exponential(self, lam: float) -> None:
         call("rk_set_rhs_exponential", self._h, lam)
+        self._rhs = ("set_rhs_exponential", (lam,))
 
     def set_rhs_logistic(self) -> None:
         call("rk_set_rhs_logistic", self._h)
+        self._rhs = ("set_rhs_logistic", ())
 
     def set_rhs_gray_scott(self, d1=2e-4, d2=1e-4, F=0.014, K=0.053, h=2.5 / 64) -> None:
         call("rk_set_rhs_gray_scott", self._h, d1, d2, F, K, h)
+        self._rhs = ("set_rhs_gray_scott", (d1, d2, F, K, h))
+
+    def copy_rhs_from(self, other: "State") -> None:
+        """Give this state the right-hand side last set on `other`."""
+        if other._rhs is not None:
+            getattr(self, other._rhs[0])(*other._rhs[1])
 
     def set_option(self, key: int, value: int) -> None:
         call("rk_set_option", self._h, key, value)
@@ -195,6 +205,10 @@ class State:
         c = (ctypes.c_double * max(k, 1))(*coef)
         hs = (ctypes.c_void_p * max(k, 1))(*[s._h for s in states])
         call("rk_lincomb", self._h, k, c, hs)
+
+    def eval_rhs(self, out: "State") -> None:
+        """out = F(self) with self's right-hand side (rk_eval_rhs)."""
+        call("rk_eval_rhs", self._h, out._h)
 
     def norm_inf(self) -> float:
         d = ctypes.c_double()

@@ -35,6 +35,29 @@ struct PwArgs {
 };
 cudaError_t launch_pointwise(int scheme, const PwArgs& a, cudaStream_t st, int num_sms);
 
+// K1 device-resident adaptive loop: the whole integrate_adaptive of a pointwise
+// RHS in one cooperative launch -- tries, grid-wide error max, controller (double-double pow,
+// rk_ddmath.cuh) and accept/reject all on the device, no host round trip per try.
+struct PwLoopResult {
+    int status;            // 0 ok, 5 diverged (NaN), 6 dt underflow, 7 stall (rk_status codes)
+    int which;             // buffer holding the final u (0: buf[0], 1: buf[1])
+    long long accepted, rejected;
+    double t, dt, last_E, last_dt;
+};
+struct PwLoopArgs {
+    double* buf[2];        // buf[0] = u on entry; ping-pong
+    int64_t count;
+    int rhs;
+    double lambda;
+    double t0, t1, dt0, atol, rtol;
+    double a[13][13], b[13], e[13];  // the scheme's coefficients as doubles (rat_double)
+    double e_rej, e_acc, emin;       // -1/(q-1), -1/p, 5^-p (host-computed, as the host controller)
+    int max_tries;
+    unsigned long long* red;         // [3] zeroed: per-try error-max slots (rotating)
+    PwLoopResult* res;
+};
+cudaError_t launch_pointwise_loop(int scheme, const PwLoopArgs& a, cudaStream_t st, int device);
+
 // K1 (Adams–Bashforth): nsteps k-step updates with the history in registers.
 struct AbPwArgs {
     double* u;         // in/out
@@ -44,8 +67,11 @@ struct AbPwArgs {
     double lambda;
     int nsteps;
     double g[8];       // dt*beta_j, newest first
+    double m[8];       // Adams–Bashforth–Moulton: dt*m_j corrector weights (m_0: F(u_p))
 };
 cudaError_t launch_ab_pointwise(int k, const AbPwArgs& a, cudaStream_t st, int num_sms);
+// K1 (Adams–Bashforth–Moulton, PECE): nsteps steps, history in registers, 2 RHS per step.
+cudaError_t launch_abm_pointwise(int k, const AbPwArgs& a, cudaStream_t st, int num_sms);
 // f = F(u) for a pointwise RHS (history bootstrap).
 cudaError_t launch_rhs_pointwise(const double* u, double* f, int64_t count, int rhs, double lambda,
                                  cudaStream_t st, int num_sms);

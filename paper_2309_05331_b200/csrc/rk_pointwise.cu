@@ -7,6 +7,11 @@
 // credits for Odeint's speed).  Expression trees follow DESIGN.md R-17 exactly:
 //   Y_i = u (+) (g_ij (x) k_j) over a_ij != 0, left to right;  u_new likewise with beta_j;
 //   e = (delta_j (x) k_j) (+) ... over e_j != 0;  r = |e| / (atol (+) rtol (x) (|u| (+) dt (x) |k1|)).
+#include <cooperative_groups.h>
+
+#include <cfloat>
+
+#include "rk_ddmath.cuh"
 #include "rk_device.cuh"
 #include "rk_kernels.cuh"
 #include "rk_tableau.h"
@@ -24,6 +29,25 @@ __host__ __device__ constexpr int s_eff(int S, bool err) {
     return n;
 }
 
+// Nonzero pattern of a tableau, evaluated at compile time: used through a constexpr object so
+// the rational arithmetic (err_weight's b - bhat with gcd reduction) can never be left to run
+// time inside the kernel.
+struct PwMask {
+    bool a[13][13];
+    bool b[13];
+    bool e[13];
+};
+template <int S>
+__host__ __device__ constexpr PwMask pw_mask() {
+    PwMask m{};
+    for (int i = 0; i < 13; ++i) {
+        for (int j = 0; j < 13; ++j) m.a[i][j] = a_nz(S, i, j);
+        m.b[i] = b_nz(S, i);
+        m.e[i] = e_nz(S, i);
+    }
+    return m;
+}
+
 template <int RHS>
 __device__ __forceinline__ double f_pointwise(double y, double lambda) {
     if constexpr (RHS == RHS_EXP) return mul(lambda, y);
@@ -33,6 +57,7 @@ __device__ __forceinline__ double f_pointwise(double y, double lambda) {
 template <int S, int RHS, bool ERR>
 __device__ __forceinline__ double pw_steps(double x, const PwArgs& a, unsigned long long& rmax) {
     constexpr int SE = s_eff(S, ERR);
+    constexpr PwMask M = pw_mask<S>();
     const int nsteps = ERR ? 1 : a.nsteps;
     for (int n = 0; n < nsteps; ++n) {
         double k[13];
@@ -41,19 +66,19 @@ __device__ __forceinline__ double pw_steps(double x, const PwArgs& a, unsigned l
             double y = x;
 #pragma unroll
             for (int j = 0; j < i; ++j)
-                if (a_nz(S, i, j)) y = add(y, mul(a.cf.g[i][j], k[j]));
+                if (M.a[i][j]) y = add(y, mul(a.cf.g[i][j], k[j]));
             k[i] = f_pointwise<RHS>(y, a.lambda);
         }
         double w = x;
 #pragma unroll
         for (int j = 0; j < SE; ++j)
-            if (b_nz(S, j)) w = add(w, mul(a.cf.beta[j], k[j]));
+            if (M.b[j]) w = add(w, mul(a.cf.beta[j], k[j]));
         if constexpr (ERR) {
             double e = 0.0;
             bool first = true;
 #pragma unroll
             for (int j = 0; j < SE; ++j) {
-                if (!e_nz(S, j)) continue;
+                if (!M.e[j]) continue;
                 const double t = mul(a.cf.delta[j], k[j]);
                 e = first ? t : add(e, t);
                 first = false;
@@ -107,6 +132,158 @@ static cudaError_t launch_s(const PwArgs& a, cudaStream_t st, int num_sms) {
     return launch_s_rhs<S, RHS_LOGISTIC>(a, st, num_sms);
 }
 
+// ---- device-resident adaptive loop (R-27) ------------------------
+// The host loop of rk_integrate_adaptive (Odeint integrate_adaptive; R-16) and its
+// controller (R-12), replayed on the device by every thread in lock step: each try runs the
+// K1 step of every element (pw_steps, the same arithmetic as the host-driven launch), the
+// error-ratio max is combined with one atomicMax per CTA and a grid-wide barrier, and all
+// threads then take the same accept/reject decision from the same E.  Only the final state
+// and the counters return to the host.
+__device__ __noinline__ double step_adjust_dev(double E, double e_rej, double e_acc, double emin, double dt,
+                                               int* ok) {
+    if (E > 1.0) {
+        double fac = __dmul_rn(0.9, pow_dd(E, e_rej));
+        if (fac < 0.2) fac = 0.2;
+        *ok = 0;
+        return __dmul_rn(dt, fac);
+    }
+    *ok = 1;
+    if (E < 0.5) {
+        double Ec = emin;
+        if (E > Ec) Ec = E;
+        return __dmul_rn(dt, __dmul_rn(0.9, pow_dd(Ec, e_acc)));
+    }
+    return dt;
+}
+
+template <int S, int RHS>
+__global__ void __launch_bounds__(256) pointwise_loop_kernel(const PwLoopArgs a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ PwArgs sa;        // this try's coefficients (dt * tableau)
+    __shared__ double s_dtn;     // controller result, computed once per CTA
+    __shared__ int s_ok;
+    constexpr int SE = s_eff(S, true);
+    const double* u = a.buf[0];
+    double* un = a.buf[1];
+    int which = 0;
+    double t = a.t0, dt = a.dt0, E = 0.0;
+    long long acc = 0, rej = 0;
+    unsigned tri = 0;
+    int status = 0;
+    while (__dsub_rn(a.t1, t) > DBL_EPSILON) {
+        if (__dsub_rn(__dadd_rn(t, dt), a.t1) > DBL_EPSILON) dt = __dsub_rn(a.t1, t);
+        int tries = 0;
+        for (;;) {
+            if (dt < __dmul_rn(16.0 * DBL_EPSILON, fmax(fabs(t), 1.0))) {
+                status = 6;
+                goto done;
+            }
+            for (int q = threadIdx.x; q < SE * SE; q += blockDim.x) {
+                const int i = q / SE, j = q % SE;
+                sa.cf.g[i][j] = __dmul_rn(dt, a.a[i][j]);
+            }
+            if (threadIdx.x < SE) {
+                sa.cf.beta[threadIdx.x] = __dmul_rn(dt, a.b[threadIdx.x]);
+                sa.cf.delta[threadIdx.x] = __dmul_rn(dt, a.e[threadIdx.x]);
+            }
+            if (threadIdx.x == 0) {
+                sa.lambda = a.lambda;
+                sa.dt = dt;
+                sa.atol = a.atol;
+                sa.rtol = a.rtol;
+            }
+            __syncthreads();
+            unsigned long long rmax = 0ull;
+            {
+                const int64_t n2 = a.count >> 1;
+                const double2* u2 = reinterpret_cast<const double2*>(u);
+                double2* o2 = reinterpret_cast<double2*>(un);
+                const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+                for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
+                    double2 v = u2[i];
+                    v.x = pw_steps<S, RHS, true>(v.x, sa, rmax);
+                    v.y = pw_steps<S, RHS, true>(v.y, sa, rmax);
+                    o2[i] = v;
+                }
+                if ((a.count & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+                    un[a.count - 1] = pw_steps<S, RHS, true>(u[a.count - 1], sa, rmax);
+            }
+            block_max_to_global(rmax, a.red + tri % 3);
+            grid.sync();
+            // slot (tri+2)%3 was last read before this barrier (try tri-1): clear it for try tri+2
+            if (blockIdx.x == 0 && threadIdx.x == 0) a.red[(tri + 2) % 3] = 0ull;
+            const unsigned long long eb = __ldcg(a.red + tri % 3);
+            ++tri;
+            E = __longlong_as_double((long long)eb);
+            if (isnan(E)) {
+                status = 5;
+                goto done;
+            }
+            if (threadIdx.x == 0) {  // same inputs in every CTA -> the same decision everywhere
+                int ok = 0;
+                s_dtn = step_adjust_dev(E, a.e_rej, a.e_acc, a.emin, dt, &ok);
+                s_ok = ok;
+            }
+            __syncthreads();
+            const double dtn = s_dtn;
+            const bool ok = s_ok != 0;
+            if (ok) {
+                const double* tmp = u;
+                u = un;
+                un = const_cast<double*>(tmp);
+                which ^= 1;
+                t = __dadd_rn(t, dt);
+                dt = dtn;
+                ++acc;
+                break;
+            }
+            dt = dtn;
+            ++rej;
+            if (++tries >= a.max_tries) {
+                status = 7;
+                goto done;
+            }
+        }
+    }
+done:
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.res->status = status;
+        a.res->which = which;
+        a.res->accepted = acc;
+        a.res->rejected = rej;
+        a.res->t = t;
+        a.res->dt = dt;
+        a.res->last_E = E;
+    }
+}
+
+template <int S, int RHS>
+static cudaError_t launch_loop_s_rhs(const PwLoopArgs& a, cudaStream_t st, int device) {
+    int per_sm = 0, sms = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pointwise_loop_kernel<S, RHS>, 256, 0);
+    if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = ((a.count + 1) / 2 + 255) / 256;
+    const int64_t cap = (int64_t)sms * per_sm;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    void* args[] = {const_cast<PwLoopArgs*>(&a)};
+    return cudaLaunchCooperativeKernel((void*)pointwise_loop_kernel<S, RHS>, dim3((unsigned)blocks), dim3(256),
+                                       args, 0, st);
+}
+
+cudaError_t launch_pointwise_loop(int scheme, const PwLoopArgs& a, cudaStream_t st, int device) {
+    const bool ex = a.rhs == RHS_EXP;
+    switch (scheme) {
+    case 2: return ex ? launch_loop_s_rhs<2, RHS_EXP>(a, st, device) : launch_loop_s_rhs<2, RHS_LOGISTIC>(a, st, device);
+    case 3: return ex ? launch_loop_s_rhs<3, RHS_EXP>(a, st, device) : launch_loop_s_rhs<3, RHS_LOGISTIC>(a, st, device);
+    case 4: return ex ? launch_loop_s_rhs<4, RHS_EXP>(a, st, device) : launch_loop_s_rhs<4, RHS_LOGISTIC>(a, st, device);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
 // ---- Adams–Bashforth (Table 1 multi-step row): f_n = F(u_n),
 // u_{n+1} = u_n (+) g_0 f_n (+) g_1 f_{n-1} (+) ... newest first (R-24).  The k-1
 // past slopes stay in registers across all nsteps; each element is read and written once.
@@ -155,6 +332,63 @@ cudaError_t launch_ab_pointwise(int k, const AbPwArgs& a, cudaStream_t st, int n
     case 6: return launch_ab_k<6>(a, b, st);
     case 7: return launch_ab_k<7>(a, b, st);
     case 8: return launch_ab_k<8>(a, b, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+// Adams–Bashforth–Moulton k, PECE (R-26), nsteps steps per launch:
+//   f = F(u_n); p = u_n (+) g_0 f (+) g_1 f_{n-1} ...; fp = F(p);
+//   u_{n+1} = u_n (+) m_0 fp (+) m_1 f (+) m_2 f_{n-1} ...   (newest first)
+template <int K, int RHS>
+__global__ void __launch_bounds__(256) abm_pointwise_kernel(const AbPwArgs a) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.count; i += stride) {
+        double x = a.u[i];
+        double h[K > 1 ? K - 1 : 1];
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j) h[j] = a.hist[j][i];
+        for (int n = 0; n < a.nsteps; ++n) {
+            const double f = f_pointwise<RHS>(x, a.lambda);
+            double p = add(x, mul(a.g[0], f));
+#pragma unroll
+            for (int j = 0; j < K - 1; ++j) p = add(p, mul(a.g[j + 1], h[j]));
+            const double fp = f_pointwise<RHS>(p, a.lambda);
+            double w = add(x, mul(a.m[0], fp));
+            if (K > 1) w = add(w, mul(a.m[1], f));
+#pragma unroll
+            for (int j = 0; j + 2 < K; ++j) w = add(w, mul(a.m[j + 2], h[j]));
+#pragma unroll
+            for (int j = K - 2; j > 0; --j) h[j] = h[j - 1];
+            if (K > 1) h[0] = f;
+            x = w;
+        }
+        a.u[i] = x;
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j) a.hist[j][i] = h[j];
+    }
+}
+
+template <int K>
+static cudaError_t launch_abm_k(const AbPwArgs& a, unsigned blocks, cudaStream_t st) {
+    if (a.rhs == RHS_EXP) abm_pointwise_kernel<K, RHS_EXP><<<blocks, 256, 0, st>>>(a);
+    else abm_pointwise_kernel<K, RHS_LOGISTIC><<<blocks, 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_abm_pointwise(int k, const AbPwArgs& a, cudaStream_t st, int num_sms) {
+    int64_t blocks = (a.count + 255) / 256;
+    if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+    if (blocks < 1) blocks = 1;
+    const unsigned b = (unsigned)blocks;
+    switch (k) {
+    case 1: return launch_abm_k<1>(a, b, st);
+    case 2: return launch_abm_k<2>(a, b, st);
+    case 3: return launch_abm_k<3>(a, b, st);
+    case 4: return launch_abm_k<4>(a, b, st);
+    case 5: return launch_abm_k<5>(a, b, st);
+    case 6: return launch_abm_k<6>(a, b, st);
+    case 7: return launch_abm_k<7>(a, b, st);
+    case 8: return launch_abm_k<8>(a, b, st);
     default: return cudaErrorInvalidValue;
     }
 }

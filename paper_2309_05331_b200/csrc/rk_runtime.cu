@@ -45,6 +45,7 @@ struct rk_ctx_s {
     int rank = 0, world = 1, device = 0;
     cudaStream_t stream = nullptr, comm = nullptr;
     bool own_stream = false;
+    cudaStream_t capture = nullptr;  // private stream for CUDA-graph capture (RK_OPT_USE_GRAPH)
     ncclComm_t nccl = nullptr;
     int num_sms = 148;
     rk_status poisoned = RK_OK;
@@ -139,7 +140,8 @@ struct rk_state_s {
     int rhs = RHS_NONE;
     double lambda = 0.0, d1 = 0.0, d2 = 0.0, F = 0.0, K = 0.0, h = 1.0;
     // options
-    bool overlap = true, loopback = false, timing = false, use_graph = false;
+    bool overlap = true, loopback = false, timing = false, use_graph = false, device_loop = false;
+    unsigned long long* d_loop = nullptr;  // device loop: [3] error-max slots + PwLoopResult
     int max_tries = 500;
     // stats
     rk_stats stats{};
@@ -244,7 +246,7 @@ static Coeffs coeffs_of(int scheme) {
     return C;
 }
 
-static bool valid_scheme(int s) { return (s >= RK_EULER && s <= RK_MIDPOINT) || is_ab_scheme(s); }
+static bool valid_scheme(int s) { return (s >= RK_EULER && s <= RK_MIDPOINT) || is_multistep(s); }
 
 struct StagePlan {
     int scheme = 0, adaptive = 0, stage = 0;
@@ -252,6 +254,7 @@ struct StagePlan {
     double g[kMaxSlots] = {0}, beta[kMaxSlots] = {0}, delta[kMaxSlots] = {0};
     double beta_new = 0.0, delta_new = 0.0;
     int out_hist = -1;  // >= 0: the stage writes its k into Adams–Bashforth history slot
+    double* out_ptr = nullptr;  // non-null: the stage's k goes here (rk_eval_rhs)
 };
 
 static std::vector<StagePlan> build_plan(int scheme, bool adaptive, double dt) {
@@ -315,7 +318,7 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     a.base = p.sp.base_unew ? st->u_new : st->u;
     a.tm_base = (p.sp.base_unew ? st->tm_unew : st->tm_u).m[hb];
     int ny = 0;
-    const bool ab = is_ab_scheme(p.scheme);  // slots are history entries, newest first
+    const bool ab = is_multistep(p.scheme);  // slots are history entries, newest first
     for (int s = 0; s < p.sp.nslots; ++s) {
         const int src = p.sp.src[s];
         const int box = hb + (p.sp.halo[s] ? 0 : 1);
@@ -329,8 +332,9 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     a.nyslots = ny;
     a.beta_new = p.beta_new;
     a.delta_new = p.delta_new;
-    a.out_k = p.out_hist >= 0 ? st->hist[p.out_hist]
-                              : (p.sp.out_k >= 0 ? st->k[p.sp.out_k] : nullptr);
+    a.out_k = p.out_ptr ? p.out_ptr
+                        : (p.out_hist >= 0 ? st->hist[p.out_hist]
+                                           : (p.sp.out_k >= 0 ? st->k[p.sp.out_k] : nullptr));
     a.out_u = p.sp.writes_u ? st->u_new : nullptr;
     a.errmax = st->d_err;
     a.dt = dt;
@@ -463,6 +467,7 @@ static rk_status halo_exchange(rk_state st) {
 
 static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
     rk_ctx ctx = st->ctx;
+    TRY(ensure_halo(st));  // every entry path (RK plans, Adams steps, eval_rhs) lands here
     GsStageArgs a = stage_args(st, p, dt, atol, rtol);
     const int nzl = (int)st->local;
     st->stats.rhs_evals += 1;
@@ -641,16 +646,21 @@ static rk_status ab_bootstrap_step(rk_state st, double dt) {
     return rk_fixed_step(st, RK_FEHLBERG78, dt);
 }
 
-// nsteps Adams–Bashforth steps (bootstrapping first while the history is short)
-static rk_status ab_steps(rk_state st, int k, double dt, int64_t nsteps) {
+// nsteps Adams–Bashforth (abm = false) or Adams–Bashforth–Moulton PECE (abm = true) steps,
+// bootstrapping first while the history is short (R-23); the history ring is shared: it holds
+// F at the past points of the trajectory whichever Adams method produced them.
+static rk_status ab_steps(rk_state st, int k, double dt, int64_t nsteps, bool abm = false) {
     TRY(ab_prepare(st, k, dt));
     while (nsteps > 0 && st->ab_count < k - 1) {
         TRY(ab_bootstrap_step(st, dt));
         --nsteps;
     }
     if (nsteps <= 0) return RK_OK;
-    double g[8];
-    for (int j = 0; j < k; ++j) g[j] = dt * rat_double(ab_beta(k, j));
+    double g[8], m[8];
+    for (int j = 0; j < k; ++j) {
+        g[j] = dt * rat_double(ab_beta(k, j));
+        m[j] = dt * rat_double(am_beta(k, j));
+    }
     if (!st->grid) {  // all remaining steps in one launch, history in registers
         AbPwArgs a{};
         a.u = st->u;
@@ -658,14 +668,40 @@ static rk_status ab_steps(rk_state st, int k, double dt, int64_t nsteps) {
         a.count = st->count;
         a.rhs = st->rhs;
         a.lambda = st->lambda;
-        for (int j = 0; j < k; ++j) a.g[j] = g[j];
+        for (int j = 0; j < k; ++j) {
+            a.g[j] = g[j];
+            a.m[j] = m[j];
+        }
         while (nsteps > 0) {
             a.nsteps = (int)std::min<int64_t>(nsteps, 1 << 20);
-            CK_CTX(st->ctx, launch_ab_pointwise(k, a, st->ctx->stream, st->ctx->num_sms));
+            if (abm) CK_CTX(st->ctx, launch_abm_pointwise(k, a, st->ctx->stream, st->ctx->num_sms));
+            else CK_CTX(st->ctx, launch_ab_pointwise(k, a, st->ctx->stream, st->ctx->num_sms));
             st->stats.kernel_launches += 1;
-            st->stats.rhs_evals += a.nsteps;
+            st->stats.rhs_evals += (abm ? 2 : 1) * (int64_t)a.nsteps;
             st->stats.steps += a.nsteps;
             nsteps -= a.nsteps;
+        }
+        return RK_OK;
+    }
+    if (abm) {
+        for (; nsteps > 0; --nsteps) {
+            StagePlan e;  // E: f_n = F(u_n) into the scratch slot
+            e.scheme = RK_RK4;
+            e.stage = 0;
+            e.sp = stage_spec(RK_RK4, false, 0);
+            e.out_hist = k - 1;
+            TRY(run_gs_stage(st, e, dt, 0.0, 0.0));
+            StagePlan p;  // PEC: Y = u_p from f_n .. f_{n-k+1}; corrector into u_new
+            p.scheme = kSchemeABM0 + k;
+            p.stage = 0;
+            p.sp = stage_spec(p.scheme, false, 0);
+            for (int s = 0; s < k; ++s) p.g[s] = g[s];
+            for (int s = 0; s < k - 1; ++s) p.beta[s] = m[s + 1];
+            p.beta_new = m[0];
+            TRY(run_gs_stage(st, p, dt, 0.0, 0.0));
+            swap_u(st);
+            ab_rotate(st);
+            st->stats.steps += 1;
         }
         return RK_OK;
     }
@@ -688,6 +724,7 @@ static rk_status ab_steps(rk_state st, int k, double dt, int64_t nsteps) {
 // one fixed step of any scheme (public do_step / integrate_const path)
 static rk_status fixed_step(rk_state st, int scheme, double dt) {
     if (is_ab_scheme(scheme)) return ab_steps(st, scheme - kSchemeAB0, dt, 1);
+    if (is_abm_scheme(scheme)) return ab_steps(st, scheme - kSchemeABM0, dt, 1, true);
     ab_invalidate(st);
     return rk_fixed_step(st, scheme, dt);
 }
@@ -735,6 +772,109 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
     *E_out = E;
     *dt_next = dtn;
     return RK_OK;
+}
+
+// RK_OPT_USE_GRAPH: fixed grid steps replayed from one CUDA graph.  The stage
+// launches of two consecutive steps (u/u_new ping-pong back to the starting buffers) are
+// captured once and replayed, removing the per-launch host cost that bounds small grids
+// (configs[2], 64^3).  Single GPU without the halo path; the launches are the same kernels
+// with the same arguments, so results are identical.
+static rk_status graph_steps(rk_state st, int scheme, double dt, int64_t n) {
+    rk_ctx ctx = st->ctx;
+    TRY(fixed_step(st, scheme, dt));  // allocates the k buffers, configures the kernels
+    --n;
+    const rk_stats before = st->stats;
+    // capture on a private stream (the ctx stream may be the legacy default stream, which
+    // cannot be captured); the graph is then launched on the ctx stream
+    if (!ctx->capture) CK_CTX(ctx, cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    const cudaStream_t work = ctx->stream;
+    CK_CTX(ctx, cudaStreamBeginCapture(ctx->capture, cudaStreamCaptureModeThreadLocal));
+    ctx->stream = ctx->capture;
+    rk_status rc = fixed_step(st, scheme, dt);
+    if (rc == RK_OK) rc = fixed_step(st, scheme, dt);
+    ctx->stream = work;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->capture, &graph);
+    TRY(rc);
+    CK_CTX(ctx, ce);
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK_CTX(ctx, ie);
+    // the capture ran the host bookkeeping of 2 steps (stats, pointer swaps) but no kernels
+    const int64_t dl = st->stats.kernel_launches - before.kernel_launches;
+    const int64_t ds = st->stats.stage_launches - before.stage_launches;
+    const int64_t dr = st->stats.rhs_evals - before.rhs_evals;
+    const int64_t db = st->stats.stage_bytes - before.stage_bytes;
+    const int64_t pairs = n / 2;
+    for (int64_t i = 0; i < pairs; ++i) CK_CTX(ctx, cudaGraphLaunch(exec, ctx->stream));
+    cudaGraphExecDestroy(exec);
+    st->stats.kernel_launches += dl * (pairs - 1);
+    st->stats.stage_launches += ds * (pairs - 1);
+    st->stats.rhs_evals += dr * (pairs - 1);
+    st->stats.stage_bytes += db * (pairs - 1);
+    st->stats.steps += 2 * (pairs - 1);
+    if (n % 2) TRY(fixed_step(st, scheme, dt));
+    return RK_OK;
+}
+
+// The whole adaptive integration of a vector state in one cooperative launch (RK_OPT_DEVICE_LOOP).
+static rk_status device_adaptive_loop(rk_state st, int scheme, double t0, double t1, double dt0,
+                                      double atol, double rtol, int64_t* accepted, int64_t* rejected) {
+    rk_ctx ctx = st->ctx;
+    const Coeffs C = coeffs_of(scheme);
+    ab_invalidate(st);
+    st->k1_valid = false;
+    if (!st->d_loop) {
+        void* p = nullptr;
+        CK_CTX(ctx, cudaMalloc(&p, 3 * sizeof(unsigned long long) + sizeof(PwLoopResult)));
+        st->d_loop = static_cast<unsigned long long*>(p);
+    }
+    PwLoopArgs a{};
+    a.buf[0] = st->u;
+    a.buf[1] = st->u_new;
+    a.count = st->count;
+    a.rhs = st->rhs;
+    a.lambda = st->lambda;
+    a.t0 = t0;
+    a.t1 = t1;
+    a.dt0 = dt0;
+    a.atol = atol;
+    a.rtol = rtol;
+    for (int i = 0; i < 13; ++i) {
+        for (int j = 0; j < 13; ++j) a.a[i][j] = C.a[i][j];
+        a.b[i] = C.b[i];
+        a.e[i] = C.e[i];
+    }
+    a.e_rej = -1.0 / (double)(C.err_order - 1);  // the host controller's exponents (step_adjust)
+    a.e_acc = -1.0 / (double)C.order;
+    a.emin = std::pow(5.0, -(double)C.order);
+    a.max_tries = st->max_tries;
+    a.red = st->d_loop;
+    a.res = reinterpret_cast<PwLoopResult*>(st->d_loop + 3);
+    CK_CTX(ctx, cudaMemsetAsync(st->d_loop, 0, 3 * sizeof(unsigned long long) + sizeof(PwLoopResult), ctx->stream));
+    CK_CTX(ctx, launch_pointwise_loop(scheme, a, ctx->stream, ctx->device));
+    PwLoopResult r{};
+    CK_CTX(ctx, cudaMemcpyAsync(&r, a.res, sizeof r, cudaMemcpyDeviceToHost, ctx->stream));
+    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    if (r.which) swap_u(st);
+    const int64_t tries = r.accepted + r.rejected;
+    st->stats.kernel_launches += 1;
+    st->stats.tries += tries;
+    st->stats.accepted += r.accepted;
+    st->stats.rejected += r.rejected;
+    st->stats.rhs_evals += tries * (int64_t)num_stages(scheme, true);
+    st->stats.last_err_ratio = r.last_E;
+    st->stats.last_dt = r.dt;
+    if (accepted) *accepted = r.accepted;
+    if (rejected) *rejected = r.rejected;
+    switch (r.status) {
+    case 0: return RK_OK;
+    case 5: return fail(RK_ERR_DIVERGED, "non-finite error ratio at t=%.17g dt=%.17g", r.t, r.dt);
+    case 6: return fail(RK_ERR_DT_UNDERFLOW, "dt underflow at t=%.17g", r.t);
+    case 7: return fail(RK_ERR_STALL, "more than %d tries at t=%.17g", st->max_tries, r.t);
+    default: return fail(RK_ERR_CUDA, "device loop status %d", r.status);
+    }
 }
 
 // ====================================================================================
@@ -870,6 +1010,7 @@ rk_status rk_ctx_destroy(rk_ctx ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
     if (ctx->comm) cudaStreamDestroy(ctx->comm);
+    if (ctx->capture) cudaStreamDestroy(ctx->capture);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     cudaFree(ctx->d_scratch);
     cudaFreeHost(ctx->h_scratch);
@@ -967,6 +1108,7 @@ rk_status rk_state_destroy(rk_state st) {
     cudaFree(st->ghostbuf);
     cudaFree(st->d_err);
     cudaFreeHost(st->h_err);
+    cudaFree(st->d_loop);
     if (st->ev_pack) cudaEventDestroy(st->ev_pack);
     if (st->ev_halo) cudaEventDestroy(st->ev_halo);
     for (auto& p : st->pending) {
@@ -1099,6 +1241,7 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
         break;
     case RK_OPT_TIMING: st->timing = value != 0; break;
     case RK_OPT_USE_GRAPH: st->use_graph = value != 0; break;
+    case RK_OPT_DEVICE_LOOP: st->device_loop = value != 0; break;
     default: return fail(RK_ERR_ARG, "unknown option %d", key);
     }
     return RK_OK;
@@ -1145,6 +1288,8 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
     }
     if (is_ab_scheme(scheme)) {
         TRY(ab_steps(st, scheme - kSchemeAB0, dt, n));
+    } else if (is_abm_scheme(scheme)) {
+        TRY(ab_steps(st, scheme - kSchemeABM0, dt, n, true));
     } else if (!st->grid) {
         // pointwise RHS: all n steps of every element in registers, chunked launches
         ab_invalidate(st);
@@ -1157,6 +1302,8 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
         }
         st->k1_valid = false;
         st->stats.steps += n;
+    } else if (st->use_graph && !halo_path(st) && !st->timing && n >= 5) {
+        TRY(graph_steps(st, scheme, dt, n));
     } else {
         for (int64_t i = 0; i < n; ++i) TRY(fixed_step(st, scheme, dt));
     }
@@ -1176,6 +1323,8 @@ rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double
         return fail(RK_ERR_UNSUPPORTED, "scheme %d has no embedded error estimate", (int)scheme);
     TRY(check_rhs(st));
     DeviceGuard g(st->ctx->device);
+    if (st->device_loop && !st->grid && st->ctx->world == 1)
+        return device_adaptive_loop(st, scheme, t0, t1, dt0, atol, rtol, accepted, rejected);
     int64_t acc = 0, rej = 0;
     double t = t0, dt = dt0;
     rk_status rc = RK_OK;
@@ -1251,6 +1400,32 @@ rk_status rk_norm_inf(rk_state st, double* out) {
     CK_CTX(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
     std::memcpy(out, ctx->h_scratch, 8);
+    return RK_OK;
+}
+
+rk_status rk_eval_rhs(rk_state in, rk_state out) {
+    TRY(check_state(in));
+    TRY(check_state(out));
+    if (in == out) return fail(RK_ERR_ARG, "eval_rhs: out must differ from in");
+    if (in->ctx != out->ctx || in->count != out->count || in->grid != out->grid || in->ncomp != out->ncomp ||
+        in->nx != out->nx || in->ny != out->ny || in->nz != out->nz || in->n != out->n)
+        return fail(RK_ERR_CONTRACT, "eval_rhs: out does not conform to in");
+    TRY(check_rhs(in));
+    rk_ctx ctx = in->ctx;
+    DeviceGuard g(ctx->device);
+    if (in->grid) {
+        // the k1 = F(u) stage kernel of every scheme, its output redirected to out.u
+        StagePlan p = build_plan(RK_RK4, false, 0.0)[0];
+        p.out_ptr = out->u;
+        TRY(ensure_halo(in));
+        TRY(run_gs_stage(in, p, 0.0, 0.0, 0.0));
+    } else {
+        CK_CTX(ctx, launch_rhs_pointwise(in->u, out->u, in->count, in->rhs, in->lambda, ctx->stream, ctx->num_sms));
+        in->stats.kernel_launches += 1;
+        in->stats.rhs_evals += 1;
+    }
+    out->k1_valid = false;
+    ab_invalidate(out);
     return RK_OK;
 }
 

@@ -23,12 +23,18 @@ enum Epilogue {
     EPI_FINAL_ERR = 2,    // EPI_FINAL + error ratio max
     EPI_FINAL_EPART = 3,  // EPI_FINAL + store e' = e + delta_i k_i
     EPI_TAIL_ERR = 4,     // Y = u_new (base); store k_i; e = e' + delta_i k_i; ratio max
-    EPI_AB = 5            // Adams–Bashforth: store f_n; u_new = u + g_0 f_n + sum_s g_s h_s
+    EPI_AB = 5,           // Adams–Bashforth: store f_n; u_new = u + g_0 f_n + sum_s g_s h_s
+    EPI_ABM = 6           // ABM corrector: Y = u_p (slots), u_new = u + m_0 F(u_p) + sum_s m_s h_s
 };
 
 // Scheme ids of the Adams–Bashforth k-step methods (rk_b200.h RK_ADAMS_BASHFORTH1..8).
 constexpr int kSchemeAB0 = 10;
 __host__ __device__ constexpr bool is_ab_scheme(int S) { return S > kSchemeAB0 && S <= kSchemeAB0 + 8; }
+// ... and of the Adams–Bashforth–Moulton (PECE) methods (RK_ADAMS_BASHFORTH_MOULTON1..8)
+constexpr int kSchemeABM0 = 20;
+__host__ __device__ constexpr bool is_abm_scheme(int S) { return S > kSchemeABM0 && S <= kSchemeABM0 + 8; }
+// schemes whose slots are Adams history entries (resolved by the host's history ring)
+__host__ __device__ constexpr bool is_multistep(int S) { return is_ab_scheme(S) || is_abm_scheme(S); }
 
 constexpr int kMaxSlots = 10;  // RKF78 adaptive final stage: k1, k4..k12
 constexpr int SLOT_U = -1;  // slot source: the state u itself (TAIL stage: old u)
@@ -78,7 +84,7 @@ __host__ __device__ constexpr int stage_rows(const StageSpec& P) {
 }
 
 __host__ __device__ constexpr int num_stages(int S, bool ad) {
-    return is_ab_scheme(S) ? 1 : last_stage(tableau_of(S), ad) + 1;
+    return is_multistep(S) ? 1 : last_stage(tableau_of(S), ad) + 1;
 }
 
 __host__ __device__ constexpr StageSpec stage_spec(int S, bool ad, int i) {
@@ -99,6 +105,27 @@ __host__ __device__ constexpr StageSpec stage_spec(int S, bool ad, int i) {
         p.bnew = true;
         p.writes_u = true;
         p.out_k = 0;
+        return p;
+    }
+    if (is_abm_scheme(S)) {
+        // PEC of one PECE step (the final E, F(u_{n+1}), is the next step's k1-type launch):
+        // slot 0 = f_n (history scratch, just evaluated), slot s = f_{n-s}; all enter
+        // Y = u_p = u + sum_s (dt beta_s) slot_s; the corrector adds m_0 F(u_p) first, then
+        // m_{s+1} slot_s for s < k-1 (newest first, R-26).  No k is stored.
+        if (ad || i != 0) return p;
+        const int k = S - kSchemeABM0;
+        p.valid = 1;
+        p.epi = EPI_ABM;
+        p.nslots = k;
+        for (int s = 0; s < k; ++s) {
+            p.src[s] = s == 0 ? k - 1 : s - 1;  // history ring positions (host rk_runtime.cu)
+            p.j[s] = s;
+            p.halo[s] = true;
+            p.gnz[s] = true;
+            p.bnz[s] = s < k - 1;
+        }
+        p.bnew = true;
+        p.writes_u = true;
         return p;
     }
     const Tableau T = tableau_of(S);

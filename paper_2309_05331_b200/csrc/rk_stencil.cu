@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     constexpr bool ESUM = EPI == EPI_FINAL_ERR || EPI == EPI_FINAL_EPART;  // e from slots
     constexpr bool RATIO = EPI == EPI_FINAL_ERR || EPI == EPI_TAIL_ERR;
     constexpr bool STORE_K = EPI == EPI_K || EPI == EPI_TAIL_ERR || EPI == EPI_AB;
-    constexpr bool AB = EPI == EPI_AB;
+    constexpr bool AB = EPI == EPI_AB || EPI == EPI_ABM;  // Adams epilogue (raw own-cell terms)
     using ES = EState<AB ? NS : 0>;
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr bool YD = LY.ydirect;
@@ -431,10 +431,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                 const int64_t slice = qo + c * G.cs;
                 if constexpr (STORE_K) store_cell(a.out_k, G, slice, cell[r], f[c]);
                 if constexpr (AB) {
-                    // u_{n+1} = u_n (+) g_0 f_n (+) g_1 f_{n-1} (+) ... newest first (R-24)
+                    // u_{n+1} = u_n (+) g_0 f (+) g_1 h_0 (+) ... newest first (R-24, R-26);
+                    // AB: f = f_n, h = f_{n-1}...; ABM: f = F(u_p), h = f_n, f_{n-1}...
                     double wv = add(ec.w[c], mul(a.beta_new, f[c]));
 #pragma unroll
-                    for (int s = 0; s < NS; ++s) wv = add(wv, mul(a.beta[s], ec.h[s][c]));
+                    for (int s = 0; s < NS; ++s)
+                        if (P.bnz[s]) wv = add(wv, mul(a.beta[s], ec.h[s][c]));
                     store_cell(a.out_u, G, slice, cell[r], wv);
                 }
                 if constexpr (FIN) {
@@ -653,6 +655,14 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
     case 32: return launch_one<16, 0, 0>(a, grid, st);
     case 34: return launch_one<17, 0, 0>(a, grid, st);
     case 36: return launch_one<18, 0, 0>(a, grid, st);
+    case 42: return launch_one<21, 0, 0>(a, grid, st);  // Adams–Bashforth–Moulton 1..8: PEC launch
+    case 44: return launch_one<22, 0, 0>(a, grid, st);
+    case 46: return launch_one<23, 0, 0>(a, grid, st);
+    case 48: return launch_one<24, 0, 0>(a, grid, st);
+    case 50: return launch_one<25, 0, 0>(a, grid, st);
+    case 52: return launch_one<26, 0, 0>(a, grid, st);
+    case 54: return launch_one<27, 0, 0>(a, grid, st);
+    case 56: return launch_one<28, 0, 0>(a, grid, st);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -129,4 +129,22 @@ __host__ __device__ constexpr Rat ab_beta(int k, int j) {
     return (k >= 1 && k <= 8 && j >= 0 && j < k) ? T[k - 1][j] : Rat{0, 1};
 }
 
+// Adams–Moulton k-term weights m_j (j = 0 weighs f_{n+1}, then f_n, f_{n-1} ...), the corrector
+// of the Adams–Bashforth–Moulton row (R-26).  Standard values, reduced.
+__host__ __device__ constexpr Rat am_beta(int k, int j) {
+    constexpr Rat T[8][8] = {
+        {{1, 1}},
+        {{1, 2}, {1, 2}},
+        {{5, 12}, {2, 3}, {-1, 12}},
+        {{3, 8}, {19, 24}, {-5, 24}, {1, 24}},
+        {{251, 720}, {323, 360}, {-11, 30}, {53, 360}, {-19, 720}},
+        {{95, 288}, {1427, 1440}, {-133, 240}, {241, 720}, {-173, 1440}, {3, 160}},
+        {{19087, 60480}, {2713, 2520}, {-15487, 20160}, {586, 945}, {-6737, 20160}, {263, 2520},
+         {-863, 60480}},
+        {{5257, 17280}, {139849, 120960}, {-4511, 4480}, {123133, 120960}, {-88547, 120960},
+         {1537, 4480}, {-11351, 120960}, {275, 24192}},
+    };
+    return (k >= 1 && k <= 8 && j >= 0 && j < k) ? T[k - 1][j] : Rat{0, 1};
+}
+
 }  // namespace rkb

@@ -359,11 +359,14 @@ def test_ab_vector_bitwise(ctx, k, rhs):
 
 @pytest.mark.parametrize("k", [1, 2, 4, 8])
 @pytest.mark.parametrize("dims", [(16, 12, 10), (33, 17, 9)], ids=lambda d: "x".join(map(str, d)))
-def test_ab_grid_bitwise(ctx, k, dims):
+@pytest.mark.parametrize("loopback", [0, 1])
+def test_ab_grid_bitwise(ctx, k, dims, loopback):
+    import paper_2309_05331_b200 as rk
     nx, ny, nz = dims
     u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=7) + 0.01 * rk_inputs.random_state(
         2 * nx * ny * nz, 11).reshape(nz, 2, ny, nx)
     st = gs_state(ctx, nx, ny, nz, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, loopback)
     p = oracle.gray_scott_problem(nx, ny, nz)
     nsteps = k + 4
     for m in range(nsteps):
@@ -386,3 +389,248 @@ def test_ab_history_restarts(ctx):
     for _ in range(4):
         st.do_step("ab3", 0.0, 0.05)
     assert bitwise(st.get(), oracle.ab_integrate(p, 3, mid, 0.0, 0.05, 4))
+
+
+# ---------------------------------------------------------------------------------------
+# f4: rk_eval_rhs and the unfused "native" RK4 ablation
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dims", [(16, 16, 16), (33, 17, 9), (1, 1, 3), (70, 9, 20)],
+                         ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("loopback", [0, 1])
+def test_eval_rhs_grid_bitwise(ctx, dims, loopback):
+    import paper_2309_05331_b200 as rk
+    nx, ny, nz = dims
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=3) + 0.01 * rk_inputs.random_state(
+        2 * nx * ny * nz, 4).reshape(nz, 2, ny, nx)
+    st = gs_state(ctx, nx, ny, nz, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, loopback)
+    out = ctx.grid(nx, ny, nz, 2)
+    st.eval_rhs(out)
+    assert bitwise(out.get(), oracle.rhs(oracle.gray_scott_problem(nx, ny, nz), u0))
+    assert bitwise(st.get(), u0)  # input untouched
+
+
+@pytest.mark.parametrize("rhs", ["exp", "logistic"])
+def test_eval_rhs_vector_bitwise(ctx, rhs):
+    n = 100003
+    u0 = rk_inputs.logistic_u0(n) if rhs == "logistic" else rk_inputs.exp_decay_u0(n)
+    st = ctx.vector(n)
+    if rhs == "exp":
+        st.set_rhs_exponential(-0.7)
+        p = oracle.exp_problem(n, -0.7)
+    else:
+        st.set_rhs_logistic()
+        p = oracle.logistic_problem(n)
+    st.set(u0)
+    out = ctx.vector(n)
+    st.eval_rhs(out)
+    assert bitwise(out.get(), oracle.rhs(p, u0))
+
+
+def test_eval_rhs_errors(ctx):
+    import paper_2309_05331_b200 as rk
+    a, b = ctx.vector(10), ctx.vector(11)
+    with pytest.raises(rk.RKError) as e:
+        a.eval_rhs(a)
+    assert e.value.status == "RK_ERR_ARG"
+    a.set_rhs_logistic()
+    with pytest.raises(rk.RKError) as e:
+        a.eval_rhs(b)
+    assert e.value.status == "RK_ERR_CONTRACT"
+    c = ctx.vector(10)
+    with pytest.raises(rk.RKError) as e:
+        c.eval_rhs(a)  # no RHS on the input
+    assert e.value.status == "RK_ERR_STATE"
+
+
+@pytest.mark.parametrize("dims", [(33, 17, 9), (64, 64, 64)], ids=lambda d: "x".join(map(str, d)))
+def test_native_rk4_equals_fused_grid(ctx, dims):
+    """The unfused RK4 (eval_rhs + lincomb per stage) and the fused stage kernels evaluate the
+    same expression trees (R-17): bitwise equal to each other and to the oracle."""
+    from paper_2309_05331_b200.ablation import NativeRK4
+    nx, ny, nz = dims
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=42) + 0.01 * rk_inputs.random_state(
+        2 * nx * ny * nz, 5).reshape(nz, 2, ny, nx)
+    fused = gs_state(ctx, nx, ny, nz, u0)
+    native = gs_state(ctx, nx, ny, nz, u0)
+    nat = NativeRK4(native)
+    p = oracle.gray_scott_problem(nx, ny, nz)
+    u = u0
+    for k in range(3):
+        fused.do_step("rk4", float(k), 1.0)
+        nat.step(1.0)
+        u = oracle.step(p, oracle.RK4, float(k), 1.0, u)
+        assert bitwise(native.get(), fused.get()) and bitwise(native.get(), u), k
+    nat.close()
+
+
+def test_native_rk4_equals_fused_vector(ctx):
+    from paper_2309_05331_b200.ablation import NativeRK4
+    n = 262144  # the exponential-family 512^2 workload (P:L253)
+    u0 = rk_inputs.exp_family_u0(512)  # du/dt = u, u = A(x,y) e^t (P:L208, P:L212)
+    fused, native = ctx.vector(n), ctx.vector(n)
+    for s in (fused, native):
+        s.set_rhs_exponential(1.0)
+        s.set(u0)
+    nat = NativeRK4(native)
+    for k in range(4):
+        fused.do_step("rk4", 0.0, 0.01)
+        nat.step(0.01)
+    assert bitwise(native.get(), fused.get())
+    nat.close()
+
+
+# ---------------------------------------------------------------------------------------
+# Adams–Bashforth–Moulton k = 1..8, PECE (Table 1, P:L69; DESIGN.md R-26)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("k", range(1, 9))
+@pytest.mark.parametrize("rhs", ["exp", "logistic"])
+def test_abm_vector_bitwise(ctx, k, rhs):
+    n = 10001
+    if rhs == "exp":
+        u0 = rk_inputs.exp_decay_u0(n)
+        p = oracle.exp_problem(n, -1.0)
+    else:
+        u0 = rk_inputs.logistic_u0(n)
+        p = oracle.logistic_problem(n)
+    st = ctx.vector(n)
+    st.set_rhs_exponential(-1.0) if rhs == "exp" else st.set_rhs_logistic()
+    st.set(u0)
+    dt = 2.0 ** -5
+    steps = st.integrate_const(f"abm{k}", 0.0, 1.0, dt)
+    assert steps == _odeint_steps(0.0, 1.0, dt)
+    assert bitwise(st.get(), oracle.abm_integrate(p, k, u0, 0.0, dt, steps))
+    for _ in range(3):
+        st.do_step(f"abm{k}", 0.0, dt)
+    assert bitwise(st.get(), oracle.abm_integrate(p, k, u0, 0.0, dt, steps + 3))
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("dims", [(16, 12, 10), (33, 17, 9), (8, 8, 1)], ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("loopback", [0, 1])
+def test_abm_grid_bitwise(ctx, k, dims, loopback):
+    import paper_2309_05331_b200 as rk
+    nx, ny, nz = dims
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=8) + 0.01 * rk_inputs.random_state(
+        2 * nx * ny * nz, 12).reshape(nz, 2, ny, nx)
+    st = gs_state(ctx, nx, ny, nz, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, loopback)
+    p = oracle.gray_scott_problem(nx, ny, nz)
+    nsteps = k + 3
+    for m in range(nsteps):
+        st.do_step(f"abm{k}", float(m), 1.0)
+    assert bitwise(st.get(), oracle.abm_integrate(p, k, u0, 0.0, 1.0, nsteps))
+    st.set(u0)
+    assert st.integrate_const(f"abm{k}", 0.0, float(nsteps), 1.0) == nsteps
+    assert bitwise(st.get(), oracle.abm_integrate(p, k, u0, 0.0, 1.0, nsteps))
+
+
+def test_abm_stats_two_rhs_per_step(ctx):
+    n = 16
+    st = gs_state(ctx, n, n, n, rk_inputs.gray_scott_ic(n, n, n))
+    for _ in range(3):  # bootstrap of k = 4
+        st.do_step("abm4", 0.0, 1.0)
+    st.reset_stats()
+    st.do_step("abm4", 0.0, 1.0)
+    s = st.stats()
+    assert s["rhs_evals"] == 2 and s["stage_launches"] == 2
+
+
+# ---------------------------------------------------------------------------------------
+# f3: device-resident adaptive loop (RK_OPT_DEVICE_LOOP; DESIGN.md R-27)
+# ---------------------------------------------------------------------------------------
+def _adaptive_vec(ctx, rhs, n, u0, scheme, t0, t1, dt0, tol, device_loop, max_tries=None):
+    import paper_2309_05331_b200 as rk
+    st = ctx.vector(n)
+    st.set_rhs_exponential(-1.0) if rhs == "exp" else st.set_rhs_logistic()
+    st.set(u0)
+    st.set_option(rk.OPT_DEVICE_LOOP, 1 if device_loop else 0)
+    if max_tries:
+        st.set_option(rk.OPT_MAX_TRIES, max_tries)
+    a, r = st.integrate_adaptive(scheme, t0, t1, dt0, tol, tol)
+    s = st.stats()
+    return st.get(), a, r, s
+
+
+@pytest.mark.parametrize("scheme,tol,acc_rej", [("dopri5", 1e-8, (51, 2)), ("cash_karp54", 1e-8, None),
+                                                ("rkf78", 1e-10, None)])
+def test_device_loop_config2(ctx, scheme, tol, acc_rej):
+    """Config 2 through the one-launch device loop: counts and final state identical to the
+    oracle (and to the host-driven loop)."""
+    n = 1000000
+    u0 = rk_inputs.logistic_u0(n)
+    g, a, r, s = _adaptive_vec(ctx, "logistic", n, u0, scheme, -5.0, 5.0, 0.1, tol, True)
+    uo, ao, ro, rc = oracle.integrate_adaptive(oracle.logistic_problem(n), OS[scheme], u0, -5.0,
+                                               5.0, 0.1, tol, tol)
+    assert rc == 0 and (a, r) == (ao, ro)
+    if acc_rej:
+        assert (a, r) == acc_rej
+    assert bitwise(g, uo)
+    assert s["kernel_launches"] == 1 and s["tries"] == a + r
+
+
+@pytest.mark.parametrize("scheme", ["dopri5", "cash_karp54", "rkf78"])
+@pytest.mark.parametrize("tol", [1e-3, 1e-5, 1e-7, 1e-9, 1e-11, 1e-13])
+@pytest.mark.parametrize("rhs", ["exp", "logistic"])
+def test_device_loop_matches_host_loop(ctx, scheme, tol, rhs):
+    """Many controller evaluations (rejections included, dt0 too large on purpose): the device
+    controller's double-double pow reproduces the host's libm pow on every call."""
+    n = 30001
+    u0 = rk_inputs.logistic_u0(n) if rhs == "logistic" else rk_inputs.exp_decay_u0(n)
+    t0, t1 = (-5.0, 5.0) if rhs == "logistic" else (0.0, 3.0)
+    gd, ad, rd, sd = _adaptive_vec(ctx, rhs, n, u0, scheme, t0, t1, 2.0, tol, True)
+    gh, ah, rh, sh = _adaptive_vec(ctx, rhs, n, u0, scheme, t0, t1, 2.0, tol, False)
+    assert (ad, rd) == (ah, rh)
+    assert bitwise(gd, gh)
+    assert sd["last_dt"] == sh["last_dt"]
+
+
+def test_device_loop_errors(ctx):
+    import paper_2309_05331_b200 as rk
+    n = 1000
+    x = np.full(n, 0.5)
+    x[7] = np.nan
+    with pytest.raises(rk.RKError) as e:
+        _adaptive_vec(ctx, "logistic", n, x, "dopri5", 0.0, 1.0, 0.1, 1e-6, True)
+    assert e.value.status == "RK_ERR_DIVERGED"
+    with pytest.raises(rk.RKError) as e:  # dt0 = 50 needs several rejections: stall at 1 try
+        _adaptive_vec(ctx, "logistic", n, rk_inputs.logistic_u0(n), "dopri5", -5.0, 50.0, 50.0, 1e-10, True,
+                      max_tries=1)
+    assert e.value.status == "RK_ERR_STALL"
+
+
+@pytest.mark.parametrize("scheme,nsteps", [("rk4", 20), ("dopri5", 7), ("euler", 6), ("rkf78", 5)])
+def test_graph_replay_integrate_const(ctx, scheme, nsteps):
+    """RK_OPT_USE_GRAPH: the fixed steps replayed from a captured CUDA graph give the oracle's
+    state bitwise, and the same counters as launching them one by one."""
+    import paper_2309_05331_b200 as rk
+    n = 64
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42) + 0.01 * rk_inputs.random_state(2 * n ** 3, 6).reshape(n, 2, n, n)
+    p = oracle.gray_scott_problem(n, n, n)
+    uo, so = oracle.integrate_const(p, OS[scheme], u0, 0.0, float(nsteps), 1.0)
+    stats = []
+    for graph in (1, 0):
+        st = gs_state(ctx, n, n, n, u0)
+        st.set_option(rk.OPT_USE_GRAPH, graph)
+        assert st.integrate_const(scheme, 0.0, float(nsteps), 1.0) == so == nsteps
+        assert bitwise(st.get(), uo), graph
+        s = st.stats()
+        stats.append({k: s[k] for k in ("steps", "rhs_evals", "stage_launches", "kernel_launches", "stage_bytes")})
+        st.close()
+    assert stats[0] == stats[1]
+
+
+def test_graph_replay_on_torch_stream():
+    """The ctx stream may be torch's current (legacy default) stream, which cannot be captured:
+    the graph is captured on a private stream and replayed on the ctx stream."""
+    import torch
+    import paper_2309_05331_b200 as rk
+    c = rk.Context(0, 1, 0, torch.cuda.current_stream())
+    n = 32
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=1)
+    st = gs_state(c, n, n, n, u0)
+    st.set_option(rk.OPT_USE_GRAPH, 1)
+    assert st.integrate_const("rk4", 0.0, 9.0, 1.0) == 9
+    uo, _ = oracle.integrate_const(oracle.gray_scott_problem(n, n, n), oracle.RK4, u0, 0.0, 9.0, 1.0)
+    assert bitwise(st.get(), uo)
+    c.close()
