@@ -175,7 +175,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
-    ap.add_argument("--legs", default="adaptive,rk4,rk4_native,exp512,small,e2e,cpu",
+    ap.add_argument("--legs", default="adaptive,rk4,strong,rk4_native,exp512,small,e2e,cpu",
                     help="comma list of legs (profiling runs use e.g. --legs rk4)")
     ap.add_argument("--no-extra", action="store_true", help="same as --legs adaptive")
     ap.add_argument("--overlap", type=int, default=1, help="halo exchange overlapped (N > 1)")
@@ -471,23 +471,78 @@ def main():
             v.close()
         return out
 
+    def strong_leg():
+        # configs[3]: 512^3 in total, z-slab over the ranks (strong scaling), DOPRI5 adaptive
+        # tol 1e-6 and RK4 dt = 1, as the headline but with nz_local = 512 / N
+        sg = ctx.grid(n, n, n, 2)
+        sg.set_rhs_gray_scott(h=H)
+        sg.set_option(rk.OPT_HALO_OVERLAP, args.overlap)
+        us = torch.from_numpy(rk_inputs.gray_scott_ic(n, n, n, seed=42, z0=sg.begin, nzl=sg.local,
+                                                      zblocks=1)).cuda(local)
+        sg.set(us)
+        t, dt = 0.0, 1.0
+
+        def acc_step():
+            nonlocal t, dt
+            tries = 0
+            while True:
+                ok, _, dtn = sg.try_step("dopri5", t, dt, TOL, TOL)
+                tries += 1
+                if ok:
+                    t, dt = t + dt, dtn
+                    return tries
+                dt = dtn
+        for _ in range(args.warmup):
+            acc_step()
+        barrier()
+        ev0.record(stream)
+        tries = sum(acc_step() for _ in range(args.steps))
+        ev1.record(stream)
+        barrier()
+        ms_a = max_over_ranks(ev0.elapsed_time(ev1))
+        sg.set(us)
+        for _ in range(args.warmup):
+            sg.do_step("rk4", 0.0, 1.0)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            sg.do_step("rk4", 0.0, 1.0)
+        ev1.record(stream)
+        barrier()
+        ms_r = max_over_ranks(ev0.elapsed_time(ev1))
+        sg.close()
+        return {"config": {"workload": "gray_scott_512^3_total", "nz_per_gpu": int(sg.local), "scaling": "strong"},
+                "dopri5_adaptive": {"value": n ** 3 * args.steps / (ms_a / 1e3), "unit": "cell-updates/s",
+                                    "ms_per_step": ms_a / args.steps, "tries": tries},
+                "rk4": {"value": n ** 3 * args.steps / (ms_r / 1e3), "unit": "cell-updates/s",
+                        "ms_per_step": ms_r / args.steps}}
+
+    def run_leg(fn, *a):
+        # an extra leg that fails reports its error instead of losing the headline line
+        try:
+            return fn(*a)
+        except Exception as exc:  # noqa: BLE001
+            return {"error": f"{type(exc).__name__}: {exc}"}
+
     line = adaptive_leg() if "adaptive" in legs else {}
     extra = {}
     if "rk4" in legs:
-        extra["rk4"] = rk4_leg(args.overlap)
+        extra["rk4"] = run_leg(rk4_leg, args.overlap)
         if world > 1:
-            extra["rk4_overlap_off"] = rk4_leg(0)
+            extra["rk4_overlap_off"] = run_leg(rk4_leg, 0)
+    if "strong" in legs and world > 1:
+        extra["strong"] = run_leg(strong_leg)
     if "rk4_native" in legs:
-        extra["rk4_native"] = native_rk4_leg()
+        extra["rk4_native"] = run_leg(native_rk4_leg)
     if "exp512" in legs:
-        extra["exp512"] = exp512_leg()
+        extra["exp512"] = run_leg(exp512_leg)
     if "small" in legs:
-        extra["small_configs"] = small_configs_leg()
+        extra["small_configs"] = run_leg(small_configs_leg)
     for sch in (("euler", "midpoint", "cash_karp54", "dopri5", "rkf78") + tuple(f"ab{k}" for k in range(1, 9))
                 + tuple(f"abm{k}" for k in range(1, 9))):
         # scheme sweep (configs[4])
         if sch in legs:
-            extra[sch] = rk4_leg(args.overlap, sch)
+            extra[sch] = run_leg(rk4_leg, args.overlap, sch)
     if extra:
         line["extra"] = extra
     if "e2e" in legs:

@@ -215,7 +215,7 @@ def _sample_block(u, z, y, x, r=8):
 
 
 @pytest.mark.parametrize("scheme,adaptive", [("rk4", False), ("dopri5", True), ("dopri5", False),
-                                             ("cash_karp54", True), ("euler", False),
+                                             ("cash_karp54", True), ("euler", False), ("midpoint", False),
                                              ("rkf78", False), ("rkf78", True)])
 def test_512_sampled_parity(ctx, scheme, adaptive):
     """One step (or one adaptive try) at 512^3 exactly as bench.py runs it; every sampled
@@ -246,6 +246,31 @@ def test_512_sampled_parity(ctx, scheme, adaptive):
     for (z, y, x) in pts:
         blk = _sample_block(u0, z, y, x, r)
         out = oracle.step(p, OS[scheme], 0.0, dt, blk).reshape(blk.shape)
+        assert bitwise(g[z, :, y, x], out[r, :, r, r]), (z, y, x)
+
+
+@pytest.mark.parametrize("method", ["ab2", "abm2", "ab4"])
+def test_512_sampled_parity_adams(ctx, method):
+    """Adams steps at 512^3 in bench.py's launch configuration: RKF78 start-up then Adams
+    steps; sampled cells against the oracle on their periodic neighbourhoods."""
+    n = 512
+    k = int(method.lstrip("abm"))
+    nsteps = k  # k-1 start-up steps + 1 Adams step
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    st = gs_state(ctx, n, n, n, u0)
+    for m in range(nsteps):
+        st.do_step(method, float(m), 1.0)
+    g = st.get()
+    lo, hi = rk_inputs.cube_range(n)
+    rng = np.random.default_rng(1)
+    pts = [(lo, lo, lo), (hi - 1, hi, lo - 1), (0, 0, 0), (511, 511, 511)] + \
+          [tuple(rng.integers(lo - 4, hi + 4, 3)) for _ in range(6)]
+    r = 14 * (k - 1) + 4
+    p = oracle.gray_scott_problem(2 * r + 1, 2 * r + 1, 2 * r + 1)
+    run = oracle.abm_integrate if method.startswith("abm") else oracle.ab_integrate
+    for (z, y, x) in pts:
+        blk = _sample_block(u0, z, y, x, r)
+        out = run(p, k, blk, 0.0, 1.0, nsteps).reshape(blk.shape)
         assert bitwise(g[z, :, y, x], out[r, :, r, r]), (z, y, x)
 
 
