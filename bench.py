@@ -175,7 +175,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
-    ap.add_argument("--legs", default="adaptive,rk4,strong,rk4_native,exp512,small,e2e,cpu",
+    ap.add_argument("--legs", default="adaptive,rk4,halo,strong,rk4_native,exp512,small,e2e,cpu",
                     help="comma list of legs (profiling runs use e.g. --legs rk4)")
     ap.add_argument("--no-extra", action="store_true", help="same as --legs adaptive")
     ap.add_argument("--overlap", type=int, default=1, help="halo exchange overlapped (N > 1)")
@@ -308,8 +308,10 @@ def main():
             line["halo"] = h
         return line
 
-    def rk4_leg(overlap: int, scheme: str = "rk4"):
+    def rk4_leg(overlap: int, scheme: str = "rk4", p2p: int = 0, loopback: int = 0):
         st.set_option(rk.OPT_HALO_OVERLAP, overlap)
+        st.set_option(rk.OPT_HALO_LOOPBACK, loopback)
+        st.set_option(rk.OPT_HALO_P2P, p2p)
         st.set(u0_dev)
         # Adams–Bashforth k: the first k-1 steps are RKF78 bootstrap steps; keep them untimed
         nwarm = max(args.warmup, int(scheme.lstrip("abm")) if scheme.startswith("ab") else 0)
@@ -327,9 +329,12 @@ def main():
         s4 = st.stats()
         st.set_option(rk.OPT_TIMING, 0)
         st.set_option(rk.OPT_HALO_OVERLAP, args.overlap)
+        st.set_option(rk.OPT_HALO_P2P, 0)
+        st.set_option(rk.OPT_HALO_LOOPBACK, 0)
         a4 = s4["stage_bytes"] / (s4["stage_kernel_ms"] / 1e3) / 1e9 if s4["stage_kernel_ms"] else None
         out = {"value": cells_total * args.steps / (ms4 / 1e3), "ms_per_step": ms4 / args.steps,
                "halo_overlap": bool(overlap), "scheme": scheme,
+               "halo_path": ("p2p" if p2p else "nccl") + (" (loopback)" if loopback else ""),
                "roofline": {"bound": "hbm", "achieved": a4, "peak": peak, "unit": "GB/s",
                             "frac": a4 / peak if a4 else None,
                             "traffic": traffic.get(scheme, {}).get("bytes_per_launch"),
@@ -530,6 +535,14 @@ def main():
         extra["rk4"] = run_leg(rk4_leg, args.overlap)
         if world > 1:
             extra["rk4_overlap_off"] = run_leg(rk4_leg, 0)
+    if "halo" in legs:
+        # f3: the halo machinery on RK4 -- N = 1: loopback self-exchange through NCCL's path
+        # (device copy) and through the P2P path; N > 1: P2P stores over NVLink vs NCCL above
+        if world == 1:
+            extra["rk4_loopback_nccl"] = run_leg(rk4_leg, args.overlap, "rk4", 0, 1)
+            extra["rk4_loopback_p2p"] = run_leg(rk4_leg, args.overlap, "rk4", 1, 1)
+        else:
+            extra["rk4_p2p"] = run_leg(rk4_leg, args.overlap, "rk4", 1, 0)
     if "strong" in legs and world > 1:
         extra["strong"] = run_leg(strong_leg)
     if "rk4_native" in legs:

@@ -100,10 +100,18 @@ typedef enum {
     RK_OPT_USE_GRAPH = 5,    /* 1: rk_integrate_const of a grid (world == 1, no loopback, >= 5
                                 steps) replays pairs of steps from one captured CUDA graph
                                 (SURVEY f3): identical results, no per-launch host cost   */
-    RK_OPT_DEVICE_LOOP = 6   /* 1: rk_integrate_adaptive of a vector state (world == 1) runs
+    RK_OPT_DEVICE_LOOP = 6,  /* 1: rk_integrate_adaptive of a vector state (world == 1) runs
                                 as one cooperative kernel: tries, error max, controller and
                                 accept/reject on the device, no host sync per try (
                                 DESIGN.md R-27).  Same results; else the host loop is used.   */
+    RK_OPT_HALO_P2P = 7      /* grid, halo path (world > 1 or HALO_LOOPBACK): 1 replaces the
+                                NCCL exchange by peer-to-peer stores -- the pack kernel writes
+                                Y_i's boundary planes straight into the neighbours' (double-
+                                buffered) ghost planes through CUDA IPC mappings over NVLink
+                                and raises their ready flags; the boundary launch waits on them
+                                and hands the buffers back.  Collective: set it on
+                                every rank; the first stage maps the neighbours (NCCL
+                                all-gather of IPC handles).  Same results bit for bit.      */
 } rk_option;
 
 /* Counters since creation or the last rk_reset_stats. */

@@ -27,6 +27,16 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     return v;
 }
 
+// System-scope acquire load / release store (flags written by another GPU over NVLink).
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Block-wide max then one atomicMax per CTA.  Must be called by every thread of the CTA.
 __device__ __forceinline__ void block_max_to_global(unsigned long long v, unsigned long long* out) {
     __shared__ unsigned long long s_red[32];

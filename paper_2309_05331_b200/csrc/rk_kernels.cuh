@@ -89,6 +89,20 @@ struct GridGeom {
     int64_t ps;     // plane stride = 2*cs
 };
 
+// Device-side handshake of the peer-to-peer halo path (RK_OPT_HALO_P2P): a
+// launch first waits until both wait flags reach wait_min (acquire, system scope), and its
+// last CTA to finish stores seq into both notify flags (release, system scope) -- flags that
+// may live in a neighbour GPU's memory (CUDA IPC over NVLink).  count: a CTA completion
+// counter, reset by the last CTA.  on == 0: no handshake.
+struct P2pSync {
+    const unsigned long long* wait[2];
+    unsigned long long wait_min;
+    unsigned long long* notify[2];
+    unsigned long long* count;
+    unsigned long long seq;
+    int on;
+};
+
 // K3: fused Gray–Scott stage kernel.  Which terms exist is compile-time (StageSpec of
 // (scheme, adaptive, stage)); the runtime arguments are pointers, TMA maps and values.
 struct GsStageArgs {
@@ -112,6 +126,7 @@ struct GsStageArgs {
     int zchunk;                      // output planes per CTA
     int zmode;                       // 0: contiguous chunks; 1: chunk 0 = plane 0, chunk 1 = nzl-1
     int nyslots;                     // pack kernel: slots [0, nyslots) with g != 0 (Y terms)
+    P2pSync sync;                    // boundary launch of the P2P halo path (else on = 0)
 };
 // (scheme, adaptive, stage) selects the compile-time StageSpec instance.
 cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageArgs& a,
@@ -121,8 +136,10 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
 // (stage_rows(spec) selects the pair).
 cudaError_t encode_grid_maps(CUtensorMap* maps, const double* base, const GridGeom& g, int nplanes);
 
-// Y_i on own planes 0 and nzl-1 (whole padded planes) -> send = [lo plane | hi plane].
-cudaError_t launch_gs_pack(const GsStageArgs& a, double* send, cudaStream_t st);
+// Y_i on own planes 0 and nzl-1 (whole padded planes) -> dst[0] (plane 0), dst[1] (plane
+// nzl-1): the NCCL send buffer, or the neighbours' ghost planes (P2P, with the handshake).
+cudaError_t launch_gs_pack(const GsStageArgs& a, double* dst0, double* dst1, const P2pSync& sync,
+                           cudaStream_t st);
 // Refresh the periodic ring of every (plane, component) slice of a padded array (after a
 // user copy into the interior); nslices = planes * components.
 cudaError_t launch_fill_ring(double* a, const GridGeom& g, int nslices, cudaStream_t st);

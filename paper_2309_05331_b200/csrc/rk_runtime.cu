@@ -134,6 +134,16 @@ struct rk_state_s {
     double* sendbuf = nullptr;       // [lo plane | hi plane]
     double* ghostbuf = nullptr;      // [ghost_hi | ghost_lo] (so one message serves world==2)
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    // peer-to-peer halo (RK_OPT_HALO_P2P): the pack kernel stores Y_i's boundary planes straight
+    // into the neighbours' ghost planes (CUDA IPC over NVLink) with a flag handshake
+    bool p2p = false, p2p_ready = false;
+    double* pghost = nullptr;               // [parity][ghost_hi, ghost_lo][plane], written by peers
+    unsigned long long* pflags = nullptr;   // [READY_LO, READY_HI, ACK_LO, ACK_HI, COUNT, ...]
+    double* peer_ghost[2] = {};             // [0] lower neighbour's pghost, [1] upper's
+    unsigned long long* peer_flags[2] = {};
+    void* ipc_mapped[4] = {};               // IPC mappings to close on destroy
+    Maps tm_pg[2][2]{};                     // [parity][0 ghost_hi, 1 ghost_lo]
+    unsigned long long p2p_seq = 0;
     unsigned long long* d_err = nullptr;
     unsigned long long* h_err = nullptr;
     // rhs
@@ -465,6 +475,119 @@ static rk_status halo_exchange(rk_state st) {
     return RK_OK;
 }
 
+// ---- peer-to-peer halo path (RK_OPT_HALO_P2P) --------------------------------
+enum { P2P_READY_LO = 0, P2P_READY_HI = 1, P2P_ACK_LO = 2, P2P_ACK_HI = 3, P2P_COUNT = 4, P2P_FLAGS = 8 };
+
+// Collective (first P2P stage on every rank): double-buffered ghost planes + flags, their CUDA
+// IPC handles all-gathered over NCCL, the neighbours' buffers mapped into this process.
+static rk_status ensure_p2p(rk_state st) {
+    if (st->p2p_ready) return RK_OK;
+    rk_ctx ctx = st->ctx;
+    const int64_t pv = plane_values(st);
+    TRY(dev_alloc(ctx, &st->pghost, 4 * pv));
+    {
+        void* f = nullptr;
+        CK_CTX(ctx, cudaMalloc(&f, P2P_FLAGS * sizeof(unsigned long long)));
+        st->pflags = static_cast<unsigned long long*>(f);
+    }
+    CK_CTX(ctx, cudaMemsetAsync(st->pghost, 0, sizeof(double) * 4 * pv, ctx->stream));
+    CK_CTX(ctx, cudaMemsetAsync(st->pflags, 0, P2P_FLAGS * sizeof(unsigned long long), ctx->stream));
+    for (int b = 0; b < 2; ++b)
+        for (int g = 0; g < 2; ++g)
+            CK_CTX(ctx, encode_grid_maps(st->tm_pg[b][g].m, st->pghost + (2 * b + g) * pv, st->geo, 1));
+    const int lower = (ctx->rank + ctx->world - 1) % ctx->world, upper = (ctx->rank + 1) % ctx->world;
+    if (ctx->world == 1) {  // loopback: both neighbours are this rank
+        st->peer_ghost[0] = st->peer_ghost[1] = st->pghost;
+        st->peer_flags[0] = st->peer_flags[1] = st->pflags;
+    } else {
+        cudaIpcMemHandle_t mine[2];
+        CK_CTX(ctx, cudaIpcGetMemHandle(&mine[0], st->pghost));
+        CK_CTX(ctx, cudaIpcGetMemHandle(&mine[1], st->pflags));
+        const size_t hb = sizeof mine;
+        unsigned char* d = nullptr;
+        CK_CTX(ctx, cudaMalloc((void**)&d, hb * (ctx->world + 1)));
+        CK_CTX(ctx, cudaMemcpyAsync(d, mine, hb, cudaMemcpyHostToDevice, ctx->stream));
+        NK_CTX(ctx, ncclAllGather(d, d + hb, hb, ncclUint8, ctx->nccl, ctx->stream));
+        std::vector<unsigned char> all(hb * ctx->world);
+        CK_CTX(ctx, cudaMemcpyAsync(all.data(), d + hb, all.size(), cudaMemcpyDeviceToHost, ctx->stream));
+        CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+        cudaFree(d);
+        int nmap = 0;
+        for (int dir = 0; dir < 2; ++dir) {
+            const int peer = dir == 0 ? lower : upper;
+            if (dir == 1 && upper == lower) {  // world == 2: one peer on both sides
+                st->peer_ghost[1] = st->peer_ghost[0];
+                st->peer_flags[1] = st->peer_flags[0];
+                break;
+            }
+            cudaIpcMemHandle_t h[2];
+            std::memcpy(h, all.data() + hb * peer, hb);
+            void* pg = nullptr;
+            void* pf = nullptr;
+            CK_CTX(ctx, cudaIpcOpenMemHandle(&pg, h[0], cudaIpcMemLazyEnablePeerAccess));
+            st->ipc_mapped[nmap++] = pg;
+            CK_CTX(ctx, cudaIpcOpenMemHandle(&pf, h[1], cudaIpcMemLazyEnablePeerAccess));
+            st->ipc_mapped[nmap++] = pf;
+            st->peer_ghost[dir] = static_cast<double*>(pg);
+            st->peer_flags[dir] = static_cast<unsigned long long*>(pf);
+        }
+    }
+    st->p2p_ready = true;
+    return RK_OK;
+}
+
+// One stage with P2P halos: pack (waits until the neighbours released this parity's ghost
+// planes, stores Y_i's boundary planes into them, raises their ready flags) -> interior planes
+// -> boundary planes (wait for this rank's ready flags, then release the ghosts to the
+// neighbours).  Ghost planes alternate between two parities so a stage's stores never wait for
+// the previous stage's reads.
+static rk_status run_gs_stage_p2p(rk_state st, const StagePlan& p, GsStageArgs& a) {
+    rk_ctx ctx = st->ctx;
+    TRY(ensure_p2p(st));
+    const int nzl = (int)st->local;
+    const int64_t pv = plane_values(st);
+    const unsigned long long seq = ++st->p2p_seq;
+    const int b = (int)(seq & 1);
+    P2pSync ps{};
+    ps.on = 1;
+    ps.wait[0] = st->pflags + P2P_ACK_LO;
+    ps.wait[1] = st->pflags + P2P_ACK_HI;
+    ps.wait_min = seq >= 2 ? seq - 2 : 0;
+    ps.notify[0] = st->peer_flags[0] + P2P_READY_HI;  // my plane 0 is the lower neighbour's ghost_hi
+    ps.notify[1] = st->peer_flags[1] + P2P_READY_LO;  // my plane nzl-1 is the upper's ghost_lo
+    ps.count = st->pflags + P2P_COUNT;
+    ps.seq = seq;
+    CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->peer_ghost[0] + (2 * b + 0) * pv,
+                               st->peer_ghost[1] + (2 * b + 1) * pv, ps, ctx->stream));
+    st->stats.kernel_launches += 1;
+    st->stats.halo_exchanges += 1;
+    st->stats.halo_bytes += (int64_t)sizeof(double) * 2 * pv;
+    const int hb = 2 * (stage_rows(p.sp) - 1);
+    a.has_ghi = 1;
+    a.has_glo = 1;
+    a.tm_ghi = st->tm_pg[b][0].m[hb];
+    a.tm_glo = st->tm_pg[b][1].m[hb];
+    if (nzl > 2) {
+        GsStageArgs in = a;  // interior planes [1, nzl-1) never touch ghost planes
+        in.z_lo = 1;
+        in.z_hi = nzl - 1;
+        in.zchunk = pick_zchunk(st, p, nzl - 2);
+        TRY(launch_stage_timed(st, p, in));
+    }
+    GsStageArgs bd = a;
+    bd.zmode = 1;
+    P2pSync& bs = bd.sync;
+    bs.on = 1;
+    bs.wait[0] = st->pflags + P2P_READY_LO;
+    bs.wait[1] = st->pflags + P2P_READY_HI;
+    bs.wait_min = seq;
+    bs.notify[0] = st->peer_flags[0] + P2P_ACK_HI;  // my ghost_lo came from the lower neighbour
+    bs.notify[1] = st->peer_flags[1] + P2P_ACK_LO;  // my ghost_hi came from the upper neighbour
+    bs.count = st->pflags + P2P_COUNT;
+    bs.seq = seq;
+    return launch_stage_timed(st, p, bd);
+}
+
 static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
     rk_ctx ctx = st->ctx;
     TRY(ensure_halo(st));  // every entry path (RK plans, Adams steps, eval_rhs) lands here
@@ -475,8 +598,9 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
         a.zchunk = pick_zchunk(st, p, nzl);
         return launch_stage_timed(st, p, a);
     }
+    if (st->p2p) return run_gs_stage_p2p(st, p, a);
     // multi-GPU path: Y_i on the two boundary planes -> neighbours' ghost planes
-    CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->sendbuf, ctx->stream));
+    CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->sendbuf, st->sendbuf + plane_values(st), P2pSync{}, ctx->stream));
     st->stats.kernel_launches += 1;
     TRY(halo_exchange(st));
     a.has_ghi = 1;
@@ -1106,6 +1230,10 @@ rk_status rk_state_destroy(rk_state st) {
     for (int j = 0; j < st->nhist; ++j) cudaFree(st->hist[j]);
     cudaFree(st->sendbuf);
     cudaFree(st->ghostbuf);
+    for (void* m : st->ipc_mapped)
+        if (m) cudaIpcCloseMemHandle(m);
+    cudaFree(st->pghost);
+    cudaFree(st->pflags);
     cudaFree(st->d_err);
     cudaFreeHost(st->h_err);
     cudaFree(st->d_loop);
@@ -1242,6 +1370,10 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
     case RK_OPT_TIMING: st->timing = value != 0; break;
     case RK_OPT_USE_GRAPH: st->use_graph = value != 0; break;
     case RK_OPT_DEVICE_LOOP: st->device_loop = value != 0; break;
+    case RK_OPT_HALO_P2P:
+        if (value != 0 && !st->grid) return fail(RK_ERR_ARG, "RK_OPT_HALO_P2P needs a grid state");
+        st->p2p = value != 0;
+        break;
     default: return fail(RK_ERR_ARG, "unknown option %d", key);
     }
     return RK_OK;

@@ -139,6 +139,32 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// P2P halo handshake (P2pSync, rk_kernels.cuh): every CTA waits for the flags on entry; the
+// last CTA to finish publishes seq.  Every thread fences its own stores before the count.
+__device__ __forceinline__ void p2p_wait(const P2pSync& s) {
+    if (!s.on) return;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+            while (ld_acquire_sys(s.wait[d]) < s.wait_min) __nanosleep(64);
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void p2p_notify(const P2pSync& s) {
+    if (!s.on) return;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long nb = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+        if (atomicAdd(s.count, 1ull) + 1 == nb) {
+            *s.count = 0ull;  // the next launch on this stream starts after this one ends
+            __threadfence_system();
+            st_release_sys(s.notify[0], s.seq);
+            st_release_sys(s.notify[1], s.seq);
+        }
+    }
+}
+
 __device__ __forceinline__ bool plane_is_ghost(const GsStageArgs& a, int p) {
     return (p < 0 && a.has_glo) || (p >= a.geo.nzl && a.has_ghi);
 }
@@ -212,7 +238,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         zb = blockIdx.y == 0 ? 0 : G.nzl - 1;
         ze = zb + 1;
     }
-    if (zb >= ze) return;  // CTA-uniform, before any barrier
+    p2p_wait(a.sync);  // P2P boundary launch: the neighbours' ghost planes have landed
+    if (zb >= ze) {    // CTA-uniform, before any other barrier
+        p2p_notify(a.sync);
+        return;
+    }
     const int nplanes = ze - zb + 2;  // planes zb-1 .. ze; plane i is global zb-1+i
 
     // own cells: column lx, rows ly0 + 8r (r < ROWS)
@@ -496,11 +526,14 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         }
     }
     if constexpr (RATIO) block_max_to_global(rbits, a.errmax);
+    p2p_notify(a.sync);  // P2P: ghost planes consumed -> the neighbours may overwrite them
 }
 
 // ---- halo-plane pack and ring fill -------------------------------------------------------
 template <int NY>
-__global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, double* __restrict__ send) {
+__global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, double* __restrict__ dst0,
+                                                      double* __restrict__ dst1, const P2pSync sync) {
+    p2p_wait(sync);  // P2P: the neighbours have consumed what the previous use of dst held
     const int64_t ps = a.geo.ps, total = 2 * ps;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -509,8 +542,9 @@ __global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, doubl
         double v = __ldg(a.base + base);
 #pragma unroll
         for (int s = 0; s < NY; ++s) v = add(v, mul(a.g[s], __ldg(a.slot[s] + base)));
-        send[e] = v;
+        (sel ? dst1 : dst0)[rest] = v;
     }
+    p2p_notify(sync);  // P2P: ghost planes stored -> neighbours may read them
 }
 
 __global__ void fill_ring_kernel(double* __restrict__ p, GridGeom g, int nslices) {
@@ -667,22 +701,23 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
     }
 }
 
-cudaError_t launch_gs_pack(const GsStageArgs& a, double* send, cudaStream_t st) {
+cudaError_t launch_gs_pack(const GsStageArgs& a, double* dst0, double* dst1, const P2pSync& sync,
+                           cudaStream_t st) {
     const int64_t total = 2 * a.geo.ps;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     switch (a.nyslots) {
-    case 0: gs_pack_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 1: gs_pack_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 2: gs_pack_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 3: gs_pack_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 4: gs_pack_kernel<4><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 5: gs_pack_kernel<5><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 6: gs_pack_kernel<6><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 7: gs_pack_kernel<7><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 8: gs_pack_kernel<8><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 9: gs_pack_kernel<9><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
-    case 10: gs_pack_kernel<10><<<(unsigned)blocks, 256, 0, st>>>(a, send); break;
+    case 0: gs_pack_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 1: gs_pack_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 2: gs_pack_kernel<2><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 3: gs_pack_kernel<3><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 4: gs_pack_kernel<4><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 5: gs_pack_kernel<5><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 6: gs_pack_kernel<6><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 7: gs_pack_kernel<7><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 8: gs_pack_kernel<8><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 9: gs_pack_kernel<9><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
+    case 10: gs_pack_kernel<10><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -659,3 +659,55 @@ def test_graph_replay_on_torch_stream():
     uo, _ = oracle.integrate_const(oracle.gray_scott_problem(n, n, n), oracle.RK4, u0, 0.0, 9.0, 1.0)
     assert bitwise(st.get(), uo)
     c.close()
+
+
+# ---------------------------------------------------------------------------------------
+# f3: peer-to-peer halo stores with the flag handshake (RK_OPT_HALO_P2P), loopback on 1 GPU
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("scheme", ["rk4", "dopri5", "rkf78", "ab3", "abm2"])
+@pytest.mark.parametrize("dims", [(16, 16, 16), (33, 17, 9), (8, 8, 1), (8, 8, 2), (8, 8, 3)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_gs_halo_p2p_loopback_bitwise(ctx, scheme, dims):
+    """The P2P path (pack stores into the neighbours' double-buffered ghost planes, ready/ack
+    flags, interior + boundary launches) with this rank as both neighbours: bitwise equal to
+    the oracle over several stages and steps (both ghost parities, flag sequence > 2)."""
+    import paper_2309_05331_b200 as rk
+    nx, ny, nz = dims
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=2) + 0.01 * rk_inputs.random_state(
+        2 * nx * ny * nz, 10).reshape(nz, 2, ny, nx)
+    st = gs_state(ctx, nx, ny, nz, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+    st.set_option(rk.OPT_HALO_P2P, 1)
+    p = oracle.gray_scott_problem(nx, ny, nz)
+    nsteps = 4
+    for m in range(nsteps):
+        st.do_step(scheme, float(m), 1.0)
+    if scheme.startswith("abm"):
+        ref = oracle.abm_integrate(p, int(scheme[3:]), u0, 0.0, 1.0, nsteps)
+    elif scheme.startswith("ab"):
+        ref = oracle.ab_integrate(p, int(scheme[2:]), u0, 0.0, 1.0, nsteps)
+    else:
+        ref = u0
+        for m in range(nsteps):
+            ref = oracle.step(p, OS[scheme], float(m), 1.0, ref)
+    assert bitwise(st.get(), ref)
+    s = st.stats()
+    assert s["halo_exchanges"] >= 4
+
+
+def test_gs_halo_p2p_adaptive_counts(ctx):
+    import paper_2309_05331_b200 as rk
+    n = 24
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    st = gs_state(ctx, n, n, n, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+    st.set_option(rk.OPT_HALO_P2P, 1)
+    a, r = st.integrate_adaptive("dopri5", 0.0, 20.0, 1.0, 1e-6, 1e-6)
+    uo, ao, ro, rc = oracle.integrate_adaptive(oracle.gray_scott_problem(n, n, n), oracle.DOPRI5, u0,
+                                               0.0, 20.0, 1.0, 1e-6, 1e-6)
+    assert rc == 0 and (a, r) == (ao, ro)
+    assert bitwise(st.get(), uo)
+    out = ctx.grid(n, n, n, 2)
+    st.set(u0)
+    st.eval_rhs(out)
+    assert bitwise(out.get(), oracle.rhs(oracle.gray_scott_problem(n, n, n), u0))
