@@ -541,7 +541,7 @@ def main():
         if world == 1:
             extra["rk4_loopback_nccl"] = run_leg(rk4_leg, args.overlap, "rk4", 0, 1)
             extra["rk4_loopback_p2p"] = run_leg(rk4_leg, args.overlap, "rk4", 1, 1)
-        else:
+        elif "p2p" in legs:  # opt-in at N > 1: needs CUDA IPC between the rank processes
             extra["rk4_p2p"] = run_leg(rk4_leg, args.overlap, "rk4", 1, 0)
     if "strong" in legs and world > 1:
         extra["strong"] = run_leg(strong_leg)
