@@ -22,7 +22,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "rkb200")
 LIB = os.path.join(PKG, "librkb200.so")
 SOURCES = ["rk_runtime.cu", "rk_stencil.cu", "rk_pointwise.cu", "rk_algebra.cu"]
-HEADERS = ["rk_kernels.cuh", "rk_device.cuh", "rk_tableau.h"]
+HEADERS = ["rk_kernels.cuh", "rk_device.cuh", "rk_tableau.h", "rk_stage_spec.h", "rk_ddmath.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-prec-div=true",

@@ -34,6 +34,9 @@ namespace rkb {
 
 namespace {
 
+// The kernel's helper lambdas capture its per-thread state by reference: keep them inlined.
+#define INLINE __attribute__((always_inline))
+
 constexpr int TX = 32;  // tile width (one warp per row)
 constexpr int NT = 256;  // threads per CTA (8 warps); a thread owns ROWS cells of a column
 constexpr int BW = TX + 2;
@@ -267,8 +270,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     else if (tid < 2 * BW + TH) pos_h = (tid - 2 * BW + 1) * BW;
     else if (tid < NHALO) pos_h = (tid - 2 * BW - TH + 1) * BW + (BW - 1);
 
-    auto stage_of = [&](int i) -> unsigned char* { return smem + (size_t)(i % R) * LY.stage_bytes; };
-    auto issue = [&](int i) {  // thread 0 only
+    auto stage_of = [&](int i) INLINE -> unsigned char* { return smem + (size_t)(i % R) * LY.stage_bytes; };
+    auto issue = [&](int i) INLINE {  // thread 0 only
         const int p = zb - 1 + i;
         unsigned char* st = stage_of(i);
         uint64_t* b = &bar[i % R];
@@ -288,10 +291,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
             }
         }
     };
-    auto wait_plane = [&](int i) { mbar_wait(&bar[i % R], (uint32_t)((i / R) & 1)); };
+    auto wait_plane = [&](int i) INLINE { mbar_wait(&bar[i % R], (uint32_t)((i / R) & 1)); };
 
     // Y at ring-box position hp, component c (base + Y slots; a ghost plane is Y itself)
-    auto y_at = [&](const unsigned char* st, int c, int hp, bool ghost) -> double {
+    auto y_at = [&](const unsigned char* st, int c, int hp, bool ghost) INLINE -> double {
         double v = reinterpret_cast<const double*>(st)[c * BOX + hp];
         if (!ghost && !P.base_unew) {
 #pragma unroll
@@ -302,11 +305,11 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         return v;
     };
     // own-cell value of slot s (ring box or interior box), component c, tile row r
-    auto sval = [&](const unsigned char* st, int s, int c, int r) -> double {
+    auto sval = [&](const unsigned char* st, int s, int c, int r) INLINE -> double {
         const double* p = reinterpret_cast<const double*>(st + LY.off[s]);
         return P.halo[s] ? p[c * BOX + pos[r]] : p[c * OWN_BOX + poi[r]];
     };
-    auto make_estate = [&](const unsigned char* st, int r, ES& es) {
+    auto make_estate = [&](const unsigned char* st, int r, ES& es) INLINE {
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const double ub = reinterpret_cast<const double*>(st)[c * BOX + pos[r]];
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     }
 
     // One output plane z: Ym, Yc hold Y(z-1), Y(z); Yp receives Y(z+1).
-    auto step = [&](int z, double (&Ym)[ROWS][2], double (&Yc)[ROWS][2], double (&Yp)[ROWS][2]) {
+    auto step = [&](int z, double (&Ym)[ROWS][2], double (&Yc)[ROWS][2], double (&Yp)[ROWS][2]) INLINE {
         const int i = z - zb + 2;  // plane z+1
         const bool more = z + 1 < ze;  // plane z+1 is an output plane of this CTA
         // [A] plane z+1 from the ring
