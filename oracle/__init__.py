@@ -98,6 +98,16 @@ def lib():
                                              ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                              i64p, i64p]
         L.orc_integrate_adaptive.restype = ctypes.c_int
+        L.orc_error_ratio_max_spec.argtypes = [ctypes.c_int64, dp, dp, dp, ctypes.c_double,
+                                               ctypes.c_double]
+        L.orc_error_ratio_max_spec.restype = ctypes.c_double
+        L.orc_controller_spec.argtypes = [ctypes.c_double, ctypes.c_int, dp]
+        L.orc_controller_spec.restype = ctypes.c_int
+        L.orc_integrate_adaptive_ctrl.argtypes = [P, ctypes.c_int, dp, ctypes.c_double,
+                                                  ctypes.c_double, ctypes.c_double,
+                                                  ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                                  ctypes.c_int, i64p, i64p]
+        L.orc_integrate_adaptive_ctrl.restype = ctypes.c_int
         L.orc_lincomb.argtypes = [ctypes.c_int64, dp, ctypes.c_int, dp, ctypes.POINTER(dp)]
         L.orc_lincomb.restype = ctypes.c_int
         L.orc_norm_inf.argtypes = [ctypes.c_int64, dp]
@@ -179,6 +189,19 @@ def controller(E: float, dt: float, p: int = 5, q: int = 4):
     return bool(acc), d.value
 
 
+def error_ratio_max_spec(err, u_old, u_new, atol, rtol) -> float:
+    """SPEC's elementwise_err_ratio (R-28)."""
+    err, u_old, u_new = _arr(err), _arr(u_old), _arr(u_new)
+    return lib().orc_error_ratio_max_spec(err.size, _ptr(err), _ptr(u_old), _ptr(u_new), atol, rtol)
+
+
+def controller_spec(E: float, dt: float, p: int = 5):
+    """SPEC's elementary controller (R-28).  Returns (accepted, dt_next)."""
+    d = ctypes.c_double(dt)
+    acc = lib().orc_controller_spec(E, p, ctypes.byref(d))
+    return bool(acc), d.value
+
+
 def integrate_const(p: Problem, scheme: int, u, t0: float, t1: float, dt: float):
     """Returns (u_final, steps)."""
     u = _arr(u).copy()
@@ -195,6 +218,21 @@ def integrate_adaptive(p: Problem, scheme: int, u, t0, t1, dt0, atol, rtol):
     a, r = ctypes.c_int64(), ctypes.c_int64()
     rc = lib().orc_integrate_adaptive(ctypes.byref(p), scheme, _ptr(u), t0, t1, dt0, atol, rtol,
                                       ctypes.byref(a), ctypes.byref(r))
+    return u, a.value, r.value, rc
+
+
+CTRL_ODEINT, CTRL_SPEC = 0, 1
+
+
+def integrate_adaptive_ctrl(p: Problem, scheme: int, u, t0, t1, dt0, atol, rtol,
+                            controller: int = CTRL_ODEINT, max_tries: int = 500):
+    """integrate_adaptive with the controller reading of choice (R-12 Odeint, R-28 SPEC).
+    Returns (u_final, accepted, rejected, rc)."""
+    u = _arr(u).copy()
+    a, r = ctypes.c_int64(), ctypes.c_int64()
+    rc = lib().orc_integrate_adaptive_ctrl(ctypes.byref(p), scheme, _ptr(u), t0, t1, dt0, atol,
+                                           rtol, controller, max_tries, ctypes.byref(a),
+                                           ctypes.byref(r))
     return u, a.value, r.value, rc
 
 

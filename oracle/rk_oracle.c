@@ -344,13 +344,46 @@ int orc_integrate_const(const orc_problem* p, int scheme, double* u, double t0, 
     return ORC_OK;
 }
 
-int orc_integrate_adaptive(const orc_problem* p, int scheme, double* u, double t0, double t1,
-                           double dt0, double atol, double rtol, int64_t* accepted,
-                           int64_t* rejected) {
+/* SPEC's elementwise_err_ratio, reading R-28. */
+double orc_error_ratio_max_spec(int64_t count, const double* err, const double* u_old,
+                                const double* u_new, double atol, double rtol) {
+    double E = 0.0;
+    for (int64_t i = 0; i < count; ++i) {
+        const double a = fabs(u_old[i]), b = fabs(u_new[i]);
+        const double m = a >= b ? a : b;
+        const double r = fabs(err[i]) / (atol + rtol * m);
+        if (isnan(r)) return NAN;
+        if (r > E) E = r;
+    }
+    return E;
+}
+
+/* SPEC's try_step step-size rule, reading R-28. */
+int orc_controller_spec(double E, int p, double* dt) {
+    if (E <= 1.0) {
+        /* accepted: dt_next = dt*min(grow_cap, max(shrink_floor, safety*err^(-1/p))) */
+        double fac = (9.0 / 10.0) * pow(E, -1.0 / (double)p);
+        if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
+        if (fac > 5.0) fac = 5.0;
+        *dt = *dt * fac;
+        return 1;
+    }
+    /* rejected: dt_next = dt*max(shrink_floor, safety*err^(-1/(p-1))) */
+    double fac = (9.0 / 10.0) * pow(E, -1.0 / (double)(p - 1));
+    if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
+    *dt = *dt * fac;
+    return 0;
+}
+
+int orc_integrate_adaptive_ctrl(const orc_problem* p, int scheme, double* u, double t0,
+                                double t1, double dt0, double atol, double rtol, int controller,
+                                int max_tries, int64_t* accepted, int64_t* rejected) {
     const tableau* T = get_tableau(scheme);
     if (!T) return ORC_ERR_ARG;
     if (!T->has_err) return ORC_ERR_UNSUPPORTED;
-    if (!(dt0 > 0.0) || !(t1 > t0) || !(atol > 0.0) || !(rtol >= 0.0)) return ORC_ERR_ARG;
+    if (!(dt0 > 0.0) || !(t1 > t0) || !(atol > 0.0) || !(rtol >= 0.0) || max_tries < 1 ||
+        (controller != ORC_CTRL_ODEINT && controller != ORC_CTRL_SPEC))
+        return ORC_ERR_ARG;
     const int64_t count = p->n * p->ncomp;
     double* un = (double*)malloc(sizeof(double) * (size_t)count);
     double* er = (double*)malloc(sizeof(double) * (size_t)count);
@@ -360,22 +393,28 @@ int orc_integrate_adaptive(const orc_problem* p, int scheme, double* u, double t
     double t = t0, dt = dt0;
     while (t1 - t > DBL_EPSILON) {
         if ((t + dt) - t1 > DBL_EPSILON) dt = t1 - t;
-        orc_rhs(p, u, k1); /* dxdt at the start of the step (ratio denominator) */
+        if (controller == ORC_CTRL_ODEINT)
+            orc_rhs(p, u, k1); /* dxdt at the start of the step (ratio denominator) */
         int tries = 0;
         for (;;) {
             rc = orc_step(p, scheme, t, dt, u, un, er);
             if (rc != ORC_OK) goto done;
-            const double E = orc_error_ratio_max(count, er, u, k1, dt, atol, rtol);
+            const double E = controller == ORC_CTRL_ODEINT
+                                 ? orc_error_ratio_max(count, er, u, k1, dt, atol, rtol)
+                                 : orc_error_ratio_max_spec(count, er, u, un, atol, rtol);
             if (isnan(E)) { rc = ORC_ERR_DIVERGED; goto done; }
             const double dt_used = dt;
-            if (orc_controller(E, T->order, T->err_order, &dt)) {
+            const int ok = controller == ORC_CTRL_ODEINT
+                               ? orc_controller(E, T->order, T->err_order, &dt)
+                               : orc_controller_spec(E, T->order, &dt);
+            if (ok) {
                 memcpy(u, un, sizeof(double) * (size_t)count);
                 t = t + dt_used;
                 ++acc;
                 break;
             }
             ++rej;
-            if (++tries >= 500) { rc = ORC_ERR_STALL; goto done; }
+            if (++tries >= max_tries) { rc = ORC_ERR_STALL; goto done; }
         }
     }
 done:
@@ -383,6 +422,13 @@ done:
     *accepted = acc;
     *rejected = rej;
     return rc;
+}
+
+int orc_integrate_adaptive(const orc_problem* p, int scheme, double* u, double t0, double t1,
+                           double dt0, double atol, double rtol, int64_t* accepted,
+                           int64_t* rejected) {
+    return orc_integrate_adaptive_ctrl(p, scheme, u, t0, t1, dt0, atol, rtol, ORC_CTRL_ODEINT,
+                                       500, accepted, rejected);
 }
 
 /* ------------------------------------------------------------------------------

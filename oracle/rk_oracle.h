@@ -87,6 +87,26 @@ int orc_integrate_adaptive(const orc_problem* p, int scheme, double* u, double t
                            double dt0, double atol, double rtol, int64_t* accepted,
                            int64_t* rejected);
 
+/* The alternative controller reading of DESIGN.md R-28: SPEC's elementary controller
+ * (S:L218-233), kept behind an option because the paper delegates the constants to Odeint
+ * and SURVEY Z12 ships Odeint's.
+ * Ratio (S:L75-83 elementwise_err_ratio):
+ *   r = |err| / (atol + rtol*m),  m = |u_old| if |u_old| >= |u_new| else |u_new|,
+ *   E = max r over all elements (NaN in any r makes E NaN). */
+double orc_error_ratio_max_spec(int64_t count, const double* err, const double* u_old,
+                                const double* u_new, double atol, double rtol);
+/* SPEC try_step, p = order of the propagated solution:
+ *   E <= 1: accept, dt *= min(5, max(0.2, 0.9*E^(-1/p)))      (E == 0: x5, the grow cap)
+ *   E >  1: reject, dt *= max(0.2, 0.9*E^(-1/(p-1))).
+ * Returns 1 if accepted, 0 if rejected. */
+int orc_controller_spec(double E, int p, double* dt);
+enum { ORC_CTRL_ODEINT = 0, ORC_CTRL_SPEC = 1 };
+/* integrate_adaptive with a choice of controller (ORC_CTRL_*); the Odeint choice is exactly
+ * orc_integrate_adaptive.  max_tries: tries per step before ORC_ERR_STALL (Odeint 500). */
+int orc_integrate_adaptive_ctrl(const orc_problem* p, int scheme, double* u, double t0,
+                                double t1, double dt0, double atol, double rtol, int controller,
+                                int max_tries, int64_t* accepted, int64_t* rejected);
+
 /* Adams–Bashforth k-step coefficients beta_0..beta_{k-1} (newest first) as exact rationals
  * (Table 1 "multi-step, Adams-Bashforth 1..8").  Returns k, or -1 if k not in 1..8. */
 int orc_ab_coefficients(int k, int64_t* num, int64_t* den);
