@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define RK_ABI_VERSION 1
+#define RK_ABI_VERSION 2
 #define RK_UNIQUE_ID_BYTES 128
 
 typedef struct rk_ctx_s* rk_ctx;     /* one per rank: device, streams, NCCL communicator */
@@ -53,7 +53,9 @@ typedef enum {
     RK_ERR_CONTRACT = 2,     /* shape mismatch (lincomb), arity k not in [1,14]   */
     RK_ERR_UNSUPPORTED = 3,  /* adaptive stepping with a scheme without error estimate   */
     RK_ERR_STATE = 4,        /* RHS unset; Gray–Scott on a vector state or ncomp != 2     */
-    RK_ERR_DIVERGED = 5,     /* non-finite error ratio (NaN) during adaptive stepping     */
+    RK_ERR_DIVERGED = 5,     /* non-finite error ratio (NaN) during adaptive stepping, or a
+                                non-finite state found by RK_OPT_CHECK_FINITE (the
+                                time is in the message and in rk_stats.diverged_t)       */
     RK_ERR_DT_UNDERFLOW = 6, /* adaptive dt fell below 16*eps*max(|t|,1)                  */
     RK_ERR_STALL = 7,        /* more than 500 tries for one step (Odeint default)         */
     RK_ERR_CUDA = 8,         /* CUDA error; the ctx is poisoned                           */
@@ -104,7 +106,7 @@ typedef enum {
                                 as one cooperative kernel: tries, error max, controller and
                                 accept/reject on the device, no host sync per try (
                                 DESIGN.md R-27).  Same results; else the host loop is used.   */
-    RK_OPT_HALO_P2P = 7      /* grid, halo path (world > 1 or HALO_LOOPBACK): 1 replaces the
+    RK_OPT_HALO_P2P = 7,     /* grid, halo path (world > 1 or HALO_LOOPBACK): 1 replaces the
                                 NCCL exchange by peer-to-peer stores -- the pack kernel writes
                                 Y_i's boundary planes straight into the neighbours' (double-
                                 buffered) ghost planes through CUDA IPC mappings over NVLink
@@ -112,6 +114,19 @@ typedef enum {
                                 and hands the buffers back.  Collective: set it on
                                 every rank; the first stage maps the neighbours (NCCL
                                 all-gather of IPC handles).  Same results bit for bit.      */
+    RK_OPT_CONTROLLER = 8,   /* error-control reading (P:L42 fixes the semantics only):
+                                0 (default) Odeint's (R-12): r = |e|/(atol + rtol*
+                                (|u| + dt*|k1|)), reject if E > 1 with dt *= max(0.9E^(-1/(q-1)),
+                                0.2), grow only below E = 0.5;  1 SPEC's elementary controller
+                                (R-28): r = |e|/(atol + rtol*max(|u|,
+                                |u_new|)), accept iff E <= 1, dt *= min(5, max(0.2, 0.9E^(-1/p)))
+                                on accept, max(0.2, 0.9E^(-1/(p-1))) on reject, p = the scheme's
+                                order.  Applies to rk_try_step and rk_integrate_adaptive.    */
+    RK_OPT_CHECK_FINITE = 9  /* n >= 1: after every n-th completed step (and at the end of an
+                                integrate call) check the state with the max-norm reduction;
+                                a NaN/Inf gives RK_ERR_DIVERGED at that t.  Costs one
+                                state read per check (vector integrate_const: the n steps run
+                                in one launch).  0 (default): no check.                   */
 } rk_option;
 
 /* Counters since creation or the last rk_reset_stats. */
@@ -133,6 +148,7 @@ typedef struct {
                                  launch (1 + #k_j read) arrays read + arrays written, over
                                  the launch's cells; halo re-reads,
                                  ghost planes and reductions are not counted              */
+    double diverged_t;        /* t at which RK_OPT_CHECK_FINITE found a non-finite state  */
 } rk_stats;
 
 /* ---- library ------------------------------------------------------------------------ */
@@ -148,6 +164,8 @@ rk_status rk_tableau(rk_scheme scheme, double* a, double* b, double* e, double* 
 /* Odeint default step adjuster (R-12/R-14) applied to E and *dt: returns 1 in
  * *accepted if E <= 1 (then dt grows when E < 0.5), 0 if rejected (dt shrinks). */
 rk_status rk_controller(rk_scheme scheme, double E, double* dt, int* accepted);
+/* The same for either reading of RK_OPT_CONTROLLER (0 Odeint R-12, 1 SPEC R-28). */
+rk_status rk_step_adjust(rk_scheme scheme, int controller, double E, double* dt, int* accepted);
 
 /* Per-stage halo exchange of a z-slab grid (P:L168, P:L176 ghost_get), as
  * executed by every stage on the comm stream.  Buffers hold padded planes of Y_i:
@@ -212,8 +230,9 @@ rk_status rk_set_option(rk_state st, int key, int64_t value);
 /* One explicit step u <- u + dt*sum_j b_j k_j in place ("do_step()"). */
 rk_status rk_do_step(rk_state st, rk_scheme scheme, double t, double dt);
 /* One error-controlled try: computes the embedded error ratio
- * E = max_i |e_i| / (atol + rtol*(|u_i| + dt*|k1_i|)) (R-12/R-13), accepts
- * (u <- u_new) iff E <= 1, and proposes the next dt.  CK54 / DOPRI5 only. */
+ * E = max_i |e_i| / (atol + rtol*(|u_i| + dt*|k1_i|)) (R-12/R-13; or SPEC's ratio
+ * under RK_OPT_CONTROLLER = 1), accepts (u <- u_new) iff E <= 1, and proposes the next dt.
+ * CK54 / DOPRI5 / RKF78 only. */
 rk_status rk_try_step(rk_state st, rk_scheme scheme, double t, double dt, double atol,
                       double rtol, int* accepted, double* err_ratio, double* dt_next);
 /* Fixed-step loop of Odeint's integrate_const (R-15): steps while

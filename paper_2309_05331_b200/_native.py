@@ -15,6 +15,9 @@ STATUS = {0: "RK_OK", 1: "RK_ERR_ARG", 2: "RK_ERR_CONTRACT", 3: "RK_ERR_UNSUPPOR
           4: "RK_ERR_STATE", 5: "RK_ERR_DIVERGED", 6: "RK_ERR_DT_UNDERFLOW", 7: "RK_ERR_STALL",
           8: "RK_ERR_CUDA", 9: "RK_ERR_NCCL", 10: "RK_ERR_OOM"}
 OPT_HALO_OVERLAP, OPT_HALO_LOOPBACK, OPT_MAX_TRIES, OPT_TIMING, OPT_USE_GRAPH, OPT_DEVICE_LOOP, OPT_HALO_P2P = 1, 2, 3, 4, 5, 6, 7
+OPT_CONTROLLER, OPT_CHECK_FINITE = 8, 9
+CTRL_ODEINT, CTRL_SPEC = 0, 1
+ABI_VERSION = 2
 UNIQUE_ID_BYTES = 128
 
 
@@ -32,7 +35,7 @@ class Stats(ctypes.Structure):
                 ("halo_bytes", ctypes.c_int64), ("stage_launches", ctypes.c_int64),
                 ("stage_kernel_ms", ctypes.c_double), ("halo_ms", ctypes.c_double),
                 ("last_err_ratio", ctypes.c_double), ("last_dt", ctypes.c_double),
-                ("stage_bytes", ctypes.c_int64)]
+                ("stage_bytes", ctypes.c_int64), ("diverged_t", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -60,6 +63,7 @@ SIGNATURES = {
     "rk_partition": (_i, [_i64, _i, _i, _i64p, _i64p]),
     "rk_tableau": (_i, [_i, _dp, _dp, _dp, _dp, _ip, _ip, _ip]),
     "rk_controller": (_i, [_i, _d, _dp, _ip]),
+    "rk_step_adjust": (_i, [_i, _i, _d, _dp, _ip]),
     "rk_halo_plan_get": (_i, [_i, _i, _p(HaloPlan)]),
     "rk_nccl_unique_id": (_i, [_v]),
     "rk_ctx_create": (_i, [_i, _i, _i, _v, _v, _p(_v)]),
@@ -101,7 +105,7 @@ def lib() -> ctypes.CDLL:
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
-        if L.rk_abi_version() != 1:
+        if L.rk_abi_version() != ABI_VERSION:
             raise ImportError("librkb200.so ABI version mismatch")
         _lib = L
     return _lib

@@ -262,8 +262,11 @@ def halo_plan(world: int, rank: int) -> dict:
                      for m in p.msg[:p.nmsg]]}
 
 
-def controller(scheme, E: float, dt: float):
-    """Library's host step adjuster: returns (accepted, dt_next)."""
+def controller(scheme, E: float, dt: float, kind: int = 0):
+    """Library's host step adjuster (kind 0: Odeint R-12, 1: SPEC R-28): (accepted, dt_next)."""
     d, a = ctypes.c_double(dt), ctypes.c_int()
-    call("rk_controller", _scheme(scheme), E, ctypes.byref(d), ctypes.byref(a))
+    if kind == 0:
+        call("rk_controller", _scheme(scheme), E, ctypes.byref(d), ctypes.byref(a))
+    else:
+        call("rk_step_adjust", _scheme(scheme), kind, E, ctypes.byref(d), ctypes.byref(a))
     return bool(a.value), d.value

@@ -31,6 +31,7 @@ struct PwArgs {
     int nsteps;        // >= 1 fixed steps in registers (ignored with error ratio)
     double dt, atol, rtol;
     unsigned long long* errmax;  // error-ratio max (uint64 bits), non-null => error mode
+    int ctrl;          // error ratio reading: 0 Odeint (R-12), 1 SPEC (R-28)
     PwCoef cf;
 };
 cudaError_t launch_pointwise(int scheme, const PwArgs& a, cudaStream_t st, int num_sms);
@@ -51,7 +52,9 @@ struct PwLoopArgs {
     double lambda;
     double t0, t1, dt0, atol, rtol;
     double a[13][13], b[13], e[13];  // the scheme's coefficients as doubles (rat_double)
-    double e_rej, e_acc, emin;       // -1/(q-1), -1/p, 5^-p (host-computed, as the host controller)
+    double e_rej, e_acc, emin;       // controller exponents / floor (host-computed, as the host
+                                     // controller): Odeint -1/(q-1), -1/p, 5^-p; SPEC -1/(p-1), -1/p
+    int ctrl;                        // 0 Odeint (R-12), 1 SPEC (R-28)
     int max_tries;
     unsigned long long* red;         // [3] zeroed: per-try error-max slots (rotating)
     PwLoopResult* res;
@@ -128,7 +131,8 @@ struct GsStageArgs {
     int nyslots;                     // pack kernel: slots [0, nyslots) with g != 0 (Y terms)
     P2pSync sync;                    // boundary launch of the P2P halo path (else on = 0)
 };
-// (scheme, adaptive, stage) selects the compile-time StageSpec instance.
+// (scheme, adaptive, stage) selects the compile-time StageSpec instance; adaptive: 0 fixed step,
+// 1 error-controlled with Odeint's ratio (R-12), 2 with SPEC's ratio (R-28).
 cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageArgs& a,
                             cudaStream_t st, int* nlaunch);
 // 4D tensor maps over a padded array of `nplanes` planes, maps[4]: for 32x8 tiles the

@@ -6,7 +6,8 @@
 // many stages or fixed steps it covers (the "on-the-fly computation of stages" the paper
 // credits for Odeint's speed).  Expression trees follow DESIGN.md R-17 exactly:
 //   Y_i = u (+) (g_ij (x) k_j) over a_ij != 0, left to right;  u_new likewise with beta_j;
-//   e = (delta_j (x) k_j) (+) ... over e_j != 0;  r = |e| / (atol (+) rtol (x) (|u| (+) dt (x) |k1|)).
+//   e = (delta_j (x) k_j) (+) ... over e_j != 0;  r = |e| / (atol (+) rtol (x) (|u| (+) dt (x) |k1|))
+//   (Odeint, R-12) or r = |e| / (atol (+) rtol (x) max(|u|, |u_new|)) (SPEC, R-28).
 #include <cooperative_groups.h>
 
 #include <cfloat>
@@ -54,9 +55,10 @@ __device__ __forceinline__ double f_pointwise(double y, double lambda) {
     else return mul(y, sub(1.0, y));
 }
 
-template <int S, int RHS, bool ERR>
+// ERR: 0 no error estimate, 1 Odeint's ratio (R-12), 2 SPEC's ratio (R-28)
+template <int S, int RHS, int ERR>
 __device__ __forceinline__ double pw_steps(double x, const PwArgs& a, unsigned long long& rmax) {
-    constexpr int SE = s_eff(S, ERR);
+    constexpr int SE = s_eff(S, ERR != 0);
     constexpr PwMask M = pw_mask<S>();
     const int nsteps = ERR ? 1 : a.nsteps;
     for (int n = 0; n < nsteps; ++n) {
@@ -73,7 +75,7 @@ __device__ __forceinline__ double pw_steps(double x, const PwArgs& a, unsigned l
 #pragma unroll
         for (int j = 0; j < SE; ++j)
             if (M.b[j]) w = add(w, mul(a.cf.beta[j], k[j]));
-        if constexpr (ERR) {
+        if constexpr (ERR != 0) {
             double e = 0.0;
             bool first = true;
 #pragma unroll
@@ -83,7 +85,13 @@ __device__ __forceinline__ double pw_steps(double x, const PwArgs& a, unsigned l
                 e = first ? t : add(e, t);
                 first = false;
             }
-            const double den = add(a.atol, mul(a.rtol, add(fabs(x), mul(a.dt, fabs(k[0])))));
+            double den;
+            if constexpr (ERR == 2) {
+                const double au = fabs(x), aw = fabs(w);
+                den = add(a.atol, mul(a.rtol, au >= aw ? au : aw));
+            } else {
+                den = add(a.atol, mul(a.rtol, add(fabs(x), mul(a.dt, fabs(k[0])))));
+            }
             const unsigned long long rb = ratio_bits(fabs(e) / den);
             rmax = rb > rmax ? rb : rmax;
         }
@@ -92,7 +100,7 @@ __device__ __forceinline__ double pw_steps(double x, const PwArgs& a, unsigned l
     return x;
 }
 
-template <int S, int RHS, bool ERR>
+template <int S, int RHS, int ERR>
 __global__ void __launch_bounds__(256) pointwise_kernel(const PwArgs a) {
     unsigned long long rmax = 0ull;
     const int64_t n2 = a.count >> 1;
@@ -109,7 +117,7 @@ __global__ void __launch_bounds__(256) pointwise_kernel(const PwArgs a) {
         const int64_t i = a.count - 1;
         a.u_out[i] = pw_steps<S, RHS, ERR>(a.u[i], a, rmax);
     }
-    if constexpr (ERR) block_max_to_global(rmax, a.errmax);
+    if constexpr (ERR != 0) block_max_to_global(rmax, a.errmax);
 }
 
 template <int S, int RHS>
@@ -119,10 +127,12 @@ static cudaError_t launch_s_rhs(const PwArgs& a, cudaStream_t st, int num_sms) {
     const int64_t cap = (int64_t)num_sms * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    if (a.errmax)
-        pointwise_kernel<S, RHS, true><<<(unsigned)blocks, 256, 0, st>>>(a);
+    if (a.errmax && a.ctrl == 1)
+        pointwise_kernel<S, RHS, 2><<<(unsigned)blocks, 256, 0, st>>>(a);
+    else if (a.errmax)
+        pointwise_kernel<S, RHS, 1><<<(unsigned)blocks, 256, 0, st>>>(a);
     else
-        pointwise_kernel<S, RHS, false><<<(unsigned)blocks, 256, 0, st>>>(a);
+        pointwise_kernel<S, RHS, 0><<<(unsigned)blocks, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -139,8 +149,21 @@ static cudaError_t launch_s(const PwArgs& a, cudaStream_t st, int num_sms) {
 // error-ratio max is combined with one atomicMax per CTA and a grid-wide barrier, and all
 // threads then take the same accept/reject decision from the same E.  Only the final state
 // and the counters return to the host.
-__device__ __noinline__ double step_adjust_dev(double E, double e_rej, double e_acc, double emin, double dt,
-                                               int* ok) {
+__device__ __noinline__ double step_adjust_dev(double E, double e_rej, double e_acc, double emin, int ctrl,
+                                               double dt, int* ok) {
+    if (ctrl == 1) {  // SPEC's elementary controller (R-28): always rescale
+        if (E <= 1.0) {
+            double fac = E == 0.0 ? 5.0 : __dmul_rn(0.9, pow_dd(E, e_acc));
+            if (fac < 0.2) fac = 0.2;
+            if (fac > 5.0) fac = 5.0;
+            *ok = 1;
+            return __dmul_rn(dt, fac);
+        }
+        double fac = __dmul_rn(0.9, pow_dd(E, e_rej));
+        if (fac < 0.2) fac = 0.2;
+        *ok = 0;
+        return __dmul_rn(dt, fac);
+    }
     if (E > 1.0) {
         double fac = __dmul_rn(0.9, pow_dd(E, e_rej));
         if (fac < 0.2) fac = 0.2;
@@ -156,7 +179,7 @@ __device__ __noinline__ double step_adjust_dev(double E, double e_rej, double e_
     return dt;
 }
 
-template <int S, int RHS>
+template <int S, int RHS, int ERR>
 __global__ void __launch_bounds__(256) pointwise_loop_kernel(const PwLoopArgs a) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -202,12 +225,12 @@ __global__ void __launch_bounds__(256) pointwise_loop_kernel(const PwLoopArgs a)
                 const int64_t stride = (int64_t)gridDim.x * blockDim.x;
                 for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride) {
                     double2 v = u2[i];
-                    v.x = pw_steps<S, RHS, true>(v.x, sa, rmax);
-                    v.y = pw_steps<S, RHS, true>(v.y, sa, rmax);
+                    v.x = pw_steps<S, RHS, ERR>(v.x, sa, rmax);
+                    v.y = pw_steps<S, RHS, ERR>(v.y, sa, rmax);
                     o2[i] = v;
                 }
                 if ((a.count & 1) && blockIdx.x == 0 && threadIdx.x == 0)
-                    un[a.count - 1] = pw_steps<S, RHS, true>(u[a.count - 1], sa, rmax);
+                    un[a.count - 1] = pw_steps<S, RHS, ERR>(u[a.count - 1], sa, rmax);
             }
             block_max_to_global(rmax, a.red + tri % 3);
             grid.sync();
@@ -222,7 +245,7 @@ __global__ void __launch_bounds__(256) pointwise_loop_kernel(const PwLoopArgs a)
             }
             if (threadIdx.x == 0) {  // same inputs in every CTA -> the same decision everywhere
                 int ok = 0;
-                s_dtn = step_adjust_dev(E, a.e_rej, a.e_acc, a.emin, dt, &ok);
+                s_dtn = step_adjust_dev(E, a.e_rej, a.e_acc, a.emin, a.ctrl, dt, &ok);
                 s_ok = ok;
             }
             __syncthreads();
@@ -258,10 +281,10 @@ done:
     }
 }
 
-template <int S, int RHS>
-static cudaError_t launch_loop_s_rhs(const PwLoopArgs& a, cudaStream_t st, int device) {
+template <int S, int RHS, int ERR>
+static cudaError_t launch_loop_err(const PwLoopArgs& a, cudaStream_t st, int device) {
     int per_sm = 0, sms = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pointwise_loop_kernel<S, RHS>, 256, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pointwise_loop_kernel<S, RHS, ERR>, 256, 0);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
@@ -270,8 +293,13 @@ static cudaError_t launch_loop_s_rhs(const PwLoopArgs& a, cudaStream_t st, int d
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     void* args[] = {const_cast<PwLoopArgs*>(&a)};
-    return cudaLaunchCooperativeKernel((void*)pointwise_loop_kernel<S, RHS>, dim3((unsigned)blocks), dim3(256),
-                                       args, 0, st);
+    return cudaLaunchCooperativeKernel((void*)pointwise_loop_kernel<S, RHS, ERR>, dim3((unsigned)blocks),
+                                       dim3(256), args, 0, st);
+}
+
+template <int S, int RHS>
+static cudaError_t launch_loop_s_rhs(const PwLoopArgs& a, cudaStream_t st, int device) {
+    return a.ctrl == 1 ? launch_loop_err<S, RHS, 2>(a, st, device) : launch_loop_err<S, RHS, 1>(a, st, device);
 }
 
 cudaError_t launch_pointwise_loop(int scheme, const PwLoopArgs& a, cudaStream_t st, int device) {

@@ -153,6 +153,9 @@ struct rk_state_s {
     bool overlap = true, loopback = false, timing = false, use_graph = false, device_loop = false;
     unsigned long long* d_loop = nullptr;  // device loop: [3] error-max slots + PwLoopResult
     int max_tries = 500;
+    int controller = 0;          // RK_OPT_CONTROLLER: 0 Odeint (R-12), 1 SPEC (R-28)
+    int64_t check_finite = 0;    // RK_OPT_CHECK_FINITE: check u every n steps (0: never)
+    int64_t since_check = 0;     // steps since the last finiteness check
     // stats
     rk_stats stats{};
     std::vector<TimedPair> pending;
@@ -267,14 +270,16 @@ struct StagePlan {
     double* out_ptr = nullptr;  // non-null: the stage's k goes here (rk_eval_rhs)
 };
 
-static std::vector<StagePlan> build_plan(int scheme, bool adaptive, double dt) {
+// adaptive: 0 fixed step, 1 error-controlled (Odeint ratio, R-12), 2 error-controlled (SPEC
+// ratio, R-28)
+static std::vector<StagePlan> build_plan(int scheme, int adaptive, double dt) {
     const Coeffs C = coeffs_of(scheme);
     std::vector<StagePlan> plan;
     const int n = num_stages(scheme, adaptive);
     for (int i = 0; i < n; ++i) {
         StagePlan p;
         p.scheme = scheme;
-        p.adaptive = adaptive ? 1 : 0;
+        p.adaptive = adaptive;
         p.stage = i;
         p.sp = stage_spec(scheme, adaptive, i);
         for (int s = 0; s < p.sp.nslots; ++s) {
@@ -666,6 +671,7 @@ static rk_status run_pointwise(rk_state st, int scheme, double dt, int nsteps, b
     a.atol = atol;
     a.rtol = rtol;
     a.errmax = err ? st->d_err : nullptr;
+    a.ctrl = st->controller;
     a.cf = pw_coef(scheme, dt);
     if (err) CK_CTX(ctx, cudaMemsetAsync(st->d_err, 0, sizeof(unsigned long long), ctx->stream));
     CK_CTX(ctx, launch_pointwise(scheme, a, ctx->stream, ctx->num_sms));
@@ -692,6 +698,57 @@ static bool step_adjust(double E, int p, int q, double* dt) {
     return true;
 }
 
+// SPEC's elementary controller (R-28), p = order of the propagated
+// solution: accept iff E <= 1 and always rescale, dt *= min(5, max(0.2, 0.9 E^(-1/p))); on
+// reject dt *= max(0.2, 0.9 E^(-1/(p-1))).
+static bool step_adjust_spec(double E, int p, double* dt) {
+    if (E <= 1.0) {
+        double fac = (9.0 / 10.0) * std::pow(E, -1.0 / (double)p);
+        if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
+        if (fac > 5.0) fac = 5.0;
+        *dt = *dt * fac;
+        return true;
+    }
+    double fac = (9.0 / 10.0) * std::pow(E, -1.0 / (double)(p - 1));
+    if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
+    *dt = *dt * fac;
+    return false;
+}
+
+static bool adjust(int controller, double E, int p, int q, double* dt) {
+    return controller == 1 ? step_adjust_spec(E, p, dt) : step_adjust(E, p, q, dt);
+}
+
+// Global max |u| (collective), NaN if any element is NaN: the norm_inf reduction (K4).
+static rk_status global_norm_inf(rk_state st, double* out) {
+    rk_ctx ctx = st->ctx;
+    CK_CTX(ctx, cudaMemsetAsync(ctx->d_scratch, 0, 8, ctx->stream));
+    CK_CTX(ctx, launch_norm_inf(st->u, st->alloc, ctx->d_scratch, ctx->stream, ctx->num_sms));
+    st->stats.kernel_launches += 1;
+    if (ctx->world > 1)
+        NK_CTX(ctx, ncclAllReduce(ctx->d_scratch, ctx->d_scratch, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
+    CK_CTX(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(out, ctx->h_scratch, 8);
+    return RK_OK;
+}
+
+// RK_OPT_CHECK_FINITE: after every n-th completed step (force: now), a non-finite state is
+// RK_ERR_DIVERGED carrying the time t it was found at (stats.diverged_t).
+static rk_status finite_check(rk_state st, int64_t steps_done, double t, bool force) {
+    if (st->check_finite <= 0) return RK_OK;
+    st->since_check += steps_done;
+    if (!force && st->since_check < st->check_finite) return RK_OK;
+    st->since_check = 0;
+    double m = 0.0;
+    TRY(global_norm_inf(st, &m));
+    if (!std::isfinite(m)) {
+        st->stats.diverged_t = t;
+        return fail(RK_ERR_DIVERGED, "non-finite state at t=%.17g", t);
+    }
+    return RK_OK;
+}
+
 static rk_status check_rhs(rk_state st) {
     if (st->rhs == RHS_NONE) return fail(RK_ERR_STATE, "RHS not set");
     if (st->rhs == RHS_GRAY_SCOTT && (!st->grid || st->ncomp != 2))
@@ -704,7 +761,7 @@ static rk_status check_rhs(rk_state st) {
 // one fixed Runge–Kutta step, u <- u_new (does not touch the Adams–Bashforth history)
 static rk_status rk_fixed_step(rk_state st, int scheme, double dt) {
     if (st->grid) {
-        auto plan = build_plan(scheme, false, dt);
+        auto plan = build_plan(scheme, 0, dt);
         TRY(run_grid_plan(st, plan, dt, 0.0, 0.0));
     } else {
         TRY(run_pointwise(st, scheme, dt, 1, false, 0.0, 0.0));
@@ -861,7 +918,7 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
     ab_invalidate(st);
     int fsal_k = -1;  // FSAL: buffer holding k_s = F(u_new), the next step's k1
     if (st->grid) {
-        auto plan = build_plan(scheme, true, dt);
+        auto plan = build_plan(scheme, st->controller == 1 ? 2 : 1, dt);
         if (plan.back().sp.epi == EPI_TAIL_ERR) fsal_k = plan.back().sp.out_k;
         TRY(run_grid_plan(st, plan, dt, atol, rtol));
     } else {
@@ -878,7 +935,7 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
     st->stats.last_err_ratio = E;
     if (std::isnan(E)) return fail(RK_ERR_DIVERGED, "non-finite error ratio at t=%.17g dt=%.17g", t, dt);
     double dtn = dt;
-    const bool acc = step_adjust(E, C.order, C.err_order, &dtn);
+    const bool acc = adjust(st->controller, E, C.order, C.err_order, &dtn);
     st->stats.last_dt = dtn;
     if (acc) {
         swap_u(st);
@@ -970,7 +1027,8 @@ static rk_status device_adaptive_loop(rk_state st, int scheme, double t0, double
         a.b[i] = C.b[i];
         a.e[i] = C.e[i];
     }
-    a.e_rej = -1.0 / (double)(C.err_order - 1);  // the host controller's exponents (step_adjust)
+    a.ctrl = st->controller;  // the host controller's exponents (step_adjust / step_adjust_spec)
+    a.e_rej = st->controller == 1 ? -1.0 / (double)(C.order - 1) : -1.0 / (double)(C.err_order - 1);
     a.e_acc = -1.0 / (double)C.order;
     a.emin = std::pow(5.0, -(double)C.order);
     a.max_tries = st->max_tries;
@@ -1043,6 +1101,16 @@ rk_status rk_controller(rk_scheme scheme, double E, double* dt, int* accepted) {
     if (C.err_order == 0) return fail(RK_ERR_UNSUPPORTED, "scheme has no error estimate");
     if (std::isnan(E)) return fail(RK_ERR_DIVERGED, "NaN error ratio");
     *accepted = step_adjust(E, C.order, C.err_order, dt) ? 1 : 0;
+    return RK_OK;
+}
+
+rk_status rk_step_adjust(rk_scheme scheme, int controller, double E, double* dt, int* accepted) {
+    if (!valid_scheme(scheme) || !dt || !accepted || (controller != 0 && controller != 1))
+        return fail(RK_ERR_ARG, "bad arguments");
+    const Coeffs C = coeffs_of(scheme);
+    if (C.err_order == 0) return fail(RK_ERR_UNSUPPORTED, "scheme has no error estimate");
+    if (std::isnan(E)) return fail(RK_ERR_DIVERGED, "NaN error ratio");
+    *accepted = adjust(controller, E, C.order, C.err_order, dt) ? 1 : 0;
     return RK_OK;
 }
 
@@ -1370,6 +1438,15 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
     case RK_OPT_TIMING: st->timing = value != 0; break;
     case RK_OPT_USE_GRAPH: st->use_graph = value != 0; break;
     case RK_OPT_DEVICE_LOOP: st->device_loop = value != 0; break;
+    case RK_OPT_CONTROLLER:
+        if (value != 0 && value != 1) return fail(RK_ERR_ARG, "controller must be 0 (Odeint) or 1 (SPEC)");
+        st->controller = (int)value;
+        break;
+    case RK_OPT_CHECK_FINITE:
+        if (value < 0) return fail(RK_ERR_ARG, "check interval must be >= 0");
+        st->check_finite = value;
+        st->since_check = 0;
+        break;
     case RK_OPT_HALO_P2P:
         if (value != 0 && !st->grid) return fail(RK_ERR_ARG, "RK_OPT_HALO_P2P needs a grid state");
         st->p2p = value != 0;
@@ -1380,13 +1457,13 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
 }
 
 rk_status rk_do_step(rk_state st, rk_scheme scheme, double t, double dt) {
-    (void)t;
     TRY(check_state(st));
     if (!valid_scheme(scheme)) return fail(RK_ERR_ARG, "bad scheme %d", (int)scheme);
     if (!(dt > 0.0) || !std::isfinite(dt)) return fail(RK_ERR_ARG, "dt must be finite and > 0");
     TRY(check_rhs(st));
     DeviceGuard g(st->ctx->device);
-    return fixed_step(st, scheme, dt);
+    TRY(fixed_step(st, scheme, dt));
+    return finite_check(st, 1, t + dt, false);
 }
 
 rk_status rk_try_step(rk_state st, rk_scheme scheme, double t, double dt, double atol, double rtol,
@@ -1418,7 +1495,13 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
         ++n;
         t = t0 + (double)n * dt;
     }
-    if (is_ab_scheme(scheme)) {
+    if (st->check_finite > 0 && (st->grid || is_multistep(scheme))) {
+        // step by step, so a non-finite state is caught within check_finite steps
+        for (int64_t i = 0; i < n; ++i) {
+            TRY(fixed_step(st, scheme, dt));
+            TRY(finite_check(st, 1, t0 + (double)(i + 1) * dt, false));
+        }
+    } else if (is_ab_scheme(scheme)) {
         TRY(ab_steps(st, scheme - kSchemeAB0, dt, n));
     } else if (is_abm_scheme(scheme)) {
         TRY(ab_steps(st, scheme - kSchemeABM0, dt, n, true));
@@ -1426,11 +1509,13 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
         // pointwise RHS: all n steps of every element in registers, chunked launches
         ab_invalidate(st);
         int64_t left = n;
+        const int64_t cap = st->check_finite > 0 ? std::min<int64_t>(st->check_finite, 1 << 20) : (1 << 20);
         while (left > 0) {
-            const int chunk = (int)std::min<int64_t>(left, 1 << 20);
+            const int chunk = (int)std::min<int64_t>(left, cap);
             TRY(run_pointwise(st, scheme, dt, chunk, false, 0.0, 0.0));
             swap_u(st);
             left -= chunk;
+            TRY(finite_check(st, chunk, t0 + (double)(n - left) * dt, false));
         }
         st->k1_valid = false;
         st->stats.steps += n;
@@ -1439,6 +1524,7 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
     } else {
         for (int64_t i = 0; i < n; ++i) TRY(fixed_step(st, scheme, dt));
     }
+    TRY(finite_check(st, 0, t0 + (double)n * dt, true));
     CK_CTX(st->ctx, cudaStreamSynchronize(st->ctx->stream));
     if (steps) *steps = n;
     return RK_OK;
@@ -1455,8 +1541,10 @@ rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double
         return fail(RK_ERR_UNSUPPORTED, "scheme %d has no embedded error estimate", (int)scheme);
     TRY(check_rhs(st));
     DeviceGuard g(st->ctx->device);
-    if (st->device_loop && !st->grid && st->ctx->world == 1)
-        return device_adaptive_loop(st, scheme, t0, t1, dt0, atol, rtol, accepted, rejected);
+    if (st->device_loop && !st->grid && st->ctx->world == 1) {
+        TRY(device_adaptive_loop(st, scheme, t0, t1, dt0, atol, rtol, accepted, rejected));
+        return finite_check(st, 0, t1, true);
+    }
     int64_t acc = 0, rej = 0;
     double t = t0, dt = dt0;
     rk_status rc = RK_OK;
@@ -1476,6 +1564,8 @@ rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double
                 t = t + dt;
                 dt = dtn;
                 ++acc;
+                rc = finite_check(st, 1, t, false);
+                if (rc != RK_OK) goto done;
                 break;
             }
             dt = dtn;
@@ -1486,6 +1576,7 @@ rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double
             }
         }
     }
+    rc = finite_check(st, 0, t, true);
 done:
     if (accepted) *accepted = acc;
     if (rejected) *rejected = rej;
@@ -1522,17 +1613,8 @@ rk_status rk_lincomb(rk_state out, int k, const double* coef, const rk_state* in
 rk_status rk_norm_inf(rk_state st, double* out) {
     TRY(check_state(st));
     if (!out) return fail(RK_ERR_ARG, "null output");
-    rk_ctx ctx = st->ctx;
-    DeviceGuard g(ctx->device);
-    CK_CTX(ctx, cudaMemsetAsync(ctx->d_scratch, 0, 8, ctx->stream));
-    CK_CTX(ctx, launch_norm_inf(st->u, st->alloc, ctx->d_scratch, ctx->stream, ctx->num_sms));
-    st->stats.kernel_launches += 1;
-    if (ctx->world > 1)
-        NK_CTX(ctx, ncclAllReduce(ctx->d_scratch, ctx->d_scratch, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
-    CK_CTX(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
-    std::memcpy(out, ctx->h_scratch, 8);
-    return RK_OK;
+    DeviceGuard g(st->ctx->device);
+    return global_norm_inf(st, out);
 }
 
 rk_status rk_eval_rhs(rk_state in, rk_state out) {
@@ -1547,7 +1629,7 @@ rk_status rk_eval_rhs(rk_state in, rk_state out) {
     DeviceGuard g(ctx->device);
     if (in->grid) {
         // the k1 = F(u) stage kernel of every scheme, its output redirected to out.u
-        StagePlan p = build_plan(RK_RK4, false, 0.0)[0];
+        StagePlan p = build_plan(RK_RK4, 0, 0.0)[0];
         p.out_ptr = out->u;
         TRY(ensure_halo(in));
         TRY(run_gs_stage(in, p, 0.0, 0.0, 0.0));

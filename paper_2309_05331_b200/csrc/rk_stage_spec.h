@@ -12,6 +12,9 @@
 // later stage needs); stage s reads Y_s = u_new directly (a_sj = b_j), computes
 // k_s = F(u_new) (the next step's k1), e = e' + delta_s k_s and the ratio (EPI_TAIL_ERR).
 // That is 31 arrays per try instead of 33.
+// The adaptive flag `ad` also names the error-ratio reading: 1 = Odeint's
+// r = |e|/(atol + rtol(|u| + dt|k1|)) (R-12), 2 = SPEC's r = |e|/(atol + rtol max(|u|, |u_new|))
+// (R-28), which needs no k1: the FSAL tail then reads e' and u only (30 arrays).
 #pragma once
 #include "rk_tableau.h"
 
@@ -87,7 +90,7 @@ __host__ __device__ constexpr int num_stages(int S, bool ad) {
     return is_multistep(S) ? 1 : last_stage(tableau_of(S), ad) + 1;
 }
 
-__host__ __device__ constexpr StageSpec stage_spec(int S, bool ad, int i) {
+__host__ __device__ constexpr StageSpec stage_spec(int S, int ad, int i) {
     StageSpec p{};
     if (is_ab_scheme(S)) {
         // one RHS evaluation per step: base = u_n (tile + ring), slots = f_{n-1} .. f_{n-k+1}
@@ -134,16 +137,16 @@ __host__ __device__ constexpr StageSpec stage_spec(int S, bool ad, int i) {
     if (i < 0 || i > L) return p;
     const bool fsal = is_fsal(T, ad);
     p.valid = 1;
-    if (fsal && i == L) {  // TAIL: Y_s = u_new, slots e' (k_{L-1} buffer), u, k1
+    if (fsal && i == L) {  // TAIL: Y_s = u_new, slots e' (k_{L-1} buffer), u, k1 (Odeint ratio)
         p.epi = EPI_TAIL_ERR;
         p.base_unew = true;
-        p.nslots = 3;
+        p.nslots = ad == 2 ? 2 : 3;
         p.src[0] = L - 1; p.j[0] = L - 1;
         p.src[1] = SLOT_U; p.j[1] = 0;
         p.src[2] = 0; p.j[2] = 0;
         p.epart = 0;
         p.den_u = 1;
-        p.den_k1 = 2;
+        p.den_k1 = ad == 2 ? -1 : 2;
         p.dnew = t_enz(T, i);
         p.out_k = 1;  // k2's buffer: dead after the stage values (a_s2 = 0 for DOPRI5)
         return p;
@@ -151,7 +154,7 @@ __host__ __device__ constexpr StageSpec stage_spec(int S, bool ad, int i) {
     const bool fin = fsal ? (i == L - 1) : (i == L);
     const bool err = ad && fin;
     for (int j = 0; j < i; ++j) {
-        const bool need = t_anz(T, i, j) || (fin && t_bnz(T, j)) || (err && (t_enz(T, j) || j == 0));
+        const bool need = t_anz(T, i, j) || (fin && t_bnz(T, j)) || (err && (t_enz(T, j) || (ad == 1 && j == 0)));
         if (!need) continue;
         const int s = p.nslots++;
         p.src[s] = j;
@@ -160,7 +163,7 @@ __host__ __device__ constexpr StageSpec stage_spec(int S, bool ad, int i) {
         p.gnz[s] = t_anz(T, i, j);
         p.bnz[s] = fin && t_bnz(T, j);
         p.dnz[s] = err && t_enz(T, j);
-        if (err && j == 0) p.den_k1 = s;
+        if (err && ad == 1 && j == 0) p.den_k1 = s;
     }
     if (!fin) {
         p.epi = EPI_K;

@@ -105,9 +105,9 @@ __host__ __device__ constexpr Layout layout_of(const StageSpec& P) {
 }
 
 template <int S, int AD, int I>
-constexpr int kRows = stage_rows(stage_spec(S, AD != 0, I));
+constexpr int kRows = stage_rows(stage_spec(S, AD, I));
 template <int S, int AD, int I>
-constexpr int kMinBlocks = layout_of<kRows<S, AD, I>>(stage_spec(S, AD != 0, I)).minb;
+constexpr int kMinBlocks = layout_of<kRows<S, AD, I>>(stage_spec(S, AD, I)).minb;
 
 // ---- PTX wrappers -------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -210,7 +210,7 @@ __host__ __device__ constexpr bool has_prev_e(const StageSpec& P) {
 
 template <int S, int AD, int I>
 __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(const __grid_constant__ GsStageArgs a) {
-    constexpr StageSpec P = stage_spec(S, AD != 0, I);
+    constexpr StageSpec P = stage_spec(S, AD, I);
     constexpr int ROWS = stage_rows(P);
     using T = Tile<ROWS>;
     constexpr int TH = T::TH, BH = T::BH, BOX = T::BOX, OWN_BOX = T::OWN_BOX, NHALO = T::NHALO;
@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     constexpr bool RATIO = EPI == EPI_FINAL_ERR || EPI == EPI_TAIL_ERR;
     constexpr bool STORE_K = EPI == EPI_K || EPI == EPI_TAIL_ERR || EPI == EPI_AB;
     constexpr bool AB = EPI == EPI_AB || EPI == EPI_ABM;  // Adams epilogue (raw own-cell terms)
+    constexpr bool SPECR = AD == 2;  // SPEC's ratio denominator max(|u|, |u_new|) (R-28)
     using ES = EState<AB ? NS : 0>;
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr bool YD = LY.ydirect;
@@ -340,8 +341,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
             if constexpr (EPI == EPI_TAIL_ERR) es.e[c] = sval(st, P.epart, c, r);
             if constexpr (RATIO) {
                 const double uu = P.den_u >= 0 ? sval(st, P.den_u, c, r) : ub;
-                const double k1 = sval(st, P.den_k1, c, r);
-                es.d[c] = add(a.atol, mul(a.rtol, add(fabs(uu), mul(a.dt, fabs(k1)))));
+                if constexpr (SPECR) {
+                    es.d[c] = fabs(uu);  // completed with |u_new| in the epilogue
+                } else {
+                    const double k1 = sval(st, P.den_k1, c, r);
+                    es.d[c] = add(a.atol, mul(a.rtol, add(fabs(uu), mul(a.dt, fabs(k1)))));
+                }
             }
         }
     };
@@ -472,9 +477,10 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                         if (P.bnz[s]) wv = add(wv, mul(a.beta[s], ec.h[s][c]));
                     store_cell(a.out_u, G, slice, cell[r], wv);
                 }
+                double unew = 0.0;
                 if constexpr (FIN) {
-                    const double wv = P.bnew ? add(ec.w[c], mul(a.beta_new, f[c])) : ec.w[c];
-                    store_cell(a.out_u, G, slice, cell[r], wv);
+                    unew = P.bnew ? add(ec.w[c], mul(a.beta_new, f[c])) : ec.w[c];
+                    store_cell(a.out_u, G, slice, cell[r], unew);
                 }
                 double e = ec.e[c];
                 if constexpr (ESUM || EPI == EPI_TAIL_ERR) {
@@ -488,7 +494,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                     // r = |e| / d exactly; skip the division when e == 0 (r = +0) or when
                     // |e| <= rmax*d*(1-2^-52) (a normal number) proves r <= rmax by
                     // monotone rounding; NaN never skips.
-                    const double ae = fabs(e), dd = ec.d[c];
+                    double dd = ec.d[c];
+                    if constexpr (SPECR) {  // TAIL: the stage's Y is u_new itself
+                        const double m = fabs(FIN ? unew : Yc[r][c]);
+                        dd = add(a.atol, mul(a.rtol, dd >= m ? dd : m));
+                    }
+                    const double ae = fabs(e);
                     const double th = mul(mul(rmax, dd), 0.99999999999999978);
                     if (!(ae == 0.0 || (ae <= th && th >= 2.2250738585072014e-308))) {
                         const double rr = ae / dd;
@@ -569,7 +580,7 @@ __global__ void fill_ring_kernel(double* __restrict__ p, GridGeom g, int nslices
 
 template <int S, int AD, int I>
 cudaError_t launch_one(const GsStageArgs& a, dim3 grid, cudaStream_t st) {
-    constexpr StageSpec P = stage_spec(S, AD != 0, I);
+    constexpr StageSpec P = stage_spec(S, AD, I);
     static_assert(P.valid, "invalid stage");
     constexpr int bytes = layout_of<kRows<S, AD, I>>(P).smem;
     static bool configured = false;
@@ -586,13 +597,15 @@ cudaError_t launch_one(const GsStageArgs& a, dim3 grid, cudaStream_t st) {
 // Stages whose spec does not depend on the adaptive flag share one instantiation.
 template <int S, int AD, int I>
 cudaError_t launch_norm(const GsStageArgs& a, dim3 grid, cudaStream_t st) {
-    constexpr StageSpec P = stage_spec(S, AD != 0, I);
+    constexpr StageSpec P = stage_spec(S, AD, I);
     if constexpr (!P.valid) {
         return cudaErrorInvalidValue;
     } else if constexpr (P.epi == EPI_K && I == 0) {
         return launch_one<1, 0, 0>(a, grid, st);  // k1 = F(u): identical for every scheme
     } else if constexpr (P.epi == EPI_K && AD != 0) {
         return launch_one<S, 0, I>(a, grid, st);
+    } else if constexpr (AD == 2 && P.epi != EPI_FINAL_ERR && P.epi != EPI_TAIL_ERR) {
+        return launch_one<S, 1, I>(a, grid, st);  // only the ratio stages differ (R-28)
     } else {
         return launch_one<S, AD, I>(a, grid, st);
     }
@@ -660,7 +673,7 @@ cudaError_t encode_grid_maps(CUtensorMap* maps, const double* base, const GridGe
 
 cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageArgs& a,
                             cudaStream_t st, int* nlaunch) {
-    const int th = 8 * stage_rows(stage_spec(scheme, adaptive != 0, stage));
+    const int th = 8 * stage_rows(stage_spec(scheme, adaptive, stage));
     const int ntx = (a.geo.nx + TX - 1) / TX, nty = (a.geo.ny + th - 1) / th;
     const int tiles = ntx * nty;
     int nchunks;
@@ -673,6 +686,14 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
     }
     dim3 grid((unsigned)tiles, (unsigned)nchunks);
     if (nlaunch) ++*nlaunch;
+    if (adaptive == 2) {  // SPEC's error ratio (R-28)
+        switch (scheme) {
+        case 2: return launch_stage_i<2, 2>(stage, a, grid, st);
+        case 3: return launch_stage_i<3, 2>(stage, a, grid, st);
+        case 4: return launch_stage_i<4, 2>(stage, a, grid, st);
+        default: return cudaErrorInvalidValue;
+        }
+    }
     const int ad = adaptive ? 1 : 0;
     switch (scheme * 2 + ad) {
     case 0: return launch_stage_i<0, 0>(stage, a, grid, st);

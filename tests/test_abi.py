@@ -40,7 +40,7 @@ def test_exports_every_declared_symbol(rk):
 
 
 def test_abi_version(rk):
-    assert rk.lib().rk_abi_version() == 1
+    assert rk.lib().rk_abi_version() == 2
 
 
 @pytest.mark.parametrize("n,world", [(8, 2), (7, 2), (512, 24), (512, 8), (13, 13), (1, 1)])
@@ -78,6 +78,17 @@ def test_controller_bitwise_equal_to_oracle(rk):
         for E in Es:
             dt = float(rng.uniform(1e-3, 10.0))
             assert rk.controller(scheme, E, dt) == oracle.controller(E, dt, p, q), (E, dt)
+
+
+def test_spec_controller_bitwise_equal_to_oracle(rk):
+    """RK_OPT_CONTROLLER = 1 (R-28): the library's SPEC step adjuster equals the
+    oracle's (pinned in test_oracle_spec_controller.py) bit for bit."""
+    rng = np.random.default_rng(12)
+    Es = list(10.0 ** rng.uniform(-12, 4, 2000)) + [0.0, 0.5, 1.0, 1.0 + 2 ** -52, 1e-300, 1e300]
+    for scheme, p in (("cash_karp54", 5), ("dopri5", 5), ("rkf78", 8)):
+        for E in Es:
+            dt = float(rng.uniform(1e-3, 10.0))
+            assert rk.controller(scheme, E, dt, kind=1) == oracle.controller_spec(E, dt, p), (E, dt)
 
 
 def test_controller_errors(rk):

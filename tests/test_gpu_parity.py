@@ -711,3 +711,114 @@ def test_gs_halo_p2p_adaptive_counts(ctx):
     st.set(u0)
     st.eval_rhs(out)
     assert bitwise(out.get(), oracle.rhs(oracle.gray_scott_problem(n, n, n), u0))
+
+
+# ---------------------------------------------------------------------------------------
+# RK_OPT_CONTROLLER = 1: SPEC's elementary controller and ratio (R-28)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("scheme", ["dopri5", "cash_karp54", "rkf78"])
+@pytest.mark.parametrize("device_loop", [0, 1])
+def test_spec_controller_vector(ctx, scheme, device_loop):
+    """Config 2 input under SPEC's reading: counts identical to the oracle's, final state
+    bitwise, for the host-driven try loop and the device-resident loop."""
+    import paper_2309_05331_b200 as rk
+    n = 200001
+    u0 = rk_inputs.logistic_u0(n)
+    st = ctx.vector(n)
+    st.set_rhs_logistic()
+    st.set(u0)
+    st.set_option(rk.OPT_CONTROLLER, rk.CTRL_SPEC)
+    st.set_option(rk.OPT_DEVICE_LOOP, device_loop)
+    a, r = st.integrate_adaptive(scheme, -5.0, 5.0, 2.0, 1e-8, 1e-8)
+    uo, ao, ro, rc = oracle.integrate_adaptive_ctrl(oracle.logistic_problem(n), OS[scheme], u0,
+                                                    -5.0, 5.0, 2.0, 1e-8, 1e-8, oracle.CTRL_SPEC)
+    assert rc == 0 and (a, r) == (ao, ro) and r > 0
+    assert bitwise(st.get(), uo)
+
+
+def test_spec_controller_vector_golden(ctx):
+    """SURVEY Z12 [calc]: the paper's single logistic curve, DOPRI5 tol 1e-8: 46 / 3."""
+    import paper_2309_05331_b200 as rk
+    st = ctx.vector(1)
+    st.set_rhs_logistic()
+    st.set(rk_inputs.logistic_u0(1, -5.0, False))
+    st.set_option(rk.OPT_CONTROLLER, rk.CTRL_SPEC)
+    assert st.integrate_adaptive("dopri5", -5.0, 5.0, 0.1, 1e-8, 1e-8) == (46, 3)
+
+
+@pytest.mark.parametrize("scheme", ["dopri5", "cash_karp54", "rkf78"])
+@pytest.mark.parametrize("loopback", [0, 1])
+def test_spec_controller_gray_scott(ctx, scheme, loopback):
+    """Gray–Scott under SPEC's reading (the SPEC ratio epilogue of the fused stage kernel,
+    DOPRI5's 2-slot FSAL tail): counts and final state bitwise vs the oracle."""
+    import paper_2309_05331_b200 as rk
+    nx, ny, nz = 33, 17, 12
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=5) + 0.02 * rk_inputs.random_state(
+        2 * nx * ny * nz, 9).reshape(nz, 2, ny, nx)
+    st = gs_state(ctx, nx, ny, nz, u0)
+    st.set_option(rk.OPT_CONTROLLER, rk.CTRL_SPEC)
+    st.set_option(rk.OPT_HALO_LOOPBACK, loopback)
+    a, r = st.integrate_adaptive(scheme, 0.0, 20.0, 4.0, 1e-6, 1e-6)
+    uo, ao, ro, rc = oracle.integrate_adaptive_ctrl(oracle.gray_scott_problem(nx, ny, nz),
+                                                    OS[scheme], u0, 0.0, 20.0, 4.0, 1e-6, 1e-6,
+                                                    oracle.CTRL_SPEC)
+    assert rc == 0 and (a, r) == (ao, ro) and a > 0
+    assert bitwise(st.get(), uo)
+
+
+def test_spec_try_step_ratio(ctx):
+    """One SPEC try: E equals the oracle's max |e|/(atol + rtol max(|u|, |u_new|))."""
+    import paper_2309_05331_b200 as rk
+    n = 24
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=3) + 0.05 * rk_inputs.random_state(
+        2 * n ** 3, 4).reshape(n, 2, n, n)
+    p = oracle.gray_scott_problem(n, n, n)
+    for scheme in ("dopri5", "cash_karp54", "rkf78"):
+        st = gs_state(ctx, n, n, n, u0)
+        st.set_option(rk.OPT_CONTROLLER, rk.CTRL_SPEC)
+        for dt in (4.0, 1.0, 0.25):
+            st.set(u0)
+            acc, E, dtn = st.try_step(scheme, 0.0, dt, 1e-7, 1e-7)
+            un, err = oracle.step(p, OS[scheme], 0.0, dt, u0, with_error=True)
+            assert E == oracle.error_ratio_max_spec(err, u0, un, 1e-7, 1e-7)
+            assert (acc, dtn) == oracle.controller_spec(E, dt, 8 if scheme == "rkf78" else 5)
+            assert bitwise(st.get(), un if acc else u0)
+
+
+# ---------------------------------------------------------------------------------------
+# RK_OPT_CHECK_FINITE: a non-finite state is RK_ERR_DIVERGED carrying t (S:L148)
+# ---------------------------------------------------------------------------------------
+def test_check_finite_grid(ctx):
+    import paper_2309_05331_b200 as rk
+    n = 16
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=1)
+    st = gs_state(ctx, n, n, n, u0)
+    st.set_option(rk.OPT_CHECK_FINITE, 1)
+    assert st.integrate_const("rk4", 0.0, 5.0, 1.0) == 5           # finite: no error
+    st.set_rhs_gray_scott(d1=1e6)                                  # explicit RK blows up
+    with pytest.raises(rk.RKError) as e:
+        st.integrate_const("rk4", 0.0, 400.0, 1.0)
+    assert e.value.status == "RK_ERR_DIVERGED"
+    t = st.stats()["diverged_t"]
+    assert 1.0 <= t < 400.0 and t == int(t)
+    assert not np.all(np.isfinite(st.get()))
+
+
+def test_check_finite_vector_and_default_off(ctx):
+    import paper_2309_05331_b200 as rk
+    st = ctx.vector(1000)
+    st.set_rhs_exponential(1.0)
+    st.set(np.full(1000, 1.0))
+    assert st.integrate_const("rk4", 0.0, 1000.0, 1.0) == 1000      # overflows, unchecked
+    assert not np.all(np.isfinite(st.get()))
+    st.set(np.full(1000, 1.0))
+    st.set_option(rk.OPT_CHECK_FINITE, 64)
+    with pytest.raises(rk.RKError) as e:
+        st.integrate_const("rk4", 0.0, 1000.0, 1.0)
+    assert e.value.status == "RK_ERR_DIVERGED"
+    assert st.stats()["diverged_t"] in [64.0 * j for j in range(1, 16)]
+    st.set(np.full(1000, 1.0))
+    with pytest.raises(rk.RKError) as e:
+        for i in range(1000):
+            st.do_step("rk4", float(i), 1.0)
+    assert e.value.status == "RK_ERR_DIVERGED"
