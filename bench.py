@@ -434,8 +434,11 @@ def main():
             g = ctx.grid(n64, n64, n64, 2)
             g.set_rhs_gray_scott(h=H)
             u64 = rk_inputs.gray_scott_ic(n64, n64, n64, seed=42)
-            for graph in (0, 1):
-                g.set_option(rk.OPT_USE_GRAPH, graph)
+            for mode in ("launches", "graph", "persistent"):
+                graph = mode == "graph"
+                g.set_option(rk.OPT_USE_GRAPH, 1 if graph else 0)
+                # persistent: K5, all stages of all steps in one cooperative launch
+                g.set_option(rk.OPT_COOP_MAX_CELLS, n64 ** 3 if mode == "persistent" else 0)
                 g.set(u64)
                 g.integrate_const("rk4", 0.0, 20.0, 1.0)
                 ms = []
@@ -448,7 +451,8 @@ def main():
                     torch.cuda.synchronize()
                     ms.append(ev0.elapsed_time(ev1))
                 m = statistics.median(ms)
-                out["gs64_rk4_graph" if graph else "gs64_rk4"] = {
+                out[{"launches": "gs64_rk4", "graph": "gs64_rk4_graph",
+                     "persistent": "gs64_rk4_persistent"}[mode]] = {
                     "value": n64 ** 3 * 20 / (m / 1e3), "unit": "cell-updates/s", "ms_per_step": m / 20,
                     "config": "configs[2]: 64^3, RK4, dt=1, t in [0,20], median of integrate_const calls"}
             g.close()

@@ -122,11 +122,16 @@ typedef enum {
                                 |u_new|)), accept iff E <= 1, dt *= min(5, max(0.2, 0.9E^(-1/p)))
                                 on accept, max(0.2, 0.9E^(-1/(p-1))) on reject, p = the scheme's
                                 order.  Applies to rk_try_step and rk_integrate_adaptive.    */
-    RK_OPT_CHECK_FINITE = 9  /* n >= 1: after every n-th completed step (and at the end of an
+    RK_OPT_CHECK_FINITE = 9, /* n >= 1: after every n-th completed step (and at the end of an
                                 integrate call) check the state with the max-norm reduction;
                                 a NaN/Inf gives RK_ERR_DIVERGED at that t.  Costs one
                                 state read per check (vector integrate_const: the n steps run
                                 in one launch).  0 (default): no check.                   */
+    RK_OPT_COOP_MAX_CELLS = 10 /* fixed RK steps (do_step / integrate_const) of a Gray–Scott grid
+                                with at most this many cells, one GPU, no halo path, run as one
+                                persistent cooperative launch (all stages of all steps, grid-
+                                wide barrier between stages): same results bit for
+                                bit, no per-stage launch cost.  Default 2^18 (64^3); 0 = off. */
 } rk_option;
 
 /* Counters since creation or the last rk_reset_stats. */

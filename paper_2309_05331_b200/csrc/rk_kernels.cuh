@@ -149,6 +149,22 @@ cudaError_t launch_gs_pack(const GsStageArgs& a, double* dst0, double* dst1, con
 cudaError_t launch_fill_ring(double* a, const GridGeom& g, int nslices, cudaStream_t st);
 
 // ---------------------------------------------------------------------------------------
+// K5: whole fixed-step RK steps of Gray–Scott on a small single-GPU grid in one persistent
+// cooperative launch (rk_smallgrid.cu; grid-wide barrier between stages, u/u_new ping-pong).
+struct GsCoopArgs {
+    double* buf[2];        // buf[0] = u on entry, buf[1] = u_new; after nsteps u is buf[nsteps & 1]
+    double* k[13];         // k_j buffers (padded layout); k_last is not stored
+    double* ybuf[2];       // stage values Y_i (padded layout), alternating between stages
+    GridGeom geo;          // nzl = nz: one GPU, z wraps by index
+    double g[13][13];      // dt * a_ij
+    double beta[13];       // dt * b_j
+    double d1, d2, F, FK, inv_h2;
+    int nsteps;
+};
+cudaError_t launch_gs_coop(int scheme, const GsCoopArgs& a, cudaStream_t st, int device);
+int coop_last_stage(int scheme);  // last stage index (b_j != 0) = number of stored k_j
+
+// ---------------------------------------------------------------------------------------
 // K2 / K4: algebra.
 struct LincombArgs {
     double* out;

@@ -129,6 +129,7 @@ struct rk_state_s {
     int ab_k = 0, ab_count = 0, nhist = 0;
     double ab_dt = 0.0;
     double* hist[8] = {nullptr};
+    double* ybuf[2] = {nullptr};     // K5 stage values (RK_OPT_COOP_MAX_CELLS)
     Maps tm_hist[8]{};
     // halo (grid, world > 1 or loopback)
     double* sendbuf = nullptr;       // [lo plane | hi plane]
@@ -156,6 +157,7 @@ struct rk_state_s {
     int controller = 0;          // RK_OPT_CONTROLLER: 0 Odeint (R-12), 1 SPEC (R-28)
     int64_t check_finite = 0;    // RK_OPT_CHECK_FINITE: check u every n steps (0: never)
     int64_t since_check = 0;     // steps since the last finiteness check
+    int64_t coop_max_cells = 1 << 18;  // RK_OPT_COOP_MAX_CELLS: persistent-step path up to here
     // stats
     rk_stats stats{};
     std::vector<TimedPair> pending;
@@ -758,8 +760,69 @@ static rk_status check_rhs(rk_state st) {
     return RK_OK;
 }
 
+// K5 (rk_smallgrid.cu): fixed RK steps of a small single-GPU grid in one cooperative launch
+static bool coop_path(rk_state st, int scheme) {
+    return st->grid && st->rhs == RHS_GRAY_SCOTT && st->ctx->world == 1 && !st->loopback && !st->p2p &&
+           scheme >= RK_EULER && scheme <= RK_MIDPOINT && st->local * st->nx * st->ny <= st->coop_max_cells;
+}
+
+static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
+    rk_ctx ctx = st->ctx;
+    const int last = coop_last_stage(scheme);
+    TRY(ensure_k(st, std::max(last, 1)));
+    for (int b = 0; b < 2; ++b)
+        if (!st->ybuf[b]) TRY(alloc_array(st, &st->ybuf[b], nullptr));
+    const Coeffs C = coeffs_of(scheme);
+    GsCoopArgs a{};
+    a.geo = st->geo;
+    for (int j = 0; j < 13; ++j) a.k[j] = j < st->nk ? st->k[j] : nullptr;
+    a.ybuf[0] = st->ybuf[0];
+    a.ybuf[1] = st->ybuf[1];
+    for (int i = 0; i < C.s; ++i) {
+        for (int j = 0; j < i; ++j) a.g[i][j] = dt * C.a[i][j];
+        a.beta[i] = dt * C.b[i];
+    }
+    a.d1 = st->d1;
+    a.d2 = st->d2;
+    a.F = st->F;
+    a.FK = st->F + st->K;
+    a.inv_h2 = 1.0 / (st->h * st->h);
+    // algorithmic bytes: the stage-by-stage schedule's, per step
+    int64_t arrays = 0;
+    for (const StagePlan& p : build_plan(scheme, 0, dt))
+        arrays += 1 + p.sp.nslots + (p.sp.out_k >= 0 ? 1 : 0) + (p.sp.writes_u ? 1 : 0);
+    const int64_t cells = st->local * st->nx * st->ny;
+    while (n > 0) {
+        const int chunk = (int)std::min<int64_t>(n, 1 << 20);
+        a.nsteps = chunk;
+        a.buf[0] = st->u;
+        a.buf[1] = st->u_new;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (st->timing) {
+            e0 = pool_event(st);
+            e1 = pool_event(st);
+            CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+        }
+        CK_CTX(ctx, launch_gs_coop(scheme, a, ctx->stream, ctx->device));
+        if (st->timing) {
+            CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+            st->pending.push_back({e0, e1, 0});
+        }
+        if (chunk & 1) swap_u(st);
+        st->stats.kernel_launches += 1;
+        st->stats.stage_launches += 1;
+        st->stats.rhs_evals += (int64_t)(last + 1) * chunk;
+        st->stats.stage_bytes += arrays * cells * 2 * (int64_t)sizeof(double) * chunk;
+        st->stats.steps += chunk;
+        n -= chunk;
+    }
+    st->k1_valid = false;
+    return RK_OK;
+}
+
 // one fixed Runge–Kutta step, u <- u_new (does not touch the Adams–Bashforth history)
 static rk_status rk_fixed_step(rk_state st, int scheme, double dt) {
+    if (coop_path(st, scheme)) return coop_steps(st, scheme, dt, 1);
     if (st->grid) {
         auto plan = build_plan(scheme, 0, dt);
         TRY(run_grid_plan(st, plan, dt, 0.0, 0.0));
@@ -1296,6 +1359,8 @@ rk_status rk_state_destroy(rk_state st) {
     cudaFree(st->u_new);
     for (int j = 0; j < st->nk; ++j) cudaFree(st->k[j]);
     for (int j = 0; j < st->nhist; ++j) cudaFree(st->hist[j]);
+    cudaFree(st->ybuf[0]);
+    cudaFree(st->ybuf[1]);
     cudaFree(st->sendbuf);
     cudaFree(st->ghostbuf);
     for (void* m : st->ipc_mapped)
@@ -1447,6 +1512,10 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
         st->check_finite = value;
         st->since_check = 0;
         break;
+    case RK_OPT_COOP_MAX_CELLS:
+        if (value < 0) return fail(RK_ERR_ARG, "cell limit must be >= 0");
+        st->coop_max_cells = value;
+        break;
     case RK_OPT_HALO_P2P:
         if (value != 0 && !st->grid) return fail(RK_ERR_ARG, "RK_OPT_HALO_P2P needs a grid state");
         st->p2p = value != 0;
@@ -1519,6 +1588,9 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
         }
         st->k1_valid = false;
         st->stats.steps += n;
+    } else if (coop_path(st, scheme)) {
+        ab_invalidate(st);
+        TRY(coop_steps(st, scheme, dt, n));
     } else if (st->use_graph && !halo_path(st) && !st->timing && n >= 5) {
         TRY(graph_steps(st, scheme, dt, n));
     } else {

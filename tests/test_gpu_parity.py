@@ -30,10 +30,15 @@ def bitwise(a, b):
     return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-def gs_state(ctx, nx, ny, nz, u0, **prm):
+def gs_state(ctx, nx, ny, nz, u0, coop=False, **prm):
+    """A Gray–Scott state.  coop=False pins fixed steps to the stage-by-stage TMA stencil
+    path (K3); coop=True leaves the persistent small-grid path (K5) on (library default)."""
+    import paper_2309_05331_b200 as rk
     st = ctx.grid(nx, ny, nz, 2)
     st.set_rhs_gray_scott(**prm)
     st.set(u0)
+    if not coop:
+        st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
     return st
 
 
@@ -120,12 +125,13 @@ GRIDS = [(4, 4, 4), (8, 8, 8), (16, 16, 16), (33, 17, 9), (64, 40, 12), (1, 1, 3
 
 @pytest.mark.parametrize("scheme", SCHEMES)
 @pytest.mark.parametrize("dims", GRIDS, ids=lambda d: "x".join(map(str, d)))
-def test_gs_steps_bitwise(ctx, scheme, dims):
+@pytest.mark.parametrize("coop", [False, True], ids=["k3", "k5"])
+def test_gs_steps_bitwise(ctx, scheme, dims, coop):
     nx, ny, nz = dims
     u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=42)
     # perturb so every cell is non-trivial (the IC is mostly the (1,0) steady state)
     u0 = u0 + 0.01 * rk_inputs.random_state(u0.size, 5).reshape(u0.shape)
-    st = gs_state(ctx, nx, ny, nz, u0)
+    st = gs_state(ctx, nx, ny, nz, u0, coop=coop)
     p = oracle.gray_scott_problem(nx, ny, nz)
     u = u0
     for k in range(3):
@@ -157,11 +163,13 @@ def test_gs_halo_loopback_bitwise(ctx, scheme, dims, overlap):
     assert st.stats()["halo_exchanges"] > 0
 
 
-def test_config3_gray_scott_64_rk4(ctx):
-    """BASELINE configs[2]: 64^3 periodic, RK4, dt=1, t in [0,20]: bitwise after every step."""
+@pytest.mark.parametrize("coop", [False, True], ids=["k3", "k5"])
+def test_config3_gray_scott_64_rk4(ctx, coop):
+    """BASELINE configs[2]: 64^3 periodic, RK4, dt=1, t in [0,20]: bitwise after every step,
+    through the stage-by-stage stencil path (k3) and the persistent one-launch path (k5)."""
     n = 64
     u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
-    st = gs_state(ctx, n, n, n, u0)
+    st = gs_state(ctx, n, n, n, u0, coop=coop)
     p = oracle.gray_scott_problem(n, n, n)
     u = u0
     for k in range(20):
@@ -822,3 +830,58 @@ def test_check_finite_vector_and_default_off(ctx):
         for i in range(1000):
             st.do_step("rk4", float(i), 1.0)
     assert e.value.status == "RK_ERR_DIVERGED"
+
+
+# ---------------------------------------------------------------------------------------
+# K5: persistent cooperative small-grid steps (RK_OPT_COOP_MAX_CELLS, rk_smallgrid.cu)
+# ---------------------------------------------------------------------------------------
+@pytest.mark.parametrize("scheme", SCHEMES)
+@pytest.mark.parametrize("dims", [(64, 64, 64), (33, 17, 9), (1, 1, 3), (70, 9, 20)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_coop_integrate_const_one_launch(ctx, scheme, dims):
+    """integrate_const through K5: one launch for all steps (odd and even counts, so the final
+    state sits in either ping-pong buffer), bitwise equal to the oracle, counters as K3's."""
+    nx, ny, nz = dims
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=8) + 0.01 * rk_inputs.random_state(
+        2 * nx * ny * nz, 3).reshape(nz, 2, ny, nx)
+    p = oracle.gray_scott_problem(nx, ny, nz)
+    for nsteps in (5, 6):
+        uo, so = oracle.integrate_const(p, OS[scheme], u0, 0.0, float(nsteps), 1.0)
+        stats = []
+        for coop in (True, False):
+            st = gs_state(ctx, nx, ny, nz, u0, coop=coop)
+            assert st.integrate_const(scheme, 0.0, float(nsteps), 1.0) == so == nsteps
+            assert bitwise(st.get(), uo), (coop, nsteps)
+            s = st.stats()
+            stats.append(s)
+            st.close()
+        assert stats[0]["kernel_launches"] == 2  # ring fill of set() + one K5 launch
+        for k in ("steps", "rhs_evals", "stage_bytes"):
+            assert stats[0][k] == stats[1][k], k
+
+
+def test_coop_threshold_and_mixing(ctx):
+    """Above RK_OPT_COOP_MAX_CELLS the stage path runs; K5 steps, K3 steps and adaptive tries
+    interleave on one state (FSAL k1 invalidated by K5 steps) with the oracle's results."""
+    import paper_2309_05331_b200 as rk
+    n = 24
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=2)
+    p = oracle.gray_scott_problem(n, n, n)
+    st = gs_state(ctx, n, n, n, u0, coop=True)
+    st.set_option(rk.OPT_COOP_MAX_CELLS, n ** 3 - 1)
+    st.do_step("rk4", 0.0, 1.0)
+    assert st.stats()["kernel_launches"] == 1 + 4  # ring fill of set() + 4 stage launches
+    st.set_option(rk.OPT_COOP_MAX_CELLS, n ** 3)
+    st.do_step("rk4", 1.0, 1.0)
+    acc, E, dtn = st.try_step("dopri5", 2.0, 1.0, 1e-6, 1e-6)
+    st.do_step("dopri5", 3.0, 0.5)
+    acc2, E2, _ = st.try_step("dopri5", 3.5, 0.5, 1e-6, 1e-6)
+    u = oracle.step(p, oracle.RK4, 0.0, 1.0, u0)
+    u = oracle.step(p, oracle.RK4, 1.0, 1.0, u)
+    un, err = oracle.step(p, oracle.DOPRI5, 2.0, 1.0, u, with_error=True)
+    assert E == oracle.error_ratio_max(err, u, oracle.rhs(p, u), 1.0, 1e-6, 1e-6)
+    u = un if acc else u
+    u = oracle.step(p, oracle.DOPRI5, 3.0, 0.5, u)
+    un, err = oracle.step(p, oracle.DOPRI5, 3.5, 0.5, u, with_error=True)
+    assert E2 == oracle.error_ratio_max(err, u, oracle.rhs(p, u), 0.5, 1e-6, 1e-6)
+    assert bitwise(st.get(), un if acc2 else u)

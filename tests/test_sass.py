@@ -61,3 +61,13 @@ def test_no_fma_contraction_in_stencil_arithmetic(sass):
     IEEE division sequence of the error-ratio stages, never in k-only stages."""
     for (s, ad, i) in [(1, 0, 0), (1, 0, 1), (3, 0, 2), (0, 0, 0)]:
         assert "DFMA" not in _stage(sass, s, ad, i), (s, ad, i)
+
+
+@pytest.mark.parametrize("s", [0, 1, 2, 3, 5])
+def test_persistent_small_grid_kernel(sass, s):
+    """K5 (rk_smallgrid.cu), configs[2]'s path: registers only and no FMA contraction (R-17)
+    in the Euler / RK4 / Cash–Karp / DOPRI5 / midpoint instances (RKF78's spills 32 B)."""
+    hits = [v for k, v in sass.items() if f"gs_coop_kernelILi{s}E" in k]
+    assert len(hits) == 1
+    assert not re.search(r"\b(STL|LDL)\b", hits[0])
+    assert "DFMA" not in hits[0]
