@@ -956,7 +956,7 @@ static rk_status ab_steps(rk_state st, int k, double dt, int64_t nsteps, bool ab
         p.sp = stage_spec(p.scheme, false, 0);
         for (int s = 0; s < k - 1; ++s) p.beta[s] = g[s + 1];
         p.beta_new = g[0];
-        p.out_hist = k - 1;
+        p.out_hist = k > 1 ? k - 1 : -1;  // AB1 keeps no history (rk_stage_spec.h)
         TRY(run_gs_stage(st, p, dt, 0.0, 0.0));
         swap_u(st);
         ab_rotate(st);

@@ -107,7 +107,7 @@ __host__ __device__ constexpr StageSpec stage_spec(int S, int ad, int i) {
         }
         p.bnew = true;
         p.writes_u = true;
-        p.out_k = 0;
+        p.out_k = k > 1 ? 0 : -1;  // AB1 (= Euler) keeps no history: f_n is never read again
         return p;
     }
     if (is_abm_scheme(S)) {

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     constexpr bool FIN = EPI == EPI_FINAL || EPI == EPI_FINAL_ERR || EPI == EPI_FINAL_EPART;
     constexpr bool ESUM = EPI == EPI_FINAL_ERR || EPI == EPI_FINAL_EPART;  // e from slots
     constexpr bool RATIO = EPI == EPI_FINAL_ERR || EPI == EPI_TAIL_ERR;
-    constexpr bool STORE_K = EPI == EPI_K || EPI == EPI_TAIL_ERR || EPI == EPI_AB;
+    constexpr bool STORE_K = EPI == EPI_K || EPI == EPI_TAIL_ERR || (EPI == EPI_AB && P.out_k >= 0);
     constexpr bool AB = EPI == EPI_AB || EPI == EPI_ABM;  // Adams epilogue (raw own-cell terms)
     constexpr bool SPECR = AD == 2;  // SPEC's ratio denominator max(|u|, |u_new|) (R-28)
     using ES = EState<AB ? NS : 0>;
