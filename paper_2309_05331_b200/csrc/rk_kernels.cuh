@@ -119,6 +119,9 @@ struct GsStageArgs {
     double beta[kMaxSlots];          // dt*b_j per slot
     double delta[kMaxSlots];         // dt*e_j per slot
     double beta_new, delta_new;      // weights of the k_i computed by this stage
+    double g2[kMaxSlots], g2_new;    // EPI_AHEAD: dt*a_Fj per slot and dt*a_Fi (final stage F)
+    double* out_w;                   // EPI_AHEAD: partial final combination W
+    double* out_e;                   // EPI_AHEAD (error control): partial error sum E
     double* out_k;
     double* out_u;
     unsigned long long* errmax;

@@ -268,6 +268,7 @@ struct StagePlan {
     StageSpec sp{};
     double g[kMaxSlots] = {0}, beta[kMaxSlots] = {0}, delta[kMaxSlots] = {0};
     double beta_new = 0.0, delta_new = 0.0;
+    double g2[kMaxSlots] = {0}, g2_new = 0.0;  // EPI_AHEAD: the final stage's a_Fj (x dt)
     int out_hist = -1;  // >= 0: the stage writes its k into Adams–Bashforth history slot
     double* out_ptr = nullptr;  // non-null: the stage's k goes here (rk_eval_rhs)
 };
@@ -292,6 +293,10 @@ static std::vector<StagePlan> build_plan(int scheme, int adaptive, double dt) {
         }
         p.beta_new = p.sp.bnew ? dt * C.b[i] : 0.0;
         p.delta_new = p.sp.dnew ? dt * C.e[i] : 0.0;
+        if (p.sp.epi == EPI_AHEAD) {
+            for (int s = 0; s < p.sp.nslots; ++s) p.g2[s] = p.sp.anz2[s] ? dt * C.a[i + 1][p.sp.j[s]] : 0.0;
+            p.g2_new = p.sp.a2new ? dt * C.a[i + 1][i] : 0.0;
+        }
         plan.push_back(p);
     }
     return plan;
@@ -301,6 +306,7 @@ static int plan_num_k(const std::vector<StagePlan>& plan) {
     int nk = 0;
     for (auto& p : plan) {
         if (p.sp.out_k >= 0) nk = std::max(nk, p.sp.out_k + 1);
+        nk = std::max(nk, std::max(p.sp.out_w, std::max(p.sp.out_e, p.sp.base_src)) + 1);
         for (int s = 0; s < p.sp.nslots; ++s)
             if (p.sp.src[s] >= 0) nk = std::max(nk, p.sp.src[s] + 1);
     }
@@ -332,8 +338,8 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     GsStageArgs a{};
     a.geo = st->geo;
     const int hb = 2 * (stage_rows(p.sp) - 1);  // map pair of this stage's tile height
-    a.base = p.sp.base_unew ? st->u_new : st->u;
-    a.tm_base = (p.sp.base_unew ? st->tm_unew : st->tm_u).m[hb];
+    a.base = p.sp.base_src >= 0 ? st->k[p.sp.base_src] : (p.sp.base_unew ? st->u_new : st->u);
+    a.tm_base = (p.sp.base_src >= 0 ? st->tm_k[p.sp.base_src] : (p.sp.base_unew ? st->tm_unew : st->tm_u)).m[hb];
     int ny = 0;
     const bool ab = is_multistep(p.scheme);  // slots are history entries, newest first
     for (int s = 0; s < p.sp.nslots; ++s) {
@@ -344,6 +350,7 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
         a.g[s] = p.g[s];
         a.beta[s] = p.beta[s];
         a.delta[s] = p.delta[s];
+        a.g2[s] = p.g2[s];
         if (p.sp.gnz[s]) ++ny;
     }
     a.nyslots = ny;
@@ -353,6 +360,9 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
                         : (p.out_hist >= 0 ? st->hist[p.out_hist]
                                            : (p.sp.out_k >= 0 ? st->k[p.sp.out_k] : nullptr));
     a.out_u = p.sp.writes_u ? st->u_new : nullptr;
+    a.g2_new = p.g2_new;
+    a.out_w = p.sp.out_w >= 0 ? st->k[p.sp.out_w] : nullptr;
+    a.out_e = p.sp.out_e >= 0 ? st->k[p.sp.out_e] : nullptr;
     a.errmax = st->d_err;
     a.dt = dt;
     a.atol = atol;
@@ -373,7 +383,7 @@ static GsStageArgs pack_args(const GsStageArgs& a, const StagePlan& p) {
     GsStageArgs q = a;
     int n = 0;
     for (int s = 0; s < p.sp.nslots; ++s) {
-        if (!p.sp.gnz[s] || p.sp.base_unew) continue;
+        if (!p.sp.gnz[s] || p.sp.base_unew || p.sp.base_src >= 0) continue;
         q.slot[n] = a.slot[s];
         q.g[n] = a.g[s];
         ++n;
@@ -384,22 +394,23 @@ static GsStageArgs pack_args(const GsStageArgs& a, const StagePlan& p) {
 
 // Planes per CTA.  Short z chunks keep y-neighbouring tiles (which re-read each other's
 // ring rows through L2) progressing together; measured at 512^2 planes (profiles/r1_*tune*):
-// 16 planes for stages with <= 1 k input (4 CTAs/SM), 32 for the two-output DOPRI5 stage 6,
-// 48 otherwise.  Small grids: shorten further so every SM gets work.
+// 8 for Y-direct stages, 16 for other two-row stages and for the multi-output write-ahead
+// stage (2.88 ms at 16 vs 3.26 at 32, 3.67 at 48 for DOPRI5's, gpurun_out tune_zc*), 48
+// otherwise.  Small grids: shorten further so every SM gets work.
 static int pick_zchunk(rk_state st, const StagePlan& p, int range) {
     if (range <= 0) return 1;
     if (const char* e = getenv("RKB_ZCHUNK")) {  // developer tuning knob
         const int v = atoi(e);
         if (v > 0) return std::min(v, range);
     }
-    // classes: 0 Y-direct (no slot enters Y), 1 other two-row stages, 2 EPART, 3 the rest
+    // classes: 0 Y-direct (no slot enters Y), 1 other two-row stages, 2 AHEAD / EPART, 3 the rest
     bool yd = true;
     for (int s = 0; s < p.sp.nslots; ++s) yd = yd && !p.sp.gnz[s];
-    const int cls = yd ? 0 : (stage_rows(p.sp) == 2 ? 1 : (p.sp.epi == EPI_FINAL_EPART ? 2 : 3));
+    const int cls = yd ? 0 : (stage_rows(p.sp) == 2 ? 1 : (p.sp.epi == EPI_FINAL_EPART || p.sp.epi == EPI_AHEAD ? 2 : 3));
     static int tab[4] = {0, 0, 0, 0};
     static bool parsed = false;
     if (!parsed) {  // developer tuning knob RKB_ZC="yd,light,epart,heavy"
-        const int def[4] = {8, 16, 32, 48};
+        const int def[4] = {8, 16, 16, 48};
         for (int c = 0; c < 4; ++c) tab[c] = def[c];
         if (const char* e = getenv("RKB_ZC")) {
             int v[4], n = sscanf(e, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]);
@@ -430,7 +441,8 @@ static rk_status launch_stage_timed(rk_state st, const StagePlan& p, GsStageArgs
     st->stats.stage_launches += nl;
     if (nl) {
         const int64_t planes = a.zmode == 1 ? (a.geo.nzl > 1 ? 2 : 1) : (int64_t)(a.z_hi - a.z_lo);
-        const int64_t arrays = 1 + p.sp.nslots + (a.out_k ? 1 : 0) + (a.out_u ? 1 : 0);
+        const int64_t arrays = 1 + p.sp.nslots + (a.out_k ? 1 : 0) + (a.out_u ? 1 : 0) + (a.out_w ? 1 : 0) +
+                               (a.out_e ? 1 : 0);
         st->stats.stage_bytes += planes * st->nx * st->ny * 2 * (int64_t)sizeof(double) * arrays;
     }
     if (st->timing) {
@@ -790,7 +802,8 @@ static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
     // algorithmic bytes: the stage-by-stage schedule's, per step
     int64_t arrays = 0;
     for (const StagePlan& p : build_plan(scheme, 0, dt))
-        arrays += 1 + p.sp.nslots + (p.sp.out_k >= 0 ? 1 : 0) + (p.sp.writes_u ? 1 : 0);
+        arrays += 1 + p.sp.nslots + (p.sp.out_k >= 0 ? 1 : 0) + (p.sp.writes_u ? 1 : 0) + (p.sp.out_w >= 0 ? 1 : 0) +
+                  (p.sp.out_e >= 0 ? 1 : 0);
     const int64_t cells = st->local * st->nx * st->ny;
     while (n > 0) {
         const int chunk = (int)std::min<int64_t>(n, 1 << 20);

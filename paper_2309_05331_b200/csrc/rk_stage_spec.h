@@ -27,7 +27,9 @@ enum Epilogue {
     EPI_FINAL_EPART = 3,  // EPI_FINAL + store e' = e + delta_i k_i
     EPI_TAIL_ERR = 4,     // Y = u_new (base); store k_i; e = e' + delta_i k_i; ratio max
     EPI_AB = 5,           // Adams–Bashforth: store f_n; u_new = u + g_0 f_n + sum_s g_s h_s
-    EPI_ABM = 6           // ABM corrector: Y = u_p (slots), u_new = u + m_0 F(u_p) + sum_s m_s h_s
+    EPI_ABM = 6,          // ABM corrector: Y = u_p (slots), u_new = u + m_0 F(u_p) + sum_s m_s h_s
+    EPI_AHEAD = 7         // stage before the final one: store Y_F = u + sum a_Fj k_j (tile + ring),
+                          // W = u + sum b_j k_j and (adaptive) E = sum e_j k_j, all through j = i
 };
 
 // Scheme ids of the Adams–Bashforth k-step methods (rk_b200.h RK_ADAMS_BASHFORTH1..8).
@@ -57,11 +59,21 @@ struct StageSpec {
     int den_u = SLOT_U - 1;                // TAIL: slot holding old u for the ratio (else base)
     int den_k1 = -1;                       // slot holding k1 for the ratio
     int epart = -1;                        // TAIL: slot holding e'
+    // "write ahead": the stage A = F-1 before the final-combination stage F
+    // stores F's stage value and the partial final / error sums instead of k_A, so stage F
+    // reads one halo array and one or two own-cell arrays instead of u and every k_j.
+    bool anz2[kMaxSlots] = {};             // AHEAD: a_Fj != 0 (slot enters Y_F)
+    bool a2new = false;                    // AHEAD: a_FA != 0
+    int out_w = -1, out_e = -1;            // AHEAD: k buffers receiving W and E
+    int base_src = -1;                     // F after AHEAD: k buffer holding Y_F (the base)
+    int wslot = -1, eslot = -1;            // F after AHEAD: slots holding W and E
 };
 
 __host__ __device__ constexpr bool t_anz(const Tableau& T, int i, int j) { return rat_nz(T.a[i][j]); }
 __host__ __device__ constexpr bool t_bnz(const Tableau& T, int j) { return rat_nz(T.b[j]); }
 __host__ __device__ constexpr bool t_enz(const Tableau& T, int j) { return rat_nz(err_weight(T, j)); }
+__host__ __device__ constexpr int last_stage(const Tableau& T, bool ad);
+__host__ __device__ constexpr bool is_fsal(const Tableau& T, bool ad);
 
 __host__ __device__ constexpr int last_stage(const Tableau& T, bool ad) {
     int last = 0;
@@ -77,6 +89,35 @@ __host__ __device__ constexpr bool is_fsal(const Tableau& T, bool ad) {
     for (int j = 0; j < L; ++j)
         if (T.a[L][j].n * T.b[j].d != T.b[j].n * T.a[L][j].d) return false;
     return true;
+}
+
+// Index of the final-combination stage (u_new): the last stage, or the one before DOPRI5's tail.
+__host__ __device__ constexpr int fin_stage(const Tableau& T, bool ad) {
+    return is_fsal(T, ad) ? last_stage(T, ad) - 1 : last_stage(T, ad);
+}
+
+// Whether the final stage F is fed by a write-ahead stage A = F-1: only for fixed steps and
+// FSAL error control (a non-FSAL error stage needs u and k1 at F for the ratio), and only if
+// it moves fewer arrays (reads + writes of stages A and F) and fits the slot limit.
+__host__ __device__ constexpr bool use_ahead(const Tableau& T, int ad) {
+    if (T.s == 0 || (ad && T.err_order == 0)) return false;
+    const bool fsal = is_fsal(T, ad != 0);
+    if (ad && !fsal) return false;
+    const int F = fin_stage(T, ad != 0), A = F - 1;
+    if (A < 0) return false;
+    int curA = 2, curF = 1 + (ad ? 2 : 1), ahA = 1 + 2 + (ad ? 1 : 0), ahF = 1 + 1 + (ad ? 1 : 0) + (ad ? 2 : 1);
+    int slotsA = 0;
+    for (int j = 0; j < A; ++j) {
+        if (t_anz(T, A, j)) ++curA;
+        const bool needF = t_anz(T, F, j) || t_bnz(T, j) || (ad && t_enz(T, j));
+        if (needF) ++curF;
+        if (t_anz(T, A, j) || needF) {
+            ++ahA;
+            ++slotsA;
+        }
+    }
+    if (t_anz(T, F, A) || t_bnz(T, A) || (ad && t_enz(T, A))) ++curF;  // k_A itself
+    return slotsA <= kMaxSlots && ahA + ahF < curA + curF;
 }
 
 // Tile rows per thread in the stencil kernel (1 or 2).  Two-row tiles (32x16) amortise the
@@ -153,6 +194,51 @@ __host__ __device__ constexpr StageSpec stage_spec(int S, int ad, int i) {
     }
     const bool fin = fsal ? (i == L - 1) : (i == L);
     const bool err = ad && fin;
+    const int F = fin_stage(T, ad != 0);
+    if (use_ahead(T, ad) && i == F - 1) {  // AHEAD: Y_F, W (and E) at own cells
+        for (int j = 0; j < i; ++j) {
+            const bool need = t_anz(T, i, j) || t_anz(T, F, j) || t_bnz(T, j) || (ad && t_enz(T, j));
+            if (!need) continue;
+            const int s = p.nslots++;
+            p.src[s] = j;
+            p.j[s] = j;
+            p.halo[s] = t_anz(T, i, j);
+            p.gnz[s] = t_anz(T, i, j);
+            p.anz2[s] = t_anz(T, F, j);
+            p.bnz[s] = t_bnz(T, j);
+            p.dnz[s] = ad && t_enz(T, j);
+        }
+        p.epi = EPI_AHEAD;
+        p.a2new = t_anz(T, F, i);
+        p.bnew = t_bnz(T, i);
+        p.dnew = ad && t_enz(T, i);
+        p.out_k = i;                        // Y_F into k_A's buffer (k_A is never stored)
+        p.out_w = ad ? F + 1 : F;           // fixed: k_F's buffer (never stored)
+        p.out_e = ad ? F + 2 : -1;          // FSAL: k_F's buffer receives e' at stage F
+        return p;
+    }
+    if (use_ahead(T, ad) && i == F) {  // final stage fed by AHEAD: Y_F is the base (Y-direct)
+        p.base_src = F - 1;
+        p.nslots = ad ? 2 : 1;
+        p.src[0] = ad ? F + 1 : F;
+        p.j[0] = F - 1;
+        p.wslot = 0;
+        if (ad) {
+            p.src[1] = F + 2;
+            p.j[1] = F - 1;
+            p.eslot = 1;
+        }
+        p.writes_u = true;
+        p.bnew = t_bnz(T, i);
+        if (!ad) {
+            p.epi = EPI_FINAL;
+        } else {
+            p.epi = EPI_FINAL_EPART;
+            p.dnew = t_enz(T, i);
+            p.out_k = i;
+        }
+        return p;
+    }
     for (int j = 0; j < i; ++j) {
         const bool need = t_anz(T, i, j) || (fin && t_bnz(T, j)) || (err && (t_enz(T, j) || (ad == 1 && j == 0)));
         if (!need) continue;

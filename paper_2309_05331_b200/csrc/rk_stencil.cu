@@ -199,11 +199,12 @@ struct EState {
     double e[2];  // sum delta_j k_j (first term not added to 0), or e' (TAIL)
     double d[2];  // atol (+) rtol (x) (|u| (+) dt (x) |k1|)
     double h[NH > 0 ? NH : 1][2];  // Adams–Bashforth: f_{n-1} .. f_{n-k+1} at the own cell
+    double y2[2];  // AHEAD: u (+) sum a_Fj k_j (the final stage's value, without k_i)
 };
 
 // the error sum already holds a term before delta_i k_i is added
 __host__ __device__ constexpr bool has_prev_e(const StageSpec& P) {
-    bool h = P.epi == EPI_TAIL_ERR;
+    bool h = P.epi == EPI_TAIL_ERR || P.eslot >= 0;
     for (int s = 0; s < P.nslots; ++s) h = h || P.dnz[s];
     return h;
 }
@@ -222,6 +223,9 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     constexpr bool STORE_K = EPI == EPI_K || EPI == EPI_TAIL_ERR || (EPI == EPI_AB && P.out_k >= 0);
     constexpr bool AB = EPI == EPI_AB || EPI == EPI_ABM;  // Adams epilogue (raw own-cell terms)
     constexpr bool SPECR = AD == 2;  // SPEC's ratio denominator max(|u|, |u_new|) (R-28)
+    constexpr bool AHEAD = EPI == EPI_AHEAD;         // write-ahead stage (rk_stage_spec.h)
+    constexpr bool AHEAD_E = AHEAD && P.out_e >= 0;  // ... with the partial error sum
+    constexpr bool WSLOT = P.wslot >= 0, ESLOT = P.eslot >= 0;  // final stage fed by AHEAD
     using ES = EState<AB ? NS : 0>;
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr bool YD = LY.ydirect;
@@ -297,7 +301,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     // Y at ring-box position hp, component c (base + Y slots; a ghost plane is Y itself)
     auto y_at = [&](const unsigned char* st, int c, int hp, bool ghost) INLINE -> double {
         double v = reinterpret_cast<const double*>(st)[c * BOX + hp];
-        if (!ghost && !P.base_unew) {
+        if (!ghost && !P.base_unew && P.base_src < 0) {
 #pragma unroll
             for (int s = 0; s < NS; ++s)
                 if (P.gnz[s])
@@ -319,14 +323,25 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
 #pragma unroll
                 for (int s = 0; s < NS; ++s) es.h[s][c] = sval(st, s, c, r);
             }
-            if constexpr (FIN) {
+            if constexpr (FIN && WSLOT) {
+                es.w[c] = sval(st, P.wslot, c, r);  // W from the write-ahead stage
+            } else if constexpr (FIN || AHEAD) {
                 double wv = ub;
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
                     if (P.bnz[s]) wv = add(wv, mul(a.beta[s], sval(st, s, c, r)));
                 es.w[c] = wv;
             }
-            if constexpr (ESUM) {
+            if constexpr (AHEAD) {
+                double yv = ub;
+#pragma unroll
+                for (int s = 0; s < NS; ++s)
+                    if (P.anz2[s]) yv = add(yv, mul(a.g2[s], sval(st, s, c, r)));
+                es.y2[c] = yv;
+            }
+            if constexpr (ESUM && ESLOT) {
+                es.e[c] = sval(st, P.eslot, c, r);  // E from the write-ahead stage
+            } else if constexpr (ESUM || AHEAD_E) {
                 double e = 0.0;
                 bool first = true;
 #pragma unroll
@@ -482,14 +497,19 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                     unew = P.bnew ? add(ec.w[c], mul(a.beta_new, f[c])) : ec.w[c];
                     store_cell(a.out_u, G, slice, cell[r], unew);
                 }
+                if constexpr (AHEAD) {  // Y_F (read with its ring by stage F), W, E
+                    store_cell(a.out_k, G, slice, cell[r], P.a2new ? add(ec.y2[c], mul(a.g2_new, f[c])) : ec.y2[c]);
+                    store_cell(a.out_w, G, slice, cell[r], P.bnew ? add(ec.w[c], mul(a.beta_new, f[c])) : ec.w[c]);
+                }
                 double e = ec.e[c];
-                if constexpr (ESUM || EPI == EPI_TAIL_ERR) {
+                if constexpr (ESUM || EPI == EPI_TAIL_ERR || AHEAD_E) {
                     if constexpr (DNEW) {
                         const double t = mul(a.delta_new, f[c]);
                         e = HAS_PREV_E ? add(e, t) : t;
                     }
                 }
                 if constexpr (EPI == EPI_FINAL_EPART) store_cell(a.out_k, G, slice, cell[r], e);
+                if constexpr (AHEAD_E) store_cell(a.out_e, G, slice, cell[r], e);
                 if constexpr (RATIO) {
                     // r = |e| / d exactly; skip the division when e == 0 (r = +0) or when
                     // |e| <= rmax*d*(1-2^-52) (a normal number) proves r <= rmax by
@@ -602,8 +622,8 @@ cudaError_t launch_norm(const GsStageArgs& a, dim3 grid, cudaStream_t st) {
         return cudaErrorInvalidValue;
     } else if constexpr (P.epi == EPI_K && I == 0) {
         return launch_one<1, 0, 0>(a, grid, st);  // k1 = F(u): identical for every scheme
-    } else if constexpr (P.epi == EPI_K && AD != 0) {
-        return launch_one<S, 0, I>(a, grid, st);
+    } else if constexpr (P.epi == EPI_K && AD != 0 && stage_spec(S, 0, I).epi == EPI_K) {
+        return launch_one<S, 0, I>(a, grid, st);  // same k-only stage (not AHEAD when fixed)
     } else if constexpr (AD == 2 && P.epi != EPI_FINAL_ERR && P.epi != EPI_TAIL_ERR) {
         return launch_one<S, 1, I>(a, grid, st);  // only the ratio stages differ (R-28)
     } else {
