@@ -168,6 +168,11 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------
+# B/cell per step of each scheme's fused stage-by-stage schedule (the gate's
+# bytes; this build moves fewer for DOPRI5 / CK54 through the write-ahead stage)
+SURVEY_BYTES = {"euler": 32, "rk4": 208, "cash_karp54": 432, "dopri5": 432}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -229,6 +234,10 @@ def main():
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    def survey_gate(bytes_per_cell, cell_tries, ms):
+        eff = bytes_per_cell * cell_tries / (ms / 1e3) / 1e9
+        return {"bytes_per_cell": bytes_per_cell, "effective_gbs": eff, "frac": eff / peak, "target_frac": 0.70}
 
     def halo_of(s):
         if world == 1 or not s["halo_exchanges"]:
@@ -299,7 +308,10 @@ def main():
                          "algorithmic_bytes_per_launch": s["stage_bytes"] / max(1, s["stage_launches"]),
                          "algorithmic_bytes_per_cell_try": step_bytes / cells_local,
                          "avg_launch_ms": k_ms / max(1, s["stage_launches"]),
-                         "launches": s["stage_launches"], "peak_source": peak_src},
+                         "launches": s["stage_launches"], "peak_source": peak_src,
+                         # SURVEY §8d gate: cells x tries x 528 B (its DOPRI5 adaptive schedule)
+                         # over the whole timed region, against >= 0.70 of the measured peak
+                         "survey_gate": survey_gate(528, cells_local * tries, ms)},
             "gpu_launches": s["kernel_launches"],
             "clocks": getattr(clk, "result", None),
         }
@@ -341,6 +353,8 @@ def main():
                             "algorithmic_bytes_per_cell_step": s4["stage_bytes"] / args.steps / cells_local,
                             "avg_launch_ms": s4["stage_kernel_ms"] / max(1, s4["stage_launches"])},
                "gpu_launches": s4["kernel_launches"]}
+        if scheme in SURVEY_BYTES:  # SURVEY §8d's per-scheme B/cell (stage-by-stage schedule)
+            out["roofline"]["survey_gate"] = survey_gate(SURVEY_BYTES[scheme], cells_local * args.steps, ms4)
         h = halo_of(s4)
         if h:
             out["halo"] = h
@@ -455,6 +469,27 @@ def main():
                      "persistent": "gs64_rk4_persistent"}[mode]] = {
                     "value": n64 ** 3 * 20 / (m / 1e3), "unit": "cell-updates/s", "ms_per_step": m / 20,
                     "config": "configs[2]: 64^3, RK4, dt=1, t in [0,20], median of integrate_const calls"}
+            # DOPRI5 error control on the same 64^3 grid (tol 1e-6, dt0 = 1, t in [0, 20]): the
+            # host-driven try loop over K3 stage launches vs the whole loop in one K5 launch
+            g.set_option(rk.OPT_USE_GRAPH, 0)
+            for dl in (0, 1):
+                g.set_option(rk.OPT_DEVICE_LOOP, dl)
+                g.set_option(rk.OPT_COOP_MAX_CELLS, n64 ** 3 if dl else 0)
+                ms, tries, acc = [], 0, 0
+                for _ in range(max(3, args.steps)):
+                    g.set(u64)
+                    torch.cuda.synchronize()
+                    ev0.record(stream)
+                    a, r = g.integrate_adaptive("dopri5", 0.0, 20.0, 1.0, TOL, TOL)
+                    ev1.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(ev0.elapsed_time(ev1))
+                    tries, acc = a + r, a
+                m = statistics.median(ms)
+                out["gs64_dopri5_adaptive_device_loop" if dl else "gs64_dopri5_adaptive"] = {
+                    "value": n64 ** 3 * acc / (m / 1e3), "unit": "cell-updates/s", "ms_per_step": m / acc,
+                    "tries": tries, "accepted": acc, "us_per_try": 1e3 * m / tries,
+                    "config": "64^3, DOPRI5 tol 1e-6, dt0 1, t in [0,20], median of integrate_adaptive calls"}
             g.close()
             nv = 1000000
             v = ctx.vector(nv)

@@ -102,8 +102,9 @@ typedef enum {
     RK_OPT_USE_GRAPH = 5,    /* 1: rk_integrate_const of a grid (world == 1, no loopback, >= 5
                                 steps) replays pairs of steps from one captured CUDA graph
                                 (SURVEY f3): identical results, no per-launch host cost   */
-    RK_OPT_DEVICE_LOOP = 6,  /* 1: rk_integrate_adaptive of a vector state (world == 1) runs
-                                as one cooperative kernel: tries, error max, controller and
+    RK_OPT_DEVICE_LOOP = 6,  /* 1: rk_integrate_adaptive of a vector state, or of a grid within
+                                RK_OPT_COOP_MAX_CELLS (no halo path), on one GPU runs as one
+                                cooperative kernel: tries, error max, controller and
                                 accept/reject on the device, no host sync per try (
                                 DESIGN.md R-27).  Same results; else the host loop is used.   */
     RK_OPT_HALO_P2P = 7,     /* grid, halo path (world > 1 or HALO_LOOPBACK): 1 replaces the

@@ -140,4 +140,38 @@ __device__ inline double pow_dd(double x, double y) {
     return dd_exp_round(dd_mul_d(dd_log(x), y));
 }
 
+// The host step adjusters (rk_runtime.cu step_adjust / step_adjust_spec; R-12, R-28)
+// on the device, with pow_dd for libm's pow: e_rej / e_acc are the host-computed exponents,
+// emin = 5^-p (Odeint's clamp).  Used by the device-resident adaptive loops (vector: K1 loop,
+// grid: K5 loop); every thread of a grid evaluates it on the same inputs -> the same decision.
+static __device__ __noinline__ double step_adjust_dev(double E, double e_rej, double e_acc, double emin, int ctrl,
+                                                      double dt, int* ok) {
+    if (ctrl == 1) {  // SPEC's elementary controller (R-28): always rescale
+        if (E <= 1.0) {
+            double fac = E == 0.0 ? 5.0 : __dmul_rn(0.9, pow_dd(E, e_acc));
+            if (fac < 0.2) fac = 0.2;
+            if (fac > 5.0) fac = 5.0;
+            *ok = 1;
+            return __dmul_rn(dt, fac);
+        }
+        double fac = __dmul_rn(0.9, pow_dd(E, e_rej));
+        if (fac < 0.2) fac = 0.2;
+        *ok = 0;
+        return __dmul_rn(dt, fac);
+    }
+    if (E > 1.0) {
+        double fac = __dmul_rn(0.9, pow_dd(E, e_rej));
+        if (fac < 0.2) fac = 0.2;
+        *ok = 0;
+        return __dmul_rn(dt, fac);
+    }
+    *ok = 1;
+    if (E < 0.5) {
+        double Ec = emin;
+        if (E > Ec) Ec = E;
+        return __dmul_rn(dt, __dmul_rn(0.9, pow_dd(Ec, e_acc)));
+    }
+    return dt;
+}
+
 }  // namespace rkb

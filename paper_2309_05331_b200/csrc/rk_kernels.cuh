@@ -152,20 +152,38 @@ cudaError_t launch_gs_pack(const GsStageArgs& a, double* dst0, double* dst1, con
 cudaError_t launch_fill_ring(double* a, const GridGeom& g, int nslices, cudaStream_t st);
 
 // ---------------------------------------------------------------------------------------
-// K5: whole fixed-step RK steps of Gray–Scott on a small single-GPU grid in one persistent
+// K5: whole RK integrations of Gray–Scott on a small single-GPU grid in one persistent
 // cooperative launch (rk_smallgrid.cu; grid-wide barrier between stages, u/u_new ping-pong).
+struct CoopCoef {          // dt-scaled coefficients of a step / try
+    double g[13][13];      // dt * a_ij
+    double beta[13];       // dt * b_j
+    double delta[13];      // dt * (b_j - bhat_j)
+};
 struct GsCoopArgs {
     double* buf[2];        // buf[0] = u on entry, buf[1] = u_new; after nsteps u is buf[nsteps & 1]
     double* k[13];         // k_j buffers (padded layout); k_last is not stored
     double* ybuf[2];       // stage values Y_i (padded layout), alternating between stages
     GridGeom geo;          // nzl = nz: one GPU, z wraps by index
-    double g[13][13];      // dt * a_ij
-    double beta[13];       // dt * b_j
+    CoopCoef cf;           // fixed steps: the step's coefficients
     double d1, d2, F, FK, inv_h2;
-    int nsteps;
+    int nsteps;            // fixed steps
 };
 cudaError_t launch_gs_coop(int scheme, const GsCoopArgs& a, cudaStream_t st, int device);
-int coop_last_stage(int scheme);  // last stage index (b_j != 0) = number of stored k_j
+int coop_last_stage(int scheme);           // last stage index (b_j != 0) = number of stored k_j
+int coop_last_stage_adaptive(int scheme);  // last stage with b_j or e_j != 0 (CK54/DOPRI5/RKF78)
+// The whole integrate_adaptive (RK_OPT_DEVICE_LOOP on a small grid): tries, error max and
+// the controller on the device; results in *res (as the vector loop's PwLoopResult).
+struct GsCoopLoopArgs {
+    GsCoopArgs c;          // buffers, geometry, RHS parameters (c.cf, c.nsteps unused)
+    double A[13][13], B[13], Ew[13];  // the scheme's a_ij, b_j, e_j as doubles (rat_double)
+    double t0, t1, dt0, atol, rtol;
+    double e_rej, e_acc, emin;        // the host controller's exponents / clamp
+    int ctrl;                         // 0 Odeint (R-12), 1 SPEC (R-28)
+    int max_tries;
+    unsigned long long* red;          // [3] zeroed: per-try error-max slots (rotating)
+    PwLoopResult* res;
+};
+cudaError_t launch_gs_coop_adaptive(int scheme, const GsCoopLoopArgs& a, cudaStream_t st, int device);
 
 // ---------------------------------------------------------------------------------------
 // K2 / K4: algebra.

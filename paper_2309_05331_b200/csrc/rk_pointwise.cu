@@ -149,36 +149,6 @@ static cudaError_t launch_s(const PwArgs& a, cudaStream_t st, int num_sms) {
 // error-ratio max is combined with one atomicMax per CTA and a grid-wide barrier, and all
 // threads then take the same accept/reject decision from the same E.  Only the final state
 // and the counters return to the host.
-__device__ __noinline__ double step_adjust_dev(double E, double e_rej, double e_acc, double emin, int ctrl,
-                                               double dt, int* ok) {
-    if (ctrl == 1) {  // SPEC's elementary controller (R-28): always rescale
-        if (E <= 1.0) {
-            double fac = E == 0.0 ? 5.0 : __dmul_rn(0.9, pow_dd(E, e_acc));
-            if (fac < 0.2) fac = 0.2;
-            if (fac > 5.0) fac = 5.0;
-            *ok = 1;
-            return __dmul_rn(dt, fac);
-        }
-        double fac = __dmul_rn(0.9, pow_dd(E, e_rej));
-        if (fac < 0.2) fac = 0.2;
-        *ok = 0;
-        return __dmul_rn(dt, fac);
-    }
-    if (E > 1.0) {
-        double fac = __dmul_rn(0.9, pow_dd(E, e_rej));
-        if (fac < 0.2) fac = 0.2;
-        *ok = 0;
-        return __dmul_rn(dt, fac);
-    }
-    *ok = 1;
-    if (E < 0.5) {
-        double Ec = emin;
-        if (E > Ec) Ec = E;
-        return __dmul_rn(dt, __dmul_rn(0.9, pow_dd(Ec, e_acc)));
-    }
-    return dt;
-}
-
 template <int S, int RHS, int ERR>
 __global__ void __launch_bounds__(256) pointwise_loop_kernel(const PwLoopArgs a) {
     namespace cg = cooperative_groups;

@@ -791,8 +791,8 @@ static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
     a.ybuf[0] = st->ybuf[0];
     a.ybuf[1] = st->ybuf[1];
     for (int i = 0; i < C.s; ++i) {
-        for (int j = 0; j < i; ++j) a.g[i][j] = dt * C.a[i][j];
-        a.beta[i] = dt * C.b[i];
+        for (int j = 0; j < i; ++j) a.cf.g[i][j] = dt * C.a[i][j];
+        a.cf.beta[i] = dt * C.b[i];
     }
     a.d1 = st->d1;
     a.d2 = st->d2;
@@ -1111,7 +1111,43 @@ static rk_status device_adaptive_loop(rk_state st, int scheme, double t0, double
     a.red = st->d_loop;
     a.res = reinterpret_cast<PwLoopResult*>(st->d_loop + 3);
     CK_CTX(ctx, cudaMemsetAsync(st->d_loop, 0, 3 * sizeof(unsigned long long) + sizeof(PwLoopResult), ctx->stream));
-    CK_CTX(ctx, launch_pointwise_loop(scheme, a, ctx->stream, ctx->device));
+    if (st->grid) {  // K5: the stencil stages, error max and controller in one cooperative launch
+        GsCoopLoopArgs g{};
+        TRY(ensure_k(st, std::max(coop_last_stage_adaptive(scheme), 1)));
+        for (int b = 0; b < 2; ++b)
+            if (!st->ybuf[b]) TRY(alloc_array(st, &st->ybuf[b], nullptr));
+        g.c.buf[0] = st->u;
+        g.c.buf[1] = st->u_new;
+        for (int j = 0; j < 13; ++j) g.c.k[j] = j < st->nk ? st->k[j] : nullptr;
+        g.c.ybuf[0] = st->ybuf[0];
+        g.c.ybuf[1] = st->ybuf[1];
+        g.c.geo = st->geo;
+        g.c.d1 = st->d1;
+        g.c.d2 = st->d2;
+        g.c.F = st->F;
+        g.c.FK = st->F + st->K;
+        g.c.inv_h2 = 1.0 / (st->h * st->h);
+        for (int i = 0; i < 13; ++i) {
+            for (int j = 0; j < 13; ++j) g.A[i][j] = a.a[i][j];
+            g.B[i] = a.b[i];
+            g.Ew[i] = a.e[i];
+        }
+        g.t0 = t0;
+        g.t1 = t1;
+        g.dt0 = dt0;
+        g.atol = atol;
+        g.rtol = rtol;
+        g.e_rej = a.e_rej;
+        g.e_acc = a.e_acc;
+        g.emin = a.emin;
+        g.ctrl = a.ctrl;
+        g.max_tries = a.max_tries;
+        g.red = a.red;
+        g.res = a.res;
+        CK_CTX(ctx, launch_gs_coop_adaptive(scheme, g, ctx->stream, ctx->device));
+    } else {
+        CK_CTX(ctx, launch_pointwise_loop(scheme, a, ctx->stream, ctx->device));
+    }
     PwLoopResult r{};
     CK_CTX(ctx, cudaMemcpyAsync(&r, a.res, sizeof r, cudaMemcpyDeviceToHost, ctx->stream));
     CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
@@ -1121,7 +1157,7 @@ static rk_status device_adaptive_loop(rk_state st, int scheme, double t0, double
     st->stats.tries += tries;
     st->stats.accepted += r.accepted;
     st->stats.rejected += r.rejected;
-    st->stats.rhs_evals += tries * (int64_t)num_stages(scheme, true);
+    st->stats.rhs_evals += tries * (int64_t)(st->grid ? coop_last_stage_adaptive(scheme) + 1 : num_stages(scheme, true));
     st->stats.last_err_ratio = r.last_E;
     st->stats.last_dt = r.dt;
     if (accepted) *accepted = r.accepted;
@@ -1626,7 +1662,8 @@ rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double
         return fail(RK_ERR_UNSUPPORTED, "scheme %d has no embedded error estimate", (int)scheme);
     TRY(check_rhs(st));
     DeviceGuard g(st->ctx->device);
-    if (st->device_loop && !st->grid && st->ctx->world == 1) {
+    if (st->device_loop && st->ctx->world == 1 &&
+        (!st->grid || (!st->loopback && !st->p2p && st->local * st->nx * st->ny <= st->coop_max_cells))) {
         TRY(device_adaptive_loop(st, scheme, t0, t1, dt0, atol, rtol, accepted, rejected));
         return finite_check(st, 0, t1, true);
     }
