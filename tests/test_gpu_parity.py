@@ -947,3 +947,27 @@ def test_device_loop_grid_errors(ctx):
         _gs_adaptive(ctx, (n, n, n), u0 + 0.05 * rk_inputs.random_state(2 * n ** 3, 2).reshape(n, 2, n, n),
                      "dopri5", 20.0, 1e-10, 1, max_tries=1)
     assert e.value.status == "RK_ERR_STALL"
+
+
+@pytest.mark.parametrize("scheme", ["dopri5", "cash_karp54", "rkf78"])
+@pytest.mark.parametrize("p2p", [0, 1], ids=["nccl_path", "p2p"])
+@pytest.mark.parametrize("overlap", [1, 0])
+@pytest.mark.parametrize("dims", [(24, 24, 24), (33, 17, 3), (16, 8, 2), (16, 8, 1)],
+                         ids=lambda d: "x".join(map(str, d)))
+def test_gs_halo_loopback_adaptive(ctx, scheme, p2p, overlap, dims):
+    """Error-controlled runs through the multi-GPU stage path on one GPU (pack, ghost planes,
+    interior + boundary launches; the write-ahead stage's Y_F is what the final stage's pack
+    ships): counts and final state bitwise vs the oracle, incl. slabs of 1..3 planes."""
+    import paper_2309_05331_b200 as rk
+    nx, ny, nz = dims
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=6) + 0.02 * rk_inputs.random_state(
+        2 * nx * ny * nz, 8).reshape(nz, 2, ny, nx)
+    st = gs_state(ctx, nx, ny, nz, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+    st.set_option(rk.OPT_HALO_P2P, p2p)
+    st.set_option(rk.OPT_HALO_OVERLAP, overlap)
+    a, r = st.integrate_adaptive(scheme, 0.0, 10.0, 4.0, 1e-6, 1e-6)
+    uo, ao, ro, rc = oracle.integrate_adaptive(oracle.gray_scott_problem(nx, ny, nz), OS[scheme], u0,
+                                               0.0, 10.0, 4.0, 1e-6, 1e-6)
+    assert rc == 0 and (a, r) == (ao, ro) and r > 0
+    assert bitwise(st.get(), uo)
