@@ -561,6 +561,56 @@ def main():
             v.close()
         return out
 
+    def strong_emul_leg():
+        # configs[3] on ONE GPU: the per-GPU share of a G-way strong-scaling run (512 x 512 x
+        # 512/G slab of the 512^3 IC) through the multi-GPU stage path in loopback mode (pack,
+        # ghost planes, interior + overlapped boundary launches; the exchange is a device copy
+        # on the comm stream instead of NCCL over NVLink).  Compute-side efficiency only:
+        # T(512^3) / (G * T(slab)); NVLink time is not in it.
+        out = {}
+        for G in (1, 2, 4, 8):
+            nzl = n // G
+            eg = ctx.grid(n, n, nzl, 2)
+            eg.set_rhs_gray_scott(h=H)
+            eg.set_option(rk.OPT_HALO_LOOPBACK, 1 if G > 1 else 0)
+            ue = torch.from_numpy(rk_inputs.gray_scott_ic(n, n, n, seed=42, z0=0, nzl=nzl, zblocks=1)).cuda(local)
+            res = {}
+            for scheme in ("dopri5", "rk4"):
+                eg.set(ue)
+                t, dt = 0.0, 1.0
+
+                def one():
+                    nonlocal t, dt
+                    if scheme == "rk4":
+                        eg.do_step("rk4", t, 1.0)
+                        return 1
+                    k = 0
+                    while True:
+                        ok, _, dtn = eg.try_step("dopri5", t, dt, TOL, TOL)
+                        k += 1
+                        if ok:
+                            t, dt = t + dt, dtn
+                            return k
+                        dt = dtn
+                for _ in range(args.warmup):
+                    one()
+                barrier()
+                ev0.record(stream)
+                tries = sum(one() for _ in range(args.steps))
+                ev1.record(stream)
+                barrier()
+                ms = ev0.elapsed_time(ev1) / args.steps
+                res[scheme] = {"ms_per_step": ms, "tries": tries}
+            eg.close()
+            out[f"G{G}"] = {"nz_per_gpu": nzl, **res}
+        for G in (2, 4, 8):
+            for scheme in ("dopri5", "rk4"):
+                b1 = out["G1"][scheme]["ms_per_step"] / out["G1"][scheme]["tries"]
+                bg = out[f"G{G}"][scheme]["ms_per_step"] / out[f"G{G}"][scheme]["tries"]
+                out[f"G{G}"][scheme]["compute_efficiency_per_try"] = b1 / (G * bg)
+        out["config"] = "per-GPU share of configs[3] (512^3 strong scaling) on one GPU, loopback halo path"
+        return out
+
     def strong_leg():
         # configs[3]: 512^3 in total, z-slab over the ranks (strong scaling), DOPRI5 adaptive
         # tol 1e-6 and RK4 dt = 1, as the headline but with nz_local = 512 / N
@@ -628,6 +678,8 @@ def main():
             extra["rk4_loopback_p2p"] = run_leg(rk4_leg, args.overlap, "rk4", 1, 1)
         elif "p2p" in legs:  # opt-in at N > 1: needs CUDA IPC between the rank processes
             extra["rk4_p2p"] = run_leg(rk4_leg, args.overlap, "rk4", 1, 0)
+    if "strong_emul" in legs and world == 1:
+        extra["strong_emul"] = run_leg(strong_emul_leg)
     if "strong" in legs and world > 1:
         extra["strong"] = run_leg(strong_leg)
     if "rk4_native" in legs:

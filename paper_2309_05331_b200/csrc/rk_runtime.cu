@@ -44,6 +44,7 @@ static rk_status fail(rk_status s, const char* fmt, ...) {
 struct rk_ctx_s {
     int rank = 0, world = 1, device = 0;
     cudaStream_t stream = nullptr, comm = nullptr;
+    cudaStream_t bnd = nullptr;  // halo path: pack + boundary-plane launches, beside the interior
     bool own_stream = false;
     cudaStream_t capture = nullptr;  // private stream for CUDA-graph capture (RK_OPT_USE_GRAPH)
     ncclComm_t nccl = nullptr;
@@ -135,6 +136,7 @@ struct rk_state_s {
     double* sendbuf = nullptr;       // [lo plane | hi plane]
     double* ghostbuf = nullptr;      // [ghost_hi | ghost_lo] (so one message serves world==2)
     cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_bnd = nullptr;  // stage start on the compute stream / boundary done
     // peer-to-peer halo (RK_OPT_HALO_P2P): the pack kernel stores Y_i's boundary planes straight
     // into the neighbours' ghost planes (CUDA IPC over NVLink) with a flag handshake
     bool p2p = false, p2p_ready = false;
@@ -226,6 +228,7 @@ static rk_status resolve_timing(rk_state st) {
     rk_ctx ctx = st->ctx;
     CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
     if (ctx->comm) CK_CTX(ctx, cudaStreamSynchronize(ctx->comm));
+    if (ctx->bnd) CK_CTX(ctx, cudaStreamSynchronize(ctx->bnd));
     for (auto& p : st->pending) {
         float ms = 0.f;
         CK_CTX(ctx, cudaEventElapsedTime(&ms, p.a, p.b));
@@ -331,6 +334,8 @@ static rk_status ensure_halo(rk_state st) {
     CK_CTX(st->ctx, encode_grid_maps(st->tm_glo.m, st->ghostbuf + plane_values(st), st->geo, 1));
     CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_pack, cudaEventDisableTiming));
     CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_halo, cudaEventDisableTiming));
+    CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_ready, cudaEventDisableTiming));
+    CK_CTX(st->ctx, cudaEventCreateWithFlags(&st->ev_bnd, cudaEventDisableTiming));
     return RK_OK;
 }
 
@@ -427,16 +432,17 @@ static int pick_zchunk(rk_state st, const StagePlan& p, int range) {
     return std::min(zc, range);
 }
 
-static rk_status launch_stage_timed(rk_state st, const StagePlan& p, GsStageArgs& a) {
+static rk_status launch_stage_timed(rk_state st, const StagePlan& p, GsStageArgs& a, cudaStream_t sm = nullptr) {
     rk_ctx ctx = st->ctx;
+    if (!sm) sm = ctx->stream;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (st->timing) {
         e0 = pool_event(st);
         e1 = pool_event(st);
-        CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+        CK_CTX(ctx, cudaEventRecord(e0, sm));
     }
     int nl = 0;
-    CK_CTX(ctx, launch_gs_stage(p.scheme, p.adaptive, p.stage, a, ctx->stream, &nl));
+    CK_CTX(ctx, launch_gs_stage(p.scheme, p.adaptive, p.stage, a, sm, &nl));
     st->stats.kernel_launches += nl;
     st->stats.stage_launches += nl;
     if (nl) {
@@ -446,17 +452,18 @@ static rk_status launch_stage_timed(rk_state st, const StagePlan& p, GsStageArgs
         st->stats.stage_bytes += planes * st->nx * st->ny * 2 * (int64_t)sizeof(double) * arrays;
     }
     if (st->timing) {
-        CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+        CK_CTX(ctx, cudaEventRecord(e1, sm));
         st->pending.push_back({e0, e1, 0});
         if (st->pending.size() > 4096) TRY(resolve_timing(st));
     }
     return RK_OK;
 }
 
-static rk_status halo_exchange(rk_state st) {
+// exchange the planes packed on stream `src` (comm stream; ev_halo marks completion)
+static rk_status halo_exchange(rk_state st, cudaStream_t src) {
     rk_ctx ctx = st->ctx;
     const int64_t pv = plane_values(st);
-    CK_CTX(ctx, cudaEventRecord(st->ev_pack, ctx->stream));
+    CK_CTX(ctx, cudaEventRecord(st->ev_pack, src));
     CK_CTX(ctx, cudaStreamWaitEvent(ctx->comm, st->ev_pack, 0));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (st->timing) {
@@ -576,8 +583,11 @@ static rk_status run_gs_stage_p2p(rk_state st, const StagePlan& p, GsStageArgs& 
     ps.notify[1] = st->peer_flags[1] + P2P_READY_LO;  // my plane nzl-1 is the upper's ghost_lo
     ps.count = st->pflags + P2P_COUNT;
     ps.seq = seq;
+    // the boundary stream starts from everything the compute stream has issued so far
+    CK_CTX(ctx, cudaEventRecord(st->ev_ready, ctx->stream));
+    CK_CTX(ctx, cudaStreamWaitEvent(ctx->bnd, st->ev_ready, 0));
     CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->peer_ghost[0] + (2 * b + 0) * pv,
-                               st->peer_ghost[1] + (2 * b + 1) * pv, ps, ctx->stream));
+                               st->peer_ghost[1] + (2 * b + 1) * pv, ps, ctx->bnd));
     st->stats.kernel_launches += 1;
     st->stats.halo_exchanges += 1;
     st->stats.halo_bytes += (int64_t)sizeof(double) * 2 * pv;
@@ -604,7 +614,10 @@ static rk_status run_gs_stage_p2p(rk_state st, const StagePlan& p, GsStageArgs& 
     bs.notify[1] = st->peer_flags[1] + P2P_ACK_LO;  // my ghost_hi came from the upper neighbour
     bs.count = st->pflags + P2P_COUNT;
     bs.seq = seq;
-    return launch_stage_timed(st, p, bd);
+    TRY(launch_stage_timed(st, p, bd, ctx->bnd));  // beside the interior launch
+    CK_CTX(ctx, cudaEventRecord(st->ev_bnd, ctx->bnd));
+    CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_bnd, 0));  // stage complete on the compute stream
+    return RK_OK;
 }
 
 static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
@@ -619,24 +632,35 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
     }
     if (st->p2p) return run_gs_stage_p2p(st, p, a);
     // multi-GPU path: Y_i on the two boundary planes -> neighbours' ghost planes
-    CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->sendbuf, st->sendbuf + plane_values(st), P2pSync{}, ctx->stream));
-    st->stats.kernel_launches += 1;
-    TRY(halo_exchange(st));
     a.has_ghi = 1;
     a.has_glo = 1;
     a.tm_ghi = st->tm_ghi.m[2 * (stage_rows(p.sp) - 1)];
     a.tm_glo = st->tm_glo.m[2 * (stage_rows(p.sp) - 1)];
     if (st->overlap && nzl > 2) {
+        // boundary stream: pack -> (comm stream: exchange) -> boundary planes, all beside the
+        // interior launch on the compute stream; the two join at the end of the stage (the
+        // next stage's interior reads the boundary planes as z neighbours)
+        CK_CTX(ctx, cudaEventRecord(st->ev_ready, ctx->stream));
+        CK_CTX(ctx, cudaStreamWaitEvent(ctx->bnd, st->ev_ready, 0));
+        CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->sendbuf, st->sendbuf + plane_values(st), P2pSync{}, ctx->bnd));
+        st->stats.kernel_launches += 1;
+        TRY(halo_exchange(st, ctx->bnd));
         GsStageArgs in = a;  // interior planes [1, nzl-1) never touch ghost planes
         in.z_lo = 1;
         in.z_hi = nzl - 1;
         in.zchunk = pick_zchunk(st, p, nzl - 2);
         TRY(launch_stage_timed(st, p, in));
-        CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_halo, 0));
+        CK_CTX(ctx, cudaStreamWaitEvent(ctx->bnd, st->ev_halo, 0));
         GsStageArgs bd = a;
         bd.zmode = 1;
-        return launch_stage_timed(st, p, bd);
+        TRY(launch_stage_timed(st, p, bd, ctx->bnd));
+        CK_CTX(ctx, cudaEventRecord(st->ev_bnd, ctx->bnd));
+        CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_bnd, 0));
+        return RK_OK;
     }
+    CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->sendbuf, st->sendbuf + plane_values(st), P2pSync{}, ctx->stream));
+    st->stats.kernel_launches += 1;
+    TRY(halo_exchange(st, ctx->stream));
     CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_halo, 0));
     a.zchunk = pick_zchunk(st, p, nzl);
     return launch_stage_timed(st, p, a);
@@ -1280,6 +1304,7 @@ rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* 
     auto bail = [&](rk_status s) {
         if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
         if (ctx->comm) cudaStreamDestroy(ctx->comm);
+        if (ctx->bnd) cudaStreamDestroy(ctx->bnd);
         delete ctx;
         return s;
     };
@@ -1292,8 +1317,9 @@ rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* 
     }
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if (cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi) != cudaSuccess)
-        return bail(fail(RK_ERR_CUDA, "comm stream create failed"));
+    if (cudaStreamCreateWithPriority(&ctx->comm, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&ctx->bnd, cudaStreamNonBlocking, hi) != cudaSuccess)
+        return bail(fail(RK_ERR_CUDA, "comm / boundary stream create failed"));
     if (cudaMalloc((void**)&ctx->d_scratch, 8) != cudaSuccess ||
         cudaMallocHost((void**)&ctx->h_scratch, 8) != cudaSuccess)
         return bail(fail(RK_ERR_OOM, "scratch allocation failed"));
@@ -1314,6 +1340,7 @@ rk_status rk_ctx_destroy(rk_ctx ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
     if (ctx->comm) cudaStreamDestroy(ctx->comm);
+    if (ctx->bnd) cudaStreamDestroy(ctx->bnd);
     if (ctx->capture) cudaStreamDestroy(ctx->capture);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     cudaFree(ctx->d_scratch);
@@ -1404,6 +1431,7 @@ rk_status rk_state_destroy(rk_state st) {
     DeviceGuard g(st->ctx->device);
     cudaStreamSynchronize(st->ctx->stream);
     if (st->ctx->comm) cudaStreamSynchronize(st->ctx->comm);
+    if (st->ctx->bnd) cudaStreamSynchronize(st->ctx->bnd);
     cudaFree(st->u);
     cudaFree(st->u_new);
     for (int j = 0; j < st->nk; ++j) cudaFree(st->k[j]);
@@ -1421,6 +1449,8 @@ rk_status rk_state_destroy(rk_state st) {
     cudaFree(st->d_loop);
     if (st->ev_pack) cudaEventDestroy(st->ev_pack);
     if (st->ev_halo) cudaEventDestroy(st->ev_halo);
+    if (st->ev_ready) cudaEventDestroy(st->ev_ready);
+    if (st->ev_bnd) cudaEventDestroy(st->ev_bnd);
     for (auto& p : st->pending) {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
