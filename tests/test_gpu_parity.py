@@ -971,3 +971,29 @@ def test_gs_halo_loopback_adaptive(ctx, scheme, p2p, overlap, dims):
                                                0.0, 10.0, 4.0, 1e-6, 1e-6)
     assert rc == 0 and (a, r) == (ao, ro) and r > 0
     assert bitwise(st.get(), uo)
+
+
+def test_max_size_1024_cubed_rk4(ctx):
+    """Maximum size: a 1024^3 grid (2^31 values per array, 16 GiB; five arrays for RK4 fill
+    ~81 GiB of HBM), so padded offsets of the upper planes exceed int32.  One RK4 step in the
+    default launch configuration; sampled cells (incl. the last planes and the periodic
+    corners) bitwise against the oracle on their radius-5 neighbourhoods."""
+    import gc
+    gc.collect()
+    n = 1024
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    st = gs_state(ctx, n, n, n, u0)
+    st.do_step("rk4", 0.0, 1.0)
+    g = st.get()
+    st.close()
+    lo, hi = rk_inputs.cube_range(n)
+    pts = [(1023, 1023, 1023), (1023, 0, 511), (1022, 1023, 0), (0, 0, 0), (lo, lo, lo),
+           (hi - 1, hi, lo - 1), (hi, 700, hi - 1), (900, lo + 3, hi)]
+    r = 5
+    p = oracle.gray_scott_problem(2 * r + 1, 2 * r + 1, 2 * r + 1)
+    for (z, y, x) in pts:
+        blk = _sample_block(u0, z, y, x, r)
+        out = oracle.step(p, oracle.RK4, 0.0, 1.0, blk).reshape(blk.shape)
+        assert bitwise(g[z, :, y, x], out[r, :, r, r]), (z, y, x)
+    del g, u0
+    gc.collect()
