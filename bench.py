@@ -406,6 +406,30 @@ def main():
             out["halo"] = h
         return out
 
+    # K6 (RK_OPT_FUSED_STEP, one GPU): the whole step in one launch, stage values on chip.
+    # Bound by the FP64 pipe / latency, not HBM: roofline against the FP64 issue rate
+    # (148 SMs x 64 non-FMA fp64 ops/clk x the sampled SM clock) with the algorithmic op count
+    # per cell-step (RK4 168, midpoint 78; margin re-evaluations not counted).
+    K6_OPS = {"rk4": 168, "midpoint": 78}
+
+    def k6_leg(scheme):
+        st.set_option(rk.OPT_FUSED_STEP, 1)
+        with ClockSampler(local) as clk:
+            out = rk4_leg(args.overlap, scheme)
+        st.set_option(rk.OPT_FUSED_STEP, 0)
+        mhz = (getattr(clk, "result", None) or {}).get("sm_mhz") or 1965.0
+        peak_ops = 148 * 64 * mhz * 1e6 / 1e12
+        ms = out["ms_per_step"]
+        k_ms = out["roofline"]["avg_launch_ms"]
+        ach = K6_OPS[scheme] * cells_local / (k_ms / 1e3) / 1e12 if k_ms else None
+        out["hbm_bytes_per_cell_step"] = out["roofline"]["algorithmic_bytes_per_cell_step"]
+        out["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak_ops, "unit": "TFLOP/s (fp64, non-FMA)",
+                           "frac": ach / peak_ops if ach else None, "ops_per_cell_step": K6_OPS[scheme],
+                           "avg_launch_ms": k_ms}
+        out["kernel"] = "gs_fused_kernel (K6: whole step per launch, temporal blocking over the stages)"
+        out["ms_per_step"] = ms
+        return out
+
     def e2e_leg():
         # the same metric through the C-ABI with HOST buffers: every step copies the state in
         # (pinned H2D) and the result out (pinned D2H) inside the timed region
@@ -684,6 +708,9 @@ def main():
         extra["strong"] = run_leg(strong_leg)
     if "rk4_native" in legs:
         extra["rk4_native"] = run_leg(native_rk4_leg)
+    for sch in ("rk4", "midpoint"):  # opt-in: --legs rk4_k6,midpoint_k6 (K6)
+        if sch + "_k6" in legs and world == 1:
+            extra[sch + "_k6"] = run_leg(k6_leg, sch)
     if "exp512" in legs:
         extra["exp512"] = run_leg(exp512_leg)
     if "small" in legs:

@@ -128,11 +128,17 @@ typedef enum {
                                 a NaN/Inf gives RK_ERR_DIVERGED at that t.  Costs one
                                 state read per check (vector integrate_const: the n steps run
                                 in one launch).  0 (default): no check.                   */
-    RK_OPT_COOP_MAX_CELLS = 10 /* fixed RK steps (do_step / integrate_const) of a Gray–Scott grid
+    RK_OPT_COOP_MAX_CELLS = 10,/* fixed RK steps (do_step / integrate_const) of a Gray–Scott grid
                                 with at most this many cells, one GPU, no halo path, run as one
                                 persistent cooperative launch (all stages of all steps, grid-
                                 wide barrier between stages): same results bit for
                                 bit, no per-stage launch cost.  Default 2^18 (64^3); 0 = off. */
+    RK_OPT_FUSED_STEP = 11     /* 1: fixed RK4 / explicit-midpoint steps of a Gray–Scott grid
+                                (one GPU, no halo path, above RK_OPT_COOP_MAX_CELLS) run as ONE
+                                launch per step that keeps every stage value on chip (temporal
+                                blocking across the stages, K6): u read and
+                                u_new written once per step (32 B/cell instead of 208 / 80),
+                                same results bit for bit.  0: stage-by-stage launches.       */
 } rk_option;
 
 /* Counters since creation or the last rk_reset_stats. */

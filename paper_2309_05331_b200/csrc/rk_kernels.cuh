@@ -186,6 +186,24 @@ struct GsCoopLoopArgs {
 cudaError_t launch_gs_coop_adaptive(int scheme, const GsCoopLoopArgs& a, cudaStream_t st, int device);
 
 // ---------------------------------------------------------------------------------------
+// K6: one whole fixed step of a chained-stage scheme (Y_s = u + g_s k_{s-1}: RK4, explicit
+// midpoint) of Gray–Scott in ONE launch, temporal blocking across the stages (rk_fused.cu).
+struct GsFusedArgs {
+    CUtensorMap tm_u;      // u: box of a 32x16 tile + L-cell margin (encode_fused_map)
+    const double* u;       // u (periodic margin patches on the domain edge)
+    double* out;           // u_new (padded layout, ring copies written)
+    GridGeom geo;          // nzl = nz: one GPU, z wraps by index
+    double g[4];           // g[s] = dt*a_{s+1,s}: Y_{s+1} = u (+) g[s] (x) k_s (1-based stages)
+    double beta[4];        // beta[j] = dt*b_{j+1}
+    double d1, d2, F, FK, inv_h2;
+    int zchunk;            // output planes per CTA
+};
+bool fused_scheme(int scheme);  // RK4 and explicit midpoint
+int fused_halo(int scheme);     // L = stages = margin cells
+cudaError_t encode_fused_map(CUtensorMap* map, const double* base, const GridGeom& g, int nplanes, int L);
+cudaError_t launch_gs_fused(int scheme, const GsFusedArgs& a, cudaStream_t st);
+
+// ---------------------------------------------------------------------------------------
 // K2 / K4: algebra.
 struct LincombArgs {
     double* out;

@@ -160,6 +160,7 @@ struct rk_state_s {
     int64_t check_finite = 0;    // RK_OPT_CHECK_FINITE: check u every n steps (0: never)
     int64_t since_check = 0;     // steps since the last finiteness check
     int64_t coop_max_cells = 1 << 18;  // RK_OPT_COOP_MAX_CELLS: persistent-step path up to here
+    bool fused = false;          // RK_OPT_FUSED_STEP: K6 whole-step launches (RK4, midpoint)
     // stats
     rk_stats stats{};
     std::vector<TimedPair> pending;
@@ -857,9 +858,70 @@ static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
     return RK_OK;
 }
 
+// K6 (rk_fused.cu): a whole fixed step of RK4 / explicit midpoint in one launch, temporal
+// blocking across the stages (one GPU, no halo path)
+static bool fused_path(rk_state st, int scheme) {
+    return st->fused && st->grid && st->ncomp == 2 && st->rhs == RHS_GRAY_SCOTT && st->ctx->world == 1 &&
+           !st->loopback && !st->p2p && fused_scheme(scheme);
+}
+
+static int pick_fused_zchunk(rk_state st) {
+    const int nz = (int)st->local;
+    int zc = 64;  // measured at 512^3: 8 / 16 / 32 / 64 / 128 -> 7.10 / 5.74 / 5.08 / 4.79 / ~4.8 ms (RK4)
+    if (const char* e = getenv("RKB_FZ")) {  // developer tuning knob
+        const int v = atoi(e);
+        if (v > 0) zc = v;
+    }
+    const int64_t tiles = ((st->nx + 31) / 32) * ((st->ny + 15) / 16);
+    while (zc > 2 && tiles * ((nz + zc - 1) / zc) < 2 * st->ctx->num_sms) zc /= 2;
+    return std::max(1, std::min(zc, nz));
+}
+
+static rk_status fused_steps(rk_state st, int scheme, double dt, int64_t n) {
+    rk_ctx ctx = st->ctx;
+    const Coeffs C = coeffs_of(scheme);
+    GsFusedArgs a{};
+    a.geo = st->geo;
+    for (int s = 1; s < C.s; ++s) a.g[s] = dt * C.a[s][s - 1];
+    for (int j = 0; j < C.s; ++j) a.beta[j] = dt * C.b[j];
+    a.d1 = st->d1;
+    a.d2 = st->d2;
+    a.F = st->F;
+    a.FK = st->F + st->K;
+    a.inv_h2 = 1.0 / (st->h * st->h);
+    a.zchunk = pick_fused_zchunk(st);
+    const int64_t cells = st->local * st->nx * st->ny;
+    for (int64_t i = 0; i < n; ++i) {
+        CK_CTX(ctx, encode_fused_map(&a.tm_u, st->u, st->geo, (int)st->local, fused_halo(scheme)));
+        a.u = st->u;
+        a.out = st->u_new;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (st->timing) {
+            e0 = pool_event(st);
+            e1 = pool_event(st);
+            CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+        }
+        CK_CTX(ctx, launch_gs_fused(scheme, a, ctx->stream));
+        if (st->timing) {
+            CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+            st->pending.push_back({e0, e1, 0});
+            if (st->pending.size() > 4096) TRY(resolve_timing(st));
+        }
+        swap_u(st);
+        st->stats.kernel_launches += 1;
+        st->stats.stage_launches += 1;
+        st->stats.rhs_evals += C.s;
+        st->stats.stage_bytes += 2 * cells * 2 * (int64_t)sizeof(double);  // u in, u_new out
+        st->stats.steps += 1;
+    }
+    st->k1_valid = false;
+    return RK_OK;
+}
+
 // one fixed Runge–Kutta step, u <- u_new (does not touch the Adams–Bashforth history)
 static rk_status rk_fixed_step(rk_state st, int scheme, double dt) {
     if (coop_path(st, scheme)) return coop_steps(st, scheme, dt, 1);
+    if (fused_path(st, scheme)) return fused_steps(st, scheme, dt, 1);
     if (st->grid) {
         auto plan = build_plan(scheme, 0, dt);
         TRY(run_grid_plan(st, plan, dt, 0.0, 0.0));
@@ -1595,6 +1657,7 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
         if (value < 0) return fail(RK_ERR_ARG, "cell limit must be >= 0");
         st->coop_max_cells = value;
         break;
+    case RK_OPT_FUSED_STEP: st->fused = value != 0; break;
     case RK_OPT_HALO_P2P:
         if (value != 0 && !st->grid) return fail(RK_ERR_ARG, "RK_OPT_HALO_P2P needs a grid state");
         st->p2p = value != 0;
