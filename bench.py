@@ -166,6 +166,44 @@ def oracle_all_cores(nz_each=4, tries=4):
     return cells / (t1 - t0), workers, t1 - t0
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_small_configs():
+    """the oracle on BASELINE configs[0..2] in full, one host core (the GPU side of
+    the same runs is extra.small_configs / extra.exp512)."""
+    import oracle
+    import rk_inputs
+    out = {}
+    n1 = 100000  # configs[0]: du/dt = -u, RK4, t in [0, 1], dt = 0.1
+    t = time.perf_counter()
+    _, steps = oracle.integrate_const(oracle.exp_problem(n1, -1.0), oracle.RK4, rk_inputs.exp_decay_u0(n1),
+                                      0.0, 1.0, 0.1)
+    sec = time.perf_counter() - t
+    out["config0_exp_rk4"] = {"value": n1 * steps / sec, "unit": "element-updates/s", "seconds": sec, "steps": steps}
+    n2 = 1000000  # configs[1]: logistic, DOPRI5 adaptive tol 1e-8 on [-5, 5]
+    t = time.perf_counter()
+    _, acc, rej, _ = oracle.integrate_adaptive(oracle.logistic_problem(n2), oracle.DOPRI5, rk_inputs.logistic_u0(n2),
+                                               -5.0, 5.0, 0.1, 1e-8, 1e-8)
+    sec = time.perf_counter() - t
+    out["config1_logistic_dopri5"] = {"value": n2 * (acc + rej) / sec, "unit": "element-tries/s", "seconds": sec,
+                                      "accepted": acc, "rejected": rej}
+    n3 = 64  # configs[2]: Gray-Scott 64^3, RK4 dt = 1, t in [0, 20]
+    u0 = rk_inputs.gray_scott_ic(n3, n3, n3, seed=42)
+    t = time.perf_counter()
+    _, steps = oracle.integrate_const(oracle.gray_scott_problem(n3, n3, n3), oracle.RK4, u0, 0.0, 20.0, 1.0)
+    sec = time.perf_counter() - t
+    out["config2_gs64_rk4"] = {"value": n3 ** 3 * steps / sec, "unit": "cell-updates/s", "seconds": sec, "steps": steps}
+    return out
+
+
 def cpu_baseline(nz_sample=128):
     secs, cells = oracle_try_seconds(nz_sample)
     single = cells / secs
@@ -175,8 +213,12 @@ def cpu_baseline(nz_sample=128):
         return {"value": single, "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
                 "sample": f"one DOPRI5 try on a 512x512x{nz_sample} slab, single thread, {secs:.1f} s "
                           f"(all-core run failed: {e})"}
+    try:
+        small = oracle_small_configs()
+    except Exception as e:
+        small = {"error": str(e)}
     return {"value": v, "unit": "cell-updates/s", "cores": workers, "kind": "oracle",
-            "single_core_value": single,
+            "single_core_value": single, "cpu_model": cpu_model(), "small_configs_single_core": small,
             "sample": f"all host cores: {workers} processes of the single-threaded C oracle (-O2 "
                       f"-ffp-contract=off), each 4 DOPRI5 error-controlled tries (7 RHS evals, "
                       f"error ratio, max norm, controller) on its own 512x512x4 periodic slab, "
@@ -226,7 +268,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
-    ap.add_argument("--legs", default="adaptive,rk4,halo,strong,strong_emul,rk4_native,exp512,small,e2e,cpu",
+    ap.add_argument("--legs", default="adaptive,rk4,repeats,halo,strong,strong_emul,rk4_native,exp512,small,e2e,cpu",
                     help="comma list of legs (profiling runs use e.g. --legs rk4)")
     ap.add_argument("--no-extra", action="store_true", help="same as --legs adaptive")
     ap.add_argument("--overlap", type=int, default=1, help="halo exchange overlapped (N > 1)")
@@ -692,6 +734,22 @@ def main():
     extra = {}
     if "rk4" in legs:
         extra["rk4"] = run_leg(rk4_leg, args.overlap)
+    if "repeats" in legs:
+        # each config 3 times, mean and min (the headline line is the first run)
+        def rep(fn, *a):
+            try:
+                return [fn(*a)["ms_per_step"] for _ in range(2)]
+            except Exception:  # noqa: BLE001
+                return []
+        rp = {}
+        if "adaptive" in legs and line:
+            ms = [line["ms_per_step"]] + rep(adaptive_leg)
+            rp["dopri5_adaptive_ms_per_step"] = {"runs": ms, "mean": sum(ms) / len(ms), "min": min(ms)}
+        if "rk4" in legs and "ms_per_step" in extra.get("rk4", {}):
+            ms = [extra["rk4"]["ms_per_step"]] + rep(rk4_leg, args.overlap)
+            rp["rk4_ms_per_step"] = {"runs": ms, "mean": sum(ms) / len(ms), "min": min(ms)}
+        extra["repeats"] = rp
+    if "rk4" in legs:
         if world > 1:
             extra["rk4_overlap_off"] = run_leg(rk4_leg, 0)
     if "halo" in legs:

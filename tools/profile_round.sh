@@ -4,9 +4,9 @@
 #   DOPRI5 try and one RK4 step, dram bytes of one step of every other scheme leg.
 #   Summaries are written on the box (tools/make_profiles.py) into gpurun_out/profiles_TAG/;
 #   the bulky .ncu-rep files are deleted there except the DOPRI5 one (gpurun returns <= 64 MiB).
-TAG=${1:-r1_v5}
+TAG=${1:-r1_v6}
 O=gpurun_out
-LEGS=adaptive,rk4,rk4_native,exp512,small,e2e,cpu,euler,midpoint,cash_karp54,dopri5,rkf78,ab1,ab2,ab4,ab8,abm1,abm2,abm4,abm8
+LEGS=adaptive,rk4,repeats,rk4_native,rk4_k6,midpoint_k6,exp512,small,e2e,cpu,euler,midpoint,cash_karp54,dopri5,rkf78,ab1,ab2,ab4,ab8,abm1,abm2,abm4,abm8
 timeout 1200 python bench.py --legs $LEGS > $O/${TAG}_bench.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/${TAG}_launches.csv python bench.py --legs adaptive --steps 2 --warmup 3 > $O/${TAG}_launches.log 2>&1
