@@ -361,7 +361,13 @@ __global__ void __launch_bounds__(FNT, 1) gs_fused_kernel(const __grid_constant_
                 }
             }
         }
-        __syncthreads();
+        // Barriers: the patched margin must be visible (edge CTAs only: elsewhere every thread
+        // waited on the plane itself); one between consecutive stages (stage s+1 reads the Y
+        // plane stage s just wrote).  The u plane t-NEED+1 is last read by stage L-1 (its Y_L),
+        // so it is refilled right after the barrier before stage L.  A window slot that stage s
+        // rewrites in the next iteration was last read by stage s+1 of this one, at least one
+        // barrier earlier -- except for L = 2 (stage 1 rewrites what stage 2 just read).
+        if (edge) __syncthreads();
         {
             const double* U = uslot(t);
 #pragma unroll
@@ -372,27 +378,32 @@ __global__ void __launch_bounds__(FNT, 1) gs_fused_kernel(const __grid_constant_
             uq[0][0] = U[o_ub];
             uq[0][1] = U[UBOX + o_ub];
         }
+        auto refill = [&]() FINLINE {
+            if (tid == 0) {
+                const int nxt = t - NEED + 1 + R;
+                if (t >= NEED - 1 && nxt < nU) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the patches
+                    issue(nxt);
+                }
+            }
+        };
         stage(std::integral_constant<int, 1>{}, qc, t);
         if constexpr (L >= 2) {
             __syncthreads();
+            if constexpr (L == 2) refill();
             stage(std::integral_constant<int, 2>{}, qc, t);
         }
         if constexpr (L >= 3) {
             __syncthreads();
+            if constexpr (L == 3) refill();
             stage(std::integral_constant<int, 3>{}, qc, t);
         }
         if constexpr (L >= 4) {
             __syncthreads();
+            refill();
             stage(std::integral_constant<int, 4>{}, qc, t);
         }
-        __syncthreads();  // u plane index t-NEED+1 is free
-        if (tid == 0) {
-            const int nxt = t - NEED + 1 + R;
-            if (t >= NEED - 1 && nxt < nU) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the patches
-                issue(nxt);
-            }
-        }
+        if constexpr (L <= 2) __syncthreads();
     };
 
     for (int t0 = 0; t0 < nU; t0 += L) {
