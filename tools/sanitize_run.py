@@ -1,5 +1,5 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
-every scheme on a ragged 16x12x10 grid, the loopback multi-GPU halo path, adaptive tries,
+every scheme on a ragged 40x12x10 grid (K5) and 40x21x13 (K3, K6), the loopback multi-GPU halo path, adaptive tries,
 Adams-Bashforth and the algebra ops.  Run:  compute-sanitizer --tool racecheck python tools/sanitize_run.py
 """
 import os
@@ -23,6 +23,18 @@ for loop in (0, 1):
         st.do_step(s, 0.0, 1.0)
     for s in ("cash_karp54", "dopri5", "rkf78"):
         st.try_step(s, 0.0, 0.5, 1e-6, 1e-6)
+    st.get()
+    st.close()
+# the stage-by-stage kernels on a small grid (K5 off) and K6 (whole-step fusion, several z chunks)
+os.environ["RKB_FZ"] = "3"
+for fused in (0, 1):
+    st = ctx.grid(nx, ny + 9, nz + 3, 2)
+    st.set_rhs_gray_scott()
+    st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
+    st.set_option(rk.OPT_FUSED_STEP, fused)
+    st.set(rk_inputs.gray_scott_ic(nx, ny + 9, nz + 3, seed=4))
+    for s in ("midpoint", "rk4", "dopri5"):
+        st.do_step(s, 0.0, 1.0)
     st.get()
     st.close()
 v = ctx.vector(1001)
