@@ -328,11 +328,15 @@ def main():
         return {"bytes_per_cell": bytes_per_cell, "effective_gbs": eff, "frac": eff / peak, "target_frac": 0.70}
 
     def halo_of(s):
-        if world == 1 or not s["halo_exchanges"]:
+        # halo time (comm-stream CUDA events around each exchange) and its GB/s, reported
+        # separately; one GPU: the loopback self-exchange (a device copy)
+        if not s["halo_exchanges"]:
             return None
+        gbs = (s["halo_bytes"] / (s["halo_ms"] / 1e3) / 1e9) if s["halo_ms"] else None
         return {"exchanges": s["halo_exchanges"], "ms_per_exchange": s["halo_ms"] / s["halo_exchanges"],
                 "bytes_per_exchange": s["halo_bytes"] / s["halo_exchanges"],
-                "nvlink_gbs": (s["halo_bytes"] / (s["halo_ms"] / 1e3) / 1e9) if s["halo_ms"] else None}
+                "transport": "nccl over nvlink" if world > 1 else "loopback (device copy, one GPU)",
+                ("nvlink_gbs" if world > 1 else "gbs"): gbs}
 
     # ---- headline: DOPRI5 adaptive, one accepted step per "step" ---------------------
     state = {"t": 0.0, "dt": 1.0}
