@@ -618,6 +618,17 @@ def test_device_loop_matches_host_loop(ctx, scheme, tol, rhs):
     assert sd["last_dt"] == sh["last_dt"]
 
 
+@pytest.mark.parametrize("n", [1, 2, 7, 262145, 3000001])
+def test_device_loop_sizes(ctx, n):
+    """The device loop from 1 element to more elements than the cooperative grid has threads
+    (grid-stride tries, odd tails): equal to the host loop bit for bit."""
+    u0 = rk_inputs.logistic_u0(n) if n > 1 else np.array([0.25])
+    gd, ad, rd, sd = _adaptive_vec(ctx, "logistic", n, u0, "dopri5", -5.0, 5.0, 0.5, 1e-7, True)
+    gh, ah, rh, sh = _adaptive_vec(ctx, "logistic", n, u0, "dopri5", -5.0, 5.0, 0.5, 1e-7, False)
+    assert (ad, rd) == (ah, rh)
+    assert bitwise(gd, gh)
+
+
 def test_device_loop_errors(ctx):
     import paper_2309_05331_b200 as rk
     n = 1000
