@@ -394,6 +394,7 @@ def main():
                        "parallelism": f"z-slab x{world} (NCCL send/recv halos + allreduce max)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
+                         "frac_of_datasheet_8000": (achieved / 8000.0) if achieved else None,
                          "traffic": traffic.get("dopri5_adaptive", {}).get("bytes_per_launch"),
                          "kernel": "gs_stage_kernel (K3: fused stage value + 7-pt stencil + "
                                    "reaction + epilogue), all stage launches of the timed tries",
