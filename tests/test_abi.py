@@ -110,6 +110,21 @@ def test_no_gpu_is_a_loud_error(rk):
     assert e.value.status == "RK_ERR_CUDA"
 
 
+def test_only_test_infrastructure_touches_oracle():
+    """oracle/ is test infrastructure: outside tests/, only __graft_entry__.py (smoke) and
+    bench.py (cpu_baseline / --impl reference) may import it."""
+    allowed = {"__graft_entry__.py", "bench.py"}
+    for dirpath, dirs, files in os.walk(ROOT):
+        rel = os.path.relpath(dirpath, ROOT)
+        if rel.split(os.sep)[0] in ("tests", "oracle", ".git", "build", "gpurun_out", "baseline"):
+            dirs[:] = []
+            continue
+        for f in files:
+            if f.endswith(".py") and f not in allowed:
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, os.path.join(rel, f)
+
+
 def test_product_never_imports_oracle():
     """The product package shares no code with oracle/ (DESIGN.md §Boundary)."""
     pkg = os.path.join(ROOT, "paper_2309_05331_b200")
