@@ -14,9 +14,13 @@
 //     partial final sums W = u (+) beta_1 k_1 (+) ... in registers (one own cell per thread);
 //   * the last stage stores u_new (with its periodic ring copies).
 // HBM traffic per step is u once (+ the margins re-read by neighbouring CTAs through L2) and
-// u_new once: 32 B/cell instead of the stage-by-stage 208 (RK4) / 80 (midpoint).  The
-// step becomes bound by the FP64 pipe and shared memory; the margin re-evaluations cost
-// (38*22 + 36*20 + 34*18 + 32*16) / (4*32*16) = 1.31x the RK4 stencil work.
+// u_new once: 32 B/cell instead of the stage-by-stage 208 (RK4) / 80 (midpoint), for
+// (38*22 + 36*20 + 34*18 + 32*16) / (4*32*16) = 1.31x the RK4 stencil work (margins).
+// Measured on the B200 this is SLOWER than the stage-by-stage kernels (RK4 4.65-4.69 vs 4.42
+// ms at 512^3): 196 KB of shared memory allow one 16-warp CTA per SM and every stage phase
+// ends in a CTA barrier, so the kernel is latency-bound at ~36 % FP64-pipe use (DESIGN.md §7,
+// profiles/r1_k6_fused_rk4_ncu.txt).  It is therefore opt-in (RK_OPT_FUSED_STEP), an ablation
+// that locates the stage-by-stage roofline against on-chip fusion on this part.
 //
 // Arithmetic is the stage kernel's (K3, rk_stencil.cu) expression for expression (DESIGN.md
 // R-17): the Laplacian in difference form (x, then y, then z), the same reaction trees,
