@@ -42,6 +42,11 @@ namespace rkb {
 
 namespace {
 
+#ifndef RKB_COOP_NT
+#define RKB_COOP_NT 1024
+#endif
+constexpr int kCoopThreads = RKB_COOP_NT;  // threads per CTA of the persistent kernels
+
 struct CoopMask {
     bool a[13][13];
     bool b[13];
@@ -212,7 +217,7 @@ __device__ __forceinline__ StageEnv env_of(const GsCoopArgs& a) {
 
 // ---- fixed steps -------------------------------------------------------------------------
 template <int S, int MINB>
-__global__ void __launch_bounds__(256, MINB) gs_coop_kernel(const __grid_constant__ GsCoopArgs a) {
+__global__ void __launch_bounds__(kCoopThreads, MINB) gs_coop_kernel(const __grid_constant__ GsCoopArgs a) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     const StageEnv v = env_of(a);
     double* u = a.buf[0];
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(256, MINB) gs_coop_kernel(const __grid_constan
 
 // ---- the whole integrate_adaptive --------------------------------------------------------
 template <int S, int MODE, int MINB>
-__global__ void __launch_bounds__(256, MINB) gs_coop_adaptive_kernel(const __grid_constant__ GsCoopLoopArgs a) {
+__global__ void __launch_bounds__(kCoopThreads, MINB) gs_coop_adaptive_kernel(const __grid_constant__ GsCoopLoopArgs a) {
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
     __shared__ CoopCoef cf;   // this try's dt-scaled coefficients
     __shared__ double s_dtn;  // controller result, computed once per CTA
@@ -316,22 +321,24 @@ done:
 template <typename K>
 cudaError_t coop_launch(K kernel, void* arg, const GridGeom& g, cudaStream_t st, int device) {
     int per_sm = 0, sms = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kCoopThreads, 0);
     if (e != cudaSuccess) return e;
     e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
     const int64_t ncell = (int64_t)g.nzl * g.ny * g.nx;
-    int64_t blocks = (ncell + 255) / 256;
+    int64_t blocks = (ncell + kCoopThreads - 1) / kCoopThreads;
     const int64_t cap = (int64_t)sms * per_sm;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     void* args[] = {arg};
-    return cudaLaunchCooperativeKernel((void*)kernel, dim3((unsigned)blocks), dim3(256), args, 0, st);
+    return cudaLaunchCooperativeKernel((void*)kernel, dim3((unsigned)blocks), dim3(kCoopThreads), args, 0, st);
 }
 
-// 4 CTAs of 256 threads per SM (64 registers): measured best at 16^3..64^3 against 6 and 8
-// (more CTAs make every grid-wide barrier slower; tools/prof_small.py)
-constexpr int kCoopMinBlocks = 4;
+// One CTA of 1024 threads per SM (64 registers): the grid-wide barrier then counts 148
+// arrivals instead of 592.  configs[2] (64^3 RK4, 20 steps, one launch): 31.9 us/step with
+// 4 x 256 threads per SM, 31.4 with 2 x 512, 27.6 with 1 x 1024 (measured on the B200; 6 and
+// 8 CTAs of 256 were slower still, tools/prof_small.py).
+constexpr int kCoopMinBlocks = 1024 / kCoopThreads;
 
 template <int S>
 cudaError_t launch_coop_s(const GsCoopArgs& a, cudaStream_t st, int device) {
