@@ -268,7 +268,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
-    ap.add_argument("--legs", default="adaptive,rk4,repeats,halo,strong,strong_emul,rk4_native,rk4_k6,exp512,small,e2e,cpu",
+    ap.add_argument("--legs", default="adaptive,rk4,repeats,halo,exposed,strong,strong_emul,rk4_native,rk4_k6,exp512,small,e2e,cpu",
                     help="comma list of legs (profiling runs use e.g. --legs rk4)")
     ap.add_argument("--no-extra", action="store_true", help="same as --legs adaptive")
     ap.add_argument("--overlap", type=int, default=1, help="halo exchange overlapped (N > 1)")
@@ -728,6 +728,37 @@ def main():
                 "rk4": {"value": n ** 3 * args.steps / (ms_r / 1e3), "unit": "cell-updates/s",
                         "ms_per_step": ms_r / args.steps}}
 
+    def exposed_halo_leg():
+        # exposed halo = T(overlap on) - T(no-comm run of the same slab).  N > 1:
+        # every rank also runs its own slab as a one-GPU periodic problem (z wraps locally, no
+        # exchange) on a private context; N = 1: the loopback halo path against the plain one.
+        def rk4_ms(state):
+            state.set_option(rk.OPT_HALO_OVERLAP, 1)
+            for _ in range(args.warmup):
+                state.do_step("rk4", 0.0, 1.0)
+            barrier()
+            ev0.record(stream)
+            for k in range(args.steps):
+                state.do_step("rk4", float(k), 1.0)
+            ev1.record(stream)
+            barrier()
+            return max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+        st.set(u0_dev)
+        if world == 1:
+            st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+        t_on = rk4_ms(st)
+        st.set_option(rk.OPT_HALO_LOOPBACK, 0)
+        c1 = rk.Context(0, 1, local, stream)
+        solo = c1.grid(n, n, int(st.local), 2)
+        solo.set_rhs_gray_scott(h=H)
+        solo.set(u0_dev)
+        t_off = rk4_ms(solo)
+        solo.close()
+        c1.close()
+        return {"scheme": "rk4", "ms_per_step_halo_overlapped": t_on, "ms_per_step_no_comm": t_off,
+                "exposed_halo_ms_per_step": t_on - t_off, "exposed_frac": (t_on - t_off) / t_off,
+                "halo_path": "nccl send/recv" if world > 1 else "loopback (one GPU)"}
+
     def run_leg(fn, *a):
         # an extra leg that fails reports its error instead of losing the headline line
         try:
@@ -765,6 +796,8 @@ def main():
             extra["rk4_loopback_p2p"] = run_leg(rk4_leg, args.overlap, "rk4", 1, 1)
         elif "p2p" in legs:  # opt-in at N > 1: needs CUDA IPC between the rank processes
             extra["rk4_p2p"] = run_leg(rk4_leg, args.overlap, "rk4", 1, 0)
+    if "exposed" in legs:
+        extra["exposed_halo"] = run_leg(exposed_halo_leg)
     if "strong_emul" in legs and world == 1:
         extra["strong_emul"] = run_leg(strong_emul_leg)
     if "strong" in legs and world > 1:
