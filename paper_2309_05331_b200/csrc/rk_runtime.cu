@@ -409,17 +409,21 @@ static int pick_zchunk(rk_state st, const StagePlan& p, int range) {
         const int v = atoi(e);
         if (v > 0) return std::min(v, range);
     }
-    // classes: 0 Y-direct (no slot enters Y), 1 other two-row stages, 2 AHEAD / EPART, 3 the rest
+    // classes: 0 Y-direct (no slot enters Y), 1 other two-row stages, 2 AHEAD / EPART, 3 the rest,
+    // 4 Adams–Bashforth with one or two history slots (Y-direct too; measured at 512^3: AB2
+    // 1.59 -> 1.48 ms, AB3 1.72 -> 1.68 ms at 4 planes instead of 8, while AB4 is flat and AB8
+    // loses, gpurun_out zab2*)
     bool yd = true;
     for (int s = 0; s < p.sp.nslots; ++s) yd = yd && !p.sp.gnz[s];
-    const int cls = yd ? 0 : (stage_rows(p.sp) == 2 ? 1 : (p.sp.epi == EPI_FINAL_EPART || p.sp.epi == EPI_AHEAD ? 2 : 3));
-    static int tab[4] = {0, 0, 0, 0};
+    const int cls = yd ? (p.sp.epi == EPI_AB && p.sp.nslots > 0 && p.sp.nslots <= 2 ? 4 : 0)
+                       : (stage_rows(p.sp) == 2 ? 1 : (p.sp.epi == EPI_FINAL_EPART || p.sp.epi == EPI_AHEAD ? 2 : 3));
+    static int tab[5] = {0, 0, 0, 0, 0};
     static bool parsed = false;
-    if (!parsed) {  // developer tuning knob RKB_ZC="yd,light,epart,heavy"
-        const int def[4] = {8, 16, 16, 48};
-        for (int c = 0; c < 4; ++c) tab[c] = def[c];
+    if (!parsed) {  // developer tuning knob RKB_ZC="yd,light,epart,heavy,ab"
+        const int def[5] = {8, 16, 16, 48, 4};
+        for (int c = 0; c < 5; ++c) tab[c] = def[c];
         if (const char* e = getenv("RKB_ZC")) {
-            int v[4], n = sscanf(e, "%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3]);
+            int v[5], n = sscanf(e, "%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4]);
             for (int c = 0; c < n; ++c)
                 if (v[c] > 0) tab[c] = v[c];
         }
