@@ -1008,3 +1008,22 @@ def test_max_size_1024_cubed_rk4(ctx):
         assert bitwise(g[z, :, y, x], out[r, :, r, r]), (z, y, x)
     del g, u0
     gc.collect()
+
+
+@pytest.mark.parametrize("coop", [True, False], ids=["k5", "k3"])
+def test_gs32_20000_steps_bitwise_golden(ctx, coop):
+    """20000 RK4 steps of Gray–Scott 32^3 (S:L515 run length): the final state's SHA-256 equals
+    the oracle's (tests/golden/gs32_rk4_20000.json, written by make_gs32_longrun.py from oracle/
+    only).  C1 decays into fp64 denormals on the way, so this pins FTZ-free arithmetic."""
+    import hashlib
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "gs32_rk4_20000.json")))
+    n = 32
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    st = gs_state(ctx, n, n, n, u0, coop=coop)
+    steps = st.integrate_const("rk4", 0.0, float(gold["steps"]), 1.0)
+    assert steps == gold["steps"]
+    g = np.ascontiguousarray(st.get(), dtype="<f8")
+    assert float(g[:, 1].min()) == gold["c1_min"] and float(g[:, 0].max()) == gold["c0_max"]
+    assert hashlib.sha256(g.tobytes()).hexdigest() == gold["sha256_final"]
