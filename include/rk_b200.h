@@ -133,12 +133,18 @@ typedef enum {
                                 persistent cooperative launch (all stages of all steps, grid-
                                 wide barrier between stages): same results bit for
                                 bit, no per-stage launch cost.  Default 2^18 (64^3); 0 = off. */
-    RK_OPT_FUSED_STEP = 11     /* 1: fixed RK4 / explicit-midpoint steps of a Gray–Scott grid
+    RK_OPT_FUSED_STEP = 11,    /* 1: fixed RK4 / explicit-midpoint steps of a Gray–Scott grid
                                 (one GPU, no halo path, above RK_OPT_COOP_MAX_CELLS) run as ONE
                                 launch per step that keeps every stage value on chip (temporal
                                 blocking across the stages, K6): u read and
                                 u_new written once per step (32 B/cell instead of 208 / 80),
                                 same results bit for bit.  0: stage-by-stage launches.       */
+    RK_OPT_COMM_TIMEOUT_MS = 12 /* multi-GPU failure detection, applies to the state's context:
+                                host waits on a stream with NCCL work poll the stream and
+                                ncclCommGetAsyncError; an asynchronous NCCL error, or a wait
+                                longer than this many ms (> 0), aborts the communicator and
+                                returns RK_ERR_NCCL (context poisoned).  0 (default): no
+                                deadline (asynchronous errors are still detected).  >= 0.   */
 } rk_option;
 
 /* Counters since creation or the last rk_reset_stats. */

@@ -8,8 +8,11 @@
 // P:L198) and the host step-size controller (R-12).
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cfloat>
 #include <cmath>
 #include <cstdarg>
@@ -48,6 +51,7 @@ struct rk_ctx_s {
     bool own_stream = false;
     cudaStream_t capture = nullptr;  // private stream for CUDA-graph capture (RK_OPT_USE_GRAPH)
     ncclComm_t nccl = nullptr;
+    int64_t comm_timeout_ms = 0;  // RK_OPT_COMM_TIMEOUT_MS: abort a collective wait after this
     int num_sms = 148;
     rk_status poisoned = RK_OK;
     unsigned long long* d_scratch = nullptr;  // 8 B reduction word (norm_inf)
@@ -80,6 +84,48 @@ struct rk_ctx_s {
         rk_status s_ = (call);             \
         if (s_ != RK_OK) return s_;        \
     } while (0)
+
+// NVTX ranges (SURVEY §5 tracing): a try, a stage, a halo exchange, a whole-step launch and the
+// integrate drivers show up by name in Nsight Systems / ncu --nvtx; header-only NVTX3, inert
+// when no tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// Wait for stream s.  With a NCCL communicator the host polls instead of blocking, so an
+// asynchronous NCCL error (a peer died, a link failed) or the RK_OPT_COMM_TIMEOUT_MS deadline
+// aborts the communicator and returns RK_ERR_NCCL (the context is poisoned) instead of hanging
+// in a collective forever (SURVEY §5 failure detection).
+static rk_status ctx_wait(rk_ctx ctx, cudaStream_t s) {
+    if (!ctx->nccl) {
+        CK_CTX(ctx, cudaStreamSynchronize(s));
+        return RK_OK;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return RK_OK;
+        if (q != cudaErrorNotReady) CK_CTX(ctx, q);
+        ncclResult_t ar = ncclSuccess;
+        NK_CTX(ctx, ncclCommGetAsyncError(ctx->nccl, &ar));
+        const bool late = ctx->comm_timeout_ms > 0 &&
+                          std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(ctx->comm_timeout_ms);
+        if ((ar != ncclSuccess && ar != ncclInProgress) || late) {
+            ncclCommAbort(ctx->nccl);
+            ctx->nccl = nullptr;
+            ctx->poisoned = RK_ERR_NCCL;
+            if (late)
+                return fail(RK_ERR_NCCL, "collective wait exceeded %lld ms on rank %d: communicator aborted",
+                            (long long)ctx->comm_timeout_ms, ctx->rank);
+            return fail(RK_ERR_NCCL, "asynchronous NCCL error %s on rank %d: communicator aborted",
+                        ncclGetErrorString(ar), ctx->rank);
+        }
+        if (spin >= 256) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
 
 struct DeviceGuard {
     int prev = -1;
@@ -227,9 +273,9 @@ static cudaEvent_t pool_event(rk_state st) {
 static rk_status resolve_timing(rk_state st) {
     if (st->pending.empty()) return RK_OK;
     rk_ctx ctx = st->ctx;
-    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
-    if (ctx->comm) CK_CTX(ctx, cudaStreamSynchronize(ctx->comm));
-    if (ctx->bnd) CK_CTX(ctx, cudaStreamSynchronize(ctx->bnd));
+    TRY(ctx_wait(ctx, ctx->stream));
+    if (ctx->comm) TRY(ctx_wait(ctx, ctx->comm));
+    if (ctx->bnd) TRY(ctx_wait(ctx, ctx->bnd));
     for (auto& p : st->pending) {
         float ms = 0.f;
         CK_CTX(ctx, cudaEventElapsedTime(&ms, p.a, p.b));
@@ -466,6 +512,7 @@ static rk_status launch_stage_timed(rk_state st, const StagePlan& p, GsStageArgs
 
 // exchange the planes packed on stream `src` (comm stream; ev_halo marks completion)
 static rk_status halo_exchange(rk_state st, cudaStream_t src) {
+    NvtxRange nv("rk halo exchange");
     rk_ctx ctx = st->ctx;
     const int64_t pv = plane_values(st);
     CK_CTX(ctx, cudaEventRecord(st->ev_pack, src));
@@ -541,7 +588,7 @@ static rk_status ensure_p2p(rk_state st) {
         NK_CTX(ctx, ncclAllGather(d, d + hb, hb, ncclUint8, ctx->nccl, ctx->stream));
         std::vector<unsigned char> all(hb * ctx->world);
         CK_CTX(ctx, cudaMemcpyAsync(all.data(), d + hb, all.size(), cudaMemcpyDeviceToHost, ctx->stream));
-        CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+        TRY(ctx_wait(ctx, ctx->stream));
         cudaFree(d);
         int nmap = 0;
         for (int dir = 0; dir < 2; ++dir) {
@@ -626,6 +673,7 @@ static rk_status run_gs_stage_p2p(rk_state st, const StagePlan& p, GsStageArgs& 
 }
 
 static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
+    NvtxRange nv("rk stage");
     rk_ctx ctx = st->ctx;
     TRY(ensure_halo(st));  // every entry path (RK plans, Adams steps, eval_rhs) lands here
     GsStageArgs a = stage_args(st, p, dt, atol, rtol);
@@ -771,7 +819,7 @@ static rk_status global_norm_inf(rk_state st, double* out) {
     if (ctx->world > 1)
         NK_CTX(ctx, ncclAllReduce(ctx->d_scratch, ctx->d_scratch, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
     CK_CTX(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    TRY(ctx_wait(ctx, ctx->stream));
     std::memcpy(out, ctx->h_scratch, 8);
     return RK_OK;
 }
@@ -808,6 +856,7 @@ static bool coop_path(rk_state st, int scheme) {
 }
 
 static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
+    NvtxRange nv("rk persistent steps (K5)");
     rk_ctx ctx = st->ctx;
     const int last = coop_last_stage(scheme);
     TRY(ensure_k(st, std::max(last, 1)));
@@ -882,6 +931,7 @@ static int pick_fused_zchunk(rk_state st) {
 }
 
 static rk_status fused_steps(rk_state st, int scheme, double dt, int64_t n) {
+    NvtxRange nv("rk fused steps (K6)");
     rk_ctx ctx = st->ctx;
     const Coeffs C = coeffs_of(scheme);
     GsFusedArgs a{};
@@ -1079,6 +1129,7 @@ static rk_status fixed_step(rk_state st, int scheme, double dt) {
 // one try: E (global), accept -> swap
 static rk_status one_try(rk_state st, int scheme, double t, double dt, double atol, double rtol,
                          int* accepted, double* E_out, double* dt_next) {
+    NvtxRange nv("rk try");
     rk_ctx ctx = st->ctx;
     const Coeffs C = coeffs_of(scheme);
     ab_invalidate(st);
@@ -1094,7 +1145,7 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
         NK_CTX(ctx, ncclAllReduce(st->d_err, st->d_err, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
     CK_CTX(ctx, cudaMemcpyAsync(st->h_err, st->d_err, sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, ctx->stream));
-    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    TRY(ctx_wait(ctx, ctx->stream));
     double E;
     std::memcpy(&E, st->h_err, sizeof E);
     st->stats.tries += 1;
@@ -1240,7 +1291,7 @@ static rk_status device_adaptive_loop(rk_state st, int scheme, double t0, double
     }
     PwLoopResult r{};
     CK_CTX(ctx, cudaMemcpyAsync(&r, a.res, sizeof r, cudaMemcpyDeviceToHost, ctx->stream));
-    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    TRY(ctx_wait(ctx, ctx->stream));
     if (r.which) swap_u(st);
     const int64_t tries = r.accepted + r.rejected;
     st->stats.kernel_launches += 1;
@@ -1421,7 +1472,7 @@ static rk_status state_common(rk_ctx ctx, rk_state st) {
     TRY(alloc_array(st, &st->u_new, &st->tm_unew));
     CK_CTX(ctx, cudaMalloc((void**)&st->d_err, sizeof(unsigned long long)));
     CK_CTX(ctx, cudaMallocHost((void**)&st->h_err, sizeof(unsigned long long)));
-    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    TRY(ctx_wait(ctx, ctx->stream));
     return RK_OK;
 }
 
@@ -1577,7 +1628,7 @@ rk_status rk_state_set(rk_state st, const double* src, int src_on_device) {
     } else {
         CK_CTX(ctx, cudaMemcpyAsync(st->u, src, sizeof(double) * (size_t)st->count, kind, ctx->stream));
     }
-    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    TRY(ctx_wait(ctx, ctx->stream));
     st->k1_valid = false;
     ab_invalidate(st);
     return RK_OK;
@@ -1595,7 +1646,7 @@ rk_status rk_state_get(rk_state st, double* dst, int dst_on_device) {
     } else {
         CK_CTX(ctx, cudaMemcpyAsync(dst, st->u, sizeof(double) * (size_t)st->count, kind, ctx->stream));
     }
-    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));
+    TRY(ctx_wait(ctx, ctx->stream));
     return RK_OK;
 }
 
@@ -1662,6 +1713,10 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
         st->coop_max_cells = value;
         break;
     case RK_OPT_FUSED_STEP: st->fused = value != 0; break;
+    case RK_OPT_COMM_TIMEOUT_MS:
+        if (value < 0) return fail(RK_ERR_ARG, "RK_OPT_COMM_TIMEOUT_MS must be >= 0");
+        st->ctx->comm_timeout_ms = value;
+        break;
     case RK_OPT_HALO_P2P:
         if (value != 0 && !st->grid) return fail(RK_ERR_ARG, "RK_OPT_HALO_P2P needs a grid state");
         st->p2p = value != 0;
@@ -1672,6 +1727,7 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
 }
 
 rk_status rk_do_step(rk_state st, rk_scheme scheme, double t, double dt) {
+    NvtxRange nv("rk_do_step");
     TRY(check_state(st));
     if (!valid_scheme(scheme)) return fail(RK_ERR_ARG, "bad scheme %d", (int)scheme);
     if (!(dt > 0.0) || !std::isfinite(dt)) return fail(RK_ERR_ARG, "dt must be finite and > 0");
@@ -1697,6 +1753,7 @@ rk_status rk_try_step(rk_state st, rk_scheme scheme, double t, double dt, double
 
 rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1, double dt,
                              int64_t* steps) {
+    NvtxRange nv("rk_integrate_const");
     TRY(check_state(st));
     if (!valid_scheme(scheme)) return fail(RK_ERR_ARG, "bad scheme %d", (int)scheme);
     if (!(dt > 0.0) || !std::isfinite(dt)) return fail(RK_ERR_ARG, "dt must be finite and > 0");
@@ -1743,13 +1800,14 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
         for (int64_t i = 0; i < n; ++i) TRY(fixed_step(st, scheme, dt));
     }
     TRY(finite_check(st, 0, t0 + (double)n * dt, true));
-    CK_CTX(st->ctx, cudaStreamSynchronize(st->ctx->stream));
+    TRY(ctx_wait(st->ctx, st->ctx->stream));
     if (steps) *steps = n;
     return RK_OK;
 }
 
 rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double t1, double dt0,
                                 double atol, double rtol, int64_t* accepted, int64_t* rejected) {
+    NvtxRange nv("rk_integrate_adaptive");
     TRY(check_state(st));
     if (!valid_scheme(scheme)) return fail(RK_ERR_ARG, "bad scheme %d", (int)scheme);
     if (!(dt0 > 0.0) || !std::isfinite(dt0)) return fail(RK_ERR_ARG, "dt0 must be finite and > 0");
@@ -1825,7 +1883,7 @@ rk_status rk_lincomb(rk_state out, int k, const double* coef, const rk_state* in
     out->stats.kernel_launches += 1;
     out->k1_valid = false;
     ab_invalidate(out);
-    CK_CTX(out->ctx, cudaStreamSynchronize(out->ctx->stream));
+    TRY(ctx_wait(out->ctx, out->ctx->stream));
     return RK_OK;
 }
 

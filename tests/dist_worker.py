@@ -24,6 +24,7 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     stream = torch.cuda.current_stream()
     ctx = rk.Context.from_torch_distributed(local, stream)
+    # failure detection on: host waits poll NCCL's async error state (10-minute deadline)
     nx, ny, nz = 40, 24, 7 * world + 3  # ragged slabs (remainder planes on the low ranks)
     u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=42)
     u0 = u0 + 0.01 * rk_inputs.random_state(u0.size, 5).reshape(u0.shape)
@@ -39,6 +40,7 @@ def main():
         for overlap in (1, 0):
             st = ctx.grid(nx, ny, nz, 2)
             st.set_rhs_gray_scott()
+            st.set_option(rk.OPT_COMM_TIMEOUT_MS, 600000)
             if world == 1:  # one GPU: the same halo code path through the loopback exchange
                 st.set_option(rk.OPT_HALO_LOOPBACK, 1)
             st.set_option(rk.OPT_HALO_OVERLAP, overlap)

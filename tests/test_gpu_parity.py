@@ -347,6 +347,25 @@ def test_error_conventions(ctx):
     assert e.value.status == "RK_ERR_DIVERGED"
 
 
+def test_comm_timeout_option(ctx):
+    """RK_OPT_COMM_TIMEOUT_MS (failure detection): >= 0 accepted; on one GPU there
+    is no communicator, so results are unchanged; a negative deadline is an argument error."""
+    import paper_2309_05331_b200 as rk
+    v = ctx.vector(1001)
+    v.set_rhs_logistic()
+    u0 = rk_inputs.logistic_u0(1001)
+    v.set(u0)
+    v.set_option(rk.OPT_COMM_TIMEOUT_MS, 5000)
+    a, r = v.integrate_adaptive("dopri5", -5.0, 5.0, 0.1, 1e-8, 1e-8)
+    uo, ao, ro, rc = oracle.integrate_adaptive(oracle.logistic_problem(1001), OS["dopri5"], u0, -5.0, 5.0, 0.1,
+                                               1e-8, 1e-8)
+    assert (a, r) == (ao, ro) and bitwise(v.get(), uo)
+    with pytest.raises(rk.RKError) as e:
+        v.set_option(rk.OPT_COMM_TIMEOUT_MS, -1)
+    assert e.value.status == "RK_ERR_ARG"
+    v.set_option(rk.OPT_COMM_TIMEOUT_MS, 0)
+
+
 def test_stats_count_launches(ctx):
     n = 16
     st = gs_state(ctx, n, n, n, rk_inputs.gray_scott_ic(n, n, n))
