@@ -76,7 +76,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        L = ctypes.CDLL(build())
+        # ORACLE_LIB: an alternative build of the same source (the sanitizer test's ASan/UBSan build)
+        L = ctypes.CDLL(os.environ.get("ORACLE_LIB") or build())
         P = ctypes.POINTER(Problem)
         dp = ctypes.POINTER(ctypes.c_double)
         i64p = ctypes.POINTER(ctypes.c_int64)

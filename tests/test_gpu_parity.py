@@ -1046,3 +1046,39 @@ def test_gs32_20000_steps_bitwise_golden(ctx, coop):
     g = np.ascontiguousarray(st.get(), dtype="<f8")
     assert float(g[:, 1].min()) == gold["c1_min"] and float(g[:, 0].max()) == gold["c0_max"]
     assert hashlib.sha256(g.tobytes()).hexdigest() == gold["sha256_final"]
+
+
+def test_checkpoint_resume_bitwise(ctx):
+    """Checkpoint = rk_state_get (+ t, dt), resume = rk_state_set on a NEW state: the resumed
+    run equals the uninterrupted one bit for bit -- fixed RK4 through integrate_const, and
+    error-controlled DOPRI5 through try_step (same accepted dt sequence; the resumed state
+    recomputes k1 = F(u), the same value FSAL would have carried)."""
+    nx, ny, nz = 40, 24, 20
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=8) + 0.01 * rk_inputs.random_state(2 * nx * ny * nz, 2).reshape(nz, 2, ny, nx)
+    a = gs_state(ctx, nx, ny, nz, u0)
+    a.integrate_const("rk4", 0.0, 10.0, 1.0)
+    b = gs_state(ctx, nx, ny, nz, u0)
+    b.integrate_const("rk4", 0.0, 5.0, 1.0)
+    c = gs_state(ctx, nx, ny, nz, b.get())
+    c.integrate_const("rk4", 5.0, 10.0, 1.0)
+    assert bitwise(a.get(), c.get())
+
+    def accepted_steps(st, t, dt, n):
+        seq = []
+        while len(seq) < n:
+            ok, E, dtn = st.try_step("dopri5", t, dt, 1e-6, 1e-6)
+            if ok:
+                seq.append(dt)
+                t += dt
+            dt = dtn
+        return t, dt, seq
+
+    full = gs_state(ctx, nx, ny, nz, u0)
+    _, _, seq_full = accepted_steps(full, 0.0, 1.0, 8)
+    part = gs_state(ctx, nx, ny, nz, u0)
+    t, dt, seq1 = accepted_steps(part, 0.0, 1.0, 3)
+    ck = part.get()
+    res = gs_state(ctx, nx, ny, nz, ck)
+    _, _, seq2 = accepted_steps(res, t, dt, 5)
+    assert seq1 + seq2 == seq_full
+    assert bitwise(full.get(), res.get())
