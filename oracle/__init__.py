@@ -21,9 +21,9 @@ _SRC = os.path.join(_HERE, "rk_oracle.c")
 _HDR = os.path.join(_HERE, "rk_oracle.h")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-EULER, RK4, CASH_KARP54, DOPRI5, RKF78, MIDPOINT = 0, 1, 2, 3, 4, 5
+EULER, RK4, CASH_KARP54, DOPRI5, RKF78, MIDPOINT, MODIFIED_MIDPOINT = 0, 1, 2, 3, 4, 5, 6
 SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5,
-           "rkf78": RKF78, "midpoint": MIDPOINT}
+           "rkf78": RKF78, "midpoint": MIDPOINT, "modified_midpoint": MODIFIED_MIDPOINT}
 RHS_EXP, RHS_LOGISTIC, RHS_GRAY_SCOTT = 0, 1, 2
 OK, ERR_ARG, ERR_UNSUPPORTED, ERR_DIVERGED, ERR_STALL = 0, 1, 2, 3, 4
 

@@ -43,14 +43,30 @@ static const tableau TAB_EULER = {
     {{0, 1}},
 };
 
-/* Modified midpoint (Table 1, order 2) read as the explicit midpoint rule: an Euler
- * half step, then the full step with the midpoint slope (R-22). */
+/* Explicit midpoint rule (order 2): an Euler half step, then the full step with the midpoint
+ * slope.  Kept under its own name; Table 1's "modified midpoint" is TAB_MODIFIED_MIDPOINT
+ * below (R-22). */
 static const tableau TAB_MIDPOINT = {
     2, 2, 0, 0,
     {{0, 1}, {1, 2}},
     {{{0, 1}},
      {{1, 2}}},
     {{0, 1}, {1, 1}},
+    {{0, 1}},
+};
+
+/* Modified midpoint (Table 1, order 2) = Odeint's modified_midpoint, Gragg's scheme with
+ * its default n = 2 substeps of h = dt/2 (R-22):
+ *     x1 = u + h F(u),  x2 = u + 2h F(x1),  u_new = (x1 + x2 + h F(x2)) / 2.
+ * Substituting x1 and x2 gives the 3-stage Butcher form used here (R-17 arithmetic):
+ *     Y2 = u + (dt/2) k1,  Y3 = u + dt k2,  u_new = u + (dt/4) k1 + (dt/2) k2 + (dt/4) k3. */
+static const tableau TAB_MODIFIED_MIDPOINT = {
+    3, 2, 0, 0,
+    {{0, 1}, {1, 2}, {1, 1}},
+    {{{0, 1}},
+     {{1, 2}},
+     {{0, 1}, {1, 1}}},
+    {{1, 4}, {1, 2}, {1, 4}},
     {{0, 1}},
 };
 
@@ -122,6 +138,7 @@ static const tableau* get_tableau(int scheme) {
     case ORC_DOPRI5: return &TAB_DOPRI5;
     case ORC_RKF78: return &TAB_RKF78;
     case ORC_MIDPOINT: return &TAB_MIDPOINT;
+    case ORC_MODIFIED_MIDPOINT: return &TAB_MODIFIED_MIDPOINT;
     default: return NULL;
     }
 }

@@ -28,7 +28,7 @@ extern "C" {
 
 /* Schemes of Table 1 on the hot path. */
 enum { ORC_EULER = 0, ORC_RK4 = 1, ORC_CASH_KARP54 = 2, ORC_DOPRI5 = 3, ORC_RKF78 = 4,
-       ORC_MIDPOINT = 5 };
+       ORC_MIDPOINT = 5 /* explicit midpoint */, ORC_MODIFIED_MIDPOINT = 6 /* Gragg, Table 1 P:L58 */ };
 /* RHS kinds: Eq. 1a as du/dt = lambda*u, Eq. 1b, Eq. 3 / Listing 2. */
 enum { ORC_RHS_EXP = 0, ORC_RHS_LOGISTIC = 1, ORC_RHS_GRAY_SCOTT = 2 };
 /* Status codes. */

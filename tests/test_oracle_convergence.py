@@ -15,7 +15,7 @@ import oracle
 import rk_inputs
 
 ORDERS = {oracle.EULER: 1, oracle.RK4: 4, oracle.CASH_KARP54: 5, oracle.DOPRI5: 5,
-          oracle.MIDPOINT: 2}
+          oracle.MIDPOINT: 2, oracle.MODIFIED_MIDPOINT: 2}
 
 
 def run_traj(p, scheme, u0, t0, t1, dt, exact):

@@ -19,7 +19,8 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden")
 EPS = np.finfo(np.float64).eps
 POLYS = json.load(open(os.path.join(GOLD, "stability_polys.json")))
 NAMES = {oracle.EULER: "euler", oracle.RK4: "rk4", oracle.CASH_KARP54: "cash_karp54",
-         oracle.DOPRI5: "dopri5", oracle.MIDPOINT: "midpoint"}
+         oracle.DOPRI5: "dopri5", oracle.MIDPOINT: "midpoint",
+         oracle.MODIFIED_MIDPOINT: "modified_midpoint"}
 
 
 def R(name, z, which="b"):

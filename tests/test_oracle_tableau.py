@@ -82,7 +82,8 @@ def test_tree_counts():
 
 SCHEMES = [("euler", oracle.EULER, 1, None), ("rk4", oracle.RK4, 4, None),
            ("cash_karp54", oracle.CASH_KARP54, 5, 4), ("dopri5", oracle.DOPRI5, 5, 4),
-           ("rkf78", oracle.RKF78, 8, 7), ("midpoint", oracle.MIDPOINT, 2, None)]
+           ("rkf78", oracle.RKF78, 8, 7), ("midpoint", oracle.MIDPOINT, 2, None),
+           ("modified_midpoint", oracle.MODIFIED_MIDPOINT, 2, None)]
 
 
 def test_tree_counts_to_order_9():
