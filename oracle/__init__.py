@@ -37,7 +37,7 @@ def build(force: bool = False) -> str:
         os.path.getmtime(f) > os.path.getmtime(_LIB) for f in (_SRC, _HDR))
     if force or stale:
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lquadmath", "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 

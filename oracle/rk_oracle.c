@@ -16,6 +16,7 @@
 
 #include <float.h>
 #include <math.h>
+#include <quadmath.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -322,19 +323,28 @@ double orc_error_ratio_max(int64_t count, const double* err, const double* u, co
     return E;
 }
 
+/* The controller's x^y, correctly rounded (R-27): evaluated in binary128
+ * (libquadmath powq, 113-bit significand) and rounded once to double.  Double rounding can
+ * only differ from the correctly rounded value when x^y lies within ~2^-110 (relative) of a
+ * double rounding midpoint.  Pinned against 60-digit decimal arithmetic
+ * (tests/test_oracle_adaptive.py::test_controller_pow_correctly_rounded). */
+static double cr_pow(double x, double y) {
+    return (double)powq((__float128)x, (__float128)y);
+}
+
 int orc_controller(double E, int p, int q, double* dt) {
     if (E > 1.0) {
         /* reject: decrease_step */
-        double fac = (9.0 / 10.0) * pow(E, -1.0 / (double)(q - 1));
+        double fac = (9.0 / 10.0) * cr_pow(E, -1.0 / (double)(q - 1));
         if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
         *dt = *dt * fac;
         return 0;
     }
     /* accept: increase_step */
     if (E < 0.5) {
-        double Ec = pow(5.0, -(double)p);
+        double Ec = cr_pow(5.0, -(double)p);
         if (E > Ec) Ec = E;
-        *dt = *dt * ((9.0 / 10.0) * pow(Ec, -1.0 / (double)p));
+        *dt = *dt * ((9.0 / 10.0) * cr_pow(Ec, -1.0 / (double)p));
     }
     return 1;
 }
@@ -379,14 +389,14 @@ double orc_error_ratio_max_spec(int64_t count, const double* err, const double* 
 int orc_controller_spec(double E, int p, double* dt) {
     if (E <= 1.0) {
         /* accepted: dt_next = dt*min(grow_cap, max(shrink_floor, safety*err^(-1/p))) */
-        double fac = (9.0 / 10.0) * pow(E, -1.0 / (double)p);
+        double fac = (9.0 / 10.0) * cr_pow(E, -1.0 / (double)p);
         if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
         if (fac > 5.0) fac = 5.0;
         *dt = *dt * fac;
         return 1;
     }
     /* rejected: dt_next = dt*max(shrink_floor, safety*err^(-1/(p-1))) */
-    double fac = (9.0 / 10.0) * pow(E, -1.0 / (double)(p - 1));
+    double fac = (9.0 / 10.0) * cr_pow(E, -1.0 / (double)(p - 1));
     if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
     *dt = *dt * fac;
     return 0;

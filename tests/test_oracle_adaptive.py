@@ -119,3 +119,40 @@ def test_rkf78_adaptive_meets_tolerance():
                                                     -5.0, 5.0, 0.1, tol, tol)
         assert rc == oracle.OK and acc > 0
         assert abs(u[0] - 1.0 / (1.0 + math.exp(-5.0))) <= 100 * tol
+
+
+def _cr_pow(x: float, y: float) -> float:
+    """x^y correctly rounded to double: Python's decimal computes non-integral powers
+    correctly rounded at the context precision (60 digits here), float() rounds once more."""
+    from decimal import Decimal, localcontext
+    with localcontext() as c:
+        c.prec = 60
+        return float(Decimal(x) ** Decimal(y))
+
+
+def test_controller_pow_correctly_rounded():
+    """DESIGN.md R-27: the controller's pow is the correctly rounded x^y (the oracle evaluates
+    it in binary128 and rounds once; the library in double-double).  Every dt the oracle
+    proposes equals the one built from 60-digit decimal powers with the same fp64 steps
+    (fac = 0.9 * x^y, clamps, dt * fac).  glibc's pow misses ~0.1 % of these arguments by an
+    ulp, so this pin separates the two readings."""
+    rng = np.random.default_rng(27)
+    Es = list(10.0 ** rng.uniform(-12, 4, 3000)) + [0.3, 0.49, 1.5, 10.0, 5.0 ** -5, 1e-300]
+    emin = _cr_pow(5.0, -5.0)
+    for E in Es:
+        E = float(E)
+        for dt0 in (1.0, 0.1):
+            acc, dt = oracle.controller(E, dt0)
+            if E > 1.0:
+                want = dt0 * max(0.9 * _cr_pow(E, -1.0 / 3.0), 0.2)
+            elif E < 0.5:
+                want = dt0 * (0.9 * _cr_pow(max(E, emin), -1.0 / 5.0))
+            else:
+                want = dt0
+            assert acc == (E <= 1.0) and dt == want, (E, dt0, dt, want)
+            acc_s, dt_s = oracle.controller_spec(E, dt0, 5)
+            if E <= 1.0:
+                want_s = dt0 * min(5.0, max(0.2, 0.9 * _cr_pow(E, -1.0 / 5.0)))
+            else:
+                want_s = dt0 * max(0.2, 0.9 * _cr_pow(E, -1.0 / 4.0))
+            assert acc_s == (E <= 1.0) and dt_s == want_s, (E, dt0, dt_s, want_s)

@@ -57,7 +57,7 @@ def test_oracle_asan_ubsan():
     lib = os.path.join(tmp, "liboracle.so")
     b = subprocess.run(["gcc", "-O1", "-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined",
                         "-fno-sanitize-recover=undefined", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-                        "-std=c11", os.path.join(ROOT, "oracle", "rk_oracle.c"), "-o", lib, "-lm"],
+                        "-std=c11", os.path.join(ROOT, "oracle", "rk_oracle.c"), "-o", lib, "-lquadmath", "-lm"],
                        capture_output=True, text=True)
     assert b.returncode == 0, b.stderr
     base = dict(os.environ, PYTHONPATH=ROOT)
