@@ -268,7 +268,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
-    ap.add_argument("--legs", default="adaptive,rk4,repeats,halo,exposed,strong,strong_emul,rk4_native,rk4_k6,exp512,small,e2e,cpu",
+    ap.add_argument("--legs", default="adaptive,rk4,repeats,try_loop,halo,exposed,strong,strong_emul,rk4_native,rk4_k6,exp512,small,e2e,cpu",
                     help="comma list of legs (profiling runs use e.g. --legs rk4)")
     ap.add_argument("--no-extra", action="store_true", help="same as --legs adaptive")
     ap.add_argument("--overlap", type=int, default=1, help="halo exchange overlapped (N > 1)")
@@ -352,19 +352,28 @@ def main():
                 return tries
             state["dt"] = dtn
 
+    T1 = 20.0  # configs[3]/[4]: DOPRI5 adaptive over t in [0, 20], dt0 = 1
+
+    def integrate_step(src):
+        """One bench "step" = one pass of the whole hot path over the configs[3]/[4] input:
+        rk_state_set of the seeded IC (src: device tensor, or pinned host tensor for e2e) and
+        rk_integrate_adaptive from t = 0 to 20 (the a8 driver: every try's stages, halo path,
+        error max + allreduce, controller, FSAL).  Returns (accepted, rejected)."""
+        st.set(src)
+        return st.integrate_adaptive("dopri5", 0.0, T1, 1.0, TOL, TOL)
+
     def adaptive_leg():
-        st.set(u0_dev)
-        state["t"], state["dt"] = 0.0, 1.0
         for _ in range(args.warmup):
-            adaptive_step()
+            integrate_step(u0_dev)
         st.set_option(rk.OPT_TIMING, 1)
         st.reset_stats()
         barrier()
-        tries = 0
+        acc = rej = 0
         with ClockSampler(local) as clk:
             ev0.record(stream)
             for _ in range(args.steps):
-                tries += adaptive_step()
+                a, r = integrate_step(u0_dev)
+                acc, rej = acc + a, rej + r
             ev1.record(stream)
             barrier()
         ms = max_over_ranks(ev0.elapsed_time(ev1))
@@ -375,7 +384,8 @@ def main():
         step_bytes = s["stage_bytes"] / max(1, s["tries"])
         line = {
             "metric": "gray_scott_cell_updates_per_s",
-            "value": cells_total * args.steps / (ms / 1e3),
+            # a cell-update = one cell advanced by one ACCEPTED Runge-Kutta step
+            "value": cells_total * acc / (ms / 1e3),
             "unit": "cell-updates/s",
             "n_gpus": world,
             "steps": args.steps,
@@ -388,7 +398,12 @@ def main():
             "data": "synthetic (seeded Gray-Scott IC, DESIGN.md R-6)",
             "config": {"workload": "gray_scott_dopri5_adaptive_512^3_per_gpu", "nx": n, "ny": n,
                        "nz_global": nzg, "nz_per_gpu": int(st.local), "h": H, "atol": TOL,
-                       "rtol": TOL, "scheme": "dopri5 (FSAL, error-controlled)", "tries": tries,
+                       "rtol": TOL, "scheme": "dopri5 (FSAL, error-controlled)",
+                       "step": "one rk_integrate_adaptive call over t in [0, 20], dt0 = 1, from the "
+                               "seeded IC (rk_state_set from HBM inside the timed region)",
+                       "accepted_per_step": acc / args.steps, "rejected_per_step": rej / args.steps,
+                       "tries": s["tries"], "ms_per_accepted_rk_step": ms / max(1, acc),
+                       "ms_per_try": ms / max(1, s["tries"]),
                        "halo_overlap": bool(args.overlap),
                        "l2": "no flush: every array is 2 GiB per GPU, >> 126 MB L2",
                        "parallelism": f"z-slab x{world} (NCCL send/recv halos + allreduce max)"},
@@ -396,6 +411,10 @@ def main():
                          "frac": (achieved / peak) if achieved else None,
                          "frac_of_datasheet_8000": (achieved / 8000.0) if achieved else None,
                          "traffic": traffic.get("dopri5_adaptive", {}).get("bytes_per_launch"),
+                         "traffic_source": "not measured in this run: dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum per stage launch of one DOPRI5 try "
+                                           "from the committed ncu --set full capture "
+                                           f"(profiles/ncu_traffic.json: {str(traffic.get('_source', '?'))[:40]})",
                          "kernel": "gs_stage_kernel (K3: fused stage value + 7-pt stencil + "
                                    "reaction + epilogue), all stage launches of the timed tries",
                          "algorithmic_bytes_per_launch": s["stage_bytes"] / max(1, s["stage_launches"]),
@@ -404,7 +423,7 @@ def main():
                          "launches": s["stage_launches"], "peak_source": peak_src,
                          # SURVEY §8d gate: cells x tries x 528 B (its DOPRI5 adaptive schedule)
                          # over the whole timed region, against >= 0.70 of the measured peak
-                         "survey_gate": survey_gate(528, cells_local * tries, ms)},
+                         "survey_gate": survey_gate(528, cells_local * s["tries"], ms)},
             "gpu_launches": s["kernel_launches"],
             "clocks": getattr(clk, "result", None),
         }
@@ -412,6 +431,35 @@ def main():
         if h:
             line["halo"] = h
         return line
+
+    # the try_step loop of round 1 (one accepted step per "step", Python-driven): kept as an extra
+    state = {"t": 0.0, "dt": 1.0}
+
+    def adaptive_step():
+        tries = 0
+        while True:
+            acc, E, dtn = st.try_step("dopri5", state["t"], state["dt"], TOL, TOL)
+            tries += 1
+            if acc:
+                state["t"] += state["dt"]
+                state["dt"] = dtn
+                return tries
+            state["dt"] = dtn
+
+    def try_loop_leg():
+        st.set(u0_dev)
+        state["t"], state["dt"] = 0.0, 1.0
+        for _ in range(args.warmup):
+            adaptive_step()
+        barrier()
+        ev0.record(stream)
+        tries = sum(adaptive_step() for _ in range(args.steps))
+        ev1.record(stream)
+        barrier()
+        ms = max_over_ranks(ev0.elapsed_time(ev1))
+        return {"value": cells_total * args.steps / (ms / 1e3), "unit": "cell-updates/s",
+                "ms_per_step": ms / args.steps, "tries": tries,
+                "config": "rk_try_step driven from Python, one accepted DOPRI5 step per step"}
 
     def rk4_leg(overlap: int, scheme: str = "rk4", p2p: int = 0, loopback: int = 0):
         st.set_option(rk.OPT_HALO_OVERLAP, overlap)
@@ -478,25 +526,25 @@ def main():
         return out
 
     def e2e_leg():
-        # the same metric through the C-ABI with HOST buffers: every step copies the state in
-        # (pinned H2D) and the result out (pinned D2H) inside the timed region
+        # the same metric through the C-ABI with HOST buffers: every step copies the IC in
+        # (pinned H2D, rk_state_set), integrates (rk_integrate_adaptive, incl. its 8-byte
+        # error-ratio D2H per try) and copies the result out (pinned D2H, rk_state_get)
         host_in = torch.from_numpy(u0).pin_memory()
         host_out = torch.empty_like(host_in).pin_memory()
-        st.set(host_in)
-        state["t"], state["dt"] = 0.0, 1.0
-        adaptive_step()
+        integrate_step(host_in)
         ke = max(1, min(args.steps, 5))
         barrier()
+        acc = 0
         ev0.record(stream)
         for _ in range(ke):
-            st.set(host_in)   # H2D of the step's input state
-            adaptive_step()   # includes the 8-byte error-ratio D2H per try
-            st.get(host_out)  # D2H of the step's result
+            a, _ = integrate_step(host_in)  # H2D of the step's input state + the integration
+            acc += a
+            st.get(host_out)                # D2H of the step's result
         ev1.record(stream)
         barrier()
         mse = max_over_ranks(ev0.elapsed_time(ev1))
-        return {"value": cells_total * ke / (mse / 1e3), "unit": "cell-updates/s",
-                "h2d_bytes_per_step": u0.nbytes, "d2h_bytes_per_step": u0.nbytes + 8,
+        return {"value": cells_total * acc / (mse / 1e3), "unit": "cell-updates/s",
+                "h2d_bytes_per_step": u0.nbytes, "d2h_bytes_per_step": u0.nbytes,
                 "steps": ke, "ms_per_step": mse / ke}
 
     def native_rk4_leg():
@@ -770,6 +818,18 @@ def main():
     extra = {}
     if "rk4" in legs:
         extra["rk4"] = run_leg(rk4_leg, args.overlap)
+        r4 = extra["rk4"]
+        if line and "roofline" in r4:
+            # north_star's second target workload, kept inside `roofline` (the driver's parsed
+            # record keeps this object but not `extra`)
+            line["roofline"]["rk4_512"] = {
+                "workload": "gray_scott_rk4_dt1_512^3_per_gpu (do_step x K)", "value": r4["value"],
+                "unit": "cell-updates/s", "ms_per_step": r4["ms_per_step"],
+                "achieved": r4["roofline"]["achieved"], "frac": r4["roofline"]["frac"],
+                "algorithmic_bytes_per_cell_step": r4["roofline"]["algorithmic_bytes_per_cell_step"],
+                "traffic": r4["roofline"]["traffic"]}
+    if "try_loop" in legs:
+        extra["dopri5_try_loop"] = run_leg(try_loop_leg)
     if "repeats" in legs:
         # each config 3 times, mean and min (the headline line is the first run)
         def rep(fn, *a):

@@ -72,7 +72,13 @@ typedef enum {
     RK_CASH_KARP54 = 2,  /* Cash–Karp 5(4), fixed or error-controlled      */
     RK_DOPRI5 = 3,       /* Dormand–Prince 5(4), FSAL, fixed or error-controlled  */
     RK_FEHLBERG78 = 4,   /* Runge–Kutta–Fehlberg 7(8), fixed or error-controlled  */
-    RK_MIDPOINT = 5,     /* modified midpoint, order 2 (R-22)            */
+    RK_EXPLICIT_MIDPOINT = 5, /* explicit midpoint rule, order 2: Euler half step, then the
+                                 full step with the midpoint slope (R-22)  */
+    RK_MIDPOINT = RK_EXPLICIT_MIDPOINT, /* (ABI v2 name of the same scheme)                   */
+    RK_MODIFIED_MIDPOINT = 6, /* modified midpoint, order 2 (Table 1) = Odeint's
+                                 modified_midpoint: Gragg's scheme with 2 substeps h = dt/2,
+                                 3 RHS evaluations; computed in its Butcher form c = (0,1/2,1),
+                                 a21 = 1/2, a32 = 1, b = (1/4,1/2,1/4) (R-22, R-17) */
     /* Adams–Bashforth k-step, order k, fixed dt only (Table 1 multi-step row).
      * The state keeps the last k-1 slopes F(u_{n-j}); the first k-1 steps after any other
      * change of u (set, another scheme, a new dt) are RKF78 bootstrap steps (R-23).

@@ -15,9 +15,11 @@ import numpy as np
 from . import _native
 from ._native import Stats, call
 
-EULER, RK4, CASH_KARP54, DOPRI5, FEHLBERG78, MIDPOINT = 0, 1, 2, 3, 4, 5
+EULER, RK4, CASH_KARP54, DOPRI5, FEHLBERG78, MIDPOINT, MODIFIED_MIDPOINT = 0, 1, 2, 3, 4, 5, 6
+EXPLICIT_MIDPOINT = MIDPOINT
 SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5,
-           "rkf78": FEHLBERG78, "midpoint": MIDPOINT}
+           "rkf78": FEHLBERG78, "midpoint": MIDPOINT, "explicit_midpoint": MIDPOINT,
+           "modified_midpoint": MODIFIED_MIDPOINT}
 SCHEMES.update({f"ab{k}": 10 + k for k in range(1, 9)})  # Adams–Bashforth k (rk_b200.h)
 SCHEMES.update({f"abm{k}": 20 + k for k in range(1, 9)})  # Adams–Bashforth–Moulton k (PECE)
 
@@ -34,6 +36,14 @@ def _stream_handle(stream) -> int | None:
         return None
     h = stream if isinstance(stream, int) else int(stream.cuda_stream)
     return h if h != 0 else 1
+
+
+def _order_after_torch(t) -> None:
+    """The library copies on the ctx stream, which need not be torch's current stream: let the
+    torch work already queued on `t` (writes before set, reads before get) finish first."""
+    if t.is_cuda:
+        import torch
+        torch.cuda.current_stream(t.device).synchronize()
 
 
 def broadcast_unique_id(group=None, device: int | None = None) -> bytes:
@@ -136,6 +146,7 @@ class State:
         if hasattr(src, "data_ptr"):  # torch
             assert src.dtype.__repr__() == "torch.float64" and src.is_contiguous()
             assert src.numel() == self.size
+            _order_after_torch(src)
             call("rk_state_set", self._h, ctypes.c_void_p(src.data_ptr()), 1 if src.is_cuda else 0)
         else:
             a = np.ascontiguousarray(src, dtype=np.float64)
@@ -148,6 +159,7 @@ class State:
             out = np.empty(self.local_shape, dtype=np.float64)
         if hasattr(out, "data_ptr"):
             assert out.numel() == self.size and out.is_contiguous()
+            _order_after_torch(out)
             call("rk_state_get", self._h, ctypes.c_void_p(out.data_ptr()), 1 if out.is_cuda else 0)
         else:
             assert out.size == self.size and out.flags.c_contiguous and out.dtype == np.float64

@@ -438,7 +438,7 @@ cudaError_t launch_fused_t(const GsFusedArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-bool fused_scheme(int scheme) { return scheme == 1 || scheme == 5; }
+bool fused_scheme(int scheme) { return scheme == 1 || scheme == 5 || scheme == 6; }
 
 int fused_halo(int scheme) { return fused_scheme(scheme) ? tableau_of(scheme).s : 0; }
 
@@ -466,6 +466,7 @@ cudaError_t launch_gs_fused(int scheme, const GsFusedArgs& a, cudaStream_t st) {
     switch (scheme) {
     case 1: return launch_fused_t<1>(a, st);  // RK4
     case 5: return launch_fused_t<5>(a, st);  // explicit midpoint
+    case 6: return launch_fused_t<6>(a, st);  // modified midpoint (Gragg, 2 substeps)
     default: return cudaErrorInvalidValue;
     }
 }

@@ -418,6 +418,7 @@ cudaError_t launch_pointwise(int scheme, const PwArgs& a, cudaStream_t st, int n
     case 3: return launch_s<3>(a, st, num_sms);
     case 4: return launch_s<4>(a, st, num_sms);
     case 5: return launch_s<5>(a, st, num_sms);
+    case 6: return launch_s<6>(a, st, num_sms);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -19,11 +19,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <string>
 #include <utility>
 #include <vector>
 
 #include "rk_b200.h"
+#include "rk_ddmath.cuh"
 #include "rk_kernels.cuh"
 #include "rk_tableau.h"
 
@@ -57,6 +59,10 @@ struct rk_ctx_s {
     unsigned long long* d_scratch = nullptr;  // 8 B reduction word (norm_inf)
     unsigned long long* h_scratch = nullptr;  // pinned
     std::vector<rk_state_s*> states;          // live states (destroyed with the ctx)
+    // progress marks: an event recorded behind every collective; a host wait restarts its
+    // RK_OPT_COMM_TIMEOUT_MS clock whenever one of them completes (ctx_wait)
+    std::deque<cudaEvent_t> marks;
+    std::vector<cudaEvent_t> mark_pool;
 };
 
 #define CK_CTX(ctx, call)                                                                     \
@@ -95,18 +101,45 @@ struct NvtxRange {
     NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
+// Record a progress mark behind a collective just enqueued on stream s (ctx_wait).
+static void mark_progress(rk_ctx ctx, cudaStream_t s) {
+    if (!ctx->nccl || ctx->comm_timeout_ms <= 0 || ctx->marks.size() >= 512) return;
+    cudaEvent_t e = nullptr;
+    if (!ctx->mark_pool.empty()) {
+        e = ctx->mark_pool.back();
+        ctx->mark_pool.pop_back();
+    } else if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    if (cudaEventRecord(e, s) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->mark_pool.push_back(e);
+        return;
+    }
+    ctx->marks.push_back(e);
+}
+
 // Wait for stream s.  With a NCCL communicator the host polls instead of blocking, so an
 // asynchronous NCCL error (a peer died, a link failed) or the RK_OPT_COMM_TIMEOUT_MS deadline
 // aborts the communicator and returns RK_ERR_NCCL (the context is poisoned) instead of hanging
-// in a collective forever (SURVEY §5 failure detection).
+// in a collective forever (SURVEY §5 failure detection).  The deadline runs from the last
+// PROGRESS: the start of the wait or the completion of the latest collective mark
+// (mark_progress), so queued compute behind many collectives does not count against it -- only
+// the longest stretch without a completed collective does.
 static rk_status ctx_wait(rk_ctx ctx, cudaStream_t s) {
     if (!ctx->nccl) {
         CK_CTX(ctx, cudaStreamSynchronize(s));
         return RK_OK;
     }
-    const auto t0 = std::chrono::steady_clock::now();
+    auto t0 = std::chrono::steady_clock::now();
     for (unsigned spin = 0;; ++spin) {
         const cudaError_t q = cudaStreamQuery(s);
+        while (!ctx->marks.empty() && cudaEventQuery(ctx->marks.front()) == cudaSuccess) {
+            ctx->mark_pool.push_back(ctx->marks.front());
+            ctx->marks.pop_front();
+            t0 = std::chrono::steady_clock::now();
+        }
         if (q == cudaSuccess) return RK_OK;
         if (q != cudaErrorNotReady) CK_CTX(ctx, q);
         ncclResult_t ar = ncclSuccess;
@@ -118,13 +151,29 @@ static rk_status ctx_wait(rk_ctx ctx, cudaStream_t s) {
             ctx->nccl = nullptr;
             ctx->poisoned = RK_ERR_NCCL;
             if (late)
-                return fail(RK_ERR_NCCL, "collective wait exceeded %lld ms on rank %d: communicator aborted",
+                return fail(RK_ERR_NCCL, "no collective progress for %lld ms on rank %d: communicator aborted",
                             (long long)ctx->comm_timeout_ms, ctx->rank);
             return fail(RK_ERR_NCCL, "asynchronous NCCL error %s on rank %d: communicator aborted",
                         ncclGetErrorString(ar), ctx->rank);
         }
         if (spin >= 256) std::this_thread::sleep_for(std::chrono::microseconds(20));
     }
+}
+
+// Teardown wait: a context poisoned by a NCCL failure may have kernels spinning on peer flags
+// (P2P halos) that the abort does not release, so its streams are drained for a bounded time
+// only (then the buffers are leaked rather than freed under a running kernel).
+static bool drain_stream(rk_ctx ctx, cudaStream_t s) {
+    if (!s) return true;
+    if (ctx->poisoned != RK_ERR_NCCL) return cudaStreamSynchronize(s) == cudaSuccess;
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto lim = std::chrono::milliseconds(std::max<int64_t>(ctx->comm_timeout_ms, 2000));
+    while (cudaStreamQuery(s) == cudaErrorNotReady) {
+        if (std::chrono::steady_clock::now() - t0 > lim) return false;
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
+    cudaGetLastError();
+    return true;
 }
 
 struct DeviceGuard {
@@ -247,9 +296,11 @@ static rk_status ensure_k(rk_state st, int nk) {
     return RK_OK;
 }
 
+// u changes: whatever k1 held is F(old u) now (an accepted FSAL try re-validates it after)
 static void swap_u(rk_state st) {
     std::swap(st->u, st->u_new);
     std::swap(st->tm_u, st->tm_unew);
+    st->k1_valid = false;
 }
 
 static void swap_k(rk_state st, int i, int j) {
@@ -311,7 +362,7 @@ static Coeffs coeffs_of(int scheme) {
     return C;
 }
 
-static bool valid_scheme(int s) { return (s >= RK_EULER && s <= RK_MIDPOINT) || is_multistep(s); }
+static bool valid_scheme(int s) { return (s >= RK_EULER && s <= RK_MODIFIED_MIDPOINT) || is_multistep(s); }
 
 struct StagePlan {
     int scheme = 0, adaptive = 0, stage = 0;
@@ -372,7 +423,21 @@ static bool is_ratio_stage(const StagePlan& p) {
 // ------------------------------------------------------------------------------------
 static bool halo_path(rk_state st) { return st->ctx->world > 1 || st->loopback; }
 
+// The collectives of a state run through NCCL on the multi-GPU path and on the one-GPU
+// loopback path; the latter uses a 1-rank communicator (ncclSend / ncclRecv to self, a 1-rank
+// allreduce), so it executes exactly the NCCL calls of the multi-GPU run.
+static bool use_nccl(rk_state st) { return st->ctx->nccl && halo_path(st); }
+
+static rk_status ensure_self_comm(rk_ctx ctx) {
+    if (ctx->nccl || ctx->world != 1) return RK_OK;
+    ncclUniqueId id;
+    NK_CTX(ctx, ncclGetUniqueId(&id));
+    NK_CTX(ctx, ncclCommInitRank(&ctx->nccl, 1, id, 0));
+    return RK_OK;
+}
+
 static rk_status ensure_halo(rk_state st) {
+    if (st->loopback) TRY(ensure_self_comm(st->ctx));
     if (!halo_path(st) || st->sendbuf) return RK_OK;
     TRY(dev_alloc(st->ctx, &st->sendbuf, 2 * plane_values(st)));
     TRY(dev_alloc(st->ctx, &st->ghostbuf, 2 * plane_values(st)));
@@ -525,13 +590,8 @@ static rk_status halo_exchange(rk_state st, cudaStream_t src) {
     }
     rk_halo_plan plan;
     TRY(rk_halo_plan_get(ctx->world, ctx->rank, &plan));
-    if (ctx->world == 1) {
-        // loopback self-exchange: my lower neighbour is myself (ghost_lo <- my hi plane)
-        const rk_halo_msg& m = plan.msg[0];
-        CK_CTX(ctx, cudaMemcpyAsync(st->ghostbuf + m.slot * pv, st->sendbuf + m.slot * pv,
-                                    sizeof(double) * m.nplanes * pv, cudaMemcpyDeviceToDevice,
-                                    ctx->comm));
-    } else {
+    if (!ctx->nccl) return fail(RK_ERR_STATE, "halo exchange without a NCCL communicator");
+    {  // world == 1 (loopback): one 2-plane message to self, [lo|hi] -> [ghost_hi|ghost_lo]
         NK_CTX(ctx, ncclGroupStart());
         for (int i = 0; i < plan.nmsg; ++i) {
             const rk_halo_msg& m = plan.msg[i];
@@ -542,6 +602,7 @@ static rk_status halo_exchange(rk_state st, cudaStream_t src) {
                 NK_CTX(ctx, ncclSend(st->sendbuf + m.slot * pv, cnt, ncclDouble, m.peer, ctx->nccl, ctx->comm));
         }
         NK_CTX(ctx, ncclGroupEnd());
+        mark_progress(ctx, ctx->comm);
     }
     if (st->timing) {
         CK_CTX(ctx, cudaEventRecord(e1, ctx->comm));
@@ -772,43 +833,26 @@ static rk_status run_pointwise(rk_state st, int scheme, double dt, int nsteps, b
 }
 
 // ------------------------------------------------------------------------------------
-// controller (host, Odeint default_step_adjuster; R-12, R-14)
+// controller (host, Odeint default_step_adjuster; R-12, R-14; SPEC's R-28), with
+// the correctly rounded pow of rk_ddmath.cuh (R-27) -- the same function the device-resident
+// loops run, so host and device decisions agree bit for bit
 // ------------------------------------------------------------------------------------
-static bool step_adjust(double E, int p, int q, double* dt) {
-    if (E > 1.0) {
-        double fac = (9.0 / 10.0) * std::pow(E, -1.0 / (double)(q - 1));
-        if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
-        *dt = *dt * fac;
-        return false;
-    }
-    if (E < 0.5) {
-        double Ec = std::pow(5.0, -(double)p);
-        if (E > Ec) Ec = E;
-        *dt = *dt * ((9.0 / 10.0) * std::pow(Ec, -1.0 / (double)p));
-    }
-    return true;
-}
-
-// SPEC's elementary controller (R-28), p = order of the propagated
-// solution: accept iff E <= 1 and always rescale, dt *= min(5, max(0.2, 0.9 E^(-1/p))); on
-// reject dt *= max(0.2, 0.9 E^(-1/(p-1))).
-static bool step_adjust_spec(double E, int p, double* dt) {
-    if (E <= 1.0) {
-        double fac = (9.0 / 10.0) * std::pow(E, -1.0 / (double)p);
-        if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
-        if (fac > 5.0) fac = 5.0;
-        *dt = *dt * fac;
-        return true;
-    }
-    double fac = (9.0 / 10.0) * std::pow(E, -1.0 / (double)(p - 1));
-    if (fac < 1.0 / 5.0) fac = 1.0 / 5.0;
-    *dt = *dt * fac;
-    return false;
+struct CtrlExp {
+    double e_rej, e_acc, emin;
+};
+static CtrlExp ctrl_exponents(int controller, int p, int q) {
+    return {controller == 1 ? -1.0 / (double)(p - 1) : -1.0 / (double)(q - 1), -1.0 / (double)p,
+            pow_dd(5.0, -(double)p)};
 }
 
 static bool adjust(int controller, double E, int p, int q, double* dt) {
-    return controller == 1 ? step_adjust_spec(E, p, dt) : step_adjust(E, p, q, dt);
+    const CtrlExp x = ctrl_exponents(controller, p, q);
+    int ok = 0;
+    *dt = step_adjust_dev(E, x.e_rej, x.e_acc, x.emin, controller, *dt, &ok);
+    return ok != 0;
 }
+
+static bool step_adjust(double E, int p, int q, double* dt) { return adjust(0, E, p, q, dt); }
 
 // Global max |u| (collective), NaN if any element is NaN: the norm_inf reduction (K4).
 static rk_status global_norm_inf(rk_state st, double* out) {
@@ -816,8 +860,10 @@ static rk_status global_norm_inf(rk_state st, double* out) {
     CK_CTX(ctx, cudaMemsetAsync(ctx->d_scratch, 0, 8, ctx->stream));
     CK_CTX(ctx, launch_norm_inf(st->u, st->alloc, ctx->d_scratch, ctx->stream, ctx->num_sms));
     st->stats.kernel_launches += 1;
-    if (ctx->world > 1)
+    if (use_nccl(st)) {
         NK_CTX(ctx, ncclAllReduce(ctx->d_scratch, ctx->d_scratch, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
+        mark_progress(ctx, ctx->stream);
+    }
     CK_CTX(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
     TRY(ctx_wait(ctx, ctx->stream));
     std::memcpy(out, ctx->h_scratch, 8);
@@ -852,7 +898,7 @@ static rk_status check_rhs(rk_state st) {
 // K5 (rk_smallgrid.cu): fixed RK steps of a small single-GPU grid in one cooperative launch
 static bool coop_path(rk_state st, int scheme) {
     return st->grid && st->rhs == RHS_GRAY_SCOTT && st->ctx->world == 1 && !st->loopback && !st->p2p &&
-           scheme >= RK_EULER && scheme <= RK_MIDPOINT && st->local * st->nx * st->ny <= st->coop_max_cells;
+           scheme >= RK_EULER && scheme <= RK_MODIFIED_MIDPOINT && st->local * st->nx * st->ny <= st->coop_max_cells;
 }
 
 static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
@@ -1048,6 +1094,7 @@ static rk_status ab_bootstrap_step(rk_state st, double dt) {
 // F at the past points of the trajectory whichever Adams method produced them.
 static rk_status ab_steps(rk_state st, int k, double dt, int64_t nsteps, bool abm = false) {
     TRY(ab_prepare(st, k, dt));
+    st->k1_valid = false;  // u moves (vectors: in place); k[0] no longer holds F(u)
     while (nsteps > 0 && st->ab_count < k - 1) {
         TRY(ab_bootstrap_step(st, dt));
         --nsteps;
@@ -1141,8 +1188,10 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
     } else {
         TRY(run_pointwise(st, scheme, dt, 1, true, atol, rtol));
     }
-    if (ctx->world > 1)
+    if (use_nccl(st)) {  // global max of E's bit pattern (loopback: a 1-rank allreduce)
         NK_CTX(ctx, ncclAllReduce(st->d_err, st->d_err, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
+        mark_progress(ctx, ctx->stream);
+    }
     CK_CTX(ctx, cudaMemcpyAsync(st->h_err, st->d_err, sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, ctx->stream));
     TRY(ctx_wait(ctx, ctx->stream));
@@ -1244,10 +1293,11 @@ static rk_status device_adaptive_loop(rk_state st, int scheme, double t0, double
         a.b[i] = C.b[i];
         a.e[i] = C.e[i];
     }
-    a.ctrl = st->controller;  // the host controller's exponents (step_adjust / step_adjust_spec)
-    a.e_rej = st->controller == 1 ? -1.0 / (double)(C.order - 1) : -1.0 / (double)(C.err_order - 1);
-    a.e_acc = -1.0 / (double)C.order;
-    a.emin = std::pow(5.0, -(double)C.order);
+    a.ctrl = st->controller;  // the host controller's exponents (adjust)
+    const CtrlExp cx = ctrl_exponents(st->controller, C.order, C.err_order);
+    a.e_rej = cx.e_rej;
+    a.e_acc = cx.e_acc;
+    a.emin = cx.emin;
     a.max_tries = st->max_tries;
     a.red = st->d_loop;
     a.res = reinterpret_cast<PwLoopResult*>(st->d_loop + 3);
@@ -1454,8 +1504,10 @@ rk_status rk_ctx_destroy(rk_ctx ctx) {
     if (!ctx) return RK_OK;
     DeviceGuard g(ctx->device);
     while (!ctx->states.empty()) rk_state_destroy(ctx->states.back());
-    cudaStreamSynchronize(ctx->stream);
+    drain_stream(ctx, ctx->stream);
     if (ctx->nccl) ncclCommDestroy(ctx->nccl);
+    for (auto e : ctx->marks) cudaEventDestroy(e);
+    for (auto e : ctx->mark_pool) cudaEventDestroy(e);
     if (ctx->comm) cudaStreamDestroy(ctx->comm);
     if (ctx->bnd) cudaStreamDestroy(ctx->bnd);
     if (ctx->capture) cudaStreamDestroy(ctx->capture);
@@ -1546,9 +1598,15 @@ rk_status rk_state_create_vector(rk_ctx ctx, int64_t n, int ncomp, rk_state* out
 rk_status rk_state_destroy(rk_state st) {
     if (!st) return RK_OK;
     DeviceGuard g(st->ctx->device);
-    cudaStreamSynchronize(st->ctx->stream);
-    if (st->ctx->comm) cudaStreamSynchronize(st->ctx->comm);
-    if (st->ctx->bnd) cudaStreamSynchronize(st->ctx->bnd);
+    bool idle = drain_stream(st->ctx, st->ctx->stream);
+    idle = drain_stream(st->ctx, st->ctx->comm) && idle;
+    idle = drain_stream(st->ctx, st->ctx->bnd) && idle;
+    if (!idle) {  // kernels still spinning after a NCCL failure: leak the device buffers
+        auto& v = st->ctx->states;
+        v.erase(std::remove(v.begin(), v.end(), st), v.end());
+        delete st;
+        return RK_OK;
+    }
     cudaFree(st->u);
     cudaFree(st->u_new);
     for (int j = 0; j < st->nk; ++j) cudaFree(st->k[j]);

@@ -362,6 +362,7 @@ int coop_last_stage(int scheme) {
     case 3: return coop_mask<3>().last;
     case 4: return coop_mask<4>().last;
     case 5: return coop_mask<5>().last;
+    case 6: return coop_mask<6>().last;
     default: return -1;
     }
 }
@@ -383,6 +384,7 @@ cudaError_t launch_gs_coop(int scheme, const GsCoopArgs& a, cudaStream_t st, int
     case 3: return launch_coop_s<3>(a, st, device);
     case 4: return launch_coop_s<4>(a, st, device);
     case 5: return launch_coop_s<5>(a, st, device);
+    case 6: return launch_coop_s<6>(a, st, device);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -725,6 +725,7 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
     case 8: return launch_stage_i<4, 0>(stage, a, grid, st);
     case 9: return launch_stage_i<4, 1>(stage, a, grid, st);
     case 10: return launch_stage_i<5, 0>(stage, a, grid, st);
+    case 12: return launch_stage_i<6, 0>(stage, a, grid, st);
     case 22: return launch_one<11, 0, 0>(a, grid, st);  // Adams–Bashforth 1..8: one launch/step
     case 24: return launch_one<12, 0, 0>(a, grid, st);
     case 26: return launch_one<13, 0, 0>(a, grid, st);

@@ -79,8 +79,13 @@ __host__ __device__ constexpr Tableau tableau_of(int scheme) {
              {41, 840}, {41, 840}},
             {{41, 840}, {0, 1}, {0, 1}, {0, 1}, {0, 1}, {34, 105}, {9, 35}, {9, 35}, {9, 280}, {9, 280},
              {41, 840}, {0, 1}, {0, 1}}};
-    case 5:  // modified midpoint as the explicit midpoint rule (R-22)
+    case 5:  // explicit midpoint rule, order 2 (R-22)
         return Tableau{2, 2, 0, {{0, 1}, {1, 2}}, {{}, {{1, 2}}}, {{0, 1}, {1, 1}}, {{0, 1}}};
+    case 6:  // modified midpoint = Odeint's modified_midpoint, Gragg with 2 substeps
+             // h = dt/2: x1 = u + hF(u), x2 = u + 2hF(x1), u_new = (x1 + x2 + hF(x2))/2, i.e. the
+             // 3-stage Butcher form c = (0, 1/2, 1), a21 = 1/2, a32 = 1, b = (1/4, 1/2, 1/4) (R-22)
+        return Tableau{3, 2, 0, {{0, 1}, {1, 2}, {1, 1}}, {{}, {{1, 2}}, {{0, 1}, {1, 1}}},
+                       {{1, 4}, {1, 2}, {1, 4}}, {{0, 1}}};
     default:
         return Tableau{0, 0, 0, {}, {}, {}, {}};
     }

@@ -54,7 +54,8 @@ def test_partition_rejects_empty_ranks(rk):
     assert e.value.status == "RK_ERR_ARG"
 
 
-@pytest.mark.parametrize("name", ["euler", "rk4", "cash_karp54", "dopri5", "rkf78", "midpoint"])
+@pytest.mark.parametrize("name", ["euler", "rk4", "cash_karp54", "dopri5", "rkf78", "midpoint",
+                                  "modified_midpoint"])
 def test_tableau_bitwise_equal_to_oracle(rk, name):
     lt = rk.tableau(name)
     ot = oracle.tableau(oracle.SCHEMES[name])

@@ -54,3 +54,5 @@ def test_gpu_arm_json_line():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 64 ** 3 * 2 * 8
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert "rk4" in d["extra"] and d["extra"]["rk4"]["value"] > 0
+    assert rf["rk4_512"]["value"] > 0 and rf["rk4_512"]["frac"] > 0
+    assert d["config"]["accepted_per_step"] > 0

@@ -13,7 +13,7 @@ import rk_inputs
 pytestmark = pytest.mark.gpu
 
 OS = oracle.SCHEMES
-FUSED = ["rk4", "midpoint"]
+FUSED = ["rk4", "midpoint", "modified_midpoint"]
 
 
 @pytest.fixture(scope="module")
