@@ -60,7 +60,8 @@ __host__ __device__ constexpr bool b_nz(int S, int j) { return rat_nz(tableau_of
 template <int S>
 struct FCfg {
     static constexpr int L = tableau_of(S).s;
-    static constexpr int UW = FX + 2 * L + 2;  // u box: padded columns x0-L .. (even start, 16 B)
+    static constexpr int XL = (L + 1) / 2 * 2;  // left margin rounded up to even (16-byte TMA start)
+    static constexpr int UW = FX + 2 * XL + 2;  // u box: padded columns x0-XL .. (even start, 16 B)
     static constexpr int UH = FY + 2 * L;
     static constexpr int UBOX = UW * UH;       // cells per component
     static constexpr int UBYTES = 2 * UBOX * 8;
@@ -160,7 +161,7 @@ __device__ __forceinline__ void gs_rhs_q(const double* v0, int cs, int pitch, co
 template <int S>
 __global__ void __launch_bounds__(FNT, 1) gs_fused_kernel(const __grid_constant__ GsFusedArgs a) {
     using C = FCfg<S>;
-    constexpr int L = C::L, UW = C::UW, UBOX = C::UBOX, R = C::R, NEED = C::NEED, UQ = NEED;
+    constexpr int L = C::L, XL = C::XL, UW = C::UW, UBOX = C::UBOX, R = C::R, NEED = C::NEED, UQ = NEED;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::woff(L + 1));
 
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(FNT, 1) gs_fused_kernel(const __grid_constant_
     // own cell
     const int lx = tid % FX, ly = tid / FX;
     const bool own = x0 + lx < G.nx && y0 + ly < G.ny;
-    const int o_ub = (lx + L + 1) + (ly + L) * UW;
+    const int o_ub = (lx + XL + 1) + (ly + L) * UW;
     int o_w[L + 1];  // window position of the own cell in Y_s's window (s >= 2)
 #pragma unroll
     for (int s = 2; s <= L; ++s) o_w[s] = (lx + C::hw(s)) + (ly + C::hw(s)) * C::ww(s);
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(FNT, 1) gs_fused_kernel(const __grid_constant_
         rg_on[s] = tid < C::nring(r);
         int rx = 0, ry = 0;
         if (rg_on[s]) ring_coord(tid, r, rx, ry);
-        rg_ub[s] = (rx + L + 1) + (ry + L) * UW;
+        rg_ub[s] = (rx + XL + 1) + (ry + L) * UW;
         rg_wc[s] = s >= 2 ? (rx + C::hw(s)) + (ry + C::hw(s)) * C::ww(s) : 0;
         rg_wn[s] = (rx + C::hw(s + 1)) + (ry + C::hw(s + 1)) * C::ww(s + 1);
     }
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(FNT, 1) gs_fused_kernel(const __grid_constant_
 #pragma unroll
     for (int k = 0; k < C::NFIX; ++k) {
         const int p = tid + k * FNT;
-        const int x = x0 - L - 1 + p % UW, y = y0 - L + p / UW;
+        const int x = x0 - XL - 1 + p % UW, y = y0 - L + p / UW;
         // the padded layout holds cells x in [0, nx), y in [-1, ny] and y in [0, ny), x in
         // [-1, nx] (not the ring corners); everything else wraps
         const bool held = (x >= 0 && x < G.nx && y >= -1 && y <= G.ny) || (y >= 0 && y < G.ny && x >= -1 && x <= G.nx);
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(FNT, 1) gs_fused_kernel(const __grid_constant_
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
             "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_addr(uslot(i))),
-            "l"(reinterpret_cast<uint64_t>(&a.tm_u)), "r"(smem_addr(b)), "r"(x0 - L), "r"(y0 - L + 1), "r"(0),
+            "l"(reinterpret_cast<uint64_t>(&a.tm_u)), "r"(smem_addr(b)), "r"(x0 - XL), "r"(y0 - L + 1), "r"(0),
             "r"(plane_of(i))
             : "memory");
     };
@@ -453,7 +454,8 @@ cudaError_t encode_fused_map(CUtensorMap* map, const double* base, const GridGeo
     }
     const cuuint64_t dims[4] = {(cuuint64_t)g.P, (cuuint64_t)(g.ny + 2), 2, (cuuint64_t)nplanes};
     const cuuint64_t strides[3] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.cs * 8, (cuuint64_t)g.ps * 8};
-    const cuuint32_t box[4] = {(cuuint32_t)(FX + 2 * L + 2), (cuuint32_t)(FY + 2 * L), 2, 1};
+    const int XL = (L + 1) / 2 * 2;  // FCfg<S>::XL
+    const cuuint32_t box[4] = {(cuuint32_t)(FX + 2 * XL + 2), (cuuint32_t)(FY + 2 * L), 2, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -126,6 +126,8 @@ struct GsStageArgs {
     double* out_u;
     unsigned long long* errmax;
     double dt, atol, rtol;
+    const double* dtp;               // non-null (device-resident try loop): this try's dt on the
+                                     // device; g/beta/delta/g2 then hold the raw coefficients
     double d1, d2, F, FK, inv_h2;
     int has_glo, has_ghi;
     int z_lo, z_hi;                  // output planes [z_lo, z_hi) (zmode 0)

@@ -234,6 +234,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
 
     const GridGeom& G = a.geo;
     const int tid = threadIdx.x;
+    // Coefficients: the host passes dt*a_ij (etc.) pre-scaled and dtp == null (scale 1.0: x*1 is
+    // exact), or -- in the device-resident try loop, where dt changes on the device -- the raw
+    // Butcher coefficients and dtp -> this try's dt: fl(dt*a_ij) is the same single rounding the
+    // host would do, so both give the same bits.
+    const double dsc = a.dtp ? *a.dtp : 1.0;
+    const double dtv = a.dtp ? *a.dtp : a.dt;
     const int ntx = (G.nx + TX - 1) / TX;
     const int x0 = (int)(blockIdx.x % ntx) * TX, y0 = (int)(blockIdx.x / ntx) * TH;
     const int w = min(TX, G.nx - x0), hg = min(TH, G.ny - y0);
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
 #pragma unroll
             for (int s = 0; s < NS; ++s)
                 if (P.gnz[s])
-                    v = add(v, mul(a.g[s], reinterpret_cast<const double*>(st + LY.off[s])[c * BOX + hp]));
+                    v = add(v, mul(mul(dsc, a.g[s]), reinterpret_cast<const double*>(st + LY.off[s])[c * BOX + hp]));
         }
         return v;
     };
@@ -329,14 +335,14 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                 double wv = ub;
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
-                    if (P.bnz[s]) wv = add(wv, mul(a.beta[s], sval(st, s, c, r)));
+                    if (P.bnz[s]) wv = add(wv, mul(mul(dsc, a.beta[s]), sval(st, s, c, r)));
                 es.w[c] = wv;
             }
             if constexpr (AHEAD) {
                 double yv = ub;
 #pragma unroll
                 for (int s = 0; s < NS; ++s)
-                    if (P.anz2[s]) yv = add(yv, mul(a.g2[s], sval(st, s, c, r)));
+                    if (P.anz2[s]) yv = add(yv, mul(mul(dsc, a.g2[s]), sval(st, s, c, r)));
                 es.y2[c] = yv;
             }
             if constexpr (ESUM && ESLOT) {
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
 #pragma unroll
                 for (int s = 0; s < NS; ++s) {
                     if (!P.dnz[s]) continue;
-                    const double t = mul(a.delta[s], sval(st, s, c, r));
+                    const double t = mul(mul(dsc, a.delta[s]), sval(st, s, c, r));
                     e = first ? t : add(e, t);
                     first = false;
                 }
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                     es.d[c] = fabs(uu);  // completed with |u_new| in the epilogue
                 } else {
                     const double k1 = sval(st, P.den_k1, c, r);
-                    es.d[c] = add(a.atol, mul(a.rtol, add(fabs(uu), mul(a.dt, fabs(k1)))));
+                    es.d[c] = add(a.atol, mul(a.rtol, add(fabs(uu), mul(dtv, fabs(k1)))));
                 }
             }
         }
@@ -486,25 +492,25 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                 if constexpr (AB) {
                     // u_{n+1} = u_n (+) g_0 f (+) g_1 h_0 (+) ... newest first (R-24, R-26);
                     // AB: f = f_n, h = f_{n-1}...; ABM: f = F(u_p), h = f_n, f_{n-1}...
-                    double wv = add(ec.w[c], mul(a.beta_new, f[c]));
+                    double wv = add(ec.w[c], mul(mul(dsc, a.beta_new), f[c]));
 #pragma unroll
                     for (int s = 0; s < NS; ++s)
-                        if (P.bnz[s]) wv = add(wv, mul(a.beta[s], ec.h[s][c]));
+                        if (P.bnz[s]) wv = add(wv, mul(mul(dsc, a.beta[s]), ec.h[s][c]));
                     store_cell(a.out_u, G, slice, cell[r], wv);
                 }
                 double unew = 0.0;
                 if constexpr (FIN) {
-                    unew = P.bnew ? add(ec.w[c], mul(a.beta_new, f[c])) : ec.w[c];
+                    unew = P.bnew ? add(ec.w[c], mul(mul(dsc, a.beta_new), f[c])) : ec.w[c];
                     store_cell(a.out_u, G, slice, cell[r], unew);
                 }
                 if constexpr (AHEAD) {  // Y_F (read with its ring by stage F), W, E
-                    store_cell(a.out_k, G, slice, cell[r], P.a2new ? add(ec.y2[c], mul(a.g2_new, f[c])) : ec.y2[c]);
-                    store_cell(a.out_w, G, slice, cell[r], P.bnew ? add(ec.w[c], mul(a.beta_new, f[c])) : ec.w[c]);
+                    store_cell(a.out_k, G, slice, cell[r], P.a2new ? add(ec.y2[c], mul(mul(dsc, a.g2_new), f[c])) : ec.y2[c]);
+                    store_cell(a.out_w, G, slice, cell[r], P.bnew ? add(ec.w[c], mul(mul(dsc, a.beta_new), f[c])) : ec.w[c]);
                 }
                 double e = ec.e[c];
                 if constexpr (ESUM || EPI == EPI_TAIL_ERR || AHEAD_E) {
                     if constexpr (DNEW) {
-                        const double t = mul(a.delta_new, f[c]);
+                        const double t = mul(mul(dsc, a.delta_new), f[c]);
                         e = HAS_PREV_E ? add(e, t) : t;
                     }
                 }
@@ -568,6 +574,7 @@ template <int NY>
 __global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, double* __restrict__ dst0,
                                                       double* __restrict__ dst1, const P2pSync sync) {
     p2p_wait(sync);  // P2P: the neighbours have consumed what the previous use of dst held
+    const double dsc = a.dtp ? *a.dtp : 1.0;  // as in gs_stage_kernel
     const int64_t ps = a.geo.ps, total = 2 * ps;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -575,7 +582,7 @@ __global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, doubl
         const int64_t base = (sel ? (int64_t)(a.geo.nzl - 1) : 0) * ps + rest;
         double v = __ldg(a.base + base);
 #pragma unroll
-        for (int s = 0; s < NY; ++s) v = add(v, mul(a.g[s], __ldg(a.slot[s] + base)));
+        for (int s = 0; s < NY; ++s) v = add(v, mul(mul(dsc, a.g[s]), __ldg(a.slot[s] + base)));
         (sel ? dst1 : dst0)[rest] = v;
     }
     p2p_notify(sync);  // P2P: ghost planes stored -> neighbours may read them
