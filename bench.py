@@ -268,7 +268,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
-    ap.add_argument("--legs", default="adaptive,rk4,repeats,try_loop,halo,exposed,strong,strong_emul,rk4_native,rk4_k6,exp512,small,e2e,cpu",
+    ap.add_argument("--legs", default="adaptive,rk4,repeats,try_loop,device_loop,halo,exposed,strong,strong_emul,rk4_native,rk4_k6,exp512,small,e2e,cpu",
                     help="comma list of legs (profiling runs use e.g. --legs rk4)")
     ap.add_argument("--no-extra", action="store_true", help="same as --legs adaptive")
     ap.add_argument("--overlap", type=int, default=1, help="halo exchange overlapped (N > 1)")
@@ -680,6 +680,45 @@ def main():
             v.close()
         return out
 
+    def device_loop_leg():
+        # f3: the whole integrate_adaptive as one CUDA-graph launch (RK_OPT_DEVICE_LOOP: no host
+        # round trip per try) vs the host-driven try loop, at 512^3 and on the G = 8 strong-
+        # scaling share (512 x 512 x 64 slab, one GPU, no exchange), DOPRI5 tol 1e-6, [0, 20]
+        out = {}
+        for nzl in (n, n // 8):
+            g = ctx.grid(n, n, nzl, 2) if nzl != n else st
+            if g is not st:
+                g.set_rhs_gray_scott(h=H)
+            # the G = 8 share holding the middle of the IC cube (non-trivial dynamics)
+            ug = u0_dev if g is st else torch.from_numpy(
+                rk_inputs.gray_scott_ic(n, n, n, seed=42, z0=(n - nzl) // 2, nzl=nzl, zblocks=1)).cuda(local)
+            res = {}
+            for dl in (0, 1):
+                g.set_option(rk.OPT_DEVICE_LOOP, dl)
+                g.set(ug)
+                g.integrate_adaptive("dopri5", 0.0, T1, 1.0, TOL, TOL)  # warm-up (and graph build)
+                ms, tries, acc = [], 0, 0
+                for _ in range(max(3, args.warmup)):
+                    g.set(ug)
+                    barrier()
+                    ev0.record(stream)
+                    a, r = g.integrate_adaptive("dopri5", 0.0, T1, 1.0, TOL, TOL)
+                    ev1.record(stream)
+                    barrier()
+                    ms.append(max_over_ranks(ev0.elapsed_time(ev1)))
+                    tries, acc = a + r, a
+                m = statistics.median(ms)
+                res["device_loop" if dl else "host_loop"] = {
+                    "value": n * n * nzl * acc / (m / 1e3), "unit": "cell-updates/s", "ms_per_integration": m,
+                    "ms_per_try": m / tries, "tries": tries, "accepted": acc}
+            g.set_option(rk.OPT_DEVICE_LOOP, 0)
+            if g is not st:
+                g.close()
+            res["speedup"] = res["host_loop"]["ms_per_integration"] / res["device_loop"]["ms_per_integration"]
+            out[f"nz{nzl}"] = res
+        out["config"] = "DOPRI5 tol 1e-6, t in [0, 20], dt0 1; median of 3 integrate_adaptive calls"
+        return out
+
     def strong_emul_leg():
         # configs[3] on ONE GPU: the per-GPU share of a G-way strong-scaling run (512 x 512 x
         # 512/G slab of the 512^3 IC) through the multi-GPU stage path in loopback mode (pack,
@@ -858,6 +897,8 @@ def main():
             extra["rk4_p2p"] = run_leg(rk4_leg, args.overlap, "rk4", 1, 0)
     if "exposed" in legs:
         extra["exposed_halo"] = run_leg(exposed_halo_leg)
+    if "device_loop" in legs and world == 1:
+        extra["device_loop"] = run_leg(device_loop_leg)
     if "strong_emul" in legs and world == 1:
         extra["strong_emul"] = run_leg(strong_emul_leg)
     if "strong" in legs and world > 1:

@@ -256,6 +256,8 @@ struct rk_state_s {
     int64_t since_check = 0;     // steps since the last finiteness check
     int64_t coop_max_cells = 1 << 18;  // RK_OPT_COOP_MAX_CELLS: persistent-step path up to here
     bool fused = false;          // RK_OPT_FUSED_STEP: K6 whole-step launches (RK4, midpoint)
+    const double* gl_dtp = nullptr;  // set while capturing the device-resident try loop (GLoop)
+    struct GraphLoop* gloop = nullptr;
     // stats
     rk_stats stats{};
     std::vector<TimedPair> pending;
@@ -482,6 +484,7 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     a.out_e = p.sp.out_e >= 0 ? st->k[p.sp.out_e] : nullptr;
     a.errmax = st->d_err;
     a.dt = dt;
+    a.dtp = st->gl_dtp;
     a.atol = atol;
     a.rtol = rtol;
     a.d1 = st->d1;
@@ -1362,6 +1365,323 @@ static rk_status device_adaptive_loop(rk_state st, int scheme, double t0, double
     }
 }
 
+// ------------------------------------------------------------------------------------
+// Device-resident adaptive loop for grids beyond the K5 size (RK_OPT_DEVICE_LOOP):
+// the whole integrate_adaptive as ONE CUDA-graph launch with a conditional WHILE node.  Body:
+//   select kernel (sets the SWITCH value: buffer parity x whether k1 must be evaluated)
+//   -> SWITCH over 4 captured try bodies (the stage launches of one try for each u/u_new (and
+//      FSAL k1/k7) buffer assignment, with and without stage 1), dt read on the device (dtp)
+//   -> controller kernel (R-12 / R-28 with the correctly rounded pow, R-16 truncation, stall /
+//      underflow / NaN rules, accept = flip the parity) which sets the WHILE condition.
+// No host round trip per try; results equal the host loop bit for bit (same kernels, the same
+// fl(dt*a_ij), the same controller function).
+// ------------------------------------------------------------------------------------
+struct GLoopDev {  // device-resident loop state
+    double t, dt, t1, dt_try, last_E, last_dt;
+    long long acc, rej, k1_evals;
+    int tries, status, parity, need_k1;
+};
+struct GLoopParams {
+    double e_rej, e_acc, emin;
+    int ctrl, max_tries, fsal;
+};
+
+__global__ void gloop_select_kernel(const GLoopDev* s, cudaGraphConditionalHandle hs) {
+    cudaGraphSetConditional(hs, (unsigned)(s->parity * 2 + s->need_k1));
+}
+
+__global__ void gloop_ctrl_kernel(GLoopDev* s, const unsigned long long* err, GLoopParams p,
+                                  cudaGraphConditionalHandle hw) {
+    const double E = __longlong_as_double((long long)*err);
+    if (s->need_k1) s->k1_evals += 1;
+    s->last_E = E;
+    if (isnan(E)) {  // R-14: NaN -> RK_ERR_DIVERGED
+        s->status = RK_ERR_DIVERGED;
+        cudaGraphSetConditional(hw, 0);
+        return;
+    }
+    int ok = 0;
+    double dt = step_adjust_dev(E, p.e_rej, p.e_acc, p.emin, p.ctrl, s->dt_try, &ok);
+    s->last_dt = dt;
+    double t = s->t;
+    if (ok) {
+        t = t + s->dt_try;
+        s->t = t;
+        s->acc += 1;
+        s->parity ^= 1;
+        s->need_k1 = p.fsal ? 0 : 1;
+        s->tries = 0;
+        if (!(s->t1 - t > DBL_EPSILON)) {  // R-16: t1 reached
+            s->dt = dt;
+            cudaGraphSetConditional(hw, 0);
+            return;
+        }
+        if ((t + dt) - s->t1 > DBL_EPSILON) dt = s->t1 - t;
+    } else {
+        s->rej += 1;
+        s->need_k1 = 0;  // k1 = F(u) of this u is valid (FSAL or evaluated by this try)
+        if (++s->tries >= p.max_tries) {
+            s->dt = dt;
+            s->status = RK_ERR_STALL;
+            cudaGraphSetConditional(hw, 0);
+            return;
+        }
+    }
+    s->dt = dt;
+    if (dt < 16.0 * DBL_EPSILON * fmax(fabs(t), 1.0)) {
+        s->status = RK_ERR_DT_UNDERFLOW;
+        cudaGraphSetConditional(hw, 0);
+        return;
+    }
+    s->dt_try = dt;
+    cudaGraphSetConditional(hw, 1);
+}
+
+struct GraphLoop {
+    cudaGraphExec_t exec = nullptr;
+    GLoopDev* dev = nullptr;
+    // what the captured launches baked in
+    int scheme = -1, ctrl = -1, fsal_k = -1, max_tries = 0;
+    double atol = 0, rtol = 0, d1 = 0, d2 = 0, F = 0, K = 0, h = 0;
+    double* bu[2] = {};   // parity p: u = bu[p], u_new = bu[1-p]
+    Maps mu[2]{};
+    double* bk[2] = {};   // FSAL, parity p: k1 = bk[p], k7 = bk[1-p]
+    Maps mk[2]{};
+    double* k[13] = {};   // every k buffer pointer at capture
+    int nk = 0;
+    int64_t try_bytes = 0, k1_bytes = 0;  // algorithmic bytes of stages 2..s / of stage 1
+    int nstages = 0;
+};
+
+static void gloop_destroy(rk_state st) {
+    GraphLoop* g = st->gloop;
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    cudaFree(g->dev);
+    delete g;
+    st->gloop = nullptr;
+}
+
+static bool gloop_path(rk_state st) {
+    return st->device_loop && st->grid && st->rhs == RHS_GRAY_SCOTT && !halo_path(st) &&
+           st->check_finite == 0 && !st->timing;
+}
+
+static int64_t plan_stage_bytes(rk_state st, const StagePlan& p) {
+    const int64_t arrays = 1 + p.sp.nslots + (p.sp.out_k >= 0 ? 1 : 0) + (p.sp.writes_u ? 1 : 0) +
+                           (p.sp.out_w >= 0 ? 1 : 0) + (p.sp.out_e >= 0 ? 1 : 0);
+    return st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double) * arrays;
+}
+
+static void gloop_assign(rk_state st, GraphLoop* g, int parity) {
+    st->u = g->bu[parity];
+    st->u_new = g->bu[1 - parity];
+    st->tm_u = g->mu[parity];
+    st->tm_unew = g->mu[1 - parity];
+    if (g->fsal_k > 0) {
+        st->k[0] = g->bk[parity];
+        st->k[g->fsal_k] = g->bk[1 - parity];
+        st->tm_k[0] = g->mk[parity];
+        st->tm_k[g->fsal_k] = g->mk[1 - parity];
+    }
+}
+
+static bool gloop_matches(rk_state st, const GraphLoop* g, int scheme, double atol, double rtol) {
+    if (!g || !g->exec || g->scheme != scheme || g->ctrl != st->controller || g->max_tries != st->max_tries ||
+        g->atol != atol || g->rtol != rtol ||
+        g->d1 != st->d1 || g->d2 != st->d2 || g->F != st->F || g->K != st->K || g->h != st->h || g->nk != st->nk)
+        return false;
+    if (!((st->u == g->bu[0] && st->u_new == g->bu[1]) || (st->u == g->bu[1] && st->u_new == g->bu[0]))) return false;
+    for (int j = 0; j < st->nk; ++j) {
+        if (g->fsal_k > 0 && (j == 0 || j == g->fsal_k)) {
+            if (st->k[j] != g->bk[0] && st->k[j] != g->bk[1]) return false;
+        } else if (st->k[j] != g->k[j]) {
+            return false;
+        }
+    }
+    return true;
+}
+
+static rk_status gloop_build(rk_state st, int scheme, double atol, double rtol) {
+    rk_ctx ctx = st->ctx;
+    gloop_destroy(st);
+    const int adaptive = st->controller == 1 ? 2 : 1;
+    const std::vector<StagePlan> plan = build_plan(scheme, adaptive, 1.0);  // raw coefficients
+    TRY(ensure_k(st, plan_num_k(plan)));
+    GraphLoop* g = new GraphLoop();
+    st->gloop = g;
+    g->scheme = scheme;
+    g->ctrl = st->controller;
+    g->max_tries = st->max_tries;
+    g->atol = atol;
+    g->rtol = rtol;
+    g->d1 = st->d1;
+    g->d2 = st->d2;
+    g->F = st->F;
+    g->K = st->K;
+    g->h = st->h;
+    g->nk = st->nk;
+    g->nstages = (int)plan.size();
+    g->fsal_k = plan.back().sp.epi == EPI_TAIL_ERR ? plan.back().sp.out_k : -1;
+    g->bu[0] = st->u;
+    g->bu[1] = st->u_new;
+    g->mu[0] = st->tm_u;
+    g->mu[1] = st->tm_unew;
+    if (g->fsal_k > 0) {
+        g->bk[0] = st->k[0];
+        g->bk[1] = st->k[g->fsal_k];
+        g->mk[0] = st->tm_k[0];
+        g->mk[1] = st->tm_k[g->fsal_k];
+    }
+    for (int j = 0; j < st->nk; ++j) g->k[j] = st->k[j];
+    for (const StagePlan& p : plan) (p.stage == 0 ? g->k1_bytes : g->try_bytes) += plan_stage_bytes(st, p);
+    CK_CTX(ctx, cudaMalloc((void**)&g->dev, sizeof(GLoopDev)));
+    if (!ctx->capture) CK_CTX(ctx, cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking));
+
+    cudaGraph_t graph = nullptr;
+    CK_CTX(ctx, cudaGraphCreate(&graph, 0));
+    struct GraphGuard {
+        cudaGraph_t g;
+        ~GraphGuard() { if (g) cudaGraphDestroy(g); }
+    } guard{graph};
+    cudaGraphConditionalHandle hw, hs;
+    CK_CTX(ctx, cudaGraphConditionalHandleCreate(&hw, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams wp{};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = hw;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CK_CTX(ctx, cudaGraphAddNode(&wnode, graph, nullptr, 0, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+    CK_CTX(ctx, cudaGraphConditionalHandleCreate(&hs, body, 0, 0));
+    // select -> switch -> controller
+    cudaGraphNode_t sel, sw, ctl;
+    {
+        GLoopDev* dv = g->dev;
+        void* args[] = {&dv, &hs};
+        cudaKernelNodeParams kp{};
+        kp.func = (void*)gloop_select_kernel;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args;
+        CK_CTX(ctx, cudaGraphAddKernelNode(&sel, body, nullptr, 0, &kp));
+    }
+    cudaGraphNodeParams sp{};
+    sp.type = cudaGraphNodeTypeConditional;
+    sp.conditional.handle = hs;
+    sp.conditional.type = cudaGraphCondTypeSwitch;
+    sp.conditional.size = 4;
+    CK_CTX(ctx, cudaGraphAddNode(&sw, body, &sel, 1, &sp));
+    // the four try bodies, captured with this state's launch code
+    const bool k1_save = st->k1_valid;
+    const rk_stats stats_save = st->stats;
+    const cudaStream_t work = ctx->stream;
+    const double* dtp = &g->dev->dt_try;
+    rk_status rc = RK_OK;
+    for (int j = 0; j < 4 && rc == RK_OK; ++j) {
+        const int parity = j / 2, need_k1 = j % 2;
+        gloop_assign(st, g, parity);
+        cudaError_t ce = cudaStreamBeginCaptureToGraph(ctx->capture, sp.conditional.phGraph_out[j], nullptr, nullptr, 0,
+                                                       cudaStreamCaptureModeThreadLocal);
+        if (ce != cudaSuccess) {
+            ctx->poisoned = RK_ERR_CUDA;
+            rc = fail(RK_ERR_CUDA, "capture of the try body: %s", cudaGetErrorString(ce));
+            break;
+        }
+        ctx->stream = ctx->capture;
+        st->gl_dtp = dtp;
+        st->k1_valid = need_k1 == 0;
+        rc = run_grid_plan(st, plan, 1.0, atol, rtol);
+        st->gl_dtp = nullptr;
+        ctx->stream = work;
+        cudaGraph_t out = nullptr;
+        ce = cudaStreamEndCapture(ctx->capture, &out);
+        if (rc == RK_OK && ce != cudaSuccess) {
+            ctx->poisoned = RK_ERR_CUDA;
+            rc = fail(RK_ERR_CUDA, "capture of the try body: %s", cudaGetErrorString(ce));
+        }
+    }
+    gloop_assign(st, g, 0);  // bu[0] / bk[0] are the assignment found at the start of the build
+    st->stats = stats_save;
+    st->k1_valid = k1_save;
+    TRY(rc);
+    {
+        GLoopDev* dv = g->dev;
+        unsigned long long* err = st->d_err;
+        GLoopParams prm{};
+        const Coeffs C = coeffs_of(scheme);
+        const CtrlExp cx = ctrl_exponents(st->controller, C.order, C.err_order);
+        prm.e_rej = cx.e_rej;
+        prm.e_acc = cx.e_acc;
+        prm.emin = cx.emin;
+        prm.ctrl = st->controller;
+        prm.max_tries = st->max_tries;
+        prm.fsal = g->fsal_k > 0 ? 1 : 0;
+        void* args[] = {&dv, &err, &prm, &hw};
+        cudaKernelNodeParams kp{};
+        kp.func = (void*)gloop_ctrl_kernel;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args;
+        CK_CTX(ctx, cudaGraphAddKernelNode(&ctl, body, &sw, 1, &kp));
+    }
+    CK_CTX(ctx, cudaGraphInstantiate(&g->exec, graph, 0));
+    return RK_OK;
+}
+
+static rk_status graph_adaptive_loop(rk_state st, int scheme, double t0, double t1, double dt0, double atol,
+                                     double rtol, int64_t* accepted, int64_t* rejected) {
+    NvtxRange nv("rk device-resident try loop (graph)");
+    rk_ctx ctx = st->ctx;
+    ab_invalidate(st);
+    if (accepted) *accepted = 0;
+    if (rejected) *rejected = 0;
+    double t = t0, dt = dt0;
+    if (!(t1 - t > DBL_EPSILON)) return RK_OK;
+    if ((t + dt) - t1 > DBL_EPSILON) dt = t1 - t;
+    if (dt < 16.0 * DBL_EPSILON * std::max(std::fabs(t), 1.0)) return fail(RK_ERR_DT_UNDERFLOW, "dt underflow at t=%.17g", t);
+    if (!gloop_matches(st, st->gloop, scheme, atol, rtol)) TRY(gloop_build(st, scheme, atol, rtol));
+    GraphLoop* g = st->gloop;
+    const int p0 = st->u == g->bu[0] ? 0 : 1;
+    bool need_k1 = !st->k1_valid;
+    if (g->fsal_k > 0 && st->k[0] != g->bk[p0]) need_k1 = true;  // a valid k1 sits in the other buffer
+    gloop_assign(st, g, p0);
+    GLoopDev h{};
+    h.t = t;
+    h.dt = dt;
+    h.t1 = t1;
+    h.dt_try = dt;
+    h.parity = p0;
+    h.need_k1 = need_k1 ? 1 : 0;
+    CK_CTX(ctx, cudaMemcpyAsync(g->dev, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+    CK_CTX(ctx, cudaGraphLaunch(g->exec, ctx->stream));
+    CK_CTX(ctx, cudaMemcpyAsync(&h, g->dev, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+    TRY(ctx_wait(ctx, ctx->stream));
+    gloop_assign(st, g, h.parity);
+    st->k1_valid = h.need_k1 == 0;
+    const int64_t tries = h.acc + h.rej;
+    st->stats.tries += tries;
+    st->stats.accepted += h.acc;
+    st->stats.rejected += h.rej;
+    const int64_t launches = tries * (g->nstages - 1) + h.k1_evals;
+    st->stats.stage_launches += launches;
+    st->stats.rhs_evals += launches;
+    st->stats.kernel_launches += launches + 2 * tries;
+    st->stats.stage_bytes += tries * g->try_bytes + h.k1_evals * g->k1_bytes;
+    st->stats.last_err_ratio = h.last_E;
+    st->stats.last_dt = h.last_dt;
+    if (accepted) *accepted = h.acc;
+    if (rejected) *rejected = h.rej;
+    switch (h.status) {
+    case 0: return RK_OK;
+    case RK_ERR_DIVERGED: return fail(RK_ERR_DIVERGED, "non-finite error ratio at t=%.17g dt=%.17g", h.t, h.dt_try);
+    case RK_ERR_DT_UNDERFLOW: return fail(RK_ERR_DT_UNDERFLOW, "dt underflow at t=%.17g", h.t);
+    case RK_ERR_STALL: return fail(RK_ERR_STALL, "more than %d tries at t=%.17g", st->max_tries, h.t);
+    default: return fail(RK_ERR_CUDA, "device loop status %d", h.status);
+    }
+}
+
 // ====================================================================================
 // C-ABI
 // ====================================================================================
@@ -1607,6 +1927,7 @@ rk_status rk_state_destroy(rk_state st) {
         delete st;
         return RK_OK;
     }
+    gloop_destroy(st);
     cudaFree(st->u);
     cudaFree(st->u_new);
     for (int j = 0; j < st->nk; ++j) cudaFree(st->k[j]);
@@ -1880,6 +2201,7 @@ rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double
         TRY(device_adaptive_loop(st, scheme, t0, t1, dt0, atol, rtol, accepted, rejected));
         return finite_check(st, 0, t1, true);
     }
+    if (gloop_path(st)) return graph_adaptive_loop(st, scheme, t0, t1, dt0, atol, rtol, accepted, rejected);
     int64_t acc = 0, rej = 0;
     double t = t0, dt = dt0;
     rk_status rc = RK_OK;
