@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define RK_ABI_VERSION 2
+#define RK_ABI_VERSION 3
 #define RK_UNIQUE_ID_BYTES 128
 
 typedef struct rk_ctx_s* rk_ctx;     /* one per rank: device, streams, NCCL communicator */
@@ -108,19 +108,27 @@ typedef enum {
     RK_OPT_USE_GRAPH = 5,    /* 1: rk_integrate_const of a grid (world == 1, no loopback, >= 5
                                 steps) replays pairs of steps from one captured CUDA graph
                                 (SURVEY f3): identical results, no per-launch host cost   */
-    RK_OPT_DEVICE_LOOP = 6,  /* 1: rk_integrate_adaptive of a vector state, or of a grid within
-                                RK_OPT_COOP_MAX_CELLS (no halo path), on one GPU runs as one
-                                cooperative kernel: tries, error max, controller and
-                                accept/reject on the device, no host sync per try (
-                                DESIGN.md R-27).  Same results; else the host loop is used.   */
-    RK_OPT_HALO_P2P = 7,     /* grid, halo path (world > 1 or HALO_LOOPBACK): 1 replaces the
-                                NCCL exchange by peer-to-peer stores -- the pack kernel writes
-                                Y_i's boundary planes straight into the neighbours' (double-
-                                buffered) ghost planes through CUDA IPC mappings over NVLink
-                                and raises their ready flags; the boundary launch waits on them
-                                and hands the buffers back.  Collective: set it on
-                                every rank; the first stage maps the neighbours (NCCL
-                                all-gather of IPC handles).  Same results bit for bit.      */
+    RK_OPT_DEVICE_LOOP = 6,  /* 1: rk_integrate_adaptive without a host round trip per try
+                                (R-27): a vector state, or a grid within
+                                RK_OPT_COOP_MAX_CELLS (one GPU, no halo path), runs as one
+                                cooperative kernel; any other Gray–Scott grid -- one GPU, or the
+                                P2P transport at any world -- as ONE CUDA-graph launch (a
+                                conditional WHILE node over the try's stage launches and a
+                                controller kernel; RK_OPT_TIMING and RK_OPT_CHECK_FINITE off).
+                                Same results bit for bit; otherwise (NCCL transport) the host
+                                loop is used.                                               */
+    RK_OPT_HALO_P2P = 7,     /* halo path (world > 1 or HALO_LOOPBACK): 1 replaces NCCL by
+                                peer-to-peer stores and atomics -- the pack kernel writes Y_i's
+                                boundary planes straight into the neighbours' (double-buffered)
+                                ghost planes through CUDA IPC mappings over NVLink and raises
+                                their ready flags; the boundary launch waits on them and hands
+                                the buffers back; the error-ratio / norm allreduce(max) is
+                                atomicMax into every rank's mapped flag block plus an arrival
+                                barrier.  The stage sequence numbers live on the
+                                device, so RK_OPT_DEVICE_LOOP also runs on this transport.
+                                Collective: set it on every rank; with NCCL the first use maps
+                                the peers (NCCL all-gather of IPC handles), without NCCL see
+                                rk_p2p_export.  Same results bit for bit.                   */
     RK_OPT_CONTROLLER = 8,   /* error-control reading (P:L42 fixes the semantics only):
                                 0 (default) Odeint's (R-12): r = |e|/(atol + rtol*
                                 (|u| + dt*|k1|)), reject if E > 1 with dt *= max(0.9E^(-1/(q-1)),
@@ -145,12 +153,26 @@ typedef enum {
                                 blocking across the stages, K6): u read and
                                 u_new written once per step (32 B/cell instead of 208 / 80),
                                 same results bit for bit.  0: stage-by-stage launches.       */
-    RK_OPT_COMM_TIMEOUT_MS = 12 /* multi-GPU failure detection, applies to the state's context:
+    RK_OPT_COMM_TIMEOUT_MS = 12,/* multi-GPU failure detection, applies to the state's context:
                                 host waits on a stream with NCCL work poll the stream and
-                                ncclCommGetAsyncError; an asynchronous NCCL error, or a wait
-                                longer than this many ms (> 0), aborts the communicator and
+                                ncclCommGetAsyncError; an asynchronous NCCL error, or no
+                                collective completing for this many ms (> 0; the clock restarts
+                                whenever a collective issued by the ctx completes, so it must
+                                exceed the longest stretch of compute between two collectives,
+                                not the whole queued backlog), aborts the communicator and
                                 returns RK_ERR_NCCL (context poisoned).  0 (default): no
                                 deadline (asynchronous errors are still detected).  >= 0.   */
+    RK_OPT_ERROR_SPIKE = 13,  /* fault injection: n >= 1 -- the n-th error-controlled try
+                                of this rank from now (host try loop) has its local error ratio
+                                raised to at least 1e6 before the allreduce, forcing a rejection
+                                on every rank (u unchanged, dt shrunk by the controller's floor).
+                                Counted per rank; 0 (default): off.                          */
+    RK_OPT_CHECK_ARGS = 14    /* debug (SURVEY §8b "Collectives"): 1 -- every collective call
+                                (do_step, try_step, integrate_*, norm_inf, eval_rhs) first
+                                all-reduces a hash of its call kind and scalar arguments and
+                                returns RK_ERR_CONTRACT on every rank when the ranks disagree
+                                (a mismatched MPI-style call sequence).  Costs one host sync per
+                                call.  0 (default): off.                                       */
 } rk_option;
 
 /* Counters since creation or the last rk_reset_stats. */
@@ -216,7 +238,13 @@ rk_status rk_halo_plan_get(int world, int rank, rk_halo_plan* out);
  * (torch.distributed) to all ranks before rk_ctx_create.  Not needed when world == 1. */
 rk_status rk_nccl_unique_id(void* out);
 /* Collective when world > 1.  device: CUDA ordinal; cuda_stream: cudaStream_t to order
- * work on (NULL = a new non-blocking stream owned by the ctx); uid: NULL if world == 1. */
+ * work on (NULL = a new non-blocking stream owned by the ctx); uid: NULL if world == 1.
+ * world > 1 with uid == NULL creates a context WITHOUT NCCL: its states use the P2P transport
+ * only (RK_OPT_HALO_P2P forced on: halos and the error / norm allreduce run in this library's
+ * kernels over CUDA IPC mappings), and the caller exchanges the IPC handles of each state with
+ * rk_p2p_export / rk_p2p_import before its first collective call -- e.g. several processes
+ * sharing one GPU (NCCL refuses two ranks on one device), or a launcher with its own
+ * out-of-band channel. */
 rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* cuda_stream,
                         rk_ctx* out);
 rk_status rk_ctx_destroy(rk_ctx ctx);
@@ -282,6 +310,19 @@ rk_status rk_norm_inf(rk_state st, double* out);
  * unfused "native" stepping of the ablation.  Errors: RK_ERR_CONTRACT
  * on a shape mismatch, RK_ERR_ARG if out == in, RK_ERR_STATE if in has no RHS. */
 rk_status rk_eval_rhs(rk_state in, rk_state out);
+
+/* P2P transport (RK_OPT_HALO_P2P) without NCCL.  rk_p2p_export writes this rank's
+ * CUDA IPC handles for the state (its double-buffered ghost planes and its flag block, both
+ * allocated and zeroed here) into out (capacity bytes) and their size into *nbytes (out == NULL:
+ * size query only).  The caller all-gathers them (any channel, e.g. torch.distributed over
+ * gloo) and passes every rank's bytes, concatenated in rank order, to rk_p2p_import, which maps
+ * the z-neighbours' ghost planes and every rank's flag block (the fused allreduce(max) writes
+ * into all of them).  Collective; once per state, before its first step.  With NCCL the library
+ * does this exchange itself on the first P2P stage.  Errors: RK_ERR_STATE if the state does not
+ * use the P2P transport or is already connected, RK_ERR_ARG on a size mismatch, RK_ERR_CUDA if
+ * a handle cannot be mapped. */
+rk_status rk_p2p_export(rk_state st, void* out, int64_t capacity, int64_t* nbytes);
+rk_status rk_p2p_import(rk_state st, const void* all, int64_t nbytes_per_rank);
 
 rk_status rk_get_stats(rk_state st, rk_stats* out);
 rk_status rk_reset_stats(rk_state st);

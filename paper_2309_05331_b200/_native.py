@@ -16,9 +16,9 @@ STATUS = {0: "RK_OK", 1: "RK_ERR_ARG", 2: "RK_ERR_CONTRACT", 3: "RK_ERR_UNSUPPOR
           8: "RK_ERR_CUDA", 9: "RK_ERR_NCCL", 10: "RK_ERR_OOM"}
 OPT_HALO_OVERLAP, OPT_HALO_LOOPBACK, OPT_MAX_TRIES, OPT_TIMING, OPT_USE_GRAPH, OPT_DEVICE_LOOP, OPT_HALO_P2P = 1, 2, 3, 4, 5, 6, 7
 OPT_CONTROLLER, OPT_CHECK_FINITE, OPT_COOP_MAX_CELLS = 8, 9, 10
-OPT_FUSED_STEP, OPT_COMM_TIMEOUT_MS = 11, 12
+OPT_FUSED_STEP, OPT_COMM_TIMEOUT_MS, OPT_ERROR_SPIKE, OPT_CHECK_ARGS = 11, 12, 13, 14
 CTRL_ODEINT, CTRL_SPEC = 0, 1
-ABI_VERSION = 2
+ABI_VERSION = 3
 UNIQUE_ID_BYTES = 128
 
 
@@ -87,6 +87,8 @@ SIGNATURES = {
     "rk_lincomb": (_i, [_v, _i, _dp, _p(_v)]),
     "rk_norm_inf": (_i, [_v, _dp]),
     "rk_eval_rhs": (_i, [_v, _v]),
+    "rk_p2p_export": (_i, [_v, _v, _i64, _i64p]),
+    "rk_p2p_import": (_i, [_v, _v, _i64]),
     "rk_get_stats": (_i, [_v, _p(Stats)]),
     "rk_reset_stats": (_i, [_v]),
 }

@@ -61,18 +61,23 @@ def broadcast_unique_id(group=None, device: int | None = None) -> bytes:
 
 
 class Context:
-    """One per rank (one process per device).  world > 1 needs the NCCL unique id,
-    which ``Context.from_torch_distributed`` broadcasts over the torch process group."""
+    """One per rank (one process per device).  world > 1 with NCCL needs the NCCL
+    unique id, which ``Context.from_torch_distributed`` broadcasts over the torch process group;
+    world > 1 without one is a P2P-only context (rk_ctx_create): every state exchanges its CUDA
+    IPC handles over ``p2p_group`` (a torch process group, e.g. gloo) when it is created."""
 
     def __init__(self, rank: int = 0, world: int = 1, device: int = 0, stream=None,
-                 unique_id: bytes | None = None):
+                 unique_id: bytes | None = None, p2p_group=None):
         L = _native.lib()
         h = ctypes.c_void_p()
         uid = None
-        if world > 1:
-            if unique_id is None or len(unique_id) != _native.UNIQUE_ID_BYTES:
-                raise ValueError("world > 1 needs a 128-byte NCCL unique id")
+        if world > 1 and unique_id is not None:
+            if len(unique_id) != _native.UNIQUE_ID_BYTES:
+                raise ValueError("the NCCL unique id has 128 bytes")
             uid = ctypes.create_string_buffer(bytes(unique_id), _native.UNIQUE_ID_BYTES)
+        elif world > 1 and p2p_group is None:
+            raise ValueError("world > 1 needs the NCCL unique id or a process group for the P2P handles")
+        self._p2p_group = p2p_group if uid is None and world > 1 else None
         sh = _stream_handle(stream)
         call("rk_ctx_create", rank, world, device, uid, ctypes.c_void_p(sh) if sh else None,
              ctypes.byref(h))
@@ -88,25 +93,35 @@ class Context:
         return buf.raw
 
     @classmethod
-    def from_torch_distributed(cls, device: int, stream=None, group=None) -> "Context":
+    def from_torch_distributed(cls, device: int, stream=None, group=None, transport: str = "nccl") -> "Context":
+        """transport "nccl": NCCL communicator (unique id broadcast over `group`); "p2p": no NCCL,
+        every state's IPC handles are all-gathered over `group` (works for several ranks on
+        one GPU, which NCCL refuses)."""
         import torch.distributed as dist
         rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if transport == "p2p" and world > 1:
+            return cls(rank, world, device, stream, None, p2p_group=group if group is not None else dist.group.WORLD)
         uid = broadcast_unique_id(group, device) if world > 1 else None
         return cls(rank, world, device, stream, uid)
+
+    def _connect(self, st: "State") -> "State":
+        if self._p2p_group is not None:  # P2P-only context: exchange the IPC handles (collective)
+            st.p2p_connect(self._p2p_group)
+        return st
 
     def grid(self, nx: int, ny: int, nz: int, ncomp: int = 2) -> "State":
         h = ctypes.c_void_p()
         call("rk_state_create_grid", self._h, nx, ny, nz, ncomp, ctypes.byref(h))
         st = State(self, h, grid=True, dims=(nx, ny, nz), ncomp=ncomp)
         self._states.add(st)
-        return st
+        return self._connect(st)
 
     def vector(self, n: int, ncomp: int = 1) -> "State":
         h = ctypes.c_void_p()
         call("rk_state_create_vector", self._h, n, ncomp, ctypes.byref(h))
         st = State(self, h, grid=False, dims=(n,), ncomp=ncomp)
         self._states.add(st)
-        return st
+        return self._connect(st)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -209,6 +224,19 @@ class State:
         call("rk_integrate_adaptive", self._h, _scheme(scheme), t0, t1, dt0, atol, rtol,
              ctypes.byref(a), ctypes.byref(r))
         return a.value, r.value
+
+    def p2p_connect(self, group=None) -> None:
+        """P2P transport without NCCL: all-gather this state's CUDA IPC handles over the torch
+        process group and map the peers (rk_p2p_export / rk_p2p_import; collective)."""
+        import torch.distributed as dist
+        n = ctypes.c_int64()
+        call("rk_p2p_export", self._h, None, 0, ctypes.byref(n))
+        buf = ctypes.create_string_buffer(n.value)
+        call("rk_p2p_export", self._h, buf, n.value, ctypes.byref(n))
+        parts = [None] * dist.get_world_size(group)
+        dist.all_gather_object(parts, buf.raw[:n.value], group=group)
+        blob = b"".join(parts)
+        call("rk_p2p_import", self._h, ctypes.create_string_buffer(blob, len(blob)), n.value)
 
     # ---- algebra -------------------------------------------------------------------
     def lincomb(self, coef, states) -> None:

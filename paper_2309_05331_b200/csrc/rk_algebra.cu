@@ -62,6 +62,14 @@ __global__ void __launch_bounds__(256) norm_inf_kernel(const double* __restrict_
     block_max_to_global(m, out);
 }
 
+// RK_OPT_ERROR_SPIKE: raise a try's local error-ratio max to at least v (fault injection)
+__global__ void inject_max_kernel(unsigned long long* word, double v) { atomicMax(word, ratio_bits(v)); }
+
+cudaError_t launch_inject_max(unsigned long long* word, double v, cudaStream_t st) {
+    inject_max_kernel<<<1, 1, 0, st>>>(word, v);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_norm_inf(const double* x, int64_t count, unsigned long long* out,
                             cudaStream_t st, int num_sms) {
     int64_t blocks = (count + 255) / 256;

@@ -92,17 +92,33 @@ struct GridGeom {
     int64_t ps;     // plane stride = 2*cs
 };
 
-// Device-side handshake of the peer-to-peer halo path (RK_OPT_HALO_P2P): a
-// launch first waits until both wait flags reach wait_min (acquire, system scope), and its
-// last CTA to finish stores seq into both notify flags (release, system scope) -- flags that
-// may live in a neighbour GPU's memory (CUDA IPC over NVLink).  count: a CTA completion
-// counter, reset by the last CTA.  on == 0: no handshake.
+// Device-side handshake of the peer-to-peer halo path (RK_OPT_HALO_P2P).  The
+// stage sequence number lives on the device (*seqp + 1 = this stage; the boundary launch's last
+// CTA advances *seqp), so the same launches can be replayed from a CUDA graph.  A launch first
+// waits until both wait flags reach its minimum (acquire, system scope): the pack launch (role
+// 0) until both neighbours acknowledged stage seq-2 on this parity, the boundary launch (role 1)
+// until both ghost planes of stage seq have landed.  Its last CTA to finish stores seq into
+// both notify flags (release, system scope) -- flags that may live in a neighbour GPU's memory
+// (CUDA IPC over NVLink).  count: a CTA completion counter, reset by the last CTA.  Ghost
+// planes alternate between two parities, seq & 1.  on == 0: no handshake.
+// Word layout of a rank's P2P flag block (IPC-exported; neighbours and, for the reduction, every
+// rank write into it).
+enum P2pFlag {
+    P2P_READY_LO = 0, P2P_READY_HI = 1,  // ghost planes of stage seq landed (written by neighbours)
+    P2P_ACK_LO = 2, P2P_ACK_HI = 3,      // neighbours consumed the planes this rank sent them
+    P2P_COUNT = 4,                       // CTA completion counter of the current launch
+    P2P_SEQ = 5,                         // stages completed (device-resident sequence number)
+    P2P_RED0 = 6, P2P_RED1 = 7,          // allreduce(max) slots, double-buffered by round
+    P2P_ARRIVE = 8,                      // allreduce arrivals (world per round, monotonic)
+    P2P_ROUND = 9,                       // allreduce rounds completed by this rank
+    P2P_FLAGS = 16
+};
 struct P2pSync {
     const unsigned long long* wait[2];
-    unsigned long long wait_min;
     unsigned long long* notify[2];
     unsigned long long* count;
-    unsigned long long seq;
+    unsigned long long* seqp;
+    int role;
     int on;
 };
 
@@ -112,6 +128,7 @@ struct GsStageArgs {
     CUtensorMap tm_base;             // Y source: u (or u_new for EPI_TAIL_ERR), tile+ring box
     CUtensorMap tm_slot[kMaxSlots];  // slot s: tile+ring box if it enters Y, else interior box
     CUtensorMap tm_glo, tm_ghi;      // ghost planes z=-1, z=nzl (multi-GPU); else periodic wrap
+    CUtensorMap tm_glo1, tm_ghi1;    // P2P: the ghost planes of parity 1 (tm_glo/tm_ghi: parity 0)
     GridGeom geo;
     const double* base;              // raw pointers (pack kernel)
     const double* slot[kMaxSlots];
@@ -133,6 +150,7 @@ struct GsStageArgs {
     int z_lo, z_hi;                  // output planes [z_lo, z_hi) (zmode 0)
     int zchunk;                      // output planes per CTA
     int zmode;                       // 0: contiguous chunks; 1: chunk 0 = plane 0, chunk 1 = nzl-1
+    int zpair;                       // zmode 0: chunks paired, lower one swept downwards (K3)
     int nyslots;                     // pack kernel: slots [0, nyslots) with g != 0 (Y terms)
     P2pSync sync;                    // boundary launch of the P2P halo path (else on = 0)
 };
@@ -146,12 +164,22 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
 cudaError_t encode_grid_maps(CUtensorMap* maps, const double* base, const GridGeom& g, int nplanes);
 
 // Y_i on own planes 0 and nzl-1 (whole padded planes) -> dst[0] (plane 0), dst[1] (plane
-// nzl-1): the NCCL send buffer, or the neighbours' ghost planes (P2P, with the handshake).
+// nzl-1): the NCCL send buffer, or the neighbours' ghost planes (P2P, with the handshake; dst
+// then points at parity 0 and parity 1 lies 2 planes further).
 cudaError_t launch_gs_pack(const GsStageArgs& a, double* dst0, double* dst1, const P2pSync& sync,
                            cudaStream_t st);
 // Refresh the periodic ring of every (plane, component) slice of a padded array (after a
 // user copy into the interior); nslices = planes * components.
 cudaError_t launch_fill_ring(double* a, const GridGeom& g, int nslices, cudaStream_t st);
+
+// Fused allreduce(max) of one uint64 word over the ranks' mapped P2P flag blocks (SURVEY f3:
+// the NCCL allreduce replaced by NVLink atomics): every rank atomicMax-es its word into slot
+// (round & 1) of every rank's block, raises every rank's arrival counter, waits for all world
+// arrivals of this round, and reads the result back into *word.  flags[q]: rank q's block
+// (flags[rank] = this rank's own); one thread; round counter on the device.
+cudaError_t launch_p2p_allreduce_max(unsigned long long* word, unsigned long long* const* flags, int world,
+                                     int rank, cudaStream_t st);
+constexpr int P2P_MAX_WORLD = 16;
 
 // ---------------------------------------------------------------------------------------
 // K5: whole RK integrations of Gray–Scott on a small single-GPU grid in one persistent
@@ -217,5 +245,7 @@ struct LincombArgs {
 cudaError_t launch_lincomb(const LincombArgs& a, cudaStream_t st, int num_sms);
 cudaError_t launch_norm_inf(const double* x, int64_t count, unsigned long long* out,
                             cudaStream_t st, int num_sms);
+// atomicMax(word, bits of v) (v >= 0): fault injection into an error-ratio max
+cudaError_t launch_inject_max(unsigned long long* word, double v, cudaStream_t st);
 
 }  // namespace rkb

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <initializer_list>
 #include <string>
 #include <utility>
 #include <vector>
@@ -236,12 +237,12 @@ struct rk_state_s {
     // into the neighbours' ghost planes (CUDA IPC over NVLink) with a flag handshake
     bool p2p = false, p2p_ready = false;
     double* pghost = nullptr;               // [parity][ghost_hi, ghost_lo][plane], written by peers
-    unsigned long long* pflags = nullptr;   // [READY_LO, READY_HI, ACK_LO, ACK_HI, COUNT, ...]
+    unsigned long long* pflags = nullptr;   // this rank's flag block (rk_kernels.cuh P2pFlag)
     double* peer_ghost[2] = {};             // [0] lower neighbour's pghost, [1] upper's
     unsigned long long* peer_flags[2] = {};
-    void* ipc_mapped[4] = {};               // IPC mappings to close on destroy
+    unsigned long long* rank_flags[P2P_MAX_WORLD] = {};  // every rank's flag block (allreduce)
+    std::vector<void*> ipc_mapped;          // IPC mappings to close on destroy
     Maps tm_pg[2][2]{};                     // [parity][0 ghost_hi, 1 ghost_lo]
-    unsigned long long p2p_seq = 0;
     unsigned long long* d_err = nullptr;
     unsigned long long* h_err = nullptr;
     // rhs
@@ -256,6 +257,8 @@ struct rk_state_s {
     int64_t since_check = 0;     // steps since the last finiteness check
     int64_t coop_max_cells = 1 << 18;  // RK_OPT_COOP_MAX_CELLS: persistent-step path up to here
     bool fused = false;          // RK_OPT_FUSED_STEP: K6 whole-step launches (RK4, midpoint)
+    int64_t spike_at = 0, spike_seen = 0;  // RK_OPT_ERROR_SPIKE: inject at try number spike_at
+    bool check_args = false;     // RK_OPT_CHECK_ARGS: hash-compare collective call arguments
     const double* gl_dtp = nullptr;  // set while capturing the device-resident try loop (GLoop)
     struct GraphLoop* gloop = nullptr;
     // stats
@@ -453,6 +456,17 @@ static rk_status ensure_halo(rk_state st) {
     return RK_OK;
 }
 
+// Paired opposite-direction chunk sweeps in K3 (rk_stencil.cu); RKB_ZPAIR=0/1 is a developer
+// knob for A/B measurements.
+static int zpair_default() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("RKB_ZPAIR");
+        v = e ? (atoi(e) != 0) : 1;
+    }
+    return v;
+}
+
 static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
     GsStageArgs a{};
     a.geo = st->geo;
@@ -495,6 +509,7 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     a.z_lo = 0;
     a.z_hi = (int)st->local;
     a.zmode = 0;
+    a.zpair = zpair_default();
     return a;
 }
 
@@ -618,100 +633,151 @@ static rk_status halo_exchange(rk_state st, cudaStream_t src) {
 }
 
 // ---- peer-to-peer halo path (RK_OPT_HALO_P2P) --------------------------------
-enum { P2P_READY_LO = 0, P2P_READY_HI = 1, P2P_ACK_LO = 2, P2P_ACK_HI = 3, P2P_COUNT = 4, P2P_FLAGS = 8 };
+// A rank's exported CUDA IPC handles: its ghost planes (grid states) and its flag block.
+struct P2pHandles {
+    cudaIpcMemHandle_t ghost, flags;
+    int has_ghost;
+};
 
-// Collective (first P2P stage on every rank): double-buffered ghost planes + flags, their CUDA
-// IPC handles all-gathered over NCCL, the neighbours' buffers mapped into this process.
-static rk_status ensure_p2p(rk_state st) {
-    if (st->p2p_ready) return RK_OK;
+static bool p2p_needed(rk_state st) { return st->p2p && (st->ctx->world > 1 || st->loopback); }
+
+// this rank's double-buffered ghost planes (grids) and flag block, zeroed
+static rk_status p2p_alloc(rk_state st) {
+    if (st->pflags) return RK_OK;
     rk_ctx ctx = st->ctx;
-    const int64_t pv = plane_values(st);
-    TRY(dev_alloc(ctx, &st->pghost, 4 * pv));
-    {
-        void* f = nullptr;
-        CK_CTX(ctx, cudaMalloc(&f, P2P_FLAGS * sizeof(unsigned long long)));
-        st->pflags = static_cast<unsigned long long*>(f);
+    if (st->grid) {
+        const int64_t pv = plane_values(st);
+        TRY(dev_alloc(ctx, &st->pghost, 4 * pv));
+        CK_CTX(ctx, cudaMemsetAsync(st->pghost, 0, sizeof(double) * 4 * pv, ctx->stream));
+        for (int b = 0; b < 2; ++b)
+            for (int g = 0; g < 2; ++g)
+                CK_CTX(ctx, encode_grid_maps(st->tm_pg[b][g].m, st->pghost + (2 * b + g) * pv, st->geo, 1));
     }
-    CK_CTX(ctx, cudaMemsetAsync(st->pghost, 0, sizeof(double) * 4 * pv, ctx->stream));
+    void* f = nullptr;
+    CK_CTX(ctx, cudaMalloc(&f, P2P_FLAGS * sizeof(unsigned long long)));
+    st->pflags = static_cast<unsigned long long*>(f);
     CK_CTX(ctx, cudaMemsetAsync(st->pflags, 0, P2P_FLAGS * sizeof(unsigned long long), ctx->stream));
-    for (int b = 0; b < 2; ++b)
-        for (int g = 0; g < 2; ++g)
-            CK_CTX(ctx, encode_grid_maps(st->tm_pg[b][g].m, st->pghost + (2 * b + g) * pv, st->geo, 1));
-    const int lower = (ctx->rank + ctx->world - 1) % ctx->world, upper = (ctx->rank + 1) % ctx->world;
-    if (ctx->world == 1) {  // loopback: both neighbours are this rank
-        st->peer_ghost[0] = st->peer_ghost[1] = st->pghost;
-        st->peer_flags[0] = st->peer_flags[1] = st->pflags;
-    } else {
-        cudaIpcMemHandle_t mine[2];
-        CK_CTX(ctx, cudaIpcGetMemHandle(&mine[0], st->pghost));
-        CK_CTX(ctx, cudaIpcGetMemHandle(&mine[1], st->pflags));
-        const size_t hb = sizeof mine;
-        unsigned char* d = nullptr;
-        CK_CTX(ctx, cudaMalloc((void**)&d, hb * (ctx->world + 1)));
-        CK_CTX(ctx, cudaMemcpyAsync(d, mine, hb, cudaMemcpyHostToDevice, ctx->stream));
-        NK_CTX(ctx, ncclAllGather(d, d + hb, hb, ncclUint8, ctx->nccl, ctx->stream));
-        std::vector<unsigned char> all(hb * ctx->world);
-        CK_CTX(ctx, cudaMemcpyAsync(all.data(), d + hb, all.size(), cudaMemcpyDeviceToHost, ctx->stream));
-        TRY(ctx_wait(ctx, ctx->stream));
-        cudaFree(d);
-        int nmap = 0;
+    CK_CTX(ctx, cudaStreamSynchronize(ctx->stream));  // zeroed before any peer can map and write
+    return RK_OK;
+}
+
+static rk_status p2p_export(rk_state st, P2pHandles* h) {
+    TRY(p2p_alloc(st));
+    *h = P2pHandles{};
+    h->has_ghost = st->pghost ? 1 : 0;
+    if (st->pghost) CK_CTX(st->ctx, cudaIpcGetMemHandle(&h->ghost, st->pghost));
+    CK_CTX(st->ctx, cudaIpcGetMemHandle(&h->flags, st->pflags));
+    return RK_OK;
+}
+
+// map the neighbours' ghost planes and every rank's flag block from all ranks' handles
+static rk_status p2p_map(rk_state st, const P2pHandles* all) {
+    rk_ctx ctx = st->ctx;
+    const int world = ctx->world, rank = ctx->rank;
+    if (world > P2P_MAX_WORLD) return fail(RK_ERR_UNSUPPORTED, "P2P transport: world %d > %d", world, P2P_MAX_WORLD);
+    std::vector<unsigned long long*> fl(world, nullptr);
+    fl[rank] = st->pflags;
+    for (int q = 0; q < world; ++q) {
+        if (q == rank) continue;
+        void* pf = nullptr;
+        CK_CTX(ctx, cudaIpcOpenMemHandle(&pf, all[q].flags, cudaIpcMemLazyEnablePeerAccess));
+        st->ipc_mapped.push_back(pf);
+        fl[q] = static_cast<unsigned long long*>(pf);
+    }
+    for (int q = 0; q < world; ++q) st->rank_flags[q] = fl[q];
+    const int lower = (rank + world - 1) % world, upper = (rank + 1) % world;
+    st->peer_flags[0] = fl[lower];
+    st->peer_flags[1] = fl[upper];
+    if (st->grid) {
+        double* pg[2] = {st->pghost, st->pghost};
         for (int dir = 0; dir < 2; ++dir) {
-            const int peer = dir == 0 ? lower : upper;
+            const int q = dir == 0 ? lower : upper;
+            if (q == rank) continue;
             if (dir == 1 && upper == lower) {  // world == 2: one peer on both sides
-                st->peer_ghost[1] = st->peer_ghost[0];
-                st->peer_flags[1] = st->peer_flags[0];
+                pg[1] = pg[0];
                 break;
             }
-            cudaIpcMemHandle_t h[2];
-            std::memcpy(h, all.data() + hb * peer, hb);
-            void* pg = nullptr;
-            void* pf = nullptr;
-            CK_CTX(ctx, cudaIpcOpenMemHandle(&pg, h[0], cudaIpcMemLazyEnablePeerAccess));
-            st->ipc_mapped[nmap++] = pg;
-            CK_CTX(ctx, cudaIpcOpenMemHandle(&pf, h[1], cudaIpcMemLazyEnablePeerAccess));
-            st->ipc_mapped[nmap++] = pf;
-            st->peer_ghost[dir] = static_cast<double*>(pg);
-            st->peer_flags[dir] = static_cast<unsigned long long*>(pf);
+            if (!all[q].has_ghost) return fail(RK_ERR_CONTRACT, "P2P: rank %d exported no ghost planes", q);
+            void* g = nullptr;
+            CK_CTX(ctx, cudaIpcOpenMemHandle(&g, all[q].ghost, cudaIpcMemLazyEnablePeerAccess));
+            st->ipc_mapped.push_back(g);
+            pg[dir] = static_cast<double*>(g);
         }
+        st->peer_ghost[0] = pg[0];
+        st->peer_ghost[1] = pg[1];
     }
     st->p2p_ready = true;
     return RK_OK;
 }
 
+// Collective (first P2P use on every rank): double-buffered ghost planes + flags; with NCCL the
+// handles are all-gathered here, without NCCL (rk_p2p_import) the caller has exchanged them.
+static rk_status ensure_p2p(rk_state st) {
+    if (st->p2p_ready) return RK_OK;
+    rk_ctx ctx = st->ctx;
+    P2pHandles mine{};
+    TRY(p2p_export(st, &mine));
+    if (ctx->world == 1) {  // loopback: both neighbours are this rank
+        return p2p_map(st, &mine);
+    }
+    if (!ctx->nccl)
+        return fail(RK_ERR_STATE, "P2P transport without NCCL: exchange the handles with rk_p2p_export / rk_p2p_import first");
+    const size_t hb = sizeof mine;
+    unsigned char* d = nullptr;
+    CK_CTX(ctx, cudaMalloc((void**)&d, hb * (ctx->world + 1)));
+    CK_CTX(ctx, cudaMemcpyAsync(d, &mine, hb, cudaMemcpyHostToDevice, ctx->stream));
+    NK_CTX(ctx, ncclAllGather(d, d + hb, hb, ncclUint8, ctx->nccl, ctx->stream));
+    std::vector<P2pHandles> all(ctx->world);
+    CK_CTX(ctx, cudaMemcpyAsync(all.data(), d + hb, hb * ctx->world, cudaMemcpyDeviceToHost, ctx->stream));
+    TRY(ctx_wait(ctx, ctx->stream));
+    cudaFree(d);
+    return p2p_map(st, all.data());
+}
+
 // One stage with P2P halos: pack (waits until the neighbours released this parity's ghost
 // planes, stores Y_i's boundary planes into them, raises their ready flags) -> interior planes
 // -> boundary planes (wait for this rank's ready flags, then release the ghosts to the
-// neighbours).  Ghost planes alternate between two parities so a stage's stores never wait for
-// the previous stage's reads.
+// neighbours and advance the device-resident stage counter).  Ghost planes alternate between
+// two parities so a stage's stores never wait for the previous stage's reads.  Nothing here
+// depends on host-side state, so the same launches replay from a CUDA graph.
 static rk_status run_gs_stage_p2p(rk_state st, const StagePlan& p, GsStageArgs& a) {
     rk_ctx ctx = st->ctx;
     TRY(ensure_p2p(st));
     const int nzl = (int)st->local;
     const int64_t pv = plane_values(st);
-    const unsigned long long seq = ++st->p2p_seq;
-    const int b = (int)(seq & 1);
     P2pSync ps{};
     ps.on = 1;
+    ps.role = 0;
     ps.wait[0] = st->pflags + P2P_ACK_LO;
     ps.wait[1] = st->pflags + P2P_ACK_HI;
-    ps.wait_min = seq >= 2 ? seq - 2 : 0;
     ps.notify[0] = st->peer_flags[0] + P2P_READY_HI;  // my plane 0 is the lower neighbour's ghost_hi
     ps.notify[1] = st->peer_flags[1] + P2P_READY_LO;  // my plane nzl-1 is the upper's ghost_lo
     ps.count = st->pflags + P2P_COUNT;
-    ps.seq = seq;
+    ps.seqp = st->pflags + P2P_SEQ;
     // the boundary stream starts from everything the compute stream has issued so far
     CK_CTX(ctx, cudaEventRecord(st->ev_ready, ctx->stream));
     CK_CTX(ctx, cudaStreamWaitEvent(ctx->bnd, st->ev_ready, 0));
-    CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->peer_ghost[0] + (2 * b + 0) * pv,
-                               st->peer_ghost[1] + (2 * b + 1) * pv, ps, ctx->bnd));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (st->timing) {  // the exchange: the pack kernel's stores into the neighbours' ghost planes
+        e0 = pool_event(st);
+        e1 = pool_event(st);
+        CK_CTX(ctx, cudaEventRecord(e0, ctx->bnd));
+    }
+    CK_CTX(ctx, launch_gs_pack(pack_args(a, p), st->peer_ghost[0] + 0 * pv, st->peer_ghost[1] + 1 * pv, ps, ctx->bnd));
+    if (st->timing) {
+        CK_CTX(ctx, cudaEventRecord(e1, ctx->bnd));
+        st->pending.push_back({e0, e1, 1});
+    }
     st->stats.kernel_launches += 1;
     st->stats.halo_exchanges += 1;
     st->stats.halo_bytes += (int64_t)sizeof(double) * 2 * pv;
     const int hb = 2 * (stage_rows(p.sp) - 1);
     a.has_ghi = 1;
     a.has_glo = 1;
-    a.tm_ghi = st->tm_pg[b][0].m[hb];
-    a.tm_glo = st->tm_pg[b][1].m[hb];
+    a.tm_ghi = st->tm_pg[0][0].m[hb];
+    a.tm_glo = st->tm_pg[0][1].m[hb];
+    a.tm_ghi1 = st->tm_pg[1][0].m[hb];
+    a.tm_glo1 = st->tm_pg[1][1].m[hb];
     if (nzl > 2) {
         GsStageArgs in = a;  // interior planes [1, nzl-1) never touch ghost planes
         in.z_lo = 1;
@@ -723,16 +789,36 @@ static rk_status run_gs_stage_p2p(rk_state st, const StagePlan& p, GsStageArgs& 
     bd.zmode = 1;
     P2pSync& bs = bd.sync;
     bs.on = 1;
+    bs.role = 1;
     bs.wait[0] = st->pflags + P2P_READY_LO;
     bs.wait[1] = st->pflags + P2P_READY_HI;
-    bs.wait_min = seq;
     bs.notify[0] = st->peer_flags[0] + P2P_ACK_HI;  // my ghost_lo came from the lower neighbour
     bs.notify[1] = st->peer_flags[1] + P2P_ACK_LO;  // my ghost_hi came from the upper neighbour
     bs.count = st->pflags + P2P_COUNT;
-    bs.seq = seq;
+    bs.seqp = st->pflags + P2P_SEQ;
     TRY(launch_stage_timed(st, p, bd, ctx->bnd));  // beside the interior launch
     CK_CTX(ctx, cudaEventRecord(st->ev_bnd, ctx->bnd));
     CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_bnd, 0));  // stage complete on the compute stream
+    return RK_OK;
+}
+
+// Global max of one uint64 word on the stream (collective): P2P atomics over NVLink when the
+// state uses the P2P transport (no NCCL on the data path; graph-capturable), else NCCL's
+// allreduce (world > 1 or the loopback's 1-rank communicator), else nothing to do.
+static rk_status allreduce_max_word(rk_state st, unsigned long long* word) {
+    rk_ctx ctx = st->ctx;
+    if (p2p_needed(st)) {
+        TRY(ensure_p2p(st));
+        CK_CTX(ctx, launch_p2p_allreduce_max(word, st->rank_flags, ctx->world, ctx->rank, ctx->stream));
+        st->stats.kernel_launches += 1;
+        return RK_OK;
+    }
+    if (ctx->nccl && halo_path(st)) {
+        NK_CTX(ctx, ncclAllReduce(word, word, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
+        mark_progress(ctx, ctx->stream);
+        return RK_OK;
+    }
+    if (ctx->world > 1) return fail(RK_ERR_STATE, "no transport for the allreduce (no NCCL, no P2P)");
     return RK_OK;
 }
 
@@ -857,16 +943,37 @@ static bool adjust(int controller, double E, int p, int q, double* dt) {
 
 static bool step_adjust(double E, int p, int q, double* dt) { return adjust(0, E, p, q, dt); }
 
+// RK_OPT_CHECK_ARGS (SURVEY §8b "Collectives"): every rank hashes (call kind, scalar args)
+// and the ranks all-reduce max(h) and max(~h) = ~min(h); equal max and min <=> identical calls.
+static rk_status check_collective_args(rk_state st, int kind, std::initializer_list<double> args) {
+    if (!st->check_args || st->ctx->world == 1) return RK_OK;
+    rk_ctx ctx = st->ctx;
+    uint64_t h = 1469598103934665603ull ^ (uint64_t)kind;  // FNV-1a over the argument bytes
+    for (double v : args) {
+        unsigned char b[8];
+        std::memcpy(b, &v, 8);
+        for (unsigned char c : b) h = (h ^ c) * 1099511628211ull;
+    }
+    unsigned long long hv[2] = {h, ~h};
+    for (int j = 0; j < 2; ++j) {
+        CK_CTX(ctx, cudaMemcpyAsync(ctx->d_scratch, &hv[j], 8, cudaMemcpyHostToDevice, ctx->stream));
+        TRY(allreduce_max_word(st, ctx->d_scratch));
+        CK_CTX(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        TRY(ctx_wait(ctx, ctx->stream));
+        hv[j] = *ctx->h_scratch;
+    }
+    if (hv[0] != ~hv[1])
+        return fail(RK_ERR_CONTRACT, "collective call %d: the ranks' arguments differ (RK_OPT_CHECK_ARGS)", kind);
+    return RK_OK;
+}
+
 // Global max |u| (collective), NaN if any element is NaN: the norm_inf reduction (K4).
 static rk_status global_norm_inf(rk_state st, double* out) {
     rk_ctx ctx = st->ctx;
     CK_CTX(ctx, cudaMemsetAsync(ctx->d_scratch, 0, 8, ctx->stream));
     CK_CTX(ctx, launch_norm_inf(st->u, st->alloc, ctx->d_scratch, ctx->stream, ctx->num_sms));
     st->stats.kernel_launches += 1;
-    if (use_nccl(st)) {
-        NK_CTX(ctx, ncclAllReduce(ctx->d_scratch, ctx->d_scratch, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
-        mark_progress(ctx, ctx->stream);
-    }
+    TRY(allreduce_max_word(st, ctx->d_scratch));
     CK_CTX(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
     TRY(ctx_wait(ctx, ctx->stream));
     std::memcpy(out, ctx->h_scratch, 8);
@@ -1191,10 +1298,11 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
     } else {
         TRY(run_pointwise(st, scheme, dt, 1, true, atol, rtol));
     }
-    if (use_nccl(st)) {  // global max of E's bit pattern (loopback: a 1-rank allreduce)
-        NK_CTX(ctx, ncclAllReduce(st->d_err, st->d_err, 1, ncclUint64, ncclMax, ctx->nccl, ctx->stream));
-        mark_progress(ctx, ctx->stream);
+    if (st->spike_at > 0 && ++st->spike_seen == st->spike_at) {  // RK_OPT_ERROR_SPIKE
+        CK_CTX(ctx, launch_inject_max(st->d_err, 1e6, ctx->stream));
+        st->stats.kernel_launches += 1;
     }
+    TRY(allreduce_max_word(st, st->d_err));  // global max of E's bit pattern
     CK_CTX(ctx, cudaMemcpyAsync(st->h_err, st->d_err, sizeof(unsigned long long),
                                 cudaMemcpyDeviceToHost, ctx->stream));
     TRY(ctx_wait(ctx, ctx->stream));
@@ -1462,8 +1570,11 @@ static void gloop_destroy(rk_state st) {
     st->gloop = nullptr;
 }
 
+// one GPU without exchange, or the P2P transport (halos and the E allreduce in this library's
+// kernels); the NCCL transport keeps the host loop (NCCL calls inside conditional graph bodies
+// are not relied on)
 static bool gloop_path(rk_state st) {
-    return st->device_loop && st->grid && st->rhs == RHS_GRAY_SCOTT && !halo_path(st) &&
+    return st->device_loop && st->grid && st->rhs == RHS_GRAY_SCOTT && (!halo_path(st) || p2p_needed(st)) &&
            st->check_finite == 0 && !st->timing;
 }
 
@@ -1537,6 +1648,8 @@ static rk_status gloop_build(rk_state st, int scheme, double atol, double rtol) 
     for (const StagePlan& p : plan) (p.stage == 0 ? g->k1_bytes : g->try_bytes) += plan_stage_bytes(st, p);
     CK_CTX(ctx, cudaMalloc((void**)&g->dev, sizeof(GLoopDev)));
     if (!ctx->capture) CK_CTX(ctx, cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking));
+    TRY(ensure_halo(st));                    // ghost buffers / events exist before the capture
+    if (p2p_needed(st)) TRY(ensure_p2p(st));  // ... and the P2P mappings (collective)
 
     cudaGraph_t graph = nullptr;
     CK_CTX(ctx, cudaGraphCreate(&graph, 0));
@@ -1593,6 +1706,7 @@ static rk_status gloop_build(rk_state st, int scheme, double atol, double rtol) 
         st->gl_dtp = dtp;
         st->k1_valid = need_k1 == 0;
         rc = run_grid_plan(st, plan, 1.0, atol, rtol);
+        if (rc == RK_OK) rc = allreduce_max_word(st, st->d_err);  // P2P transport: NVLink atomics
         st->gl_dtp = nullptr;
         ctx->stream = work;
         cudaGraph_t out = nullptr;
@@ -1773,7 +1887,9 @@ rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* 
                         rk_ctx* out) {
     if (!out || world < 1 || rank < 0 || rank >= world || device < 0)
         return fail(RK_ERR_ARG, "rk_ctx_create: bad arguments");
-    if (world > 1 && !uid) return fail(RK_ERR_ARG, "world > 1 needs the NCCL unique id");
+    // world > 1 without a NCCL unique id: a context whose states use the P2P transport only
+    // (halos and reductions in this library's kernels over CUDA IPC mappings that the caller
+    // exchanges with rk_p2p_export / rk_p2p_import), e.g. several processes sharing one GPU
     *out = nullptr;
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -1810,7 +1926,7 @@ rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* 
     if (cudaMalloc((void**)&ctx->d_scratch, 8) != cudaSuccess ||
         cudaMallocHost((void**)&ctx->h_scratch, 8) != cudaSuccess)
         return bail(fail(RK_ERR_OOM, "scratch allocation failed"));
-    if (world > 1) {
+    if (world > 1 && uid) {
         ncclUniqueId id;
         std::memcpy(&id, uid, sizeof id);
         ncclResult_t r = ncclCommInitRank(&ctx->nccl, world, id, rank);
@@ -1840,6 +1956,7 @@ rk_status rk_ctx_destroy(rk_ctx ctx) {
 
 static rk_status state_common(rk_ctx ctx, rk_state st) {
     DeviceGuard g(ctx->device);
+    st->p2p = ctx->world > 1 && !ctx->nccl;  // no NCCL: the P2P transport is the only one
     TRY(alloc_array(st, &st->u, &st->tm_u));
     TRY(alloc_array(st, &st->u_new, &st->tm_unew));
     CK_CTX(ctx, cudaMalloc((void**)&st->d_err, sizeof(unsigned long long)));
@@ -2096,8 +2213,17 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
         if (value < 0) return fail(RK_ERR_ARG, "RK_OPT_COMM_TIMEOUT_MS must be >= 0");
         st->ctx->comm_timeout_ms = value;
         break;
+    case RK_OPT_ERROR_SPIKE:
+        if (value < 0) return fail(RK_ERR_ARG, "RK_OPT_ERROR_SPIKE must be >= 0");
+        st->spike_at = value;
+        st->spike_seen = 0;
+        break;
+    case RK_OPT_CHECK_ARGS: st->check_args = value != 0; break;
     case RK_OPT_HALO_P2P:
-        if (value != 0 && !st->grid) return fail(RK_ERR_ARG, "RK_OPT_HALO_P2P needs a grid state");
+        if (value == 0 && st->ctx->world > 1 && !st->ctx->nccl)
+            return fail(RK_ERR_ARG, "a context without NCCL has only the P2P transport");
+        if (st->p2p_ready && (value != 0) != st->p2p)
+            return fail(RK_ERR_STATE, "the P2P transport is already connected on this state");
         st->p2p = value != 0;
         break;
     default: return fail(RK_ERR_ARG, "unknown option %d", key);
@@ -2112,6 +2238,7 @@ rk_status rk_do_step(rk_state st, rk_scheme scheme, double t, double dt) {
     if (!(dt > 0.0) || !std::isfinite(dt)) return fail(RK_ERR_ARG, "dt must be finite and > 0");
     TRY(check_rhs(st));
     DeviceGuard g(st->ctx->device);
+    TRY(check_collective_args(st, 1, {(double)scheme, t, dt}));
     TRY(fixed_step(st, scheme, dt));
     return finite_check(st, 1, t + dt, false);
 }
@@ -2127,6 +2254,7 @@ rk_status rk_try_step(rk_state st, rk_scheme scheme, double t, double dt, double
         return fail(RK_ERR_UNSUPPORTED, "scheme %d has no embedded error estimate", (int)scheme);
     TRY(check_rhs(st));
     DeviceGuard g(st->ctx->device);
+    TRY(check_collective_args(st, 2, {(double)scheme, t, dt, atol, rtol}));
     return one_try(st, scheme, t, dt, atol, rtol, accepted, err_ratio, dt_next);
 }
 
@@ -2139,6 +2267,7 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
     if (!(t1 > t0)) return fail(RK_ERR_ARG, "need t1 > t0");
     TRY(check_rhs(st));
     DeviceGuard g(st->ctx->device);
+    TRY(check_collective_args(st, 3, {(double)scheme, t0, t1, dt}));
     // Odeint integrate_const: while (t_n + dt) - t1 <= eps, t_n = t0 + n*dt
     int64_t n = 0;
     double t = t0;
@@ -2196,6 +2325,7 @@ rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double
         return fail(RK_ERR_UNSUPPORTED, "scheme %d has no embedded error estimate", (int)scheme);
     TRY(check_rhs(st));
     DeviceGuard g(st->ctx->device);
+    TRY(check_collective_args(st, 4, {(double)scheme, t0, t1, dt0, atol, rtol}));
     if (st->device_loop && st->ctx->world == 1 &&
         (!st->grid || (!st->loopback && !st->p2p && st->local * st->nx * st->ny <= st->coop_max_cells))) {
         TRY(device_adaptive_loop(st, scheme, t0, t1, dt0, atol, rtol, accepted, rejected));
@@ -2271,6 +2401,7 @@ rk_status rk_norm_inf(rk_state st, double* out) {
     TRY(check_state(st));
     if (!out) return fail(RK_ERR_ARG, "null output");
     DeviceGuard g(st->ctx->device);
+    TRY(check_collective_args(st, 5, {}));
     return global_norm_inf(st, out);
 }
 
@@ -2284,6 +2415,7 @@ rk_status rk_eval_rhs(rk_state in, rk_state out) {
     TRY(check_rhs(in));
     rk_ctx ctx = in->ctx;
     DeviceGuard g(ctx->device);
+    TRY(check_collective_args(in, 6, {}));
     if (in->grid) {
         // the k1 = F(u) stage kernel of every scheme, its output redirected to out.u
         StagePlan p = build_plan(RK_RK4, 0, 0.0)[0];
@@ -2298,6 +2430,34 @@ rk_status rk_eval_rhs(rk_state in, rk_state out) {
     out->k1_valid = false;
     ab_invalidate(out);
     return RK_OK;
+}
+
+rk_status rk_p2p_export(rk_state st, void* out, int64_t capacity, int64_t* nbytes) {
+    TRY(check_state(st));
+    if (!nbytes) return fail(RK_ERR_ARG, "null nbytes");
+    *nbytes = (int64_t)sizeof(P2pHandles);
+    if (!out) return RK_OK;  // size query
+    if (capacity < (int64_t)sizeof(P2pHandles)) return fail(RK_ERR_ARG, "buffer too small (%lld < %lld)",
+                                                           (long long)capacity, (long long)sizeof(P2pHandles));
+    if (!st->p2p) return fail(RK_ERR_STATE, "the state does not use the P2P transport (RK_OPT_HALO_P2P)");
+    DeviceGuard g(st->ctx->device);
+    P2pHandles h{};
+    TRY(p2p_export(st, &h));
+    std::memcpy(out, &h, sizeof h);
+    return RK_OK;
+}
+
+rk_status rk_p2p_import(rk_state st, const void* all, int64_t nbytes_per_rank) {
+    TRY(check_state(st));
+    if (!all || nbytes_per_rank != (int64_t)sizeof(P2pHandles))
+        return fail(RK_ERR_ARG, "expected world x %lld bytes from rk_p2p_export", (long long)sizeof(P2pHandles));
+    if (!st->p2p) return fail(RK_ERR_STATE, "the state does not use the P2P transport (RK_OPT_HALO_P2P)");
+    if (st->p2p_ready) return fail(RK_ERR_STATE, "P2P transport already connected");
+    DeviceGuard g(st->ctx->device);
+    TRY(p2p_alloc(st));
+    std::vector<P2pHandles> v((size_t)st->ctx->world);
+    std::memcpy(v.data(), all, sizeof(P2pHandles) * v.size());
+    return p2p_map(st, v.data());
 }
 
 rk_status rk_get_stats(rk_state st, rk_stats* out) {

@@ -142,18 +142,26 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
-// P2P halo handshake (P2pSync, rk_kernels.cuh): every CTA waits for the flags on entry; the
-// last CTA to finish publishes seq.  Every thread fences its own stores before the count.
-__device__ __forceinline__ void p2p_wait(const P2pSync& s) {
-    if (!s.on) return;
+// P2P halo handshake (P2pSync, rk_kernels.cuh): every CTA reads this stage's sequence number
+// (*seqp + 1: the counter only advances at the end of the stage's boundary launch, after every
+// CTA of it has started) and waits for the flags on entry; the last CTA to finish publishes
+// seq (and, for the boundary launch, advances the counter).  Every thread fences its own
+// stores before the count.  Returns seq (0 without handshake).
+__device__ __forceinline__ unsigned long long p2p_wait(const P2pSync& s) {
+    if (!s.on) return 0ull;
+    __shared__ unsigned long long s_seq;
     if (threadIdx.x == 0) {
+        const unsigned long long seq = *(volatile const unsigned long long*)s.seqp + 1;
+        const unsigned long long wmin = s.role == 0 ? (seq >= 2 ? seq - 2 : 0ull) : seq;
 #pragma unroll
         for (int d = 0; d < 2; ++d)
-            while (ld_acquire_sys(s.wait[d]) < s.wait_min) __nanosleep(64);
+            while (ld_acquire_sys(s.wait[d]) < wmin) __nanosleep(64);
+        s_seq = seq;
     }
     __syncthreads();
+    return s_seq;
 }
-__device__ __forceinline__ void p2p_notify(const P2pSync& s) {
+__device__ __forceinline__ void p2p_notify(const P2pSync& s, unsigned long long seq) {
     if (!s.on) return;
     __threadfence_system();
     __syncthreads();
@@ -162,8 +170,9 @@ __device__ __forceinline__ void p2p_notify(const P2pSync& s) {
         if (atomicAdd(s.count, 1ull) + 1 == nb) {
             *s.count = 0ull;  // the next launch on this stream starts after this one ends
             __threadfence_system();
-            st_release_sys(s.notify[0], s.seq);
-            st_release_sys(s.notify[1], s.seq);
+            st_release_sys(s.notify[0], seq);
+            st_release_sys(s.notify[1], seq);
+            if (s.role == 1) *s.seqp = seq;  // stage complete on this rank
         }
     }
 }
@@ -241,23 +250,37 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     const double dsc = a.dtp ? *a.dtp : 1.0;
     const double dtv = a.dtp ? *a.dtp : a.dt;
     const int ntx = (G.nx + TX - 1) / TX;
-    const int x0 = (int)(blockIdx.x % ntx) * TX, y0 = (int)(blockIdx.x / ntx) * TH;
+    // Paired chunks (a.zpair, zmode 0): CTAs 2t and 2t+1 of a grid row own the same xy tile t
+    // in chunks 2m and 2m+1 and are launched together; the lower one sweeps DOWN from the shared
+    // chunk boundary and the upper one UP from it, so the two planes around that boundary are
+    // read by both at the same moment (the second read hits L2) instead of a chunk-wave apart.
+    const int tile = a.zpair && a.zmode == 0 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int x0 = (tile % ntx) * TX, y0 = (tile / ntx) * TH;
     const int w = min(TX, G.nx - x0), hg = min(TH, G.ny - y0);
 
     int zb, ze;
+    bool desc = false;  // sweep z downwards (from ze-1 to zb)
     if (a.zmode == 0) {
-        zb = a.z_lo + (int)blockIdx.y * a.zchunk;
+        const int chunk = a.zpair ? 2 * (int)blockIdx.y + (int)(blockIdx.x & 1) : (int)blockIdx.y;
+        desc = a.zpair && (blockIdx.x & 1) == 0;
+        zb = a.z_lo + chunk * a.zchunk;
         ze = min(zb + a.zchunk, a.z_hi);
     } else {
         zb = blockIdx.y == 0 ? 0 : G.nzl - 1;
         ze = zb + 1;
     }
-    p2p_wait(a.sync);  // P2P boundary launch: the neighbours' ghost planes have landed
+    const int dz = desc ? -1 : 1;
+    const int zfirst = desc ? ze - 1 : zb;  // first output plane of the sweep
+    const int nout = ze - zb;
+    // sweep plane index i (0 = the z-halo plane before the first output plane) -> global plane
+    auto pidx = [&](int i) INLINE -> int { return desc ? ze - i : zb - 1 + i; };
+    const unsigned long long seq = p2p_wait(a.sync);  // P2P boundary launch: ghost planes landed
+    const bool gpar = (seq & 1ull) != 0;                // P2P: ghost-plane parity of this stage
     if (zb >= ze) {    // CTA-uniform, before any other barrier
-        p2p_notify(a.sync);
+        p2p_notify(a.sync, seq);
         return;
     }
-    const int nplanes = ze - zb + 2;  // planes zb-1 .. ze; plane i is global zb-1+i
+    const int nplanes = ze - zb + 2;  // planes zb-1 .. ze in sweep order (pidx)
 
     // own cells: column lx, rows ly0 + 8r (r < ROWS)
     const int lx = tid % TX, ly0 = tid / TX;
@@ -283,12 +306,12 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
 
     auto stage_of = [&](int i) INLINE -> unsigned char* { return smem + (size_t)(i % R) * LY.stage_bytes; };
     auto issue = [&](int i) INLINE {  // thread 0 only
-        const int p = zb - 1 + i;
+        const int p = pidx(i);
         unsigned char* st = stage_of(i);
         uint64_t* b = &bar[i % R];
         if (plane_is_ghost(a, p)) {
             mbar_expect_tx(b, T::BOX_BYTES);
-            tma_load_4d(st, p < 0 ? &a.tm_glo : &a.tm_ghi, b, x0, y0, 0, 0);
+            tma_load_4d(st, p < 0 ? (gpar ? &a.tm_glo1 : &a.tm_glo) : (gpar ? &a.tm_ghi1 : &a.tm_ghi), b, x0, y0, 0, 0);
         } else {
             const int q = p < 0 ? p + G.nzl : (p >= G.nzl ? p - G.nzl : p);
             // z-halo planes feed only Y: own-cell slots are not loaded there
@@ -396,7 +419,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     {
         wait_plane(0);
         const unsigned char* s0 = stage_of(0);
-        const bool gh = plane_is_ghost(a, zb - 1);
+        const bool gh = plane_is_ghost(a, pidx(0));
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
             Y0[r][0] = y_at(s0, 0, pos[r], gh);
@@ -428,14 +451,15 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         }
     }
 
-    // One output plane z: Ym, Yc hold Y(z-1), Y(z); Yp receives Y(z+1).
-    auto step = [&](int z, double (&Ym)[ROWS][2], double (&Yc)[ROWS][2], double (&Yp)[ROWS][2]) INLINE {
-        const int i = z - zb + 2;  // plane z+1
-        const bool more = z + 1 < ze;  // plane z+1 is an output plane of this CTA
-        // [A] plane z+1 from the ring
+    // Output step k (plane z = zfirst + k*dz): Ym, Yc hold Y(z-dz), Y(z); Yp receives Y(z+dz).
+    auto step = [&](int k, double (&Ym)[ROWS][2], double (&Yc)[ROWS][2], double (&Yp)[ROWS][2]) INLINE {
+        const int z = zfirst + k * dz;
+        const int i = k + 2;         // plane z+dz
+        const bool more = k + 1 < nout;  // plane z+dz is an output plane of this CTA
+        // [A] plane z+dz from the ring
         wait_plane(i);
         const unsigned char* si = stage_of(i);
-        const bool gh = plane_is_ghost(a, z + 1);
+        const bool gh = plane_is_ghost(a, z + dz);
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
             Yp[r][0] = y_at(si, 0, pos[r], gh);
@@ -446,7 +470,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         if constexpr (YD) {
             yc = reinterpret_cast<const double*>(sc);
         } else {
-            const int b = (z - zb) & 1;
+            const int b = k & 1;
             yc = sY + b * 2 * BOX;
             double* yn = sY + (b ^ 1) * 2 * BOX;
             if (more) {
@@ -477,7 +501,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                 const double ctr = Yc[r][c];
                 double s = add(sub(v[-1], ctr), sub(v[1], ctr));
                 s = add(s, add(sub(v[-BW], ctr), sub(v[BW], ctr)));
-                s = add(s, add(sub(Ym[r][c], ctr), sub(Yp[r][c], ctr)));
+                const double zlo = desc ? Yp[r][c] : Ym[r][c], zhi = desc ? Ym[r][c] : Yp[r][c];
+                s = add(s, add(sub(zlo, ctr), sub(zhi, ctr)));  // Y(z-1), then Y(z+1) (R-17)
                 L[c] = mul(s, a.inv_h2);
             }
             const double C0 = Yc[r][0], C1 = Yc[r][1];
@@ -549,16 +574,16 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         }
     };
 
-    int z = zb;
+    int k = 0;
     if constexpr (ROWS == 2 || YD) {  // rotate the z queue by renaming: no register moves
-        for (; z + 2 < ze; z += 3) {
-            step(z, Y0, Y1, Y2);
-            step(z + 1, Y1, Y2, Y0);
-            step(z + 2, Y2, Y0, Y1);
+        for (; k + 2 < nout; k += 3) {
+            step(k, Y0, Y1, Y2);
+            step(k + 1, Y1, Y2, Y0);
+            step(k + 2, Y2, Y0, Y1);
         }
     }
-    for (; z < ze; ++z) {
-        step(z, Y0, Y1, Y2);
+    for (; k < nout; ++k) {
+        step(k, Y0, Y1, Y2);
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
             Y0[r][0] = Y1[r][0]; Y0[r][1] = Y1[r][1];
@@ -566,16 +591,20 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
         }
     }
     if constexpr (RATIO) block_max_to_global(rbits, a.errmax);
-    p2p_notify(a.sync);  // P2P: ghost planes consumed -> the neighbours may overwrite them
+    p2p_notify(a.sync, seq);  // P2P: ghost planes consumed -> the neighbours may overwrite them
 }
 
 // ---- halo-plane pack and ring fill -------------------------------------------------------
 template <int NY>
 __global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, double* __restrict__ dst0,
                                                       double* __restrict__ dst1, const P2pSync sync) {
-    p2p_wait(sync);  // P2P: the neighbours have consumed what the previous use of dst held
-    const double dsc = a.dtp ? *a.dtp : 1.0;  // as in gs_stage_kernel
+    const unsigned long long seq = p2p_wait(sync);  // P2P: the previous use of dst was consumed
+    const double dsc = a.dtp ? *a.dtp : 1.0;         // as in gs_stage_kernel
     const int64_t ps = a.geo.ps, total = 2 * ps;
+    if (seq & 1ull) {  // P2P: ghost planes of parity 1
+        dst0 += 2 * ps;
+        dst1 += 2 * ps;
+    }
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t sel = e / ps, rest = e - sel * ps;
@@ -585,7 +614,7 @@ __global__ void __launch_bounds__(256) gs_pack_kernel(const GsStageArgs a, doubl
         for (int s = 0; s < NY; ++s) v = add(v, mul(mul(dsc, a.g[s]), __ldg(a.slot[s] + base)));
         (sel ? dst1 : dst0)[rest] = v;
     }
-    p2p_notify(sync);  // P2P: ghost planes stored -> neighbours may read them
+    p2p_notify(sync, seq);  // P2P: ghost planes stored -> neighbours may read them
 }
 
 __global__ void fill_ring_kernel(double* __restrict__ p, GridGeom g, int nslices) {
@@ -603,6 +632,27 @@ __global__ void fill_ring_kernel(double* __restrict__ p, GridGeom g, int nslices
             b[(int64_t)(g.ny + 1) * g.P + t + 1] = b[(int64_t)g.P + t + 1];
         }
     }
+}
+
+// Fused allreduce(max) over the ranks' P2P flag blocks (launch_p2p_allreduce_max).  Round r uses
+// slot r & 1 of every block; this rank zeroes its own other slot before arriving (nobody writes
+// it again before every rank has arrived in this round, and it was last read in round r-1).
+struct FlagPtrs {
+    unsigned long long* f[P2P_MAX_WORLD];
+};
+__global__ void p2p_allreduce_max_kernel(unsigned long long* word, FlagPtrs fl, int world, int rank) {
+    unsigned long long* mine = fl.f[rank];
+    const unsigned long long r = mine[P2P_ROUND];
+    const int slot = P2P_RED0 + (int)(r & 1ull);
+    const unsigned long long v = *word;
+    mine[P2P_RED0 + (int)((r + 1) & 1ull)] = 0ull;
+    for (int q = 0; q < world; ++q) atomicMax_system(fl.f[q] + slot, v);
+    __threadfence_system();
+    for (int q = 0; q < world; ++q) atomicAdd_system(fl.f[q] + P2P_ARRIVE, 1ull);
+    const unsigned long long need = (unsigned long long)world * (r + 1);
+    while (ld_acquire_sys(mine + P2P_ARRIVE) < need) __nanosleep(32);
+    *word = ld_acquire_sys(mine + slot);
+    mine[P2P_ROUND] = r + 1;
 }
 
 template <int S, int AD, int I>
@@ -712,6 +762,7 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
         nchunks = (range + a.zchunk - 1) / a.zchunk;
     }
     dim3 grid((unsigned)tiles, (unsigned)nchunks);
+    if (a.zpair && a.zmode == 0) grid = dim3((unsigned)(2 * tiles), (unsigned)((nchunks + 1) / 2));
     if (nlaunch) ++*nlaunch;
     if (adaptive == 2) {  // SPEC's error ratio (R-28)
         switch (scheme) {
@@ -772,6 +823,15 @@ cudaError_t launch_gs_pack(const GsStageArgs& a, double* dst0, double* dst1, con
     case 10: gs_pack_kernel<10><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
     default: return cudaErrorInvalidValue;
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_allreduce_max(unsigned long long* word, unsigned long long* const* flags, int world,
+                                     int rank, cudaStream_t st) {
+    if (world < 1 || world > P2P_MAX_WORLD || rank < 0 || rank >= world) return cudaErrorInvalidValue;
+    FlagPtrs fl{};
+    for (int q = 0; q < world; ++q) fl.f[q] = flags[q];
+    p2p_allreduce_max_kernel<<<1, 1, 0, st>>>(word, fl, world, rank);
     return cudaGetLastError();
 }
 

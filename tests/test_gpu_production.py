@@ -212,3 +212,44 @@ def test_loopback_runs_nccl():
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "nccl_loopback_info.txt"), "w") as f:
         f.write("\n".join(lines[:200]) + "\n")
+
+
+@pytest.mark.parametrize("kind", ["grid", "vector"])
+def test_error_spike_forces_rejection(ctx, kind):
+    """RK_OPT_ERROR_SPIKE (S:L519 criterion 8): the spiked try is rejected, leaves u bitwise
+    unchanged, and shrinks dt by at least the safety factor (here to the 1/5 floor: E >= 1e6);
+    the next tries proceed normally (the host loop and the oracle agree again)."""
+    import paper_2309_05331_b200 as rk
+    if kind == "grid":
+        dims = (24, 16, 12)
+        u0 = rk_inputs.gray_scott_ic(*dims, seed=3) + 0.01 * rk_inputs.random_state(2 * 24 * 16 * 12, 4).reshape(12, 2, 16, 24)
+        st = gs_state(ctx, dims, u0)
+        p = oracle.gray_scott_problem(*dims)
+        dt = 1.0
+    else:
+        n = 1000
+        u0 = rk_inputs.logistic_u0(n)
+        st = ctx.vector(n)
+        st.set_rhs_logistic()
+        st.set(u0)
+        p = oracle.logistic_problem(n)
+        dt = 0.1
+    st.set_option(rk.OPT_ERROR_SPIKE, 1)
+    acc, E, dtn = st.try_step("dopri5", 0.0, dt, 1e-6, 1e-6)
+    assert not acc and E >= 1e6
+    assert bitwise(st.get(), u0)
+    assert dtn <= 0.9 * dt and dtn == dt * 0.2
+    acc, E, dtn2 = st.try_step("dopri5", 0.0, dtn, 1e-6, 1e-6)  # spike consumed: normal try
+    un, err = oracle.step(p, oracle.DOPRI5, 0.0, dtn, u0, with_error=True)
+    assert E == oracle.error_ratio_max(err, u0, oracle.rhs(p, u0), dtn, 1e-6, 1e-6)
+    assert bitwise(st.get(), un if acc else u0)
+    # inside integrate_adaptive: the spiked 2nd try is rejected on top of the natural rejections
+    st.set(u0)
+    a0, r0 = st.integrate_adaptive("dopri5", 0.0, 10 * dt, dt, 1e-6, 1e-6)
+    assert a0 + r0 >= 2
+    st.set(u0)
+    st.set_option(rk.OPT_ERROR_SPIKE, 2)
+    st.reset_stats()
+    a1, r1 = st.integrate_adaptive("dopri5", 0.0, 10 * dt, dt, 1e-6, 1e-6)
+    assert r1 >= r0 + 1 and a1 >= 1 and st.stats()["rejected"] == r1
+    st.close()
