@@ -25,7 +25,7 @@ EULER, RK4, CASH_KARP54, DOPRI5, RKF78, MIDPOINT, MODIFIED_MIDPOINT = 0, 1, 2, 3
 SCHEMES = {"euler": EULER, "rk4": RK4, "cash_karp54": CASH_KARP54, "dopri5": DOPRI5,
            "rkf78": RKF78, "midpoint": MIDPOINT, "modified_midpoint": MODIFIED_MIDPOINT}
 RHS_EXP, RHS_LOGISTIC, RHS_GRAY_SCOTT = 0, 1, 2
-OK, ERR_ARG, ERR_UNSUPPORTED, ERR_DIVERGED, ERR_STALL = 0, 1, 2, 3, 4
+OK, ERR_ARG, ERR_UNSUPPORTED, ERR_DIVERGED, ERR_STALL, ERR_DT_UNDERFLOW = 0, 1, 2, 3, 4, 5
 
 # -O2 -ffp-contract=off: no FMA contraction; no -ffast-math: IEEE division, no FTZ/DAZ.
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]

@@ -424,6 +424,9 @@ int orc_integrate_adaptive_ctrl(const orc_problem* p, int scheme, double* u, dou
             orc_rhs(p, u, k1); /* dxdt at the start of the step (ratio denominator) */
         int tries = 0;
         for (;;) {
+            /* step-size floor (SURVEY §8b RK_ERR_DT_UNDERFLOW; R-29): a try with
+             * dt < 16 eps max(|t|, 1) cannot advance t meaningfully */
+            if (dt < 16.0 * DBL_EPSILON * fmax(fabs(t), 1.0)) { rc = ORC_ERR_DT_UNDERFLOW; goto done; }
             rc = orc_step(p, scheme, t, dt, u, un, er);
             if (rc != ORC_OK) goto done;
             const double E = controller == ORC_CTRL_ODEINT

@@ -32,7 +32,8 @@ enum { ORC_EULER = 0, ORC_RK4 = 1, ORC_CASH_KARP54 = 2, ORC_DOPRI5 = 3, ORC_RKF7
 /* RHS kinds: Eq. 1a as du/dt = lambda*u, Eq. 1b, Eq. 3 / Listing 2. */
 enum { ORC_RHS_EXP = 0, ORC_RHS_LOGISTIC = 1, ORC_RHS_GRAY_SCOTT = 2 };
 /* Status codes. */
-enum { ORC_OK = 0, ORC_ERR_ARG = 1, ORC_ERR_UNSUPPORTED = 2, ORC_ERR_DIVERGED = 3, ORC_ERR_STALL = 4 };
+enum { ORC_OK = 0, ORC_ERR_ARG = 1, ORC_ERR_UNSUPPORTED = 2, ORC_ERR_DIVERGED = 3, ORC_ERR_STALL = 4,
+       ORC_ERR_DT_UNDERFLOW = 5 };
 
 typedef struct {
     int kind;            /* ORC_RHS_* */

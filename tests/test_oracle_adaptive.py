@@ -156,3 +156,19 @@ def test_controller_pow_correctly_rounded():
             else:
                 want_s = dt0 * max(0.2, 0.9 * _cr_pow(E, -1.0 / 4.0))
             assert acc_s == (E <= 1.0) and dt_s == want_s, (E, dt0, dt_s, want_s)
+
+
+def test_dt_underflow_floor():
+    """DESIGN.md R-29: with an unattainable tolerance every try is rejected with the
+    1/5 shrink floor (E ~ 1e290 >> 4.5^3), so dt_k = dt0 * 0.2^k (fp64 products) until the first
+    dt below 16 eps max(|t|, 1); that try is not taken: RK_ERR_DT_UNDERFLOW after exactly k
+    rejections, u untouched.  (An error ratio that is not huge would shrink by less than 5x.)"""
+    n = 8
+    u0 = rk_inputs.logistic_u0(n)
+    dt, k = 0.1, 0
+    while not dt < 16 * np.finfo(float).eps * max(abs(-5.0), 1.0):
+        dt, k = dt * 0.2, k + 1
+    u, acc, rej, rc = oracle.integrate_adaptive(oracle.logistic_problem(n), oracle.DOPRI5, u0, -5.0, 5.0, 0.1,
+                                                1e-300, 1e-300)
+    assert rc == oracle.ERR_DT_UNDERFLOW and acc == 0 and rej == k and k == 19
+    assert np.array_equal(u, u0)
