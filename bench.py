@@ -204,6 +204,34 @@ def oracle_small_configs():
     return out
 
 
+def oracle_full_512():
+    """SURVEY §8d oracle plan at full size (opt-in leg cpu_full, ~1 min, ~25 GB of host RAM): the
+    unmodified single-threaded oracle on the whole 512^3 configs[3] grid -- 2 RK4 steps (dt = 1)
+    and 1 DOPRI5 error-controlled try (7 RHS evaluations, error ratio, max norm, controller)."""
+    import oracle
+    import rk_inputs
+    n = N_PER_GPU
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    p = oracle.gray_scott_problem(n, n, n, h=H)
+    oracle.lib()
+    t = time.perf_counter()
+    u1 = oracle.step(p, oracle.RK4, 0.0, 1.0, u0)
+    oracle.step(p, oracle.RK4, 1.0, 1.0, u1)
+    t_rk4 = time.perf_counter() - t
+    del u1
+    t = time.perf_counter()
+    un, err = oracle.step(p, oracle.DOPRI5, 0.0, 1.0, u0, with_error=True)
+    E = oracle.error_ratio_max(err, u0, oracle.rhs(p, u0), 1.0, TOL, TOL)
+    acc, dtn = oracle.controller(E, 1.0)
+    t_dp = time.perf_counter() - t
+    cells = n ** 3
+    return {"rk4": {"value": 2 * cells / t_rk4, "unit": "cell-updates/s", "seconds": t_rk4, "steps": 2},
+            "dopri5_try": {"value": cells / t_dp, "unit": "cell-tries/s", "seconds": t_dp, "E": E,
+                           "accepted": bool(acc)},
+            "cores": 1, "cpu_model": cpu_model(),
+            "sample": "the whole 512^3 grid (configs[3]), single-threaded C oracle (-O2 -ffp-contract=off)"}
+
+
 def cpu_baseline(nz_sample=128):
     secs, cells = oracle_try_seconds(nz_sample)
     single = cells / secs
@@ -566,9 +594,26 @@ def main():
         # per cell and step: 4 x (Y or u -> k) + 3 x (u, k -> Y) + (u, k1..k4 -> u), 16 B arrays
         bpc = 4 * 32 + 3 * 48 + 96
         ach = bpc * cells_local * args.steps / (ms / 1e3) / 1e9
-        return {"value": cells_total * args.steps / (ms / 1e3), "ms_per_step": ms / args.steps,
-                "scheme": "rk4 unfused (4 eval_rhs + 4 lincomb launches per step)",
-                "algorithmic_bytes_per_cell_step": bpc, "achieved_gbs": ach, "frac_of_peak": ach / peak}
+        out = {"value": cells_total * args.steps / (ms / 1e3), "ms_per_step": ms / args.steps,
+               "scheme": "rk4 unfused (RK_OPT_FUSED_KERNELS = 0: 4 RHS + 4 lincomb launches per step)",
+               "algorithmic_bytes_per_cell_step": bpc, "achieved_gbs": ach, "frac_of_peak": ach / peak}
+        # the headline integration in the unfused dataflow (Y_i, k_i, u_new, e through HBM)
+        st.set_option(rk.OPT_FUSED_KERNELS, 0)
+        integrate_step(u0_dev)
+        ms_d = []
+        for _ in range(max(1, min(args.steps, 3))):
+            barrier()
+            ev0.record(stream)
+            a, r = integrate_step(u0_dev)
+            ev1.record(stream)
+            barrier()
+            ms_d.append(max_over_ranks(ev0.elapsed_time(ev1)))
+        st.set_option(rk.OPT_FUSED_KERNELS, 1)
+        m = statistics.median(ms_d)
+        out["dopri5_adaptive_unfused"] = {"value": cells_total * a / (m / 1e3), "unit": "cell-updates/s",
+                                          "ms_per_integration": m, "ms_per_try": m / (a + r), "accepted": a,
+                                          "rejected": r}
+        return out
 
     def exp512_leg():
         # f4: the exponential-family workload: 512 x 512 = 262,144
@@ -923,6 +968,8 @@ def main():
         line["e2e"] = e2e_leg()
     if "cpu" in legs and rank == 0 and world == 1:
         line["cpu_baseline"] = cpu_baseline()
+    if "cpu_full" in legs and rank == 0 and world == 1:  # opt-in: ~1 min, ~25 GB host RAM
+        line.setdefault("cpu_baseline", {})["full_512"] = oracle_full_512()
     if rank == 0:
         print(json.dumps(line), flush=True)
     st.close()

@@ -34,6 +34,7 @@
 #ifndef RK_B200_H
 #define RK_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -167,12 +168,21 @@ typedef enum {
                                 raised to at least 1e6 before the allreduce, forcing a rejection
                                 on every rank (u unchanged, dt shrunk by the controller's floor).
                                 Counted per rank; 0 (default): off.                          */
-    RK_OPT_CHECK_ARGS = 14    /* debug (SURVEY §8b "Collectives"): 1 -- every collective call
+    RK_OPT_CHECK_ARGS = 14,   /* debug (SURVEY §8b "Collectives"): 1 -- every collective call
                                 (do_step, try_step, integrate_*, norm_inf, eval_rhs) first
                                 all-reduces a hash of its call kind and scalar arguments and
                                 returns RK_ERR_CONTRACT on every rank when the ranks disagree
                                 (a mismatched MPI-style call sequence).  Costs one host sync per
                                 call.  0 (default): off.                                       */
+    RK_OPT_FUSED_KERNELS = 15 /* 1 (default): the fused stage kernels (stage values formed inside
+                                the RHS kernel, final combination and error ratio in the last
+                                stage's epilogue).  0: the unfused, Odeint-like dataflow (SURVEY
+                                §8b; the f4 ablation): per stage one lincomb launch
+                                writes Y_i and one RHS launch k_i = F(Y_i), then lincomb
+                                launches for u_new and the error estimate and a ratio-max
+                                launch -- every intermediate through HBM, the same sums in the
+                                same order, so bitwise the same results.  Runge–Kutta schemes,
+                                fixed and error-controlled (host loop); Adams steps unaffected.*/
 } rk_option;
 
 /* Counters since creation or the last rk_reset_stats. */
@@ -248,6 +258,16 @@ rk_status rk_nccl_unique_id(void* out);
 rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* cuda_stream,
                         rk_ctx* out);
 rk_status rk_ctx_destroy(rk_ctx ctx);
+/* Optional device allocator for the state arrays (u, u_new, the k_j / history / stage buffers,
+ * halo send and ghost buffers), e.g. to route them through torch's caching allocator (SURVEY
+ * §8b "allocator hook").  alloc(bytes, stream, user) returns device memory on the ctx device,
+ * usable on `stream` (the ctx stream), or NULL (-> RK_ERR_OOM); free(ptr, stream, user) releases
+ * it.  Both or neither (NULL, NULL: cudaMalloc / cudaFree, the default).  Must be set before the
+ * first state is created (RK_ERR_STATE otherwise); the functions must stay valid until every
+ * state is destroyed.  Buffers shared through CUDA IPC (P2P transport) always use cudaMalloc. */
+typedef void* (*rk_alloc_fn)(size_t bytes, void* stream, void* user);
+typedef void (*rk_free_fn)(void* ptr, void* stream, void* user);
+rk_status rk_ctx_set_allocator(rk_ctx ctx, rk_alloc_fn alloc, rk_free_fn free_fn, void* user);
 
 /* ---- state --------------------------------------------------------------------------- */
 /* Distributed Nx x Ny x Nz periodic grid of ncomp fp64 components, z-slab partitioned

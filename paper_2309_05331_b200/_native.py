@@ -16,7 +16,7 @@ STATUS = {0: "RK_OK", 1: "RK_ERR_ARG", 2: "RK_ERR_CONTRACT", 3: "RK_ERR_UNSUPPOR
           8: "RK_ERR_CUDA", 9: "RK_ERR_NCCL", 10: "RK_ERR_OOM"}
 OPT_HALO_OVERLAP, OPT_HALO_LOOPBACK, OPT_MAX_TRIES, OPT_TIMING, OPT_USE_GRAPH, OPT_DEVICE_LOOP, OPT_HALO_P2P = 1, 2, 3, 4, 5, 6, 7
 OPT_CONTROLLER, OPT_CHECK_FINITE, OPT_COOP_MAX_CELLS = 8, 9, 10
-OPT_FUSED_STEP, OPT_COMM_TIMEOUT_MS, OPT_ERROR_SPIKE, OPT_CHECK_ARGS = 11, 12, 13, 14
+OPT_FUSED_STEP, OPT_COMM_TIMEOUT_MS, OPT_ERROR_SPIKE, OPT_CHECK_ARGS, OPT_FUSED_KERNELS = 11, 12, 13, 14, 15
 CTRL_ODEINT, CTRL_SPEC = 0, 1
 ABI_VERSION = 3
 UNIQUE_ID_BYTES = 128
@@ -69,6 +69,7 @@ SIGNATURES = {
     "rk_nccl_unique_id": (_i, [_v]),
     "rk_ctx_create": (_i, [_i, _i, _i, _v, _v, _p(_v)]),
     "rk_ctx_destroy": (_i, [_v]),
+    "rk_ctx_set_allocator": (_i, [_v, _v, _v, _v]),
     "rk_state_create_grid": (_i, [_v, _i64, _i64, _i64, _i, _p(_v)]),
     "rk_state_create_vector": (_i, [_v, _i64, _i, _p(_v)]),
     "rk_state_destroy": (_i, [_v]),

@@ -38,6 +38,27 @@ def _stream_handle(stream) -> int | None:
     return h if h != 0 else 1
 
 
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+
+def _torch_allocator(device: int):
+    """ctypes callbacks routing the library's state arrays through torch's caching allocator
+    (plumbing only: the library still owns what it computes)."""
+    import torch
+
+    def alloc(nbytes, stream, _user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device, stream or 0)
+        except Exception:  # noqa: BLE001  (an exception must not cross the C ABI: NULL = OOM)
+            return None
+
+    def free(ptr, _stream, _user):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    return _ALLOC_FN(alloc), _FREE_FN(free)
+
+
 def _order_after_torch(t) -> None:
     """The library copies on the ctx stream, which need not be torch's current stream: let the
     torch work already queued on `t` (writes before set, reads before get) finish first."""
@@ -67,7 +88,7 @@ class Context:
     IPC handles over ``p2p_group`` (a torch process group, e.g. gloo) when it is created."""
 
     def __init__(self, rank: int = 0, world: int = 1, device: int = 0, stream=None,
-                 unique_id: bytes | None = None, p2p_group=None):
+                 unique_id: bytes | None = None, p2p_group=None, allocator: str | None = None):
         L = _native.lib()
         h = ctypes.c_void_p()
         uid = None
@@ -85,6 +106,13 @@ class Context:
         self._L = L
         self._states = weakref.WeakSet()
         self.rank, self.world, self.device = rank, world, device
+        self._alloc_cbs = None
+        if allocator == "torch":  # state arrays from torch's caching allocator (rk_ctx_set_allocator)
+            self._alloc_cbs = _torch_allocator(device)
+            call("rk_ctx_set_allocator", h, ctypes.cast(self._alloc_cbs[0], ctypes.c_void_p),
+                 ctypes.cast(self._alloc_cbs[1], ctypes.c_void_p), None)
+        elif allocator is not None:
+            raise ValueError("allocator: None (cudaMalloc) or 'torch'")
 
     @staticmethod
     def nccl_unique_id() -> bytes:

@@ -62,6 +62,39 @@ __global__ void __launch_bounds__(256) norm_inf_kernel(const double* __restrict_
     block_max_to_global(m, out);
 }
 
+// Unfused error control (RK_OPT_FUSED_KERNELS = 0): r = |e| / (atol + rtol*(|u| + dt*|k1|))
+// (Odeint, R-12; w = k1) or |e| / (atol + rtol*max(|u|, |u_new|)) (SPEC, R-28; w = u_new) per
+// element, the max over their bit patterns -- the fused epilogue's expression trees (R-17).
+__global__ void __launch_bounds__(256) ratio_max_kernel(const double* __restrict__ e, const double* __restrict__ u,
+                                                        const double* __restrict__ w, int64_t n, double dt,
+                                                        double atol, double rtol, int spec,
+                                                        unsigned long long* out) {
+    unsigned long long m = 0ull;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double d;
+        if (spec) {
+            const double a = fabs(__ldg(u + i)), b = fabs(__ldg(w + i));
+            d = add(atol, mul(rtol, a >= b ? a : b));
+        } else {
+            d = add(atol, mul(rtol, add(fabs(__ldg(u + i)), mul(dt, fabs(__ldg(w + i))))));
+        }
+        const unsigned long long bits = ratio_bits(fabs(__ldg(e + i)) / d);
+        m = bits > m ? bits : m;
+    }
+    block_max_to_global(m, out);
+}
+
+cudaError_t launch_ratio_max(const double* e, const double* u, const double* w, int64_t count, double dt,
+                             double atol, double rtol, int spec, unsigned long long* out, cudaStream_t st,
+                             int num_sms) {
+    int64_t blocks = (count + 255) / 256;
+    if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
+    if (blocks < 1) blocks = 1;
+    ratio_max_kernel<<<(unsigned)blocks, 256, 0, st>>>(e, u, w, count, dt, atol, rtol, spec, out);
+    return cudaGetLastError();
+}
+
 // RK_OPT_ERROR_SPIKE: raise a try's local error-ratio max to at least v (fault injection)
 __global__ void inject_max_kernel(unsigned long long* word, double v) { atomicMax(word, ratio_bits(v)); }
 

@@ -245,6 +245,11 @@ struct LincombArgs {
 cudaError_t launch_lincomb(const LincombArgs& a, cudaStream_t st, int num_sms);
 cudaError_t launch_norm_inf(const double* x, int64_t count, unsigned long long* out,
                             cudaStream_t st, int num_sms);
+// K4 (unfused error control): max over elements of the error ratio (spec = 0: w = k1, Odeint's
+// denominator; spec = 1: w = u_new, SPEC's) into *out as uint64 bits (atomicMax)
+cudaError_t launch_ratio_max(const double* e, const double* u, const double* w, int64_t count, double dt,
+                             double atol, double rtol, int spec, unsigned long long* out, cudaStream_t st,
+                             int num_sms);
 // atomicMax(word, bits of v) (v >= 0): fault injection into an error-ratio max
 cudaError_t launch_inject_max(unsigned long long* word, double v, cudaStream_t st);
 

@@ -64,6 +64,11 @@ struct rk_ctx_s {
     // RK_OPT_COMM_TIMEOUT_MS clock whenever one of them completes (ctx_wait)
     std::deque<cudaEvent_t> marks;
     std::vector<cudaEvent_t> mark_pool;
+    // rk_ctx_set_allocator: the caller's device allocator for state arrays (e.g. torch's caching
+    // allocator); null: cudaMalloc / cudaFree
+    rk_alloc_fn alloc_fn = nullptr;
+    rk_free_fn free_fn = nullptr;
+    void* alloc_user = nullptr;
 };
 
 #define CK_CTX(ctx, call)                                                                     \
@@ -258,6 +263,10 @@ struct rk_state_s {
     int64_t coop_max_cells = 1 << 18;  // RK_OPT_COOP_MAX_CELLS: persistent-step path up to here
     bool fused = false;          // RK_OPT_FUSED_STEP: K6 whole-step launches (RK4, midpoint)
     int64_t spike_at = 0, spike_seen = 0;  // RK_OPT_ERROR_SPIKE: inject at try number spike_at
+    bool fused_kernels = true;   // RK_OPT_FUSED_KERNELS = 0: Odeint-like unfused stages (ablation)
+    double* uf_y = nullptr;      // unfused: the stage value Y_i and the error estimate e
+    double* uf_e = nullptr;
+    Maps tm_uf_y{};
     bool check_args = false;     // RK_OPT_CHECK_ARGS: hash-compare collective call arguments
     const double* gl_dtp = nullptr;  // set while capturing the device-resident try loop (GLoop)
     struct GraphLoop* gloop = nullptr;
@@ -273,15 +282,29 @@ static rk_status check_state(rk_state st) {
     return RK_OK;
 }
 
+// State arrays: through the caller's allocator when one is set (rk_ctx_set_allocator), else
+// cudaMalloc.  Buffers shared with other processes (P2P ghost planes, flags) always use cudaMalloc
+// (CUDA IPC needs whole allocations).
 static rk_status dev_alloc(rk_ctx ctx, double** p, int64_t count) {
-    cudaError_t e = cudaMalloc((void**)p, sizeof(double) * (size_t)std::max<int64_t>(count, 1));
+    const size_t bytes = sizeof(double) * (size_t)std::max<int64_t>(count, 1);
+    if (ctx->alloc_fn) {
+        *p = static_cast<double*>(ctx->alloc_fn(bytes, (void*)ctx->stream, ctx->alloc_user));
+        if (!*p) return fail(RK_ERR_OOM, "the caller's allocator returned NULL for %zu bytes", bytes);
+        return RK_OK;
+    }
+    cudaError_t e = cudaMalloc((void**)p, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(RK_ERR_OOM, "cudaMalloc of %lld doubles failed: %s", (long long)count,
                     cudaGetErrorString(e));
     }
-    (void)ctx;
     return RK_OK;
+}
+
+static void dev_free(rk_ctx ctx, void* p) {
+    if (!p) return;
+    if (ctx->free_fn) ctx->free_fn(p, (void*)ctx->stream, ctx->alloc_user);
+    else cudaFree(p);
 }
 
 // zero-filled array (pads and ring corners stay 0) with its TMA tensor maps (grids)
@@ -456,17 +479,6 @@ static rk_status ensure_halo(rk_state st) {
     return RK_OK;
 }
 
-// Paired opposite-direction chunk sweeps in K3 (rk_stencil.cu); RKB_ZPAIR=0/1 is a developer
-// knob for A/B measurements.
-static int zpair_default() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("RKB_ZPAIR");
-        v = e ? (atoi(e) != 0) : 1;
-    }
-    return v;
-}
-
 static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double atol, double rtol) {
     GsStageArgs a{};
     a.geo = st->geo;
@@ -509,7 +521,7 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     a.z_lo = 0;
     a.z_hi = (int)st->local;
     a.zmode = 0;
-    a.zpair = zpair_default();
+    a.zpair = 0;  // set with the z chunk (pick_zchunk)
     return a;
 }
 
@@ -532,20 +544,38 @@ static GsStageArgs pack_args(const GsStageArgs& a, const StagePlan& p) {
 // 8 for Y-direct stages, 16 for other two-row stages and for the multi-output write-ahead
 // stage (2.88 ms at 16 vs 3.26 at 32, 3.67 at 48 for DOPRI5's, gpurun_out tune_zc*), 48
 // otherwise.  Small grids: shorten further so every SM gets work.
+// Stage classes for the z-chunk policy: 0 Y-direct (no slot enters Y), 1 other two-row stages,
+// 2 AHEAD / EPART, 3 the rest, 4 Adams–Bashforth with one or two history slots (Y-direct too;
+// measured at 512^3: AB2 1.59 -> 1.48 ms, AB3 1.72 -> 1.68 ms at 4 planes instead of 8, while
+// AB4 is flat and AB8 loses, gpurun_out zab2*)
+static int stage_class(const StagePlan& p) {
+    bool yd = true;
+    for (int s = 0; s < p.sp.nslots; ++s) yd = yd && !p.sp.gnz[s];
+    return yd ? (p.sp.epi == EPI_AB && p.sp.nslots > 0 && p.sp.nslots <= 2 ? 4 : 0)
+              : (stage_rows(p.sp) == 2 ? 1 : (p.sp.epi == EPI_FINAL_EPART || p.sp.epi == EPI_AHEAD ? 2 : 3));
+}
+
+// Paired opposite-direction chunk sweeps (GsStageArgs::zpair, rk_stencil.cu) per stage class:
+// measured per stage at 512^3 (ncu, profiles/r2_zpair_ab.txt) they cut the DRAM reads of the
+// 16-plane classes 1 and 2 (write-ahead stage 12.18 -> 11.51 GB, 2.466 -> 2.424 ms; light
+// k-stages 4.83 -> 4.61 GB) but add reads to the short Y-direct chunks and slow the 48-plane
+// stages, so classes 1 and 2 only.  RKB_ZPAIR = class bitmask (developer knob).
+static int stage_zpair(const StagePlan& p) {
+    static int mask = -1;
+    if (mask < 0) {
+        const char* e = getenv("RKB_ZPAIR");
+        mask = e ? atoi(e) : 0x6;
+    }
+    return (mask >> stage_class(p)) & 1;
+}
+
 static int pick_zchunk(rk_state st, const StagePlan& p, int range) {
     if (range <= 0) return 1;
     if (const char* e = getenv("RKB_ZCHUNK")) {  // developer tuning knob
         const int v = atoi(e);
         if (v > 0) return std::min(v, range);
     }
-    // classes: 0 Y-direct (no slot enters Y), 1 other two-row stages, 2 AHEAD / EPART, 3 the rest,
-    // 4 Adams–Bashforth with one or two history slots (Y-direct too; measured at 512^3: AB2
-    // 1.59 -> 1.48 ms, AB3 1.72 -> 1.68 ms at 4 planes instead of 8, while AB4 is flat and AB8
-    // loses, gpurun_out zab2*)
-    bool yd = true;
-    for (int s = 0; s < p.sp.nslots; ++s) yd = yd && !p.sp.gnz[s];
-    const int cls = yd ? (p.sp.epi == EPI_AB && p.sp.nslots > 0 && p.sp.nslots <= 2 ? 4 : 0)
-                       : (stage_rows(p.sp) == 2 ? 1 : (p.sp.epi == EPI_FINAL_EPART || p.sp.epi == EPI_AHEAD ? 2 : 3));
+    const int cls = stage_class(p);
     static int tab[5] = {0, 0, 0, 0, 0};
     static bool parsed = false;
     if (!parsed) {  // developer tuning knob RKB_ZC="yd,light,epart,heavy,ab"
@@ -647,7 +677,7 @@ static rk_status p2p_alloc(rk_state st) {
     rk_ctx ctx = st->ctx;
     if (st->grid) {
         const int64_t pv = plane_values(st);
-        TRY(dev_alloc(ctx, &st->pghost, 4 * pv));
+        CK_CTX(ctx, cudaMalloc((void**)&st->pghost, sizeof(double) * 4 * pv));  // IPC-exported
         CK_CTX(ctx, cudaMemsetAsync(st->pghost, 0, sizeof(double) * 4 * pv, ctx->stream));
         for (int b = 0; b < 2; ++b)
             for (int g = 0; g < 2; ++g)
@@ -783,6 +813,7 @@ static rk_status run_gs_stage_p2p(rk_state st, const StagePlan& p, GsStageArgs& 
         in.z_lo = 1;
         in.z_hi = nzl - 1;
         in.zchunk = pick_zchunk(st, p, nzl - 2);
+        in.zpair = stage_zpair(p);
         TRY(launch_stage_timed(st, p, in));
     }
     GsStageArgs bd = a;
@@ -831,6 +862,7 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
     st->stats.rhs_evals += 1;
     if (!halo_path(st)) {
         a.zchunk = pick_zchunk(st, p, nzl);
+        a.zpair = stage_zpair(p);
         return launch_stage_timed(st, p, a);
     }
     if (st->p2p) return run_gs_stage_p2p(st, p, a);
@@ -852,6 +884,7 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
         in.z_lo = 1;
         in.z_hi = nzl - 1;
         in.zchunk = pick_zchunk(st, p, nzl - 2);
+        in.zpair = stage_zpair(p);
         TRY(launch_stage_timed(st, p, in));
         CK_CTX(ctx, cudaStreamWaitEvent(ctx->bnd, st->ev_halo, 0));
         GsStageArgs bd = a;
@@ -866,6 +899,7 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
     TRY(halo_exchange(st, ctx->stream));
     CK_CTX(ctx, cudaStreamWaitEvent(ctx->stream, st->ev_halo, 0));
     a.zchunk = pick_zchunk(st, p, nzl);
+    a.zpair = stage_zpair(p);
     return launch_stage_timed(st, p, a);
 }
 
@@ -1128,8 +1162,114 @@ static rk_status fused_steps(rk_state st, int scheme, double dt, int64_t n) {
     return RK_OK;
 }
 
+// ---- RK_OPT_FUSED_KERNELS = 0: the unfused, Odeint-like dataflow (f4 ablation) ----
+// Every stage value Y_i = u + sum_j (dt a_ij) k_j goes through HBM (one lincomb launch), every
+// k_i = F(Y_i) is one RHS launch (the k1-type stage kernel reading Y_i, halo path included),
+// then u_new = u + sum_j (dt b_j) k_j and, under error control, e = sum_j (dt e_j) k_j (lincomb)
+// and the ratio max (ratio_max_kernel).  The same left-to-right sums over the nonzero
+// coefficients as the fused kernels and the oracle (R-17): bitwise the same results, only the
+// traffic differs (SURVEY §8d "arrays (unfused Odeint-like dataflow)").
+static rk_status uf_lincomb(rk_state st, double* out, int k, const double* coef, double* const* in) {
+    LincombArgs a{};
+    a.out = out;
+    a.k = k;
+    a.count = st->alloc;  // padded grids: ring copies combine linearly, pads stay 0
+    for (int j = 0; j < k; ++j) {
+        a.in[j] = in[j];
+        a.coef[j] = coef[j];
+    }
+    CK_CTX(st->ctx, launch_lincomb(a, st->ctx->stream, st->ctx->num_sms));
+    st->stats.kernel_launches += 1;
+    st->stats.stage_bytes += (int64_t)(k + 1) * st->count * (int64_t)sizeof(double);
+    return RK_OK;
+}
+
+// k = F(y): the k1-type stage (grids: K3 with y as its base array, exchanging y's boundary
+// planes on the halo path; vectors: the pointwise RHS kernel)
+static rk_status uf_eval(rk_state st, double* y, const Maps& ym, double* out) {
+    if (!st->grid) {
+        CK_CTX(st->ctx, launch_rhs_pointwise(y, out, st->count, st->rhs, st->lambda, st->ctx->stream, st->ctx->num_sms));
+        st->stats.kernel_launches += 1;
+        st->stats.rhs_evals += 1;
+        st->stats.stage_bytes += 2 * st->count * (int64_t)sizeof(double);
+        return RK_OK;
+    }
+    double* const u = st->u;
+    const Maps mu = st->tm_u;
+    st->u = y;
+    st->tm_u = ym;
+    StagePlan p = build_plan(RK_RK4, 0, 0.0)[0];
+    p.out_ptr = out;
+    const rk_status rc = run_gs_stage(st, p, 0.0, 0.0, 0.0);
+    st->u = u;
+    st->tm_u = mu;
+    return rc;
+}
+
+// the stages of one step (err = false) or one try (err = true) into st->u_new (and st->d_err)
+static rk_status unfused_stages(rk_state st, int scheme, double dt, bool err, double atol, double rtol) {
+    rk_ctx ctx = st->ctx;
+    const Coeffs C = coeffs_of(scheme);
+    const int s = num_stages(scheme, err);
+    TRY(ensure_k(st, s));
+    if (!st->uf_y) {
+        TRY(alloc_array(st, &st->uf_y, &st->tm_uf_y));
+        TRY(alloc_array(st, &st->uf_e, nullptr));
+    }
+    double coef[14];
+    double* in[14];
+    for (int i = 0; i < s; ++i) {
+        if (i == 0) {
+            if (st->k1_valid) continue;
+            TRY(uf_eval(st, st->u, st->tm_u, st->k[0]));
+            st->k1_valid = true;
+            continue;
+        }
+        int n = 0;
+        coef[n] = 1.0;
+        in[n++] = st->u;
+        for (int j = 0; j < i; ++j)
+            if (C.a[i][j] != 0.0) {
+                coef[n] = dt * C.a[i][j];
+                in[n++] = st->k[j];
+            }
+        TRY(uf_lincomb(st, st->uf_y, n, coef, in));  // Y_i
+        TRY(uf_eval(st, st->uf_y, st->tm_uf_y, st->k[i]));
+    }
+    int n = 0;
+    coef[n] = 1.0;
+    in[n++] = st->u;
+    for (int j = 0; j < s; ++j)
+        if (C.b[j] != 0.0) {
+            coef[n] = dt * C.b[j];
+            in[n++] = st->k[j];
+        }
+    TRY(uf_lincomb(st, st->u_new, n, coef, in));  // u_new
+    if (!err) return RK_OK;
+    n = 0;
+    for (int j = 0; j < s; ++j)
+        if (C.e[j] != 0.0) {
+            coef[n] = dt * C.e[j];
+            in[n++] = st->k[j];
+        }
+    TRY(uf_lincomb(st, st->uf_e, n, coef, in));  // e
+    CK_CTX(ctx, cudaMemsetAsync(st->d_err, 0, sizeof(unsigned long long), ctx->stream));
+    const bool spec = st->controller == 1;
+    CK_CTX(ctx, launch_ratio_max(st->uf_e, st->u, spec ? st->u_new : st->k[0], st->alloc, dt, atol, rtol,
+                                 spec ? 1 : 0, st->d_err, ctx->stream, ctx->num_sms));
+    st->stats.kernel_launches += 1;
+    st->stats.stage_bytes += 3 * st->count * (int64_t)sizeof(double);
+    return RK_OK;
+}
+
 // one fixed Runge–Kutta step, u <- u_new (does not touch the Adams–Bashforth history)
 static rk_status rk_fixed_step(rk_state st, int scheme, double dt) {
+    if (!st->fused_kernels) {
+        TRY(unfused_stages(st, scheme, dt, false, 0.0, 0.0));
+        swap_u(st);
+        st->stats.steps += 1;
+        return RK_OK;
+    }
     if (coop_path(st, scheme)) return coop_steps(st, scheme, dt, 1);
     if (fused_path(st, scheme)) return fused_steps(st, scheme, dt, 1);
     if (st->grid) {
@@ -1291,7 +1431,11 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
     const Coeffs C = coeffs_of(scheme);
     ab_invalidate(st);
     int fsal_k = -1;  // FSAL: buffer holding k_s = F(u_new), the next step's k1
-    if (st->grid) {
+    if (!st->fused_kernels) {
+        TRY(unfused_stages(st, scheme, dt, true, atol, rtol));
+        const Tableau T = tableau_of(scheme);
+        if (is_fsal(T, true)) fsal_k = last_stage(T, true);
+    } else if (st->grid) {
         auto plan = build_plan(scheme, st->controller == 1 ? 2 : 1, dt);
         if (plan.back().sp.epi == EPI_TAIL_ERR) fsal_k = plan.back().sp.out_k;
         TRY(run_grid_plan(st, plan, dt, atol, rtol));
@@ -1574,7 +1718,8 @@ static void gloop_destroy(rk_state st) {
 // kernels); the NCCL transport keeps the host loop (NCCL calls inside conditional graph bodies
 // are not relied on)
 static bool gloop_path(rk_state st) {
-    return st->device_loop && st->grid && st->rhs == RHS_GRAY_SCOTT && (!halo_path(st) || p2p_needed(st)) &&
+    return st->device_loop && st->fused_kernels && st->grid && st->rhs == RHS_GRAY_SCOTT &&
+           (!halo_path(st) || p2p_needed(st)) &&
            st->check_finite == 0 && !st->timing;
 }
 
@@ -1936,6 +2081,16 @@ rk_status rk_ctx_create(int rank, int world, int device, const void* uid, void* 
     return RK_OK;
 }
 
+rk_status rk_ctx_set_allocator(rk_ctx ctx, rk_alloc_fn alloc, rk_free_fn free_fn, void* user) {
+    if (!ctx) return fail(RK_ERR_ARG, "null ctx");
+    if ((alloc == nullptr) != (free_fn == nullptr)) return fail(RK_ERR_ARG, "set both allocator functions or neither");
+    if (!ctx->states.empty()) return fail(RK_ERR_STATE, "set the allocator before creating states");
+    ctx->alloc_fn = alloc;
+    ctx->free_fn = free_fn;
+    ctx->alloc_user = user;
+    return RK_OK;
+}
+
 rk_status rk_ctx_destroy(rk_ctx ctx) {
     if (!ctx) return RK_OK;
     DeviceGuard g(ctx->device);
@@ -2045,14 +2200,17 @@ rk_status rk_state_destroy(rk_state st) {
         return RK_OK;
     }
     gloop_destroy(st);
-    cudaFree(st->u);
-    cudaFree(st->u_new);
-    for (int j = 0; j < st->nk; ++j) cudaFree(st->k[j]);
-    for (int j = 0; j < st->nhist; ++j) cudaFree(st->hist[j]);
-    cudaFree(st->ybuf[0]);
-    cudaFree(st->ybuf[1]);
-    cudaFree(st->sendbuf);
-    cudaFree(st->ghostbuf);
+    rk_ctx cx = st->ctx;
+    dev_free(cx, st->uf_y);
+    dev_free(cx, st->uf_e);
+    dev_free(cx, st->u);
+    dev_free(cx, st->u_new);
+    for (int j = 0; j < st->nk; ++j) dev_free(cx, st->k[j]);
+    for (int j = 0; j < st->nhist; ++j) dev_free(cx, st->hist[j]);
+    dev_free(cx, st->ybuf[0]);
+    dev_free(cx, st->ybuf[1]);
+    dev_free(cx, st->sendbuf);
+    dev_free(cx, st->ghostbuf);
     for (void* m : st->ipc_mapped)
         if (m) cudaIpcCloseMemHandle(m);
     cudaFree(st->pghost);
@@ -2219,6 +2377,10 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
         st->spike_seen = 0;
         break;
     case RK_OPT_CHECK_ARGS: st->check_args = value != 0; break;
+    case RK_OPT_FUSED_KERNELS:
+        if (st->fused_kernels != (value != 0)) st->k1_valid = false;  // k buffers are laid out differently
+        st->fused_kernels = value != 0;
+        break;
     case RK_OPT_HALO_P2P:
         if (value == 0 && st->ctx->world > 1 && !st->ctx->nccl)
             return fail(RK_ERR_ARG, "a context without NCCL has only the P2P transport");
@@ -2285,6 +2447,8 @@ rk_status rk_integrate_const(rk_state st, rk_scheme scheme, double t0, double t1
         TRY(ab_steps(st, scheme - kSchemeAB0, dt, n));
     } else if (is_abm_scheme(scheme)) {
         TRY(ab_steps(st, scheme - kSchemeABM0, dt, n, true));
+    } else if (!st->fused_kernels) {
+        for (int64_t i = 0; i < n; ++i) TRY(fixed_step(st, scheme, dt));
     } else if (!st->grid) {
         // pointwise RHS: all n steps of every element in registers, chunked launches
         ab_invalidate(st);
@@ -2326,7 +2490,7 @@ rk_status rk_integrate_adaptive(rk_state st, rk_scheme scheme, double t0, double
     TRY(check_rhs(st));
     DeviceGuard g(st->ctx->device);
     TRY(check_collective_args(st, 4, {(double)scheme, t0, t1, dt0, atol, rtol}));
-    if (st->device_loop && st->ctx->world == 1 &&
+    if (st->device_loop && st->fused_kernels && st->ctx->world == 1 &&
         (!st->grid || (!st->loopback && !st->p2p && st->local * st->nx * st->ny <= st->coop_max_cells))) {
         TRY(device_adaptive_loop(st, scheme, t0, t1, dt0, atol, rtol, accepted, rejected));
         return finite_check(st, 0, t1, true);

@@ -253,3 +253,109 @@ def test_error_spike_forces_rejection(ctx, kind):
     a1, r1 = st.integrate_adaptive("dopri5", 0.0, 10 * dt, dt, 1e-6, 1e-6)
     assert r1 >= r0 + 1 and a1 >= 1 and st.stats()["rejected"] == r1
     st.close()
+
+
+@pytest.mark.parametrize("scheme", ["euler", "rk4", "cash_karp54", "dopri5", "rkf78", "midpoint", "modified_midpoint"])
+@pytest.mark.parametrize("loopback", [0, 1])
+def test_unfused_kernels_fixed_bitwise(ctx, scheme, loopback):
+    """RK_OPT_FUSED_KERNELS = 0 (the Odeint-like unfused dataflow): every stage value
+    and k_j through HBM, the same sums -- bitwise equal to the oracle (and so to the fused path)."""
+    import paper_2309_05331_b200 as rk
+    dims = (33, 17, 9)
+    u0 = rk_inputs.gray_scott_ic(*dims, seed=5) + 0.01 * rk_inputs.random_state(2 * 33 * 17 * 9, 6).reshape(9, 2, 17, 33)
+    st = gs_state(ctx, dims, u0, loopback)
+    st.set_option(rk.OPT_FUSED_KERNELS, 0)
+    p = oracle.gray_scott_problem(*dims)
+    u = u0
+    for k in range(2):
+        st.do_step(scheme, float(k), 1.0)
+        u = oracle.step(p, OS[scheme], float(k), 1.0, u)
+        assert bitwise(st.get(), u), (scheme, k)
+    st.close()
+
+
+@pytest.mark.parametrize("scheme", ["dopri5", "cash_karp54", "rkf78"])
+@pytest.mark.parametrize("ctrl", [0, 1], ids=["odeint", "spec"])
+@pytest.mark.parametrize("kind", ["grid", "grid_loopback", "vector"])
+def test_unfused_kernels_adaptive(ctx, scheme, ctrl, kind):
+    import paper_2309_05331_b200 as rk
+    if kind == "vector":
+        n = 5000
+        u0 = rk_inputs.logistic_u0(n)
+        st = ctx.vector(n)
+        st.set_rhs_logistic()
+        st.set(u0)
+        p, t0, t1, dt0, tol = oracle.logistic_problem(n), -5.0, 5.0, 0.1, 1e-8
+    else:
+        dims = (24, 16, 12)
+        u0 = rk_inputs.gray_scott_ic(*dims, seed=7) + 0.02 * rk_inputs.random_state(2 * 24 * 16 * 12, 8).reshape(12, 2, 16, 24)
+        st = gs_state(ctx, dims, u0, 1 if kind == "grid_loopback" else 0)
+        p, t0, t1, dt0, tol = oracle.gray_scott_problem(*dims), 0.0, 12.0, 4.0, 1e-6
+    st.set_option(rk.OPT_FUSED_KERNELS, 0)
+    st.set_option(rk.OPT_CONTROLLER, ctrl)
+    a, r = st.integrate_adaptive(scheme, t0, t1, dt0, tol, tol)
+    uo, ao, ro, rc = oracle.integrate_adaptive_ctrl(p, OS[scheme], u0, t0, t1, dt0, tol, tol, ctrl)
+    assert rc == 0 and (a, r) == (ao, ro)
+    assert bitwise(st.get(), uo)
+    st.close()
+
+
+@pytest.mark.parametrize("kind", ["vector", "grid"])
+@pytest.mark.parametrize("device_loop", [0, 1])
+def test_dt_underflow_parity(ctx, kind, device_loop):
+    """RK_ERR_DT_UNDERFLOW (R-29) at the same try as the oracle: with an unattainable
+    tolerance every try is rejected until dt < 16 eps max(|t|, 1); u is left untouched."""
+    import paper_2309_05331_b200 as rk
+    if kind == "vector":
+        n = 64
+        u0 = rk_inputs.logistic_u0(n)
+        st = ctx.vector(n)
+        st.set_rhs_logistic()
+        p, t0, t1, dt0 = oracle.logistic_problem(n), -5.0, 5.0, 0.1
+    else:
+        dims = (16, 8, 6)
+        u0 = rk_inputs.gray_scott_ic(*dims, seed=2) + 0.01 * rk_inputs.random_state(2 * 16 * 8 * 6, 3).reshape(6, 2, 8, 16)
+        st = gs_state(ctx, dims, u0)
+        p, t0, t1, dt0 = oracle.gray_scott_problem(*dims), 0.0, 20.0, 1.0
+    st.set(u0)
+    st.set_option(rk.OPT_DEVICE_LOOP, device_loop)
+    st.reset_stats()
+    uo, ao, ro, rc = oracle.integrate_adaptive(p, oracle.DOPRI5, u0, t0, t1, dt0, 1e-300, 1e-300)
+    assert rc == oracle.ERR_DT_UNDERFLOW and ao == 0 and ro > 0
+    with pytest.raises(rk.RKError) as e:
+        st.integrate_adaptive("dopri5", t0, t1, dt0, 1e-300, 1e-300)
+    assert e.value.status == "RK_ERR_DT_UNDERFLOW"
+    s = st.stats()
+    assert (s["accepted"], s["rejected"]) == (ao, ro)
+    assert bitwise(st.get(), uo) and bitwise(uo, u0)
+    st.close()
+
+
+def test_torch_allocator_hook():
+    """rk_ctx_set_allocator: with allocator="torch" the state arrays come from
+    torch's caching allocator (torch.cuda.memory_allocated grows by them and shrinks back on
+    close) and results are unchanged."""
+    import torch
+
+    import paper_2309_05331_b200 as rk
+    dims = (40, 24, 10)
+    u0 = rk_inputs.gray_scott_ic(*dims, seed=11)
+    p = oracle.gray_scott_problem(*dims)
+    torch.cuda.synchronize()
+    m0 = torch.cuda.memory_allocated(0)
+    c = rk.Context(0, 1, 0, allocator="torch")
+    st = c.grid(*dims, 2)
+    st.set_rhs_gray_scott()
+    st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
+    st.set(u0)
+    st.do_step("rk4", 0.0, 1.0)
+    acc, E, dtn = st.try_step("dopri5", 1.0, 1.0, 1e-6, 1e-6)
+    u = oracle.step(p, oracle.RK4, 0.0, 1.0, u0)
+    un, err = oracle.step(p, oracle.DOPRI5, 1.0, 1.0, u, with_error=True)
+    assert bitwise(st.get(), un if acc else u)
+    arr = (dims[1] + 2) * (dims[0] + 2 + (dims[0] % 2)) * 2 * dims[2] * 8  # one padded array
+    assert torch.cuda.memory_allocated(0) - m0 >= 8 * arr  # u, u_new, k1..k6 at least
+    st.close()
+    c.close()
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated(0) == m0
