@@ -957,7 +957,8 @@ def main():
         extra["exp512"] = run_leg(exp512_leg)
     if "small" in legs:
         extra["small_configs"] = run_leg(small_configs_leg)
-    for sch in (("euler", "midpoint", "cash_karp54", "dopri5", "rkf78") + tuple(f"ab{k}" for k in range(1, 9))
+    for sch in (("euler", "midpoint", "modified_midpoint", "cash_karp54", "dopri5", "rkf78")
+                + tuple(f"ab{k}" for k in range(1, 9))
                 + tuple(f"abm{k}" for k in range(1, 9))):
         # scheme sweep (configs[4])
         if sch in legs:

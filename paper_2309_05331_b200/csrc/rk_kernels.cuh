@@ -150,7 +150,8 @@ struct GsStageArgs {
     int z_lo, z_hi;                  // output planes [z_lo, z_hi) (zmode 0)
     int zchunk;                      // output planes per CTA
     int zmode;                       // 0: contiguous chunks; 1: chunk 0 = plane 0, chunk 1 = nzl-1
-    int zpair;                       // zmode 0: chunks paired, lower one swept downwards (K3)
+    int zpair;                       // zmode 0: chunk group size G (> 1: G consecutive chunks of a
+                                     // tile launched together, alternating sweep directions; K3)
     int nyslots;                     // pack kernel: slots [0, nyslots) with g != 0 (Y terms)
     P2pSync sync;                    // boundary launch of the P2P halo path (else on = 0)
 };

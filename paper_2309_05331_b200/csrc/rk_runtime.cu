@@ -561,12 +561,16 @@ static int stage_class(const StagePlan& p) {
 // k-stages 4.83 -> 4.61 GB) but add reads to the short Y-direct chunks and slow the 48-plane
 // stages, so classes 1 and 2 only.  RKB_ZPAIR = class bitmask (developer knob).
 static int stage_zpair(const StagePlan& p) {
-    static int mask = -1;
-    if (mask < 0) {
-        const char* e = getenv("RKB_ZPAIR");
-        mask = e ? atoi(e) : 0x6;
+    static int g[5] = {0, 0, 0, 0, 0};
+    if (!g[0]) {  // developer knob RKB_ZPAIR="g0,g1,g2,g3,g4": chunk group size per stage class
+        const int def[5] = {1, 2, 2, 1, 1};
+        for (int c = 0; c < 5; ++c) g[c] = def[c];
+        if (const char* e = getenv("RKB_ZPAIR")) {
+            int v[5], n = sscanf(e, "%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4]);
+            for (int c = 0; c < n; ++c) g[c] = v[c] > 0 ? v[c] : 1;
+        }
     }
-    return (mask >> stage_class(p)) & 1;
+    return g[stage_class(p)];
 }
 
 static int pick_zchunk(rk_state st, const StagePlan& p, int range) {

@@ -250,19 +250,23 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     const double dsc = a.dtp ? *a.dtp : 1.0;
     const double dtv = a.dtp ? *a.dtp : a.dt;
     const int ntx = (G.nx + TX - 1) / TX;
-    // Paired chunks (a.zpair, zmode 0): CTAs 2t and 2t+1 of a grid row own the same xy tile t
-    // in chunks 2m and 2m+1 and are launched together; the lower one sweeps DOWN from the shared
-    // chunk boundary and the upper one UP from it, so the two planes around that boundary are
-    // read by both at the same moment (the second read hits L2) instead of a chunk-wave apart.
-    const int tile = a.zpair && a.zmode == 0 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    // Chunk groups (a.zpair = G > 1, zmode 0): CTAs G*t .. G*t+G-1 of a grid row own the same xy
+    // tile t in G consecutive z chunks and are launched together, sweeping in alternating
+    // directions (even members down, odd members up): two neighbouring chunks then either both
+    // START at their shared boundary or both END there, so the two planes around every boundary
+    // inside the group are read by both CTAs at the same moment (the second read hits L2)
+    // instead of a chunk-wave apart.
+    const int zg = a.zmode == 0 && a.zpair > 1 ? a.zpair : 1;
+    const int tile = (int)blockIdx.x / zg;
     const int x0 = (tile % ntx) * TX, y0 = (tile / ntx) * TH;
     const int w = min(TX, G.nx - x0), hg = min(TH, G.ny - y0);
 
     int zb, ze;
     bool desc = false;  // sweep z downwards (from ze-1 to zb)
     if (a.zmode == 0) {
-        const int chunk = a.zpair ? 2 * (int)blockIdx.y + (int)(blockIdx.x & 1) : (int)blockIdx.y;
-        desc = a.zpair && (blockIdx.x & 1) == 0;
+        const int member = (int)blockIdx.x % zg;
+        const int chunk = zg * (int)blockIdx.y + member;
+        desc = zg > 1 && (member & 1) == 0;
         zb = a.z_lo + chunk * a.zchunk;
         ze = min(zb + a.zchunk, a.z_hi);
     } else {
@@ -762,7 +766,7 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
         nchunks = (range + a.zchunk - 1) / a.zchunk;
     }
     dim3 grid((unsigned)tiles, (unsigned)nchunks);
-    if (a.zpair && a.zmode == 0) grid = dim3((unsigned)(2 * tiles), (unsigned)((nchunks + 1) / 2));
+    if (a.zpair > 1 && a.zmode == 0) grid = dim3((unsigned)(a.zpair * tiles), (unsigned)((nchunks + a.zpair - 1) / a.zpair));
     if (nlaunch) ++*nlaunch;
     if (adaptive == 2) {  // SPEC's error ratio (R-28)
         switch (scheme) {

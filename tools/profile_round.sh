@@ -4,11 +4,11 @@
 #   DOPRI5 try and one RK4 step, dram bytes of one step of every other scheme leg.
 #   Summaries are written on the box (tools/make_profiles.py) into gpurun_out/profiles_TAG/;
 #   the bulky .ncu-rep files are deleted there except the DOPRI5 one (gpurun returns <= 64 MiB).
-TAG=${1:-r1_v6}
+TAG=${1:-r2_v1}
 O=gpurun_out
-LEGS=adaptive,rk4,repeats,rk4_native,rk4_k6,midpoint_k6,exp512,small,e2e,cpu,euler,midpoint,cash_karp54,dopri5,rkf78,ab1,ab2,ab4,ab8,abm1,abm2,abm4,abm8
+LEGS=adaptive,rk4,repeats,try_loop,device_loop,halo,exposed,strong_emul,rk4_native,rk4_k6,midpoint_k6,exp512,small,e2e,cpu,cpu_full,euler,midpoint,modified_midpoint,cash_karp54,dopri5,rkf78,ab1,ab2,ab4,ab8,abm1,abm2,abm4,abm8
 timeout 1200 python bench.py --legs $LEGS > $O/${TAG}_bench.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv \
     --log-file $O/${TAG}_launches.csv python bench.py --legs adaptive --steps 2 --warmup 3 > $O/${TAG}_launches.log 2>&1
 bash tools/tune.sh "" ${TAG}
 full() {  # leg, kernel regex, skip, count
@@ -21,10 +21,11 @@ dram() {  # leg, kernel regex, skip, count: cold-L2 dram bytes per launch (csv)
       --clock-control none --kernel-name-base demangled -k "regex:$2" -s $3 -c $4 --csv \
       --log-file $O/${TAG}_dram_$1.csv python bench.py --legs $1 --steps 2 --warmup 3 > $O/${TAG}_dram_$1.log 2>&1
 }
-full adaptive "gs_stage_kernel" 30 6
+full adaptive "gs_stage_kernel" 31 6
 full rk4 "gs_stage_kernel" 12 4
 dram euler "gs_stage_kernel" 3 1
 dram midpoint "gs_stage_kernel" 6 2
+dram modified_midpoint "gs_stage_kernel" 9 3
 dram cash_karp54 "gs_stage_kernel" 18 6
 dram dopri5 "gs_stage_kernel" 18 6
 dram rkf78 "gs_stage_kernel" 39 13
