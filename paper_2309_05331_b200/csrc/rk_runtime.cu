@@ -2388,8 +2388,6 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
     case RK_OPT_HALO_P2P:
         if (value == 0 && st->ctx->world > 1 && !st->ctx->nccl)
             return fail(RK_ERR_ARG, "a context without NCCL has only the P2P transport");
-        if (st->p2p_ready && (value != 0) != st->p2p)
-            return fail(RK_ERR_STATE, "the P2P transport is already connected on this state");
         st->p2p = value != 0;
         break;
     default: return fail(RK_ERR_ARG, "unknown option %d", key);
