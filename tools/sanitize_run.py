@@ -1,6 +1,8 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
-every scheme on a ragged 40x12x10 grid (K5) and 40x21x13 (K3, K6), the loopback multi-GPU halo path, adaptive tries,
-Adams-Bashforth and the algebra ops.  Run:  compute-sanitizer --tool racecheck python tools/sanitize_run.py
+every scheme on a ragged 40x12x10 grid (K5) and 40x21x13 (K3, K6), the loopback multi-GPU halo path
+(NCCL and P2P, incl. the P2P allreduce), adaptive tries, the device-resident graph loop, the
+unfused dataflow, Adams-Bashforth and the algebra ops.
+Run:  compute-sanitizer --tool racecheck python tools/sanitize_run.py
 """
 import os
 import sys
@@ -19,7 +21,7 @@ for loop in (0, 1):
     st.set_rhs_gray_scott()
     st.set_option(rk.OPT_HALO_LOOPBACK, loop)
     st.set(u0)
-    for s in ("euler", "midpoint", "rk4", "cash_karp54", "dopri5", "rkf78", "ab3"):
+    for s in ("euler", "midpoint", "modified_midpoint", "rk4", "cash_karp54", "dopri5", "rkf78", "ab3"):
         st.do_step(s, 0.0, 1.0)
     for s in ("cash_karp54", "dopri5", "rkf78"):
         st.try_step(s, 0.0, 0.5, 1e-6, 1e-6)
@@ -33,8 +35,23 @@ for fused in (0, 1):
     st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
     st.set_option(rk.OPT_FUSED_STEP, fused)
     st.set(rk_inputs.gray_scott_ic(nx, ny + 9, nz + 3, seed=4))
-    for s in ("midpoint", "rk4", "dopri5"):
+    for s in ("midpoint", "modified_midpoint", "rk4", "dopri5"):
         st.do_step(s, 0.0, 1.0)
+    st.get()
+    st.close()
+# round 2 paths: P2P loopback under error control (device stage counter + P2P allreduce), the
+# device-resident graph loop (plain and over P2P), the unfused dataflow, chunk groups (z chunks)
+for p2p, dl, fk in ((1, 0, 1), (1, 1, 1), (0, 1, 1), (0, 0, 0)):
+    st = ctx.grid(nx, ny + 9, nz + 3, 2)
+    st.set_rhs_gray_scott()
+    st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, p2p)
+    st.set_option(rk.OPT_HALO_P2P, p2p)
+    st.set_option(rk.OPT_DEVICE_LOOP, dl)
+    st.set_option(rk.OPT_FUSED_KERNELS, fk)
+    st.set(rk_inputs.gray_scott_ic(nx, ny + 9, nz + 3, seed=5))
+    st.integrate_adaptive("dopri5", 0.0, 6.0, 2.0, 1e-6, 1e-6)
+    st.integrate_adaptive("cash_karp54", 6.0, 8.0, 1.0, 1e-6, 1e-6)
     st.get()
     st.close()
 v = ctx.vector(1001)
