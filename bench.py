@@ -363,7 +363,7 @@ def main():
         gbs = (s["halo_bytes"] / (s["halo_ms"] / 1e3) / 1e9) if s["halo_ms"] else None
         return {"exchanges": s["halo_exchanges"], "ms_per_exchange": s["halo_ms"] / s["halo_exchanges"],
                 "bytes_per_exchange": s["halo_bytes"] / s["halo_exchanges"],
-                "transport": "nccl over nvlink" if world > 1 else "loopback (device copy, one GPU)",
+                "transport": "nccl over nvlink" if world > 1 else "loopback (NCCL 1-rank self send/recv, one GPU)",
                 ("nvlink_gbs" if world > 1 else "gbs"): gbs}
 
     # ---- headline: DOPRI5 adaptive, one accepted step per "step" ---------------------
@@ -767,51 +767,64 @@ def main():
     def strong_emul_leg():
         # configs[3] on ONE GPU: the per-GPU share of a G-way strong-scaling run (512 x 512 x
         # 512/G slab of the 512^3 IC) through the multi-GPU stage path in loopback mode (pack,
-        # ghost planes, interior + overlapped boundary launches; the exchange is a device copy
-        # on the comm stream instead of NCCL over NVLink).  Compute-side efficiency only:
-        # T(512^3) / (G * T(slab)); NVLink time is not in it.
+        # ghost planes, interior + overlapped boundary launches; the exchange is NCCL's self
+        # send/recv -- or the P2P stores -- on one GPU instead of NVLink).  Compute-side efficiency
+        # only: T(512^3) / (G * T(slab)) per try; NVLink time is not in it.  DOPRI5 runs whole
+        # integrations over [0, 20] of the slab holding the middle of the IC cube, through three
+        # transports / drivers: NCCL + host try loop, P2P + host try loop, P2P + the
+        # device-resident graph loop (f3: no host round trip per try); RK4 as do_step.
         out = {}
+        variants = (("nccl_host", 0, 0), ("p2p_host", 1, 0), ("p2p_device", 1, 1))
         for G in (1, 2, 4, 8):
             nzl = n // G
             eg = ctx.grid(n, n, nzl, 2)
             eg.set_rhs_gray_scott(h=H)
             eg.set_option(rk.OPT_HALO_LOOPBACK, 1 if G > 1 else 0)
-            ue = torch.from_numpy(rk_inputs.gray_scott_ic(n, n, n, seed=42, z0=0, nzl=nzl, zblocks=1)).cuda(local)
+            ue = torch.from_numpy(rk_inputs.gray_scott_ic(n, n, n, seed=42, z0=(n - nzl) // 2, nzl=nzl,
+                                                          zblocks=1)).cuda(local)
             res = {}
-            for scheme in ("dopri5", "rk4"):
+            for name, p2p, dl in (variants if G > 1 else (("host", 0, 0), ("device", 0, 1))):
+                eg.set_option(rk.OPT_HALO_P2P, p2p)
+                eg.set_option(rk.OPT_DEVICE_LOOP, dl)
                 eg.set(ue)
-                t, dt = 0.0, 1.0
-
-                def one():
-                    nonlocal t, dt
-                    if scheme == "rk4":
-                        eg.do_step("rk4", t, 1.0)
-                        return 1
-                    k = 0
-                    while True:
-                        ok, _, dtn = eg.try_step("dopri5", t, dt, TOL, TOL)
-                        k += 1
-                        if ok:
-                            t, dt = t + dt, dtn
-                            return k
-                        dt = dtn
+                eg.integrate_adaptive("dopri5", 0.0, T1, 1.0, TOL, TOL)  # warm-up / graph build
+                ms, tries = [], 0
+                for _ in range(3):
+                    eg.set(ue)
+                    barrier()
+                    ev0.record(stream)
+                    a, r = eg.integrate_adaptive("dopri5", 0.0, T1, 1.0, TOL, TOL)
+                    ev1.record(stream)
+                    barrier()
+                    ms.append(ev0.elapsed_time(ev1))
+                    tries = a + r
+                m = statistics.median(ms)
+                res["dopri5_" + name] = {"ms_per_integration": m, "tries": tries, "ms_per_try": m / tries}
+            eg.set_option(rk.OPT_DEVICE_LOOP, 0)
+            for name, p2p in ((("nccl", 0), ("p2p", 1)) if G > 1 else (("plain", 0),)):
+                eg.set_option(rk.OPT_HALO_P2P, p2p)
+                eg.set(ue)
                 for _ in range(args.warmup):
-                    one()
+                    eg.do_step("rk4", 0.0, 1.0)
                 barrier()
                 ev0.record(stream)
-                tries = sum(one() for _ in range(args.steps))
+                for _ in range(args.steps):
+                    eg.do_step("rk4", 0.0, 1.0)
                 ev1.record(stream)
                 barrier()
-                ms = ev0.elapsed_time(ev1) / args.steps
-                res[scheme] = {"ms_per_step": ms, "tries": tries}
+                res["rk4_" + name] = {"ms_per_step": ev0.elapsed_time(ev1) / args.steps}
             eg.close()
             out[f"G{G}"] = {"nz_per_gpu": nzl, **res}
+        t1_dp = out["G1"]["dopri5_host"]["ms_per_try"]
+        t1_rk = out["G1"]["rk4_plain"]["ms_per_step"]
         for G in (2, 4, 8):
-            for scheme in ("dopri5", "rk4"):
-                b1 = out["G1"][scheme]["ms_per_step"] / out["G1"][scheme]["tries"]
-                bg = out[f"G{G}"][scheme]["ms_per_step"] / out[f"G{G}"][scheme]["tries"]
-                out[f"G{G}"][scheme]["compute_efficiency_per_try"] = b1 / (G * bg)
-        out["config"] = "per-GPU share of configs[3] (512^3 strong scaling) on one GPU, loopback halo path"
+            o = out[f"G{G}"]
+            for name, _, _ in variants:
+                o["dopri5_" + name]["compute_efficiency_per_try"] = t1_dp / (G * o["dopri5_" + name]["ms_per_try"])
+            for name in ("nccl", "p2p"):
+                o["rk4_" + name]["compute_efficiency"] = t1_rk / (G * o["rk4_" + name]["ms_per_step"])
+        out["config"] = ("per-GPU share of configs[3] (512^3 strong scaling) on one GPU, loopback halo path "
+                         "(NCCL self send/recv or P2P stores); DOPRI5 tol 1e-6 integrations over [0, 20]")
         return out
 
     def strong_leg():

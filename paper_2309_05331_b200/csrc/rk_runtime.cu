@@ -465,7 +465,7 @@ static rk_status ensure_self_comm(rk_ctx ctx) {
 }
 
 static rk_status ensure_halo(rk_state st) {
-    if (st->loopback) TRY(ensure_self_comm(st->ctx));
+    if (st->loopback && !st->p2p) TRY(ensure_self_comm(st->ctx));  // the P2P transport needs no NCCL
     if (!halo_path(st) || st->sendbuf) return RK_OK;
     TRY(dev_alloc(st->ctx, &st->sendbuf, 2 * plane_values(st)));
     TRY(dev_alloc(st->ctx, &st->ghostbuf, 2 * plane_values(st)));
