@@ -161,9 +161,15 @@ __device__ __forceinline__ unsigned long long p2p_wait(const P2pSync& s) {
     __syncthreads();
     return s_seq;
 }
+// The pack launch (role 0) stores into the neighbours' memory, so every CTA fences those
+// stores at system scope before it is counted.  The boundary launch (role 1) only READ ghost
+// planes (through TMA, completed before the CTA's epilogue): its acknowledgement orders no
+// remote writes, so a device-scope fence per CTA suffices and the last CTA alone issues the
+// system-scope fence and the release stores.
 __device__ __forceinline__ void p2p_notify(const P2pSync& s, unsigned long long seq) {
     if (!s.on) return;
-    __threadfence_system();
+    if (s.role == 0) __threadfence_system();
+    else __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned long long nb = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
@@ -812,7 +818,8 @@ cudaError_t launch_gs_pack(const GsStageArgs& a, double* dst0, double* dst1, con
                            cudaStream_t st) {
     const int64_t total = 2 * a.geo.ps;
     int64_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    // P2P: every CTA fences its remote stores at system scope, so fewer, longer CTAs (2 per SM)
+    if (blocks > (sync.on ? 148 * 2 : 148 * 8)) blocks = sync.on ? 148 * 2 : 148 * 8;
     switch (a.nyslots) {
     case 0: gs_pack_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;
     case 1: gs_pack_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(a, dst0, dst1, sync); break;

@@ -17,9 +17,17 @@ ctx = rk.Context(0, 1, 0)
 # SAN_NO_NCCL=1: skip the NCCL loopback sections (compute-sanitizer racecheck and NCCL's own
 # kernels / proxy thread do not mix; every other section runs)
 NO_NCCL = os.environ.get("SAN_NO_NCCL") == "1"
+# SAN_SECTIONS: comma list of sections to run (default all): base, k3k6, r2, vector
+SECTIONS = set(os.environ.get("SAN_SECTIONS", "base,k3k6,r2,vector").split(","))
+
+
+def mark(msg):
+    print("section", msg, flush=True)
+
 nx, ny, nz = 40, 12, 10
 u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=3) + 0.01 * rk_inputs.random_state(2 * nx * ny * nz, 1).reshape(nz, 2, ny, nx)
-for loop in ((0,) if NO_NCCL else (0, 1)):
+for loop in ((0,) if NO_NCCL else (0, 1)) if "base" in SECTIONS else ():
+    mark(f"base loopback={loop}")
     st = ctx.grid(nx, ny, nz, 2)
     st.set_rhs_gray_scott()
     st.set_option(rk.OPT_HALO_LOOPBACK, loop)
@@ -32,7 +40,8 @@ for loop in ((0,) if NO_NCCL else (0, 1)):
     st.close()
 # the stage-by-stage kernels on a small grid (K5 off) and K6 (whole-step fusion, several z chunks)
 os.environ["RKB_FZ"] = "3"
-for fused in (0, 1):
+for fused in (0, 1) if "k3k6" in SECTIONS else ():
+    mark(f"k3k6 fused={fused}")
     st = ctx.grid(nx, ny + 9, nz + 3, 2)
     st.set_rhs_gray_scott()
     st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
@@ -44,7 +53,13 @@ for fused in (0, 1):
     st.close()
 # round 2 paths: P2P loopback under error control (device stage counter + P2P allreduce), the
 # device-resident graph loop (plain and over P2P), the unfused dataflow, chunk groups (z chunks)
-for p2p, dl, fk in ((1, 0, 1), (1, 1, 1), (0, 1, 1), (0, 0, 0)):
+# SAN_NO_GRAPH=1 skips the device-resident graph loop (conditional graph nodes crash the
+# racecheck tool's host side; memcheck / synccheck / initcheck run them)
+R2 = ((1, 0, 1), (1, 1, 1), (0, 1, 1), (0, 0, 0))
+if os.environ.get("SAN_NO_GRAPH") == "1":
+    R2 = tuple(v for v in R2 if v[1] == 0)
+for p2p, dl, fk in R2 if "r2" in SECTIONS else ():
+    mark(f"r2 p2p={p2p} device_loop={dl} fused_kernels={fk}")
     st = ctx.grid(nx, ny + 9, nz + 3, 2)
     st.set_rhs_gray_scott()
     st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
@@ -57,6 +72,7 @@ for p2p, dl, fk in ((1, 0, 1), (1, 1, 1), (0, 1, 1), (0, 0, 0)):
     st.integrate_adaptive("cash_karp54", 6.0, 8.0, 1.0, 1e-6, 1e-6)
     st.get()
     st.close()
+mark("vector")
 v = ctx.vector(1001)
 v.set_rhs_logistic()
 v.set(rk_inputs.logistic_u0(1001))
