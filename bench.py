@@ -355,7 +355,7 @@ def main():
         eff = bytes_per_cell * cell_tries / (ms / 1e3) / 1e9
         return {"bytes_per_cell": bytes_per_cell, "effective_gbs": eff, "frac": eff / peak, "target_frac": 0.70}
 
-    def halo_of(s):
+    def halo_of(s, p2p=False):
         # halo time (comm-stream CUDA events around each exchange) and its GB/s, reported
         # separately; one GPU: the loopback self-exchange (a device copy)
         if not s["halo_exchanges"]:
@@ -363,7 +363,8 @@ def main():
         gbs = (s["halo_bytes"] / (s["halo_ms"] / 1e3) / 1e9) if s["halo_ms"] else None
         return {"exchanges": s["halo_exchanges"], "ms_per_exchange": s["halo_ms"] / s["halo_exchanges"],
                 "bytes_per_exchange": s["halo_bytes"] / s["halo_exchanges"],
-                "transport": "nccl over nvlink" if world > 1 else "loopback (NCCL 1-rank self send/recv, one GPU)",
+                "transport": ("p2p stores" if p2p else "nccl") + (" over nvlink" if world > 1 else
+                                                                  " (loopback on one GPU)"),
                 ("nvlink_gbs" if world > 1 else "gbs"): gbs}
 
     # ---- headline: DOPRI5 adaptive, one accepted step per "step" ---------------------
@@ -524,7 +525,7 @@ def main():
                "gpu_launches": s4["kernel_launches"]}
         if scheme in SURVEY_BYTES:  # SURVEY §8d's per-scheme B/cell (stage-by-stage schedule)
             out["roofline"]["survey_gate"] = survey_gate(SURVEY_BYTES[scheme], cells_local * args.steps, ms4)
-        h = halo_of(s4)
+        h = halo_of(s4, bool(p2p))
         if h:
             out["halo"] = h
         return out

@@ -359,3 +359,23 @@ def test_torch_allocator_hook():
     c.close()
     torch.cuda.synchronize()
     assert torch.cuda.memory_allocated(0) == m0
+
+
+def test_comm_deadline_counts_progress_not_backlog(ctx):
+    """RK_OPT_COMM_TIMEOUT_MS runs from the last collective PROGRESS.  A 128^3 RK4
+    integrate_const through the loopback halo path (NCCL 1-rank communicator) enqueues ~40 ms of
+    stages and exchanges without a host wait; a 2 ms deadline must not abort it (every exchange
+    completes within a stage), and the result stays bitwise."""
+    import paper_2309_05331_b200 as rk
+    dims = (128, 128, 128)
+    u0 = rk_inputs.gray_scott_ic(*dims, seed=42)
+    st = gs_state(ctx, dims, u0, loopback=1)
+    st.set_option(rk.OPT_COMM_TIMEOUT_MS, 2)
+    n = st.integrate_const("rk4", 0.0, 60.0, 1.0)
+    assert n == 60
+    ref = gs_state(ctx, dims, u0)
+    ref.integrate_const("rk4", 0.0, 60.0, 1.0)
+    assert bitwise(st.get(), ref.get())
+    st.set_option(rk.OPT_COMM_TIMEOUT_MS, 0)
+    st.close()
+    ref.close()
