@@ -158,9 +158,10 @@ typedef enum {
                                 host waits on a stream with NCCL work poll the stream and
                                 ncclCommGetAsyncError; an asynchronous NCCL error, or no
                                 collective completing for this many ms (> 0; the clock restarts
-                                whenever a collective issued by the ctx completes, so it must
-                                exceed the longest stretch of compute between two collectives,
-                                not the whole queued backlog), aborts the communicator and
+                                whenever a collective issued by the ctx completes, and it is
+                                off while no collective is outstanding, so it must exceed the
+                                longest stretch of compute between two collectives, not the
+                                whole queued backlog), aborts the communicator and
                                 returns RK_ERR_NCCL (context poisoned).  0 (default): no
                                 deadline (asynchronous errors are still detected).  >= 0.   */
     RK_OPT_ERROR_SPIKE = 13,  /* fault injection: n >= 1 -- the n-th error-controlled try

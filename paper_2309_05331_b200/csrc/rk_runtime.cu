@@ -132,7 +132,8 @@ static void mark_progress(rk_ctx ctx, cudaStream_t s) {
 // in a collective forever (SURVEY §5 failure detection).  The deadline runs from the last
 // PROGRESS: the start of the wait or the completion of the latest collective mark
 // (mark_progress), so queued compute behind many collectives does not count against it -- only
-// the longest stretch without a completed collective does.
+// the longest stretch without a completed collective does -- and it is off once every
+// collective issued so far has completed.
 static rk_status ctx_wait(rk_ctx ctx, cudaStream_t s) {
     if (!ctx->nccl) {
         CK_CTX(ctx, cudaStreamSynchronize(s));
@@ -150,7 +151,9 @@ static rk_status ctx_wait(rk_ctx ctx, cudaStream_t s) {
         if (q != cudaErrorNotReady) CK_CTX(ctx, q);
         ncclResult_t ar = ncclSuccess;
         NK_CTX(ctx, ncclCommGetAsyncError(ctx->nccl, &ar));
-        const bool late = ctx->comm_timeout_ms > 0 &&
+        // the deadline only applies while a collective is outstanding (a mark not yet reached):
+        // plain compute queued behind the last completed collective cannot hang on a peer
+        const bool late = ctx->comm_timeout_ms > 0 && !ctx->marks.empty() &&
                           std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(ctx->comm_timeout_ms);
         if ((ar != ncclSuccess && ar != ncclInProgress) || late) {
             ncclCommAbort(ctx->nccl);

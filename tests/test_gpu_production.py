@@ -365,7 +365,8 @@ def test_comm_deadline_counts_progress_not_backlog(ctx):
     """RK_OPT_COMM_TIMEOUT_MS runs from the last collective PROGRESS.  A 128^3 RK4
     integrate_const through the loopback halo path (NCCL 1-rank communicator) enqueues ~40 ms of
     stages and exchanges without a host wait; a 2 ms deadline must not abort it (every exchange
-    completes within a stage), and the result stays bitwise."""
+    completes within a stage), nor may it abort plain compute of another state on the same
+    context once no collective is outstanding; results stay bitwise."""
     import paper_2309_05331_b200 as rk
     dims = (128, 128, 128)
     u0 = rk_inputs.gray_scott_ic(*dims, seed=42)
