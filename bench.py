@@ -534,10 +534,10 @@ def main():
     # Bound by the FP64 pipe / latency, not HBM: roofline against the FP64 issue rate
     # (148 SMs x 64 non-FMA fp64 ops/clk x the sampled SM clock) with the algorithmic op count
     # per cell-step (RK4 168, midpoint 78; margin re-evaluations not counted).
-    K6_OPS = {"rk4": 168, "midpoint": 78}
+    K6_OPS = {"rk4": 168, "midpoint": 78, "modified_midpoint": 125}
 
-    def k6_leg(scheme):
-        st.set_option(rk.OPT_FUSED_STEP, 1)
+    def k6_leg(scheme, mode=1):
+        st.set_option(rk.OPT_FUSED_STEP, mode)
         with ClockSampler(local) as clk:
             out = rk4_leg(args.overlap, scheme)
         st.set_option(rk.OPT_FUSED_STEP, 0)
@@ -550,7 +550,8 @@ def main():
         out["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak_ops, "unit": "TFLOP/s (fp64, non-FMA)",
                            "frac": ach / peak_ops if ach else None, "ops_per_cell_step": K6_OPS[scheme],
                            "avg_launch_ms": k_ms}
-        out["kernel"] = "gs_fused_kernel (K6: whole step per launch, temporal blocking over the stages)"
+        out["kernel"] = ("gs_fused_kernel (K6: whole step per launch, temporal blocking over the stages)" if mode == 1 else
+                         "gs_ws_kernel (K7: whole step per launch, warp-specialised stage groups, mbarrier hand-off)")
         out["ms_per_step"] = ms
         return out
 
@@ -964,9 +965,11 @@ def main():
         extra["strong"] = run_leg(strong_leg)
     if "rk4_native" in legs:
         extra["rk4_native"] = run_leg(native_rk4_leg)
-    for sch in ("rk4", "midpoint"):  # opt-in: --legs rk4_k6,midpoint_k6 (K6)
-        if sch + "_k6" in legs and world == 1:
-            extra[sch + "_k6"] = run_leg(k6_leg, sch)
+    for sch in ("rk4", "midpoint", "modified_midpoint"):  # --legs rk4_k6,rk4_k7,...
+        for mode in (1, 2):
+            leg = f"{sch}_k{5 + mode}"
+            if leg in legs and world == 1:
+                extra[leg] = run_leg(k6_leg, sch, mode)
     if "exp512" in legs:
         extra["exp512"] = run_leg(exp512_leg)
     if "small" in legs:

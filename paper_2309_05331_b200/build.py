@@ -21,7 +21,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "rkb200")
 LIB = os.path.join(PKG, "librkb200.so")
-SOURCES = ["rk_runtime.cu", "rk_stencil.cu", "rk_pointwise.cu", "rk_algebra.cu", "rk_smallgrid.cu", "rk_fused.cu"]
+SOURCES = ["rk_runtime.cu", "rk_stencil.cu", "rk_pointwise.cu", "rk_algebra.cu", "rk_smallgrid.cu", "rk_fused.cu",
+           "rk_fused2.cu"]
 HEADERS = ["rk_kernels.cuh", "rk_device.cuh", "rk_tableau.h", "rk_stage_spec.h", "rk_ddmath.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -233,6 +233,9 @@ bool fused_scheme(int scheme);  // RK4 and explicit midpoint
 int fused_halo(int scheme);     // L = stages = margin cells
 cudaError_t encode_fused_map(CUtensorMap* map, const double* base, const GridGeom& g, int nplanes, int L);
 cudaError_t launch_gs_fused(int scheme, const GsFusedArgs& a, cudaStream_t st);
+// K7 (rk_fused2.cu): the same step with warp-specialised stage groups handing planes over
+// through mbarriers instead of CTA-wide barriers (RK_OPT_FUSED_STEP = 2)
+cudaError_t launch_gs_fused_ws(int scheme, const GsFusedArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------------------------------------------
 // K2 / K4: algebra.

@@ -264,7 +264,7 @@ struct rk_state_s {
     int64_t check_finite = 0;    // RK_OPT_CHECK_FINITE: check u every n steps (0: never)
     int64_t since_check = 0;     // steps since the last finiteness check
     int64_t coop_max_cells = 1 << 18;  // RK_OPT_COOP_MAX_CELLS: persistent-step path up to here
-    bool fused = false;          // RK_OPT_FUSED_STEP: K6 whole-step launches (RK4, midpoint)
+    int fused = 0;               // RK_OPT_FUSED_STEP: 1 K6, 2 K7 whole-step launches (chained tableaux)
     int64_t spike_at = 0, spike_seen = 0;  // RK_OPT_ERROR_SPIKE: inject at try number spike_at
     bool fused_kernels = true;   // RK_OPT_FUSED_KERNELS = 0: Odeint-like unfused stages (ablation)
     double* uf_y = nullptr;      // unfused: the stage value Y_i and the error estimate e
@@ -1152,7 +1152,7 @@ static rk_status fused_steps(rk_state st, int scheme, double dt, int64_t n) {
             e1 = pool_event(st);
             CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
         }
-        CK_CTX(ctx, launch_gs_fused(scheme, a, ctx->stream));
+        CK_CTX(ctx, st->fused == 2 ? launch_gs_fused_ws(scheme, a, ctx->stream) : launch_gs_fused(scheme, a, ctx->stream));
         if (st->timing) {
             CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
             st->pending.push_back({e0, e1, 0});
@@ -2373,7 +2373,10 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
         if (value < 0) return fail(RK_ERR_ARG, "cell limit must be >= 0");
         st->coop_max_cells = value;
         break;
-    case RK_OPT_FUSED_STEP: st->fused = value != 0; break;
+    case RK_OPT_FUSED_STEP:
+        if (value < 0 || value > 2) return fail(RK_ERR_ARG, "RK_OPT_FUSED_STEP: 0, 1 (K6) or 2 (K7)");
+        st->fused = (int)value;
+        break;
     case RK_OPT_COMM_TIMEOUT_MS:
         if (value < 0) return fail(RK_ERR_ARG, "RK_OPT_COMM_TIMEOUT_MS must be >= 0");
         st->ctx->comm_timeout_ms = value;

@@ -1,5 +1,6 @@
-"""GPU parity of K6 (rk_fused.cu): a whole fixed RK4 / explicit-midpoint step of Gray–Scott in
-one launch (temporal blocking across the stages, RK_OPT_FUSED_STEP).  Gate: bitwise equality
+"""GPU parity of K6 (rk_fused.cu) and K7 (rk_fused2.cu, warp-specialised): a whole fixed RK4 /
+explicit- / modified-midpoint step of Gray–Scott in one launch (temporal blocking across the
+stages, RK_OPT_FUSED_STEP = 1 / 2).  Gate: bitwise equality
 with the fp64 oracle (R-17/R-18) on seeded inputs, at sizes spanning several 32x16
 tiles and z chunks with ragged tails, degenerate grids (1..5 cells per axis, where the
 L-cell periodic margin wraps several times), every z-chunk length, and 512^3 sampled cells in
@@ -29,13 +30,18 @@ def bitwise(a, b):
     return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-def fused_state(ctx, nx, ny, nz, u0):
+@pytest.fixture(params=[1, 2], ids=["k6", "k7"])
+def mode(request):
+    return request.param
+
+
+def fused_state(ctx, nx, ny, nz, u0, mode=1):
     import paper_2309_05331_b200 as rk
     st = ctx.grid(nx, ny, nz, 2)
     st.set_rhs_gray_scott()
     st.set(u0)
     st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
-    st.set_option(rk.OPT_FUSED_STEP, 1)
+    st.set_option(rk.OPT_FUSED_STEP, mode)
     return st
 
 
@@ -50,10 +56,10 @@ GRIDS = [(4, 4, 4), (8, 8, 8), (16, 16, 16), (33, 17, 9), (64, 40, 12), (1, 1, 3
 
 @pytest.mark.parametrize("scheme", FUSED)
 @pytest.mark.parametrize("dims", GRIDS, ids=lambda d: "x".join(map(str, d)))
-def test_fused_steps_bitwise(ctx, scheme, dims):
+def test_fused_steps_bitwise(ctx, mode, scheme, dims):
     nx, ny, nz = dims
     u0 = perturbed_ic(nx, ny, nz)
-    st = fused_state(ctx, nx, ny, nz, u0)
+    st = fused_state(ctx, nx, ny, nz, u0, mode)
     p = oracle.gray_scott_problem(nx, ny, nz)
     u = u0
     before = st.stats()
@@ -67,12 +73,12 @@ def test_fused_steps_bitwise(ctx, scheme, dims):
 
 @pytest.mark.parametrize("fz", [1, 2, 3, 5, 8, 64])
 @pytest.mark.parametrize("scheme", FUSED)
-def test_fused_zchunks_bitwise(ctx, scheme, fz, monkeypatch):
+def test_fused_zchunks_bitwise(ctx, mode, scheme, fz, monkeypatch):
     """Every z-chunk length gives the same bits (the chunk's L-plane z margin is recomputed)."""
     monkeypatch.setenv("RKB_FZ", str(fz))
     nx, ny, nz = 40, 20, 23
     u0 = perturbed_ic(nx, ny, nz, seed=7)
-    st = fused_state(ctx, nx, ny, nz, u0)
+    st = fused_state(ctx, nx, ny, nz, u0, mode)
     st.do_step(scheme, 0.0, 0.5)
     st.do_step(scheme, 0.5, 0.5)
     p = oracle.gray_scott_problem(nx, ny, nz)
@@ -81,11 +87,11 @@ def test_fused_zchunks_bitwise(ctx, scheme, fz, monkeypatch):
     assert bitwise(st.get(), u), fz
 
 
-def test_fused_config3_integrate_const(ctx):
+def test_fused_config3_integrate_const(ctx, mode):
     """BASELINE configs[2] through K6: 64^3, RK4, dt = 1, t in [0, 20] (20 launches)."""
     n = 64
     u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
-    st = fused_state(ctx, n, n, n, u0)
+    st = fused_state(ctx, n, n, n, u0, mode)
     steps = st.integrate_const("rk4", 0.0, 20.0, 1.0)
     uo, so = oracle.integrate_const(oracle.gray_scott_problem(n, n, n), OS["rk4"], u0, 0.0, 20.0, 1.0)
     assert steps == so == 20
@@ -93,11 +99,11 @@ def test_fused_config3_integrate_const(ctx):
 
 
 @pytest.mark.parametrize("scheme", FUSED)
-def test_fused_graph_replay(ctx, scheme):
+def test_fused_graph_replay(ctx, mode, scheme):
     import paper_2309_05331_b200 as rk
     nx, ny, nz = 48, 33, 17
     u0 = perturbed_ic(nx, ny, nz, seed=3)
-    st = fused_state(ctx, nx, ny, nz, u0)
+    st = fused_state(ctx, nx, ny, nz, u0, mode)
     st.set_option(rk.OPT_USE_GRAPH, 1)
     steps = st.integrate_const(scheme, 0.0, 7.0, 1.0)
     uo, so = oracle.integrate_const(oracle.gray_scott_problem(nx, ny, nz), OS[scheme], u0, 0.0, 7.0, 1.0)
@@ -106,13 +112,13 @@ def test_fused_graph_replay(ctx, scheme):
 
 
 @pytest.mark.parametrize("scheme", FUSED)
-def test_fused_equals_stage_kernels(ctx, scheme):
+def test_fused_equals_stage_kernels(ctx, mode, scheme):
     """K6 and the stage-by-stage K3 path agree bit for bit on a multi-tile grid."""
     import paper_2309_05331_b200 as rk
     nx, ny, nz = 200, 130, 50
     u0 = perturbed_ic(nx, ny, nz, seed=11)
-    a = fused_state(ctx, nx, ny, nz, u0)
-    b = fused_state(ctx, nx, ny, nz, u0)
+    a = fused_state(ctx, nx, ny, nz, u0, mode)
+    b = fused_state(ctx, nx, ny, nz, u0, mode)
     b.set_option(rk.OPT_FUSED_STEP, 0)
     for k in range(2):
         a.do_step(scheme, float(k), 1.0)
@@ -129,13 +135,13 @@ def _sample_block(u, z, y, x, r):
 
 
 @pytest.mark.parametrize("scheme", FUSED)
-def test_fused_512_sampled_parity(ctx, scheme):
+def test_fused_512_sampled_parity(ctx, mode, scheme):
     """One K6 step at 512^3 exactly as bench.py runs it; sampled cells (tile corners, domain
     edges and corners, the IC cube's faces) recomputed by the oracle on their periodic
     neighbourhood."""
     n = 512
     u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
-    st = fused_state(ctx, n, n, n, u0)
+    st = fused_state(ctx, n, n, n, u0, mode)
     st.do_step(scheme, 0.0, 1.0)
     g = st.get()
     lo, hi = rk_inputs.cube_range(n)

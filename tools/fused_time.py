@@ -1,4 +1,4 @@
-"""Developer timing: K6 fused whole-step vs K3 stage-by-stage at 512^3 (RK4, midpoint)."""
+"""Developer timing: K6 / K7 fused whole-step vs K3 stage-by-stage at 512^3 (RK4, midpoints)."""
 import os
 import sys
 
@@ -36,6 +36,8 @@ if __name__ == "__main__":
     for scheme in sys.argv[1:] or ["rk4", "midpoint"]:
         k3 = run(scheme, 0)
         print(f"{scheme} K3 stage-by-stage: {k3:.3f} ms/step  {512**3 / k3 / 1e6:.3e} cell-updates/s", flush=True)
-        for fz in (32, 64, 128):
-            f = run(scheme, 1, fz=fz)
-            print(f"{scheme} K6 fused fz={fz}: {f:.3f} ms/step  {512**3 / f / 1e6:.3e} cell-updates/s  x{k3 / f:.2f}", flush=True)
+        for mode in (1, 2):
+            for fz in (32, 64, 128):
+                f = run(scheme, mode, fz=fz)
+                print(f"{scheme} K{5 + mode} fused fz={fz}: {f:.3f} ms/step  {512**3 / f / 1e6:.3e} cell-updates/s  "
+                      f"x{k3 / f:.2f}", flush=True)
