@@ -394,7 +394,6 @@ def main():
     def adaptive_leg():
         for _ in range(args.warmup):
             integrate_step(u0_dev)
-        st.set_option(rk.OPT_TIMING, 1)
         st.reset_stats()
         barrier()
         acc = rej = 0
@@ -407,8 +406,18 @@ def main():
             barrier()
         ms = max_over_ranks(ev0.elapsed_time(ev1))
         s = st.stats()
+        # Per-launch durations for the roofline come from a second, identical pass with a CUDA
+        # event pair around every stage launch (RK_OPT_TIMING): recording ~280 events per
+        # integration costs ~1.4 % of the step time, so the headline pass above runs without them.
+        st.reset_stats()
+        st.set_option(rk.OPT_TIMING, 1)
+        barrier()
+        for _ in range(args.steps):
+            integrate_step(u0_dev)
+        barrier()
+        s_t = st.stats()
         st.set_option(rk.OPT_TIMING, 0)
-        k_ms = s["stage_kernel_ms"]
+        k_ms = s_t["stage_kernel_ms"] * s["stage_launches"] / max(1, s_t["stage_launches"])
         achieved = s["stage_bytes"] / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
         step_bytes = s["stage_bytes"] / max(1, s["tries"])
         line = {
@@ -450,6 +459,9 @@ def main():
                          "algorithmic_bytes_per_cell_try": step_bytes / cells_local,
                          "avg_launch_ms": k_ms / max(1, s["stage_launches"]),
                          "launches": s["stage_launches"], "peak_source": peak_src,
+                         "timing": "achieved = algorithmic bytes / CUDA-event durations of the same stage "
+                                   "launches in a second pass of the K integrations (per-launch events "
+                                   "off in the headline pass)",
                          # SURVEY §8d gate: cells x tries x 528 B (its DOPRI5 adaptive schedule)
                          # over the whole timed region, against >= 0.70 of the measured peak
                          "survey_gate": survey_gate(528, cells_local * s["tries"], ms)},
