@@ -135,3 +135,21 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracle", "from oracle", "rk_oracle", "liboracle"):
                     assert bad not in txt, (f, bad)
+
+
+def test_context_argument_validation(rk):
+    """world > 1 needs either the NCCL unique id or a process group for the P2P handle
+    exchange; an id of the wrong size is refused -- all before any device call."""
+    with pytest.raises(ValueError):
+        rk.Context(0, 2, 0)
+    with pytest.raises(ValueError):
+        rk.Context(0, 2, 0, unique_id=b"short")
+
+
+def test_option_ids_match_header(rk):
+    """The binding's option constants equal the header's rk_option values."""
+    import re
+    hdr = open(os.path.join(ROOT, "include", "rk_b200.h")).read()
+    vals = {m.group(1): int(m.group(2)) for m in re.finditer(r"^\s*RK_OPT_(\w+)\s*=\s*(\d+)", hdr, re.M)}
+    for name, v in vals.items():
+        assert getattr(rk, "OPT_" + name) == v, name
