@@ -380,3 +380,46 @@ def test_comm_deadline_counts_progress_not_backlog(ctx):
     st.set_option(rk.OPT_COMM_TIMEOUT_MS, 0)
     st.close()
     ref.close()
+
+
+def test_512_full_array_parity(ctx):
+    """The headline configuration in full (configs[3], 512^3, bench.py's launch configuration):
+    DOPRI5 error-controlled tries as integrate_adaptive takes them from the IC (dt0 = 1 is
+    rejected; the controller's dt is accepted) -- E, the decision and the proposed dt equal,
+    u unchanged after the rejection and the accepted new state equal -- and one RK4 step, EVERY
+    element bitwise against the oracle's single-domain run (~70 s of oracle time, ~25 GB of
+    host memory)."""
+    import gc
+    n = 512
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    p = oracle.gray_scott_problem(n, n, n)
+    st = gs_state(ctx, (n, n, n), u0)
+    k1 = oracle.rhs(p, u0)
+    dt = 1.0
+    for _ in range(2):  # the bench's first try (rejected at dt0 = 1), then the controller's dt
+        acc, E, dtn = st.try_step("dopri5", 0.0, dt, 1e-6, 1e-6)
+        un, err = oracle.step(p, oracle.DOPRI5, 0.0, dt, u0, with_error=True)
+        Eo = oracle.error_ratio_max(err, u0, k1, dt, 1e-6, 1e-6)
+        del err
+        gc.collect()
+        assert E == Eo, (E, Eo)
+        acc_o, dt_o = oracle.controller(Eo, dt)
+        assert (acc, dtn) == (acc_o, dt_o)
+        got = st.get()
+        want = un if acc else u0
+        assert bitwise(got, want), first_mismatch(got, want)
+        del un, got, want
+        gc.collect()
+        if acc:
+            break
+        dt = dtn
+    assert acc  # the accepted try's full new state was compared
+    del k1
+    st.set(u0)
+    st.do_step("rk4", 0.0, 1.0)
+    got = st.get()
+    want = oracle.step(p, oracle.RK4, 0.0, 1.0, u0)
+    assert bitwise(got, want), first_mismatch(got, want)
+    st.close()
+    del got, want, u0
+    gc.collect()
