@@ -423,3 +423,4 @@ def test_512_full_array_parity(ctx):
     st.close()
     del got, want, u0
     gc.collect()
+
