@@ -103,6 +103,18 @@ cudaError_t launch_inject_max(unsigned long long* word, double v, cudaStream_t s
     return cudaGetLastError();
 }
 
+// One 8-byte result (the try's error-ratio max, a norm) stored by a kernel straight into
+// page-locked host memory (mapped under unified addressing), so the host's per-try read never
+// queues on a copy engine behind a large transfer another stream has in flight.
+__global__ void publish_word_kernel(const unsigned long long* src, unsigned long long* host_dst) {
+    *reinterpret_cast<volatile unsigned long long*>(host_dst) = *reinterpret_cast<const volatile unsigned long long*>(src);
+}
+
+cudaError_t launch_publish_word(const unsigned long long* src, unsigned long long* host_dst, cudaStream_t st) {
+    publish_word_kernel<<<1, 1, 0, st>>>(src, host_dst);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_norm_inf(const double* x, int64_t count, unsigned long long* out,
                             cudaStream_t st, int num_sms) {
     int64_t blocks = (count + 255) / 256;

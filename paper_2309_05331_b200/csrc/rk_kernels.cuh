@@ -256,5 +256,7 @@ cudaError_t launch_ratio_max(const double* e, const double* u, const double* w, 
                              int num_sms);
 // atomicMax(word, bits of v) (v >= 0): fault injection into an error-ratio max
 cudaError_t launch_inject_max(unsigned long long* word, double v, cudaStream_t st);
+// *host_dst = *src by a 1-thread kernel (host_dst: cudaMallocHost memory, read after a stream wait)
+cudaError_t launch_publish_word(const unsigned long long* src, unsigned long long* host_dst, cudaStream_t st);
 
 }  // namespace rkb

@@ -1015,7 +1015,8 @@ static rk_status global_norm_inf(rk_state st, double* out) {
     CK_CTX(ctx, launch_norm_inf(st->u, st->alloc, ctx->d_scratch, ctx->stream, ctx->num_sms));
     st->stats.kernel_launches += 1;
     TRY(allreduce_max_word(st, ctx->d_scratch));
-    CK_CTX(ctx, cudaMemcpyAsync(ctx->h_scratch, ctx->d_scratch, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK_CTX(ctx, launch_publish_word(ctx->d_scratch, ctx->h_scratch, ctx->stream));
+    st->stats.kernel_launches += 1;
     TRY(ctx_wait(ctx, ctx->stream));
     std::memcpy(out, ctx->h_scratch, 8);
     return RK_OK;
@@ -1454,8 +1455,8 @@ static rk_status one_try(rk_state st, int scheme, double t, double dt, double at
         st->stats.kernel_launches += 1;
     }
     TRY(allreduce_max_word(st, st->d_err));  // global max of E's bit pattern
-    CK_CTX(ctx, cudaMemcpyAsync(st->h_err, st->d_err, sizeof(unsigned long long),
-                                cudaMemcpyDeviceToHost, ctx->stream));
+    CK_CTX(ctx, launch_publish_word(st->d_err, st->h_err, ctx->stream));  // no copy engine
+    st->stats.kernel_launches += 1;
     TRY(ctx_wait(ctx, ctx->stream));
     double E;
     std::memcpy(&E, st->h_err, sizeof E);
