@@ -627,7 +627,7 @@ def main():
         for i in range(2):
             work(i, 1)
         accs[0] = accs[1] = 0
-        kper = max(2, ke)  # per pipeline: 2*ke steps in the timed region (fill / drain amortised)
+        kper = max(2, args.steps)  # per pipeline: 2*steps in the timed region (fill / drain amortised)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(side[0])
