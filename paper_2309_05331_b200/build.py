@@ -22,7 +22,7 @@ INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "rkb200")
 LIB = os.path.join(PKG, "librkb200.so")
 SOURCES = ["rk_runtime.cu", "rk_stencil.cu", "rk_pointwise.cu", "rk_algebra.cu", "rk_smallgrid.cu", "rk_fused.cu",
-           "rk_fused2.cu"]
+           "rk_fused2.cu", "rk_pair.cu"]
 HEADERS = ["rk_kernels.cuh", "rk_device.cuh", "rk_tableau.h", "rk_stage_spec.h", "rk_ddmath.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -233,6 +233,25 @@ bool fused_scheme(int scheme);  // RK4 and explicit midpoint
 int fused_halo(int scheme);     // L = stages = margin cells
 cudaError_t encode_fused_map(CUtensorMap* map, const double* base, const GridGeom& g, int nplanes, int L);
 cudaError_t launch_gs_fused(int scheme, const GsFusedArgs& a, cudaStream_t st);
+// K8 (rk_pair.cu): two chained stages per launch (stage-pair temporal blocking, one GPU):
+// k_A = F(src) on the tile + 1 ring; Y_B = u (+) gB k_A; k_B = F(Y_B); W = Wb (+) betaA k_A
+// (+) betaB k_B with Wb = W_in or u; out = W (and out_y = u (+) gN k_B when a pair follows).
+struct PairArgs {
+    CUtensorMap tm_src;    // Y_A as stored (u, or the written-ahead Y): 38 x 20 box (encode_pair_map)
+    CUtensorMap tm_u;      // u: K3's 34 x 18 tile + ring box (PAIR_LAST)
+    const double* src;     // raw pointer of the source (periodic cells beyond the padded ring)
+    const double* w_in;    // PAIR_LAST: the partial sum W of the first pair
+    double* out;           // W (PAIR_FIRST) or u_new (ring copies written)
+    double* out_y;         // PAIR_FIRST: the next pair's stage value (ring copies written)
+    GridGeom geo;          // nzl = nz: one GPU, z wraps by index
+    double gB, gN, betaA, betaB;
+    double d1, d2, F, FK, inv_h2;
+    int zchunk;
+};
+enum { PAIR_FIRST = 0, PAIR_LAST = 1, PAIR_ONLY = 2 };
+bool pair_shape_ok(const GridGeom& g);  // nx % 32 == 0, ny % 16 == 0
+cudaError_t encode_pair_map(CUtensorMap* map, const double* base, const GridGeom& g, int nplanes);
+cudaError_t launch_gs_pair(int kind, const PairArgs& a, cudaStream_t st);
 // K7 (rk_fused2.cu): the same step with warp-specialised stage groups handing planes over
 // through mbarriers instead of CTA-wide barriers (RK_OPT_FUSED_STEP = 2)
 cudaError_t launch_gs_fused_ws(int scheme, const GsFusedArgs& a, cudaStream_t st);

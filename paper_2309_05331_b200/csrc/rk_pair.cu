@@ -1,0 +1,420 @@
+// rk_pair.cu — K8: two consecutive Runge–Kutta stages of Gray–Scott per launch (stage-pair
+// temporal blocking, "fused" variants).
+//
+// For tableaux whose stage values chain through one slope (Y_s = u (+) g_s k_{s-1}: classic RK4
+// P:L59, the explicit midpoint rule P:L58), a pair of stages (A, B = A+1) is one launch:
+//   k_A = F(Y_A)                  Y_A read as stored (u, or the Y written ahead by the previous
+//                                 pair), evaluated on the tile grown by one cell (the ring k_B's
+//                                 stencil needs) and never stored
+//   Y_B = u (+) g_B k_A           formed where k_A was computed
+//   k_B = F(Y_B)                  on the tile
+//   epilogue at the own cells:    W = Wb (+) beta_A k_A (+) beta_B k_B   (Wb = u, or the partial
+//                                 sum W of the previous pair; this is u_new after the last pair)
+//                                 and, when another pair follows, its stage value written ahead:
+//                                 Y_next = u (+) g_next k_B  (with the periodic ring copies)
+// RK4 is two launches -- (u -> Y_3, W) and (Y_3, u, W -> u_new), 48 + 64 = 112 B/cell/step
+// instead of 208 stage by stage -- and the explicit midpoint rule one launch (u -> u_new, 32 B
+// instead of 80), for 1.19x the stencil work of stage A (32x16 tile: 96 ring cells on 512).
+//
+// Kernel organisation (sm_100a, K3's recipe): a CTA of 256 threads owns a 32x16 xy tile (each
+// thread two ADJACENT rows of one column, so one y neighbour of each own cell is the other own
+// cell, in registers) and sweeps a chunk of z planes.  One elected thread streams, per plane, one
+// 4D TMA box per input into an R-deep mbarrier ring: Y_A's source with a 2-cell margin (38x20
+// box from the 16-byte aligned column x0-2; CTAs on the domain edge patch the periodic cells
+// beyond the padded layout's 1-cell ring in place) and u with a 1-cell margin when it is not
+// Y_A's source; W (own cells only) comes by plain loads one plane ahead.  Iteration t (stage A at plane t, stage B at plane t-1) has ONE
+// __syncthreads: [patch plane t+1]; barrier; k_A at plane t (own cells: xy neighbours from the
+// ring, z column in registers; ring cells: all from the ring) -> Y_B(t) into a 2-slot buffer
+// (own cells also in registers); k_B at plane t-1 (xy from the Y_B buffer, z from registers) ->
+// epilogue.  A thread's stage A and stage B chains are independent: 4-5 chains in flight.
+// Arithmetic is K3's expression for expression (R-17): difference-form Laplacian
+// (x, then y, then z; lower neighbour first), the same reaction trees, stage values and partial
+// sums left to right, no FMA -- bitwise equal to the oracle and to the stage-by-stage kernels for
+// any tile / chunk decomposition.  One GPU (z wraps by index), nx % 32 == 0, ny % 16 == 0 (else
+// the library runs the stage-by-stage kernels).
+#include <cudaTypedefs.h>
+
+#include "rk_device.cuh"
+#include "rk_kernels.cuh"
+
+namespace rkb {
+
+namespace {
+
+#define PINLINE __attribute__((always_inline))
+
+constexpr int PX = 32;    // tile width (one warp per row pair)
+constexpr int PTH = 16;   // tile height: 8 warps x 2 adjacent rows
+constexpr int PNT = 256;  // threads
+constexpr int BW = PX + 6;   // source box: cells x0-3 .. x0+34 (padded column x0-2: 16-byte start)
+constexpr int BH = PTH + 4;  // rows y0-2 .. y0+17
+constexpr int BOX = BW * BH;
+constexpr int HSLOT = (2 * BOX * 8 + 127) / 128 * 128;  // 12160 B
+constexpr int UW = PX + 2, UH = PTH + 2, UBOX = UW * UH;  // u box: tile + 1 ring (K3's 34x18 box)
+constexpr int USLOT = (2 * UBOX * 8 + 127) / 128 * 128;   // 9856 B
+constexpr int YBW = UW, YBH = UH, YBOX = UBOX;            // Y_B buffer: tile + 1 ring
+constexpr int YBSLOT = USLOT;
+constexpr int NRING = 2 * PX + 2 * PTH;                   // tile+1 ring without its corners: 96
+constexpr int NPATCH = 36 * BH;                           // source positions used (box cols 1..36)
+constexpr int SMEM_BUDGET = 113 * 1024;                   // 2 CTAs per SM
+
+// U1: u comes in its own 1-ring box (Y_A's source is a written-ahead Y).  The ring holds the
+// planes t-1, t, t+1 stage A reads and at least one plane in flight.
+template <bool U1>
+struct PLayout {
+    static constexpr int stage = HSLOT + (U1 ? USLOT : 0);
+    static constexpr int fixed = 2 * YBSLOT;
+    static constexpr int Rb = (SMEM_BUDGET - fixed - 64) / stage;
+    static constexpr int R = Rb > 5 ? 5 : Rb;
+    static_assert(R >= 4, "ring too shallow");
+    static constexpr int off_u = HSLOT;
+    static constexpr int yb = R * stage;           // Y_B buffer (2 slots)
+    static constexpr int bar = yb + 2 * YBSLOT;    // R mbarriers
+    static constexpr int smem = bar + R * 8;
+};
+
+__device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ int pmod(int a, int n) {
+    const int m = a % n;
+    return m < 0 ? m + n : m;
+}
+
+// reaction and scaling of one cell (K3's trees) from the Laplacian sums s[c]
+__device__ __forceinline__ void react(const double (&s)[2], const double (&ctr)[2], const PairArgs& a, double (&f)[2]) {
+    const double L0 = mul(s[0], a.inv_h2), L1 = mul(s[1], a.inv_h2);
+    const double C0 = ctr[0], C1 = ctr[1];
+    const double rc = mul(mul(C0, C1), C1);
+    f[0] = sub(add(sub(mul(a.d1, L0), rc), a.F), mul(a.F, C0));
+    f[1] = sub(add(mul(a.d2, L1), rc), mul(a.FK, C1));
+}
+
+// k = F(Y) at the thread's two own cells (rows r0 = 2w, r1 = 2w+1 of one column): v0 -> cell r0's
+// component 0 in a box of pitch `pitch` and component stride `cs`; c0 / c1 their values, zm / zp
+// their z neighbours.  Cell r0's upper y neighbour is c1 and cell r1's lower one is c0.
+__device__ __forceinline__ void rhs_two(const double* v0, int cs, int pitch, const double (&c0)[2],
+                                        const double (&c1)[2], const double (&zm0)[2], const double (&zp0)[2],
+                                        const double (&zm1)[2], const double (&zp1)[2], const PairArgs& a,
+                                        double (&f0)[2], double (&f1)[2]) {
+    double s0[2], s1[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const double* w = v0 + c * cs;
+        const double a0 = c0[c], a1 = c1[c];
+        double s = add(sub(w[-1], a0), sub(w[1], a0));
+        s = add(s, add(sub(w[-pitch], a0), sub(a1, a0)));
+        s0[c] = add(s, add(sub(zm0[c], a0), sub(zp0[c], a0)));
+        const double* w1 = w + pitch;
+        double t = add(sub(w1[-1], a1), sub(w1[1], a1));
+        t = add(t, add(sub(a0, a1), sub(w1[pitch], a1)));
+        s1[c] = add(t, add(sub(zm1[c], a1), sub(zp1[c], a1)));
+    }
+    react(s0, c0, a, f0);
+    react(s1, c1, a, f1);
+}
+
+// k = F(Y) at one cell with every value from boxes (ring cells)
+__device__ __forceinline__ void rhs_box(const double* v, const double* vm, const double* vp, int cs, int pitch,
+                                        const PairArgs& a, double (&f)[2]) {
+    double s[2], ctr[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const double* w = v + c * cs;
+        const double cc = w[0];
+        ctr[c] = cc;
+        double q = add(sub(w[-1], cc), sub(w[1], cc));
+        q = add(q, add(sub(w[-pitch], cc), sub(w[pitch], cc)));
+        s[c] = add(q, add(sub(vm[c * cs], cc), sub(vp[c * cs], cc)));
+    }
+    react(s, ctr, a, f);
+}
+
+__device__ __forceinline__ void store_ring(double* p, const GridGeom& G, bool ex0, bool ex1, bool ey0, bool ey1,
+                                           double v) {
+    p[0] = v;
+    if (ex0) p[G.nx] = v;
+    if (ex1) p[-G.nx] = v;
+    if (ey0) p[(int64_t)G.ny * G.P] = v;
+    if (ey1) p[-(int64_t)G.ny * G.P] = v;
+}
+
+template <bool U1, bool WIN, bool BA, bool YOUT>
+__global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__ PairArgs a) {
+    using LY = PLayout<U1>;
+    constexpr int R = LY::R;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LY::bar);
+    const GridGeom& G = a.geo;
+    const int tid = threadIdx.x;
+    const int ntx = G.nx / PX;
+    const int tile = (int)blockIdx.x;
+    const int x0 = (tile % ntx) * PX, y0 = (tile / ntx) * PTH;
+    const int zb = (int)blockIdx.y * a.zchunk;
+    const int ze = min(zb + a.zchunk, G.nzl);
+    if (zb >= ze) return;
+    const int nout = ze - zb;
+    const int nr = nout + 4;  // raw planes zb-2 .. ze+1; index i <-> plane zb-2+i
+    auto plane = [&](int i) PINLINE -> int { return pmod(zb - 2 + i, G.nzl); };
+    const bool edge = x0 == 0 || x0 + PX == G.nx || y0 == 0 || y0 + PTH == G.ny;  // CTA-uniform
+
+    // own cells: column lx, rows r0 = 2w, r1 = 2w+1
+    const int lx = tid % PX, w = tid / PX;
+    const int pb = (2 * w + 2) * BW + (lx + 3);   // row r0 in the source box
+    const int pu = (2 * w + 1) * UW + (lx + 1);   // row r0 in the u box / Y_B buffer
+    const int64_t coff = (int64_t)(y0 + 2 * w + 1) * G.P + (x0 + lx + 1);  // row r0, padded
+    const bool ex0 = x0 + lx == 0, ex1 = x0 + lx == G.nx - 1;
+    const bool ey0 = y0 + 2 * w == 0, ey1 = y0 + 2 * w + 1 == G.ny - 1;
+    const bool ering = ex0 || ex1 || ey0 || ey1;
+    // ring cell of the tile grown by one (no corners): top row, bottom row, left col, right col
+    const bool hr = tid < NRING;
+    int rb = 0, ru = 0;
+    if (hr) {
+        int rx, ry;
+        if (tid < PX) { rx = tid; ry = -1; }
+        else if (tid < 2 * PX) { rx = tid - PX; ry = PTH; }
+        else if (tid < 2 * PX + PTH) { rx = -1; ry = tid - 2 * PX; }
+        else { rx = PX; ry = tid - 2 * PX - PTH; }
+        rb = (ry + 2) * BW + (rx + 3);
+        ru = (ry + 1) * UW + (rx + 1);
+    }
+
+    auto raw = [&](int i) PINLINE -> unsigned char* { return smem + (size_t)(i % R) * LY::stage; };
+    auto ybs = [&](int i) PINLINE -> double* { return reinterpret_cast<double*>(smem + LY::yb + (size_t)(i & 1) * YBSLOT); };
+    auto tma = [&](void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1, int q) PINLINE {
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(s32(dst)),
+            "l"(reinterpret_cast<uint64_t>(m)), "r"(s32(b)), "r"(c0), "r"(c1), "r"(0), "r"(q)
+            : "memory");
+    };
+    auto issue = [&](int i) PINLINE {  // thread 0
+        uint64_t* b = &bar[i % R];
+        const int q = plane(i);
+        const bool mid = i >= 1 && i < nr - 1;  // u feeds Y_B at stage-A planes zb-1 .. ze
+        const uint32_t bytes = 2 * BOX * 8 + ((U1 && mid) ? 2 * UBOX * 8 : 0);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
+        unsigned char* st = raw(i);
+        tma(st, &a.tm_src, b, x0 - 2, y0 - 1, q);
+        if constexpr (U1)
+            if (mid) tma(st + LY::off_u, &a.tm_u, b, x0, y0, q);
+    };
+    auto wait = [&](int i) PINLINE {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WAITP_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WAITP_%=;\n}" ::"r"(s32(&bar[i % R])),
+            "r"((uint32_t)((i / R) & 1))
+            : "memory");
+    };
+    // edge CTAs: the source box cells the padded layout does not hold (the 2nd margin cell,
+    // the ring corners) are overwritten with their periodic images from global memory
+    auto patch = [&](int i) PINLINE {
+        double* y = reinterpret_cast<double*>(raw(i));
+        const int64_t qo = (int64_t)plane(i) * G.ps;
+        for (int q = tid; q < NPATCH; q += PNT) {
+            const int col = 1 + q % 36, row = q / 36;
+            const int x = x0 - 3 + col, yy = y0 - 2 + row;
+            const bool held = (x >= 0 && x < G.nx && yy >= -1 && yy <= G.ny) || (yy >= 0 && yy < G.ny && x >= -1 && x <= G.nx);
+            if (held) continue;
+            const int64_t src = qo + (int64_t)(pmod(yy, G.ny) + 1) * G.P + (pmod(x, G.nx) + 1);
+            y[row * BW + col] = a.src[src];
+            y[BOX + row * BW + col] = a.src[src + G.cs];
+        }
+    };
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < R; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(&bar[s])), "r"(1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int i = 0; i < (nr < R ? nr : R); ++i) issue(i);
+
+    // own-cell registers ([r] = row r0 / r1): Y_A at planes t-1, t, t+1; Y_B at t-2, t-1, t;
+    // k_A at t-1 (for the epilogue) and t; u at t-1 and t (U1); Wb at t-1 and t (WIN)
+    double yam[2][2], yac[2][2], yap[2][2];
+    double ybm[2][2] = {}, ybc[2][2] = {}, ybp[2][2] = {};
+    double kap[2][2] = {}, kac[2][2];
+    double uc[2][2] = {}, up[2][2] = {};  // U1: u at t (for Y_B) and t-1 (for the epilogue)
+    double wbn[2][2] = {}, wbp[2][2] = {};  // WIN: W at t (loaded one iteration ahead) and t-1
+    auto own_src = [&](int i, double (&v)[2][2]) PINLINE {
+        const double* s = reinterpret_cast<const double*>(raw(i));
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            v[r][0] = s[pb + r * BW];
+            v[r][1] = s[BOX + pb + r * BW];
+        }
+    };
+    wait(0);
+    if (edge) patch(0);
+    wait(1);
+    if (edge) patch(1);
+    __syncthreads();  // patched cells visible
+    own_src(0, yac);
+    own_src(1, yap);
+
+    // iteration it: stage A at plane t = zb-1+it (raw index it+1), stage B at t-1
+    for (int it = 0; it < nout + 2; ++it) {
+        const int ic = it + 1;
+        wait(it + 2);
+        if (edge) patch(it + 2);
+        __syncthreads();  // plane t+1 (patched) visible; Y_B(t-1) stored; raw plane t-2 free
+        if (tid == 0 && it - 1 >= 0 && it - 1 + R < nr) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the patches
+            issue(it - 1 + R);
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                yam[r][c] = yac[r][c];
+                yac[r][c] = yap[r][c];
+            }
+        own_src(it + 2, yap);
+        if constexpr (WIN) {  // W of plane t (used by stage B in the next iteration): plain loads
+            if (it >= 1 && it <= nout) {
+                const double* W = a.w_in + (int64_t)(zb + it - 1) * G.ps + coff;
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    wbn[r][0] = W[(int64_t)r * G.P];
+                    wbn[r][1] = W[G.cs + (int64_t)r * G.P];
+                }
+            }
+        }
+        const unsigned char* st = raw(ic);
+        const double* ya = reinterpret_cast<const double*>(st);
+        const bool ring_plane = it >= 1 && it <= nout;  // Y_B(t) is read by stage B's xy stencil
+        // ---- stage A at plane t ----
+        rhs_two(ya + pb, BOX, BW, yac[0], yac[1], yam[0], yap[0], yam[1], yap[1], a, kac[0], kac[1]);
+        if constexpr (U1) {
+            const double* U = reinterpret_cast<const double*>(st + LY::off_u);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                up[r][0] = uc[r][0]; up[r][1] = uc[r][1];
+                uc[r][0] = U[pu + r * UW];
+                uc[r][1] = U[UBOX + pu + r * UW];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                ybm[r][c] = ybc[r][c];
+                ybc[r][c] = ybp[r][c];
+                ybp[r][c] = add(U1 ? uc[r][c] : yac[r][c], mul(a.gB, kac[r][c]));
+            }
+        if (ring_plane) {
+            double* yb = ybs(ic);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                yb[pu + r * UW] = ybp[r][0];
+                yb[YBOX + pu + r * UW] = ybp[r][1];
+            }
+            if (hr) {
+                const double* ym = reinterpret_cast<const double*>(raw(ic - 1));
+                const double* yp = reinterpret_cast<const double*>(raw(ic + 1));
+                double kr[2];
+                rhs_box(ya + rb, ym + rb, yp + rb, BOX, BW, a, kr);
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const double ur = U1 ? reinterpret_cast<const double*>(st + LY::off_u)[c * UBOX + ru] : ya[c * BOX + rb];
+                    yb[c * YBOX + ru] = add(ur, mul(a.gB, kr[c]));
+                }
+            }
+        }
+        // ---- stage B at plane t-1 (output planes zb .. ze-1) ----
+        if (it >= 2) {
+            const double* yb = ybs(ic - 1);
+            double kb[2][2];
+            rhs_two(yb + pu, YBOX, YBW, ybc[0], ybc[1], ybm[0], ybp[0], ybm[1], ybp[1], a, kb[0], kb[1]);
+            const int64_t qo = (int64_t)(zb + it - 2) * G.ps;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const bool rx0 = ex0, rx1 = ex1, ry0 = r == 0 && ey0, ry1 = r == 1 && ey1;
+                const int64_t ro = qo + coff + (int64_t)r * G.P;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    // Wb: W of the previous pair, else u (= Y_A for a pair fed by u)
+                    double wv = WIN ? wbp[r][c] : (U1 ? up[r][c] : yam[r][c]);
+                    if constexpr (BA) wv = add(wv, mul(a.betaA, kap[r][c]));
+                    wv = add(wv, mul(a.betaB, kb[r][c]));
+                    double* p = a.out + ro + c * G.cs;
+                    if constexpr (YOUT) {
+                        p[0] = wv;  // W: read at own cells only, no ring copies
+                        const double yn = add(U1 ? up[r][c] : yam[r][c], mul(a.gN, kb[r][c]));
+                        double* py = a.out_y + ro + c * G.cs;
+                        if (ering) store_ring(py, G, rx0, rx1, ry0, ry1, yn);
+                        else py[0] = yn;
+                    } else {
+                        if (ering) store_ring(p, G, rx0, rx1, ry0, ry1, wv);
+                        else p[0] = wv;
+                    }
+                }
+            }
+        }
+        // epilogue inputs of plane t for the next iteration
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) kap[r][c] = kac[r][c];
+        if constexpr (WIN) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) wbp[r][c] = wbn[r][c];
+        }
+    }
+}
+
+template <bool U1, bool WIN, bool BA, bool YOUT>
+cudaError_t launch_pair_t(const PairArgs& a, cudaStream_t st) {
+    using LY = PLayout<U1>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gs_pair_kernel<U1, WIN, BA, YOUT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, LY::smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    const int tiles = (a.geo.nx / PX) * (a.geo.ny / PTH);
+    const int nch = (a.geo.nzl + a.zchunk - 1) / a.zchunk;
+    gs_pair_kernel<U1, WIN, BA, YOUT><<<dim3((unsigned)tiles, (unsigned)nch), PNT, LY::smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool pair_shape_ok(const GridGeom& g) { return g.nx % PX == 0 && g.ny % PTH == 0 && g.nx >= PX && g.ny >= PTH; }
+
+cudaError_t encode_pair_map(CUtensorMap* map, const double* base, const GridGeom& g, int nplanes) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[4] = {(cuuint64_t)g.P, (cuuint64_t)(g.ny + 2), 2, (cuuint64_t)nplanes};
+    const cuuint64_t strides[3] = {(cuuint64_t)g.P * 8, (cuuint64_t)g.cs * 8, (cuuint64_t)g.ps * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)BW, (cuuint32_t)BH, 2, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gs_pair(int kind, const PairArgs& a, cudaStream_t st) {
+    if (a.zchunk <= 0 || !pair_shape_ok(a.geo)) return cudaErrorInvalidValue;
+    switch (kind) {
+    case PAIR_FIRST: return launch_pair_t<false, false, true, true>(a, st);  // RK4 1-2: u -> Y3, W
+    case PAIR_LAST: return launch_pair_t<true, true, true, false>(a, st);    // RK4 3-4: Y3, u, W -> u_new
+    case PAIR_ONLY: return launch_pair_t<false, false, false, false>(a, st); // midpoint: u -> u_new
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace rkb

@@ -1112,7 +1112,7 @@ static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
 // K6 (rk_fused.cu): a whole fixed step of RK4 / explicit midpoint in one launch, temporal
 // blocking across the stages (one GPU, no halo path)
 static bool fused_path(rk_state st, int scheme) {
-    return st->fused && st->grid && st->ncomp == 2 && st->rhs == RHS_GRAY_SCOTT && st->ctx->world == 1 &&
+    return (st->fused == 1 || st->fused == 2) && st->grid && st->ncomp == 2 && st->rhs == RHS_GRAY_SCOTT && st->ctx->world == 1 &&
            !st->loopback && !st->p2p && fused_scheme(scheme);
 }
 
@@ -1126,6 +1126,89 @@ static int pick_fused_zchunk(rk_state st) {
     const int64_t tiles = ((st->nx + 31) / 32) * ((st->ny + 15) / 16);
     while (zc > 2 && tiles * ((nz + zc - 1) / zc) < 2 * st->ctx->num_sms) zc /= 2;
     return std::max(1, std::min(zc, nz));
+}
+
+// K8 (rk_pair.cu): RK4 as two stage-pair launches (u -> k2, W; u, k2, W -> u_new), the
+// explicit midpoint rule as one (u -> u_new); RK_OPT_FUSED_STEP = 3
+static bool pair_path(rk_state st, int scheme) {
+    return st->fused == 3 && st->grid && st->ncomp == 2 && st->rhs == RHS_GRAY_SCOTT && st->ctx->world == 1 &&
+           !st->loopback && !st->p2p && (scheme == RK_RK4 || scheme == RK_EXPLICIT_MIDPOINT) &&
+           pair_shape_ok(st->geo);
+}
+
+static int pick_pair_zchunk(rk_state st) {
+    int zc = 32;
+    if (const char* e = getenv("RKB_PZ")) {  // developer tuning knob
+        const int v = atoi(e);
+        if (v > 0) zc = v;
+    }
+    const int64_t tiles = (int64_t)(st->nx / 32) * (st->ny / 16);
+    while (zc > 2 && tiles * ((st->local + zc - 1) / zc) < 2 * st->ctx->num_sms) zc /= 2;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(zc, st->local));
+}
+
+static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
+    NvtxRange nv("rk pair steps (K8)");
+    rk_ctx ctx = st->ctx;
+    const Coeffs C = coeffs_of(scheme);
+    const bool rk4 = scheme == RK_RK4;
+    if (rk4) TRY(ensure_k(st, 2));  // k[0] <- Y3, k[1] <- W
+    PairArgs a{};
+    a.geo = st->geo;
+    a.d1 = st->d1;
+    a.d2 = st->d2;
+    a.F = st->F;
+    a.FK = st->F + st->K;
+    a.inv_h2 = 1.0 / (st->h * st->h);
+    a.zchunk = pick_pair_zchunk(st);
+    const int64_t cells = st->local * st->nx * st->ny;
+    for (int64_t i = 0; i < n; ++i) {
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (st->timing) {
+            e0 = pool_event(st);
+            e1 = pool_event(st);
+            CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+        }
+        CK_CTX(ctx, encode_pair_map(&a.tm_src, st->u, st->geo, (int)st->local));
+        a.src = st->u;
+        a.gB = dt * C.a[1][0];
+        a.betaA = dt * C.b[0];
+        a.betaB = dt * C.b[1];
+        if (rk4) {  // (u -> Y3 = u + g3 k2, W) then (Y3, u, W -> u_new)
+            a.gN = dt * C.a[2][1];
+            a.out = st->k[1];
+            a.out_y = st->k[0];
+            CK_CTX(ctx, launch_gs_pair(PAIR_FIRST, a, ctx->stream));
+            CK_CTX(ctx, encode_pair_map(&a.tm_src, st->k[0], st->geo, (int)st->local));
+            a.tm_u = st->tm_u.m[2];
+            a.src = st->k[0];
+            a.w_in = st->k[1];
+            a.gB = dt * C.a[3][2];
+            a.betaA = dt * C.b[2];
+            a.betaB = dt * C.b[3];
+            a.out = st->u_new;
+            a.out_y = nullptr;
+            CK_CTX(ctx, launch_gs_pair(PAIR_LAST, a, ctx->stream));
+        } else {  // explicit midpoint: u -> u_new (b_1 = 0)
+            a.out = st->u_new;
+            CK_CTX(ctx, launch_gs_pair(PAIR_ONLY, a, ctx->stream));
+        }
+        if (st->timing) {
+            CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+            st->pending.push_back({e0, e1, 0});
+            if (st->pending.size() > 4096) TRY(resolve_timing(st));
+        }
+        swap_u(st);
+        const int nl = rk4 ? 2 : 1;
+        st->stats.kernel_launches += nl;
+        st->stats.stage_launches += nl;
+        st->stats.rhs_evals += C.s;
+        // RK4: (u -> Y3, W) + (Y3, u, W -> u_new) = 7 arrays; midpoint: u -> u_new
+        st->stats.stage_bytes += (rk4 ? 7 : 2) * cells * 2 * (int64_t)sizeof(double);
+        st->stats.steps += 1;
+    }
+    st->k1_valid = false;
+    return RK_OK;
 }
 
 static rk_status fused_steps(rk_state st, int scheme, double dt, int64_t n) {
@@ -1279,6 +1362,7 @@ static rk_status rk_fixed_step(rk_state st, int scheme, double dt) {
         return RK_OK;
     }
     if (coop_path(st, scheme)) return coop_steps(st, scheme, dt, 1);
+    if (pair_path(st, scheme)) return pair_steps(st, scheme, dt, 1);
     if (fused_path(st, scheme)) return fused_steps(st, scheme, dt, 1);
     if (st->grid) {
         auto plan = build_plan(scheme, 0, dt);
@@ -2375,7 +2459,7 @@ rk_status rk_set_option(rk_state st, int key, int64_t value) {
         st->coop_max_cells = value;
         break;
     case RK_OPT_FUSED_STEP:
-        if (value < 0 || value > 2) return fail(RK_ERR_ARG, "RK_OPT_FUSED_STEP: 0, 1 (K6) or 2 (K7)");
+        if (value < 0 || value > 3) return fail(RK_ERR_ARG, "RK_OPT_FUSED_STEP: 0, 1 (K6), 2 (K7) or 3 (K8)");
         st->fused = (int)value;
         break;
     case RK_OPT_COMM_TIMEOUT_MS:

@@ -1,0 +1,136 @@
+"""GPU parity of K8 (rk_pair.cu, RK_OPT_FUSED_STEP = 3): two chained Runge–Kutta stages per
+launch (RK4 = two launches, explicit midpoint = one), the first stage's slope evaluated on the
+tile grown by one cell and never stored.  Gate: bitwise equality with the fp64 oracle
+(R-17) over several steps, on tile-aligned grids (nx % 32 == 0, ny % 16 == 0) from one
+tile to many with ragged z chunks, every z-chunk length (the chunk's two extra stage-A planes and
+four raw planes recomputed), the 2-cell periodic margin at every domain edge, and the
+stage-by-stage fallback on grids K8 does not take."""
+import numpy as np
+import pytest
+
+import oracle
+import rk_inputs
+
+pytestmark = pytest.mark.gpu
+OS = oracle.SCHEMES
+PAIR = ["rk4", "midpoint"]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_2309_05331_b200 as rk
+    c = rk.Context(0, 1, 0)
+    yield c
+    c.close()
+
+
+def bitwise(a, b):
+    a, b = np.asarray(a).ravel(), np.asarray(b).ravel()
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def first_mismatch(a, b):
+    a, b = np.asarray(a).ravel(), np.asarray(b).ravel()
+    bad = np.flatnonzero(a.view(np.uint64) != b.view(np.uint64))
+    return (bad.size, bad[:4], a[bad[:4]], b[bad[:4]]) if bad.size else None
+
+
+def pair_state(ctx, dims, u0, mode=3):
+    import paper_2309_05331_b200 as rk
+    st = ctx.grid(*dims, 2)
+    st.set_rhs_gray_scott()
+    st.set(u0)
+    st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
+    st.set_option(rk.OPT_FUSED_STEP, mode)
+    return st
+
+
+def perturbed_ic(nx, ny, nz, seed=42):
+    u0 = rk_inputs.gray_scott_ic(nx, ny, nz, seed=seed)
+    return u0 + 0.01 * rk_inputs.random_state(u0.size, 5).reshape(u0.shape)
+
+
+GRIDS = [(32, 16, 1), (32, 16, 3), (32, 32, 2), (64, 32, 5), (96, 48, 20), (128, 64, 37), (64, 16, 70)]
+
+
+@pytest.mark.parametrize("scheme", PAIR)
+@pytest.mark.parametrize("dims", GRIDS, ids=lambda d: "x".join(map(str, d)))
+def test_pair_steps_bitwise(ctx, scheme, dims):
+    u0 = perturbed_ic(*dims)
+    st = pair_state(ctx, dims, u0)
+    p = oracle.gray_scott_problem(*dims)
+    u = u0
+    before = st.stats()
+    for k in range(3):
+        st.do_step(scheme, float(k), 1.0)
+        u = oracle.step(p, OS[scheme], float(k), 1.0, u)
+        got = st.get()
+        assert bitwise(got, u), (scheme, dims, k, first_mismatch(got, u))
+    launches = st.stats()["stage_launches"] - before["stage_launches"]
+    st.close()
+    assert launches == 3 * (2 if scheme == "rk4" else 1)
+
+
+@pytest.mark.parametrize("pz", [1, 2, 3, 5, 8, 64])
+@pytest.mark.parametrize("scheme", PAIR)
+def test_pair_zchunks_bitwise(ctx, scheme, pz, monkeypatch):
+    monkeypatch.setenv("RKB_PZ", str(pz))
+    dims = (64, 32, 23)
+    u0 = perturbed_ic(*dims, seed=7)
+    st = pair_state(ctx, dims, u0)
+    p = oracle.gray_scott_problem(*dims)
+    u = u0
+    for k in range(2):
+        st.do_step(scheme, float(k), 1.0)
+        u = oracle.step(p, OS[scheme], float(k), 1.0, u)
+    got = st.get()
+    st.close()
+    assert bitwise(got, u), first_mismatch(got, u)
+
+
+@pytest.mark.parametrize("scheme", PAIR)
+def test_pair_production_size(ctx, scheme):
+    """256x256x100 (the production chunking of the other tests), 2 steps, every element."""
+    dims = (256, 256, 100)
+    u0 = perturbed_ic(*dims)
+    p = oracle.gray_scott_problem(*dims)
+    want = u0
+    for k in range(2):
+        want = oracle.step(p, OS[scheme], float(k), 1.0, want)
+    st = pair_state(ctx, dims, u0)
+    for k in range(2):
+        st.do_step(scheme, float(k), 1.0)
+    got = st.get()
+    st.close()
+    assert bitwise(got, want), first_mismatch(got, want)
+
+
+@pytest.mark.parametrize("dims", [(33, 17, 9), (40, 12, 6), (64, 24, 5)], ids=lambda d: "x".join(map(str, d)))
+def test_pair_fallback_unaligned(ctx, dims):
+    """Grids K8 does not take run the stage-by-stage kernels under the same option."""
+    u0 = perturbed_ic(*dims)
+    st = pair_state(ctx, dims, u0)
+    p = oracle.gray_scott_problem(*dims)
+    st.do_step("rk4", 0.0, 1.0)
+    got = st.get()
+    launches = st.stats()["stage_launches"]
+    st.close()
+    assert bitwise(got, oracle.step(p, OS["rk4"], 0.0, 1.0, u0))
+    assert launches == 4
+
+
+def test_pair_integrate_const_and_graph(ctx):
+    import paper_2309_05331_b200 as rk
+    dims = (64, 32, 16)
+    u0 = perturbed_ic(*dims, seed=3)
+    p = oracle.gray_scott_problem(*dims)
+    want, n = oracle.integrate_const(p, OS["rk4"], u0, 0.0, 5.0, 1.0)
+    st = pair_state(ctx, dims, u0)
+    assert st.integrate_const("rk4", 0.0, 5.0, 1.0) == n
+    assert bitwise(st.get(), want)
+    st.set(u0)
+    st.set_option(rk.OPT_USE_GRAPH, 1)
+    assert st.integrate_const("rk4", 0.0, 5.0, 1.0) == n
+    got = st.get()
+    st.close()
+    assert bitwise(got, want)

@@ -1,0 +1,41 @@
+"""Print the key per-kernel metrics of an .ncu-rep (raw page): time, DRAM bytes, pipe use,
+issue, warps, stalls.   python tools/ncu_keys.py report.ncu-rep"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__warps_eligible.avg.per_cycle_active", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum", "launch__registers_per_thread",
+        "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers", "lts__t_sector_hit_rate.pct",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active"]
+STALL = "smsp__average_warp_latency_issue_stalled_"
+
+
+def main(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        print("==", d.get("Kernel Name", "?")[:110])
+        for k in KEYS:
+            if k in d:
+                print(f"   {k} = {d[k]} {u.get(k, '')}")
+        st = []
+        for k, v in d.items():
+            if k.startswith("smsp__average_warp_latency_issue_stalled_") and k.endswith(".ratio"):
+                try:
+                    st.append((float(v), k[len(STALL):-6]))
+                except ValueError:
+                    pass
+        st.sort(reverse=True)
+        print("   top stalls (warps per issue): " + ", ".join(f"{n}={v:.2f}" for v, n in st[:8]))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
