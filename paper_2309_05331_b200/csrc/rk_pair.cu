@@ -22,7 +22,7 @@
 // 4D TMA box per input into an R-deep mbarrier ring: Y_A's source with a 2-cell margin (38x20
 // box from the 16-byte aligned column x0-2; CTAs on the domain edge patch the periodic cells
 // beyond the padded layout's 1-cell ring in place) and u with a 1-cell margin when it is not
-// Y_A's source; W (own cells only) comes by plain loads one plane ahead.  Iteration t (stage A at plane t, stage B at plane t-1) has ONE
+// Y_A's source; W (own cells only) comes by plain loads issued before stage A.  Iteration t (stage A at plane t, stage B at plane t-1) has ONE
 // __syncthreads: [patch plane t+1]; barrier; k_A at plane t (own cells: xy neighbours from the
 // ring, z column in registers; ring cells: all from the ring) -> Y_B(t) into a 2-slot buffer
 // (own cells also in registers); k_B at plane t-1 (xy from the Y_B buffer, z from registers) ->
@@ -33,6 +33,8 @@
 // any tile / chunk decomposition.  One GPU (z wraps by index), nx % 32 == 0, ny % 16 == 0 (else
 // the library runs the stage-by-stage kernels).
 #include <cudaTypedefs.h>
+
+#include <type_traits>
 
 #include "rk_device.cuh"
 #include "rk_kernels.cuh"
@@ -110,6 +112,30 @@ __device__ __forceinline__ void rhs_two(const double* v0, int cs, int pitch, con
     }
     react(s0, c0, a, f0);
     react(s1, c1, a, f1);
+}
+
+// The same in two parts, so a thread can start k_B's xy sums before k_A (which yields k_B's
+// upper z neighbour) is done: sxy = the x and y terms, then the z pair and the reaction -- the
+// identical expression tree.
+__device__ __forceinline__ void lap_xy_two(const double* v0, int cs, int pitch, const double (&c0)[2],
+                                           const double (&c1)[2], double (&sx0)[2], double (&sx1)[2]) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const double* w = v0 + c * cs;
+        const double a0 = c0[c], a1 = c1[c];
+        const double s = add(sub(w[-1], a0), sub(w[1], a0));
+        sx0[c] = add(s, add(sub(w[-pitch], a0), sub(a1, a0)));
+        const double* w1 = w + pitch;
+        const double t = add(sub(w1[-1], a1), sub(w1[1], a1));
+        sx1[c] = add(t, add(sub(a0, a1), sub(w1[pitch], a1)));
+    }
+}
+__device__ __forceinline__ void finish_one(const double (&sx)[2], const double (&ctr)[2], const double (&zm)[2],
+                                           const double (&zp)[2], const PairArgs& a, double (&f)[2]) {
+    double s[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) s[c] = add(sx[c], add(sub(zm[c], ctr[c]), sub(zp[c], ctr[c])));
+    react(s, ctr, a, f);
 }
 
 // k = F(Y) at one cell with every value from boxes (ring cells)
@@ -206,20 +232,47 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
             "r"((uint32_t)((i / R) & 1))
             : "memory");
     };
-    // edge CTAs: the source box cells the padded layout does not hold (the 2nd margin cell,
-    // the ring corners) are overwritten with their periodic images from global memory
-    auto patch = [&](int i) PINLINE {
-        double* y = reinterpret_cast<double*>(raw(i));
-        const int64_t qo = (int64_t)plane(i) * G.ps;
+    // Edge CTAs: the source box cells the padded layout does not hold (the 2nd margin cell, the
+    // ring corners) are overwritten with their periodic images.  The list of such cells is built
+    // once (one per thread, at most 2*20 + 2*36 + corners < 256), and every thread holding one
+    // loads its values a plane ahead into registers, so the patch after a plane lands costs two
+    // shared stores, not a global-memory round trip.
+    __shared__ int s_np;
+    __shared__ int s_pos[PNT], s_src[PNT];
+    int my_pos = -1, my_src = 0;
+    if (edge) {
+        if (tid == 0) s_np = 0;
+        __syncthreads();
         for (int q = tid; q < NPATCH; q += PNT) {
             const int col = 1 + q % 36, row = q / 36;
             const int x = x0 - 3 + col, yy = y0 - 2 + row;
             const bool held = (x >= 0 && x < G.nx && yy >= -1 && yy <= G.ny) || (yy >= 0 && yy < G.ny && x >= -1 && x <= G.nx);
             if (held) continue;
-            const int64_t src = qo + (int64_t)(pmod(yy, G.ny) + 1) * G.P + (pmod(x, G.nx) + 1);
-            y[row * BW + col] = a.src[src];
-            y[BOX + row * BW + col] = a.src[src + G.cs];
+            const int k = atomicAdd(&s_np, 1);
+            s_pos[k] = row * BW + col;
+            s_src[k] = (pmod(yy, G.ny) + 1) * G.P + (pmod(x, G.nx) + 1);
         }
+        __syncthreads();
+        if (tid < s_np) {
+            my_pos = s_pos[tid];
+            my_src = s_src[tid];
+        }
+    }
+    double pv0 = 0.0, pv1 = 0.0;  // this thread's patch values of the next plane to land
+    auto patch_load = [&](int i) PINLINE {
+        if (my_pos >= 0 && i < nr) {
+            const double* p = a.src + (int64_t)plane(i) * G.ps + my_src;
+            pv0 = p[0];
+            pv1 = p[G.cs];
+        }
+    };
+    auto patch = [&](int i) PINLINE {  // after wait(i); then load the values of plane i+1
+        if (my_pos >= 0) {
+            double* y = reinterpret_cast<double*>(raw(i));
+            y[my_pos] = pv0;
+            y[BOX + my_pos] = pv1;
+        }
+        patch_load(i + 1);
     };
 
     if (tid == 0) {
@@ -232,13 +285,16 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
     if (tid == 0)
         for (int i = 0; i < (nr < R ? nr : R); ++i) issue(i);
 
-    // own-cell registers ([r] = row r0 / r1): Y_A at planes t-1, t, t+1; Y_B at t-2, t-1, t;
-    // k_A at t-1 (for the epilogue) and t; u at t-1 and t (U1); Wb at t-1 and t (WIN)
-    double yam[2][2], yac[2][2], yap[2][2];
-    double ybm[2][2] = {}, ybc[2][2] = {}, ybp[2][2] = {};
-    double kap[2][2] = {}, kac[2][2];
-    double uc[2][2] = {}, up[2][2] = {};  // U1: u at t (for Y_B) and t-1 (for the epilogue)
-    double wbn[2][2] = {}, wbp[2][2] = {};  // WIN: W at t (loaded one iteration ahead) and t-1
+    // own-cell registers ([q][r][c]: slot q = plane mod 3 within the unrolled loop, row r0 / r1,
+    // component): Y_A at planes t-1, t, t+1; Y_B at t-2, t-1, t; k_A at t-1 (for the epilogue)
+    // and t; u at t-1 and t (U1).  The loop is unrolled by three so these queues rotate by
+    // renaming, not by register moves.
+    // own-cell Y_A: a register queue where registers allow (the u-fed pairs); the pair that also
+    // streams u and W (at the 128-register cap) reads it from the ring instead
+    constexpr bool YREG = !U1;
+    double ya_q[YREG ? 3 : 1][2][2];
+    double yb_q[3][2][2] = {}, ka_q[3][2][2] = {}, u_q[3][2][2] = {};
+    double w_q[3][2][2] = {};  // WIN: W at t-1 (stage B's epilogue) and t (loaded one plane ahead)
     auto own_src = [&](int i, double (&v)[2][2]) PINLINE {
         const double* s = reinterpret_cast<const double*>(raw(i));
 #pragma unroll
@@ -247,52 +303,78 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
             v[r][1] = s[BOX + pb + r * BW];
         }
     };
+    patch_load(0);
     wait(0);
-    if (edge) patch(0);
+    patch(0);
     wait(1);
-    if (edge) patch(1);
+    patch(1);
     __syncthreads();  // patched cells visible
-    own_src(0, yac);
-    own_src(1, yap);
+    if constexpr (YREG) {
+        own_src(0, ya_q[2]);  // plane zb-2 = "t-1" of iteration 0
+        own_src(1, ya_q[0]);  // plane zb-1 = "t"
+    }
 
-    // iteration it: stage A at plane t = zb-1+it (raw index it+1), stage B at t-1
-    for (int it = 0; it < nout + 2; ++it) {
+    // iteration it (J = it mod 3): stage A at plane t = zb-1+it (raw index it+1), stage B at t-1
+    auto step = [&](int it, auto Jc) PINLINE {
+        constexpr int J = decltype(Jc)::value;
+        constexpr int Q0 = J, QP = (J + 1) % 3, QM = (J + 2) % 3;  // planes t, t+1 / t-2, t-1
         const int ic = it + 1;
         wait(it + 2);
-        if (edge) patch(it + 2);
+        patch(it + 2);
         __syncthreads();  // plane t+1 (patched) visible; Y_B(t-1) stored; raw plane t-2 free
         if (tid == 0 && it - 1 >= 0 && it - 1 + R < nr) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the patches
             issue(it - 1 + R);
         }
+        // own-cell Y_A at t-1, t, t+1 straight from the ring (registers are the scarcer resource)
+        double yam[2][2], yac[2][2], yap[2][2];
+        if constexpr (YREG) {
+            own_src(ic + 1, ya_q[QP]);  // Y_A(t+1) (slot of Y_A(t-2))
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
+            for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                yam[r][c] = yac[r][c];
-                yac[r][c] = yap[r][c];
-            }
-        own_src(it + 2, yap);
-        if constexpr (WIN) {  // W of plane t (used by stage B in the next iteration): plain loads
+                for (int c = 0; c < 2; ++c) {  // renaming only: no moves survive unrolling
+                    yam[r][c] = ya_q[QM][r][c];
+                    yac[r][c] = ya_q[Q0][r][c];
+                    yap[r][c] = ya_q[QP][r][c];
+                }
+        } else {
+            own_src(ic - 1, yam);
+            own_src(ic, yac);
+            own_src(ic + 1, yap);
+        }
+        const bool doB = it >= 2;  // stage B at plane t-1: output planes zb .. ze-1
+        if constexpr (WIN) {  // W of plane t (stage B's epilogue in the next iteration): plain loads
             if (it >= 1 && it <= nout) {
                 const double* W = a.w_in + (int64_t)(zb + it - 1) * G.ps + coff;
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
-                    wbn[r][0] = W[(int64_t)r * G.P];
-                    wbn[r][1] = W[G.cs + (int64_t)r * G.P];
+                    w_q[Q0][r][0] = W[(int64_t)r * G.P];
+                    w_q[Q0][r][1] = W[G.cs + (int64_t)r * G.P];
                 }
             }
         }
+        const double (&wbp)[2][2] = w_q[QM];
         const unsigned char* st = raw(ic);
         const double* ya = reinterpret_cast<const double*>(st);
         const bool ring_plane = it >= 1 && it <= nout;  // Y_B(t) is read by stage B's xy stencil
+        // Y_B: (t-2) in slot QP, (t-1) in slot QM = stage B's centres, Y_B(t) -> slot Q0
+        double (&ybm)[2][2] = yb_q[QP];
+        double (&ybc)[2][2] = yb_q[QM];
+        double (&ybp)[2][2] = yb_q[Q0];
+        // ---- stage B at plane t-1, xy part (its smem reads precede this iteration's stores) ----
+        double sb0[2] = {0.0, 0.0}, sb1[2] = {0.0, 0.0};
+        if (doB) lap_xy_two(ybs(ic - 1) + pu, YBOX, YBW, ybc[0], ybc[1], sb0, sb1);
         // ---- stage A at plane t ----
+        double (&kac)[2][2] = ka_q[Q0];
+        const double (&kap)[2][2] = ka_q[QM];
         rhs_two(ya + pb, BOX, BW, yac[0], yac[1], yam[0], yap[0], yam[1], yap[1], a, kac[0], kac[1]);
+        double (&uc)[2][2] = u_q[Q0];
+        const double (&up)[2][2] = u_q[QM];
         if constexpr (U1) {
             const double* U = reinterpret_cast<const double*>(st + LY::off_u);
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                up[r][0] = uc[r][0]; up[r][1] = uc[r][1];
                 uc[r][0] = U[pu + r * UW];
                 uc[r][1] = U[UBOX + pu + r * UW];
             }
@@ -300,11 +382,7 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                ybm[r][c] = ybc[r][c];
-                ybc[r][c] = ybp[r][c];
-                ybp[r][c] = add(U1 ? uc[r][c] : yac[r][c], mul(a.gB, kac[r][c]));
-            }
+            for (int c = 0; c < 2; ++c) ybp[r][c] = add(U1 ? uc[r][c] : yac[r][c], mul(a.gB, kac[r][c]));
         if (ring_plane) {
             double* yb = ybs(ic);
 #pragma unroll
@@ -325,10 +403,10 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
             }
         }
         // ---- stage B at plane t-1 (output planes zb .. ze-1) ----
-        if (it >= 2) {
-            const double* yb = ybs(ic - 1);
+        if (doB) {
             double kb[2][2];
-            rhs_two(yb + pu, YBOX, YBW, ybc[0], ybc[1], ybm[0], ybp[0], ybm[1], ybp[1], a, kb[0], kb[1]);
+            finish_one(sb0, ybc[0], ybm[0], ybp[0], a, kb[0]);
+            finish_one(sb1, ybc[1], ybm[1], ybp[1], a, kb[1]);
             const int64_t qo = (int64_t)(zb + it - 2) * G.ps;
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
@@ -354,18 +432,16 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
                 }
             }
         }
-        // epilogue inputs of plane t for the next iteration
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int c = 0; c < 2; ++c) kap[r][c] = kac[r][c];
-        if constexpr (WIN) {
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-                for (int c = 0; c < 2; ++c) wbp[r][c] = wbn[r][c];
-        }
+    };
+    const int niter = nout + 2;
+    int it = 0;
+    for (; it + 2 < niter; it += 3) {
+        step(it, std::integral_constant<int, 0>{});
+        step(it + 1, std::integral_constant<int, 1>{});
+        step(it + 2, std::integral_constant<int, 2>{});
     }
+    if (it < niter) step(it, std::integral_constant<int, 0>{});
+    if (it + 1 < niter) step(it + 1, std::integral_constant<int, 1>{});
 }
 
 template <bool U1, bool WIN, bool BA, bool YOUT>

@@ -12,7 +12,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum", "launch__registers_per_thread",
         "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers", "lts__t_sector_hit_rate.pct",
         "l1tex__throughput.avg.pct_of_peak_sustained_active"]
-STALL = "smsp__average_warp_latency_issue_stalled_"
+STALL = "smsp__average_warps_issue_stalled_"
 
 
 def main(path):
@@ -28,9 +28,9 @@ def main(path):
                 print(f"   {k} = {d[k]} {u.get(k, '')}")
         st = []
         for k, v in d.items():
-            if k.startswith("smsp__average_warp_latency_issue_stalled_") and k.endswith(".ratio"):
+            if k.startswith(STALL) and k.endswith("_per_issue_active.ratio"):
                 try:
-                    st.append((float(v), k[len(STALL):-6]))
+                    st.append((float(v), k[len(STALL):-len("_per_issue_active.ratio")]))
                 except ValueError:
                     pass
         st.sort(reverse=True)
