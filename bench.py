@@ -287,6 +287,9 @@ def run_reference(args, rank, world):
 # B/cell per step of each scheme's fused stage-by-stage schedule (the gate's
 # bytes; this build moves fewer for DOPRI5 / CK54 through the write-ahead stage)
 SURVEY_BYTES = {"euler": 32, "rk4": 208, "cash_karp54": 432, "dopri5": 432}
+# K6 / K8 roofline: algorithmic fp64 (non-FMA) operations per cell-step
+K6_OPS = {"rk4": 168, "midpoint": 78, "modified_midpoint": 125}
+K8_LAUNCHES = {"rk4": 2, "midpoint": 1}  # K8 stage-pair launches per step
 
 
 def main():
@@ -296,7 +299,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="cells per axis per GPU (x, y, z-slab)")
-    ap.add_argument("--legs", default="adaptive,rk4,repeats,try_loop,device_loop,halo,exposed,strong,strong_emul,rk4_native,rk4_k6,exp512,small,e2e,cpu",
+    ap.add_argument("--legs", default="adaptive,rk4,rk4_k3,repeats,try_loop,device_loop,halo,exposed,strong,strong_emul,rk4_native,rk4_k6,exp512,small,e2e,cpu",
                     help="comma list of legs (profiling runs use e.g. --legs rk4)")
     ap.add_argument("--no-extra", action="store_true", help="same as --legs adaptive")
     ap.add_argument("--overlap", type=int, default=1, help="halo exchange overlapped (N > 1)")
@@ -502,7 +505,7 @@ def main():
                 "ms_per_step": ms / args.steps, "tries": tries,
                 "config": "rk_try_step driven from Python, one accepted DOPRI5 step per step"}
 
-    def rk4_leg(overlap: int, scheme: str = "rk4", p2p: int = 0, loopback: int = 0):
+    def rk4_leg(overlap: int, scheme: str = "rk4", p2p: int = 0, loopback: int = 0, k8_ok: bool = True):
         st.set_option(rk.OPT_HALO_OVERLAP, overlap)
         st.set_option(rk.OPT_HALO_LOOPBACK, loopback)
         st.set_option(rk.OPT_HALO_P2P, p2p)
@@ -526,6 +529,8 @@ def main():
         st.set_option(rk.OPT_HALO_P2P, 0)
         st.set_option(rk.OPT_HALO_LOOPBACK, 0)
         a4 = s4["stage_bytes"] / (s4["stage_kernel_ms"] / 1e3) / 1e9 if s4["stage_kernel_ms"] else None
+        k8 = (k8_ok and world == 1 and not loopback and not p2p and scheme in K8_LAUNCHES
+              and s4["stage_launches"] == K8_LAUNCHES[scheme] * args.steps)
         out = {"value": cells_total * args.steps / (ms4 / 1e3), "ms_per_step": ms4 / args.steps,
                "halo_overlap": bool(overlap), "scheme": scheme,
                "halo_path": ("p2p" if p2p else "nccl") + (" (loopback)" if loopback else ""),
@@ -537,22 +542,42 @@ def main():
                "gpu_launches": s4["kernel_launches"]}
         if scheme in SURVEY_BYTES:  # SURVEY §8d's per-scheme B/cell (stage-by-stage schedule)
             out["roofline"]["survey_gate"] = survey_gate(SURVEY_BYTES[scheme], cells_local * args.steps, ms4)
+        if k8:
+            # K8 (stage pairs, the library default for RK4 / explicit midpoint on one GPU): 112 /
+            # 32 B/cell, bound by instruction issue and FP64 latency, not HBM -- the roofline is
+            # the FP64 pipe (148 SMs x 64 non-FMA ops/clk at the max SM clock) on the
+            # algorithmic op count per cell-step (the tile-ring re-evaluations of
+            # stage A are not counted); the HBM view stays beside it
+            k_ms = out["roofline"]["avg_launch_ms"] * K8_LAUNCHES[scheme]
+            ops = K6_OPS[scheme] * cells_local / (k_ms / 1e3) / 1e12 if k_ms else None
+            peak_ops = 148 * 64 * 1965e6 / 1e12
+            out["kernel"] = "gs_pair_kernel (K8: two chained stages per launch, stage A on the tile + 1 ring)"
+            out["roofline"] = {"bound": "alu", "achieved": ops, "peak": peak_ops, "unit": "TFLOP/s (fp64, non-FMA)",
+                               "frac": ops / peak_ops if ops else None, "ops_per_cell_step": K6_OPS[scheme],
+                               "avg_launch_ms": out["roofline"]["avg_launch_ms"],
+                               "hbm": {"achieved": a4, "peak": peak, "unit": "GB/s", "frac": a4 / peak if a4 else None,
+                                       "algorithmic_bytes_per_cell_step": out["roofline"]["algorithmic_bytes_per_cell_step"]}}
         h = halo_of(s4, bool(p2p))
         if h:
             out["halo"] = h
         return out
 
-    # K6 (RK_OPT_FUSED_STEP, one GPU): the whole step in one launch, stage values on chip.
-    # Bound by the FP64 pipe / latency, not HBM: roofline against the FP64 issue rate
-    # (148 SMs x 64 non-FMA fp64 ops/clk x the sampled SM clock) with the algorithmic op count
-    # per cell-step (RK4 168, midpoint 78; margin re-evaluations not counted).
-    K6_OPS = {"rk4": 168, "midpoint": 78, "modified_midpoint": 125}
+    def k3_leg(scheme):
+        # the stage-by-stage kernels (K3, RK_OPT_FUSED_STEP = 0) on the same workload: the
+        # HBM-roofline reference the K8 default is measured against
+        st.set_option(rk.OPT_FUSED_STEP, 0)
+        try:
+            out = rk4_leg(args.overlap, scheme, k8_ok=False)
+        finally:
+            st.set_option(rk.OPT_FUSED_STEP, 3)
+        out["kernel"] = "gs_stage_kernel (K3: one stage per launch)"
+        return out
 
     def k6_leg(scheme, mode=1):
         st.set_option(rk.OPT_FUSED_STEP, mode)
         with ClockSampler(local) as clk:
-            out = rk4_leg(args.overlap, scheme)
-        st.set_option(rk.OPT_FUSED_STEP, 0)
+            out = rk4_leg(args.overlap, scheme, k8_ok=False)
+        st.set_option(rk.OPT_FUSED_STEP, 3)
         mhz = (getattr(clk, "result", None) or {}).get("sm_mhz") or 1965.0
         peak_ops = 148 * 64 * mhz * 1e6 / 1e12
         ms = out["ms_per_step"]
@@ -998,12 +1023,24 @@ def main():
         if line and "roofline" in r4:
             # north_star's second target workload, kept inside `roofline` (the driver's parsed
             # record keeps this object but not `extra`)
+            rf = r4["roofline"]
             line["roofline"]["rk4_512"] = {
                 "workload": "gray_scott_rk4_dt1_512^3_per_gpu (do_step x K)", "value": r4["value"],
-                "unit": "cell-updates/s", "ms_per_step": r4["ms_per_step"],
-                "achieved": r4["roofline"]["achieved"], "frac": r4["roofline"]["frac"],
-                "algorithmic_bytes_per_cell_step": r4["roofline"]["algorithmic_bytes_per_cell_step"],
-                "traffic": r4["roofline"]["traffic"]}
+                "unit": "cell-updates/s", "ms_per_step": r4["ms_per_step"], "kernel": r4.get("kernel", "K3"),
+                "bound": rf["bound"], "achieved": rf["achieved"], "peak": rf.get("peak"), "unit_roofline": rf.get("unit"),
+                "frac": rf["frac"]}
+            if "hbm" in rf:
+                line["roofline"]["rk4_512"]["hbm"] = rf["hbm"]
+            else:
+                line["roofline"]["rk4_512"]["algorithmic_bytes_per_cell_step"] = rf["algorithmic_bytes_per_cell_step"]
+                line["roofline"]["rk4_512"]["traffic"] = rf["traffic"]
+    if "rk4_k3" in legs and world == 1:
+        extra["rk4_k3"] = run_leg(k3_leg, "rk4")
+        if line and "rk4_512" in line.get("roofline", {}) and "ms_per_step" in extra["rk4_k3"]:
+            k3 = extra["rk4_k3"]
+            line["roofline"]["rk4_512"]["stage_by_stage"] = {
+                "kernel": "K3", "ms_per_step": k3["ms_per_step"], "frac_hbm": k3["roofline"]["frac"],
+                "algorithmic_bytes_per_cell_step": k3["roofline"]["algorithmic_bytes_per_cell_step"]}
     if "try_loop" in legs:
         extra["dopri5_try_loop"] = run_leg(try_loop_leg)
     if "repeats" in legs:
@@ -1042,6 +1079,8 @@ def main():
         extra["strong"] = run_leg(strong_leg)
     if "rk4_native" in legs:
         extra["rk4_native"] = run_leg(native_rk4_leg)
+    if "midpoint_k3" in legs and world == 1:
+        extra["midpoint_k3"] = run_leg(k3_leg, "midpoint")
     for sch in ("rk4", "midpoint", "modified_midpoint"):  # --legs rk4_k6,rk4_k7,...
         for mode in (1, 2):
             leg = f"{sch}_k{5 + mode}"

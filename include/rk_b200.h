@@ -148,15 +148,18 @@ typedef enum {
                                 persistent cooperative launch (all stages of all steps, grid-
                                 wide barrier between stages): same results bit for
                                 bit, no per-stage launch cost.  Default 2^18 (64^3); 0 = off. */
-    RK_OPT_FUSED_STEP = 11,    /* 1: fixed RK4 / explicit- / modified-midpoint steps of a Gray–Scott
-                                grid (one GPU, no halo path, above RK_OPT_COOP_MAX_CELLS) run as
-                                ONE launch per step that keeps every stage value on chip
-                                (temporal blocking across the stages, K6): u read
-                                and u_new written once per step (32 B/cell instead of 208 / 80 /
-                                144), same results bit for bit.  2: the same step with warp-
-                                specialised stage groups handing planes over through mbarriers
-                                (K7).  Both are ablations, slower than the default on the B200.
-                                0 (default): stage-by-stage launches.                        */
+    RK_OPT_FUSED_STEP = 11,    /* temporal blocking of fixed RK4 / explicit- / modified-midpoint steps
+                                of a Gray–Scott grid (one GPU, no halo path, above
+                                RK_OPT_COOP_MAX_CELLS), same results bit for bit:
+                                3 (default): K8 stage pairs -- two chained stages per launch,
+                                the first on the tile grown by one cell and never stored (RK4:
+                                two launches, 112 B/cell instead of 208; explicit midpoint: one,
+                                32 B instead of 80); needs nx % 32 == 0 and
+                                ny % 16 == 0, other grids and the modified midpoint run the
+                                stage-by-stage kernels.  1: K6, the whole step in ONE launch
+                                with every stage value on chip (32 B/cell).  2: K7, K6 with
+                                warp-specialised stage groups.  K6 and K7 are ablations, slower
+                                than K8 and K3 on the B200.  0: stage-by-stage launches (K3). */
     RK_OPT_COMM_TIMEOUT_MS = 12,/* multi-GPU failure detection, applies to the state's context:
                                 host waits on a stream with NCCL work poll the stream and
                                 ncclCommGetAsyncError; an asynchronous NCCL error, or no

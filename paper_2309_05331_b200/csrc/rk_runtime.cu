@@ -264,7 +264,7 @@ struct rk_state_s {
     int64_t check_finite = 0;    // RK_OPT_CHECK_FINITE: check u every n steps (0: never)
     int64_t since_check = 0;     // steps since the last finiteness check
     int64_t coop_max_cells = 1 << 18;  // RK_OPT_COOP_MAX_CELLS: persistent-step path up to here
-    int fused = 0;               // RK_OPT_FUSED_STEP: 1 K6, 2 K7 whole-step launches (chained tableaux)
+    int fused = 3;               // RK_OPT_FUSED_STEP: 3 K8 stage pairs (default), 1 K6 / 2 K7 whole steps, 0 stage by stage
     int64_t spike_at = 0, spike_seen = 0;  // RK_OPT_ERROR_SPIKE: inject at try number spike_at
     bool fused_kernels = true;   // RK_OPT_FUSED_KERNELS = 0: Odeint-like unfused stages (ablation)
     double* uf_y = nullptr;      // unfused: the stage value Y_i and the error estimate e

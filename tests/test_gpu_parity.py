@@ -32,13 +32,15 @@ def bitwise(a, b):
 
 def gs_state(ctx, nx, ny, nz, u0, coop=False, **prm):
     """A Gray–Scott state.  coop=False pins fixed steps to the stage-by-stage TMA stencil
-    path (K3); coop=True leaves the persistent small-grid path (K5) on (library default)."""
+    path (K3: no K5, no K8 stage pairs); coop=True leaves the persistent small-grid path (K5)
+    on (library default).  K8 has its own tests (test_gpu_pair.py)."""
     import paper_2309_05331_b200 as rk
     st = ctx.grid(nx, ny, nz, 2)
     st.set_rhs_gray_scott(**prm)
     st.set(u0)
     if not coop:
         st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
+        st.set_option(rk.OPT_FUSED_STEP, 0)
     return st
 
 
