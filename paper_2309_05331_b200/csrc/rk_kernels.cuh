@@ -238,17 +238,22 @@ cudaError_t launch_gs_fused(int scheme, const GsFusedArgs& a, cudaStream_t st);
 // (+) betaB k_B with Wb = W_in or u; out = W (and out_y = u (+) gN k_B when a pair follows).
 struct PairArgs {
     CUtensorMap tm_src;    // Y_A as stored (u, or the written-ahead Y): 38 x 20 box (encode_pair_map)
-    CUtensorMap tm_u;      // u: K3's 34 x 18 tile + ring box (PAIR_LAST)
+    CUtensorMap tm_u;      // u: K3's 34 x 18 tile + ring box (PAIR_LAST); PAIR_DP_TAIL: W
+    CUtensorMap tm_e, tm_uo, tm_k1;  // PAIR_DP_TAIL: E, u, k_1 interior boxes (L2 prefetch)
     const double* src;     // raw pointer of the source (periodic cells beyond the padded ring)
-    const double* w_in;    // PAIR_LAST: the partial sum W of the first pair
+    const double* w_in;    // PAIR_LAST: the partial sum W of the first pair; PAIR_DP_TAIL: E
+    const double* u_in;    // PAIR_DP_TAIL: u and k_1 (the ratio's denominator, own cells)
+    const double* k1_in;
+    unsigned long long* errmax;  // PAIR_DP_TAIL: block max of the error ratio's bits
     double* out;           // W (PAIR_FIRST) or u_new (ring copies written)
     double* out_y;         // PAIR_FIRST: the next pair's stage value (ring copies written)
     GridGeom geo;          // nzl = nz: one GPU, z wraps by index
-    double gB, gN, betaA, betaB;
+    double gB, gN, betaA, betaB;  // PAIR_DP_TAIL: gB = dt b_6, betaA / betaB = dt e_6 / dt e_7
+    double dt, atol, rtol;
     double d1, d2, F, FK, inv_h2;
     int zchunk;
 };
-enum { PAIR_FIRST = 0, PAIR_LAST = 1, PAIR_ONLY = 2 };
+enum { PAIR_FIRST = 0, PAIR_LAST = 1, PAIR_ONLY = 2, PAIR_DP_TAIL = 3 };
 bool pair_shape_ok(const GridGeom& g);  // nx % 32 == 0, ny % 16 == 0
 cudaError_t encode_pair_map(CUtensorMap* map, const double* base, const GridGeom& g, int nplanes);
 cudaError_t launch_gs_pair(int kind, const PairArgs& a, cudaStream_t st);

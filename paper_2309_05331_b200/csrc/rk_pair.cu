@@ -163,7 +163,11 @@ __device__ __forceinline__ void store_ring(double* p, const GridGeom& G, bool ex
     if (ey1) p[-(int64_t)G.ny * G.P] = v;
 }
 
-template <bool U1, bool WIN, bool BA, bool YOUT>
+// DP: the Dormand–Prince error-controlled tail pair (stages 6 and 7 of a try): the source is
+// Y_6 (written ahead), Y_B = W (+) (dt b_6) k_6 = u_new (a_7j = b_j, FSAL), k_B = k_7 = F(u_new);
+// the epilogue stores u_new and k_7, forms e = (E (+) (dt e_6) k_6) (+) (dt e_7) k_7 and the
+// Odeint ratio |e| / (atol (+) rtol (x) (|u| (+) dt (x) |k_1|)) with a block max.
+template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false>
 __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__ PairArgs a) {
     using LY = PLayout<U1>;
     constexpr int R = LY::R;
@@ -314,6 +318,9 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
         own_src(1, ya_q[0]);  // plane zb-1 = "t"
     }
 
+    double rmax = 0.0;                // DP: running max of the ratio (exact) and its bits
+    unsigned long long rbits = 0ull;
+
     // iteration it (J = it mod 3): stage A at plane t = zb-1+it (raw index it+1), stage B at t-1
     auto step = [&](int it, auto Jc) PINLINE {
         constexpr int J = decltype(Jc)::value;
@@ -344,7 +351,7 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
             own_src(ic + 1, yap);
         }
         const bool doB = it >= 2;  // stage B at plane t-1: output planes zb .. ze-1
-        if constexpr (WIN) {  // W of plane t (stage B's epilogue in the next iteration): plain loads
+        if constexpr (WIN && !DP) {  // W of plane t (stage B's epilogue in the next iteration): plain loads
             if (it >= 1 && it <= nout) {
                 const double* W = a.w_in + (int64_t)(zb + it - 1) * G.ps + coff;
 #pragma unroll
@@ -355,6 +362,30 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
             }
         }
         const double (&wbp)[2][2] = w_q[QM];
+        double eo[2][2] = {}, uo[2][2] = {}, k1o[2][2] = {};  // DP: E, u, k_1 at plane t-1
+        if constexpr (DP) {
+            if (doB) {  // plain loads (in L2: prefetched two planes ahead), consumed after stage A
+                const int64_t o = (int64_t)(zb + it - 2) * G.ps + coff;
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int64_t q = o + c * G.cs + (int64_t)r * G.P;
+                        eo[r][c] = a.w_in[q];
+                        uo[r][c] = a.u_in[q];
+                        k1o[r][c] = a.k1_in[q];
+                    }
+            }
+            if (tid == 0 && it + 2 >= 2 && it + 2 < nout + 2) {  // own inputs two planes ahead into L2
+                const int q = zb + it;
+#pragma unroll
+                for (int m = 0; m < 3; ++m)
+                    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                                     reinterpret_cast<uint64_t>(m == 0 ? &a.tm_e : m == 1 ? &a.tm_uo : &a.tm_k1)),
+                                 "r"(x0), "r"(y0 + 1), "r"(0), "r"(q)
+                                 : "memory");
+            }
+        }
         const unsigned char* st = raw(ic);
         const double* ya = reinterpret_cast<const double*>(st);
         const bool ring_plane = it >= 1 && it <= nout;  // Y_B(t) is read by stage B's xy stencil
@@ -414,6 +445,34 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
                 const int64_t ro = qo + coff + (int64_t)r * G.P;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
+                    if constexpr (DP) {
+                        const double un = ybc[r][c];  // Y_7 = u_new
+                        double* pu_ = a.out + ro + c * G.cs;
+                        double* pk = a.out_y + ro + c * G.cs;
+                        if (ering) {
+                            store_ring(pu_, G, rx0, rx1, ry0, ry1, un);
+                            store_ring(pk, G, rx0, rx1, ry0, ry1, kb[r][c]);
+                        } else {
+                            pu_[0] = un;
+                            pk[0] = kb[r][c];
+                        }
+                        // e' = E (+) (dt e_6) k_6 (stage 6's epilogue), e = e' (+) (dt e_7) k_7
+                        const double e = add(add(eo[r][c], mul(a.betaA, kap[r][c])), mul(a.betaB, kb[r][c]));
+                        const double dd = add(a.atol, mul(a.rtol, add(fabs(uo[r][c]), mul(a.dt, fabs(k1o[r][c])))));
+                        // r = |e| / dd exactly; the division is skipped when e == 0 or when
+                        // |e| <= rmax*dd*(1-2^-52) proves r <= rmax (K3's filter; NaN never skips)
+                        const double ae = fabs(e);
+                        const double th = mul(mul(rmax, dd), 0.99999999999999978);
+                        if (!(ae == 0.0 || (ae <= th && th >= 2.2250738585072014e-308))) {
+                            const double rr = ae / dd;
+                            const unsigned long long rbv = ratio_bits(rr);
+                            if (rbv > rbits) {
+                                rbits = rbv;
+                                rmax = rr;
+                            }
+                        }
+                        continue;
+                    }
                     // Wb: W of the previous pair, else u (= Y_A for a pair fed by u)
                     double wv = WIN ? wbp[r][c] : (U1 ? up[r][c] : yam[r][c]);
                     if constexpr (BA) wv = add(wv, mul(a.betaA, kap[r][c]));
@@ -442,21 +501,22 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
     }
     if (it < niter) step(it, std::integral_constant<int, 0>{});
     if (it + 1 < niter) step(it + 1, std::integral_constant<int, 1>{});
+    if constexpr (DP) block_max_to_global(rbits, a.errmax);
 }
 
-template <bool U1, bool WIN, bool BA, bool YOUT>
+template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false>
 cudaError_t launch_pair_t(const PairArgs& a, cudaStream_t st) {
     using LY = PLayout<U1>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gs_pair_kernel<U1, WIN, BA, YOUT>,
+        cudaError_t e = cudaFuncSetAttribute(gs_pair_kernel<U1, WIN, BA, YOUT, DP>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, LY::smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     const int tiles = (a.geo.nx / PX) * (a.geo.ny / PTH);
     const int nch = (a.geo.nzl + a.zchunk - 1) / a.zchunk;
-    gs_pair_kernel<U1, WIN, BA, YOUT><<<dim3((unsigned)tiles, (unsigned)nch), PNT, LY::smem, st>>>(a);
+    gs_pair_kernel<U1, WIN, BA, YOUT, DP><<<dim3((unsigned)tiles, (unsigned)nch), PNT, LY::smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -489,6 +549,7 @@ cudaError_t launch_gs_pair(int kind, const PairArgs& a, cudaStream_t st) {
     case PAIR_FIRST: return launch_pair_t<false, false, true, true>(a, st);  // RK4 1-2: u -> Y3, W
     case PAIR_LAST: return launch_pair_t<true, true, true, false>(a, st);    // RK4 3-4: Y3, u, W -> u_new
     case PAIR_ONLY: return launch_pair_t<false, false, false, false>(a, st); // midpoint: u -> u_new
+    case PAIR_DP_TAIL: return launch_pair_t<true, true, true, false, true>(a, st);  // DOPRI5 6-7
     default: return cudaErrorInvalidValue;
     }
 }

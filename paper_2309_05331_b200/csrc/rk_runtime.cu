@@ -910,12 +910,83 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
     return launch_stage_timed(st, p, a);
 }
 
+static int pick_pair_zchunk(rk_state st);
+
+// K8 DOPRI5 tail pair (rk_pair.cu PAIR_DP_TAIL): stages 6 and 7 of an error-controlled try
+// (Odeint ratio) in one launch on one GPU -- reads Y_6, W, E (written ahead by stage 5) and u,
+// k_1; writes u_new, k_7 (into stage 7's buffer) and the ratio max: 7 arrays instead of 10.
+static bool dp_tail_pair_ok(rk_state st, const std::vector<StagePlan>& plan) {
+    if (st->fused != 3 || !st->grid || st->ncomp != 2 || st->rhs != RHS_GRAY_SCOTT || st->ctx->world != 1 ||
+        st->loopback || st->p2p || st->gl_dtp || !pair_shape_ok(st->geo) || plan.size() != 7)
+        return false;
+    const StagePlan& f = plan[5];
+    const StagePlan& t = plan[6];
+    return f.scheme == RK_DOPRI5 && f.adaptive == 1 && f.sp.epi == EPI_FINAL_EPART && f.sp.base_src >= 0 &&
+           f.sp.wslot == 0 && f.sp.eslot == 1 && t.sp.epi == EPI_TAIL_ERR && t.sp.den_k1 >= 0;
+}
+
+static rk_status dp_tail_pair(rk_state st, const std::vector<StagePlan>& plan, double dt, double atol, double rtol) {
+    NvtxRange nv("rk stage pair (K8 DOPRI5 tail)");
+    rk_ctx ctx = st->ctx;
+    const StagePlan& f = plan[5];
+    const StagePlan& t = plan[6];
+    PairArgs a{};
+    a.geo = st->geo;
+    a.d1 = st->d1;
+    a.d2 = st->d2;
+    a.F = st->F;
+    a.FK = st->F + st->K;
+    a.inv_h2 = 1.0 / (st->h * st->h);
+    a.zchunk = pick_pair_zchunk(st);
+    double* y6 = st->k[f.sp.base_src];
+    CK_CTX(ctx, encode_pair_map(&a.tm_src, y6, st->geo, (int)st->local));
+    a.src = y6;
+    a.tm_u = st->tm_k[f.sp.src[0]].m[2];  // W: tile + 1 ring (stored with its ring by stage 5)
+    a.w_in = st->k[f.sp.src[1]];          // E
+    a.u_in = st->u;
+    a.k1_in = st->k[0];
+    a.tm_e = st->tm_k[f.sp.src[1]].m[3];  // 34 x 16 interior boxes: L2 prefetch of the own inputs
+    a.tm_uo = st->tm_u.m[3];
+    a.tm_k1 = st->tm_k[0].m[3];
+    a.out = st->u_new;
+    a.out_y = st->k[t.sp.out_k];
+    a.errmax = st->d_err;
+    a.gB = f.beta_new;
+    a.betaA = f.delta_new;
+    a.betaB = t.delta_new;
+    a.dt = dt;
+    a.atol = atol;
+    a.rtol = rtol;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (st->timing) {
+        e0 = pool_event(st);
+        e1 = pool_event(st);
+        CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+    }
+    CK_CTX(ctx, launch_gs_pair(PAIR_DP_TAIL, a, ctx->stream));
+    if (st->timing) {
+        CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+        st->pending.push_back({e0, e1, 0});
+        if (st->pending.size() > 4096) TRY(resolve_timing(st));
+    }
+    st->stats.kernel_launches += 1;
+    st->stats.stage_launches += 1;
+    st->stats.rhs_evals += 2;
+    st->stats.stage_bytes += 7 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double);
+    return RK_OK;
+}
+
 // Run the stages of one step / try.  Stage 0 (k1 = F(u)) is skipped when k1 is valid.
 static rk_status run_grid_plan(rk_state st, const std::vector<StagePlan>& plan, double dt,
                                double atol, double rtol) {
     TRY(ensure_k(st, plan_num_k(plan)));
     TRY(ensure_halo(st));
+    const bool dp_pair = dp_tail_pair_ok(st, plan);
     for (const StagePlan& p : plan) {
+        if (dp_pair && p.stage == 5) {  // stages 6 + 7 as one K8 launch
+            CK_CTX(st->ctx, cudaMemsetAsync(st->d_err, 0, sizeof(unsigned long long), st->ctx->stream));
+            return dp_tail_pair(st, plan, dt, atol, rtol);
+        }
         if (p.stage == 0 && p.sp.epi == EPI_K && st->k1_valid) continue;
         if (is_ratio_stage(p))
             CK_CTX(st->ctx, cudaMemsetAsync(st->d_err, 0, sizeof(unsigned long long), st->ctx->stream));

@@ -134,3 +134,80 @@ def test_pair_integrate_const_and_graph(ctx):
     got = st.get()
     st.close()
     assert bitwise(got, want)
+
+
+# ---- DOPRI5 error-controlled tail pair (PAIR_DP_TAIL: stages 6 + 7 in one launch) ----------
+def dp_oracle_try(dims, u0, dt, tol=1e-6):
+    p = oracle.gray_scott_problem(*dims)
+    un, err = oracle.step(p, OS["dopri5"], 0.0, dt, u0, with_error=True)
+    E = oracle.error_ratio_max(err, u0, oracle.rhs(p, u0), dt, tol, tol)
+    return un, E
+
+
+@pytest.mark.parametrize("dims", [(32, 16, 1), (32, 16, 4), (64, 32, 9), (96, 48, 20), (128, 64, 37)],
+                         ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("dt", [1.0, 4.0])
+def test_dp_tail_pair_try_bitwise(ctx, dims, dt):
+    """One try from the IC (k1 = F(u) first): E bitwise, u_new (accepted) every element; k7
+    through the next try's FSAL reuse."""
+    u0 = perturbed_ic(*dims)
+    want, E_o = dp_oracle_try(dims, u0, dt)
+    st = pair_state(ctx, dims, u0)
+    before = st.stats()["stage_launches"]
+    acc, E, _ = st.try_step("dopri5", 0.0, dt, 1e-6, 1e-6)
+    launches = st.stats()["stage_launches"] - before
+    got = st.get()
+    assert E == E_o, (E, E_o)
+    assert launches == 6  # k1, stages 2..5, the tail pair
+    assert bitwise(got, want if acc else u0), first_mismatch(got, want if acc else u0)
+    if acc:  # the next try starts from k7 (FSAL): compare its E and result too
+        want2, E2_o = dp_oracle_try(dims, want, dt)
+        acc2, E2, _ = st.try_step("dopri5", dt, dt, 1e-6, 1e-6)
+        assert E2 == E2_o
+        if acc2:
+            assert bitwise(st.get(), want2)
+    st.close()
+
+
+@pytest.mark.parametrize("pz", [1, 2, 3, 7, 64])
+def test_dp_tail_pair_zchunks(ctx, pz, monkeypatch):
+    monkeypatch.setenv("RKB_PZ", str(pz))
+    dims = (64, 32, 23)
+    u0 = perturbed_ic(*dims, seed=11)
+    want, E_o = dp_oracle_try(dims, u0, 2.0)
+    st = pair_state(ctx, dims, u0)
+    acc, E, _ = st.try_step("dopri5", 0.0, 2.0, 1e-6, 1e-6)
+    got = st.get()
+    st.close()
+    assert E == E_o
+    assert bitwise(got, want if acc else u0)
+
+
+def test_dp_tail_pair_integrate_adaptive(ctx):
+    """The headline call on a tile-aligned grid: counts identical, final state bitwise."""
+    dims = (128, 64, 48)
+    u0 = perturbed_ic(*dims, seed=7)
+    p = oracle.gray_scott_problem(*dims)
+    want, a_o, r_o, rc = oracle.integrate_adaptive(p, OS["dopri5"], u0, 0.0, 20.0, 1.0, 1e-6, 1e-6)
+    assert rc == 0 and r_o > 0
+    st = pair_state(ctx, dims, u0)
+    a, r = st.integrate_adaptive("dopri5", 0.0, 20.0, 1.0, 1e-6, 1e-6)
+    got = st.get()
+    st.close()
+    assert (a, r) == (a_o, r_o)
+    assert bitwise(got, want), first_mismatch(got, want)
+
+
+def test_dp_tail_pair_equals_stage_kernels(ctx):
+    """Same try sequence with the tail pair (default) and with the stage-by-stage kernels."""
+    import paper_2309_05331_b200 as rk
+    dims = (96, 32, 30)
+    u0 = perturbed_ic(*dims, seed=5)
+    res = []
+    for mode in (3, 0):
+        st = pair_state(ctx, dims, u0, mode)
+        seq = [st.try_step("dopri5", 0.5 * k, 0.5 + k, 1e-7, 1e-7) for k in range(4)]
+        res.append((seq, st.get()))
+        st.close()
+    assert res[0][0] == res[1][0]
+    assert bitwise(res[0][1], res[1][1])
