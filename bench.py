@@ -456,8 +456,10 @@ def main():
                                            "dram__bytes_write.sum per stage launch of one DOPRI5 try "
                                            "from the committed ncu --set full capture "
                                            f"(profiles/ncu_traffic.json: {str(traffic.get('_source', '?'))[:40]})",
-                         "kernel": "gs_stage_kernel (K3: fused stage value + 7-pt stencil + "
-                                   "reaction + epilogue), all stage launches of the timed tries",
+                         "kernel": "all stage launches of the timed tries: gs_stage_kernel (K3: fused "
+                                   "stage value + 7-pt stencil + reaction + epilogue) for stages 1-5 "
+                                   "(HBM-bound) and gs_pair_kernel (K8: stages 6 + 7 in one launch, "
+                                   "u_new / FSAL k7 / error ratio) -- 27 arrays = 432 B/cell/try",
                          "algorithmic_bytes_per_launch": s["stage_bytes"] / max(1, s["stage_launches"]),
                          "algorithmic_bytes_per_cell_try": step_bytes / cells_local,
                          "avg_launch_ms": k_ms / max(1, s["stage_launches"]),

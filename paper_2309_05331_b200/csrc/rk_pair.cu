@@ -57,6 +57,11 @@ constexpr int USLOT = (2 * UBOX * 8 + 127) / 128 * 128;   // 9856 B
 constexpr int YBW = UW, YBH = UH, YBOX = UBOX;            // Y_B buffer: tile + 1 ring
 constexpr int YBSLOT = USLOT;
 constexpr int NRING = 2 * PX + 2 * PTH;                   // tile+1 ring without its corners: 96
+#ifndef RKB_RING_WARPS
+#define RKB_RING_WARPS 3
+#endif
+constexpr int RING_WARPS = RKB_RING_WARPS;                // 3 (32 lanes; measured) or 4 (24 lanes each)
+static_assert(NRING % RING_WARPS == 0 && NRING / RING_WARPS <= 32, "ring split");
 constexpr int NPATCH = 36 * BH;                           // source positions used (box cols 1..36)
 constexpr int SMEM_BUDGET = 113 * 1024;                   // 2 CTAs per SM
 
@@ -195,14 +200,17 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
     const bool ey0 = y0 + 2 * w == 0, ey1 = y0 + 2 * w + 1 == G.ny - 1;
     const bool ering = ex0 || ex1 || ey0 || ey1;
     // ring cell of the tile grown by one (no corners): top row, bottom row, left col, right col
-    const bool hr = tid < NRING;
+    // (RING_WARPS warps share the 96 ring cells, one warp per SM sub-partition when 4)
+    constexpr int RPW = NRING / RING_WARPS;  // ring cells per ring warp
+    const int rj = (tid / 32) * RPW + (tid % 32);
+    const bool hr = tid / 32 < RING_WARPS && tid % 32 < RPW;
     int rb = 0, ru = 0;
     if (hr) {
         int rx, ry;
-        if (tid < PX) { rx = tid; ry = -1; }
-        else if (tid < 2 * PX) { rx = tid - PX; ry = PTH; }
-        else if (tid < 2 * PX + PTH) { rx = -1; ry = tid - 2 * PX; }
-        else { rx = PX; ry = tid - 2 * PX - PTH; }
+        if (rj < PX) { rx = rj; ry = -1; }
+        else if (rj < 2 * PX) { rx = rj - PX; ry = PTH; }
+        else if (rj < 2 * PX + PTH) { rx = -1; ry = rj - 2 * PX; }
+        else { rx = PX; ry = rj - 2 * PX - PTH; }
         rb = (ry + 2) * BW + (rx + 3);
         ru = (ry + 1) * UW + (rx + 1);
     }

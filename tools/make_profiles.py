@@ -54,18 +54,18 @@ def main(tag, out):
     open(os.path.join(out, f"{tag}_warm_dram.txt"), "w").write(sn.warm(os.path.join(g, f"tune_{tag}.csv")) + "\n")
     traffic = {"_source": f"{tag} (tools/profile_round.sh): dram__bytes_read.sum + dram__bytes_write.sum per "
                           "stage launch of one step, cold L2 (ncu default cache control); adaptive (one "
-                          "DOPRI5 try, 6 launches) and rk4 from ncu --set full captures, the other legs "
+                          "DOPRI5 try: 4 K3 stages + the K8 tail pair), rk4 (K8, 2 launches) and rk4_k3 from ncu --set full captures, the other legs "
                           "from metrics-only captures; abm legs: the PEC launch plus rk4's k1-type launch"}
     rk4_first = None
-    for leg in ("adaptive", "rk4"):
+    for leg in ("adaptive", "rk4", "rk4_k3"):
         rep = os.path.join(g, f"{tag}_full_{leg}.ncu-rep")
         if not os.path.exists(rep):
             print("missing", rep)
             continue
         open(os.path.join(out, f"{tag}_{leg}_full_summary.txt"), "w").write(sn.full(rep) + "\n")
         pl = full_launch_bytes(rep)
-        if leg == "rk4":
-            rk4_first = pl[0]
+        if leg == "rk4_k3":
+            rk4_first = pl[0]  # the k1-type K3 stage (abm legs)
         traffic["dopri5_adaptive" if leg == "adaptive" else leg] = {
             "bytes_per_launch": sum(b for _, b in pl) / len(pl), "launches": len(pl), "per_launch": pl}
     for f in sorted(os.listdir(g)):
