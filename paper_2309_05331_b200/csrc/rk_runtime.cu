@@ -910,7 +910,7 @@ static rk_status run_gs_stage(rk_state st, const StagePlan& p, double dt, double
     return launch_stage_timed(st, p, a);
 }
 
-static int pick_pair_zchunk(rk_state st);
+static int pick_pair_zchunk(rk_state st, int zc);
 
 // K8 DOPRI5 tail pair (rk_pair.cu PAIR_DP_TAIL): stages 6 and 7 of an error-controlled try
 // (Odeint ratio) in one launch on one GPU -- reads Y_6, W, E (written ahead by stage 5) and u,
@@ -937,7 +937,7 @@ static rk_status dp_tail_pair(rk_state st, const std::vector<StagePlan>& plan, d
     a.F = st->F;
     a.FK = st->F + st->K;
     a.inv_h2 = 1.0 / (st->h * st->h);
-    a.zchunk = pick_pair_zchunk(st);
+    a.zchunk = pick_pair_zchunk(st, 16);
     double* y6 = st->k[f.sp.base_src];
     CK_CTX(ctx, encode_pair_map(&a.tm_src, y6, st->geo, (int)st->local));
     a.src = y6;
@@ -1207,8 +1207,10 @@ static bool pair_path(rk_state st, int scheme) {
            pair_shape_ok(st->geo);
 }
 
-static int pick_pair_zchunk(rk_state st) {
-    int zc = 32;
+// z chunk of a K8 launch (measured at 512^3, tools/fused_time.py / ncu: the DOPRI5 tail pair
+// 16 planes (2.76 ms; 32: 3.03, 64: 3.72 -- longer chunks lose the y-neighbour rows from L2),
+// RK4 pairs 24 (3.15 ms per step; 16: 3.19, 32: 3.16), explicit midpoint 32 (1.14 ms))
+static int pick_pair_zchunk(rk_state st, int zc) {
     if (const char* e = getenv("RKB_PZ")) {  // developer tuning knob
         const int v = atoi(e);
         if (v > 0) zc = v;
@@ -1231,7 +1233,7 @@ static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
     a.F = st->F;
     a.FK = st->F + st->K;
     a.inv_h2 = 1.0 / (st->h * st->h);
-    a.zchunk = pick_pair_zchunk(st);
+    a.zchunk = pick_pair_zchunk(st, rk4 ? 24 : 32);
     const int64_t cells = st->local * st->nx * st->ny;
     for (int64_t i = 0; i < n; ++i) {
         cudaEvent_t e0 = nullptr, e1 = nullptr;
