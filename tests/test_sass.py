@@ -72,3 +72,22 @@ def test_persistent_small_grid_kernel(sass, s):
     assert len(hits) == 1
     assert not re.search(r"\b(STL|LDL)\b", hits[0])
     assert "DFMA" not in hits[0]
+
+
+# K8 stage pairs (rk_pair.cu): <U1, WIN, BA, YOUT, DP> instances of the RK4 pairs, the explicit
+# midpoint and the DOPRI5 tail pair -- TMA-fed, registers only (they sit at the 128-register cap
+# of two 256-thread CTAs per SM, where a spill is the first thing to regress), no FMA in the k-only
+# pairs (the DOPRI5 tail's IEEE division may use DFMA)
+K8 = [("0", "0", "1", "1", "0"), ("1", "1", "1", "0", "0"), ("0", "0", "0", "0", "0"), ("1", "1", "1", "0", "1")]
+
+
+@pytest.mark.parametrize("flags", K8, ids=lambda f: "".join(f))
+def test_k8_pair_kernels(sass, flags):
+    key = "gs_pair_kernelI" + "".join(f"Lb{b}E" for b in flags)
+    hits = [v for k, v in sass.items() if key in k]
+    assert len(hits) == 1, key
+    body = hits[0]
+    assert "UTMALDG.4D" in body
+    assert not re.search(r"\b(STL|LDL)\b", body), "local-memory traffic in a K8 pair kernel"
+    if flags[4] == "0":
+        assert "DFMA" not in body
