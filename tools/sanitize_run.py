@@ -17,8 +17,8 @@ ctx = rk.Context(0, 1, 0)
 # SAN_NO_NCCL=1: skip the NCCL loopback sections (compute-sanitizer racecheck and NCCL's own
 # kernels / proxy thread do not mix; every other section runs)
 NO_NCCL = os.environ.get("SAN_NO_NCCL") == "1"
-# SAN_SECTIONS: comma list of sections to run (default all): base, k3k6, r2, vector
-SECTIONS = set(os.environ.get("SAN_SECTIONS", "base,k3k6,r2,vector").split(","))
+# SAN_SECTIONS: comma list of sections to run (default all): base, k3k6, r2, k8, vector
+SECTIONS = set(os.environ.get("SAN_SECTIONS", "base,k3k6,r2,k8,vector").split(","))
 
 
 def mark(msg):
@@ -72,6 +72,22 @@ for p2p, dl, fk in R2 if "r2" in SECTIONS else ():
     st.integrate_adaptive("cash_karp54", 6.0, 8.0, 1.0, 1e-6, 1e-6)
     st.get()
     st.close()
+# K8 stage pairs (tile-aligned grid: RK4 pairs, the explicit midpoint pair, the DOPRI5 tail pair
+# inside error-controlled tries), several z chunks so chunk edges and the edge-CTA patch list run
+if "k8" in SECTIONS:
+    mark("k8")
+    os.environ["RKB_PZ"] = "5"
+    st = ctx.grid(64, 32, 11, 2)
+    st.set_rhs_gray_scott()
+    st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
+    st.set(rk_inputs.gray_scott_ic(64, 32, 11, seed=6))
+    for s in ("rk4", "midpoint", "rk4"):
+        st.do_step(s, 0.0, 1.0)
+    for k in range(3):
+        st.try_step("dopri5", float(k), 0.5, 1e-6, 1e-6)
+    st.get()
+    st.close()
+    os.environ.pop("RKB_PZ")
 mark("vector")
 v = ctx.vector(1001)
 v.set_rhs_logistic()
