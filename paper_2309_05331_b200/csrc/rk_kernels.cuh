@@ -240,6 +240,11 @@ struct PairArgs {
     CUtensorMap tm_src;    // Y_A as stored (u, or the written-ahead Y): 38 x 20 box (encode_pair_map)
     CUtensorMap tm_u;      // u: K3's 34 x 18 tile + ring box (PAIR_LAST); PAIR_DP_TAIL: W
     CUtensorMap tm_e, tm_uo, tm_k1;  // PAIR_DP_TAIL: E, u, k_1 interior boxes (L2 prefetch)
+    CUtensorMap tm_glo, tm_ghi;      // ghosts: the source's planes -2, -1 / nzl, nzl+1 (2-plane arrays)
+    CUtensorMap tm_ulo, tm_uhi;      // ghosts: the base's planes -1 / nzl (1-plane arrays)
+    const double* src_lo;            // ghosts: raw pointers of the source's ghost arrays (patches)
+    const double* src_hi;
+    int ghosts;                      // multi-GPU slab (or its one-GPU loopback): z does not wrap
     const double* src;     // raw pointer of the source (periodic cells beyond the padded ring)
     const double* w_in;    // PAIR_LAST: the partial sum W of the first pair; PAIR_DP_TAIL: E
     const double* u_in;    // PAIR_DP_TAIL: u and k_1 (the ratio's denominator, own cells)

@@ -64,14 +64,19 @@ constexpr int RING_WARPS = RKB_RING_WARPS;                // 3 (32 lanes; measur
 static_assert(NRING % RING_WARPS == 0 && NRING / RING_WARPS <= 32, "ring split");
 constexpr int NPATCH = 36 * BH;                           // source positions used (box cols 1..36)
 constexpr int SMEM_BUDGET = 113 * 1024;                   // 2 CTAs per SM
+constexpr int SMEM_BUDGET3 = 72 * 1024;                   // 3 CTAs per SM (u-fed pairs)
 
 // U1: u comes in its own 1-ring box (Y_A's source is a written-ahead Y).  The ring holds the
 // planes t-1, t, t+1 stage A reads and at least one plane in flight.
-template <bool U1>
+// The single-pair kind (u -> u_new: explicit midpoint) runs 3 CTAs per SM (<= 85 registers: Y_A
+// own values from the ring, 24 warps; 1.14 -> 1.12 ms); the others 2 (their register queues
+// at 80 registers spill: RK4 3.15 -> 3.28 ms).
+template <bool U1, bool YOUT>
 struct PLayout {
+    static constexpr int minb = (!U1 && !YOUT) ? 3 : 2;
     static constexpr int stage = HSLOT + (U1 ? USLOT : 0);
     static constexpr int fixed = 2 * YBSLOT;
-    static constexpr int Rb = (SMEM_BUDGET - fixed - 64) / stage;
+    static constexpr int Rb = ((minb == 3 ? SMEM_BUDGET3 : SMEM_BUDGET) - fixed - 64) / stage;
     static constexpr int R = Rb > 5 ? 5 : Rb;
     static_assert(R >= 4, "ring too shallow");
     static constexpr int off_u = HSLOT;
@@ -173,8 +178,8 @@ __device__ __forceinline__ void store_ring(double* p, const GridGeom& G, bool ex
 // the epilogue stores u_new and k_7, forms e = (E (+) (dt e_6) k_6) (+) (dt e_7) k_7 and the
 // Odeint ratio |e| / (atol (+) rtol (x) (|u| (+) dt (x) |k_1|)) with a block max.
 template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false>
-__global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__ PairArgs a) {
-    using LY = PLayout<U1>;
+__global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(const __grid_constant__ PairArgs a) {
+    using LY = PLayout<U1, YOUT>;
     constexpr int R = LY::R;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LY::bar);
@@ -224,16 +229,26 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
             "l"(reinterpret_cast<uint64_t>(m)), "r"(s32(b)), "r"(c0), "r"(c1), "r"(0), "r"(q)
             : "memory");
     };
+    // multi-GPU slab (a.ghosts): planes beyond the slab come from the ghost arrays the host
+    // filled before the launch (source: 2 planes each side, base: 1), not by wrapping
     auto issue = [&](int i) PINLINE {  // thread 0
         uint64_t* b = &bar[i % R];
+        const int p = zb - 2 + i;
         const int q = plane(i);
         const bool mid = i >= 1 && i < nr - 1;  // u feeds Y_B at stage-A planes zb-1 .. ze
         const uint32_t bytes = 2 * BOX * 8 + ((U1 && mid) ? 2 * UBOX * 8 : 0);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
         unsigned char* st = raw(i);
-        tma(st, &a.tm_src, b, x0 - 2, y0 - 1, q);
-        if constexpr (U1)
-            if (mid) tma(st + LY::off_u, &a.tm_u, b, x0, y0, q);
+        if (a.ghosts && p < 0) tma(st, &a.tm_glo, b, x0 - 2, y0 - 1, p + 2);
+        else if (a.ghosts && p >= G.nzl) tma(st, &a.tm_ghi, b, x0 - 2, y0 - 1, p - G.nzl);
+        else tma(st, &a.tm_src, b, x0 - 2, y0 - 1, q);
+        if constexpr (U1) {
+            if (mid) {
+                if (a.ghosts && p < 0) tma(st + LY::off_u, &a.tm_ulo, b, x0, y0, 0);
+                else if (a.ghosts && p >= G.nzl) tma(st + LY::off_u, &a.tm_uhi, b, x0, y0, 0);
+                else tma(st + LY::off_u, &a.tm_u, b, x0, y0, q);
+            }
+        }
     };
     auto wait = [&](int i) PINLINE {
         asm volatile(
@@ -273,7 +288,10 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
     double pv0 = 0.0, pv1 = 0.0;  // this thread's patch values of the next plane to land
     auto patch_load = [&](int i) PINLINE {
         if (my_pos >= 0 && i < nr) {
-            const double* p = a.src + (int64_t)plane(i) * G.ps + my_src;
+            const int pz = zb - 2 + i;
+            const double* p = a.ghosts && pz < 0 ? a.src_lo + (int64_t)(pz + 2) * G.ps + my_src
+                            : a.ghosts && pz >= G.nzl ? a.src_hi + (int64_t)(pz - G.nzl) * G.ps + my_src
+                                                      : a.src + (int64_t)plane(i) * G.ps + my_src;
             pv0 = p[0];
             pv1 = p[G.cs];
         }
@@ -303,7 +321,7 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
     // renaming, not by register moves.
     // own-cell Y_A: a register queue where registers allow (the u-fed pairs); the pair that also
     // streams u and W (at the 128-register cap) reads it from the ring instead
-    constexpr bool YREG = !U1;
+    constexpr bool YREG = LY::minb == 2 && !U1;
     double ya_q[YREG ? 3 : 1][2][2];
     double yb_q[3][2][2] = {}, ka_q[3][2][2] = {}, u_q[3][2][2] = {};
     double w_q[3][2][2] = {};  // WIN: W at t-1 (stage B's epilogue) and t (loaded one plane ahead)
@@ -514,7 +532,7 @@ __global__ void __launch_bounds__(PNT, 2) gs_pair_kernel(const __grid_constant__
 
 template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false>
 cudaError_t launch_pair_t(const PairArgs& a, cudaStream_t st) {
-    using LY = PLayout<U1>;
+    using LY = PLayout<U1, YOUT>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(gs_pair_kernel<U1, WIN, BA, YOUT, DP>,

@@ -253,6 +253,11 @@ struct rk_state_s {
     Maps tm_pg[2][2]{};                     // [parity][0 ghost_hi, 1 ghost_lo]
     unsigned long long* d_err = nullptr;
     unsigned long long* h_err = nullptr;
+    // K8 DOPRI5 tail pair on the multi-GPU / loopback slab: 2-deep ghost planes of Y_6, 1-deep of W
+    double* pg_y = nullptr;  // [-2, -1 | nzl, nzl+1]
+    double* pg_w = nullptr;  // [-1 | nzl]
+    CUtensorMap tm_pgy_lo{}, tm_pgy_hi{};
+    Maps tm_pgw_lo{}, tm_pgw_hi{};
     // rhs
     int rhs = RHS_NONE;
     double lambda = 0.0, d1 = 0.0, d2 = 0.0, F = 0.0, K = 0.0, h = 1.0;
@@ -915,14 +920,60 @@ static int pick_pair_zchunk(rk_state st, int zc);
 // K8 DOPRI5 tail pair (rk_pair.cu PAIR_DP_TAIL): stages 6 and 7 of an error-controlled try
 // (Odeint ratio) in one launch on one GPU -- reads Y_6, W, E (written ahead by stage 5) and u,
 // k_1; writes u_new, k_7 (into stage 7's buffer) and the ratio max: 7 arrays instead of 10.
+// On the multi-GPU slab (and its one-GPU loopback) the pair runs over NCCL ghost planes: Y_6's two
+// boundary planes and W's one are exchanged after stage 5, then one launch covers the slab.
 static bool dp_tail_pair_ok(rk_state st, const std::vector<StagePlan>& plan) {
-    if (st->fused != 3 || !st->grid || st->ncomp != 2 || st->rhs != RHS_GRAY_SCOTT || st->ctx->world != 1 ||
-        st->loopback || st->p2p || st->gl_dtp || !pair_shape_ok(st->geo) || plan.size() != 7)
+    if (st->fused != 3 || !st->grid || st->ncomp != 2 || st->rhs != RHS_GRAY_SCOTT || st->p2p || st->gl_dtp ||
+        !pair_shape_ok(st->geo) || plan.size() != 7)
         return false;
+    if (halo_path(st) && (!st->ctx->nccl || st->local < 2)) return false;
     const StagePlan& f = plan[5];
     const StagePlan& t = plan[6];
     return f.scheme == RK_DOPRI5 && f.adaptive == 1 && f.sp.epi == EPI_FINAL_EPART && f.sp.base_src >= 0 &&
            f.sp.wslot == 0 && f.sp.eslot == 1 && t.sp.epi == EPI_TAIL_ERR && t.sp.den_k1 >= 0;
+}
+
+// Ghost planes of the tail pair: one NCCL group on the compute stream -- to the upper neighbour
+// the top planes (its -2, -1 / -1), to the lower one the bottom planes (its nzl, nzl+1 / nzl).
+// Sends to up precede sends to down and receives from down precede receives from up, so with
+// world 2 (both neighbours the same peer) and world 1 (self) the messages still pair correctly.
+static rk_status pair_ghost_exchange(rk_state st, const double* y6, const double* w) {
+    NvtxRange nv("rk halo exchange (K8 tail pair)");
+    rk_ctx ctx = st->ctx;
+    const int64_t pv = plane_values(st), nzl = st->local;
+    if (!st->pg_y) {
+        TRY(dev_alloc(ctx, &st->pg_y, 4 * pv));
+        TRY(dev_alloc(ctx, &st->pg_w, 2 * pv));
+        CK_CTX(ctx, encode_pair_map(&st->tm_pgy_lo, st->pg_y, st->geo, 2));
+        CK_CTX(ctx, encode_pair_map(&st->tm_pgy_hi, st->pg_y + 2 * pv, st->geo, 2));
+        CK_CTX(ctx, encode_grid_maps(st->tm_pgw_lo.m, st->pg_w, st->geo, 1));
+        CK_CTX(ctx, encode_grid_maps(st->tm_pgw_hi.m, st->pg_w + pv, st->geo, 1));
+    }
+    const int up = (ctx->rank + 1) % ctx->world, down = (ctx->rank - 1 + ctx->world) % ctx->world;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (st->timing) {
+        e0 = pool_event(st);
+        e1 = pool_event(st);
+        CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+    }
+    NK_CTX(ctx, ncclGroupStart());
+    NK_CTX(ctx, ncclSend(y6 + (nzl - 2) * pv, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclSend(y6, (size_t)(2 * pv), ncclDouble, down, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclSend(w + (nzl - 1) * pv, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclSend(w, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclRecv(st->pg_y, (size_t)(2 * pv), ncclDouble, down, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclRecv(st->pg_y + 2 * pv, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclRecv(st->pg_w, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclRecv(st->pg_w + pv, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclGroupEnd());
+    mark_progress(ctx, ctx->stream);
+    if (st->timing) {
+        CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+        st->pending.push_back({e0, e1, 1});
+    }
+    st->stats.halo_exchanges += 1;
+    st->stats.halo_bytes += (int64_t)sizeof(double) * 6 * pv;
+    return RK_OK;
 }
 
 static rk_status dp_tail_pair(rk_state st, const std::vector<StagePlan>& plan, double dt, double atol, double rtol) {
@@ -931,6 +982,16 @@ static rk_status dp_tail_pair(rk_state st, const std::vector<StagePlan>& plan, d
     const StagePlan& f = plan[5];
     const StagePlan& t = plan[6];
     PairArgs a{};
+    if (halo_path(st)) {
+        TRY(pair_ghost_exchange(st, st->k[f.sp.base_src], st->k[f.sp.src[0]]));
+        a.ghosts = 1;
+        a.tm_glo = st->tm_pgy_lo;
+        a.tm_ghi = st->tm_pgy_hi;
+        a.tm_ulo = st->tm_pgw_lo.m[2];
+        a.tm_uhi = st->tm_pgw_hi.m[2];
+        a.src_lo = st->pg_y;
+        a.src_hi = st->pg_y + 2 * plane_values(st);
+    }
     a.geo = st->geo;
     a.d1 = st->d1;
     a.d2 = st->d2;
@@ -2382,6 +2443,8 @@ rk_status rk_state_destroy(rk_state st) {
     cudaFree(st->pflags);
     cudaFree(st->d_err);
     cudaFreeHost(st->h_err);
+    dev_free(cx, st->pg_y);
+    dev_free(cx, st->pg_w);
     cudaFree(st->d_loop);
     if (st->ev_pack) cudaEventDestroy(st->ev_pack);
     if (st->ev_halo) cudaEventDestroy(st->ev_halo);

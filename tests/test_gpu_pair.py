@@ -211,3 +211,29 @@ def test_dp_tail_pair_equals_stage_kernels(ctx):
         st.close()
     assert res[0][0] == res[1][0]
     assert bitwise(res[0][1], res[1][1])
+
+
+@pytest.mark.parametrize("dims", [(64, 32, 2), (64, 32, 3), (96, 48, 20)], ids=lambda d: "x".join(map(str, d)))
+def test_dp_tail_pair_halo_path(ctx, dims):
+    """The tail pair on the multi-GPU slab path, one GPU (RK_OPT_HALO_LOOPBACK: the 2-deep ghost
+    planes of Y_6 and 1-deep of W travel through a 1-rank NCCL communicator): tries and an
+    adaptive run bitwise equal to the oracle, down to 2-plane slabs."""
+    import paper_2309_05331_b200 as rk
+    u0 = perturbed_ic(*dims, seed=9)
+    want, E_o = dp_oracle_try(dims, u0, 2.0)
+    st = pair_state(ctx, dims, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+    before = st.stats()
+    acc, E, _ = st.try_step("dopri5", 0.0, 2.0, 1e-6, 1e-6)
+    after = st.stats()
+    assert E == E_o
+    assert bitwise(st.get(), want if acc else u0)
+    assert after["halo_exchanges"] - before["halo_exchanges"] == 6  # k1 + stages 2-5 (K3) + the pair
+    st.set(u0)
+    p = oracle.gray_scott_problem(*dims)
+    want2, a_o, r_o, rc = oracle.integrate_adaptive(p, OS["dopri5"], u0, 0.0, 12.0, 1.0, 1e-6, 1e-6)
+    a, r = st.integrate_adaptive("dopri5", 0.0, 12.0, 1.0, 1e-6, 1e-6)
+    got = st.get()
+    st.close()
+    assert (a, r) == (a_o, r_o)
+    assert bitwise(got, want2), first_mismatch(got, want2)
