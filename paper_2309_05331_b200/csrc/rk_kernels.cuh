@@ -255,6 +255,7 @@ struct PairArgs {
     GridGeom geo;          // nzl = nz: one GPU, z wraps by index
     double gB, gN, betaA, betaB;  // PAIR_DP_TAIL: gB = dt b_6, betaA / betaB = dt e_6 / dt e_7
     double dt, atol, rtol;
+    const double* dtp;     // non-null (device-resident try loop): this try's dt; the coefficients are raw
     double d1, d2, F, FK, inv_h2;
     int zchunk;
 };

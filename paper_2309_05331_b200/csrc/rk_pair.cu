@@ -193,6 +193,11 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
     if (zb >= ze) return;
     const int nout = ze - zb;
     const int nr = nout + 4;  // raw planes zb-2 .. ze+1; index i <-> plane zb-2+i
+    // Coefficients: dt-scaled by the host, or (device-resident try loop, a.dtp) raw and scaled
+    // here by this try's dt -- fl(dt * c) either way, the same single rounding (K3's rule)
+    const double dsc = a.dtp ? *a.dtp : 1.0;
+    const double cgB = mul(dsc, a.gB), cgN = mul(dsc, a.gN), cbA = mul(dsc, a.betaA), cbB = mul(dsc, a.betaB);
+    const double cdt = a.dtp ? dsc : a.dt;
     auto plane = [&](int i) PINLINE -> int { return pmod(zb - 2 + i, G.nzl); };
     const bool edge = x0 == 0 || x0 + PX == G.nx || y0 == 0 || y0 + PTH == G.ny;  // CTA-uniform
 
@@ -439,7 +444,7 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int c = 0; c < 2; ++c) ybp[r][c] = add(U1 ? uc[r][c] : yac[r][c], mul(a.gB, kac[r][c]));
+            for (int c = 0; c < 2; ++c) ybp[r][c] = add(U1 ? uc[r][c] : yac[r][c], mul(cgB, kac[r][c]));
         if (ring_plane) {
             double* yb = ybs(ic);
 #pragma unroll
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const double ur = U1 ? reinterpret_cast<const double*>(st + LY::off_u)[c * UBOX + ru] : ya[c * BOX + rb];
-                    yb[c * YBOX + ru] = add(ur, mul(a.gB, kr[c]));
+                    yb[c * YBOX + ru] = add(ur, mul(cgB, kr[c]));
                 }
             }
         }
@@ -483,8 +488,8 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
                             pk[0] = kb[r][c];
                         }
                         // e' = E (+) (dt e_6) k_6 (stage 6's epilogue), e = e' (+) (dt e_7) k_7
-                        const double e = add(add(eo[r][c], mul(a.betaA, kap[r][c])), mul(a.betaB, kb[r][c]));
-                        const double dd = add(a.atol, mul(a.rtol, add(fabs(uo[r][c]), mul(a.dt, fabs(k1o[r][c])))));
+                        const double e = add(add(eo[r][c], mul(cbA, kap[r][c])), mul(cbB, kb[r][c]));
+                        const double dd = add(a.atol, mul(a.rtol, add(fabs(uo[r][c]), mul(cdt, fabs(k1o[r][c])))));
                         // r = |e| / dd exactly; the division is skipped when e == 0 or when
                         // |e| <= rmax*dd*(1-2^-52) proves r <= rmax (K3's filter; NaN never skips)
                         const double ae = fabs(e);
@@ -501,12 +506,12 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
                     }
                     // Wb: W of the previous pair, else u (= Y_A for a pair fed by u)
                     double wv = WIN ? wbp[r][c] : (U1 ? up[r][c] : yam[r][c]);
-                    if constexpr (BA) wv = add(wv, mul(a.betaA, kap[r][c]));
-                    wv = add(wv, mul(a.betaB, kb[r][c]));
+                    if constexpr (BA) wv = add(wv, mul(cbA, kap[r][c]));
+                    wv = add(wv, mul(cbB, kb[r][c]));
                     double* p = a.out + ro + c * G.cs;
                     if constexpr (YOUT) {
                         p[0] = wv;  // W: read at own cells only, no ring copies
-                        const double yn = add(U1 ? up[r][c] : yam[r][c], mul(a.gN, kb[r][c]));
+                        const double yn = add(U1 ? up[r][c] : yam[r][c], mul(cgN, kb[r][c]));
                         double* py = a.out_y + ro + c * G.cs;
                         if (ering) store_ring(py, G, rx0, rx1, ry0, ry1, yn);
                         else py[0] = yn;

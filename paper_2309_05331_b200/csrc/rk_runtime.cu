@@ -923,7 +923,7 @@ static int pick_pair_zchunk(rk_state st, int zc);
 // On the multi-GPU slab (and its one-GPU loopback) the pair runs over NCCL ghost planes: Y_6's two
 // boundary planes and W's one are exchanged after stage 5, then one launch covers the slab.
 static bool dp_tail_pair_ok(rk_state st, const std::vector<StagePlan>& plan) {
-    if (st->fused != 3 || !st->grid || st->ncomp != 2 || st->rhs != RHS_GRAY_SCOTT || st->p2p || st->gl_dtp ||
+    if (st->fused != 3 || !st->grid || st->ncomp != 2 || st->rhs != RHS_GRAY_SCOTT || st->p2p ||
         !pair_shape_ok(st->geo) || plan.size() != 7)
         return false;
     if (halo_path(st) && (!st->ctx->nccl || st->local < 2)) return false;
@@ -1018,6 +1018,7 @@ static rk_status dp_tail_pair(rk_state st, const std::vector<StagePlan>& plan, d
     a.dt = dt;
     a.atol = atol;
     a.rtol = rtol;
+    a.dtp = st->gl_dtp;  // device-resident try loop (captured): raw plan coefficients, dt on the device
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (st->timing) {
         e0 = pool_event(st);
@@ -2017,6 +2018,9 @@ static rk_status gloop_build(rk_state st, int scheme, double atol, double rtol) 
     }
     for (int j = 0; j < st->nk; ++j) g->k[j] = st->k[j];
     for (const StagePlan& p : plan) (p.stage == 0 ? g->k1_bytes : g->try_bytes) += plan_stage_bytes(st, p);
+    if (dp_tail_pair_ok(st, plan))  // stages 6 + 7 as the K8 tail pair: 7 arrays instead of their 10
+        g->try_bytes += 7 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double) -
+                        plan_stage_bytes(st, plan[5]) - plan_stage_bytes(st, plan[6]);
     CK_CTX(ctx, cudaMalloc((void**)&g->dev, sizeof(GLoopDev)));
     if (!ctx->capture) CK_CTX(ctx, cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking));
     TRY(ensure_halo(st));                    // ghost buffers / events exist before the capture
