@@ -177,7 +177,7 @@ __device__ __forceinline__ void store_ring(double* p, const GridGeom& G, bool ex
 // Y_6 (written ahead), Y_B = W (+) (dt b_6) k_6 = u_new (a_7j = b_j, FSAL), k_B = k_7 = F(u_new);
 // the epilogue stores u_new and k_7, forms e = (E (+) (dt e_6) k_6) (+) (dt e_7) k_7 and the
 // Odeint ratio |e| / (atol (+) rtol (x) (|u| (+) dt (x) |k_1|)) with a block max.
-template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false>
+template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false, bool DTP = false>
 __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(const __grid_constant__ PairArgs a) {
     using LY = PLayout<U1, YOUT>;
     constexpr int R = LY::R;
@@ -195,9 +195,11 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
     const int nr = nout + 4;  // raw planes zb-2 .. ze+1; index i <-> plane zb-2+i
     // Coefficients: dt-scaled by the host, or (device-resident try loop, a.dtp) raw and scaled
     // here by this try's dt -- fl(dt * c) either way, the same single rounding (K3's rule)
-    const double dsc = a.dtp ? *a.dtp : 1.0;
-    const double cgB = mul(dsc, a.gB), cgN = mul(dsc, a.gN), cbA = mul(dsc, a.betaA), cbB = mul(dsc, a.betaB);
-    const double cdt = a.dtp ? dsc : a.dt;
+    // (a template flag: the host-scaled path keeps them as constant-bank operands, no registers)
+    const double dsc = DTP ? *a.dtp : 1.0;
+    const double cgB = DTP ? mul(dsc, a.gB) : a.gB, cgN = DTP ? mul(dsc, a.gN) : a.gN;
+    const double cbA = DTP ? mul(dsc, a.betaA) : a.betaA, cbB = DTP ? mul(dsc, a.betaB) : a.betaB;
+    const double cdt = DTP ? dsc : a.dt;
     auto plane = [&](int i) PINLINE -> int { return pmod(zb - 2 + i, G.nzl); };
     const bool edge = x0 == 0 || x0 + PX == G.nx || y0 == 0 || y0 + PTH == G.ny;  // CTA-uniform
 
@@ -535,19 +537,19 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
     if constexpr (DP) block_max_to_global(rbits, a.errmax);
 }
 
-template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false>
+template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false, bool DTP = false>
 cudaError_t launch_pair_t(const PairArgs& a, cudaStream_t st) {
     using LY = PLayout<U1, YOUT>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gs_pair_kernel<U1, WIN, BA, YOUT, DP>,
+        cudaError_t e = cudaFuncSetAttribute(gs_pair_kernel<U1, WIN, BA, YOUT, DP, DTP>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, LY::smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     const int tiles = (a.geo.nx / PX) * (a.geo.ny / PTH);
     const int nch = (a.geo.nzl + a.zchunk - 1) / a.zchunk;
-    gs_pair_kernel<U1, WIN, BA, YOUT, DP><<<dim3((unsigned)tiles, (unsigned)nch), PNT, LY::smem, st>>>(a);
+    gs_pair_kernel<U1, WIN, BA, YOUT, DP, DTP><<<dim3((unsigned)tiles, (unsigned)nch), PNT, LY::smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -580,7 +582,9 @@ cudaError_t launch_gs_pair(int kind, const PairArgs& a, cudaStream_t st) {
     case PAIR_FIRST: return launch_pair_t<false, false, true, true>(a, st);  // RK4 1-2: u -> Y3, W
     case PAIR_LAST: return launch_pair_t<true, true, true, false>(a, st);    // RK4 3-4: Y3, u, W -> u_new
     case PAIR_ONLY: return launch_pair_t<false, false, false, false>(a, st); // midpoint: u -> u_new
-    case PAIR_DP_TAIL: return launch_pair_t<true, true, true, false, true>(a, st);  // DOPRI5 6-7
+    case PAIR_DP_TAIL:  // DOPRI5 stages 6-7 (dt on the device inside the graph try loop)
+        return a.dtp ? launch_pair_t<true, true, true, false, true, true>(a, st)
+                     : launch_pair_t<true, true, true, false, true, false>(a, st);
     default: return cudaErrorInvalidValue;
     }
 }
