@@ -258,6 +258,10 @@ struct rk_state_s {
     double* pg_w = nullptr;  // [-1 | nzl]
     CUtensorMap tm_pgy_lo{}, tm_pgy_hi{};
     Maps tm_pgw_lo{}, tm_pgw_hi{};
+    // K8 RK4 pairs on the slab: u's ghosts (pg_y, also viewed 1-deep for pair (3,4)'s base) and Y_3's
+    double* pg_y2 = nullptr;
+    CUtensorMap tm_pgy2_lo{}, tm_pgy2_hi{};
+    Maps tm_pgu_lo{}, tm_pgu_hi{};
     // rhs
     int rhs = RHS_NONE;
     double lambda = 0.0, d1 = 0.0, d2 = 0.0, F = 0.0, K = 0.0, h = 1.0;
@@ -933,22 +937,35 @@ static bool dp_tail_pair_ok(rk_state st, const std::vector<StagePlan>& plan) {
            f.sp.wslot == 0 && f.sp.eslot == 1 && t.sp.epi == EPI_TAIL_ERR && t.sp.den_k1 >= 0;
 }
 
-// Ghost planes of the tail pair: one NCCL group on the compute stream -- to the upper neighbour
-// the top planes (its -2, -1 / -1), to the lower one the bottom planes (its nzl, nzl+1 / nzl).
+// Ghost planes of a K8 launch on the multi-GPU slab (and its one-GPU loopback): one NCCL group on
+// the compute stream -- src's two boundary planes each side into g2 ([-2, -1 | nzl, nzl+1]) and,
+// if given, base's one plane each side into pg_w ([-1 | nzl]).  To the upper neighbour go the
+// top planes (its -2, -1 / -1), to the lower one the bottom planes (its nzl, nzl+1 / nzl).
 // Sends to up precede sends to down and receives from down precede receives from up, so with
 // world 2 (both neighbours the same peer) and world 1 (self) the messages still pair correctly.
-static rk_status pair_ghost_exchange(rk_state st, const double* y6, const double* w) {
-    NvtxRange nv("rk halo exchange (K8 tail pair)");
+static rk_status pair_ghost_buffers(rk_state st) {
+    if (st->pg_y) return RK_OK;
+    rk_ctx ctx = st->ctx;
+    const int64_t pv = plane_values(st);
+    TRY(dev_alloc(ctx, &st->pg_y, 4 * pv));
+    TRY(dev_alloc(ctx, &st->pg_y2, 4 * pv));
+    TRY(dev_alloc(ctx, &st->pg_w, 2 * pv));
+    CK_CTX(ctx, encode_pair_map(&st->tm_pgy_lo, st->pg_y, st->geo, 2));
+    CK_CTX(ctx, encode_pair_map(&st->tm_pgy_hi, st->pg_y + 2 * pv, st->geo, 2));
+    CK_CTX(ctx, encode_pair_map(&st->tm_pgy2_lo, st->pg_y2, st->geo, 2));
+    CK_CTX(ctx, encode_pair_map(&st->tm_pgy2_hi, st->pg_y2 + 2 * pv, st->geo, 2));
+    CK_CTX(ctx, encode_grid_maps(st->tm_pgw_lo.m, st->pg_w, st->geo, 1));
+    CK_CTX(ctx, encode_grid_maps(st->tm_pgw_hi.m, st->pg_w + pv, st->geo, 1));
+    CK_CTX(ctx, encode_grid_maps(st->tm_pgu_lo.m, st->pg_y + pv, st->geo, 1));      // plane -1
+    CK_CTX(ctx, encode_grid_maps(st->tm_pgu_hi.m, st->pg_y + 2 * pv, st->geo, 1));  // plane nzl
+    return RK_OK;
+}
+
+static rk_status pair_ghost_exchange(rk_state st, const double* src, double* g2, const double* base) {
+    NvtxRange nv("rk halo exchange (K8 pair)");
     rk_ctx ctx = st->ctx;
     const int64_t pv = plane_values(st), nzl = st->local;
-    if (!st->pg_y) {
-        TRY(dev_alloc(ctx, &st->pg_y, 4 * pv));
-        TRY(dev_alloc(ctx, &st->pg_w, 2 * pv));
-        CK_CTX(ctx, encode_pair_map(&st->tm_pgy_lo, st->pg_y, st->geo, 2));
-        CK_CTX(ctx, encode_pair_map(&st->tm_pgy_hi, st->pg_y + 2 * pv, st->geo, 2));
-        CK_CTX(ctx, encode_grid_maps(st->tm_pgw_lo.m, st->pg_w, st->geo, 1));
-        CK_CTX(ctx, encode_grid_maps(st->tm_pgw_hi.m, st->pg_w + pv, st->geo, 1));
-    }
+    TRY(pair_ghost_buffers(st));
     const int up = (ctx->rank + 1) % ctx->world, down = (ctx->rank - 1 + ctx->world) % ctx->world;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (st->timing) {
@@ -957,14 +974,18 @@ static rk_status pair_ghost_exchange(rk_state st, const double* y6, const double
         CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
     }
     NK_CTX(ctx, ncclGroupStart());
-    NK_CTX(ctx, ncclSend(y6 + (nzl - 2) * pv, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->stream));
-    NK_CTX(ctx, ncclSend(y6, (size_t)(2 * pv), ncclDouble, down, ctx->nccl, ctx->stream));
-    NK_CTX(ctx, ncclSend(w + (nzl - 1) * pv, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->stream));
-    NK_CTX(ctx, ncclSend(w, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->stream));
-    NK_CTX(ctx, ncclRecv(st->pg_y, (size_t)(2 * pv), ncclDouble, down, ctx->nccl, ctx->stream));
-    NK_CTX(ctx, ncclRecv(st->pg_y + 2 * pv, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->stream));
-    NK_CTX(ctx, ncclRecv(st->pg_w, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->stream));
-    NK_CTX(ctx, ncclRecv(st->pg_w + pv, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclSend(src + (nzl - 2) * pv, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclSend(src, (size_t)(2 * pv), ncclDouble, down, ctx->nccl, ctx->stream));
+    if (base) {
+        NK_CTX(ctx, ncclSend(base + (nzl - 1) * pv, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->stream));
+        NK_CTX(ctx, ncclSend(base, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->stream));
+    }
+    NK_CTX(ctx, ncclRecv(g2, (size_t)(2 * pv), ncclDouble, down, ctx->nccl, ctx->stream));
+    NK_CTX(ctx, ncclRecv(g2 + 2 * pv, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->stream));
+    if (base) {
+        NK_CTX(ctx, ncclRecv(st->pg_w, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->stream));
+        NK_CTX(ctx, ncclRecv(st->pg_w + pv, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->stream));
+    }
     NK_CTX(ctx, ncclGroupEnd());
     mark_progress(ctx, ctx->stream);
     if (st->timing) {
@@ -972,7 +993,7 @@ static rk_status pair_ghost_exchange(rk_state st, const double* y6, const double
         st->pending.push_back({e0, e1, 1});
     }
     st->stats.halo_exchanges += 1;
-    st->stats.halo_bytes += (int64_t)sizeof(double) * 6 * pv;
+    st->stats.halo_bytes += (int64_t)sizeof(double) * (base ? 6 : 4) * pv;
     return RK_OK;
 }
 
@@ -983,7 +1004,8 @@ static rk_status dp_tail_pair(rk_state st, const std::vector<StagePlan>& plan, d
     const StagePlan& t = plan[6];
     PairArgs a{};
     if (halo_path(st)) {
-        TRY(pair_ghost_exchange(st, st->k[f.sp.base_src], st->k[f.sp.src[0]]));
+        TRY(pair_ghost_buffers(st));
+        TRY(pair_ghost_exchange(st, st->k[f.sp.base_src], st->pg_y, st->k[f.sp.src[0]]));
         a.ghosts = 1;
         a.tm_glo = st->tm_pgy_lo;
         a.tm_ghi = st->tm_pgy_hi;
@@ -1264,9 +1286,11 @@ static int pick_fused_zchunk(rk_state st) {
 // K8 (rk_pair.cu): RK4 as two stage-pair launches (u -> k2, W; u, k2, W -> u_new), the
 // explicit midpoint rule as one (u -> u_new); RK_OPT_FUSED_STEP = 3
 static bool pair_path(rk_state st, int scheme) {
-    return st->fused == 3 && st->grid && st->ncomp == 2 && st->rhs == RHS_GRAY_SCOTT && st->ctx->world == 1 &&
-           !st->loopback && !st->p2p && (scheme == RK_RK4 || scheme == RK_EXPLICIT_MIDPOINT) &&
-           pair_shape_ok(st->geo);
+    if (!(st->fused == 3 && st->grid && st->ncomp == 2 && st->rhs == RHS_GRAY_SCOTT && !st->p2p &&
+          (scheme == RK_RK4 || scheme == RK_EXPLICIT_MIDPOINT) && pair_shape_ok(st->geo)))
+        return false;
+    // the multi-GPU slab (or its loopback): NCCL ghost planes before each launch (2 deep)
+    return !halo_path(st) || (st->ctx->nccl && st->local >= 2);
 }
 
 // z chunk of a K8 launch (measured at 512^3, tools/fused_time.py / ncu: the DOPRI5 tail pair
@@ -1297,12 +1321,31 @@ static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
     a.inv_h2 = 1.0 / (st->h * st->h);
     a.zchunk = pick_pair_zchunk(st, rk4 ? 24 : 32);
     const int64_t cells = st->local * st->nx * st->ny;
-    for (int64_t i = 0; i < n; ++i) {
+    const bool slab = halo_path(st);  // multi-GPU slab / loopback: ghost planes, no z wrap
+    a.ghosts = slab ? 1 : 0;
+    auto launch = [&](int kind) -> rk_status {  // one pair launch, timed like a stage launch
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (st->timing) {
             e0 = pool_event(st);
             e1 = pool_event(st);
             CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+        }
+        CK_CTX(ctx, launch_gs_pair(kind, a, ctx->stream));
+        if (st->timing) {
+            CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+            st->pending.push_back({e0, e1, 0});
+            if (st->pending.size() > 4096) TRY(resolve_timing(st));
+        }
+        return RK_OK;
+    };
+    for (int64_t i = 0; i < n; ++i) {
+        if (slab) {  // u's two boundary planes each side (also pair (3,4)'s 1-deep base ghosts)
+            TRY(pair_ghost_buffers(st));
+            TRY(pair_ghost_exchange(st, st->u, st->pg_y, nullptr));
+            a.tm_glo = st->tm_pgy_lo;
+            a.tm_ghi = st->tm_pgy_hi;
+            a.src_lo = st->pg_y;
+            a.src_hi = st->pg_y + 2 * plane_values(st);
         }
         CK_CTX(ctx, encode_pair_map(&a.tm_src, st->u, st->geo, (int)st->local));
         a.src = st->u;
@@ -1313,7 +1356,16 @@ static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
             a.gN = dt * C.a[2][1];
             a.out = st->k[1];
             a.out_y = st->k[0];
-            CK_CTX(ctx, launch_gs_pair(PAIR_FIRST, a, ctx->stream));
+            TRY(launch(PAIR_FIRST));
+            if (slab) {  // Y3's ghosts; u's 1-deep ghosts are the inner planes of the first exchange
+                TRY(pair_ghost_exchange(st, st->k[0], st->pg_y2, nullptr));
+                a.tm_glo = st->tm_pgy2_lo;
+                a.tm_ghi = st->tm_pgy2_hi;
+                a.src_lo = st->pg_y2;
+                a.src_hi = st->pg_y2 + 2 * plane_values(st);
+                a.tm_ulo = st->tm_pgu_lo.m[2];
+                a.tm_uhi = st->tm_pgu_hi.m[2];
+            }
             CK_CTX(ctx, encode_pair_map(&a.tm_src, st->k[0], st->geo, (int)st->local));
             a.tm_u = st->tm_u.m[2];
             a.src = st->k[0];
@@ -1323,15 +1375,10 @@ static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
             a.betaB = dt * C.b[3];
             a.out = st->u_new;
             a.out_y = nullptr;
-            CK_CTX(ctx, launch_gs_pair(PAIR_LAST, a, ctx->stream));
+            TRY(launch(PAIR_LAST));
         } else {  // explicit midpoint: u -> u_new (b_1 = 0)
             a.out = st->u_new;
-            CK_CTX(ctx, launch_gs_pair(PAIR_ONLY, a, ctx->stream));
-        }
-        if (st->timing) {
-            CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
-            st->pending.push_back({e0, e1, 0});
-            if (st->pending.size() > 4096) TRY(resolve_timing(st));
+            TRY(launch(PAIR_ONLY));
         }
         swap_u(st);
         const int nl = rk4 ? 2 : 1;
@@ -1497,6 +1544,7 @@ static rk_status rk_fixed_step(rk_state st, int scheme, double dt) {
         return RK_OK;
     }
     if (coop_path(st, scheme)) return coop_steps(st, scheme, dt, 1);
+    if (st->grid && halo_path(st)) TRY(ensure_halo(st));  // the loopback's 1-rank communicator
     if (pair_path(st, scheme)) return pair_steps(st, scheme, dt, 1);
     if (fused_path(st, scheme)) return fused_steps(st, scheme, dt, 1);
     if (st->grid) {
@@ -2449,6 +2497,7 @@ rk_status rk_state_destroy(rk_state st) {
     cudaFreeHost(st->h_err);
     dev_free(cx, st->pg_y);
     dev_free(cx, st->pg_w);
+    dev_free(cx, st->pg_y2);
     cudaFree(st->d_loop);
     if (st->ev_pack) cudaEventDestroy(st->ev_pack);
     if (st->ev_halo) cudaEventDestroy(st->ev_halo);

@@ -237,3 +237,26 @@ def test_dp_tail_pair_halo_path(ctx, dims):
     st.close()
     assert (a, r) == (a_o, r_o)
     assert bitwise(got, want2), first_mismatch(got, want2)
+
+
+@pytest.mark.parametrize("scheme", PAIR)
+@pytest.mark.parametrize("dims", [(64, 32, 2), (64, 32, 5), (96, 48, 37)], ids=lambda d: "x".join(map(str, d)))
+def test_pair_steps_halo_path(ctx, scheme, dims):
+    """RK4 / midpoint pairs on the multi-GPU slab path, one GPU (loopback): u's and Y_3's 2-deep
+    ghost planes through a 1-rank NCCL communicator, bitwise equal to the oracle."""
+    import paper_2309_05331_b200 as rk
+    u0 = perturbed_ic(*dims, seed=4)
+    st = pair_state(ctx, dims, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+    p = oracle.gray_scott_problem(*dims)
+    u = u0
+    before = st.stats()
+    for k in range(3):
+        st.do_step(scheme, float(k), 1.0)
+        u = oracle.step(p, OS[scheme], float(k), 1.0, u)
+        got = st.get()
+        assert bitwise(got, u), (scheme, dims, k, first_mismatch(got, u))
+    after = st.stats()
+    st.close()
+    assert after["stage_launches"] - before["stage_launches"] == 3 * (2 if scheme == "rk4" else 1)
+    assert after["halo_exchanges"] - before["halo_exchanges"] == 3 * (2 if scheme == "rk4" else 1)
