@@ -149,14 +149,18 @@ typedef enum {
                                 wide barrier between stages): same results bit for
                                 bit, no per-stage launch cost.  Default 2^18 (64^3); 0 = off. */
     RK_OPT_FUSED_STEP = 11,    /* temporal blocking of fixed RK4 / explicit- / modified-midpoint steps
-                                of a Gray–Scott grid (one GPU, no halo path, above
-                                RK_OPT_COOP_MAX_CELLS), same results bit for bit:
+                                of a Gray–Scott grid (above RK_OPT_COOP_MAX_CELLS), same
+                                results bit for bit:
                                 3 (default): K8 stage pairs -- two chained stages per launch,
                                 the first on the tile grown by one cell and never stored (RK4:
                                 two launches, 112 B/cell instead of 208; explicit midpoint: one,
                                 32 B instead of 80); needs nx % 32 == 0 and
                                 ny % 16 == 0, other grids and the modified midpoint run the
-                                stage-by-stage kernels.  1: K6, the whole step in ONE launch
+                                stage-by-stage kernels; on the NCCL multi-GPU slab the pairs'
+                                2-deep ghost planes are exchanged before each pair (the P2P
+                                transport keeps the stage-by-stage kernels); with 3 the last
+                                two stages of every error-controlled DOPRI5 try are one K8
+                                launch too.  1 (one GPU, no halo path): K6, the whole step in ONE launch
                                 with every stage value on chip (32 B/cell).  2: K7, K6 with
                                 warp-specialised stage groups.  K6 and K7 are ablations, slower
                                 than K8 and K3 on the B200.  0: stage-by-stage launches (K3). */

@@ -30,8 +30,9 @@
 // Arithmetic is K3's expression for expression (R-17): difference-form Laplacian
 // (x, then y, then z; lower neighbour first), the same reaction trees, stage values and partial
 // sums left to right, no FMA -- bitwise equal to the oracle and to the stage-by-stage kernels for
-// any tile / chunk decomposition.  One GPU (z wraps by index), nx % 32 == 0, ny % 16 == 0 (else
-// the library runs the stage-by-stage kernels).
+// any tile / chunk decomposition.  nx % 32 == 0, ny % 16 == 0 (else the library runs the
+// stage-by-stage kernels).  One GPU: z wraps by index; on the multi-GPU slab (a.ghosts) the
+// planes beyond the slab come from ghost arrays exchanged by the host before the launch.
 #include <cudaTypedefs.h>
 
 #include <type_traits>
