@@ -87,6 +87,19 @@ if "k8" in SECTIONS:
         st.try_step("dopri5", float(k), 0.5, 1e-6, 1e-6)
     st.get()
     st.close()
+    if not NO_NCCL:  # the pairs on the slab path: ghost planes through the 1-rank NCCL loopback
+        mark("k8 loopback")
+        st = ctx.grid(64, 32, 11, 2)
+        st.set_rhs_gray_scott()
+        st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
+        st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+        st.set(rk_inputs.gray_scott_ic(64, 32, 11, seed=7))
+        for s in ("rk4", "midpoint"):
+            st.do_step(s, 0.0, 1.0)
+        for k in range(2):
+            st.try_step("dopri5", float(k), 0.5, 1e-6, 1e-6)
+        st.get()
+        st.close()
     os.environ.pop("RKB_PZ")
 mark("vector")
 v = ctx.vector(1001)
