@@ -155,8 +155,8 @@ typedef enum {
                                 the first on the tile grown by one cell and never stored (RK4:
                                 two launches, 112 B/cell instead of 208; explicit midpoint: one,
                                 32 B instead of 80); needs nx % 32 == 0 and
-                                ny % 16 == 0, other grids and the modified midpoint run the
-                                stage-by-stage kernels; on the NCCL multi-GPU slab the pairs'
+                                ny % 16 == 0, other grids run the stage-by-stage kernels;
+                                Gragg's modified midpoint is pair (1, 2) + its last stage; on the NCCL multi-GPU slab the pairs'
                                 2-deep ghost planes are exchanged before each pair (the P2P
                                 transport keeps the stage-by-stage kernels); with 3 the last
                                 two stages of every error-controlled DOPRI5 try are one K8

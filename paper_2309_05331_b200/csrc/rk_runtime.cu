@@ -1287,7 +1287,8 @@ static int pick_fused_zchunk(rk_state st) {
 // explicit midpoint rule as one (u -> u_new); RK_OPT_FUSED_STEP = 3
 static bool pair_path(rk_state st, int scheme) {
     if (!(st->fused == 3 && st->grid && st->ncomp == 2 && st->rhs == RHS_GRAY_SCOTT && !st->p2p &&
-          (scheme == RK_RK4 || scheme == RK_EXPLICIT_MIDPOINT) && pair_shape_ok(st->geo)))
+          (scheme == RK_RK4 || scheme == RK_EXPLICIT_MIDPOINT || scheme == RK_MODIFIED_MIDPOINT) &&
+          pair_shape_ok(st->geo)))
         return false;
     // the multi-GPU slab (or its loopback): NCCL ghost planes before each launch (2 deep)
     return !halo_path(st) || (st->ctx->nccl && st->local >= 2);
@@ -1311,7 +1312,8 @@ static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
     rk_ctx ctx = st->ctx;
     const Coeffs C = coeffs_of(scheme);
     const bool rk4 = scheme == RK_RK4;
-    if (rk4) TRY(ensure_k(st, 2));  // k[0] <- Y3, k[1] <- W
+    const bool gragg = scheme == RK_MODIFIED_MIDPOINT;  // pair (1, 2) + the K3 last stage
+    if (rk4 || gragg) TRY(ensure_k(st, 2));  // k[0] <- Y3, k[1] <- W
     PairArgs a{};
     a.geo = st->geo;
     a.d1 = st->d1;
@@ -1376,6 +1378,19 @@ static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
             a.out = st->u_new;
             a.out_y = nullptr;
             TRY(launch(PAIR_LAST));
+        } else if (gragg) {  // (u -> Y3 = u + dt k2, W) then the K3 last stage (Y3, W -> u_new)
+            a.gN = dt * C.a[2][1];
+            a.out = st->k[1];
+            a.out_y = st->k[0];
+            TRY(launch(PAIR_FIRST));
+            StagePlan q;
+            q.scheme = scheme;
+            q.adaptive = 4;
+            q.stage = 2;
+            q.sp = stage_spec(scheme, 4, 2);
+            q.beta_new = dt * C.b[2];
+            TRY(run_gs_stage(st, q, dt, 0.0, 0.0));  // counts its own launch, RHS and bytes
+            st->stats.rhs_evals -= 1;
         } else {  // explicit midpoint: u -> u_new (b_1 = 0)
             a.out = st->u_new;
             TRY(launch(PAIR_ONLY));
@@ -1385,8 +1400,8 @@ static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
         st->stats.kernel_launches += nl;
         st->stats.stage_launches += nl;
         st->stats.rhs_evals += C.s;
-        // RK4: (u -> Y3, W) + (Y3, u, W -> u_new) = 7 arrays; midpoint: u -> u_new
-        st->stats.stage_bytes += (rk4 ? 7 : 2) * cells * 2 * (int64_t)sizeof(double);
+        // RK4: (u -> Y3, W) + (Y3, u, W -> u_new) = 7 arrays; midpoint: u -> u_new; Gragg's pair: 3
+        st->stats.stage_bytes += (rk4 ? 7 : gragg ? 3 : 2) * cells * 2 * (int64_t)sizeof(double);
         st->stats.steps += 1;
     }
     st->k1_valid = false;

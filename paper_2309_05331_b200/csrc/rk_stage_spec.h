@@ -173,6 +173,21 @@ __host__ __device__ constexpr StageSpec stage_spec(int S, int ad, int i) {
         return p;
     }
     const Tableau T = tableau_of(S);
+    if (ad == 4) {  // fixed step, the last stage fed by a K8 pair that wrote ahead Y_L (k buffer 0,
+                    // with its ring) and W = u + sum_{j<L} b_j k_j (k buffer 1): Y-direct, u_new = W + b_L k_L
+        const int L4 = last_stage(T, false);
+        if (T.s < 3 || i != L4) return p;
+        p.valid = 1;
+        p.epi = EPI_FINAL;
+        p.base_src = 0;
+        p.nslots = 1;
+        p.src[0] = 1;
+        p.j[0] = L4 - 1;
+        p.wslot = 0;
+        p.writes_u = true;
+        p.bnew = t_bnz(T, L4);
+        return p;
+    }
     if (T.s == 0 || (ad && T.err_order == 0)) return p;
     const int L = last_stage(T, ad);
     if (i < 0 || i > L) return p;

@@ -774,6 +774,10 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
     dim3 grid((unsigned)tiles, (unsigned)nchunks);
     if (a.zpair > 1 && a.zmode == 0) grid = dim3((unsigned)(a.zpair * tiles), (unsigned)((nchunks + a.zpair - 1) / a.zpair));
     if (nlaunch) ++*nlaunch;
+    if (adaptive == 4) {  // the last stage after a K8 pair (Gragg's modified midpoint, stage 3)
+        if (scheme == 6 && stage == 2) return launch_one<6, 4, 2>(a, grid, st);
+        return cudaErrorInvalidValue;
+    }
     if (adaptive == 2) {  // SPEC's error ratio (R-28)
         switch (scheme) {
         case 2: return launch_stage_i<2, 2>(stage, a, grid, st);

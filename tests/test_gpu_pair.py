@@ -1,5 +1,6 @@
 """GPU parity of K8 (rk_pair.cu, RK_OPT_FUSED_STEP = 3): two chained Runge–Kutta stages per
-launch (RK4 = two launches, explicit midpoint = one), the first stage's slope evaluated on the
+launch (RK4 = two launches, explicit midpoint = one, Gragg's modified midpoint = one + its last
+stage from the written-ahead Y3 and W), the first stage's slope evaluated on the
 tile grown by one cell and never stored.  Gate: bitwise equality with the fp64 oracle
 (R-17) over several steps, on tile-aligned grids (nx % 32 == 0, ny % 16 == 0) from one
 tile to many with ragged z chunks, every z-chunk length (the chunk's two extra stage-A planes and
@@ -13,7 +14,8 @@ import rk_inputs
 
 pytestmark = pytest.mark.gpu
 OS = oracle.SCHEMES
-PAIR = ["rk4", "midpoint"]
+PAIR = ["rk4", "midpoint", "modified_midpoint"]
+LAUNCHES = {"rk4": 2, "midpoint": 1, "modified_midpoint": 2}  # K8 (+ K3 last stage for Gragg)
 
 
 @pytest.fixture(scope="module")
@@ -68,7 +70,7 @@ def test_pair_steps_bitwise(ctx, scheme, dims):
         assert bitwise(got, u), (scheme, dims, k, first_mismatch(got, u))
     launches = st.stats()["stage_launches"] - before["stage_launches"]
     st.close()
-    assert launches == 3 * (2 if scheme == "rk4" else 1)
+    assert launches == 3 * LAUNCHES[scheme]
 
 
 @pytest.mark.parametrize("pz", [1, 2, 3, 5, 8, 64])
@@ -258,5 +260,7 @@ def test_pair_steps_halo_path(ctx, scheme, dims):
         assert bitwise(got, u), (scheme, dims, k, first_mismatch(got, u))
     after = st.stats()
     st.close()
-    assert after["stage_launches"] - before["stage_launches"] == 3 * (2 if scheme == "rk4" else 1)
-    assert after["halo_exchanges"] - before["halo_exchanges"] == 3 * (2 if scheme == "rk4" else 1)
+    # on the slab Gragg's K3 last stage is an interior and a boundary launch (overlapped halo)
+    slab_launches = {"rk4": 2, "midpoint": 1, "modified_midpoint": 3 if dims[2] > 2 else 2}
+    assert after["stage_launches"] - before["stage_launches"] == 3 * slab_launches[scheme]
+    assert after["halo_exchanges"] - before["halo_exchanges"] == 3 * LAUNCHES[scheme]
