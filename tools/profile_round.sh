@@ -4,7 +4,7 @@
 #   DOPRI5 try and one RK4 step, dram bytes of one step of every other scheme leg.
 #   Summaries are written on the box (tools/make_profiles.py) into gpurun_out/profiles_TAG/;
 #   the bulky .ncu-rep files are deleted there except the DOPRI5 one (gpurun returns <= 64 MiB).
-TAG=${1:-r2_v2}
+TAG=${1:-r2_v3}
 O=gpurun_out
 LEGS=adaptive,rk4,rk4_k3,repeats,try_loop,device_loop,halo,exposed,strong_emul,rk4_native,rk4_k6,midpoint_k6,midpoint_k3,exp512,small,e2e,cpu,cpu_full,euler,midpoint,modified_midpoint,cash_karp54,dopri5,rkf78,ab1,ab2,ab4,ab8,abm1,abm2,abm4,abm8
 timeout 1200 python bench.py --legs $LEGS > $O/${TAG}_bench.log 2>&1
