@@ -289,7 +289,7 @@ def run_reference(args, rank, world):
 SURVEY_BYTES = {"euler": 32, "rk4": 208, "cash_karp54": 432, "dopri5": 432}
 # K6 / K8 roofline: algorithmic fp64 (non-FMA) operations per cell-step
 K6_OPS = {"rk4": 168, "midpoint": 78, "modified_midpoint": 125}
-K8_LAUNCHES = {"rk4": 2, "midpoint": 1}  # K8 stage-pair launches per step
+K8_LAUNCHES = {"rk4": 2, "midpoint": 1, "modified_midpoint": 2}  # K8 launches per step (Gragg: pair + K3 last stage)
 
 
 def main():
