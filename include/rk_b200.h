@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define RK_ABI_VERSION 3
+#define RK_ABI_VERSION 4
 #define RK_UNIQUE_ID_BYTES 128
 
 typedef struct rk_ctx_s* rk_ctx;     /* one per rank: device, streams, NCCL communicator */
@@ -216,6 +216,9 @@ typedef struct {
                                  the launch's cells; halo re-reads,
                                  ghost planes and reductions are not counted              */
     double diverged_t;        /* t at which RK_OPT_CHECK_FINITE found a non-finite state  */
+    int64_t pair_launches;    /* of the stage launches: K8 stage-pair launches (ABI 4)    */
+    double pair_kernel_ms;    /* ... their share of stage_kernel_ms (RK_OPT_TIMING=1)     */
+    int64_t pair_bytes;       /* ... their share of stage_bytes                           */
 } rk_stats;
 
 /* ---- library ------------------------------------------------------------------------ */

@@ -370,8 +370,9 @@ static rk_status resolve_timing(rk_state st) {
     for (auto& p : st->pending) {
         float ms = 0.f;
         CK_CTX(ctx, cudaEventElapsedTime(&ms, p.a, p.b));
-        if (p.kind == 0) st->stats.stage_kernel_ms += ms;
+        if (p.kind == 0 || p.kind == 2) st->stats.stage_kernel_ms += ms;
         else st->stats.halo_ms += ms;
+        if (p.kind == 2) st->stats.pair_kernel_ms += ms;  // K8 stage-pair launches
         st->event_pool.push_back(p.a);
         st->event_pool.push_back(p.b);
     }
@@ -1050,13 +1051,16 @@ static rk_status dp_tail_pair(rk_state st, const std::vector<StagePlan>& plan, d
     CK_CTX(ctx, launch_gs_pair(PAIR_DP_TAIL, a, ctx->stream));
     if (st->timing) {
         CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
-        st->pending.push_back({e0, e1, 0});
+        st->pending.push_back({e0, e1, 2});
         if (st->pending.size() > 4096) TRY(resolve_timing(st));
     }
+    const int64_t pb = 7 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double);
     st->stats.kernel_launches += 1;
     st->stats.stage_launches += 1;
+    st->stats.pair_launches += 1;
     st->stats.rhs_evals += 2;
-    st->stats.stage_bytes += 7 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double);
+    st->stats.stage_bytes += pb;
+    st->stats.pair_bytes += pb;
     return RK_OK;
 }
 
@@ -1335,7 +1339,7 @@ static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
         CK_CTX(ctx, launch_gs_pair(kind, a, ctx->stream));
         if (st->timing) {
             CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
-            st->pending.push_back({e0, e1, 0});
+            st->pending.push_back({e0, e1, 2});
             if (st->pending.size() > 4096) TRY(resolve_timing(st));
         }
         return RK_OK;
@@ -1399,9 +1403,12 @@ static rk_status pair_steps(rk_state st, int scheme, double dt, int64_t n) {
         const int nl = rk4 ? 2 : 1;
         st->stats.kernel_launches += nl;
         st->stats.stage_launches += nl;
+        st->stats.pair_launches += nl;
         st->stats.rhs_evals += C.s;
         // RK4: (u -> Y3, W) + (Y3, u, W -> u_new) = 7 arrays; midpoint: u -> u_new; Gragg's pair: 3
-        st->stats.stage_bytes += (rk4 ? 7 : gragg ? 3 : 2) * cells * 2 * (int64_t)sizeof(double);
+        const int64_t pb = (rk4 ? 7 : gragg ? 3 : 2) * cells * 2 * (int64_t)sizeof(double);
+        st->stats.stage_bytes += pb;
+        st->stats.pair_bytes += pb;
         st->stats.steps += 1;
     }
     st->k1_valid = false;
