@@ -264,3 +264,38 @@ def test_pair_steps_halo_path(ctx, scheme, dims):
     slab_launches = {"rk4": 2, "midpoint": 1, "modified_midpoint": 3 if dims[2] > 2 else 2}
     assert after["stage_launches"] - before["stage_launches"] == 3 * slab_launches[scheme]
     assert after["halo_exchanges"] - before["halo_exchanges"] == 3 * LAUNCHES[scheme]
+
+
+def test_pair_max_size_1024_cubed(ctx):
+    """Maximum size through K8: a 1024^3 grid (2^31 values per array; u, u_new, Y3, W ~ 69 GiB),
+    padded offsets of the upper planes beyond int32.  One RK4 step (two pair launches) and one
+    explicit-midpoint step; sampled cells (last planes, periodic corners, the IC cube's faces)
+    bitwise against the oracle on their radius-5 neighbourhoods."""
+    import gc
+    gc.collect()
+    n = 1024
+    u0 = rk_inputs.gray_scott_ic(n, n, n, seed=42)
+    st = pair_state(ctx, (n, n, n), u0)
+    before = st.stats()["pair_launches"]
+    st.do_step("rk4", 0.0, 1.0)
+    g4 = st.get()
+    st.set(u0)
+    st.do_step("midpoint", 0.0, 1.0)
+    g2 = st.get()
+    launches = st.stats()["pair_launches"] - before
+    st.close()
+    assert launches == 3
+    lo, hi = rk_inputs.cube_range(n)
+    pts = [(1023, 1023, 1023), (1023, 0, 511), (1022, 1023, 0), (0, 0, 0), (lo, lo, lo),
+           (hi - 1, hi, lo - 1), (hi, 700, hi - 1), (900, lo + 3, hi), (512, 15, 31), (1, 16, 32)]
+    r = 5
+    p = oracle.gray_scott_problem(2 * r + 1, 2 * r + 1, 2 * r + 1)
+    for (z, y, x) in pts:
+        idx = lambda c, m: [(c + d) % m for d in range(-r, r + 1)]  # noqa: E731
+        blk = np.ascontiguousarray(u0[np.ix_(idx(z, n), [0, 1], idx(y, n), idx(x, n))])
+        w4 = oracle.step(p, OS["rk4"], 0.0, 1.0, blk).reshape(blk.shape)
+        w2 = oracle.step(p, OS["midpoint"], 0.0, 1.0, blk).reshape(blk.shape)
+        assert bitwise(g4[z, :, y, x], w4[r, :, r, r]), ("rk4", z, y, x)
+        assert bitwise(g2[z, :, y, x], w2[r, :, r, r]), ("midpoint", z, y, x)
+    del g4, g2, u0
+    gc.collect()
