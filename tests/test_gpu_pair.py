@@ -299,3 +299,44 @@ def test_pair_max_size_1024_cubed(ctx):
         assert bitwise(g2[z, :, y, x], w2[r, :, r, r]), ("midpoint", z, y, x)
     del g4, g2, u0
     gc.collect()
+
+
+def _mixed_sequence(st):
+    """Every path that shares a state's k buffers, interleaved: K8 RK4 / midpoint / Gragg pairs
+    (Y3, W scratch in k buffers 0, 1), DOPRI5 tries (FSAL k1 in buffer 0, the tail pair's k7 in
+    buffer 1), Adams steps, CK54 / RKF78 stage by stage, an adaptive run."""
+    out, tries = [], []
+    st.do_step("rk4", 0.0, 1.0)
+    for k in range(2):
+        tries.append(st.try_step("dopri5", 1.0 + k, 0.5, 1e-6, 1e-6))
+    st.do_step("rk4", 2.0, 1.0)  # after an accepted FSAL try: k1 must not be reused
+    tries.append(st.try_step("dopri5", 3.0, 0.5, 1e-6, 1e-6))
+    out.append(st.get())
+    st.do_step("ab2", 4.0, 0.5)
+    st.do_step("modified_midpoint", 4.5, 0.5)
+    tries.append(st.try_step("dopri5", 5.0, 0.5, 1e-6, 1e-6))
+    st.do_step("midpoint", 5.5, 0.5)
+    tries.append(st.try_step("cash_karp54", 6.0, 0.25, 1e-6, 1e-6))
+    st.do_step("rkf78", 6.25, 0.25)
+    out.append(st.get())
+    tries.append(st.integrate_adaptive("dopri5", 6.5, 9.0, 0.5, 1e-6, 1e-6))
+    st.do_step("rk4", 9.0, 1.0)
+    out.append(st.get())
+    return out, tries
+
+
+@pytest.mark.parametrize("loopback", [0, 1], ids=["one_gpu", "slab_path"])
+def test_pair_mixed_sequence_equals_stage_kernels(ctx, loopback):
+    import paper_2309_05331_b200 as rk
+    dims = (96, 32, 21)
+    u0 = perturbed_ic(*dims, seed=12)
+    res = []
+    for mode in (3, 0):
+        st = pair_state(ctx, dims, u0, mode)
+        st.set_option(rk.OPT_HALO_LOOPBACK, loopback)
+        res.append(_mixed_sequence(st))
+        st.close()
+    (g3, t3), (g0, t0) = res
+    assert t3 == t0
+    for i, (a, b) in enumerate(zip(g3, g0)):
+        assert bitwise(a, b), (i, first_mismatch(a, b))
