@@ -257,6 +257,25 @@ typedef struct {
 } rk_halo_plan;
 rk_status rk_halo_plan_get(int world, int rank, rk_halo_plan* out);
 
+/* The ghost exchange of a K8 stage pair on the multi-GPU slab (RK_OPT_FUSED_STEP = 3, DESIGN.md
+ * §7): the pair's source needs its 2 boundary planes from each neighbour, its base (if any) 1.
+ * Messages in posting order -- all sends (to up before to down), then all receives (from down
+ * before from up) -- so that world 2 (one peer is both neighbours) and world 1 (self) pair each
+ * send with the right receive under in-order matching per peer. */
+typedef struct {
+    int recv;        /* 0: send slab planes, 1: receive into a ghost array              */
+    int peer;        /* rank                                                          */
+    int array;       /* 0: the source (2-deep ghosts), 1: the base (1-deep ghosts)    */
+    int side;        /* send: 0 the slab's bottom planes, 1 its top planes; receive: 0 the
+                        ghosts below the slab (planes -n..-1), 1 above (nzl..nzl+n-1) */
+    int nplanes;     /* 2 (source) or 1 (base)                                        */
+} rk_pair_msg;
+typedef struct {
+    int up, down, nmsg;
+    rk_pair_msg msg[8];
+} rk_pair_plan;
+rk_status rk_pair_ghost_plan(int world, int rank, int with_base, rk_pair_plan* out);
+
 /* ---- context ------------------------------------------------------------------------ */
 /* Rank 0 creates the NCCL unique id (RK_UNIQUE_ID_BYTES bytes); the caller broadcasts it
  * (torch.distributed) to all ranks before rk_ctx_create.  Not needed when world == 1. */

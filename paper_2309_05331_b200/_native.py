@@ -54,6 +54,15 @@ class HaloPlan(ctypes.Structure):
                 ("msg", HaloMsg * 4)]
 
 
+class PairMsg(ctypes.Structure):
+    _fields_ = [("recv", ctypes.c_int), ("peer", ctypes.c_int), ("array", ctypes.c_int), ("side", ctypes.c_int),
+                ("nplanes", ctypes.c_int)]
+
+
+class PairPlan(ctypes.Structure):
+    _fields_ = [("up", ctypes.c_int), ("down", ctypes.c_int), ("nmsg", ctypes.c_int), ("msg", PairMsg * 8)]
+
+
 _v, _p, _i, _i64, _d = ctypes.c_void_p, ctypes.POINTER, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 _dp = ctypes.POINTER(ctypes.c_double)
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -68,6 +77,7 @@ SIGNATURES = {
     "rk_controller": (_i, [_i, _d, _dp, _ip]),
     "rk_step_adjust": (_i, [_i, _i, _d, _dp, _ip]),
     "rk_halo_plan_get": (_i, [_i, _i, _p(HaloPlan)]),
+    "rk_pair_ghost_plan": (_i, [_i, _i, _i, _p(PairPlan)]),
     "rk_nccl_unique_id": (_i, [_v]),
     "rk_ctx_create": (_i, [_i, _i, _i, _v, _v, _p(_v)]),
     "rk_ctx_destroy": (_i, [_v]),

@@ -330,6 +330,15 @@ def halo_plan(world: int, rank: int) -> dict:
                      for m in p.msg[:p.nmsg]]}
 
 
+def pair_ghost_plan(world: int, rank: int, with_base: bool) -> dict:
+    """The ghost exchange of a K8 stage pair on the multi-GPU slab (rk_pair_ghost_plan)."""
+    p = _native.PairPlan()
+    call("rk_pair_ghost_plan", world, rank, 1 if with_base else 0, ctypes.byref(p))
+    return {"up": p.up, "down": p.down,
+            "msgs": [{"recv": bool(m.recv), "peer": m.peer, "array": m.array, "side": m.side,
+                      "nplanes": m.nplanes} for m in p.msg[:p.nmsg]]}
+
+
 def controller(scheme, E: float, dt: float, kind: int = 0):
     """Library's host step adjuster (kind 0: Odeint R-12, 1: SPEC R-28): (accepted, dt_next)."""
     d, a = ctypes.c_double(dt), ctypes.c_int()

@@ -974,18 +974,20 @@ static rk_status pair_ghost_exchange(rk_state st, const double* src, double* g2,
         e1 = pool_event(st);
         CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
     }
+    rk_pair_plan plan;
+    TRY(rk_pair_ghost_plan(ctx->world, ctx->rank, base ? 1 : 0, &plan));
     NK_CTX(ctx, ncclGroupStart());
-    NK_CTX(ctx, ncclSend(src + (nzl - 2) * pv, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->stream));
-    NK_CTX(ctx, ncclSend(src, (size_t)(2 * pv), ncclDouble, down, ctx->nccl, ctx->stream));
-    if (base) {
-        NK_CTX(ctx, ncclSend(base + (nzl - 1) * pv, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->stream));
-        NK_CTX(ctx, ncclSend(base, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->stream));
-    }
-    NK_CTX(ctx, ncclRecv(g2, (size_t)(2 * pv), ncclDouble, down, ctx->nccl, ctx->stream));
-    NK_CTX(ctx, ncclRecv(g2 + 2 * pv, (size_t)(2 * pv), ncclDouble, up, ctx->nccl, ctx->stream));
-    if (base) {
-        NK_CTX(ctx, ncclRecv(st->pg_w, (size_t)pv, ncclDouble, down, ctx->nccl, ctx->stream));
-        NK_CTX(ctx, ncclRecv(st->pg_w + pv, (size_t)pv, ncclDouble, up, ctx->nccl, ctx->stream));
+    for (int i = 0; i < plan.nmsg; ++i) {
+        const rk_pair_msg& m = plan.msg[i];
+        const size_t cnt = (size_t)(m.nplanes * pv);
+        if (m.recv) {  // ghosts below the slab at the ghost array's start, above after them
+            double* g = m.array == 0 ? g2 : st->pg_w;
+            NK_CTX(ctx, ncclRecv(g + (m.side ? m.nplanes * pv : 0), cnt, ncclDouble, m.peer, ctx->nccl, ctx->stream));
+        } else {       // the slab's bottom planes, or its top ones
+            const double* a = m.array == 0 ? src : base;
+            NK_CTX(ctx, ncclSend(a + (m.side ? (nzl - m.nplanes) * pv : 0), cnt, ncclDouble, m.peer, ctx->nccl,
+                                 ctx->stream));
+        }
     }
     NK_CTX(ctx, ncclGroupEnd());
     mark_progress(ctx, ctx->stream);
@@ -2313,6 +2315,26 @@ rk_status rk_halo_plan_get(int world, int rank, rk_halo_plan* out) {
         p.msg[1] = {0, p.down, 0, 1};  // my bottom plane   -> down's ghost_hi
         p.msg[2] = {1, p.down, 1, 1};  // ghost_lo (z = -1) <- down's top plane
         p.msg[3] = {1, p.up, 0, 1};    // ghost_hi (z=nzl)  <- up's bottom plane
+    }
+    *out = p;
+    return RK_OK;
+}
+
+rk_status rk_pair_ghost_plan(int world, int rank, int with_base, rk_pair_plan* out) {
+    if (!out || world < 1 || rank < 0 || rank >= world) return fail(RK_ERR_ARG, "rk_pair_ghost_plan: bad arguments");
+    rk_pair_plan p{};
+    p.up = (rank + 1) % world;
+    p.down = (rank - 1 + world) % world;
+    const int na = with_base ? 2 : 1;
+    for (int ar = 0; ar < na; ++ar) {  // sends: top planes to up, bottom planes to down
+        const int np = ar == 0 ? 2 : 1;
+        p.msg[p.nmsg++] = {0, p.up, ar, 1, np};
+        p.msg[p.nmsg++] = {0, p.down, ar, 0, np};
+    }
+    for (int ar = 0; ar < na; ++ar) {  // receives: ghosts below from down, above from up
+        const int np = ar == 0 ? 2 : 1;
+        p.msg[p.nmsg++] = {1, p.down, ar, 0, np};
+        p.msg[p.nmsg++] = {1, p.up, ar, 1, np};
     }
     *out = p;
     return RK_OK;

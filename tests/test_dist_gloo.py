@@ -77,3 +77,64 @@ def test_halo_plan_gloo(world, nz):
         # ghost slot 0 = plane z0+nzl (periodic), slot 1 = plane z0-1 (periodic)
         assert hi_min == hi_max == float((z0 + nzl) % nz)
         assert lo_min == lo_max == float((z0 - 1) % nz)
+
+
+def _pair_worker(rank, world, port, nz, plane_shape, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_05331_b200 as rk
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        z0, nzl = rk.partition(nz, world, rank)
+        # the slab's planes, every value tagged with the global z index (source: z, base: 1000 + z)
+        src = torch.stack([torch.full(plane_shape, float(z0 + i), dtype=torch.float64) for i in range(nzl)])
+        base = src + 1000.0
+        g2 = torch.full((4,) + plane_shape, -1.0, dtype=torch.float64)   # [-2, -1 | nzl, nzl+1]
+        g1 = torch.full((2,) + plane_shape, -1.0, dtype=torch.float64)   # [-1 | nzl]
+        plan = rk.pair_ghost_plan(world, rank, True)
+        reqs = []
+        for m in plan["msgs"]:
+            n = m["nplanes"]
+            if m["recv"]:
+                g = g2 if m["array"] == 0 else g1
+                off = n if m["side"] else 0
+                view = torch.empty((n,) + plane_shape, dtype=torch.float64)
+                reqs.append((dist.irecv(view, src=m["peer"]), view, g, off))
+            else:
+                a = src if m["array"] == 0 else base
+                view = (a[nzl - n:] if m["side"] else a[:n]).contiguous()
+                reqs.append((dist.isend(view, dst=m["peer"]), None, None, None))
+        for r, view, g, off in reqs:
+            r.wait()
+            if view is not None:
+                g[off:off + view.shape[0]] = view
+        q.put((rank, z0, nzl, [float(g2[i].mean()) for i in range(4)], [float(g1[i].mean()) for i in range(2)],
+               [float(g2[i].std()) for i in range(4)]))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - surfaced by the parent
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("world,nz", [(2, 8), (2, 5), (3, 13), (4, 9), (4, 8)])
+def test_pair_ghost_plan_gloo(world, nz):
+    """The K8 pairs' ghost exchange (rk_pair_ghost_plan, posting order as on NCCL) executed with
+    real point-to-point messages: every rank's 2-deep source ghosts and 1-deep base ghosts hold
+    its periodic z-neighbours' boundary planes, also at world 2 where one peer is both."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pair_worker, args=(r, world, port, nz, (3, 5), q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for r in sorted(res, key=lambda r: r[0]):
+        assert len(r) > 2, r
+        rank, z0, nzl, g2, g1, sd = r
+        assert nzl >= 2
+        assert g2 == [float((z0 - 2) % nz), float((z0 - 1) % nz), float((z0 + nzl) % nz), float((z0 + nzl + 1) % nz)]
+        assert g1 == [1000.0 + (z0 - 1) % nz, 1000.0 + (z0 + nzl) % nz]
+        assert max(sd) == 0.0
