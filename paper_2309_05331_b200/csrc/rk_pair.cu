@@ -65,6 +65,9 @@ constexpr int RING_WARPS = RKB_RING_WARPS;                // 3 (32 lanes; measur
 static_assert(NRING % RING_WARPS == 0 && NRING / RING_WARPS <= 32, "ring split");
 constexpr int NPATCH = 36 * BH;                           // source positions used (box cols 1..36)
 constexpr int SMEM_BUDGET = 113 * 1024;                   // 2 CTAs per SM
+#ifndef RKB_PAIR_RMAX
+#define RKB_PAIR_RMAX 5  // ring depth cap (6 measured slower: RK4 3.33 vs 3.16 ms)
+#endif
 constexpr int SMEM_BUDGET3 = 72 * 1024;                   // 3 CTAs per SM (u-fed pairs)
 
 // U1: u comes in its own 1-ring box (Y_A's source is a written-ahead Y).  The ring holds the
@@ -78,7 +81,7 @@ struct PLayout {
     static constexpr int stage = HSLOT + (U1 ? USLOT : 0);
     static constexpr int fixed = 2 * YBSLOT;
     static constexpr int Rb = ((minb == 3 ? SMEM_BUDGET3 : SMEM_BUDGET) - fixed - 64) / stage;
-    static constexpr int R = Rb > 5 ? 5 : Rb;
+    static constexpr int R = Rb > RKB_PAIR_RMAX ? RKB_PAIR_RMAX : Rb;
     static_assert(R >= 4, "ring too shallow");
     static constexpr int off_u = HSLOT;
     static constexpr int yb = R * stage;           // Y_B buffer (2 slots)
