@@ -244,6 +244,11 @@ struct PairArgs {
     CUtensorMap tm_ulo, tm_uhi;      // ghosts: the base's planes -1 / nzl (1-plane arrays)
     const double* src_lo;            // ghosts: raw pointers of the source's ghost arrays (patches)
     const double* src_hi;
+    CUtensorMap tm_glo2, tm_ghi2;    // PAIR_DP_HEAD ghosts of k_1 (2-plane arrays)
+    const double* src2;              // PAIR_DP_HEAD: k_1 (patches), and its ghost arrays
+    const double* src2_lo;
+    const double* src2_hi;
+    double gA, gB1;                  // PAIR_DP_HEAD: Y_2 = u + gA k_1, Y_3 = (u + gB1 k_1) + gB k_2
     int ghosts;                      // multi-GPU slab (or its one-GPU loopback): z does not wrap
     const double* src;     // raw pointer of the source (periodic cells beyond the padded ring)
     const double* w_in;    // PAIR_LAST: the partial sum W of the first pair; PAIR_DP_TAIL: E
@@ -259,7 +264,7 @@ struct PairArgs {
     double d1, d2, F, FK, inv_h2;
     int zchunk;
 };
-enum { PAIR_FIRST = 0, PAIR_LAST = 1, PAIR_ONLY = 2, PAIR_DP_TAIL = 3 };
+enum { PAIR_FIRST = 0, PAIR_LAST = 1, PAIR_ONLY = 2, PAIR_DP_TAIL = 3, PAIR_DP_HEAD = 4 };
 bool pair_shape_ok(const GridGeom& g);  // nx % 32 == 0, ny % 16 == 0
 cudaError_t encode_pair_map(CUtensorMap* map, const double* base, const GridGeom& g, int nplanes);
 cudaError_t launch_gs_pair(int kind, const PairArgs& a, cudaStream_t st);

@@ -75,17 +75,20 @@ constexpr int SMEM_BUDGET3 = 72 * 1024;                   // 3 CTAs per SM (u-fe
 // The single-pair kind (u -> u_new: explicit midpoint) runs 3 CTAs per SM (<= 85 registers: Y_A
 // own values from the ring, 24 warps; 1.14 -> 1.12 ms); the others 2 (their register queues
 // at 80 registers spill: RK4 3.15 -> 3.28 ms).
-template <bool U1, bool YOUT>
+// HD (the DOPRI5 head pair): u and k_1 both in 2-margin boxes, formed in place after they land
+// into Y_A = u + (dt a_21) k_1 and the base Z = u + (dt a_31) k_1; one Y_B slot (+ a second
+// barrier) so the two boxes fit two CTAs per SM.
+template <bool U1, bool YOUT, bool HD = false>
 struct PLayout {
-    static constexpr int minb = (!U1 && !YOUT) ? 3 : 2;
-    static constexpr int stage = HSLOT + (U1 ? USLOT : 0);
-    static constexpr int fixed = 2 * YBSLOT;
+    static constexpr int minb = (!U1 && !YOUT && !HD) ? 3 : 2;
+    static constexpr int stage = HSLOT + (U1 ? USLOT : 0) + (HD ? HSLOT : 0);
+    static constexpr int fixed = (HD ? 1 : 2) * YBSLOT;
     static constexpr int Rb = ((minb == 3 ? SMEM_BUDGET3 : SMEM_BUDGET) - fixed - 64) / stage;
     static constexpr int R = Rb > RKB_PAIR_RMAX ? RKB_PAIR_RMAX : Rb;
     static_assert(R >= 4, "ring too shallow");
     static constexpr int off_u = HSLOT;
-    static constexpr int yb = R * stage;           // Y_B buffer (2 slots)
-    static constexpr int bar = yb + 2 * YBSLOT;    // R mbarriers
+    static constexpr int yb = R * stage;           // Y_B buffer (2 slots; HD: 1)
+    static constexpr int bar = yb + (HD ? 1 : 2) * YBSLOT;  // R mbarriers
     static constexpr int smem = bar + R * 8;
 };
 
@@ -181,9 +184,11 @@ __device__ __forceinline__ void store_ring(double* p, const GridGeom& G, bool ex
 // Y_6 (written ahead), Y_B = W (+) (dt b_6) k_6 = u_new (a_7j = b_j, FSAL), k_B = k_7 = F(u_new);
 // the epilogue stores u_new and k_7, forms e = (E (+) (dt e_6) k_6) (+) (dt e_7) k_7 and the
 // Odeint ratio |e| / (atol (+) rtol (x) (|u| (+) dt (x) |k_1|)) with a block max.
-template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false, bool DTP = false>
-__global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(const __grid_constant__ PairArgs a) {
-    using LY = PLayout<U1, YOUT>;
+// KK: store k_A and k_B with their rings (HD: k_2, k_3 of a DOPRI5 try).
+template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false, bool DTP = false, bool KK = false, bool HD = false>
+__global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kernel(const __grid_constant__ PairArgs a) {
+    using LY = PLayout<U1, YOUT, HD>;
+    constexpr bool BASE = U1 || HD;  // Y_B's base comes from its own box (else it is Y_A's source)
     constexpr int R = LY::R;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + LY::bar);
@@ -204,6 +209,7 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
     const double cgB = DTP ? mul(dsc, a.gB) : a.gB, cgN = DTP ? mul(dsc, a.gN) : a.gN;
     const double cbA = DTP ? mul(dsc, a.betaA) : a.betaA, cbB = DTP ? mul(dsc, a.betaB) : a.betaB;
     const double cdt = DTP ? dsc : a.dt;
+    const double cgA = DTP ? mul(dsc, a.gA) : a.gA, cgB1 = DTP ? mul(dsc, a.gB1) : a.gB1;  // HD
     auto plane = [&](int i) PINLINE -> int { return pmod(zb - 2 + i, G.nzl); };
     const bool edge = x0 == 0 || x0 + PX == G.nx || y0 == 0 || y0 + PTH == G.ny;  // CTA-uniform
 
@@ -232,7 +238,12 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
     }
 
     auto raw = [&](int i) PINLINE -> unsigned char* { return smem + (size_t)(i % R) * LY::stage; };
-    auto ybs = [&](int i) PINLINE -> double* { return reinterpret_cast<double*>(smem + LY::yb + (size_t)(i & 1) * YBSLOT); };
+    auto ybs = [&](int i) PINLINE -> double* {
+        return reinterpret_cast<double*>(smem + LY::yb + (HD ? (size_t)0 : (size_t)(i & 1) * YBSLOT));
+    };
+    // base box geometry: U1 the 34x18 u box, HD the 38x20 box of the formed Z
+    const int pbase = HD ? pb : pu, rbase = HD ? rb : ru;
+    constexpr int BPITCH = HD ? BW : UW, BCS = HD ? BOX : UBOX;
     auto tma = [&](void* dst, const CUtensorMap* m, uint64_t* b, int c0, int c1, int q) PINLINE {
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
@@ -247,12 +258,17 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
         const int p = zb - 2 + i;
         const int q = plane(i);
         const bool mid = i >= 1 && i < nr - 1;  // u feeds Y_B at stage-A planes zb-1 .. ze
-        const uint32_t bytes = 2 * BOX * 8 + ((U1 && mid) ? 2 * UBOX * 8 : 0);
+        const uint32_t bytes = 2 * BOX * 8 + ((U1 && mid) ? 2 * UBOX * 8 : 0) + (HD ? 2 * BOX * 8 : 0);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
         unsigned char* st = raw(i);
         if (a.ghosts && p < 0) tma(st, &a.tm_glo, b, x0 - 2, y0 - 1, p + 2);
         else if (a.ghosts && p >= G.nzl) tma(st, &a.tm_ghi, b, x0 - 2, y0 - 1, p - G.nzl);
         else tma(st, &a.tm_src, b, x0 - 2, y0 - 1, q);
+        if constexpr (HD) {  // k_1: the same 2-margin box, every plane
+            if (a.ghosts && p < 0) tma(st + LY::off_u, &a.tm_glo2, b, x0 - 2, y0 - 1, p + 2);
+            else if (a.ghosts && p >= G.nzl) tma(st + LY::off_u, &a.tm_ghi2, b, x0 - 2, y0 - 1, p - G.nzl);
+            else tma(st + LY::off_u, &a.tm_u, b, x0 - 2, y0 - 1, q);
+        }
         if constexpr (U1) {
             if (mid) {
                 if (a.ghosts && p < 0) tma(st + LY::off_u, &a.tm_ulo, b, x0, y0, 0);
@@ -296,15 +312,39 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
             my_src = s_src[tid];
         }
     }
-    double pv0 = 0.0, pv1 = 0.0;  // this thread's patch values of the next plane to land
+    double pv0 = 0.0, pv1 = 0.0, pv2 = 0.0, pv3 = 0.0;  // this thread's patch values of the next plane
     auto patch_load = [&](int i) PINLINE {
         if (my_pos >= 0 && i < nr) {
             const int pz = zb - 2 + i;
-            const double* p = a.ghosts && pz < 0 ? a.src_lo + (int64_t)(pz + 2) * G.ps + my_src
-                            : a.ghosts && pz >= G.nzl ? a.src_hi + (int64_t)(pz - G.nzl) * G.ps + my_src
-                                                      : a.src + (int64_t)plane(i) * G.ps + my_src;
+            const int64_t o = a.ghosts && pz < 0 ? (int64_t)(pz + 2) * G.ps + my_src
+                            : a.ghosts && pz >= G.nzl ? (int64_t)(pz - G.nzl) * G.ps + my_src
+                                                      : (int64_t)plane(i) * G.ps + my_src;
+            const double* p = (a.ghosts && pz < 0 ? a.src_lo : a.ghosts && pz >= G.nzl ? a.src_hi : a.src) + o;
             pv0 = p[0];
             pv1 = p[G.cs];
+            if constexpr (HD) {
+                const double* p2 = (a.ghosts && pz < 0 ? a.src2_lo : a.ghosts && pz >= G.nzl ? a.src2_hi : a.src2) + o;
+                pv2 = p2[0];
+                pv3 = p2[G.cs];
+            }
+        }
+    };
+    // HD: after the patches, Y_A = u + (dt a_21) k_1 in place of u and Z = u + (dt a_31) k_1 in
+    // place of k_1, at every box position stage A or Y_B reads (columns 1..36)
+    auto form = [&](int i) PINLINE {
+        if constexpr (HD) {
+            if (edge) __syncthreads();  // patched cells (written by other threads) visible
+            double* y = reinterpret_cast<double*>(raw(i));
+            double* k = reinterpret_cast<double*>(raw(i) + LY::off_u);
+            for (int q = tid; q < NPATCH; q += PNT) {
+                const int pos = (q / 36) * BW + 1 + q % 36;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const double uu = y[c * BOX + pos], kk = k[c * BOX + pos];
+                    y[c * BOX + pos] = add(uu, mul(cgA, kk));
+                    k[c * BOX + pos] = add(uu, mul(cgB1, kk));
+                }
+            }
         }
     };
     auto patch = [&](int i) PINLINE {  // after wait(i); then load the values of plane i+1
@@ -312,8 +352,14 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
             double* y = reinterpret_cast<double*>(raw(i));
             y[my_pos] = pv0;
             y[BOX + my_pos] = pv1;
+            if constexpr (HD) {
+                double* k = reinterpret_cast<double*>(raw(i) + LY::off_u);
+                k[my_pos] = pv2;
+                k[BOX + my_pos] = pv3;
+            }
         }
         patch_load(i + 1);
+        form(i);
     };
 
     if (tid == 0) {
@@ -439,18 +485,31 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
         rhs_two(ya + pb, BOX, BW, yac[0], yac[1], yam[0], yap[0], yam[1], yap[1], a, kac[0], kac[1]);
         double (&uc)[2][2] = u_q[Q0];
         const double (&up)[2][2] = u_q[QM];
-        if constexpr (U1) {
+        if constexpr (BASE) {
             const double* U = reinterpret_cast<const double*>(st + LY::off_u);
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                uc[r][0] = U[pu + r * UW];
-                uc[r][1] = U[UBOX + pu + r * UW];
+                uc[r][0] = U[pbase + r * BPITCH];
+                uc[r][1] = U[BCS + pbase + r * BPITCH];
             }
         }
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
-            for (int c = 0; c < 2; ++c) ybp[r][c] = add(U1 ? uc[r][c] : yac[r][c], mul(cgB, kac[r][c]));
+            for (int c = 0; c < 2; ++c) ybp[r][c] = add(BASE ? uc[r][c] : yac[r][c], mul(cgB, kac[r][c]));
+        double yr[2] = {0.0, 0.0};  // Y_B at this thread's ring cell
+        if (ring_plane && hr) {
+            const double* ym = reinterpret_cast<const double*>(raw(ic - 1));
+            const double* yp = reinterpret_cast<const double*>(raw(ic + 1));
+            double kr[2];
+            rhs_box(ya + rb, ym + rb, yp + rb, BOX, BW, a, kr);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const double ur = BASE ? reinterpret_cast<const double*>(st + LY::off_u)[c * BCS + rbase] : ya[c * BOX + rb];
+                yr[c] = add(ur, mul(cgB, kr[c]));
+            }
+        }
+        if constexpr (HD) __syncthreads();  // one Y_B slot: every stage-B read of Y_B(t-1) is done
         if (ring_plane) {
             double* yb = ybs(ic);
 #pragma unroll
@@ -459,15 +518,8 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
                 yb[YBOX + pu + r * UW] = ybp[r][1];
             }
             if (hr) {
-                const double* ym = reinterpret_cast<const double*>(raw(ic - 1));
-                const double* yp = reinterpret_cast<const double*>(raw(ic + 1));
-                double kr[2];
-                rhs_box(ya + rb, ym + rb, yp + rb, BOX, BW, a, kr);
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const double ur = U1 ? reinterpret_cast<const double*>(st + LY::off_u)[c * UBOX + ru] : ya[c * BOX + rb];
-                    yb[c * YBOX + ru] = add(ur, mul(cgB, kr[c]));
-                }
+                yb[ru] = yr[0];
+                yb[YBOX + ru] = yr[1];
             }
         }
         // ---- stage B at plane t-1 (output planes zb .. ze-1) ----
@@ -482,6 +534,18 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
                 const int64_t ro = qo + coff + (int64_t)r * G.P;
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
+                    if constexpr (KK) {  // k_A (plane t-1) and k_B, both with their rings
+                        double* pa = a.out_y + ro + c * G.cs;
+                        double* pk = a.out + ro + c * G.cs;
+                        if (ering) {
+                            store_ring(pa, G, rx0, rx1, ry0, ry1, kap[r][c]);
+                            store_ring(pk, G, rx0, rx1, ry0, ry1, kb[r][c]);
+                        } else {
+                            pa[0] = kap[r][c];
+                            pk[0] = kb[r][c];
+                        }
+                        continue;
+                    }
                     if constexpr (DP) {
                         const double un = ybc[r][c];  // Y_7 = u_new
                         double* pu_ = a.out + ro + c * G.cs;
@@ -541,19 +605,19 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT>::minb) gs_pair_kernel(c
     if constexpr (DP) block_max_to_global(rbits, a.errmax);
 }
 
-template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false, bool DTP = false>
+template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false, bool DTP = false, bool KK = false, bool HD = false>
 cudaError_t launch_pair_t(const PairArgs& a, cudaStream_t st) {
-    using LY = PLayout<U1, YOUT>;
+    using LY = PLayout<U1, YOUT, HD>;
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gs_pair_kernel<U1, WIN, BA, YOUT, DP, DTP>,
+        cudaError_t e = cudaFuncSetAttribute(gs_pair_kernel<U1, WIN, BA, YOUT, DP, DTP, KK, HD>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, LY::smem);
         if (e != cudaSuccess) return e;
         configured = true;
     }
     const int tiles = (a.geo.nx / PX) * (a.geo.ny / PTH);
     const int nch = (a.geo.nzl + a.zchunk - 1) / a.zchunk;
-    gs_pair_kernel<U1, WIN, BA, YOUT, DP, DTP><<<dim3((unsigned)tiles, (unsigned)nch), PNT, LY::smem, st>>>(a);
+    gs_pair_kernel<U1, WIN, BA, YOUT, DP, DTP, KK, HD><<<dim3((unsigned)tiles, (unsigned)nch), PNT, LY::smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -586,6 +650,9 @@ cudaError_t launch_gs_pair(int kind, const PairArgs& a, cudaStream_t st) {
     case PAIR_FIRST: return launch_pair_t<false, false, true, true>(a, st);  // RK4 1-2: u -> Y3, W
     case PAIR_LAST: return launch_pair_t<true, true, true, false>(a, st);    // RK4 3-4: Y3, u, W -> u_new
     case PAIR_ONLY: return launch_pair_t<false, false, false, false>(a, st); // midpoint: u -> u_new
+    case PAIR_DP_HEAD:  // DOPRI5 stages 2-3: u, k1 -> k2, k3
+        return a.dtp ? launch_pair_t<false, false, false, false, false, true, true, true>(a, st)
+                     : launch_pair_t<false, false, false, false, false, false, true, true>(a, st);
     case PAIR_DP_TAIL:  // DOPRI5 stages 6-7 (dt on the device inside the graph try loop)
         return a.dtp ? launch_pair_t<true, true, true, false, true, true>(a, st)
                      : launch_pair_t<true, true, true, false, true, false>(a, st);

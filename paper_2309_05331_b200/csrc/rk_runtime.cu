@@ -1066,13 +1066,88 @@ static rk_status dp_tail_pair(rk_state st, const std::vector<StagePlan>& plan, d
     return RK_OK;
 }
 
-// Run the stages of one step / try.  Stage 0 (k1 = F(u)) is skipped when k1 is valid.
+// K8 DOPRI5 head pair (PAIR_DP_HEAD): stages 2 and 3 of a try in one launch -- u and k1 (both
+// with 2-cell margins; Y2 = u + (dt a21) k1 and Z3 = u + (dt a31) k1 formed in shared memory as
+// they land) -> k2, k3 with their rings: 4 arrays instead of stages 2 + 3's 7
+static rk_status dp_head_pair(rk_state st, double dt) {
+    NvtxRange nv("rk stage pair (K8 DOPRI5 stages 2-3)");
+    rk_ctx ctx = st->ctx;
+    const Coeffs C = coeffs_of(RK_DOPRI5);
+    PairArgs a{};
+    if (halo_path(st)) {  // u's and k1's two boundary planes each side
+        TRY(pair_ghost_buffers(st));
+        TRY(pair_ghost_exchange(st, st->u, st->pg_y, nullptr));
+        TRY(pair_ghost_exchange(st, st->k[0], st->pg_y2, nullptr));
+        a.ghosts = 1;
+        a.tm_glo = st->tm_pgy_lo;
+        a.tm_ghi = st->tm_pgy_hi;
+        a.tm_glo2 = st->tm_pgy2_lo;
+        a.tm_ghi2 = st->tm_pgy2_hi;
+        a.src_lo = st->pg_y;
+        a.src_hi = st->pg_y + 2 * plane_values(st);
+        a.src2_lo = st->pg_y2;
+        a.src2_hi = st->pg_y2 + 2 * plane_values(st);
+    }
+    a.geo = st->geo;
+    a.d1 = st->d1;
+    a.d2 = st->d2;
+    a.F = st->F;
+    a.FK = st->F + st->K;
+    a.inv_h2 = 1.0 / (st->h * st->h);
+    a.zchunk = pick_pair_zchunk(st, 16);
+    CK_CTX(ctx, encode_pair_map(&a.tm_src, st->u, st->geo, (int)st->local));
+    CK_CTX(ctx, encode_pair_map(&a.tm_u, st->k[0], st->geo, (int)st->local));  // k1, the same box
+    a.src = st->u;
+    a.src2 = st->k[0];
+    a.gA = dt * C.a[1][0];
+    a.gB1 = dt * C.a[2][0];
+    a.gB = dt * C.a[2][1];
+    a.out_y = st->k[1];  // k2
+    a.out = st->k[2];    // k3
+    a.dtp = st->gl_dtp;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (st->timing) {
+        e0 = pool_event(st);
+        e1 = pool_event(st);
+        CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+    }
+    CK_CTX(ctx, launch_gs_pair(PAIR_DP_HEAD, a, ctx->stream));
+    if (st->timing) {
+        CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+        st->pending.push_back({e0, e1, 2});
+        if (st->pending.size() > 4096) TRY(resolve_timing(st));
+    }
+    const int64_t pb = 4 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double);
+    st->stats.kernel_launches += 1;
+    st->stats.stage_launches += 1;
+    st->stats.pair_launches += 1;
+    st->stats.rhs_evals += 2;
+    st->stats.stage_bytes += pb;
+    st->stats.pair_bytes += pb;
+    return RK_OK;
+}
+
+static bool dp_head_pair_on() {  // developer A/B knob RKB_DP_HEAD=0 (default on)
+    static int v = -1;
+    if (v < 0) v = getenv("RKB_DP_HEAD") ? atoi(getenv("RKB_DP_HEAD")) : 1;
+    return v != 0;
+}
+
+// Run the stages of one step / try.  Stage 0 (k1 = F(u)) is skipped when k1 is valid.  A DOPRI5
+// try on the K8 schedule: k1 if needed, the head pair (2, 3), stage 4, the write-ahead stage 5,
+// the tail pair (6, 7) -- 23 arrays instead of 30.
 static rk_status run_grid_plan(rk_state st, const std::vector<StagePlan>& plan, double dt,
                                double atol, double rtol) {
     TRY(ensure_k(st, plan_num_k(plan)));
     TRY(ensure_halo(st));
     const bool dp_pair = dp_tail_pair_ok(st, plan);
+    const bool dp_head = dp_pair && dp_head_pair_on();
     for (const StagePlan& p : plan) {
+        if (dp_head && p.stage == 1) {
+            TRY(dp_head_pair(st, dt));
+            continue;
+        }
+        if (dp_head && p.stage == 2) continue;  // in the head pair
         if (dp_pair && p.stage == 5) {  // stages 6 + 7 as one K8 launch
             CK_CTX(st->ctx, cudaMemsetAsync(st->d_err, 0, sizeof(unsigned long long), st->ctx->stream));
             return dp_tail_pair(st, plan, dt, atol, rtol);
@@ -2090,9 +2165,13 @@ static rk_status gloop_build(rk_state st, int scheme, double atol, double rtol) 
     }
     for (int j = 0; j < st->nk; ++j) g->k[j] = st->k[j];
     for (const StagePlan& p : plan) (p.stage == 0 ? g->k1_bytes : g->try_bytes) += plan_stage_bytes(st, p);
-    if (dp_tail_pair_ok(st, plan))  // stages 6 + 7 as the K8 tail pair: 7 arrays instead of their 10
+    if (dp_tail_pair_ok(st, plan)) {  // stages 6 + 7 as the K8 tail pair: 7 arrays instead of their 10
         g->try_bytes += 7 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double) -
                         plan_stage_bytes(st, plan[5]) - plan_stage_bytes(st, plan[6]);
+        if (dp_head_pair_on())  // ... and 2 + 3 as the head pair: 4 instead of 7
+            g->try_bytes += 4 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double) -
+                            plan_stage_bytes(st, plan[1]) - plan_stage_bytes(st, plan[2]);
+    }
     CK_CTX(ctx, cudaMalloc((void**)&g->dev, sizeof(GLoopDev)));
     if (!ctx->capture) CK_CTX(ctx, cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking));
     TRY(ensure_halo(st));                    // ghost buffers / events exist before the capture

@@ -160,7 +160,7 @@ def test_dp_tail_pair_try_bitwise(ctx, dims, dt):
     launches = st.stats()["stage_launches"] - before
     got = st.get()
     assert E == E_o, (E, E_o)
-    assert launches == 6  # k1, stages 2..5, the tail pair
+    assert launches == 5  # k1, the head pair (2, 3), stages 4, 5, the tail pair (6, 7)
     assert bitwise(got, want if acc else u0), first_mismatch(got, want if acc else u0)
     if acc:  # the next try starts from k7 (FSAL): compare its E and result too
         want2, E2_o = dp_oracle_try(dims, want, dt)
@@ -230,7 +230,7 @@ def test_dp_tail_pair_halo_path(ctx, dims):
     after = st.stats()
     assert E == E_o
     assert bitwise(st.get(), want if acc else u0)
-    assert after["halo_exchanges"] - before["halo_exchanges"] == 6  # k1 + stages 2-5 (K3) + the pair
+    assert after["halo_exchanges"] - before["halo_exchanges"] == 6  # k1, head pair (u, k1), 4, 5, tail
     st.set(u0)
     p = oracle.gray_scott_problem(*dims)
     want2, a_o, r_o, rc = oracle.integrate_adaptive(p, OS["dopri5"], u0, 0.0, 12.0, 1.0, 1e-6, 1e-6)

@@ -78,8 +78,9 @@ def test_persistent_small_grid_kernel(sass, s):
 # midpoint and the DOPRI5 tail pair -- TMA-fed, registers only (they sit at the 128-register cap
 # of two 256-thread CTAs per SM, where a spill is the first thing to regress), no FMA in the k-only
 # pairs (the DOPRI5 tail's IEEE division may use DFMA)
-K8 = [("0", "0", "1", "1", "0", "0"), ("1", "1", "1", "0", "0", "0"), ("0", "0", "0", "0", "0", "0"),
-      ("1", "1", "1", "0", "1", "0")]
+K8 = [("0", "0", "1", "1", "0", "0", "0", "0"), ("1", "1", "1", "0", "0", "0", "0", "0"),
+      ("0", "0", "0", "0", "0", "0", "0", "0"), ("1", "1", "1", "0", "1", "0", "0", "0"),
+      ("0", "0", "0", "0", "0", "0", "1", "1")]
 
 
 @pytest.mark.parametrize("flags", K8, ids=lambda f: "".join(f))
