@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define RK_ABI_VERSION 4
+#define RK_ABI_VERSION 5
 #define RK_UNIQUE_ID_BYTES 128
 
 typedef struct rk_ctx_s* rk_ctx;     /* one per rank: device, streams, NCCL communicator */
@@ -219,6 +219,9 @@ typedef struct {
     int64_t pair_launches;    /* of the stage launches: K8 stage-pair launches (ABI 4)    */
     double pair_kernel_ms;    /* ... their share of stage_kernel_ms (RK_OPT_TIMING=1)     */
     int64_t pair_bytes;       /* ... their share of stage_bytes                           */
+    int64_t head_launches;    /* of the pair launches: DOPRI5 head pairs, stages 2 + 3 (ABI 5) */
+    double head_kernel_ms;    /* ... their share of pair_kernel_ms (RK_OPT_TIMING=1)      */
+    int64_t head_bytes;       /* ... their share of pair_bytes                            */
 } rk_stats;
 
 /* ---- library ------------------------------------------------------------------------ */

@@ -18,7 +18,7 @@ OPT_HALO_OVERLAP, OPT_HALO_LOOPBACK, OPT_MAX_TRIES, OPT_TIMING, OPT_USE_GRAPH, O
 OPT_CONTROLLER, OPT_CHECK_FINITE, OPT_COOP_MAX_CELLS = 8, 9, 10
 OPT_FUSED_STEP, OPT_COMM_TIMEOUT_MS, OPT_ERROR_SPIKE, OPT_CHECK_ARGS, OPT_FUSED_KERNELS = 11, 12, 13, 14, 15
 CTRL_ODEINT, CTRL_SPEC = 0, 1
-ABI_VERSION = 4
+ABI_VERSION = 5
 UNIQUE_ID_BYTES = 128
 
 
@@ -38,7 +38,8 @@ class Stats(ctypes.Structure):
                 ("last_err_ratio", ctypes.c_double), ("last_dt", ctypes.c_double),
                 ("stage_bytes", ctypes.c_int64), ("diverged_t", ctypes.c_double),
                 ("pair_launches", ctypes.c_int64), ("pair_kernel_ms", ctypes.c_double),
-                ("pair_bytes", ctypes.c_int64)]
+                ("pair_bytes", ctypes.c_int64), ("head_launches", ctypes.c_int64),
+                ("head_kernel_ms", ctypes.c_double), ("head_bytes", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + hdrs + [os.path.abspath(__file__)]):
-            jobs.append([nvcc(), *NVCC_FLAGS, *inc, "-c", s, "-o", o])
+            jobs.append([nvcc(), *NVCC_FLAGS, *os.environ.get("RKB_NVCC_EXTRA", "").split(), *inc, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

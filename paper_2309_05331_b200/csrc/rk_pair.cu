@@ -170,6 +170,21 @@ __device__ __forceinline__ void rhs_box(const double* v, const double* vm, const
     }
     react(s, ctr, a, f);
 }
+// ... the same with the lower z neighbour from registers (the ring cell's carried values)
+__device__ __forceinline__ void rhs_box_r(const double* v, const double (&vm)[2], const double* vp, int cs, int pitch,
+                                          const PairArgs& a, double (&f)[2]) {
+    double s[2], ctr[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const double* w = v + c * cs;
+        const double cc = w[0];
+        ctr[c] = cc;
+        double q = add(sub(w[-1], cc), sub(w[1], cc));
+        q = add(q, add(sub(w[-pitch], cc), sub(w[pitch], cc)));
+        s[c] = add(q, add(sub(vm[c], cc), sub(vp[c * cs], cc)));
+    }
+    react(s, ctr, a, f);
+}
 
 __device__ __forceinline__ void store_ring(double* p, const GridGeom& G, bool ex0, bool ex1, bool ey0, bool ey1,
                                            double v) {
@@ -380,6 +395,17 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
     // streams u and W (at the 128-register cap) reads it from the ring instead
     constexpr bool YREG = LY::minb == 2 && !U1;
     double ya_q[YREG ? 3 : 1][2][2];
+    // EARLY (= YREG): the ring cells carry their Y_A(t-1) in registers too, so no thread reads
+    // raw plane t-1 in iteration t: its slot is refilled one iteration earlier -- two planes of
+    // TMA lead instead of one (the head pair waited on its ring ~19 % of the time with one:
+    // 2.15 -> 1.98 ms, the DOPRI5 try 9.63 -> 9.46 ms).  The u-fed pairs cannot also carry their own cells' Y_A(t-1): 56-120 B
+    // of spills at the 128-register cap.
+#ifndef RKB_PAIR_EARLY
+#define RKB_PAIR_EARLY 1  // developer A/B (tools/ab_early.sh): 0 off, 1 the head pair only, 2 every
+                          // YREG pair (RK4's first pair: 3.27 -> 3.34 ms, so only the head pair)
+#endif
+    constexpr bool EARLY = YREG && (RKB_PAIR_EARLY == 2 || (RKB_PAIR_EARLY == 1 && HD));
+    double rc_q[EARLY ? 3 : 1][2] = {};
     double yb_q[3][2][2] = {}, ka_q[3][2][2] = {}, u_q[3][2][2] = {};
     double w_q[3][2][2] = {};  // WIN: W at t-1 (stage B's epilogue) and t (loaded one plane ahead)
     auto own_src = [&](int i, double (&v)[2][2]) PINLINE {
@@ -412,9 +438,9 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
         wait(it + 2);
         patch(it + 2);
         __syncthreads();  // plane t+1 (patched) visible; Y_B(t-1) stored; raw plane t-2 free
-        if (tid == 0 && it - 1 >= 0 && it - 1 + R < nr) {
+        if (tid == 0 && (EARLY ? it + R < nr : it - 1 >= 0 && it - 1 + R < nr)) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the patches
-            issue(it - 1 + R);
+            issue(EARLY ? it + R : it - 1 + R);  // raw plane t-1 (EARLY) / t-2 is free
         }
         // own-cell Y_A at t-1, t, t+1 straight from the ring (registers are the scarcer resource)
         double yam[2][2], yac[2][2], yap[2][2];
@@ -498,11 +524,21 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
 #pragma unroll
             for (int c = 0; c < 2; ++c) ybp[r][c] = add(BASE ? uc[r][c] : yac[r][c], mul(cgB, kac[r][c]));
         double yr[2] = {0.0, 0.0};  // Y_B at this thread's ring cell
+        if constexpr (EARLY) {
+            if (hr) {
+                rc_q[Q0][0] = ya[rb];
+                rc_q[Q0][1] = ya[BOX + rb];
+            }
+        }
         if (ring_plane && hr) {
-            const double* ym = reinterpret_cast<const double*>(raw(ic - 1));
             const double* yp = reinterpret_cast<const double*>(raw(ic + 1));
             double kr[2];
-            rhs_box(ya + rb, ym + rb, yp + rb, BOX, BW, a, kr);
+            if constexpr (EARLY) {
+                rhs_box_r(ya + rb, rc_q[QM], yp + rb, BOX, BW, a, kr);
+            } else {
+                const double* ym = reinterpret_cast<const double*>(raw(ic - 1));
+                rhs_box(ya + rb, ym + rb, yp + rb, BOX, BW, a, kr);
+            }
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const double ur = BASE ? reinterpret_cast<const double*>(st + LY::off_u)[c * BCS + rbase] : ya[c * BOX + rb];

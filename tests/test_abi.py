@@ -40,7 +40,7 @@ def test_exports_every_declared_symbol(rk):
 
 
 def test_abi_version(rk):
-    assert rk.lib().rk_abi_version() == 4
+    assert rk.lib().rk_abi_version() == 5
 
 
 @pytest.mark.parametrize("n,world", [(8, 2), (7, 2), (512, 24), (512, 8), (13, 13), (1, 1)])
