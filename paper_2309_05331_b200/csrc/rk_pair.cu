@@ -65,6 +65,9 @@ constexpr int RING_WARPS = RKB_RING_WARPS;                // 3 (32 lanes; measur
 static_assert(NRING % RING_WARPS == 0 && NRING / RING_WARPS <= 32, "ring split");
 constexpr int NPATCH = 36 * BH;                           // source positions used (box cols 1..36)
 constexpr int SMEM_BUDGET = 113 * 1024;                   // 2 CTAs per SM
+#ifndef RKB_PAIR_RU
+#define RKB_PAIR_RU 3  // u ring slots of the u-fed pairs
+#endif
 #ifndef RKB_PAIR_RMAX
 #define RKB_PAIR_RMAX 5  // ring depth cap (6 measured slower: RK4 3.33 vs 3.16 ms)
 #endif
@@ -81,15 +84,19 @@ constexpr int SMEM_BUDGET3 = 72 * 1024;                   // 3 CTAs per SM (u-fe
 template <bool U1, bool YOUT, bool HD = false>
 struct PLayout {
     static constexpr int minb = (!U1 && !YOUT && !HD) ? 3 : 2;
-    static constexpr int stage = HSLOT + (U1 ? USLOT : 0) + (HD ? HSLOT : 0);
-    static constexpr int fixed = (HD ? 1 : 2) * YBSLOT;
+    // U1: u has a ring of its own, RU slots (u(t) is read in one iteration only, so 3 slots
+    // give it two planes of lead while the source ring deepens from 4 to 5 planes)
+    static constexpr int RU = U1 ? RKB_PAIR_RU : 0;
+    static constexpr int stage = HSLOT + (HD ? HSLOT : 0);
+    static constexpr int fixed = (HD ? 1 : 2) * YBSLOT + RU * (USLOT + 8);
     static constexpr int Rb = ((minb == 3 ? SMEM_BUDGET3 : SMEM_BUDGET) - fixed - 64) / stage;
     static constexpr int R = Rb > RKB_PAIR_RMAX ? RKB_PAIR_RMAX : Rb;
     static_assert(R >= 4, "ring too shallow");
-    static constexpr int off_u = HSLOT;
-    static constexpr int yb = R * stage;           // Y_B buffer (2 slots; HD: 1)
-    static constexpr int bar = yb + (HD ? 1 : 2) * YBSLOT;  // R mbarriers
-    static constexpr int smem = bar + R * 8;
+    static constexpr int off_u = HSLOT;            // HD: k_1's box in the same ring stage
+    static constexpr int ur = R * stage;           // U1: the u ring (RU slots)
+    static constexpr int yb = ur + RU * USLOT;     // Y_B buffer (2 slots; HD: 1)
+    static constexpr int bar = yb + (HD ? 1 : 2) * YBSLOT;  // R mbarriers, then RU (U1)
+    static constexpr int smem = bar + (R + RU) * 8;
 };
 
 __device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -272,8 +279,7 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
         uint64_t* b = &bar[i % R];
         const int p = zb - 2 + i;
         const int q = plane(i);
-        const bool mid = i >= 1 && i < nr - 1;  // u feeds Y_B at stage-A planes zb-1 .. ze
-        const uint32_t bytes = 2 * BOX * 8 + ((U1 && mid) ? 2 * UBOX * 8 : 0) + (HD ? 2 * BOX * 8 : 0);
+        const uint32_t bytes = 2 * BOX * 8 + (HD ? 2 * BOX * 8 : 0);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(bytes) : "memory");
         unsigned char* st = raw(i);
         if (a.ghosts && p < 0) tma(st, &a.tm_glo, b, x0 - 2, y0 - 1, p + 2);
@@ -284,13 +290,32 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
             else if (a.ghosts && p >= G.nzl) tma(st + LY::off_u, &a.tm_ghi2, b, x0 - 2, y0 - 1, p - G.nzl);
             else tma(st + LY::off_u, &a.tm_u, b, x0 - 2, y0 - 1, q);
         }
+    };
+    // U1: u(i) (raw index i, the stage-A planes zb-1 .. ze: 1 <= i <= nr-2) into its own ring
+    constexpr int RU = LY::RU > 0 ? LY::RU : 1;
+    auto ubox = [&](int i) PINLINE -> unsigned char* {
+        return U1 ? smem + LY::ur + (size_t)((i - 1) % RU) * USLOT : raw(i) + LY::off_u;  // u(1) -> slot 0
+    };
+    auto issue_u = [&](int i) PINLINE {  // thread 0
         if constexpr (U1) {
-            if (mid) {
-                if (a.ghosts && p < 0) tma(st + LY::off_u, &a.tm_ulo, b, x0, y0, 0);
-                else if (a.ghosts && p >= G.nzl) tma(st + LY::off_u, &a.tm_uhi, b, x0, y0, 0);
-                else tma(st + LY::off_u, &a.tm_u, b, x0, y0, q);
-            }
+            uint64_t* b = &bar[R + (i - 1) % RU];
+            const int p = zb - 2 + i;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(b)), "r"(2 * UBOX * 8)
+                         : "memory");
+            unsigned char* st = ubox(i);
+            if (a.ghosts && p < 0) tma(st, &a.tm_ulo, b, x0, y0, 0);
+            else if (a.ghosts && p >= G.nzl) tma(st, &a.tm_uhi, b, x0, y0, 0);
+            else tma(st, &a.tm_u, b, x0, y0, plane(i));
         }
+    };
+    auto wait_u = [&](int i) PINLINE {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WAITU_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WAITU_%=;\n}" ::"r"(s32(&bar[R + (i - 1) % RU])),
+            "r"((uint32_t)(((i - 1) / RU) & 1))
+            : "memory");
     };
     auto wait = [&](int i) PINLINE {
         asm volatile(
@@ -379,13 +404,15 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
 
     if (tid == 0) {
 #pragma unroll
-        for (int s = 0; s < R; ++s)
+        for (int s = 0; s < R + LY::RU; ++s)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s32(&bar[s])), "r"(1) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (tid == 0)
         for (int i = 0; i < (nr < R ? nr : R); ++i) issue(i);
+    if (U1 && tid == 0)
+        for (int i = 1; i <= RU && i <= nr - 2; ++i) issue_u(i);
 
     // own-cell registers ([q][r][c]: slot q = plane mod 3 within the unrolled loop, row r0 / r1,
     // component): Y_A at planes t-1, t, t+1; Y_B at t-2, t-1, t; k_A at t-1 (for the epilogue)
@@ -442,6 +469,7 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the patches
             issue(EARLY ? it + R : it - 1 + R);  // raw plane t-1 (EARLY) / t-2 is free
         }
+        if (U1 && tid == 0 && it >= 1 && it + RU <= nr - 2) issue_u(it + RU);  // u(t-1)'s slot is free
         // own-cell Y_A at t-1, t, t+1 straight from the ring (registers are the scarcer resource)
         double yam[2][2], yac[2][2], yap[2][2];
         if constexpr (YREG) {
@@ -512,7 +540,8 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
         double (&uc)[2][2] = u_q[Q0];
         const double (&up)[2][2] = u_q[QM];
         if constexpr (BASE) {
-            const double* U = reinterpret_cast<const double*>(st + LY::off_u);
+            if constexpr (U1) wait_u(ic);
+            const double* U = reinterpret_cast<const double*>(ubox(ic));
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 uc[r][0] = U[pbase + r * BPITCH];
@@ -541,7 +570,7 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
             }
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const double ur = BASE ? reinterpret_cast<const double*>(st + LY::off_u)[c * BCS + rbase] : ya[c * BOX + rb];
+                const double ur = BASE ? reinterpret_cast<const double*>(ubox(ic))[c * BCS + rbase] : ya[c * BOX + rb];
                 yr[c] = add(ur, mul(cgB, kr[c]));
             }
         }
