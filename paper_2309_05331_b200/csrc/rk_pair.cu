@@ -370,19 +370,20 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
         }
     };
     // HD: after the patches, Y_A = u + (dt a_21) k_1 in place of u and Z = u + (dt a_31) k_1 in
-    // place of k_1, at every box position stage A or Y_B reads (columns 1..36)
+    // place of k_1, at every box position stage A or Y_B reads
     auto form = [&](int i) PINLINE {
         if constexpr (HD) {
             if (edge) __syncthreads();  // patched cells (written by other threads) visible
-            double* y = reinterpret_cast<double*>(raw(i));
-            double* k = reinterpret_cast<double*>(raw(i) + LY::off_u);
-            for (int q = tid; q < NPATCH; q += PNT) {
-                const int pos = (q / 36) * BW + 1 + q % 36;
+            // 16-byte pairs over the whole box (columns 0 and 37 are formed too and never read)
+            double2* y = reinterpret_cast<double2*>(raw(i));
+            double2* k = reinterpret_cast<double2*>(raw(i) + LY::off_u);
+            static_assert(BW % 2 == 0 && (BOX * 8) % 16 == 0 && LY::off_u % 16 == 0, "16-byte pairs");
+            for (int q = tid; q < BOX / 2; q += PNT) {
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    const double uu = y[c * BOX + pos], kk = k[c * BOX + pos];
-                    y[c * BOX + pos] = add(uu, mul(cgA, kk));
-                    k[c * BOX + pos] = add(uu, mul(cgB1, kk));
+                    const double2 uu = y[c * (BOX / 2) + q], kk = k[c * (BOX / 2) + q];
+                    y[c * (BOX / 2) + q] = make_double2(add(uu.x, mul(cgA, kk.x)), add(uu.y, mul(cgA, kk.y)));
+                    k[c * (BOX / 2) + q] = make_double2(add(uu.x, mul(cgB1, kk.x)), add(uu.y, mul(cgB1, kk.y)));
                 }
             }
         }
