@@ -49,7 +49,8 @@ namespace {
 constexpr int PX = 32;    // tile width (one warp per row pair)
 constexpr int PTH = 16;   // tile height: 8 warps x 2 adjacent rows
 constexpr int PNT = 256;  // threads
-constexpr int BW = PX + 6;   // source box: cells x0-3 .. x0+34 (padded column x0-2: 16-byte start)
+constexpr int BW = PX + 6;   // source box: cells x0-3 .. x0+34 (padded column x0-2: 16-byte start;
+                             // a 36-wide box at x0-2 (8-byte start) faults: illegal instruction)
 constexpr int BH = PTH + 4;  // rows y0-2 .. y0+17
 constexpr int BOX = BW * BH;
 constexpr int HSLOT = (2 * BOX * 8 + 127) / 128 * 128;  // 12160 B

@@ -54,7 +54,7 @@ def main(tag, out):
     open(os.path.join(out, f"{tag}_warm_dram.txt"), "w").write(sn.warm(os.path.join(g, f"tune_{tag}.csv")) + "\n")
     traffic = {"_source": f"{tag} (tools/profile_round.sh): dram__bytes_read.sum + dram__bytes_write.sum per "
                           "stage launch of one step, cold L2 (ncu default cache control); adaptive (one "
-                          "DOPRI5 try: 4 K3 stages + the K8 tail pair), rk4 (K8, 2 launches) and rk4_k3 from ncu --set full captures, the other legs "
+                          "DOPRI5 try: the K8 head pair, K3 stages 4 and 5, the K8 tail pair), rk4 (K8, 2 launches) and rk4_k3 from ncu --set full captures, the other legs "
                           "from metrics-only captures; abm legs: the PEC launch plus rk4's k1-type launch"}
     rk4_first = None
     for leg in ("adaptive", "rk4", "rk4_k3"):

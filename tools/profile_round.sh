@@ -4,7 +4,7 @@
 #   DOPRI5 try and one RK4 step, dram bytes of one step of every other scheme leg.
 #   Summaries are written on the box (tools/make_profiles.py) into gpurun_out/profiles_TAG/;
 #   the bulky .ncu-rep files are deleted there except the DOPRI5 one (gpurun returns <= 64 MiB).
-TAG=${1:-r2_v3}
+TAG=${1:-r2_v4}
 O=gpurun_out
 LEGS=adaptive,rk4,rk4_k3,repeats,try_loop,device_loop,halo,exposed,strong_emul,rk4_native,rk4_k6,midpoint_k6,midpoint_k3,exp512,small,e2e,cpu,cpu_full,euler,midpoint,modified_midpoint,cash_karp54,dopri5,rkf78,ab1,ab2,ab4,ab8,abm1,abm2,abm4,abm8
 timeout 1200 python bench.py --legs $LEGS > $O/${TAG}_bench.log 2>&1
@@ -21,8 +21,9 @@ dram() {  # leg, kernel regex, skip, count: cold-L2 dram bytes per launch (csv)
       --clock-control none --kernel-name-base demangled -k "regex:$2" -s $3 -c $4 --csv \
       --log-file $O/${TAG}_dram_$1.csv python bench.py --legs $1 --steps 2 --warmup 3 > $O/${TAG}_dram_$1.log 2>&1
 }
-# one DOPRI5 try = 4 stage launches (K3) + the tail pair (K8); skip k1 + 6 tries
-full adaptive "gs_stage_kernel|gs_pair_kernel" 31 5
+# one DOPRI5 try = the K8 head pair (stages 2 + 3), K3 stages 4 and 5, the K8 tail pair (6 + 7);
+# skip the first try's k1 + 6 tries
+full adaptive "gs_stage_kernel|gs_pair_kernel" 25 4
 # RK4: K8 (2 pair launches per step, the default) and K3 (4 stage launches)
 full rk4 "gs_pair_kernel" 6 2
 full rk4_k3 "gs_stage_kernel" 12 4
