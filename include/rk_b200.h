@@ -158,9 +158,10 @@ typedef enum {
                                 ny % 16 == 0, other grids run the stage-by-stage kernels;
                                 Gragg's modified midpoint is pair (1, 2) + its last stage; on the NCCL multi-GPU slab the pairs'
                                 2-deep ghost planes are exchanged before each pair (the P2P
-                                transport keeps the stage-by-stage kernels); with 3 the last
-                                two stages of every error-controlled DOPRI5 try are one K8
-                                launch too.  1 (one GPU, no halo path): K6, the whole step in ONE launch
+                                transport keeps the stage-by-stage kernels); with 3 stages 2 + 3
+                                and the last two stages of every error-controlled DOPRI5 try
+                                are one K8 launch each (the head and the tail pair: a try is
+                                4 launches, 384 B/cell instead of 432).  1 (one GPU, no halo path): K6, the whole step in ONE launch
                                 with every stage value on chip (32 B/cell).  2: K7, K6 with
                                 warp-specialised stage groups.  K6 and K7 are ablations, slower
                                 than K8 and K3 on the B200.  0: stage-by-stage launches (K3). */

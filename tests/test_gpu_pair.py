@@ -138,7 +138,8 @@ def test_pair_integrate_const_and_graph(ctx):
     assert bitwise(got, want)
 
 
-# ---- DOPRI5 error-controlled tail pair (PAIR_DP_TAIL: stages 6 + 7 in one launch) ----------
+# ---- DOPRI5 pairs: the head pair (PAIR_DP_HEAD: stages 2 + 3) and the error-controlled tail
+# pair (PAIR_DP_TAIL: stages 6 + 7), one launch each ----------------------------------------
 def dp_oracle_try(dims, u0, dt, tol=1e-6):
     p = oracle.gray_scott_problem(*dims)
     un, err = oracle.step(p, OS["dopri5"], 0.0, dt, u0, with_error=True)
@@ -155,12 +156,17 @@ def test_dp_tail_pair_try_bitwise(ctx, dims, dt):
     u0 = perturbed_ic(*dims)
     want, E_o = dp_oracle_try(dims, u0, dt)
     st = pair_state(ctx, dims, u0)
-    before = st.stats()["stage_launches"]
+    s0 = st.stats()
     acc, E, _ = st.try_step("dopri5", 0.0, dt, 1e-6, 1e-6)
-    launches = st.stats()["stage_launches"] - before
+    s1 = st.stats()
+    launches = s1["stage_launches"] - s0["stage_launches"]
     got = st.get()
     assert E == E_o, (E, E_o)
     assert launches == 5  # k1, the head pair (2, 3), stages 4, 5, the tail pair (6, 7)
+    assert s1["pair_launches"] - s0["pair_launches"] == 2 and s1["head_launches"] - s0["head_launches"] == 1
+    cells = dims[0] * dims[1] * dims[2]
+    assert s1["head_bytes"] - s0["head_bytes"] == 4 * 16 * cells  # u, k1 -> k2, k3 (ABI 5)
+    assert s1["pair_bytes"] - s0["pair_bytes"] == (4 + 7) * 16 * cells
     assert bitwise(got, want if acc else u0), first_mismatch(got, want if acc else u0)
     if acc:  # the next try starts from k7 (FSAL): compare its E and result too
         want2, E2_o = dp_oracle_try(dims, want, dt)
