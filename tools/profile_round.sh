@@ -30,7 +30,7 @@ full rk4_k3 "gs_stage_kernel" 12 4
 dram euler "gs_stage_kernel" 3 1
 dram midpoint "gs_pair_kernel" 3 1
 dram midpoint_k3 "gs_stage_kernel" 6 2
-dram modified_midpoint "gs_stage_kernel" 9 3
+dram modified_midpoint "gs_stage_kernel|gs_pair_kernel" 6 2
 dram cash_karp54 "gs_stage_kernel" 18 6
 dram dopri5 "gs_stage_kernel" 18 6
 dram rkf78 "gs_stage_kernel" 39 13

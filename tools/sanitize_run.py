@@ -56,7 +56,8 @@ for fused in (0, 1) if "k3k6" in SECTIONS else ():
 # SAN_NO_GRAPH=1 skips the device-resident graph loop (conditional graph nodes crash the
 # racecheck tool's host side; memcheck / synccheck / initcheck run them)
 R2 = ((1, 0, 1), (1, 1, 1), (0, 1, 1), (0, 0, 0))
-if os.environ.get("SAN_NO_GRAPH") == "1":
+NO_GRAPH = os.environ.get("SAN_NO_GRAPH") == "1"
+if NO_GRAPH:
     R2 = tuple(v for v in R2 if v[1] == 0)
 for p2p, dl, fk in R2 if "r2" in SECTIONS else ():
     mark(f"r2 p2p={p2p} device_loop={dl} fused_kernels={fk}")
@@ -72,8 +73,8 @@ for p2p, dl, fk in R2 if "r2" in SECTIONS else ():
     st.integrate_adaptive("cash_karp54", 6.0, 8.0, 1.0, 1e-6, 1e-6)
     st.get()
     st.close()
-# K8 stage pairs (tile-aligned grid: RK4 pairs, the explicit midpoint pair, the DOPRI5 tail pair
-# inside error-controlled tries), several z chunks so chunk edges and the edge-CTA patch list run
+# K8 stage pairs (tile-aligned grid: RK4 pairs, the explicit midpoint pair, Gragg's pair, the
+# DOPRI5 head and tail pairs inside error-controlled tries and the device-resident try loop), several z chunks so chunk edges and the edge-CTA patch list run
 if "k8" in SECTIONS:
     mark("k8")
     os.environ["RKB_PZ"] = "5"
@@ -81,10 +82,14 @@ if "k8" in SECTIONS:
     st.set_rhs_gray_scott()
     st.set_option(rk.OPT_COOP_MAX_CELLS, 0)
     st.set(rk_inputs.gray_scott_ic(64, 32, 11, seed=6))
-    for s in ("rk4", "midpoint", "rk4"):
+    for s in ("rk4", "midpoint", "modified_midpoint", "rk4"):
         st.do_step(s, 0.0, 1.0)
-    for k in range(3):
+    for k in range(3):  # the head pair (stages 2 + 3) and the tail pair (6 + 7) of every try
         st.try_step("dopri5", float(k), 0.5, 1e-6, 1e-6)
+    if not NO_GRAPH:  # the device-resident graph try loop: the pairs' device-dt (DTP) variants
+        st.set_option(rk.OPT_DEVICE_LOOP, 1)
+        st.integrate_adaptive("dopri5", 0.0, 2.0, 0.5, 1e-6, 1e-6)
+        st.set_option(rk.OPT_DEVICE_LOOP, 0)
     st.get()
     st.close()
     if not NO_NCCL:  # the pairs on the slab path: ghost planes through the 1-rank NCCL loopback
