@@ -185,11 +185,14 @@ static bool drain_stream(rk_ctx ctx, cudaStream_t s) {
     return true;
 }
 
+// Every API call runs on its context's device, from any host thread: cudaSetDevice also binds the
+// device's primary context to a thread that has made no CUDA call yet, which the driver-API calls
+// (cuTensorMapEncodeTiled) need -- cudaGetDevice alone reports device 0 there without binding it.
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
         cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
+        cudaSetDevice(dev);
     }
     ~DeviceGuard() {
         int cur = -1;
