@@ -425,12 +425,8 @@ template <int S>
 cudaError_t launch_fused_t(const GsFusedArgs& a, cudaStream_t st) {
     static_assert(chained(S), "K6 needs a chained-stage tableau");
     constexpr int bytes = FCfg<S>::smem;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gs_fused_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> configured{0};
+    if (cudaError_t e = smem_attr_once(configured, gs_fused_kernel<S>, bytes); e != cudaSuccess) return e;
     const int ntx = (a.geo.nx + FX - 1) / FX, nty = (a.geo.ny + FY - 1) / FY;
     const int nch = (a.geo.nzl + a.zchunk - 1) / a.zchunk;
     gs_fused_kernel<S><<<dim3((unsigned)(ntx * nty), (unsigned)nch), FNT, bytes, st>>>(a);

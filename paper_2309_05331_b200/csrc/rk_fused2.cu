@@ -429,12 +429,8 @@ template <int S>
 cudaError_t launch_ws_t(const GsFusedArgs& a, cudaStream_t st) {
     static_assert(k7_chained(S), "K7 needs a chained-stage tableau");
     constexpr int bytes = KCfg<S>::smem;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gs_ws_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> configured{0};
+    if (cudaError_t e = smem_attr_once(configured, gs_ws_kernel<S>, bytes); e != cudaSuccess) return e;
     const int ntx = (a.geo.nx + KX - 1) / KX, nty = (a.geo.ny + KY - 1) / KY;
     const int nch = (a.geo.nzl + a.zchunk - 1) / a.zchunk;
     gs_ws_kernel<S><<<dim3((unsigned)(ntx * nty), (unsigned)nch), KNT, bytes, st>>>(a);

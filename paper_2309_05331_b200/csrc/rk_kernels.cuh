@@ -7,11 +7,25 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "rk_stage_spec.h"
 
 namespace rkb {
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize once per kernel instance AND device: function
+// attributes live in the device's context, so a process driving a second device sets them again.
+template <typename K>
+inline cudaError_t smem_attr_once(std::atomic<unsigned long long>& done, K* kernel, int bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit);
+    return e;
+}
 
 enum RhsKind { RHS_NONE = -1, RHS_EXP = 0, RHS_LOGISTIC = 1, RHS_GRAY_SCOTT = 2 };
 

@@ -675,13 +675,10 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
 template <bool U1, bool WIN, bool BA, bool YOUT, bool DP = false, bool DTP = false, bool KK = false, bool HD = false>
 cudaError_t launch_pair_t(const PairArgs& a, cudaStream_t st) {
     using LY = PLayout<U1, YOUT, HD>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gs_pair_kernel<U1, WIN, BA, YOUT, DP, DTP, KK, HD>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, LY::smem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> configured{0};
+    if (cudaError_t e = smem_attr_once(configured, gs_pair_kernel<U1, WIN, BA, YOUT, DP, DTP, KK, HD>, LY::smem);
+        e != cudaSuccess)
+        return e;
     const int tiles = (a.geo.nx / PX) * (a.geo.ny / PTH);
     const int nch = (a.geo.nzl + a.zchunk - 1) / a.zchunk;
     gs_pair_kernel<U1, WIN, BA, YOUT, DP, DTP, KK, HD><<<dim3((unsigned)tiles, (unsigned)nch), PNT, LY::smem, st>>>(a);

@@ -670,13 +670,8 @@ cudaError_t launch_one(const GsStageArgs& a, dim3 grid, cudaStream_t st) {
     constexpr StageSpec P = stage_spec(S, AD, I);
     static_assert(P.valid, "invalid stage");
     constexpr int bytes = layout_of<kRows<S, AD, I>>(P).smem;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gs_stage_kernel<S, AD, I>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    static std::atomic<unsigned long long> configured{0};
+    if (cudaError_t e = smem_attr_once(configured, gs_stage_kernel<S, AD, I>, bytes); e != cudaSuccess) return e;
     gs_stage_kernel<S, AD, I><<<grid, NT, bytes, st>>>(a);
     return cudaGetLastError();
 }
