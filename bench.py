@@ -679,14 +679,23 @@ def main():
             outs.append(torch.empty_like(host_in).pin_memory())
         accs = [0, 0]
         # one integration on the GPU at a time: the other pipeline's D2H + H2D run on the copy
-        # engines meanwhile, so the GPU never waits on PCIe and two integrations never split it
-        gpu_turn = threading.Lock()
+        # engines meanwhile, so the GPU never waits on PCIe and two integrations never split it.
+        # The pipelines take strict turns (0, 1, 0, 1, ...), the same order on every rank: with
+        # N > 1 each integration runs collectives on its own context's communicator, and a
+        # first-come lock could hand rank 0's GPU to pipeline 0 and rank 1's to pipeline 1 --
+        # each waiting in a collective for a peer that waits for the lock.
+        turn = [0]
+        cv = threading.Condition()
 
         def work(i, k):
             for _ in range(k):
                 sts[i].set(host_in)
-                with gpu_turn:
-                    a, _ = sts[i].integrate_adaptive("dopri5", 0.0, T1, 1.0, TOL, TOL)
+                with cv:
+                    cv.wait_for(lambda: turn[0] % 2 == i)
+                a, _ = sts[i].integrate_adaptive("dopri5", 0.0, T1, 1.0, TOL, TOL)
+                with cv:
+                    turn[0] += 1
+                    cv.notify_all()
                 sts[i].get(outs[i])
                 accs[i] += a
 
