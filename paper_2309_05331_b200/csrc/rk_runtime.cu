@@ -1070,13 +1070,15 @@ static rk_status dp_tail_pair(rk_state st, const std::vector<StagePlan>& plan, d
     return RK_OK;
 }
 
-// K8 DOPRI5 head pair (PAIR_DP_HEAD): stages 2 and 3 of a try in one launch -- u and k1 (both
+// K8 head pair (PAIR_DP_HEAD): stages 2 and 3 of a step or try in one launch -- u and k1 (both
 // with 2-cell margins; Y2 = u + (dt a21) k1 and Z3 = u + (dt a31) k1 formed in shared memory as
-// they land) -> k2, k3 with their rings: 4 arrays instead of stages 2 + 3's 7
-static rk_status dp_head_pair(rk_state st, double dt) {
-    NvtxRange nv("rk stage pair (K8 DOPRI5 stages 2-3)");
+// they land) -> k2, k3 with their rings: 4 arrays instead of stages 2 + 3's 7.  Built for the
+// DOPRI5 try; it serves every tableau whose stages 2 and 3 are plain slope stages with a21, a31,
+// a32 != 0 (head_pair_ok: Cash–Karp 5(4), Dormand–Prince fixed and error-controlled, RKF 7(8)).
+static rk_status dp_head_pair(rk_state st, int scheme, double dt) {
+    NvtxRange nv("rk stage pair (K8 head: stages 2-3)");
     rk_ctx ctx = st->ctx;
-    const Coeffs C = coeffs_of(RK_DOPRI5);
+    const Coeffs C = coeffs_of(scheme);
     PairArgs a{};
     if (halo_path(st)) {  // u's and k1's two boundary planes each side
         TRY(pair_ghost_buffers(st));
@@ -1139,6 +1141,26 @@ static bool dp_head_pair_on() {  // developer A/B knob RKB_DP_HEAD=0 (default on
     return v != 0;
 }
 
+// Whether the head pair can take stages 2 and 3 (indices 1, 2) of this plan: one GPU or the NCCL
+// slab path (as the tail pair), and plan stages 0..2 the plain slope stages k1 -> k[0],
+// Y2 = u + a21 k1 -> k[1], Y3 = (u + a31 k1) + a32 k2 -> k[2] with nonzero a21, a31, a32 (the
+// kernel's expressions), followed by at least one more stage.
+static bool head_pair_ok(rk_state st, const std::vector<StagePlan>& plan) {
+    if (!dp_head_pair_on() || st->fused != 3 || !st->grid || st->ncomp != 2 || st->rhs != RHS_GRAY_SCOTT ||
+        st->p2p || !pair_shape_ok(st->geo) || plan.size() < 4 || is_multistep(plan[0].scheme))
+        return false;
+    if (halo_path(st) && (!st->ctx->nccl || st->local < 2)) return false;
+    const StageSpec& s0 = plan[0].sp;
+    const StageSpec& s1 = plan[1].sp;
+    const StageSpec& s2 = plan[2].sp;
+    auto plain = [](const StagePlan& p) {
+        return p.sp.epi == EPI_K && p.sp.base_src < 0 && !p.sp.base_unew && p.out_hist < 0 && !p.out_ptr;
+    };
+    return plain(plan[0]) && plain(plan[1]) && plain(plan[2]) && s0.out_k == 0 && s0.nslots == 0 &&
+           s1.out_k == 1 && s1.nslots == 1 && s1.src[0] == 0 && s1.gnz[0] && s2.out_k == 2 && s2.nslots == 2 &&
+           s2.src[0] == 0 && s2.src[1] == 1 && s2.gnz[0] && s2.gnz[1];
+}
+
 // Run the stages of one step / try.  Stage 0 (k1 = F(u)) is skipped when k1 is valid.  A DOPRI5
 // try on the K8 schedule: k1 if needed, the head pair (2, 3), stage 4, the write-ahead stage 5,
 // the tail pair (6, 7) -- 23 arrays instead of 30.
@@ -1147,10 +1169,10 @@ static rk_status run_grid_plan(rk_state st, const std::vector<StagePlan>& plan, 
     TRY(ensure_k(st, plan_num_k(plan)));
     TRY(ensure_halo(st));
     const bool dp_pair = dp_tail_pair_ok(st, plan);
-    const bool dp_head = dp_pair && dp_head_pair_on();
+    const bool dp_head = head_pair_ok(st, plan);
     for (const StagePlan& p : plan) {
         if (dp_head && p.stage == 1) {
-            TRY(dp_head_pair(st, dt));
+            TRY(dp_head_pair(st, p.scheme, dt));
             continue;
         }
         if (dp_head && p.stage == 2) continue;  // in the head pair
@@ -2171,13 +2193,12 @@ static rk_status gloop_build(rk_state st, int scheme, double atol, double rtol) 
     }
     for (int j = 0; j < st->nk; ++j) g->k[j] = st->k[j];
     for (const StagePlan& p : plan) (p.stage == 0 ? g->k1_bytes : g->try_bytes) += plan_stage_bytes(st, p);
-    if (dp_tail_pair_ok(st, plan)) {  // stages 6 + 7 as the K8 tail pair: 7 arrays instead of their 10
+    if (dp_tail_pair_ok(st, plan))  // stages 6 + 7 as the K8 tail pair: 7 arrays instead of their 10
         g->try_bytes += 7 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double) -
                         plan_stage_bytes(st, plan[5]) - plan_stage_bytes(st, plan[6]);
-        if (dp_head_pair_on())  // ... and 2 + 3 as the head pair: 4 instead of 7
-            g->try_bytes += 4 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double) -
-                            plan_stage_bytes(st, plan[1]) - plan_stage_bytes(st, plan[2]);
-    }
+    if (head_pair_ok(st, plan))  // 2 + 3 as the head pair: 4 arrays instead of 7
+        g->try_bytes += 4 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double) -
+                        plan_stage_bytes(st, plan[1]) - plan_stage_bytes(st, plan[2]);
     CK_CTX(ctx, cudaMalloc((void**)&g->dev, sizeof(GLoopDev)));
     if (!ctx->capture) CK_CTX(ctx, cudaStreamCreateWithFlags(&ctx->capture, cudaStreamNonBlocking));
     TRY(ensure_halo(st));                    // ghost buffers / events exist before the capture

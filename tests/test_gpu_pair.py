@@ -346,3 +346,74 @@ def test_pair_mixed_sequence_equals_stage_kernels(ctx, loopback):
     assert t3 == t0
     for i, (a, b) in enumerate(zip(g3, g0)):
         assert bitwise(a, b), (i, first_mismatch(a, b))
+
+
+# ---- the head pair (stages 2 + 3) on every tableau that admits it: Cash–Karp 5(4), Dormand–Prince
+# fixed step and error-controlled (both ratio readings), RKF 7(8) -------------------------------
+HEAD_CASES = [("cash_karp54", 0), ("cash_karp54", 1), ("dopri5", 0), ("rkf78", 0), ("rkf78", 1)]
+
+
+@pytest.mark.parametrize("dims", [(32, 16, 1), (64, 32, 9), (96, 48, 20)], ids=lambda d: "x".join(map(str, d)))
+@pytest.mark.parametrize("case", HEAD_CASES, ids=lambda c: f"{c[0]}-{'try' if c[1] else 'step'}")
+def test_head_pair_schemes_bitwise(ctx, case, dims):
+    """Stages 2 + 3 as one K8 launch for every eligible tableau: bitwise vs the oracle, one head
+    launch per step / try, 4 arrays instead of 7."""
+    name, adaptive = case
+    u0 = perturbed_ic(*dims, seed=21)
+    p = oracle.gray_scott_problem(*dims)
+    st = pair_state(ctx, dims, u0)
+    s0 = st.stats()
+    if adaptive:
+        acc, E, _ = st.try_step(name, 0.0, 1.0, 1e-6, 1e-6)
+        un, err = oracle.step(p, OS[name], 0.0, 1.0, u0, with_error=True)
+        assert E == oracle.error_ratio_max(err, u0, oracle.rhs(p, u0), 1.0, 1e-6, 1e-6)
+        want = un if acc else u0
+    else:
+        st.do_step(name, 0.0, 1.0)
+        want = oracle.step(p, OS[name], 0.0, 1.0, u0)
+    s1 = st.stats()
+    got = st.get()
+    st.close()
+    assert bitwise(got, want), first_mismatch(got, want)
+    assert s1["head_launches"] - s0["head_launches"] == 1
+    cells = dims[0] * dims[1] * dims[2]
+    assert s1["head_bytes"] - s0["head_bytes"] == 4 * 16 * cells
+
+
+@pytest.mark.parametrize("name", ["cash_karp54", "rkf78"])
+def test_head_pair_integrate_adaptive_counts(ctx, name):
+    """A whole error-controlled integration with the head pair in every try: accepted / rejected
+    counts identical to the oracle's, final state bitwise."""
+    dims = (64, 32, 12)
+    u0 = perturbed_ic(*dims, seed=8)
+    p = oracle.gray_scott_problem(*dims)
+    want, a_o, r_o, rc = oracle.integrate_adaptive(p, OS[name], u0, 0.0, 10.0, 1.0, 1e-6, 1e-6)
+    assert rc == 0
+    st = pair_state(ctx, dims, u0)
+    a, r = st.integrate_adaptive(name, 0.0, 10.0, 1.0, 1e-6, 1e-6)
+    got = st.get()
+    heads = st.stats()["head_launches"]
+    st.close()
+    assert (a, r) == (a_o, r_o)
+    assert heads == a + r
+    assert bitwise(got, want), first_mismatch(got, want)
+
+
+@pytest.mark.parametrize("dims", [(64, 32, 2), (64, 32, 7)], ids=lambda d: "x".join(map(str, d)))
+def test_head_pair_halo_path_ck54(ctx, dims):
+    """The head pair on the slab path (one-GPU loopback through the 1-rank NCCL communicator):
+    u's and k1's two boundary planes each side exchanged before the launch; bitwise."""
+    import paper_2309_05331_b200 as rk
+    u0 = perturbed_ic(*dims, seed=5)
+    p = oracle.gray_scott_problem(*dims)
+    un, err = oracle.step(p, OS["cash_karp54"], 0.0, 2.0, u0, with_error=True)
+    E_o = oracle.error_ratio_max(err, u0, oracle.rhs(p, u0), 2.0, 1e-6, 1e-6)
+    st = pair_state(ctx, dims, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+    acc, E, _ = st.try_step("cash_karp54", 0.0, 2.0, 1e-6, 1e-6)
+    heads = st.stats()["head_launches"]
+    got = st.get()
+    st.close()
+    assert E == E_o
+    assert heads == 1
+    assert bitwise(got, un if acc else u0), first_mismatch(got, un if acc else u0)
