@@ -151,7 +151,9 @@ struct GsStageArgs {
     double delta[kMaxSlots];         // dt*e_j per slot
     double beta_new, delta_new;      // weights of the k_i computed by this stage
     double g2[kMaxSlots], g2_new;    // EPI_AHEAD: dt*a_Fj per slot and dt*a_Fi (final stage F)
+    double g3[kMaxSlots], g3_new;    // EPI_AHEAD with out_z (fixed-step tail pair): dt*a_Lj, dt*a_Li
     double* out_w;                   // EPI_AHEAD: partial final combination W
+    double* out_z;                   // EPI_AHEAD with out_z: the last stage's base Z_L (ring)
     double* out_e;                   // EPI_AHEAD (error control): partial error sum E
     double* out_k;
     double* out_u;
@@ -278,7 +280,8 @@ struct PairArgs {
     double d1, d2, F, FK, inv_h2;
     int zchunk;
 };
-enum { PAIR_FIRST = 0, PAIR_LAST = 1, PAIR_ONLY = 2, PAIR_DP_TAIL = 3, PAIR_DP_HEAD = 4 };
+// PAIR_LAST_NOA: PAIR_LAST without the beta_A term (b_A = 0: Cash–Karp's b_5)
+enum { PAIR_FIRST = 0, PAIR_LAST = 1, PAIR_ONLY = 2, PAIR_DP_TAIL = 3, PAIR_DP_HEAD = 4, PAIR_LAST_NOA = 5 };
 bool pair_shape_ok(const GridGeom& g);  // nx % 32 == 0, ny % 16 == 0
 cudaError_t encode_pair_map(CUtensorMap* map, const double* base, const GridGeom& g, int nplanes);
 cudaError_t launch_gs_pair(int kind, const PairArgs& a, cudaStream_t st);

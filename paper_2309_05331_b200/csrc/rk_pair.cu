@@ -714,6 +714,7 @@ cudaError_t launch_gs_pair(int kind, const PairArgs& a, cudaStream_t st) {
     case PAIR_FIRST: return launch_pair_t<false, false, true, true>(a, st);  // RK4 1-2: u -> Y3, W
     case PAIR_LAST: return launch_pair_t<true, true, true, false>(a, st);    // RK4 3-4: Y3, u, W -> u_new
     case PAIR_ONLY: return launch_pair_t<false, false, false, false>(a, st); // midpoint: u -> u_new
+    case PAIR_LAST_NOA: return launch_pair_t<true, true, false, false>(a, st);  // b_A = 0 (CK54's tail)
     case PAIR_DP_HEAD:  // DOPRI5 stages 2-3: u, k1 -> k2, k3
         return a.dtp ? launch_pair_t<false, false, false, false, false, true, true, true>(a, st)
                      : launch_pair_t<false, false, false, false, false, false, true, true>(a, st);

@@ -415,22 +415,25 @@ struct StagePlan {
     double g[kMaxSlots] = {0}, beta[kMaxSlots] = {0}, delta[kMaxSlots] = {0};
     double beta_new = 0.0, delta_new = 0.0;
     double g2[kMaxSlots] = {0}, g2_new = 0.0;  // EPI_AHEAD: the final stage's a_Fj (x dt)
+    double g3[kMaxSlots] = {0}, g3_new = 0.0;  // EPI_AHEAD with out_z: the last stage's a_Lj (x dt)
     int out_hist = -1;  // >= 0: the stage writes its k into Adams–Bashforth history slot
     double* out_ptr = nullptr;  // non-null: the stage's k goes here (rk_eval_rhs)
 };
 
 // adaptive: 0 fixed step, 1 error-controlled (Odeint ratio, R-12), 2 error-controlled (SPEC
 // ratio, R-28)
+// adaptive == 5: a fixed step whose last two stages run as one K8 pair (fixed_tail_pair): the
+// plan holds stages 0 .. L-2, the last of them the write-ahead stage with Z_L (stage_spec ad 5)
 static std::vector<StagePlan> build_plan(int scheme, int adaptive, double dt) {
     const Coeffs C = coeffs_of(scheme);
     std::vector<StagePlan> plan;
-    const int n = num_stages(scheme, adaptive);
+    const int n = adaptive == 5 ? last_stage(tableau_of(scheme), false) - 1 : num_stages(scheme, adaptive);
     for (int i = 0; i < n; ++i) {
         StagePlan p;
         p.scheme = scheme;
-        p.adaptive = adaptive;
+        p.adaptive = adaptive == 5 && i < n - 1 ? 0 : adaptive;
         p.stage = i;
-        p.sp = stage_spec(scheme, adaptive, i);
+        p.sp = stage_spec(scheme, p.adaptive, i);
         for (int s = 0; s < p.sp.nslots; ++s) {
             const int j = p.sp.j[s];
             p.g[s] = p.sp.gnz[s] ? dt * C.a[i][j] : 0.0;
@@ -442,6 +445,10 @@ static std::vector<StagePlan> build_plan(int scheme, int adaptive, double dt) {
         if (p.sp.epi == EPI_AHEAD) {
             for (int s = 0; s < p.sp.nslots; ++s) p.g2[s] = p.sp.anz2[s] ? dt * C.a[i + 1][p.sp.j[s]] : 0.0;
             p.g2_new = p.sp.a2new ? dt * C.a[i + 1][i] : 0.0;
+            if (p.sp.out_z >= 0) {
+                for (int s = 0; s < p.sp.nslots; ++s) p.g3[s] = p.sp.anz3[s] ? dt * C.a[i + 2][p.sp.j[s]] : 0.0;
+                p.g3_new = p.sp.a3new ? dt * C.a[i + 2][i] : 0.0;
+            }
         }
         plan.push_back(p);
     }
@@ -452,7 +459,7 @@ static int plan_num_k(const std::vector<StagePlan>& plan) {
     int nk = 0;
     for (auto& p : plan) {
         if (p.sp.out_k >= 0) nk = std::max(nk, p.sp.out_k + 1);
-        nk = std::max(nk, std::max(p.sp.out_w, std::max(p.sp.out_e, p.sp.base_src)) + 1);
+        nk = std::max(nk, std::max(std::max(p.sp.out_w, p.sp.out_z), std::max(p.sp.out_e, p.sp.base_src)) + 1);
         for (int s = 0; s < p.sp.nslots; ++s)
             if (p.sp.src[s] >= 0) nk = std::max(nk, p.sp.src[s] + 1);
     }
@@ -513,6 +520,7 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
         a.beta[s] = p.beta[s];
         a.delta[s] = p.delta[s];
         a.g2[s] = p.g2[s];
+        a.g3[s] = p.g3[s];
         if (p.sp.gnz[s]) ++ny;
     }
     a.nyslots = ny;
@@ -525,6 +533,8 @@ static GsStageArgs stage_args(rk_state st, const StagePlan& p, double dt, double
     a.g2_new = p.g2_new;
     a.out_w = p.sp.out_w >= 0 ? st->k[p.sp.out_w] : nullptr;
     a.out_e = p.sp.out_e >= 0 ? st->k[p.sp.out_e] : nullptr;
+    a.g3_new = p.g3_new;
+    a.out_z = p.sp.out_z >= 0 ? st->k[p.sp.out_z] : nullptr;
     a.errmax = st->d_err;
     a.dt = dt;
     a.dtp = st->gl_dtp;
@@ -633,7 +643,7 @@ static rk_status launch_stage_timed(rk_state st, const StagePlan& p, GsStageArgs
     if (nl) {
         const int64_t planes = a.zmode == 1 ? (a.geo.nzl > 1 ? 2 : 1) : (int64_t)(a.z_hi - a.z_lo);
         const int64_t arrays = 1 + p.sp.nslots + (a.out_k ? 1 : 0) + (a.out_u ? 1 : 0) + (a.out_w ? 1 : 0) +
-                               (a.out_e ? 1 : 0);
+                               (a.out_e ? 1 : 0) + (a.out_z ? 1 : 0);
         st->stats.stage_bytes += planes * st->nx * st->ny * 2 * (int64_t)sizeof(double) * arrays;
     }
     if (st->timing) {
@@ -1343,7 +1353,7 @@ static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
     int64_t arrays = 0;
     for (const StagePlan& p : build_plan(scheme, 0, dt))
         arrays += 1 + p.sp.nslots + (p.sp.out_k >= 0 ? 1 : 0) + (p.sp.writes_u ? 1 : 0) + (p.sp.out_w >= 0 ? 1 : 0) +
-                  (p.sp.out_e >= 0 ? 1 : 0);
+                  (p.sp.out_e >= 0 ? 1 : 0) + (p.sp.out_z >= 0 ? 1 : 0);
     const int64_t cells = st->local * st->nx * st->ny;
     while (n > 0) {
         const int chunk = (int)std::min<int64_t>(n, 1 << 20);
@@ -1662,6 +1672,83 @@ static rk_status unfused_stages(rk_state st, int scheme, double dt, bool err, do
     return RK_OK;
 }
 
+// K8 fixed-step tail pair: the last two stages (L-1, L) of a fixed step in one launch -- the
+// write-ahead stage L-2 (stage_spec ad 5) stored Y_{L-1} (the pair's source), Z_L = u + sum_{j<=L-2}
+// a_Lj k_j (its base: Y_L = Z_L + (dt a_{L,L-1}) k_{L-1}) and W = u + sum_{j<=L-2} b_j k_j; the pair
+// (PAIR_LAST's kernel) writes u_new = (W + b_{L-1} k_{L-1}) + b_L k_L.  Cash–Karp 5(4), Dormand–Prince
+// fixed step, RKF 7(8): stages L-2 .. L move 7 + 4 arrays instead of 5 + 7 + 3 (CK54 / DOPRI5).
+static bool fixed_tail_ok(rk_state st, int scheme) {
+    static int knob = -1;  // developer A/B knob RKB_FIXED_TAIL=0 (default on)
+    if (knob < 0) knob = getenv("RKB_FIXED_TAIL") ? atoi(getenv("RKB_FIXED_TAIL")) : 1;
+    if (!knob || st->fused != 3 || !st->grid || st->ncomp != 2 || st->rhs != RHS_GRAY_SCOTT || st->p2p ||
+        !pair_shape_ok(st->geo))
+        return false;
+    if (scheme != RK_CASH_KARP54 && scheme != RK_DOPRI5 && scheme != RK_FEHLBERG78) return false;  // instantiated
+    if (halo_path(st) && (!st->ctx->nccl || st->local < 2)) return false;
+    const Tableau T = tableau_of(scheme);
+    const int L = last_stage(T, false);
+    return stage_spec(scheme, 5, L - 2).valid && t_bnz(T, L) && t_anz(T, L, L - 1);
+}
+
+static rk_status fixed_tail_pair(rk_state st, int scheme, double dt) {
+    NvtxRange nv("rk stage pair (K8 fixed-step tail)");
+    rk_ctx ctx = st->ctx;
+    const Coeffs C = coeffs_of(scheme);
+    const Tableau T = tableau_of(scheme);
+    const int L = last_stage(T, false);
+    double* y = st->k[L - 2];  // Y_{L-1}
+    double* z = st->k[L - 1];  // Z_L
+    PairArgs a{};
+    if (halo_path(st)) {  // Y_{L-1}'s two boundary planes and Z_L's one, each side
+        TRY(pair_ghost_buffers(st));
+        TRY(pair_ghost_exchange(st, y, st->pg_y, z));
+        a.ghosts = 1;
+        a.tm_glo = st->tm_pgy_lo;
+        a.tm_ghi = st->tm_pgy_hi;
+        a.tm_ulo = st->tm_pgw_lo.m[2];
+        a.tm_uhi = st->tm_pgw_hi.m[2];
+        a.src_lo = st->pg_y;
+        a.src_hi = st->pg_y + 2 * plane_values(st);
+    }
+    a.geo = st->geo;
+    a.d1 = st->d1;
+    a.d2 = st->d2;
+    a.F = st->F;
+    a.FK = st->F + st->K;
+    a.inv_h2 = 1.0 / (st->h * st->h);
+    a.zchunk = pick_pair_zchunk(st, 24);
+    CK_CTX(ctx, encode_pair_map(&a.tm_src, y, st->geo, (int)st->local));
+    a.src = y;
+    a.tm_u = st->tm_k[L - 1].m[2];  // Z_L: tile + 1 ring
+    a.w_in = st->k[L];              // W
+    a.gB = dt * C.a[L][L - 1];
+    a.betaA = dt * C.b[L - 1];
+    a.betaB = dt * C.b[L];
+    a.out = st->u_new;
+    a.dt = dt;
+    const bool ba = t_bnz(T, L - 1);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (st->timing) {
+        e0 = pool_event(st);
+        e1 = pool_event(st);
+        CK_CTX(ctx, cudaEventRecord(e0, ctx->stream));
+    }
+    CK_CTX(ctx, launch_gs_pair(ba ? PAIR_LAST : PAIR_LAST_NOA, a, ctx->stream));
+    if (st->timing) {
+        CK_CTX(ctx, cudaEventRecord(e1, ctx->stream));
+        st->pending.push_back({e0, e1, 2});
+        if (st->pending.size() > 4096) TRY(resolve_timing(st));
+    }
+    const int64_t pb = 4 * st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double);
+    st->stats.kernel_launches += 1;
+    st->stats.stage_launches += 1;
+    st->stats.pair_launches += 1;
+    st->stats.rhs_evals += 2;
+    st->stats.stage_bytes += pb;
+    st->stats.pair_bytes += pb;
+    return RK_OK;
+}
+
 // one fixed Runge–Kutta step, u <- u_new (does not touch the Adams–Bashforth history)
 static rk_status rk_fixed_step(rk_state st, int scheme, double dt) {
     if (!st->fused_kernels) {
@@ -1674,7 +1761,11 @@ static rk_status rk_fixed_step(rk_state st, int scheme, double dt) {
     if (st->grid && halo_path(st)) TRY(ensure_halo(st));  // the loopback's 1-rank communicator
     if (pair_path(st, scheme)) return pair_steps(st, scheme, dt, 1);
     if (fused_path(st, scheme)) return fused_steps(st, scheme, dt, 1);
-    if (st->grid) {
+    if (st->grid && fixed_tail_ok(st, scheme)) {
+        auto plan = build_plan(scheme, 5, dt);
+        TRY(run_grid_plan(st, plan, dt, 0.0, 0.0));
+        TRY(fixed_tail_pair(st, scheme, dt));
+    } else if (st->grid) {
         auto plan = build_plan(scheme, 0, dt);
         TRY(run_grid_plan(st, plan, dt, 0.0, 0.0));
     } else {
@@ -2127,7 +2218,7 @@ static bool gloop_path(rk_state st) {
 
 static int64_t plan_stage_bytes(rk_state st, const StagePlan& p) {
     const int64_t arrays = 1 + p.sp.nslots + (p.sp.out_k >= 0 ? 1 : 0) + (p.sp.writes_u ? 1 : 0) +
-                           (p.sp.out_w >= 0 ? 1 : 0) + (p.sp.out_e >= 0 ? 1 : 0);
+                           (p.sp.out_w >= 0 ? 1 : 0) + (p.sp.out_e >= 0 ? 1 : 0) + (p.sp.out_z >= 0 ? 1 : 0);
     return st->local * st->nx * st->ny * 2 * (int64_t)sizeof(double) * arrays;
 }
 

@@ -67,6 +67,11 @@ struct StageSpec {
     int out_w = -1, out_e = -1;            // AHEAD: k buffers receiving W and E
     int base_src = -1;                     // F after AHEAD: k buffer holding Y_F (the base)
     int wslot = -1, eslot = -1;            // F after AHEAD: slots holding W and E
+    // AHEAD for a K8 fixed-step tail pair (ad == 5): the stage i = L-2 also stores the base of the
+    // last stage's value, Z_L = u + sum_{j<=i} a_Lj k_j (tile + ring), into k buffer out_z
+    bool anz3[kMaxSlots] = {};             // a_Lj != 0
+    bool a3new = false;                    // a_Li != 0
+    int out_z = -1;
 };
 
 __host__ __device__ constexpr bool t_anz(const Tableau& T, int i, int j) { return rat_nz(T.a[i][j]); }
@@ -173,6 +178,35 @@ __host__ __device__ constexpr StageSpec stage_spec(int S, int ad, int i) {
         return p;
     }
     const Tableau T = tableau_of(S);
+    if (ad == 5) {  // fixed step whose last two stages run as one K8 pair (L-1, L): stages 0..L-3
+                    // as usual, stage L-2 writes ahead Y_{L-1} (the pair's source, ring), Z_L (the
+                    // pair's base, ring) and W = u + sum_{j<=L-2} b_j k_j (own cells)
+        const int L5 = last_stage(T, false);
+        if (T.s < 4 || L5 < 3 || i < 0 || i > L5 - 2) return p;
+        if (i < L5 - 2) return stage_spec(S, 0, i);
+        for (int j = 0; j < i; ++j) {
+            const bool need = t_anz(T, i, j) || t_anz(T, i + 1, j) || t_anz(T, i + 2, j) || t_bnz(T, j);
+            if (!need) continue;
+            const int s = p.nslots++;
+            if (s >= kMaxSlots) return StageSpec{};  // does not fit: not offered (fixed_tail_ok)
+            p.src[s] = j;
+            p.j[s] = j;
+            p.halo[s] = t_anz(T, i, j);
+            p.gnz[s] = t_anz(T, i, j);
+            p.anz2[s] = t_anz(T, i + 1, j);
+            p.anz3[s] = t_anz(T, i + 2, j);
+            p.bnz[s] = t_bnz(T, j);
+        }
+        p.valid = 1;
+        p.epi = EPI_AHEAD;
+        p.a2new = t_anz(T, i + 1, i);
+        p.a3new = t_anz(T, i + 2, i);
+        p.bnew = t_bnz(T, i);
+        p.out_k = i;      // Y_{L-1} into k_i's buffer (k_i is never stored)
+        p.out_z = i + 1;  // Z_L into k_{L-1}'s buffer (never stored)
+        p.out_w = i + 2;  // W into k_L's buffer (never stored)
+        return p;
+    }
     if (ad == 4) {  // fixed step, the last stage fed by a K8 pair that wrote ahead Y_L (k buffer 0,
                     // with its ring) and W = u + sum_{j<L} b_j k_j (k buffer 1): Y-direct, u_new = W + b_L k_L
         const int L4 = last_stage(T, false);

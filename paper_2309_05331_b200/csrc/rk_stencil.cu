@@ -215,6 +215,7 @@ struct EState {
     double d[2];  // atol (+) rtol (x) (|u| (+) dt (x) |k1|)
     double h[NH > 0 ? NH : 1][2];  // Adams–Bashforth: f_{n-1} .. f_{n-k+1} at the own cell
     double y2[2];  // AHEAD: u (+) sum a_Fj k_j (the final stage's value, without k_i)
+    double y3[2];  // AHEAD with out_z: u (+) sum a_Lj k_j (the last stage's base, without k_i)
 };
 
 // the error sum already holds a term before delta_i k_i is added
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
     constexpr bool SPECR = AD == 2;  // SPEC's ratio denominator max(|u|, |u_new|) (R-28)
     constexpr bool AHEAD = EPI == EPI_AHEAD;         // write-ahead stage (rk_stage_spec.h)
     constexpr bool AHEAD_E = AHEAD && P.out_e >= 0;  // ... with the partial error sum
+    constexpr bool ZOUT = AHEAD && P.out_z >= 0;     // ... with the last stage's base Z_L (ad 5)
     constexpr bool WSLOT = P.wslot >= 0, ESLOT = P.eslot >= 0;  // final stage fed by AHEAD
     using ES = EState<AB ? NS : 0>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -377,6 +379,13 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                 for (int s = 0; s < NS; ++s)
                     if (P.anz2[s]) yv = add(yv, mul(mul(dsc, a.g2[s]), sval(st, s, c, r)));
                 es.y2[c] = yv;
+                if constexpr (ZOUT) {
+                    double zv = ub;
+#pragma unroll
+                    for (int s = 0; s < NS; ++s)
+                        if (P.anz3[s]) zv = add(zv, mul(mul(dsc, a.g3[s]), sval(st, s, c, r)));
+                    es.y3[c] = zv;
+                }
             }
             if constexpr (ESUM && ESLOT) {
                 es.e[c] = sval(st, P.eslot, c, r);  // E from the write-ahead stage
@@ -541,6 +550,8 @@ __global__ void __launch_bounds__(NT, kMinBlocks<S, AD, I>) gs_stage_kernel(cons
                 if constexpr (AHEAD) {  // Y_F (read with its ring by stage F), W, E
                     store_cell(a.out_k, G, slice, cell[r], P.a2new ? add(ec.y2[c], mul(mul(dsc, a.g2_new), f[c])) : ec.y2[c]);
                     store_cell(a.out_w, G, slice, cell[r], P.bnew ? add(ec.w[c], mul(mul(dsc, a.beta_new), f[c])) : ec.w[c]);
+                    if constexpr (ZOUT)
+                        store_cell(a.out_z, G, slice, cell[r], P.a3new ? add(ec.y3[c], mul(mul(dsc, a.g3_new), f[c])) : ec.y3[c]);
                 }
                 double e = ec.e[c];
                 if constexpr (ESUM || EPI == EPI_TAIL_ERR || AHEAD_E) {
@@ -771,6 +782,12 @@ cudaError_t launch_gs_stage(int scheme, int adaptive, int stage, const GsStageAr
     if (nlaunch) ++*nlaunch;
     if (adaptive == 4) {  // the last stage after a K8 pair (Gragg's modified midpoint, stage 3)
         if (scheme == 6 && stage == 2) return launch_one<6, 4, 2>(a, grid, st);
+        return cudaErrorInvalidValue;
+    }
+    if (adaptive == 5) {  // the write-ahead stage before a K8 fixed-step tail pair (stage L-2)
+        if (scheme == 2 && stage == 3) return launch_one<2, 5, 3>(a, grid, st);   // Cash–Karp 5(4)
+        if (scheme == 3 && stage == 3) return launch_one<3, 5, 3>(a, grid, st);   // Dormand–Prince fixed
+        if (scheme == 4 && stage == 10) return launch_one<4, 5, 10>(a, grid, st); // RKF 7(8)
         return cudaErrorInvalidValue;
     }
     if (adaptive == 2) {  // SPEC's error ratio (R-28)

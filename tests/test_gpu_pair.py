@@ -378,6 +378,10 @@ def test_head_pair_schemes_bitwise(ctx, case, dims):
     assert s1["head_launches"] - s0["head_launches"] == 1
     cells = dims[0] * dims[1] * dims[2]
     assert s1["head_bytes"] - s0["head_bytes"] == 4 * 16 * cells
+    if not adaptive:  # + the fixed-step tail pair (stages L-1, L after the write-ahead stage L-2)
+        assert s1["pair_launches"] - s0["pair_launches"] == 2
+        if name in ("cash_karp54", "dopri5"):  # k1 2 + head 4 + stage 4 (Y5, Z6, W) 7 + tail 4
+            assert s1["stage_bytes"] - s0["stage_bytes"] == 17 * 16 * cells
 
 
 @pytest.mark.parametrize("name", ["cash_karp54", "rkf78"])
@@ -417,3 +421,43 @@ def test_head_pair_halo_path_ck54(ctx, dims):
     assert E == E_o
     assert heads == 1
     assert bitwise(got, un if acc else u0), first_mismatch(got, un if acc else u0)
+
+
+@pytest.mark.parametrize("name", ["cash_karp54", "dopri5", "rkf78"])
+@pytest.mark.parametrize("dims", [(64, 32, 2), (64, 32, 7)], ids=lambda d: "x".join(map(str, d)))
+def test_fixed_tail_pair_halo_path(ctx, name, dims):
+    """The fixed-step tail pair on the slab path (one-GPU loopback, 1-rank NCCL): Y_{L-1}'s two
+    boundary planes and Z_L's one exchanged before the launch; three steps bitwise."""
+    import paper_2309_05331_b200 as rk
+    u0 = perturbed_ic(*dims, seed=6)
+    p = oracle.gray_scott_problem(*dims)
+    want = u0
+    for m in range(3):
+        want = oracle.step(p, OS[name], float(m), 0.5, want)
+    st = pair_state(ctx, dims, u0)
+    st.set_option(rk.OPT_HALO_LOOPBACK, 1)
+    s0 = st.stats()
+    for m in range(3):
+        st.do_step(name, float(m), 0.5)
+    s1 = st.stats()
+    got = st.get()
+    st.close()
+    assert s1["pair_launches"] - s0["pair_launches"] == 6  # head + tail per step
+    assert bitwise(got, want), first_mismatch(got, want)
+
+
+@pytest.mark.parametrize("name", ["cash_karp54", "dopri5", "rkf78"])
+def test_fixed_tail_pair_integrate_const(ctx, name):
+    """integrate_const (several steps, CUDA-graph replay on) through the head and tail pairs,
+    bitwise against the oracle's steps."""
+    import paper_2309_05331_b200 as rk
+    dims = (96, 48, 20)
+    u0 = perturbed_ic(*dims, seed=9)
+    p = oracle.gray_scott_problem(*dims)
+    want, n_o = oracle.integrate_const(p, OS[name], u0, 0.0, 3.0, 0.5)
+    st = pair_state(ctx, dims, u0)
+    st.set_option(rk.OPT_USE_GRAPH, 1)
+    assert st.integrate_const(name, 0.0, 3.0, 0.5) == n_o
+    got = st.get()
+    st.close()
+    assert bitwise(got, want), first_mismatch(got, want)

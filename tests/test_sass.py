@@ -47,7 +47,9 @@ def _stage(sass, s, ad, i):
 # DOPRI5 adaptive try: k1 (first try only), stages 1..4, EPART stage 5, FSAL tail; RK4 stages
 # (DOPRI5 adaptive stage 4 is the write-ahead stage, 5 the final combination it feeds)
 HOT = [(1, 0, 0), (3, 0, 1), (3, 0, 2), (3, 0, 3), (3, 1, 4), (3, 1, 5), (3, 1, 6),
-       (1, 0, 1), (1, 0, 2), (1, 0, 3), (0, 0, 0), (5, 0, 1), (3, 0, 4), (3, 0, 5)]
+       (1, 0, 1), (1, 0, 2), (1, 0, 3), (0, 0, 0), (5, 0, 1), (3, 0, 4), (3, 0, 5),
+       # the write-ahead stages before the K8 fixed-step tail pair (Y_{L-1}, Z_L, W)
+       (2, 5, 3), (3, 5, 3), (4, 5, 10)]
 
 
 @pytest.mark.parametrize("s,ad,i", HOT)
@@ -80,7 +82,8 @@ def test_persistent_small_grid_kernel(sass, s):
 # pairs (the DOPRI5 tail's IEEE division may use DFMA)
 K8 = [("0", "0", "1", "1", "0", "0", "0", "0"), ("1", "1", "1", "0", "0", "0", "0", "0"),
       ("0", "0", "0", "0", "0", "0", "0", "0"), ("1", "1", "1", "0", "1", "0", "0", "0"),
-      ("0", "0", "0", "0", "0", "0", "1", "1")]
+      ("0", "0", "0", "0", "0", "0", "1", "1"),
+      ("1", "1", "0", "0", "0", "0", "0", "0")]  # PAIR_LAST_NOA (Cash–Karp's fixed-step tail, b_5 = 0)
 
 
 @pytest.mark.parametrize("flags", K8, ids=lambda f: "".join(f))
