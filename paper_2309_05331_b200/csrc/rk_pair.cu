@@ -662,13 +662,48 @@ __global__ void __launch_bounds__(PNT, PLayout<U1, YOUT, HD>::minb) gs_pair_kern
     };
     const int niter = nout + 2;
     int it = 0;
-    for (; it + 2 < niter; it += 3) {
-        step(it, std::integral_constant<int, 0>{});
-        step(it + 1, std::integral_constant<int, 1>{});
-        step(it + 2, std::integral_constant<int, 2>{});
+#ifndef RKB_PAIR_UNR1
+#define RKB_PAIR_UNR1 2  // the plane loop not unrolled (queues rotate by moves): 2 = the DOPRI5 tail
+                         // pair only (default: its 6.2 k-instruction unrolled body, the largest, stalled
+                         // on instruction fetch; one copy is 2.1 k: 2.80 -> 2.77 ms), 1 = every pair
+                         // kind (measured: RK4 -0.3 %, head pair +0.5 %, midpoint / CK54 tail +0.3 %), 0 = none
+#endif
+    constexpr bool UNR1 = RKB_PAIR_UNR1 == 1 || (RKB_PAIR_UNR1 == 2 && DP);
+    if constexpr (UNR1) {
+        // one copy of the body (a third of the instruction footprint); slot J = 0 every iteration,
+        // and the queues move one plane: Y_A (t-1 <- t <- t+1), ring Y_A (t-1 <- t), Y_B (t-2 <- t-1
+        // <- t), k_A, u, W (t-1 <- t)
+#pragma unroll 1
+        for (; it < niter; ++it) {
+            step(it, std::integral_constant<int, 0>{});
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    if constexpr (YREG) {
+                        ya_q[2][r][c] = ya_q[0][r][c];
+                        ya_q[0][r][c] = ya_q[1][r][c];
+                    }
+                    yb_q[1][r][c] = yb_q[2][r][c];
+                    yb_q[2][r][c] = yb_q[0][r][c];
+                    ka_q[2][r][c] = ka_q[0][r][c];
+                    u_q[2][r][c] = u_q[0][r][c];
+                    w_q[2][r][c] = w_q[0][r][c];
+                }
+            if constexpr (EARLY) {
+                rc_q[2][0] = rc_q[0][0];
+                rc_q[2][1] = rc_q[0][1];
+            }
+        }
+    } else {
+        for (; it + 2 < niter; it += 3) {
+            step(it, std::integral_constant<int, 0>{});
+            step(it + 1, std::integral_constant<int, 1>{});
+            step(it + 2, std::integral_constant<int, 2>{});
+        }
+        if (it < niter) step(it, std::integral_constant<int, 0>{});
+        if (it + 1 < niter) step(it + 1, std::integral_constant<int, 1>{});
     }
-    if (it < niter) step(it, std::integral_constant<int, 0>{});
-    if (it + 1 < niter) step(it + 1, std::integral_constant<int, 1>{});
     if constexpr (DP) block_max_to_global(rbits, a.errmax);
 }
 
