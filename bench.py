@@ -695,21 +695,33 @@ def main():
         # each waiting in a collective for a peer that waits for the lock.
         turn = [0]
         cv = threading.Condition()
+        errors = []
 
         def work(i, k):
-            for _ in range(k):
-                sts[i].set(host_in)
+            try:
+                for _ in range(k):
+                    sts[i].set(host_in)
+                    with cv:
+                        cv.wait_for(lambda: turn[0] % 2 == i or errors)
+                    if errors:
+                        return
+                    try:
+                        a, _ = sts[i].integrate_adaptive("dopri5", 0.0, T1, 1.0, TOL, TOL)
+                    finally:  # the other pipeline's turn even if this one failed
+                        with cv:
+                            turn[0] += 1
+                            cv.notify_all()
+                    sts[i].get(outs[i])
+                    accs[i] += a
+            except Exception as exc:  # noqa: BLE001 -- re-raised by the caller after the join
                 with cv:
-                    cv.wait_for(lambda: turn[0] % 2 == i)
-                a, _ = sts[i].integrate_adaptive("dopri5", 0.0, T1, 1.0, TOL, TOL)
-                with cv:
-                    turn[0] += 1
+                    errors.append(exc)
                     cv.notify_all()
-                sts[i].get(outs[i])
-                accs[i] += a
 
         for i in range(2):
             work(i, 1)
+        if errors:
+            raise errors[0]
         accs[0] = accs[1] = 0
         kper = max(2, args.steps)  # per pipeline: 2*steps in the timed region (fill / drain amortised)
         barrier()
@@ -721,6 +733,8 @@ def main():
             t.start()
         for t in th:
             t.join()
+        if errors:
+            raise errors[0]
         ej = torch.cuda.Event()
         ej.record(side[1])
         side[0].wait_event(ej)
