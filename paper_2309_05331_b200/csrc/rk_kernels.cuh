@@ -214,6 +214,7 @@ struct GsCoopArgs {
     CoopCoef cf;           // fixed steps: the step's coefficients
     double d1, d2, F, FK, inv_h2;
     int nsteps;            // fixed steps
+    unsigned int* bar;     // the grid barrier's two words (arrivals, generation), zeroed once per state
 };
 cudaError_t launch_gs_coop(int scheme, const GsCoopArgs& a, cudaStream_t st, int device);
 int coop_last_stage(int scheme);           // last stage index (b_j != 0) = number of stored k_j

@@ -238,6 +238,7 @@ struct rk_state_s {
     double ab_dt = 0.0;
     double* hist[8] = {nullptr};
     double* ybuf[2] = {nullptr};     // K5 stage values (RK_OPT_COOP_MAX_CELLS)
+    unsigned int* k5bar = nullptr;   // K5 grid-barrier words (arrivals, generation), zeroed once
     Maps tm_hist[8]{};
     // halo (grid, world > 1 or loopback)
     double* sendbuf = nullptr;       // [lo plane | hi plane]
@@ -1327,6 +1328,13 @@ static bool coop_path(rk_state st, int scheme) {
            scheme >= RK_EULER && scheme <= RK_MODIFIED_MIDPOINT && st->local * st->nx * st->ny <= st->coop_max_cells;
 }
 
+static rk_status ensure_k5bar(rk_state st) {
+    if (st->k5bar) return RK_OK;
+    CK_CTX(st->ctx, cudaMalloc((void**)&st->k5bar, 2 * sizeof(unsigned int)));
+    CK_CTX(st->ctx, cudaMemsetAsync(st->k5bar, 0, 2 * sizeof(unsigned int), st->ctx->stream));
+    return RK_OK;
+}
+
 static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
     NvtxRange nv("rk persistent steps (K5)");
     rk_ctx ctx = st->ctx;
@@ -1335,11 +1343,13 @@ static rk_status coop_steps(rk_state st, int scheme, double dt, int64_t n) {
     for (int b = 0; b < 2; ++b)
         if (!st->ybuf[b]) TRY(alloc_array(st, &st->ybuf[b], nullptr));
     const Coeffs C = coeffs_of(scheme);
+    TRY(ensure_k5bar(st));
     GsCoopArgs a{};
     a.geo = st->geo;
     for (int j = 0; j < 13; ++j) a.k[j] = j < st->nk ? st->k[j] : nullptr;
     a.ybuf[0] = st->ybuf[0];
     a.ybuf[1] = st->ybuf[1];
+    a.bar = st->k5bar;
     for (int i = 0; i < C.s; ++i) {
         for (int j = 0; j < i; ++j) a.cf.g[i][j] = dt * C.a[i][j];
         a.cf.beta[i] = dt * C.b[i];
@@ -2060,6 +2070,8 @@ static rk_status device_adaptive_loop(rk_state st, int scheme, double t0, double
         for (int j = 0; j < 13; ++j) g.c.k[j] = j < st->nk ? st->k[j] : nullptr;
         g.c.ybuf[0] = st->ybuf[0];
         g.c.ybuf[1] = st->ybuf[1];
+        TRY(ensure_k5bar(st));
+        g.c.bar = st->k5bar;
         g.c.geo = st->geo;
         g.c.d1 = st->d1;
         g.c.d2 = st->d2;
@@ -2727,6 +2739,7 @@ rk_status rk_state_destroy(rk_state st) {
     for (int j = 0; j < st->nk; ++j) dev_free(cx, st->k[j]);
     for (int j = 0; j < st->nhist; ++j) dev_free(cx, st->hist[j]);
     dev_free(cx, st->ybuf[0]);
+    cudaFree(st->k5bar);
     dev_free(cx, st->ybuf[1]);
     dev_free(cx, st->sendbuf);
     dev_free(cx, st->ghostbuf);

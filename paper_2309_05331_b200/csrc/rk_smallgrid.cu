@@ -188,16 +188,46 @@ __device__ __forceinline__ void coop_stage(const StageEnv& v, const CoopCoef& cf
     }
 }
 
+#ifndef RKB_K5_BAR
+#define RKB_K5_BAR 1  // 1: the hand-written grid barrier below (configs[2] 27.2 -> 26.4 us per 64^3 RK4
+                      // step), 0: cooperative_groups' grid_group::sync
+#endif
+// Grid-wide barrier on the state's own two words (arrivals, generation; concurrent launches of
+// other states use their own): thread 0 of each CTA arrives after a fence, the last arrival resets
+// the counter and releases the next generation, the others poll it with acquire loads
+struct GBar {
+    unsigned int* w;
+    __device__ __forceinline__ void sync() {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned int g;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(w + 1) : "memory");
+            __threadfence();
+            if (atomicAdd(w, 1u) == gridDim.x - 1) {
+                atomicExch(w, 0u);
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(w + 1), "r"(g + 1) : "memory");
+            } else {
+                unsigned int c;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(w + 1) : "memory");
+                } while (c == g);
+            }
+        }
+        __syncthreads();
+    }
+};
+
 // stages I..L with a grid-wide barrier between them (the caller synchronises after the last:
 // before the next step, or through the error-max reduction)
-template <int S, int MODE, int I>
+template <int S, int MODE, int I, class GB>
 __device__ __forceinline__ void coop_stages(const StageEnv& v, const CoopCoef& cf, const double* u, double* un,
-                                            unsigned long long& rbits, cooperative_groups::grid_group& grid) {
+                                            unsigned long long& rbits, GB& grid) {
     constexpr int L = last_of<S, MODE>();
     coop_stage<S, MODE, I>(v, cf, u, un, rbits);
     if constexpr (I < L) {
         grid.sync();  // k_I, Y_{I+1} complete everywhere before the next stage
-        coop_stages<S, MODE, I + 1>(v, cf, u, un, rbits, grid);
+        coop_stages<S, MODE, I + 1, GB>(v, cf, u, un, rbits, grid);
     }
 }
 
@@ -218,7 +248,11 @@ __device__ __forceinline__ StageEnv env_of(const GsCoopArgs& a) {
 // ---- fixed steps -------------------------------------------------------------------------
 template <int S, int MINB>
 __global__ void __launch_bounds__(kCoopThreads, MINB) gs_coop_kernel(const __grid_constant__ GsCoopArgs a) {
+#if RKB_K5_BAR
+    GBar grid{a.bar};
+#else
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+#endif
     const StageEnv v = env_of(a);
     double* u = a.buf[0];
     double* un = a.buf[1];
@@ -235,7 +269,11 @@ __global__ void __launch_bounds__(kCoopThreads, MINB) gs_coop_kernel(const __gri
 // ---- the whole integrate_adaptive --------------------------------------------------------
 template <int S, int MODE, int MINB>
 __global__ void __launch_bounds__(kCoopThreads, MINB) gs_coop_adaptive_kernel(const __grid_constant__ GsCoopLoopArgs a) {
+#if RKB_K5_BAR
+    GBar grid{a.c.bar};
+#else
     cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+#endif
     __shared__ CoopCoef cf;   // this try's dt-scaled coefficients
     __shared__ double s_dtn;  // controller result, computed once per CTA
     __shared__ int s_ok;
