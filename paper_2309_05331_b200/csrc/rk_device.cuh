@@ -52,4 +52,33 @@ __device__ __forceinline__ void block_max_to_global(unsigned long long v, unsign
     }
 }
 
+// Grid-wide barrier of the cooperative K5 kernels (one 1024-thread CTA per SM) on the state's own
+// two words (arrivals, generation; zeroed once; concurrent launches of other states use their
+// own): thread 0 of each CTA arrives after a fence, the last arrival resets the counter and
+// releases the next generation, the others poll it with acquire loads.  Replaces
+// cooperative_groups' grid_group::sync there (configs[2]: 27.2 -> 26.4-26.7 us per 64^3 RK4 step;
+// the vector device loop's 296 CTAs of 256 threads measured slower with it and keep grid_group).
+struct GBar {
+    unsigned int* w;
+    __device__ __forceinline__ void sync() {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned int g;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(w + 1) : "memory");
+            __threadfence();
+            if (atomicAdd(w, 1u) == gridDim.x - 1) {
+                atomicExch(w, 0u);
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(w + 1), "r"(g + 1) : "memory");
+            } else {
+                unsigned int c;
+                do {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(w + 1) : "memory");
+                } while (c == g);
+            }
+        }
+        __syncthreads();
+    }
+};
+
 }  // namespace rkb

@@ -151,6 +151,8 @@ static cudaError_t launch_s(const PwArgs& a, cudaStream_t st, int num_sms) {
 // and the counters return to the host.
 template <int S, int RHS, int ERR>
 __global__ void __launch_bounds__(256) pointwise_loop_kernel(const PwLoopArgs a) {
+    // (cooperative_groups' barrier: GBar measured slower here -- 296 CTAs of 256 threads, 11.5 ->
+    // 13.2 us per try of configs[1] -- while it helps K5's 148 CTAs of 1024)
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ PwArgs sa;        // this try's coefficients (dt * tableau)

@@ -189,35 +189,8 @@ __device__ __forceinline__ void coop_stage(const StageEnv& v, const CoopCoef& cf
 }
 
 #ifndef RKB_K5_BAR
-#define RKB_K5_BAR 1  // 1: the hand-written grid barrier below (configs[2] 27.2 -> 26.4 us per 64^3 RK4
-                      // step), 0: cooperative_groups' grid_group::sync
+#define RKB_K5_BAR 1  // 1: GBar (rk_device.cuh), 0: cooperative_groups' grid_group::sync
 #endif
-// Grid-wide barrier on the state's own two words (arrivals, generation; concurrent launches of
-// other states use their own): thread 0 of each CTA arrives after a fence, the last arrival resets
-// the counter and releases the next generation, the others poll it with acquire loads
-struct GBar {
-    unsigned int* w;
-    __device__ __forceinline__ void sync() {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned int g;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(w + 1) : "memory");
-            __threadfence();
-            if (atomicAdd(w, 1u) == gridDim.x - 1) {
-                atomicExch(w, 0u);
-                __threadfence();
-                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(w + 1), "r"(g + 1) : "memory");
-            } else {
-                unsigned int c;
-                do {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(w + 1) : "memory");
-                } while (c == g);
-            }
-        }
-        __syncthreads();
-    }
-};
-
 // stages I..L with a grid-wide barrier between them (the caller synchronises after the last:
 // before the next step, or through the error-max reduction)
 template <int S, int MODE, int I, class GB>
